@@ -1,0 +1,241 @@
+/* cieg.h -- C ABI of the B200-native LOBPCG hot path.
+ *
+ * This is the drop-in boundary for the reference's C++ solver/operator API in
+ * /root/reference/proj/include/ci/. Every entry point below names the
+ * reference interface it replaces (file:line). Plain pointers and sizes only:
+ * no C++ or torch types cross this boundary and no exception escapes it.
+ * Every function returns a cieg_status; on failure cieg_last_error() holds
+ * "<Type>: message" using the reference's ci::Error taxonomy
+ * (proj/include/ci/errors.hpp:9-32), so a C++ layer can rethrow the matching
+ * ci:: exception.
+ *
+ * Conventions
+ *   - Block vectors are row-major n x k doubles (BlockVectors,
+ *     proj/include/ci/block_vectors.hpp:19-54): the k components of one basis
+ *     state are adjacent.
+ *   - Small dense matrices (Grams, coefficient panels) are column-major
+ *     doubles with leading dimension = rows (Eigen::MatrixXd default).
+ *   - "_dev" pointers are device addresses on the context's GPU; "_host"
+ *     pointers are host memory (pageable or pinned).
+ *   - A context owns one CUDA stream; it is not re-entrant (one host thread
+ *     at a time), mirroring the reference's single-threaded caller
+ *     (SURVEY.md 8(b) Threading).
+ */
+#ifndef CIEG_H
+#define CIEG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  CIEG_OK = 0,
+  CIEG_ERR_DIMENSION = 1,   /* ci::DimensionMismatch */
+  CIEG_ERR_CONFIG = 2,      /* ci::ConfigError */
+  CIEG_ERR_SUBSPACE = 3,    /* ci::SubspaceCollapse */
+  CIEG_ERR_FORMAT = 4,      /* ci::FormatError */
+  CIEG_ERR_INDEFINITE = 5,  /* ci::IndefiniteGram */
+  CIEG_ERR_CUDA = 6,        /* device/runtime failure (no reference analogue) */
+  CIEG_ERR_ARGUMENT = 7,    /* null handle / bad argument (ci::Error) */
+  CIEG_ERR_BETA = 8         /* ci::BetaTooLarge */
+} cieg_status;
+
+/* Last error message of the calling thread ("" when none). */
+const char* cieg_last_error(void);
+/* Library version string. */
+const char* cieg_version(void);
+
+typedef struct cieg_ctx cieg_ctx;
+typedef struct cieg_mat cieg_mat;
+typedef struct cieg_prec cieg_prec;
+typedef struct cieg_report cieg_report;
+typedef struct cieg_host_csb cieg_host_csb;
+
+/* ---- context --------------------------------------------------------- */
+/* Bind a context (one CUDA stream) to a device. No reference analogue: the
+ * reference is host-only. */
+int cieg_ctx_create(int device, cieg_ctx** out);
+int cieg_ctx_destroy(cieg_ctx* ctx);
+int cieg_ctx_synchronize(cieg_ctx* ctx);
+/* cudaStream_t of the context, as void* (for callers that enqueue their own
+ * work, e.g. torch.cuda.ExternalStream). */
+void* cieg_ctx_stream(cieg_ctx* ctx);
+/* Number of kernels this context has launched (instrumentation). */
+uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx);
+
+/* ---- matrix ------------------------------------------------------------ */
+/* Flattened ci::CsbMatrix (proj/include/ci/csb.hpp:33-60): the lower-triangle
+ * CSB block grid, block (I,J<=I) at linear index I(I+1)/2+J, entries of one
+ * block contiguous and sorted by (row, col) with 16-bit block-local offsets.
+ * entry_offsets has nb(nb+1)/2 + 1 prefix sums into rows/cols/values. */
+typedef struct {
+  uint32_t dim;
+  uint32_t nb;                     /* CSB block count */
+  int precision;                   /* 0 = single (values32), 1 = double (values64) */
+  const uint32_t* block_boundaries;/* nb + 1 */
+  const uint64_t* entry_offsets;   /* nb(nb+1)/2 + 1 */
+  const uint16_t* rows;
+  const uint16_t* cols;
+  const void* values;              /* float or double per precision */
+} cieg_csb_view;
+
+/* Upload H once and re-tile it into the device format (row panels <= tile
+ * edge, dense-able 32-bit packed tile-local indices, 64-bit offsets).
+ * panel_bounds (npanels+1 entries, 0 .. dim) fixes the device panel grid; pass
+ * NULL to derive it from group_bounds (ngroups+1 entries, e.g. a
+ * GroupPartition's ranges) or, when both are NULL, from a fixed grid.
+ * tile_edge is 64 or 128 (0 = choose). Replaces the host-side ownership of
+ * CsbMatrix for spmm (proj/src/csb.cpp:182-193). */
+int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb,
+                       const uint32_t* group_bounds, uint32_t ngroups,
+                       uint32_t tile_edge, cieg_mat** out);
+int cieg_matrix_destroy(cieg_mat* mat);
+/* dim, stored nnz (lower incl. diagonal), device panels, device tiles,
+ * tile edge, precision, device bytes of the tile stream. */
+int cieg_matrix_info(const cieg_mat* mat, uint32_t* dim, uint64_t* nnz, uint32_t* npanels,
+                     uint64_t* ntiles, uint32_t* tile_edge, int* precision, uint64_t* bytes);
+
+/* U = (L + L^T - diag L) X  --  ci::spmm (proj/include/ci/csb.hpp:83,
+ * proj/src/csb.cpp:182-193). x_dev, y_dev: row-major dim x m device arrays
+ * (leading dimension m). Deterministic: every output row is reduced by one
+ * owner in a fixed order (bitwise identical run to run). */
+int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y_dev, uint32_t m);
+/* Same with host buffers: H2D of X, SpMM, D2H of U on the context stream,
+ * synchronous on return. This is the call a ci::spmm drop-in makes. */
+int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
+                   uint32_t m);
+
+/* ---- tall-skinny block kernels (proj/include/ci/block_vectors.hpp) ----- */
+/* X^T Y (kx x ky, column major, written to out_host) -- ci::block_inner
+ * (block_vectors.hpp:60, block_vectors.cpp:74-85). Partials are reduced in a
+ * fixed order (deterministic). */
+int cieg_block_inner(cieg_ctx* ctx, uint32_t n, const double* x_dev, uint32_t kx,
+                     const double* y_dev, uint32_t ky, double* out_host);
+/* out = Y G (G kin x kout column major, host) -- ci::linear_combination
+ * (block_vectors.hpp:64, block_vectors.cpp:118-129). */
+int cieg_linear_combination(cieg_ctx* ctx, uint32_t n, const double* y_dev, uint32_t kin,
+                            const double* g_host, uint32_t kout, double* out_dev);
+/* Y += X G -- ci::add_linear_combination (block_vectors.hpp:68,
+ * block_vectors.cpp:139-160). */
+int cieg_add_linear_combination(cieg_ctx* ctx, uint32_t n, double* y_dev, uint32_t ky,
+                                const double* x_dev, uint32_t kx, const double* g_host);
+/* Per-column Euclidean norms -- ci::column_norms (block_vectors.hpp:75). */
+int cieg_column_norms(cieg_ctx* ctx, uint32_t n, const double* x_dev, uint32_t k,
+                      double* out_host);
+
+/* ---- tile-diagonal preconditioner (proj/include/ci/precond.hpp) -------- */
+typedef struct {
+  int inner_iters;             /* FOM iteration cap, 1..3 (precond.hpp:17) */
+  int small_block_cutoff;      /* direct dense solve at or below (precond.hpp:18) */
+  int engage_after;            /* precond.hpp:19 */
+  double relres_gate;          /* precond.hpp:20 */
+  double near_converged_factor;/* precond.hpp:21 (read by nothing, as in the reference) */
+  double far_threshold;        /* precond.hpp:22 */
+  double column_floor_factor;  /* precond.hpp:27 */
+} cieg_precond_config;
+/* Defaults of ci::PrecondConfig. */
+void cieg_precond_config_default(cieg_precond_config* cfg);
+
+/* Flattened ci::TileDiagonal (hamiltonian.hpp:58-63): ngroups contiguous
+ * ranges [bounds[g], bounds[g+1]) covering [0, dim) and their dense blocks,
+ * concatenated column-major (block g has (bounds[g+1]-bounds[g])^2 entries). */
+typedef struct {
+  uint32_t dim;
+  uint32_t ngroups;
+  const uint32_t* bounds;   /* ngroups + 1 */
+  const double* blocks;     /* sum of n_g^2 */
+} cieg_tilediag_view;
+int cieg_precond_upload(cieg_ctx* ctx, const cieg_tilediag_view* tiles, cieg_prec** out);
+/* Build the tile diagonal on the device from an uploaded H and a group
+ * partition -- ci::extract_tile_diagonal (hamiltonian.cpp:178-203). */
+int cieg_precond_from_csb(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                          uint32_t ngroups, cieg_prec** out);
+int cieg_precond_destroy(cieg_prec* prec);
+
+/* ci::choose_shifts (precond.hpp:47-48, precond.cpp:13-55), host scalar
+ * logic. engage_out receives 0/1 per column. */
+int cieg_choose_shifts(uint32_t k, const double* theta, const double* res_norm,
+                       const double* x_norm, const double* relres, int iteration, double tol,
+                       const cieg_precond_config* cfg, double* mu_out, int* engage_out);
+/* W = apply_preconditioner(tiles, R, plan) -- ci::apply_preconditioner
+ * (precond.hpp:53-54, precond.cpp:160-207); r_dev/w_dev row-major n x k. */
+int cieg_precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r_dev, uint32_t k,
+                       const double* mu_host, const int* engage_host,
+                       const cieg_precond_config* cfg, double* w_dev);
+
+/* ---- LOBPCG (proj/include/ci/lobpcg.hpp) ------------------------------- */
+typedef struct {
+  int k_want;          /* lobpcg.hpp:55 */
+  double tol;          /* lobpcg.hpp:56 */
+  int max_iter;        /* lobpcg.hpp:57 */
+  cieg_precond_config precond_config; /* lobpcg.hpp:59 */
+} cieg_lobpcg_options;
+void cieg_lobpcg_options_default(cieg_lobpcg_options* opt);
+
+/* Per-iteration observer (ci::IterationView, lobpcg.hpp:47-52). x_host is the
+ * trial block (n x kt row-major) copied to the host only when an observer is
+ * installed; pointers are valid during the call only. */
+typedef void (*cieg_observer_fn)(void* user, int iteration, const double* x_host, uint32_t n,
+                                 uint32_t kt, const double* theta, const double* relres);
+
+/* ci::lobpcg_solve (lobpcg.hpp:67-68, lobpcg.cpp:216-387): X0 (host, n x kt
+ * row-major) supplies the trial block; prec may be NULL (unpreconditioned).
+ * Non-convergence is not an error: the report's converged flag is 0. */
+int cieg_lobpcg_solve(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
+                      const cieg_prec* prec, const cieg_lobpcg_options* opt,
+                      cieg_observer_fn observer, void* observer_user, cieg_report** out);
+int cieg_report_destroy(cieg_report* rep);
+/* SolveReport fields (lobpcg.hpp:34-43). */
+int cieg_report_summary(const cieg_report* rep, int* converged, int* iterations,
+                        double* norm_estimate, uint32_t* k_want, uint32_t* kt, uint64_t* history_rows);
+/* counters: spmm_calls, spmv_equivalents, precond_applications, orthogonalizations. */
+int cieg_report_counters(const cieg_report* rep, uint64_t* counters4);
+int cieg_report_eigenvalues(const cieg_report* rep, double* out /* k_want */);
+/* trial_vectors: n x kt row-major (eigenvectors are its first k_want columns). */
+int cieg_report_trial_vectors(const cieg_report* rep, double* out);
+/* history rows (iteration, column, relres, theta), in order. */
+int cieg_report_history(const cieg_report* rep, int* iteration, int* column, double* relres,
+                        double* theta);
+/* Device-event time split of the solve in milliseconds:
+ * [spmm, rayleigh_ritz, orthonormalization, preconditioner, residual, other, total]. */
+int cieg_report_timing(const cieg_report* rep, double* ms7);
+
+/* ---- synthetic sector generator (BASELINE.json configs) ---------------- */
+/* Deterministic sector/tile matrix of SURVEY.md 8(d): ns equal sectors,
+ * tile grid restarting at every sector, tiles kept for |ds| <= band with
+ * probability p (diagonal tiles always), entries with probability q, values
+ * N(0,1)/sqrt(avg full-row nnz) (Box-Muller over hash3 streams, proj/include/
+ * ci/rng.hpp), diagonal 10 s + U(-2,2). Produces a host CSB (beta-bounded,
+ * sector-aligned blocks) and its group (= tile) partition. */
+typedef struct {
+  uint32_t n;
+  uint32_t sectors;
+  uint32_t tile;      /* tile edge T */
+  uint32_t band;      /* |s_a - s_b| <= band (2) */
+  double p;           /* tile keep probability */
+  double q;           /* entry probability inside a kept tile */
+  uint64_t seed;
+  int precision;      /* 0 single, 1 double */
+  uint32_t beta;      /* CSB block bound (< 2^16) */
+} cieg_gen_params;
+/* Expected stored nnz (lower incl. diagonal) for the parameters. */
+double cieg_gen_expected_nnz(const cieg_gen_params* prm);
+/* Expected full-row off-diagonal count used for the value scale. */
+double cieg_gen_avg_row_nnz(const cieg_gen_params* prm);
+int cieg_generate_csb(const cieg_gen_params* prm, cieg_host_csb** out);
+int cieg_host_csb_destroy(cieg_host_csb* h);
+/* Borrowed views into the generated matrix (valid until destroy). */
+int cieg_host_csb_view(const cieg_host_csb* h, cieg_csb_view* view, uint64_t* nnz);
+int cieg_host_csb_groups(const cieg_host_csb* h, const uint32_t** bounds, uint32_t* ngroups);
+
+/* ci::random_block (block_vectors.cpp:162-174): out n x k row-major,
+ * entries 2*unit(hash3(seed, i, j)) - 1. */
+int cieg_random_block(uint32_t n, uint32_t k, uint64_t seed, double* out_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CIEG_H */

@@ -1,0 +1,318 @@
+// ref_capi.cpp -- TEST INFRASTRUCTURE ONLY. extern "C" bindings over the
+// UNMODIFIED reference library (compiled from /root/reference/proj/src with
+// -Dci=ciref), so Python tests and bench.py's reference arm can drive the
+// reference's own code path: ci::spmm / spmm_serial (csb.cpp:182-201),
+// block_inner / linear_combination (block_vectors.cpp:74-160),
+// choose_shifts / apply_preconditioner / fom_solve (precond.cpp),
+// extract_tile_diagonal (hamiltonian.cpp:178-203), orthonormalize and
+// lobpcg_solve (lobpcg.cpp:89-387), lanczos_solve (lanczos.cpp:24-136).
+// Never linked into the product.
+#include <omp.h>
+
+#include <cstring>
+#include <exception>
+#include <memory>
+#include <string>
+
+#include "ci/block_vectors.hpp"
+#include "ci/csb.hpp"
+#include "ci/errors.hpp"
+#include "ci/hamiltonian.hpp"
+#include "ci/lanczos.hpp"
+#include "ci/lobpcg.hpp"
+#include "ci/precond.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    g_err.clear();
+    f();
+    return 0;
+  } catch (const ci::DimensionMismatch& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const ci::ConfigError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const ci::SubspaceCollapse& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const ci::FormatError& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const ci::IndefiniteGram& e) {
+    g_err = e.what();
+    return 5;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 7;
+  }
+}
+
+ci::BlockVectors to_bv(const double* x, std::uint32_t n, std::uint32_t k) {
+  ci::BlockVectors b(n, k);
+  if (n && k) std::memcpy(b.values().data(), x, sizeof(double) * n * k);
+  return b;
+}
+
+void from_bv(const ci::BlockVectors& b, double* out) {
+  if (!b.values().empty()) std::memcpy(out, b.values().data(), sizeof(double) * b.values().size());
+}
+
+Eigen::MatrixXd to_mat(const double* colmajor, long r, long c) {
+  Eigen::MatrixXd m(r, c);
+  if (r && c) std::memcpy(m.data(), colmajor, sizeof(double) * r * c);
+  return m;
+}
+
+struct Report {
+  ci::SolveReport rep;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* ciref_last_error() { return g_err.c_str(); }
+void ciref_set_threads(int n) { omp_set_num_threads(n); }
+int ciref_max_threads() { return omp_get_max_threads(); }
+
+// Build a ci::CsbMatrix from the flattened view (same layout as cieg_csb_view).
+int ciref_matrix_create(std::uint32_t dim, std::uint32_t nb, int precision,
+                        const std::uint32_t* bounds, const std::uint64_t* offsets,
+                        const std::uint16_t* rows, const std::uint16_t* cols, const void* values,
+                        void** out) {
+  return guard([&] {
+    auto h = std::make_unique<ci::CsbMatrix>();
+    h->dim = dim;
+    h->precision = precision == 0 ? ci::Precision::Single : ci::Precision::Double;
+    h->layout.block_boundaries.assign(bounds, bounds + nb + 1);
+    h->blocks.resize(static_cast<std::size_t>(nb) * (nb + 1) / 2);
+    const float* v32 = static_cast<const float*>(values);
+    const double* v64 = static_cast<const double*>(values);
+#pragma omp parallel for schedule(dynamic, 64)
+    for (std::int64_t b = 0; b < static_cast<std::int64_t>(h->blocks.size()); ++b) {
+      ci::CoordinateBlock& blk = h->blocks[b];
+      const std::uint64_t e0 = offsets[b], e1 = offsets[b + 1];
+      blk.rows.assign(rows + e0, rows + e1);
+      blk.cols.assign(cols + e0, cols + e1);
+      if (precision == 0)
+        blk.values32.assign(v32 + e0, v32 + e1);
+      else
+        blk.values64.assign(v64 + e0, v64 + e1);
+    }
+    h->nnz_lower = offsets[h->blocks.size()];
+    *out = h.release();
+  });
+}
+
+void ciref_matrix_destroy(void* h) { delete static_cast<ci::CsbMatrix*>(h); }
+
+int ciref_spmm(void* h, const double* x, std::uint32_t m, double* y, int serial) {
+  return guard([&] {
+    const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);
+    ci::BlockVectors X = to_bv(x, H.dim, m);
+    ci::BlockVectors U = serial ? ci::spmm_serial(H, X) : ci::spmm(H, X);
+    from_bv(U, y);
+  });
+}
+
+int ciref_to_dense(void* h, double* out_colmajor) {
+  return guard([&] {
+    Eigen::MatrixXd d = ci::to_dense(*static_cast<ci::CsbMatrix*>(h));
+    std::memcpy(out_colmajor, d.data(), sizeof(double) * d.size());
+  });
+}
+
+int ciref_block_inner(std::uint32_t n, const double* x, std::uint32_t kx, const double* y,
+                      std::uint32_t ky, int serial, double* out) {
+  return guard([&] {
+    ci::BlockVectors X = to_bv(x, n, kx), Y = to_bv(y, n, ky);
+    Eigen::MatrixXd g = serial ? ci::block_inner_serial(X, Y) : ci::block_inner(X, Y);
+    std::memcpy(out, g.data(), sizeof(double) * g.size());
+  });
+}
+
+int ciref_linear_combination(std::uint32_t n, const double* y, std::uint32_t kin, const double* g,
+                             std::uint32_t kout, double* out) {
+  return guard([&] {
+    ci::BlockVectors Y = to_bv(y, n, kin);
+    from_bv(ci::linear_combination(Y, to_mat(g, kin, kout)), out);
+  });
+}
+
+int ciref_add_linear_combination(std::uint32_t n, double* y, std::uint32_t ky, const double* x,
+                                 std::uint32_t kx, const double* g) {
+  return guard([&] {
+    ci::BlockVectors Y = to_bv(y, n, ky), X = to_bv(x, n, kx);
+    ci::add_linear_combination(Y, X, to_mat(g, kx, ky));
+    from_bv(Y, y);
+  });
+}
+
+int ciref_orthonormalize(std::uint32_t n, const double* y, std::uint32_t k, double drop_tol,
+                         const double* against, std::uint32_t ka, double* out, std::uint32_t* kout) {
+  return guard([&] {
+    ci::BlockVectors Y = to_bv(y, n, k);
+    ci::BlockVectors A;
+    if (against && ka) A = to_bv(against, n, ka);
+    ci::BlockVectors Q = ci::orthonormalize(Y, drop_tol, (against && ka) ? &A : nullptr);
+    *kout = Q.width();
+    from_bv(Q, out);
+  });
+}
+
+// TileDiagonal from a group partition (ranges only are needed by
+// extract_tile_diagonal, hamiltonian.cpp:178-203).
+int ciref_tilediag_create(void* h, const std::uint32_t* bounds, std::uint32_t ng, void** out) {
+  return guard([&] {
+    ci::GroupPartition part;
+    const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);
+    part.group_of_state.resize(H.dim);
+    for (std::uint32_t g = 0; g < ng; ++g) {
+      part.group_ranges.push_back({bounds[g], bounds[g + 1]});
+      for (std::uint32_t r = bounds[g]; r < bounds[g + 1]; ++r) part.group_of_state[r] = g;
+    }
+    auto td = std::make_unique<ci::TileDiagonal>(ci::extract_tile_diagonal(H, part));
+    *out = td.release();
+  });
+}
+
+void ciref_tilediag_destroy(void* t) { delete static_cast<ci::TileDiagonal*>(t); }
+
+// Concatenated column-major blocks (sum n_g^2 doubles).
+int ciref_tilediag_blocks(void* t, double* out) {
+  return guard([&] {
+    const ci::TileDiagonal& td = *static_cast<ci::TileDiagonal*>(t);
+    std::size_t o = 0;
+    for (const Eigen::MatrixXd& b : td.blocks) {
+      std::memcpy(out + o, b.data(), sizeof(double) * b.size());
+      o += static_cast<std::size_t>(b.size());
+    }
+  });
+}
+
+static ci::PrecondConfig make_cfg(const double* c) {
+  // c: inner_iters, small_block_cutoff, engage_after, relres_gate,
+  //    near_converged_factor, far_threshold, column_floor_factor
+  ci::PrecondConfig cfg;
+  if (c) {
+    cfg.inner_iters = static_cast<int>(c[0]);
+    cfg.small_block_cutoff = static_cast<int>(c[1]);
+    cfg.engage_after = static_cast<int>(c[2]);
+    cfg.relres_gate = c[3];
+    cfg.near_converged_factor = c[4];
+    cfg.far_threshold = c[5];
+    cfg.column_floor_factor = c[6];
+  }
+  return cfg;
+}
+
+int ciref_choose_shifts(std::uint32_t k, const double* theta, const double* res_norm,
+                        const double* x_norm, const double* relres, int iteration, double tol,
+                        const double* cfg7, double* mu, int* engage) {
+  return guard([&] {
+    ci::ShiftInputs in;
+    in.theta.assign(theta, theta + k);
+    in.res_norm.assign(res_norm, res_norm + k);
+    in.x_norm.assign(x_norm, x_norm + k);
+    in.relres.assign(relres, relres + k);
+    ci::ShiftPlan p = ci::choose_shifts(in, iteration, tol, make_cfg(cfg7));
+    for (std::uint32_t j = 0; j < k; ++j) {
+      mu[j] = p.mu[j];
+      engage[j] = p.engage[j] ? 1 : 0;
+    }
+  });
+}
+
+int ciref_apply_preconditioner(void* t, std::uint32_t n, const double* r, std::uint32_t k,
+                               const double* mu, const int* engage, const double* cfg7,
+                               double* w) {
+  return guard([&] {
+    ci::ShiftPlan p;
+    p.mu.assign(mu, mu + k);
+    for (std::uint32_t j = 0; j < k; ++j) p.engage.push_back(engage[j] != 0);
+    ci::BlockVectors W = ci::apply_preconditioner(*static_cast<ci::TileDiagonal*>(t),
+                                                  to_bv(r, n, k), p, make_cfg(cfg7));
+    from_bv(W, w);
+  });
+}
+
+int ciref_fom_solve(std::uint32_t n, const double* block, std::uint32_t k, const double* mu,
+                    const double* rhs, int iters, double* out) {
+  return guard([&] {
+    Eigen::MatrixXd x = ci::fom_solve(to_mat(block, n, n), std::vector<double>(mu, mu + k),
+                                      to_mat(rhs, n, k), iters);
+    std::memcpy(out, x.data(), sizeof(double) * x.size());
+  });
+}
+
+// lobpcg_solve; opts: k_want, max_iter; tol; tilediag may be null.
+int ciref_lobpcg_solve(void* h, const double* x0, std::uint32_t kt, int k_want, double tol,
+                       int max_iter, void* tilediag, const double* cfg7, void** out) {
+  return guard([&] {
+    const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);
+    ci::LobpcgOptions opt;
+    opt.k_want = k_want;
+    opt.tol = tol;
+    opt.max_iter = max_iter;
+    opt.preconditioner = static_cast<const ci::TileDiagonal*>(tilediag);
+    opt.precond_config = make_cfg(cfg7);
+    auto r = std::make_unique<Report>();
+    r->rep = ci::lobpcg_solve(H, to_bv(x0, H.dim, kt), opt);
+    *out = r.release();
+  });
+}
+
+void ciref_report_destroy(void* r) { delete static_cast<Report*>(r); }
+
+void ciref_report_summary(void* rp, int* converged, int* iterations, double* norm_est,
+                          std::uint32_t* kt, std::uint64_t* nhist, std::uint64_t* counters4,
+                          std::uint32_t* nev) {
+  const ci::SolveReport& r = static_cast<Report*>(rp)->rep;
+  *converged = r.converged ? 1 : 0;
+  *iterations = r.iterations;
+  *norm_est = r.norm_estimate;
+  *kt = r.trial_vectors.width();
+  *nhist = r.history.size();
+  counters4[0] = r.counters.spmm_calls;
+  counters4[1] = r.counters.spmv_equivalents;
+  counters4[2] = r.counters.precond_applications;
+  counters4[3] = r.counters.orthogonalizations;
+  *nev = static_cast<std::uint32_t>(r.eigenvalues.size());
+}
+
+void ciref_report_arrays(void* rp, double* eigenvalues, double* trial, int* h_iter, int* h_col,
+                         double* h_relres, double* h_theta) {
+  const ci::SolveReport& r = static_cast<Report*>(rp)->rep;
+  for (std::size_t j = 0; j < r.eigenvalues.size(); ++j) eigenvalues[j] = r.eigenvalues[j];
+  from_bv(r.trial_vectors, trial);
+  for (std::size_t i = 0; i < r.history.size(); ++i) {
+    h_iter[i] = r.history[i].iteration;
+    h_col[i] = r.history[i].column;
+    h_relres[i] = r.history[i].relres;
+    h_theta[i] = r.history[i].theta;
+  }
+}
+
+// Lanczos baseline (lanczos.cpp:24-136); v0 dense vector of length dim.
+int ciref_lanczos_solve(void* h, const double* v0, int k_want, double tol, int max_iter,
+                        void** out) {
+  return guard([&] {
+    const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);
+    Eigen::VectorXd v(H.dim);
+    std::memcpy(v.data(), v0, sizeof(double) * H.dim);
+    ci::LanczosOptions opt;
+    opt.k_want = k_want;
+    opt.tol = tol;
+    opt.max_iter = max_iter;
+    auto r = std::make_unique<Report>();
+    r->rep = ci::lanczos_solve(H, v, opt);
+    *out = r.release();
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,437 @@
+// blockvec.cu -- K2/K3/K4: the tall-skinny LOBPCG block kernels.
+//
+//   K2 gram     : L^T R over column-concatenated views ([X W P] without the
+//                 hcat copies), FP64 tensor pipe (DMMA m8n8k4), each warp
+//                 streams a contiguous row range, warp/block/grid partials are
+//                 reduced in a fixed order (deterministic, like the
+//                 reference's fixed panel order, block_vectors.cpp:74-85).
+//   K3 combine  : out = [out] + [Y1 Y2 Y3] G with up to two output blocks, so
+//                 X' = XG1 + WG2 + PG3 and P' = WG2 + PG3 come out of one pass
+//                 (lobpcg.cpp:341-361); row-local, so it may run in place.
+//                 Replaces linear_combination / add_linear_combination
+//                 (block_vectors.cpp:101-160).
+//   K4 residual : R = HX - X Theta (lobpcg.cpp:256-261).
+#include <algorithm>
+#include <cstring>
+
+#include "blockvec.hpp"
+#include "device_common.cuh"
+
+namespace cieg {
+namespace {
+
+constexpr int kGramWarps = 4;
+
+template <int MT, int NT>
+__global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R, std::uint32_t n,
+                                                               std::uint32_t rows_per_warp,
+                                                               double* partials) {
+  constexpr int MA = 8 * MT, NB = 8 * NT;
+  __shared__ double red[MA * NB];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+
+  const double* pa[MT];
+  std::uint32_t la[MT];
+  const double* pb[NT];
+  std::uint32_t lb[NT];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    std::uint32_t c = 8 * mt + g;
+    pa[mt] = nullptr;
+    la[mt] = 0;
+    for (int s = 0; s < L.nseg; ++s) {
+      if (c < L.s[s].w) {
+        pa[mt] = L.s[s].p + c;
+        la[mt] = L.s[s].ld;
+        break;
+      }
+      c -= L.s[s].w;
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    std::uint32_t c = 8 * nt + g;
+    pb[nt] = nullptr;
+    lb[nt] = 0;
+    for (int s = 0; s < R.nseg; ++s) {
+      if (c < R.s[s].w) {
+        pb[nt] = R.s[s].p + c;
+        lb[nt] = R.s[s].ld;
+        break;
+      }
+      c -= R.s[s].w;
+    }
+  }
+
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+
+  const std::uint64_t gw = static_cast<std::uint64_t>(blockIdx.x) * kGramWarps + warp;
+  const std::uint64_t r0 = gw * rows_per_warp;
+  const std::uint64_t r1 = std::min<std::uint64_t>(n, r0 + rows_per_warp);
+  for (std::uint64_t i0 = r0; i0 < r1; i0 += 4) {
+    const std::uint64_t i = i0 + q;
+    const bool ok = i < r1;
+    double a[MT], b[NT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) a[mt] = (ok && pa[mt]) ? __ldg(pa[mt] + i * la[mt]) : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[nt] = (ok && pb[nt]) ? __ldg(pb[nt] + i * lb[nt]) : 0.0;
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+  }
+
+  // warps fold their partials into one buffer in warp order (deterministic)
+  for (int w = 0; w < kGramWarps; ++w) {
+    if (warp == w) {
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          const int row = 8 * mt + g, col = 8 * nt + 2 * q;
+          if (w == 0) {
+            red[row * NB + col] = acc[mt][nt][0];
+            red[row * NB + col + 1] = acc[mt][nt][1];
+          } else {
+            red[row * NB + col] += acc[mt][nt][0];
+            red[row * NB + col + 1] += acc[mt][nt][1];
+          }
+        }
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < MA * NB; e += 32 * kGramWarps)
+    partials[static_cast<std::size_t>(blockIdx.x) * MA * NB + e] = red[e];
+}
+
+// out[a + kx*b] (column major) = sum over blocks, in block order.
+__global__ void gram_reduce_kernel(const double* partials, int nblocks, int MA, int NB, int kx,
+                                   int ky, double* out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= kx * ky) return;
+  const int a = e % kx, b = e / kx;
+  double s = 0.0;
+  for (int k = 0; k < nblocks; ++k) s += partials[static_cast<std::size_t>(k) * MA * NB + a * NB + b];
+  out[e] = s;
+}
+
+template <int MT, int NT>
+void launch_gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R, int blocks,
+                 std::uint32_t rpw, double* partials) {
+  gram_kernel<MT, NT><<<blocks, 32 * kGramWarps, 0, ctx->stream>>>(L, R, n, rpw, partials);
+}
+
+using GramLauncher = void (*)(cieg_ctx*, std::uint32_t, const View3&, const View3&, int,
+                              std::uint32_t, double*);
+
+template <int MT, int... NTs>
+constexpr GramLauncher pick_nt(int nt, std::integer_sequence<int, NTs...>) {
+  GramLauncher table[] = {&launch_gram<MT, NTs + 1>...};
+  return table[nt - 1];
+}
+
+GramLauncher gram_launcher(int mt, int nt) {
+  using S = std::make_integer_sequence<int, 6>;
+  switch (mt) {
+    case 1: return pick_nt<1>(nt, S{});
+    case 2: return pick_nt<2>(nt, S{});
+    case 3: return pick_nt<3>(nt, S{});
+    case 4: return pick_nt<4>(nt, S{});
+    case 5: return pick_nt<5>(nt, S{});
+    default: return pick_nt<6>(nt, S{});
+  }
+}
+
+// ---------------------------------------------------------------- combine
+constexpr int kCombineMaxG = 3712;  // doubles carried as a kernel parameter (<= 32 KB)
+
+struct CombineParams {
+  View3 in;
+  Out2 out;
+  std::uint32_t n, kin, kout;
+  int accumulate;
+  const double* g_dev;  // used when kin*kout > kCombineMaxG
+  double g[kCombineMaxG];
+};
+
+constexpr int kCombineWarps = 8;
+
+template <int OT>
+__global__ void __launch_bounds__(32 * kCombineWarps)
+    combine_kernel(const __grid_constant__ CombineParams p) {
+  constexpr int SG = 8 * OT + 4;
+  extern __shared__ double gs[];  // [padded kin rows][SG]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const double* gsrc = p.g_dev ? p.g_dev : p.g;
+
+  // Stage G per segment with rows padded to a multiple of 4 (zero pad).
+  int poff[3];
+  {
+    int off = 0, src = 0;
+    for (int s = 0; s < p.in.nseg; ++s) {
+      poff[s] = off;
+      const int w = static_cast<int>(p.in.s[s].w), wp = (w + 3) & ~3;
+      for (int e = threadIdx.x; e < wp * SG; e += blockDim.x) {
+        const int k = e / SG, c = e - k * SG;
+        gs[(off + k) * SG + c] =
+            (k < w && c < static_cast<int>(p.kout)) ? gsrc[(src + k) + static_cast<std::size_t>(c) * p.kin] : 0.0;
+      }
+      off += wp;
+      src += w;
+    }
+  }
+  __syncthreads();
+
+  const std::uint64_t ngroups = (p.n + 7) / 8;
+  for (std::uint64_t grp = static_cast<std::uint64_t>(blockIdx.x) * kCombineWarps + warp; grp < ngroups;
+       grp += static_cast<std::uint64_t>(gridDim.x) * kCombineWarps) {
+    const std::uint64_t i0 = grp * 8;
+    double acc[OT][2];
+    // C fragment rows i0 + g, columns 8 nt + 2q (+1)
+    const std::uint64_t crow = i0 + g;
+#pragma unroll
+    for (int nt = 0; nt < OT; ++nt) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = 0.0;
+        const std::uint32_t c = 8 * nt + 2 * q + h;
+        if (p.accumulate && crow < p.n && c < p.kout) {
+          if (c < p.out.w0)
+            v = p.out.o0[crow * p.out.ld0 + c];
+          else
+            v = p.out.o1[crow * p.out.ld1 + (c - p.out.w0)];
+        }
+        acc[nt][h] = v;
+      }
+    }
+    const std::uint64_t arow = i0 + g;
+    for (int s = 0; s < p.in.nseg; ++s) {
+      const double* base = p.in.s[s].p;
+      const std::uint32_t ld = p.in.s[s].ld, w = p.in.s[s].w;
+      const int ksteps = static_cast<int>((w + 3) / 4);
+      const double* gsb = gs + (poff[s] + q) * SG + g;
+      for (int ks = 0; ks < ksteps; ++ks) {
+        const std::uint32_t k = 4 * ks + q;
+        const double a = (arow < p.n && k < w) ? base[arow * ld + k] : 0.0;
+#pragma unroll
+        for (int nt = 0; nt < OT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a, gsb[4 * ks * SG + 8 * nt]);
+      }
+    }
+    if (crow < p.n) {
+#pragma unroll
+      for (int nt = 0; nt < OT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const std::uint32_t c = 8 * nt + 2 * q + h;
+          if (c >= p.kout) continue;
+          if (c < p.out.w0)
+            p.out.o0[crow * p.out.ld0 + c] = acc[nt][h];
+          else
+            p.out.o1[crow * p.out.ld1 + (c - p.out.w0)] = acc[nt][h];
+        }
+    }
+  }
+}
+
+template <int OT>
+void launch_combine(cieg_ctx* ctx, const CombineParams& prm, int blocks) {
+  constexpr int SG = 8 * OT + 4;
+  int rows = 0;
+  for (int s = 0; s < prm.in.nseg; ++s) rows += (static_cast<int>(prm.in.s[s].w) + 3) & ~3;
+  const std::size_t smem = sizeof(double) * static_cast<std::size_t>(std::max(rows, 4)) * SG;
+  if (smem > 48 * 1024)
+    CIEG_CUDA(cudaFuncSetAttribute(combine_kernel<OT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+  combine_kernel<OT><<<blocks, 32 * kCombineWarps, smem, ctx->stream>>>(prm);
+}
+
+// ---------------------------------------------------------------- residual
+__global__ void residual_kernel(std::uint64_t total, std::uint32_t k, const double* __restrict__ hx,
+                                const double* __restrict__ x, const double* __restrict__ theta,
+                                double* __restrict__ r) {
+  for (std::uint64_t e = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    const std::uint32_t j = static_cast<std::uint32_t>(e % k);
+    r[e] = hx[e] - theta[j] * x[e];
+  }
+}
+
+__global__ void gather_kernel(std::uint64_t n, std::uint32_t ksrc, const double* __restrict__ src,
+                              std::uint32_t kd, const std::uint32_t* __restrict__ cols,
+                              double* __restrict__ dst) {
+  const std::uint64_t total = n * kd;
+  for (std::uint64_t e = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+    const std::uint64_t i = e / kd;
+    const std::uint32_t j = static_cast<std::uint32_t>(e - i * kd);
+    dst[e] = src[i * ksrc + cols[j]];
+  }
+}
+
+int grid_for(cieg_ctx* ctx, std::uint64_t work, int per_block) {
+  const std::uint64_t want = (work + per_block - 1) / per_block;
+  return static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, 4ull * ctx->sm_count)));
+}
+
+}  // namespace
+
+std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R) {
+  const std::uint32_t kx = L.width, ky = R.width;
+  std::vector<double> out(static_cast<std::size_t>(kx) * ky, 0.0);
+  if (kx == 0 || ky == 0) return out;
+  if (kx > 48 || ky > 48) fail(CIEG_ERR_CONFIG, "gram: block width above 48");
+  const int MT = static_cast<int>((kx + 7) / 8), NT = static_cast<int>((ky + 7) / 8);
+  // fixed decomposition: rows_per_warp multiple of 4, at most 2 blocks per SM
+  const int max_blocks = 2 * ctx->sm_count;
+  std::uint64_t rpw = (static_cast<std::uint64_t>(n) + max_blocks * kGramWarps - 1) / (max_blocks * kGramWarps);
+  rpw = std::max<std::uint64_t>(64, (rpw + 3) & ~3ull);
+  const int blocks = static_cast<int>(std::max<std::uint64_t>(1, (n + rpw * kGramWarps - 1) / (rpw * kGramWarps)));
+  const int MA = 8 * MT, NB = 8 * NT;
+  double* partials = static_cast<double*>(ctx->scratch_red.get(sizeof(double) * blocks * MA * NB + 64));
+  double* dout = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 48 * 48));
+  if (n > 0) {
+    gram_launcher(MT, NT)(ctx, n, L, R, blocks, static_cast<std::uint32_t>(rpw), partials);
+    CIEG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    const int e = static_cast<int>(kx * ky);
+    gram_reduce_kernel<<<(e + 127) / 128, 128, 0, ctx->stream>>>(partials, blocks, MA, NB,
+                                                                  static_cast<int>(kx), static_cast<int>(ky), dout);
+    CIEG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+    double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
+    CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    std::memcpy(out.data(), pin, sizeof(double) * e);
+  }
+  return out;
+}
+
+void combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_host, std::uint32_t kout,
+             const Out2& out, bool accumulate) {
+  if (n == 0 || kout == 0) return;
+  if (kout > 48) fail(CIEG_ERR_CONFIG, "combine: output width above 48");
+  if (out.w0 + out.w1 != kout) fail(CIEG_ERR_DIMENSION, "combine: output split mismatch");
+  const std::uint32_t kin = in.width;
+  if (kin == 0) {
+    if (!accumulate) {  // Y * G with an empty Y is a zero block
+      for (int k = 0; k < 2; ++k) {
+        double* o = k == 0 ? out.o0 : out.o1;
+        const std::uint32_t w = k == 0 ? out.w0 : out.w1, ld = k == 0 ? out.ld0 : out.ld1;
+        if (!o || w == 0) continue;
+        CIEG_CUDA(cudaMemset2DAsync(o, ld * sizeof(double), 0, w * sizeof(double), n, ctx->stream));
+      }
+    }
+    return;
+  }
+  static thread_local CombineParams prm;  // ~30 KB: keep off the stack
+  prm.in = in;
+  prm.out = out;
+  prm.n = n;
+  prm.kin = kin;
+  prm.kout = kout;
+  prm.accumulate = accumulate ? 1 : 0;
+  const std::size_t ng = static_cast<std::size_t>(kin) * kout;
+  DevBuf* gbuf = nullptr;
+  if (ng <= static_cast<std::size_t>(kCombineMaxG)) {
+    std::memcpy(prm.g, g_host, sizeof(double) * ng);
+    prm.g_dev = nullptr;
+  } else {
+    gbuf = &ctx->scratch_small;
+    double* d = static_cast<double*>(gbuf->get(sizeof(double) * ng));
+    CIEG_CUDA(cudaMemcpyAsync(d, g_host, sizeof(double) * ng, cudaMemcpyHostToDevice, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    prm.g_dev = d;
+  }
+  const int OT = static_cast<int>((kout + 7) / 8);
+  const int blocks = grid_for(ctx, (n + 7) / 8, kCombineWarps * 4);
+  switch (OT) {
+    case 1: launch_combine<1>(ctx, prm, blocks); break;
+    case 2: launch_combine<2>(ctx, prm, blocks); break;
+    case 3: launch_combine<3>(ctx, prm, blocks); break;
+    case 4: launch_combine<4>(ctx, prm, blocks); break;
+    case 5: launch_combine<5>(ctx, prm, blocks); break;
+    default: launch_combine<6>(ctx, prm, blocks); break;
+  }
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+void residual(cieg_ctx* ctx, std::uint32_t n, std::uint32_t k, const double* hx, const double* x,
+              const double* theta_host, double* r) {
+  if (n == 0 || k == 0) return;
+  double* th = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 64));
+  // theta travels through a small pinned staging copy, ordered on the stream
+  double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(pin, theta_host, sizeof(double) * k);
+  CIEG_CUDA(cudaMemcpyAsync(th, pin, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
+  const std::uint64_t total = static_cast<std::uint64_t>(n) * k;
+  residual_kernel<<<grid_for(ctx, total, 1024), 256, 0, ctx->stream>>>(total, k, hx, x, th, r);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+void gather_columns(cieg_ctx* ctx, std::uint32_t n, const double* src, std::uint32_t ksrc,
+                    const std::vector<std::uint32_t>& cols, double* dst) {
+  const std::uint32_t kd = static_cast<std::uint32_t>(cols.size());
+  if (n == 0 || kd == 0) return;
+  std::uint32_t* dc = static_cast<std::uint32_t*>(ctx->scratch_small.get(sizeof(std::uint32_t) * 64 + 64));
+  std::uint32_t* pin = static_cast<std::uint32_t*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(pin, cols.data(), sizeof(std::uint32_t) * kd);
+  CIEG_CUDA(cudaMemcpyAsync(dc, pin, sizeof(std::uint32_t) * kd, cudaMemcpyHostToDevice, ctx->stream));
+  const std::uint64_t total = static_cast<std::uint64_t>(n) * kd;
+  gather_kernel<<<grid_for(ctx, total, 1024), 256, 0, ctx->stream>>>(n, ksrc, src, kd, dc, dst);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+}  // namespace cieg
+
+// ------------------------------------------------------------------ C ABI
+extern "C" {
+
+int cieg_block_inner(cieg_ctx* ctx, uint32_t n, const double* x_dev, uint32_t kx, const double* y_dev,
+                     uint32_t ky, double* out_host) {
+  return cieg::guarded([&] {
+    if (!ctx || (!out_host && kx && ky)) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_block_inner: null argument");
+    auto g = cieg::gram(ctx, n, cieg::view({cieg::seg(x_dev, kx)}), cieg::view({cieg::seg(y_dev, ky)}));
+    std::memcpy(out_host, g.data(), sizeof(double) * g.size());
+  });
+}
+
+int cieg_linear_combination(cieg_ctx* ctx, uint32_t n, const double* y_dev, uint32_t kin,
+                            const double* g_host, uint32_t kout, double* out_dev) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_linear_combination: null context");
+    if (y_dev == out_dev && kin != kout)
+      cieg::fail(CIEG_ERR_ARGUMENT, "cieg_linear_combination: in-place needs equal widths");
+    cieg::combine(ctx, n, cieg::view({cieg::seg(y_dev, kin)}), g_host, kout, cieg::out1(out_dev, kout), false);
+  });
+}
+
+int cieg_add_linear_combination(cieg_ctx* ctx, uint32_t n, double* y_dev, uint32_t ky, const double* x_dev,
+                                uint32_t kx, const double* g_host) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_add_linear_combination: null context");
+    cieg::combine(ctx, n, cieg::view({cieg::seg(x_dev, kx)}), g_host, ky, cieg::out1(y_dev, ky), true);
+  });
+}
+
+int cieg_column_norms(cieg_ctx* ctx, uint32_t n, const double* x_dev, uint32_t k, double* out_host) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_column_norms: null context");
+    auto v = cieg::view({cieg::seg(x_dev, k)});
+    auto g = cieg::gram(ctx, n, v, v);
+    for (uint32_t j = 0; j < k; ++j) out_host[j] = std::sqrt(g[j + static_cast<std::size_t>(k) * j]);
+  });
+}
+
+}  // extern "C"

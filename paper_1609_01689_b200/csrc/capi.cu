@@ -1,0 +1,189 @@
+// capi.cu -- C ABI plumbing: errors, contexts, matrix upload, SpMM entry
+// points (include/cieg.h).
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+
+#include "context.hpp"
+#include "tiling.hpp"
+
+namespace cieg {
+
+namespace {
+thread_local std::string g_last_error;
+}
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+void clear_last_error() { g_last_error.clear(); }
+
+template <typename T>
+T* upload_vec(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* d = nullptr;
+  CIEG_CUDA(cudaMalloc(&d, v.size() * sizeof(T)));
+  CIEG_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+}  // namespace cieg
+
+cieg_mat::~cieg_mat() {
+  cudaFree(panel_start);
+  cudaFree(tile_off);
+  cudaFree(idx);
+  cudaFree(val);
+  cudaFree(work_off);
+  cudaFree(work_tile);
+  cudaFree(work_other);
+  cudaFree(work_kind);
+}
+
+extern "C" {
+
+const char* cieg_last_error(void) { return cieg::g_last_error.c_str(); }
+const char* cieg_version(void) { return "cieg 0.1 (sm_100a)"; }
+
+int cieg_ctx_create(int device, cieg_ctx** out) {
+  return cieg::guarded([&] {
+    if (!out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_ctx_create: null output");
+    int n = 0;
+    CIEG_CUDA(cudaGetDeviceCount(&n));
+    if (device < 0 || device >= n) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_ctx_create: bad device index");
+    CIEG_CUDA(cudaSetDevice(device));
+    auto* c = new cieg_ctx;
+    c->device = device;
+    cudaDeviceProp prop;
+    CIEG_CUDA(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+      cieg::fail(CIEG_ERR_CUDA, std::string("libcieg is built for sm_100a; device is ") + prop.name);
+    c->sm_count = prop.multiProcessorCount;
+    CIEG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    *out = c;
+  });
+}
+
+int cieg_ctx_destroy(cieg_ctx* ctx) {
+  if (!ctx) return CIEG_OK;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->scratch_x.release();
+  ctx->scratch_y.release();
+  ctx->scratch_red.release();
+  ctx->scratch_small.release();
+  ctx->pinned_small.release();
+  cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return CIEG_OK;
+}
+
+int cieg_ctx_synchronize(cieg_ctx* ctx) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+void* cieg_ctx_stream(cieg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                       uint32_t ngroups, uint32_t tile_edge, cieg_mat** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !csb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_upload: null argument");
+    if (csb->precision != 0 && csb->precision != 1)
+      cieg::fail(CIEG_ERR_FORMAT, "bad precision tag");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    std::uint32_t te = tile_edge;
+    if (te == 0) {
+      // Tile edge follows the group size: 64-row groups -> 64, else 128.
+      te = 128;
+      if (group_bounds && ngroups > 0) {
+        std::uint32_t mx = 0;
+        for (std::uint32_t g = 0; g < ngroups; ++g) mx = std::max(mx, group_bounds[g + 1] - group_bounds[g]);
+        if (mx <= 64) te = 64;
+      }
+    }
+    if (te != 64 && te != 128) cieg::fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
+    std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te);
+    cieg::HostTiles ht;
+    cieg::build_tiles(*csb, panels, te, ht);
+
+    auto* m = new cieg_mat;
+    try {
+      m->ctx = ctx;
+      m->dim = ht.dim;
+      m->tile_edge = te;
+      m->precision = ht.precision;
+      m->nnz = ht.nnz;
+      m->npanels = ht.npanels();
+      m->ntiles = ht.ntiles();
+      m->panel_start_host = ht.panel_start;
+      m->panel_start = cieg::upload_vec(ht.panel_start);
+      m->tile_off = cieg::upload_vec(ht.tile_off);
+      m->idx = cieg::upload_vec(ht.idx);
+      if (ht.precision == 0)
+        m->val = cieg::upload_vec(ht.val32);
+      else
+        m->val = cieg::upload_vec(ht.val64);
+      m->work_off = cieg::upload_vec(ht.work_off);
+      m->work_tile = cieg::upload_vec(ht.work_tile);
+      m->work_other = cieg::upload_vec(ht.work_other);
+      m->work_kind = cieg::upload_vec(ht.work_kind);
+      m->tile_bytes = ht.nnz * (4 + (ht.precision == 0 ? 4 : 8));
+    } catch (...) {
+      delete m;
+      throw;
+    }
+    *out = m;
+  });
+}
+
+int cieg_matrix_destroy(cieg_mat* mat) {
+  if (mat) {
+    cudaSetDevice(mat->ctx->device);
+    cudaStreamSynchronize(mat->ctx->stream);
+    delete mat;
+  }
+  return CIEG_OK;
+}
+
+int cieg_matrix_info(const cieg_mat* m, uint32_t* dim, uint64_t* nnz, uint32_t* npanels,
+                     uint64_t* ntiles, uint32_t* tile_edge, int* precision, uint64_t* bytes) {
+  return cieg::guarded([&] {
+    if (!m) cieg::fail(CIEG_ERR_ARGUMENT, "null matrix");
+    if (dim) *dim = m->dim;
+    if (nnz) *nnz = m->nnz;
+    if (npanels) *npanels = m->npanels;
+    if (ntiles) *ntiles = m->ntiles;
+    if (tile_edge) *tile_edge = m->tile_edge;
+    if (precision) *precision = m->precision;
+    if (bytes) *bytes = m->tile_bytes;
+  });
+}
+
+int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y_dev, uint32_t m) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm: null handle");
+    if ((!x_dev || !y_dev) && m > 0 && mat->dim > 0) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm: null vector");
+    if (x_dev == y_dev && m > 0) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm: X and U must not alias");
+    cieg::launch_spmm(ctx, mat, x_dev, m, y_dev, m, m);
+  });
+}
+
+int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
+                   uint32_t m) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host: null handle");
+    const std::size_t bytes = static_cast<std::size_t>(mat->dim) * m * sizeof(double);
+    if (bytes == 0) return;
+    if (!x_host || !y_host) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host: null vector");
+    double* dx = static_cast<double*>(ctx->scratch_x.get(bytes));
+    double* dy = static_cast<double*>(ctx->scratch_y.get(bytes));
+    CIEG_CUDA(cudaMemcpyAsync(dx, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    cieg::launch_spmm(ctx, mat, dx, m, dy, m, m);
+    CIEG_CUDA(cudaMemcpyAsync(y_host, dy, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// context.hpp -- device-side objects behind the opaque C handles.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "cieg_internal.hpp"
+
+namespace cieg {
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(CIEG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CIEG_CUDA(call) ::cieg::cuda_check((call), #call)
+
+// Growable device scratch buffer.
+struct DevBuf {
+  void* ptr = nullptr;
+  std::size_t bytes = 0;
+  void* get(std::size_t want) {
+    if (want > bytes) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      CIEG_CUDA(cudaMalloc(&ptr, want));
+      bytes = want;
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+struct PinnedBuf {
+  void* ptr = nullptr;
+  std::size_t bytes = 0;
+  void* get(std::size_t want) {
+    if (want > bytes) {
+      if (ptr) cudaFreeHost(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      CIEG_CUDA(cudaMallocHost(&ptr, want));
+      bytes = want;
+    }
+    return ptr;
+  }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+}  // namespace cieg
+
+struct cieg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::uint64_t launches = 0;
+  int sm_count = 148;
+  cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
+  cieg::PinnedBuf pinned_small;
+};
+
+struct cieg_mat {
+  cieg_ctx* ctx = nullptr;
+  std::uint32_t dim = 0;
+  std::uint32_t tile_edge = 0;
+  int precision = 0;
+  std::uint64_t nnz = 0;
+  std::uint32_t npanels = 0;
+  std::uint64_t ntiles = 0;
+  std::uint64_t tile_bytes = 0;
+  std::vector<std::uint32_t> panel_start_host;
+  // device arrays
+  std::uint32_t* panel_start = nullptr;
+  std::uint64_t* tile_off = nullptr;
+  std::uint32_t* idx = nullptr;
+  void* val = nullptr;
+  std::uint32_t* work_off = nullptr;
+  std::uint32_t* work_tile = nullptr;
+  std::uint32_t* work_other = nullptr;
+  std::uint32_t* work_kind = nullptr;
+  ~cieg_mat();
+};
+
+namespace cieg {
+
+// Launch the owner-computes SpMM over device X/Y (row-major, ld = ldx/ldy).
+void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
+                 std::uint32_t ldy, std::uint32_t mcols);
+
+}  // namespace cieg

@@ -1,0 +1,657 @@
+// precond.cu -- K5: tile-diagonal preconditioner with per-column shifts,
+// replacing ci::apply_preconditioner (proj/src/precond.cpp:160-207).
+//
+//   * groups with n_g <= small_block_cutoff: one CTA per (group, distinct
+//     shift) -- partial-pivot LU of (H~_g - mu I) in shared memory, the
+//     |U_ii| <= 1e-14 max|U_ii| singularity test, one perturbation
+//     mu + 1e-8 (1 + |mu|), then pass-through (precond.cpp:61-83); the
+//     columns sharing a shift share the factorization (precond.cpp:183-192);
+//   * larger groups: one CTA per (group, column chunk) running the fused
+//     multi-RHS FOM (precond.cpp:87-158): one dense block product advances
+//     every Krylov space, two-pass MGS, lucky breakdown at 1e-12, Hessenberg
+//     solve by partial-pivot LU.
+// Arithmetic is kept un-fused (mul then add) and every reduction runs in the
+// reference's sequential order, so for identical inputs the result is
+// bitwise identical to the reference compiled on the host.
+#include <cstdio>
+#include <cstring>
+#include <map>
+
+#include "precond.hpp"
+
+#define DMUL __dmul_rn
+#define DADD __dadd_rn
+#define DSUB __dsub_rn
+#define DDIV __ddiv_rn
+
+cieg_prec::~cieg_prec() {
+  cudaFree(bounds);
+  cudaFree(block_off);
+  cudaFree(blocks);
+}
+
+namespace cieg {
+
+ShiftPlan choose_shifts(const std::vector<double>& theta, const std::vector<double>& res_norm,
+                        const std::vector<double>& x_norm, const std::vector<double>& relres,
+                        int iteration, double tol, const cieg_precond_config& cfg) {
+  const std::size_t k = theta.size();
+  ShiftPlan plan;
+  plan.mu = theta;
+  plan.engage.assign(k, 1);
+  if (iteration <= cfg.engage_after) {
+    plan.engage.assign(k, 0);
+  } else if (!relres.empty() && relres[0] > cfg.relres_gate) {
+    plan.engage.assign(k, 0);
+  } else {
+    for (std::size_t j = 0; j < k; ++j)
+      if (relres[j] <= cfg.column_floor_factor * tol) plan.engage[j] = 0;
+  }
+  for (std::size_t j = 0; j < k; ++j) {
+    const double backed = theta[j] - 2.0 * res_norm[j] / x_norm[j];
+    plan.mu[j] = j == 0 ? backed : std::min(backed, plan.mu[0]);
+  }
+  std::size_t first_far = k;
+  for (std::size_t i = 0; i < k; ++i)
+    if (relres[i] > cfg.far_threshold) {
+      first_far = i;
+      break;
+    }
+  if (first_far < k) {
+    const double carried = plan.mu[first_far > 0 ? first_far - 1 : 0];
+    for (std::size_t t = first_far; t < k; ++t) plan.mu[t] = carried;
+  }
+  return plan;
+}
+
+namespace {
+
+constexpr int kMaxDirect = 64;
+constexpr int kLuThreads = 128;
+constexpr int kMaxCols = 64;
+
+struct LuParams {
+  const std::uint32_t* bounds;
+  const std::uint64_t* block_off;
+  const double* blocks;
+  const std::uint32_t* groups;  // small group ids
+  const double* r;
+  double* w;
+  std::uint32_t k;              // row stride of R / W
+  int nshift;
+  double shift[kMaxCols];
+  int col_start[kMaxCols + 1];  // columns of shift s: cols[col_start[s] .. col_start[s+1])
+  int cols[kMaxCols];
+  int* singular_count;
+};
+
+__device__ bool lu_factor(double* A, int n, int ld, int* perm, double mu, const double* src,
+                          double* red_v, int* red_i) {
+  const int tid = threadIdx.x;
+  for (int e = tid; e < n * n; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    double v = src[e];
+    if (i == j) v = DSUB(v, mu);
+    A[i + j * ld] = v;
+  }
+  for (int i = tid; i < n; i += blockDim.x) perm[i] = i;
+  __syncthreads();
+  for (int k = 0; k < n; ++k) {
+    if (tid == 0) {  // first occurrence of the largest |a_ik|, i >= k
+      int p = k;
+      double best = fabs(A[k + k * ld]);
+      for (int i = k + 1; i < n; ++i) {
+        const double v = fabs(A[i + k * ld]);
+        if (v > best) {
+          best = v;
+          p = i;
+        }
+      }
+      red_i[0] = p;
+    }
+    __syncthreads();
+    const int p = red_i[0];
+    if (p != k) {
+      for (int j = tid; j < n; j += blockDim.x) {
+        const double t = A[k + j * ld];
+        A[k + j * ld] = A[p + j * ld];
+        A[p + j * ld] = t;
+      }
+      if (tid == 0) {
+        const int t = perm[k];
+        perm[k] = perm[p];
+        perm[p] = t;
+      }
+    }
+    __syncthreads();
+    const double piv = A[k + k * ld];
+    if (piv != 0.0)
+      for (int i = k + 1 + tid; i < n; i += blockDim.x) A[i + k * ld] = DDIV(A[i + k * ld], piv);
+    __syncthreads();
+    const int m = n - k - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = k + 1 + e % m, j = k + 1 + e / m;
+      const double ukj = A[k + j * ld];
+      if (ukj != 0.0) A[i + j * ld] = DSUB(A[i + j * ld], DMUL(A[i + k * ld], ukj));
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    double mx = fabs(A[0]), mn = fabs(A[0]);
+    for (int i = 1; i < n; ++i) {
+      const double v = fabs(A[i + i * ld]);
+      mx = v > mx ? v : mx;
+      mn = v < mn ? v : mn;
+    }
+    const double scale = mx > 1e-300 ? mx : 1e-300;
+    red_i[1] = (mn <= 1e-14 * scale) ? 1 : 0;
+  }
+  __syncthreads();
+  (void)red_v;
+  return red_i[1] == 0;
+}
+
+__global__ void __launch_bounds__(kLuThreads) lu_direct_kernel(const __grid_constant__ LuParams p) {
+  __shared__ double A[kMaxDirect * (kMaxDirect + 1)];
+  extern __shared__ double tmp_dyn[];  // [columns of this shift][kMaxDirect]
+  __shared__ int perm[kMaxDirect];
+  __shared__ double red_v[4];
+  __shared__ int red_i[4];
+  const std::uint32_t grp = p.groups[blockIdx.x];
+  const int s = blockIdx.y;
+  const std::uint32_t r0 = p.bounds[grp];
+  const int n = static_cast<int>(p.bounds[grp + 1] - r0);
+  const int ld = n + 1;
+  const double* src = p.blocks + p.block_off[grp];
+  double mu = p.shift[s];
+  bool ok = lu_factor(A, n, ld, perm, mu, src, red_v, red_i);
+  if (!ok) {
+    mu = mu + 1e-8 * (1.0 + fabs(mu));
+    ok = lu_factor(A, n, ld, perm, mu, src, red_v, red_i);
+  }
+  if (!ok) {  // pass-through: W keeps R for these columns
+    if (threadIdx.x == 0) {
+      atomicAdd(p.singular_count, 1);
+    }
+    return;
+  }
+  const int c0 = p.col_start[s], c1 = p.col_start[s + 1];
+  for (int ci = c0 + static_cast<int>(threadIdx.x); ci < c1; ci += blockDim.x) {
+    const int j = p.cols[ci];
+    double* t = tmp_dyn + static_cast<std::size_t>(ci - c0) * kMaxDirect;
+    for (int i = 0; i < n; ++i) t[i] = p.r[static_cast<std::size_t>(r0 + perm[i]) * p.k + j];
+    for (int i = 0; i < n; ++i) {
+      double acc = t[i];
+      for (int kk = 0; kk < i; ++kk) acc = DSUB(acc, DMUL(A[i + kk * ld], t[kk]));
+      t[i] = acc;
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double acc = t[i];
+      for (int kk = i + 1; kk < n; ++kk) acc = DSUB(acc, DMUL(A[i + kk * ld], t[kk]));
+      t[i] = DDIV(acc, A[i + i * ld]);
+    }
+    for (int i = 0; i < n; ++i) p.w[static_cast<std::size_t>(r0 + i) * p.k + j] = t[i];
+  }
+}
+
+// ------------------------------------------------------------------ FOM
+constexpr int kFomThreads = 256;
+constexpr int kFomMaxSteps = 3;
+
+struct FomParams {
+  const std::uint32_t* bounds;
+  const std::uint64_t* block_off;
+  const double* blocks;
+  const std::uint32_t* groups;  // large group ids
+  const double* r;
+  double* w;
+  std::uint32_t k;
+  int ncols;                     // engaged columns
+  int chunk;                     // columns per CTA
+  int iters;
+  int cols[kMaxCols];
+  double mu[kMaxCols];
+};
+
+// Small partial-pivot LU solve (dense_small.hpp order) of hm (m x m, col-major).
+__device__ void tiny_lu_solve(double* hm, int m, double* rhs) {
+  int perm[kFomMaxSteps];
+  for (int i = 0; i < m; ++i) perm[i] = i;
+  for (int k = 0; k < m; ++k) {
+    int p = k;
+    double best = fabs(hm[k + k * m]);
+    for (int i = k + 1; i < m; ++i) {
+      const double v = fabs(hm[i + k * m]);
+      if (v > best) {
+        best = v;
+        p = i;
+      }
+    }
+    if (p != k) {
+      for (int j = 0; j < m; ++j) {
+        const double t = hm[k + j * m];
+        hm[k + j * m] = hm[p + j * m];
+        hm[p + j * m] = t;
+      }
+      const int t = perm[k];
+      perm[k] = perm[p];
+      perm[p] = t;
+    }
+    const double piv = hm[k + k * m];
+    if (piv != 0.0)
+      for (int i = k + 1; i < m; ++i) hm[i + k * m] = DDIV(hm[i + k * m], piv);
+    for (int j = k + 1; j < m; ++j) {
+      const double ukj = hm[k + j * m];
+      if (ukj == 0.0) continue;
+      for (int i = k + 1; i < m; ++i) hm[i + j * m] = DSUB(hm[i + j * m], DMUL(hm[i + k * m], ukj));
+    }
+  }
+  double t[kFomMaxSteps];
+  for (int i = 0; i < m; ++i) t[i] = rhs[perm[i]];
+  for (int i = 0; i < m; ++i) {
+    double s = t[i];
+    for (int kk = 0; kk < i; ++kk) s = DSUB(s, DMUL(hm[i + kk * m], t[kk]));
+    t[i] = s;
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    double s = t[i];
+    for (int kk = i + 1; kk < m; ++kk) s = DSUB(s, DMUL(hm[i + kk * m], t[kk]));
+    t[i] = DDIV(s, hm[i + i * m]);
+  }
+  for (int i = 0; i < m; ++i) rhs[i] = t[i];
+}
+
+__global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant__ FomParams p) {
+  extern __shared__ double sm[];
+  const std::uint32_t grp = p.groups[blockIdx.x];
+  const std::uint32_t r0 = p.bounds[grp];
+  const int n = static_cast<int>(p.bounds[grp + 1] - r0);
+  const int cbeg = blockIdx.y * p.chunk;
+  const int cc = min(p.chunk, p.ncols - cbeg);
+  const int CC = p.chunk;
+  const int mmax = min(p.iters, n);
+  // layout: basis[(mmax+1)][n][CC], wv[n][CC], hess[CC][4*3], beta[CC], flags
+  double* basis = sm;
+  double* wv = basis + static_cast<std::size_t>(mmax + 1) * n * CC;
+  double* hess = wv + static_cast<std::size_t>(n) * CC;                 // CC * 16
+  double* beta = hess + CC * 16;                                        // CC
+  double* scal = beta + CC;                                             // CC (scale / norm scratch)
+  int* active = reinterpret_cast<int*>(scal + CC);                      // CC
+  int* steps = active + CC;                                             // CC
+  int* done = steps + CC;                                               // CC: finished with m = done
+  const double* blk = p.blocks + p.block_off[grp];
+  const int tid = threadIdx.x;
+  auto B = [&](int m, int i, int c) -> double& { return basis[(static_cast<std::size_t>(m) * n + i) * CC + c]; };
+
+  // beta_j = ||rhs_j||, sequential order
+  for (int c = tid; c < cc; c += blockDim.x) {
+    const int j = p.cols[cbeg + c];
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) {
+      const double v = p.r[static_cast<std::size_t>(r0 + i) * p.k + j];
+      s = DADD(s, DMUL(v, v));
+    }
+    beta[c] = sqrt(s);
+    active[c] = beta[c] != 0.0;
+    steps[c] = 0;
+    done[c] = 0;
+    for (int e = 0; e < 16; ++e) hess[c * 16 + e] = 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * cc; e += blockDim.x) {
+    const int i = e / cc, c = e - i * cc;
+    const int j = p.cols[cbeg + c];
+    const double v = p.r[static_cast<std::size_t>(r0 + i) * p.k + j];
+    B(0, i, c) = beta[c] != 0.0 ? DDIV(v, beta[c]) : 0.0;
+  }
+  __syncthreads();
+
+  const int H_LD = 4;  // hess[c] is (mmax+1) x mmax, column major, ld 4
+  for (int m = 0; m < mmax; ++m) {
+    // z = block * v_m for active columns (sequential k order per element)
+    for (int i = tid; i < n; i += blockDim.x) {
+      double z[kMaxCols > 16 ? 16 : kMaxCols];
+      for (int c = 0; c < cc; ++c) z[c] = 0.0;
+      for (int kk = 0; kk < n; ++kk) {
+        const double a = blk[i + static_cast<std::size_t>(kk) * n];
+        for (int c = 0; c < cc; ++c)
+          if (active[c]) z[c] = DADD(z[c], DMUL(a, B(m, kk, c)));
+      }
+      for (int c = 0; c < cc; ++c)
+        if (active[c]) wv[i * CC + c] = DSUB(z[c], DMUL(p.mu[cbeg + c], B(m, i, c)));
+    }
+    __syncthreads();
+    // scale = max(beta, ||w||)
+    for (int c = tid; c < cc; c += blockDim.x) {
+      if (!active[c]) continue;
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s = DADD(s, DMUL(wv[i * CC + c], wv[i * CC + c]));
+      const double nw = sqrt(s);
+      scal[c] = beta[c] > nw ? beta[c] : nw;
+    }
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int ib = 0; ib <= m; ++ib) {
+        for (int c = tid; c < cc; c += blockDim.x) {
+          if (!active[c]) continue;
+          double h = 0.0;
+          for (int i = 0; i < n; ++i) h = DADD(h, DMUL(B(ib, i, c), wv[i * CC + c]));
+          double& hh = hess[c * 16 + ib + m * H_LD];
+          hh = pass == 0 ? h : DADD(hh, h);
+          // stash h for the row update
+          hess[c * 16 + 12 + (ib & 3)] = h;
+        }
+        __syncthreads();
+        for (int e = tid; e < n * cc; e += blockDim.x) {
+          const int i = e / cc, c = e - i * cc;
+          if (!active[c]) continue;
+          const double h = hess[c * 16 + 12 + (ib & 3)];
+          wv[i * CC + c] = DSUB(wv[i * CC + c], DMUL(h, B(ib, i, c)));
+        }
+        __syncthreads();
+      }
+    }
+    // norm, breakdown test, next basis vector
+    for (int c = tid; c < cc; c += blockDim.x) {
+      if (!active[c]) continue;
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s = DADD(s, DMUL(wv[i * CC + c], wv[i * CC + c]));
+      const double nrm = sqrt(s);
+      steps[c] = m + 1;
+      const double sc = scal[c] > 1.0 ? scal[c] : 1.0;
+      if (nrm <= 1e-12 * sc) {
+        hess[c * 16 + (m + 1) + m * H_LD] = 0.0;
+        active[c] = 0;
+        done[c] = m + 1;  // lucky breakdown: finish with m+1 steps
+      } else {
+        hess[c * 16 + (m + 1) + m * H_LD] = nrm;
+        scal[c] = nrm;
+      }
+    }
+    __syncthreads();
+    if (m + 1 <= mmax) {
+      for (int e = tid; e < n * cc; e += blockDim.x) {
+        const int i = e / cc, c = e - i * cc;
+        if (!active[c]) continue;
+        B(m + 1, i, c) = DDIV(wv[i * CC + c], scal[c]);
+      }
+    }
+    __syncthreads();
+  }
+  // finish every column that ran (active ones with steps, and breakdowns)
+  __shared__ double ycoef[kMaxCols][kFomMaxSteps];
+  for (int c = tid; c < cc; c += blockDim.x) {
+    const int m = done[c] ? done[c] : (active[c] ? steps[c] : 0);
+    if (m == 0) {
+      done[c] = 0;
+      continue;
+    }
+    double hm[kFomMaxSteps * kFomMaxSteps];
+    for (int a = 0; a < m; ++a)
+      for (int b = 0; b < m; ++b) hm[a + b * m] = hess[c * 16 + a + b * H_LD];
+    double rhs[kFomMaxSteps] = {0.0, 0.0, 0.0};
+    rhs[0] = beta[c];
+    tiny_lu_solve(hm, m, rhs);
+    for (int a = 0; a < m; ++a) ycoef[c][a] = rhs[a];
+    done[c] = m;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * cc; e += blockDim.x) {
+    const int i = e / cc, c = e - i * cc;
+    const int j = p.cols[cbeg + c];
+    const int m = done[c];
+    double x = 0.0;
+    for (int a = 0; a < m; ++a) x = DADD(x, DMUL(B(a, i, c), ycoef[c][a]));
+    p.w[static_cast<std::size_t>(r0 + i) * p.k + j] = x;
+  }
+}
+
+}  // namespace
+
+int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::uint32_t k,
+                  const ShiftPlan& plan, const cieg_precond_config& cfg, double* w) {
+  const std::size_t bytes = static_cast<std::size_t>(prec->dim) * k * sizeof(double);
+  if (w != r && bytes) CIEG_CUDA(cudaMemcpyAsync(w, r, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
+  std::vector<int> engaged;
+  for (std::uint32_t j = 0; j < k; ++j)
+    if (plan.engage[j]) engaged.push_back(static_cast<int>(j));
+  if (engaged.empty() || prec->ngroups == 0) return 0;
+  if (engaged.size() > static_cast<std::size_t>(kMaxCols)) fail(CIEG_ERR_CONFIG, "preconditioner: more than 64 columns");
+  if (cfg.inner_iters < 1) fail(CIEG_ERR_CONFIG, "fom_solve: iters must be >= 1");
+
+  std::vector<std::uint32_t> small, large;
+  for (std::uint32_t g = 0; g < prec->ngroups; ++g) {
+    const std::uint32_t sz = prec->bounds_host[g + 1] - prec->bounds_host[g];
+    if (sz == 0) continue;
+    (static_cast<int>(sz) <= cfg.small_block_cutoff ? small : large).push_back(g);
+  }
+  std::uint32_t* dgroups = static_cast<std::uint32_t*>(
+      ctx->scratch_red.get(sizeof(std::uint32_t) * (small.size() + large.size() + 64) + 256));
+  int* dcount = reinterpret_cast<int*>(dgroups + small.size() + large.size() + 32);
+  CIEG_CUDA(cudaMemsetAsync(dcount, 0, sizeof(int), ctx->stream));
+  if (!small.empty())
+    CIEG_CUDA(cudaMemcpyAsync(dgroups, small.data(), sizeof(std::uint32_t) * small.size(),
+                              cudaMemcpyHostToDevice, ctx->stream));
+  if (!large.empty())
+    CIEG_CUDA(cudaMemcpyAsync(dgroups + small.size(), large.data(), sizeof(std::uint32_t) * large.size(),
+                              cudaMemcpyHostToDevice, ctx->stream));
+
+  if (!small.empty()) {
+    if (cfg.small_block_cutoff > kMaxDirect && prec->max_group > static_cast<std::uint32_t>(kMaxDirect))
+      fail(CIEG_ERR_CONFIG, "direct tile solve supports groups up to 64 rows");
+    static thread_local LuParams lp;
+    lp.bounds = prec->bounds;
+    lp.block_off = prec->block_off;
+    lp.blocks = prec->blocks;
+    lp.groups = dgroups;
+    lp.r = r;
+    lp.w = w;
+    lp.k = k;
+    lp.singular_count = dcount;
+    std::map<double, std::vector<int>> by_shift;  // ascending, like the reference's std::map
+    for (int j : engaged) by_shift[plan.mu[j]].push_back(j);
+    lp.nshift = static_cast<int>(by_shift.size());
+    int s = 0, o = 0;
+    for (auto& [mu, cols] : by_shift) {
+      lp.shift[s] = mu;
+      lp.col_start[s] = o;
+      for (int j : cols) lp.cols[o++] = j;
+      ++s;
+    }
+    lp.col_start[s] = o;
+    int maxcols = 0;
+    for (int t = 0; t < lp.nshift; ++t) maxcols = std::max(maxcols, lp.col_start[t + 1] - lp.col_start[t]);
+    const std::size_t smem = sizeof(double) * static_cast<std::size_t>(maxcols) * kMaxDirect;
+    CIEG_CUDA(cudaFuncSetAttribute(lu_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    dim3 grid(static_cast<unsigned>(small.size()), static_cast<unsigned>(lp.nshift));
+    lu_direct_kernel<<<grid, kLuThreads, smem, ctx->stream>>>(lp);
+    CIEG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  if (!large.empty()) {
+    static thread_local FomParams fp;
+    fp.bounds = prec->bounds;
+    fp.block_off = prec->block_off;
+    fp.blocks = prec->blocks;
+    fp.groups = dgroups + small.size();
+    fp.r = r;
+    fp.w = w;
+    fp.k = k;
+    fp.ncols = static_cast<int>(engaged.size());
+    fp.iters = cfg.inner_iters;
+    for (std::size_t c = 0; c < engaged.size(); ++c) {
+      fp.cols[c] = engaged[c];
+      fp.mu[c] = plan.mu[engaged[c]];
+    }
+    const int mmax = std::min<int>(cfg.inner_iters, static_cast<int>(prec->max_group));
+    if (mmax > kFomMaxSteps) fail(CIEG_ERR_CONFIG, "fom_solve: inner_iters above 3 is not supported");
+    // chunk so that shared memory stays below ~200 KB
+    const std::size_t n = prec->max_group;
+    int chunk = 16;
+    auto smem_for = [&](int cc) {
+      return sizeof(double) * ((mmax + 1) * n * cc + n * cc + cc * 16 + 2 * cc) + sizeof(int) * 3 * cc;
+    };
+    while (chunk > 1 && smem_for(chunk) > 200 * 1024) chunk /= 2;
+    if (smem_for(chunk) > 220 * 1024) fail(CIEG_ERR_CONFIG, "FOM tile too large for shared memory");
+    fp.chunk = chunk;
+    const std::size_t smem = smem_for(chunk);
+    CIEG_CUDA(cudaFuncSetAttribute(fom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
+    fom_kernel<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+    CIEG_CUDA(cudaGetLastError());
+    ++ctx->launches;
+  }
+  int* pin = static_cast<int*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
+  CIEG_CUDA(cudaMemcpyAsync(pin, dcount, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  const int singular = pin[0];
+  for (int i = 0; i < singular; ++i)
+    std::fprintf(stderr, "ci-eigen: singular shifted tile block; passing residual through\n");
+  return singular;
+}
+
+}  // namespace cieg
+
+namespace {
+
+cieg_prec* make_prec(cieg_ctx* ctx, std::uint32_t dim, std::uint32_t ng, const std::uint32_t* bounds,
+                     const double* blocks_host) {
+  if (ng > 0 && (bounds[0] != 0 || bounds[ng] != dim))
+    cieg::fail(CIEG_ERR_DIMENSION, "apply_preconditioner: tiles do not cover the basis");
+  auto* p = new cieg_prec;
+  try {
+    p->ctx = ctx;
+    p->dim = dim;
+    p->ngroups = ng;
+    p->bounds_host.assign(bounds, bounds + ng + 1);
+    p->block_off_host.resize(ng + 1, 0);
+    for (std::uint32_t g = 0; g < ng; ++g) {
+      const std::uint64_t sz = bounds[g + 1] - bounds[g];
+      p->max_group = std::max<std::uint32_t>(p->max_group, static_cast<std::uint32_t>(sz));
+      p->block_off_host[g + 1] = p->block_off_host[g] + sz * sz;
+    }
+    CIEG_CUDA(cudaMalloc(&p->bounds, sizeof(std::uint32_t) * (ng + 1)));
+    CIEG_CUDA(cudaMemcpy(p->bounds, bounds, sizeof(std::uint32_t) * (ng + 1), cudaMemcpyHostToDevice));
+    CIEG_CUDA(cudaMalloc(&p->block_off, sizeof(std::uint64_t) * (ng + 1)));
+    CIEG_CUDA(cudaMemcpy(p->block_off, p->block_off_host.data(), sizeof(std::uint64_t) * (ng + 1),
+                         cudaMemcpyHostToDevice));
+    const std::uint64_t total = p->block_off_host[ng];
+    CIEG_CUDA(cudaMalloc(&p->blocks, sizeof(double) * std::max<std::uint64_t>(total, 1)));
+    if (total)
+      CIEG_CUDA(cudaMemcpy(p->blocks, blocks_host, sizeof(double) * total, cudaMemcpyHostToDevice));
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  return p;
+}
+
+}  // namespace
+
+extern "C" {
+
+void cieg_precond_config_default(cieg_precond_config* c) {
+  if (!c) return;
+  c->inner_iters = 3;
+  c->small_block_cutoff = 64;
+  c->engage_after = 3;
+  c->relres_gate = 1e-1;
+  c->near_converged_factor = 10.0;
+  c->far_threshold = 1e-2;
+  c->column_floor_factor = 100.0;
+}
+
+int cieg_precond_upload(cieg_ctx* ctx, const cieg_tilediag_view* t, cieg_prec** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !t || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_precond_upload: null argument");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    *out = make_prec(ctx, t->dim, t->ngroups, t->bounds, t->blocks);
+  });
+}
+
+// ci::extract_tile_diagonal (hamiltonian.cpp:178-203): dense f64 blocks from
+// the diagonal CSB blocks, mirrored.
+int cieg_precond_from_csb(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* gb, uint32_t ng,
+                          cieg_prec** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !csb || !gb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_precond_from_csb: null argument");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    const std::uint32_t dim = csb->dim;
+    if (gb[0] != 0 || gb[ng] != dim) cieg::fail(CIEG_ERR_DIMENSION, "group bounds do not cover [0, dim)");
+    std::vector<std::uint32_t> group_of(dim);
+    std::vector<std::uint64_t> off(ng + 1, 0);
+    for (std::uint32_t g = 0; g < ng; ++g) {
+      const std::uint64_t sz = gb[g + 1] - gb[g];
+      off[g + 1] = off[g] + sz * sz;
+      for (std::uint32_t r = gb[g]; r < gb[g + 1]; ++r) group_of[r] = g;
+    }
+    std::vector<double> blocks(off[ng], 0.0);
+    const float* v32 = static_cast<const float*>(csb->values);
+    const double* v64 = static_cast<const double*>(csb->values);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (std::int64_t i64 = 0; i64 < static_cast<std::int64_t>(csb->nb); ++i64) {
+      const std::uint32_t i = static_cast<std::uint32_t>(i64);
+      const std::uint64_t bid = static_cast<std::uint64_t>(i) * (i + 1) / 2 + i;
+      const std::uint32_t base = csb->block_boundaries[i];
+      for (std::uint64_t e = csb->entry_offsets[bid]; e < csb->entry_offsets[bid + 1]; ++e) {
+        const std::uint32_t r = base + csb->rows[e], c = base + csb->cols[e];
+        const std::uint32_t g = group_of[r];
+        if (group_of[c] != g) continue;
+        const std::uint32_t s = gb[g];
+        const std::uint64_t n = gb[g + 1] - s;
+        const double v = csb->precision == 0 ? static_cast<double>(v32[e]) : v64[e];
+        blocks[off[g] + (r - s) + (c - s) * n] = v;
+        blocks[off[g] + (c - s) + (r - s) * n] = v;
+      }
+    }
+    *out = make_prec(ctx, dim, ng, gb, blocks.data());
+  });
+}
+
+int cieg_precond_destroy(cieg_prec* p) {
+  if (p) {
+    cudaSetDevice(p->ctx->device);
+    cudaStreamSynchronize(p->ctx->stream);
+    delete p;
+  }
+  return CIEG_OK;
+}
+
+int cieg_choose_shifts(uint32_t k, const double* theta, const double* res_norm, const double* x_norm,
+                       const double* relres, int iteration, double tol, const cieg_precond_config* cfg,
+                       double* mu_out, int* engage_out) {
+  return cieg::guarded([&] {
+    cieg_precond_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      cieg_precond_config_default(&c);
+    auto plan = cieg::choose_shifts(std::vector<double>(theta, theta + k), std::vector<double>(res_norm, res_norm + k),
+                                    std::vector<double>(x_norm, x_norm + k), std::vector<double>(relres, relres + k),
+                                    iteration, tol, c);
+    for (uint32_t j = 0; j < k; ++j) {
+      mu_out[j] = plan.mu[j];
+      engage_out[j] = plan.engage[j];
+    }
+  });
+}
+
+int cieg_precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r_dev, uint32_t k,
+                       const double* mu_host, const int* engage_host, const cieg_precond_config* cfg,
+                       double* w_dev) {
+  return cieg::guarded([&] {
+    if (!ctx || !prec) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_precond_apply: null handle");
+    cieg_precond_config c;
+    if (cfg)
+      c = *cfg;
+    else
+      cieg_precond_config_default(&c);
+    cieg::ShiftPlan plan;
+    plan.mu.assign(mu_host, mu_host + k);
+    plan.engage.assign(engage_host, engage_host + k);
+    cieg::precond_apply(ctx, prec, r_dev, k, plan, c, w_dev);
+  });
+}
+
+}  // extern "C"

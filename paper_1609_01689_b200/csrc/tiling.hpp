@@ -1,0 +1,55 @@
+// tiling.hpp -- host-side re-tiling of a flattened CsbMatrix into the device
+// tile stream used by the SpMM kernels.
+//
+// Device format:
+//   * rows are cut into panels of <= tile_edge rows (panel_start[npanels+1]);
+//     panels follow group boundaries, so a device tile (PI, PJ) is the union
+//     of whole reference tiles and keeps their density;
+//   * one stored tile per nonzero (PI >= PJ) panel pair, entries as a packed
+//     32-bit tile-local index (row | col << 16) plus the value (f32 or f64),
+//     tiles back to back with 64-bit offsets;
+//   * an owner work list per panel P: the tiles whose product lands in P's
+//     rows -- (P, J) row parts, (I, P) transposed parts, (P, P) symmetric --
+//     so one CTA computes all of Y[P] and writes it exactly once
+//     (owner-computes; deterministic, no atomics).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+#include "cieg_internal.hpp"
+
+namespace cieg {
+
+enum WorkKind : std::uint32_t { kRowPart = 0, kTransposed = 1, kDiagonal = 2 };
+
+struct HostTiles {
+  std::uint32_t dim = 0;
+  std::uint32_t tile_edge = 0;
+  int precision = 0;
+  std::uint64_t nnz = 0;
+  std::vector<std::uint32_t> panel_start;      // npanels + 1
+  std::vector<std::uint64_t> tile_off;         // ntiles + 1
+  std::vector<std::uint32_t> tile_pi, tile_pj; // panel pair of each tile
+  std::vector<std::uint32_t> idx;              // packed r | c << 16 (panel-local)
+  std::vector<float> val32;
+  std::vector<double> val64;
+  // owner work lists: items [work_off[P], work_off[P+1]) of (tile, other, kind)
+  std::vector<std::uint32_t> work_off;
+  std::vector<std::uint32_t> work_tile, work_other, work_kind;
+
+  std::uint32_t npanels() const { return static_cast<std::uint32_t>(panel_start.size() - 1); }
+  std::uint64_t ntiles() const { return tile_pi.size(); }
+};
+
+// Panel plan from group bounds: groups larger than tile_edge are split into
+// tile_edge chunks; consecutive groups are merged while the panel stays
+// <= tile_edge and every merged group is smaller than tile_edge / 2 (small
+// physics-style groups), otherwise each group is its own panel.
+std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* group_bounds,
+                                       std::uint32_t ngroups, std::uint32_t tile_edge);
+
+void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& panels,
+                 std::uint32_t tile_edge, HostTiles& out);
+
+}  // namespace cieg
