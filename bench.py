@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""bench.py -- the BASELINE.json headline on B200: fused symmetric SpMM
+H.X + H^T.X GB/s (% of the measured HBM roofline) on config 2 (n = 2e6,
+256-row tiles, fp32 H, fp64 X/Y, m = 16), plus the LOBPCG time-to-solution of
+config 1 as a side record.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one fused SpMM over the whole matrix with X resident in HBM
+(value); e2e = the same SpMM through the C-ABI host call cieg_spmm_host with
+pinned host X/U, H2D + kernel + D2H inside the timed region. H (6.4 GB) and
+X/U (256 MB each) exceed the 126 MB L2, so no flush is needed between steps.
+--impl reference times the UNMODIFIED reference ci::spmm (oracle/_ref,
+OpenMP on all host cores) on the same matrix.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+FP64_PEAK_TFLOPS = 37.0  # measured: tools/microbench/fp64_probe.cu (DFMA and DMMA both 37.0 TF/s)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def load_traffic(workload):
+    """dram bytes per launch from the committed ncu --set full capture."""
+    p = os.path.join(REPO, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 7 and parts[0].replace(".", "").isdigit():
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def gen_matrix(cfg, rank):
+    t = time.time()
+    h = cfg.generate(seed=cfg.seed + rank)
+    return h, time.time() - t
+
+
+def reference_arm(args):
+    """--impl reference: the reference's own ci::spmm on the host cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1609_01689_b200 import configs
+    from oracle import ref
+
+    cfg = configs.CFG2
+    h, _ = gen_matrix(cfg, 0)
+    m = cfg.m
+    cores = ref.max_threads()
+    # Bounded sample: the leading principal submatrix (whole CSB block rows) sized
+    # so that warmup + steps stay within ~90 s of CPU time.
+    probe = _leading_block(h, max(1, h.block_count() // 16))
+    rp = ref.RefMatrix(probe)
+    xp = np.random.default_rng(0).standard_normal((probe.dim, m))
+    rp.spmm(xp)
+    t0 = time.perf_counter()
+    rp.spmm(xp)
+    t_probe = time.perf_counter() - t0
+    rate = probe.nnz_lower / max(t_probe, 1e-9)
+    budget = 90.0 / max(1, args.steps + args.warmup)
+    frac_nnz = min(1.0, budget * rate / h.nnz_lower)
+    nbk = max(1, min(h.block_count(), int(round(h.block_count() * frac_nnz))))
+    sample = h if nbk == h.block_count() else _leading_block(h, nbk)
+    del rp, probe
+    rm = ref.RefMatrix(sample)
+    x = np.random.default_rng(1).standard_normal((sample.dim, m))
+    for _ in range(args.warmup):
+        rm.spmm(x)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        rm.spmm(x)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    nbytes = configs.spmm_bytes(sample.nnz_lower, sample.dim, m, sample.precision)
+    gbs = nbytes / t / 1e9
+    desc = (f"ci::spmm (reference, OpenMP {cores} threads) on the leading {sample.dim} rows "
+            f"({sample.nnz_lower} stored nnz, {100.0 * sample.nnz_lower / h.nnz_lower:.1f}% of config 2), m={m}")
+    line = {
+        "metric": "spmm_gbs", "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (fp32 H promoted)", "data": "synthetic (seeded sector generator)",
+        "config": {"workload": cfg.name, "n": cfg.n, "nnz_stored": h.nnz_lower, "m": m, "tile": cfg.tile,
+                   "p": cfg.p(), "q": cfg.q, "sample_rows": sample.dim},
+        "impl": "reference",
+        "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+                         "sample": desc},
+        "e2e": {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _leading_block(h, nbk):
+    """Leading principal submatrix made of the first nbk CSB block rows."""
+    from paper_1609_01689_b200 import ci
+
+    nblk = nbk * (nbk + 1) // 2
+    e = int(h.entry_offsets[nblk])
+    dim = int(h.block_boundaries[nbk])
+    groups = None
+    if h.groups is not None:
+        groups = h.groups[h.groups <= dim]
+        if groups[-1] != dim:
+            groups = np.append(groups, np.uint32(dim))
+    return ci.CsbMatrix(dim=dim, precision=h.precision, block_boundaries=h.block_boundaries[:nbk + 1].copy(),
+                        entry_offsets=h.entry_offsets[:nblk + 1].copy(), rows=h.rows[:e], cols=h.cols[:e],
+                        values=h.values[:e], groups=groups, beta=h.beta)
+
+
+def cpu_baseline(h, m):
+    """cpu_baseline record: reference ci::spmm on a bounded sample (~10-20 s)."""
+    from paper_1609_01689_b200 import configs
+    from oracle import ref
+
+    if not ref.available():
+        return None
+    cores = ref.max_threads()
+    nbk = max(1, h.block_count() // 4)
+    sample = _leading_block(h, nbk)
+    rm = ref.RefMatrix(sample)
+    x = np.random.default_rng(2).standard_normal((sample.dim, m))
+    rm.spmm(x)
+    ts = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        rm.spmm(x)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    gbs = configs.spmm_bytes(sample.nnz_lower, sample.dim, m, sample.precision) / t / 1e9
+    return {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+            "sample": f"ci::spmm x3 on the leading {sample.dim} rows ({sample.nnz_lower} nnz) of config 2, m={m}"}
+
+
+def lobpcg_record():
+    """Config-1 LOBPCG time-to-solution (GPU) with the reference's iteration count."""
+    from paper_1609_01689_b200 import ci, configs
+
+    cfg = configs.CFG1
+    h = cfg.generate()
+    td = ci.extract_tile_diagonal(h)
+    x0 = ci.random_block(h.dim, cfg.kt, 42)
+    opt = ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol, preconditioner=td)
+    ci.lobpcg_solve(h, x0, opt)  # warm
+    t0 = time.perf_counter()
+    rep = ci.lobpcg_solve(h, x0, opt)
+    ms = (time.perf_counter() - t0) * 1e3
+    out = {"workload": cfg.name, "iterations": rep.iterations, "converged": rep.converged, "ms": round(ms, 2),
+           "split_ms": {k: round(v, 2) for k, v in rep.timing_ms.items()},
+           "eigenvalues": [float(v) for v in rep.eigenvalues]}
+    try:
+        from oracle import ref
+
+        if ref.available():
+            rm = ref.RefMatrix(h)
+            rtd = ref.RefTileDiagonal(rm, h.groups)
+            t0 = time.perf_counter()
+            rr = ref.lobpcg_solve(rm, x0, cfg.k_want, cfg.tol, 500, rtd)
+            out["reference"] = {"iterations": rr.iterations, "ms": round((time.perf_counter() - t0) * 1e3, 2),
+                                "cores": ref.max_threads()}
+            out["max_rel_eig_diff"] = float(np.max(np.abs(rep.eigenvalues - rr.eigenvalues) / np.abs(rr.eigenvalues)))
+    except Exception as e:  # the record is informative only
+        out["reference_error"] = str(e)
+    return out
+
+
+def ours(args):
+    import torch
+
+    from paper_1609_01689_b200 import ci, configs
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    cfg = configs.CFG2
+    m = args.m or cfg.m
+    h, t_gen = gen_matrix(cfg, rank)
+    dev = ci.Device(local)
+    t0 = time.time()
+    dm = ci.DeviceMatrix(h, dev)
+    t_up = time.time() - t0
+    n = h.dim
+    stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", local))
+    x = torch.from_numpy(ci.random_block(n, m, 5)).cuda()
+    y = torch.empty_like(x)
+    torch.cuda.synchronize()
+
+    def step():
+        dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    dev.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    l0 = dev.launches
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        ev1.synchronize()
+    dev.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    launches = dev.launches - l0
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nbytes = configs.spmm_bytes(h.nnz_lower, n, m, h.precision)
+    flops = configs.spmm_flops(h.nnz_lower, n, m)
+    gbs = nbytes / (ms * 1e-3) / 1e9
+    total_gbs = gbs * world
+
+    # e2e: the C-ABI host call with pinned host buffers
+    xh = torch.from_numpy(ci.random_block(n, m, 6)).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    xn, yn = xh.numpy(), yh.numpy()
+    for _ in range(max(1, args.warmup)):
+        dm.spmm_host(xn)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    ke = max(3, min(args.steps, 10))
+    import ctypes as C
+
+    from paper_1609_01689_b200 import _lib
+
+    lib = _lib.load()
+    e0.record(stream)
+    for _ in range(ke):
+        rc = lib.cieg_spmm_host(dev.handle, dm.handle, xn.ctypes.data_as(C.POINTER(C.c_double)),
+                                yn.ctypes.data_as(C.POINTER(C.c_double)), m)
+        if rc:
+            raise RuntimeError(lib.cieg_last_error().decode())
+    e1.record(stream)
+    e1.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / ke
+    e2e_gbs = nbytes / (ms_e2e * 1e-3) / 1e9 * world
+
+    peak, peak_kind = load_peaks()
+    if rank != 0:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+        return 0
+    line = {
+        "metric": "spmm_gbs", "value": round(total_gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64 (fp32 H promoted exactly)",
+        "data": "synthetic (seeded sector generator, BASELINE config 2)",
+        "config": {"workload": cfg.name, "n": n, "nnz_stored": h.nnz_lower, "m": m, "tile": cfg.tile,
+                   "p": round(cfg.p(), 8), "q": cfg.q, "device_tile_edge": dm.tile_edge, "device_tiles": dm.ntiles,
+                   "l2": "inputs larger than L2 (H 6.4 GB, X/U 256 MB each); no flush",
+                   "parallelism": "single GPU" if world == 1 else f"replicas x{world} (one shard-sized matrix per rank)",
+                   "gen_s": round(t_gen, 1), "upload_s": round(t_up, 1)},
+        "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peak, "unit": "GB/s",
+                     "frac": round(gbs / peak, 4), "traffic": load_traffic(cfg.name), "peak_kind": peak_kind,
+                     "fp64_tflops": round(flops / (ms * 1e-3) / 1e12, 3), "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                     "fp64_frac": round(flops / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
+                     "bytes_per_launch": nbytes, "flops_per_launch": flops},
+        "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": n * m * 8,
+                "d2h_bytes_per_step": n * m * 8, "ms_per_step": round(ms_e2e, 4),
+                "call": "cieg_spmm_host (pinned host X/U)"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(h, m)
+    if world == 1 and not args.no_lobpcg:
+        line["lobpcg"] = lobpcg_record()
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--m", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-lobpcg", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return reference_arm(args)
+    return ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

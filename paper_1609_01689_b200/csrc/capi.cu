@@ -104,6 +104,7 @@ int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* 
       }
     }
     if (te != 64 && te != 128) cieg::fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
+    if (csb->precision == 1) te = 64;  // fp64 dense tiles: 64 rows keep two buffers in shared memory
     std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te);
     cieg::HostTiles ht;
     cieg::build_tiles(*csb, panels, te, ht);
@@ -129,7 +130,7 @@ int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* 
       m->work_tile = cieg::upload_vec(ht.work_tile);
       m->work_other = cieg::upload_vec(ht.work_other);
       m->work_kind = cieg::upload_vec(ht.work_kind);
-      m->tile_bytes = ht.nnz * (4 + (ht.precision == 0 ? 4 : 8));
+      m->tile_bytes = ht.tile_off.back() * (4 + (ht.precision == 0 ? 4 : 8));
     } catch (...) {
       delete m;
       throw;

@@ -134,13 +134,20 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
       out.tile_pj[t] = rowtiles[P][k].pj;
       out.tile_off[t + 1] = rowtiles[P][k].idx.size();
     }
+  // Each tile's entry list is padded to a multiple of 4 with sentinel entries
+  // (index 0xffffffff, value 0) so the kernels stream it with 128-bit loads.
+  out.nnz = 0;
+  for (std::uint64_t t = 0; t < nt; ++t) {
+    out.nnz += out.tile_off[t + 1];
+    out.tile_off[t + 1] = (out.tile_off[t + 1] + 3) & ~std::uint64_t{3};
+  }
   for (std::uint64_t t = 0; t < nt; ++t) out.tile_off[t + 1] += out.tile_off[t];
-  out.nnz = out.tile_off[nt];
-  out.idx.resize(out.nnz);
+  const std::uint64_t slots = out.tile_off[nt];
+  out.idx.assign(slots, 0xffffffffu);
   if (single)
-    out.val32.resize(out.nnz);
+    out.val32.assign(slots, 0.0f);
   else
-    out.val64.resize(out.nnz);
+    out.val64.assign(slots, 0.0);
 #pragma omp parallel for schedule(dynamic, 8)
   for (std::int64_t p64 = 0; p64 < static_cast<std::int64_t>(np); ++p64) {
     const std::uint32_t P = static_cast<std::uint32_t>(p64);

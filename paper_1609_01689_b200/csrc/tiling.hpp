@@ -27,7 +27,7 @@ struct HostTiles {
   std::uint32_t dim = 0;
   std::uint32_t tile_edge = 0;
   int precision = 0;
-  std::uint64_t nnz = 0;
+  std::uint64_t nnz = 0;  // real entries (tile lists are padded to quads)
   std::vector<std::uint32_t> panel_start;      // npanels + 1
   std::vector<std::uint64_t> tile_off;         // ntiles + 1
   std::vector<std::uint32_t> tile_pi, tile_pj; // panel pair of each tile
