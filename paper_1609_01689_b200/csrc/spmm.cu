@@ -8,14 +8,17 @@
 //     once: no atomics, no zero-fill, bitwise deterministic run to run. Every
 //     off-diagonal tile is therefore streamed twice (once per owner); at
 //     m >= 8 the kernel is FP64-bound, so the extra bytes hide under the math.
-//   * persistent, warp-specialised CTA (one per SM): 4 producer warps clear a
-//     dense shared-memory tile, scatter the next work item's packed
-//     (row | col << 16, value) entries into it -- transposed on the fly for
-//     transposed parts, mirrored for the diagonal tile, so the consumer loop
-//     is uniform -- and stage the partner panel's X slab; 4 consumer warps run
-//     the panel product on the FP64 tensor pipe (DMMA m8n8k4) out of the other
-//     buffer. The two stages hand buffers over with named barriers
-//     (FULL/EMPTY per buffer), so scatter latency hides behind the DMMAs.
+//   * persistent, warp-specialised CTA (one per SM). 8 producer warps stream
+//     the work items' packed entry lists with 128-bit loads into a register
+//     double buffer (the next 4096-entry batch is in flight while the current
+//     one is placed), clear a dense shared-memory tile and scatter the
+//     entries into it with one store each -- the 32-bit index carries the
+//     entry's offset in both orientations (row part / transposed part), the
+//     diagonal tile is mirrored -- and stage the partner panel's X slab,
+//     prefetched one item ahead in registers. 8 consumer warps run the panel
+//     product on the FP64 tensor pipe (DMMA m8n8k4) out of the other tile
+//     buffer. Producer and consumers hand the two buffers over with named
+//     barriers (FULL/EMPTY per buffer).
 //   * fp32 values are promoted to fp64 exactly on fragment load (F2F runs on
 //     its own unit, measured not to slow DMMA); products and sums are fp64,
 //     the reference's precision contract (csb.hpp:79-82).
@@ -44,10 +47,12 @@ struct SpmmArgs {
   std::uint32_t ldx, ldy, mcols, npanels;
 };
 
-constexpr int kProducerWarps = 4;
-constexpr int kConsumerWarps = 4;
+constexpr int kProducerWarps = 8;
+constexpr int kConsumerWarps = 8;
 constexpr int kThreads = 32 * (kProducerWarps + kConsumerWarps);
 constexpr int kProducerThreads = 32 * kProducerWarps;
+constexpr int kQuads = 4;                                  // entry quads per producer thread per batch
+constexpr int kChunkQuads = kQuads * kProducerThreads;     // 1024 quads = 4096 entries per batch
 // named barrier ids (0 is __syncthreads)
 constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProducers = 5;
 
@@ -57,30 +62,15 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
-
 template <typename V, int TD, int NT>
 struct Shape {
-  static constexpr int kSA = TD + 4;              // words (f32) or doubles (f64); S = 4 mod 16
-  static constexpr int kSX = 8 * NT + 4;          // doubles
-  static constexpr int kMT = TD / 8 / kConsumerWarps;  // m-tiles per consumer warp
-  static constexpr std::size_t kTileBytes = sizeof(V) * TD * kSA;
+  static constexpr int kSA = TD + 4;                    // row stride (elements), 4 mod 16
+  static constexpr int kSX = 8 * NT + 4;                // doubles
+  static constexpr int kMT = TD / 8 / kConsumerWarps;   // m-tiles per consumer warp
+  static constexpr std::size_t kTileBytes = ((sizeof(V) * TD * kSA + 15) / 16) * 16;
   static constexpr std::size_t kSlabBytes = sizeof(double) * TD * kSX;
   static constexpr std::size_t kSmem = 2 * (kTileBytes + kSlabBytes);
-};
-
-constexpr int kQuads = 4;  // entry quads per producer thread per batch
-
-template <typename V>
-struct Quad;
-template <>
-struct Quad<float> {
-  uint4 id;
-  float4 v;
-};
-template <>
-struct Quad<double> {
-  uint4 id;
-  double2 v0, v1;
+  static constexpr int kSlabPer = TD * 8 * NT / kProducerThreads;  // slab doubles per producer thread
 };
 
 struct Item {
@@ -99,6 +89,88 @@ __device__ __forceinline__ void fetch_item(const SpmmArgs& a, std::uint32_t w, I
   it.q1 = __ldg(a.tile_off + tile + 1) >> 2;
 }
 
+// Walks the CTA's (panel, item, chunk) sequence.
+struct Cursor {
+  std::uint32_t P, w;
+  Item it;
+  std::uint64_t q;  // first quad of the current chunk
+  bool valid;
+
+  __device__ __forceinline__ bool seek_panel(const SpmmArgs& a) {
+    while (w >= a.work_off[P + 1]) {
+      P += gridDim.x;
+      if (P >= a.npanels) return false;
+      w = a.work_off[P];
+    }
+    return true;
+  }
+  __device__ __forceinline__ void init(const SpmmArgs& a) {
+    P = blockIdx.x;
+    valid = P < a.npanels;
+    if (!valid) return;
+    w = a.work_off[P];
+    valid = seek_panel(a);
+    if (valid) {
+      fetch_item(a, w, it);
+      q = it.q0;
+    }
+  }
+  // next item after the current one (for slab prefetch); false at the end
+  __device__ __forceinline__ bool peek_next(const SpmmArgs& a, Item& nit) const {
+    Cursor c = *this;
+    ++c.w;
+    if (!c.seek_panel(a)) return false;
+    fetch_item(a, c.w, nit);
+    return true;
+  }
+  __device__ __forceinline__ void next_chunk(const SpmmArgs& a) {
+    q += kChunkQuads;
+    if (q < it.q1) return;
+    ++w;
+    valid = seek_panel(a);
+    if (valid) {
+      fetch_item(a, w, it);
+      q = it.q0;
+    }
+  }
+};
+
+template <typename V, int TD, int NT>
+__device__ __forceinline__ void load_slab(const SpmmArgs& a, const Item& it, int pt,
+                                          double (&xv)[Shape<V, TD, NT>::kSlabPer]) {
+#pragma unroll
+  for (int j = 0; j < Shape<V, TD, NT>::kSlabPer; ++j) {
+    const int e = pt + j * kProducerThreads;
+    const int k = e / (8 * NT), t = e - k * (8 * NT);
+    xv[j] = (k < it.orow && t < static_cast<int>(a.mcols)) ? __ldg(a.x + static_cast<std::size_t>(it.o0 + k) * a.ldx + t)
+                                                            : 0.0;
+  }
+}
+
+template <int KIND, typename V>
+__device__ __forceinline__ void put(V* A, std::uint32_t id, V v) {
+  if (KIND == 1) {
+    A[id >> 16] = v;
+  } else {
+    A[id & 0xffffu] = v;
+    if (KIND == 2) A[id >> 16] = v;
+  }
+}
+
+template <typename V>
+struct Quad;
+template <>
+struct Quad<float> {
+  uint4 id;
+  float4 v;
+};
+template <>
+struct Quad<double> {
+  uint4 id;
+  double2 v0, v1;
+};
+constexpr std::uint32_t kNoQuad = 0xffffffffu;  // marks an empty batch slot (never a real index)
+
 __device__ __forceinline__ void load_quad(const SpmmArgs& a, const float* val, std::uint64_t q, Quad<float>& o) {
   o.id = __ldg(reinterpret_cast<const uint4*>(a.idx) + q);
   o.v = __ldg(reinterpret_cast<const float4*>(val) + q);
@@ -109,61 +181,19 @@ __device__ __forceinline__ void load_quad(const SpmmArgs& a, const double* val, 
   o.v1 = __ldg(reinterpret_cast<const double2*>(val) + 2 * q + 1);
 }
 
-template <typename V>
-__device__ __forceinline__ void load_batch(const SpmmArgs& a, const V* val, const Item& it, std::uint64_t qb, int pt,
-                                           Quad<V> (&out)[kQuads]) {
-#pragma unroll
-  for (int j = 0; j < kQuads; ++j) {
-    const std::uint64_t q = qb + pt + j * kProducerThreads;
-    if (q < it.q1)
-      load_quad(a, val, q, out[j]);
-    else
-      out[j].id = make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu);
-  }
+template <int KIND>
+__device__ __forceinline__ void put4(float* A, const Quad<float>& b) {
+  put<KIND>(A, b.id.x, b.v.x);
+  put<KIND>(A, b.id.y, b.v.y);
+  put<KIND>(A, b.id.z, b.v.z);
+  put<KIND>(A, b.id.w, b.v.w);
 }
-
-template <int TD, int NT, int kPer>
-__device__ __forceinline__ void load_slab(const SpmmArgs& a, const Item& it, int pt, double (&xv)[kPer]) {
-#pragma unroll
-  for (int j = 0; j < kPer; ++j) {
-    const int e = pt + j * kProducerThreads;
-    const int k = e / (8 * NT), t = e - k * (8 * NT);
-    xv[j] = (k < it.orow && t < static_cast<int>(a.mcols)) ? __ldg(a.x + static_cast<std::size_t>(it.o0 + k) * a.ldx + t)
-                                                            : 0.0;
-  }
-}
-
-template <typename V, int SA>
-__device__ __forceinline__ void put(V* A, std::uint32_t kind, std::uint32_t id, V v) {
-  if (id == 0xffffffffu) return;
-  const std::uint32_t r = id & 0xffffu, c = id >> 16;
-  if (kind == 1u) {
-    A[c * SA + r] = v;
-  } else {
-    A[r * SA + c] = v;
-    if (kind == 2u) A[c * SA + r] = v;
-  }
-}
-
-template <typename V, int SA>
-__device__ __forceinline__ void scatter(V* A, std::uint32_t kind, const Quad<float> (&b)[kQuads]) {
-#pragma unroll
-  for (int j = 0; j < kQuads; ++j) {
-    put<float, SA>(A, kind, b[j].id.x, b[j].v.x);
-    put<float, SA>(A, kind, b[j].id.y, b[j].v.y);
-    put<float, SA>(A, kind, b[j].id.z, b[j].v.z);
-    put<float, SA>(A, kind, b[j].id.w, b[j].v.w);
-  }
-}
-template <typename V, int SA>
-__device__ __forceinline__ void scatter(V* A, std::uint32_t kind, const Quad<double> (&b)[kQuads]) {
-#pragma unroll
-  for (int j = 0; j < kQuads; ++j) {
-    put<double, SA>(A, kind, b[j].id.x, b[j].v0.x);
-    put<double, SA>(A, kind, b[j].id.y, b[j].v0.y);
-    put<double, SA>(A, kind, b[j].id.z, b[j].v1.x);
-    put<double, SA>(A, kind, b[j].id.w, b[j].v1.y);
-  }
+template <int KIND>
+__device__ __forceinline__ void put4(double* A, const Quad<double>& b) {
+  put<KIND>(A, b.id.x, b.v0.x);
+  put<KIND>(A, b.id.y, b.v0.y);
+  put<KIND>(A, b.id.z, b.v1.x);
+  put<KIND>(A, b.id.w, b.v1.y);
 }
 
 template <typename V, int TD, int NT>
@@ -174,7 +204,6 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
   auto slab_buf = [&](int b) { return reinterpret_cast<double*>(smem + 2 * S::kTileBytes + b * S::kSlabBytes); };
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const V* val = static_cast<const V*>(a.val);
 
   // Total work items of this CTA (to balance the EMPTY barrier arrivals).
   std::uint32_t total = 0;
@@ -182,37 +211,31 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 
   if (warp < kProducerWarps) {
     // ------------------------------------------------------------ producer
-    // Software-pipelined: the next batch of entry quads (or the first batch
-    // of the next work item plus its X slab) is in flight while the current
-    // batch is scattered.
-    const int pt = tid;  // 0 .. 127
-    constexpr int kSlabElems = TD * 8 * NT;
-    constexpr int kPer = kSlabElems / kProducerThreads;
-    std::uint32_t P = blockIdx.x;
-    if (P >= a.npanels) return;
-    std::uint32_t w = a.work_off[P];
-    while (w >= a.work_off[P + 1]) {
-      P += gridDim.x;
-      if (P >= a.npanels) return;
-      w = a.work_off[P];
-    }
-    auto advance = [&]() -> bool {
-      ++w;
-      while (w >= a.work_off[P + 1]) {
-        P += gridDim.x;
-        if (P >= a.npanels) return false;
-        w = a.work_off[P];
-      }
-      return true;
-    };
-    Item it, nit;
-    fetch_item(a, w, it);
+    // Register double buffer: the next batch of entry quads (possibly the
+    // first batch of the next work item) is in flight while the current one
+    // is scattered; the next item's X slab is prefetched a whole item ahead.
+    const int pt = tid;  // 0 .. 255
+    Cursor issue, use;
+    issue.init(a);
+    if (!issue.valid) return;
+    use = issue;
     Quad<V> cur[kQuads], nxt[kQuads];
-    load_batch(a, val, it, it.q0, pt, cur);
-    double xv[kPer];
-    load_slab<TD, NT, kPer>(a, it, pt, xv);
+    auto load_batch = [&](Quad<V>(&out)[kQuads]) {
+#pragma unroll
+      for (int j = 0; j < kQuads; ++j) {
+        const std::uint64_t q = issue.q + pt + static_cast<std::uint64_t>(j) * kProducerThreads;
+        if (issue.valid && q < issue.it.q1)
+          load_quad(a, static_cast<const V*>(a.val), q, out[j]);
+        else
+          out[j].id.x = kNoQuad;
+      }
+      if (issue.valid) issue.next_chunk(a);
+    };
+    load_batch(cur);
+    double xv[S::kSlabPer];
+    load_slab<V, TD, NT>(a, use.it, pt, xv);
     int buf = 0;
-    for (;;) {
+    while (use.valid) {
       bar_sync(kBarEmpty0 + buf, kThreads);
       V* A = tile_buf(buf);
       {
@@ -223,35 +246,37 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       }
       double* X = slab_buf(buf);
 #pragma unroll
-      for (int j = 0; j < kPer; ++j) {
+      for (int j = 0; j < S::kSlabPer; ++j) {
         const int e = pt + j * kProducerThreads;
         const int k = e / (8 * NT), t = e - k * (8 * NT);
         X[k * S::kSX + t] = xv[j];
       }
+      {
+        Item nit;
+        if (use.peek_next(a, nit)) load_slab<V, TD, NT>(a, nit, pt, xv);
+      }
       bar_sync(kBarProducers, kProducerThreads);  // clear before scatter
-      bool next_exists = false;
-      for (std::uint64_t qb = it.q0;; qb += kQuads * kProducerThreads) {
-        const std::uint64_t qn = qb + kQuads * kProducerThreads;
-        const bool more = qn < it.q1;
-        if (more) {
-          load_batch(a, val, it, qn, pt, nxt);
-        } else {
-          next_exists = advance();
-          if (next_exists) {
-            fetch_item(a, w, nit);
-            load_batch(a, val, nit, nit.q0, pt, nxt);
-          }
+      const std::uint32_t kind = use.it.kind;
+      for (;;) {
+        load_batch(nxt);
+#pragma unroll
+        for (int j = 0; j < kQuads; ++j) {
+          if (cur[j].id.x == kNoQuad) continue;
+          if (kind == 0u)
+            put4<0>(A, cur[j]);
+          else if (kind == 1u)
+            put4<1>(A, cur[j]);
+          else
+            put4<2>(A, cur[j]);
         }
-        scatter<V, S::kSA>(A, it.kind, cur);
 #pragma unroll
         for (int j = 0; j < kQuads; ++j) cur[j] = nxt[j];
-        if (!more) break;
+        const std::uint32_t w_before = use.w, p_before = use.P;
+        use.next_chunk(a);
+        if (!use.valid || use.w != w_before || use.P != p_before) break;
       }
       bar_arrive(kBarFull0 + buf, kThreads);
       buf ^= 1;
-      if (!next_exists) break;
-      it = nit;
-      load_slab<TD, NT, kPer>(a, it, pt, xv);
     }
   } else {
     // ------------------------------------------------------------ consumer
@@ -272,24 +297,29 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
       const bool live = m_base < prow;
       for (std::uint32_t w = a.work_off[P]; w < a.work_off[P + 1]; ++w) {
-        const std::uint32_t other = __ldg(a.work_other + w);
-        const int orow = static_cast<int>(__ldg(a.panel_start + other + 1) - __ldg(a.panel_start + other));
         bar_sync(kBarFull0 + buf, kThreads);
         if (live) {
+          // Rows >= orow of the slab and of the tile are zero: all TD/4
+          // k-steps run. Groups of 4 k-steps load every fragment into its own
+          // register before the group's DMMAs issue.
           const V* A = tile_buf(buf) + (m_base + g) * S::kSA + q;
           const double* xb = slab_buf(buf) + q * S::kSX + g;
-          const int ksteps = (orow + 3) >> 2;
-#pragma unroll 2
-          for (int ks = 0; ks < ksteps; ++ks) {
-            double af[S::kMT];
+#pragma unroll 1
+          for (int k0 = 0; k0 < TD / 4; k0 += 4) {
+            double af[4][S::kMT], bf[4][NT];
 #pragma unroll
-            for (int j = 0; j < S::kMT; ++j) af[j] = static_cast<double>(A[j * 8 * S::kSA + 4 * ks]);
+            for (int u = 0; u < 4; ++u) {
 #pragma unroll
-            for (int n = 0; n < NT; ++n) {
-              const double b = xb[4 * ks * S::kSX + 8 * n];
+              for (int j = 0; j < S::kMT; ++j) af[u][j] = static_cast<double>(A[j * 8 * S::kSA + 4 * (k0 + u)]);
 #pragma unroll
-              for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], af[j], b);
+              for (int n = 0; n < NT; ++n) bf[u][n] = xb[4 * (k0 + u) * S::kSX + 8 * n];
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+              for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], af[u][j], bf[u][n]);
           }
         }
         ++done;
@@ -321,12 +351,14 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 template <typename V, int TD, int NT>
 void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   using S = Shape<V, TD, NT>;
+  static_assert(S::kSmem <= 227 * 1024, "shared memory budget");
   auto kern = spmm_ws_kernel<V, TD, NT>;
   CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::kSmem)));
   int per_sm = 0;
   CIEG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, S::kSmem));
   per_sm = std::max(1, per_sm);
-  const unsigned grid = static_cast<unsigned>(std::min<std::uint64_t>(m->npanels, static_cast<std::uint64_t>(per_sm) * ctx->sm_count));
+  const unsigned grid =
+      static_cast<unsigned>(std::min<std::uint64_t>(m->npanels, static_cast<std::uint64_t>(per_sm) * ctx->sm_count));
   kern<<<grid, kThreads, S::kSmem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;

@@ -45,6 +45,8 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
     if (panels[p + 1] <= panels[p] || panels[p + 1] - panels[p] > te)
       fail(CIEG_ERR_CONFIG, "panel plan violates the tile edge");
 
+  const std::uint32_t sa = te + 4;
+  const std::uint32_t sentinel = te | (te << 16);  // row 0, pad column te: never read
   std::vector<std::uint32_t> panel_of(dim);
   for (std::uint32_t p = 0; p < np; ++p)
     for (std::uint32_t r = panels[p]; r < panels[p + 1]; ++r) panel_of[r] = p;
@@ -108,7 +110,10 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
             }
           }
           const std::uint32_t rl = a - r0, cl = b - panels[pj];
-          tb->idx.push_back(rl | (cl << 16));
+          // Packed tile-local index: the entry's shared-memory offset in the
+          // row-part orientation (r * SA + c) and in the transposed one
+          // (c * SA + r), SA = tile_edge + 4 (the kernels' padded row stride).
+          tb->idx.push_back((rl * sa + cl) | ((cl * sa + rl) << 16));
           tb->v.push_back(single ? static_cast<double>(v32[e]) : v64[e]);
         }
       }
@@ -135,7 +140,9 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
       out.tile_off[t + 1] = rowtiles[P][k].idx.size();
     }
   // Each tile's entry list is padded to a multiple of 4 with sentinel entries
-  // (index 0xffffffff, value 0) so the kernels stream it with 128-bit loads.
+  // (value 0, offset = pad column te of row 0, which the consumers never
+  // read) so the kernels stream it with 128-bit copies and scatter without
+  // branches.
   out.nnz = 0;
   for (std::uint64_t t = 0; t < nt; ++t) {
     out.nnz += out.tile_off[t + 1];
@@ -143,7 +150,7 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
   }
   for (std::uint64_t t = 0; t < nt; ++t) out.tile_off[t + 1] += out.tile_off[t];
   const std::uint64_t slots = out.tile_off[nt];
-  out.idx.assign(slots, 0xffffffffu);
+  out.idx.assign(slots, sentinel);
   if (single)
     out.val32.assign(slots, 0.0f);
   else
