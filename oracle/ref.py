@@ -69,6 +69,32 @@ class RefMatrix:
         _chk(load().ciref_spmm(self.handle, _p(x), C.c_uint32(x.shape[1]), _p(y), C.c_int(1 if serial else 0)))
         return y
 
+    @classmethod
+    def load(cls, path):
+        """ci::load_csb of a CSB1 file (handle only; h-less)."""
+        lib = load()
+        out = C.c_void_p()
+        _chk(lib.ciref_matrix_load(str(path).encode(), C.byref(out)))
+        obj = cls.__new__(cls)
+        obj.h = None
+        obj.handle = out
+        obj._fin = weakref.finalize(obj, lib.ciref_matrix_destroy, out)
+        return obj
+
+    def save(self, path):
+        _chk(load().ciref_matrix_save(self.handle, str(path).encode()))
+
+    def summary(self):
+        d, z, nb, p = C.c_uint32(), C.c_uint64(), C.c_uint32(), C.c_int()
+        load().ciref_matrix_summary(self.handle, C.byref(d), C.byref(z), C.byref(nb), C.byref(p))
+        return d.value, z.value, nb.value, p.value
+
+    def spmm_dim(self, x, serial=True):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        y = np.empty_like(x)
+        _chk(load().ciref_spmm(self.handle, _p(x), C.c_uint32(x.shape[1]), _p(y), C.c_int(1 if serial else 0)))
+        return y
+
     def to_dense(self):
         d = np.empty((self.h.dim, self.h.dim), order="F")
         _chk(load().ciref_to_dense(self.handle, d.ctypes.data_as(C.POINTER(C.c_double))))

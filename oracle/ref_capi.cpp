@@ -111,6 +111,21 @@ int ciref_matrix_create(std::uint32_t dim, std::uint32_t nb, int precision,
 
 void ciref_matrix_destroy(void* h) { delete static_cast<ci::CsbMatrix*>(h); }
 
+// ci::load_csb (csb.cpp:295-331) / ci::save_csb (csb.cpp:256-293).
+int ciref_matrix_load(const char* path, void** out) {
+  return guard([&] { *out = new ci::CsbMatrix(ci::load_csb(path)); });
+}
+int ciref_matrix_save(void* h, const char* path) {
+  return guard([&] { ci::save_csb(*static_cast<ci::CsbMatrix*>(h), path); });
+}
+void ciref_matrix_summary(void* h, std::uint32_t* dim, std::uint64_t* nnz, std::uint32_t* nb, int* precision) {
+  const ci::CsbMatrix& m = *static_cast<ci::CsbMatrix*>(h);
+  *dim = m.dim;
+  *nnz = m.nnz_lower;
+  *nb = m.block_count();
+  *precision = m.precision == ci::Precision::Single ? 0 : 1;
+}
+
 int ciref_spmm(void* h, const double* x, std::uint32_t m, double* y, int serial) {
   return guard([&] {
     const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);

@@ -1,0 +1,113 @@
+"""CPU suite for the drop-in boundary: libcieg.so loads, exports every entry
+point declared in include/cieg.h, host-only entry points behave like the
+reference, and device entry points fail loudly (no CPU fallback) when no GPU
+is present. CSB1 interchange with the reference's own reader/writer."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+from paper_1609_01689_b200 import _lib, ci
+
+
+def header_symbols():
+    txt = open(os.path.join(ROOT, "include", "cieg.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(cieg_[a-z0-9_]+)\s*\(", txt)) - {"cieg_observer_fn"})
+
+
+def test_header_declares_entry_points():
+    syms = header_symbols()
+    assert "cieg_spmm" in syms and "cieg_lobpcg_solve" in syms and len(syms) >= 35
+
+
+def test_library_exports_every_header_symbol():
+    lib = ctypes.CDLL(str(_lib.LIB_PATH))
+    missing = [s for s in header_symbols() if not hasattr(lib, s)]
+    assert not missing, missing
+    # and the ctypes signature table covers the same set
+    assert set(header_symbols()) == set(_lib.SIGNATURES)
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_lib.LIB_PATH} 2>/dev/null").read()
+    assert "sm_100a" in out and "sm_90" not in out
+
+
+def test_version_and_errors_on_null_handles():
+    lib = _lib.load()
+    assert b"sm_100a" in lib.cieg_version()
+    rc = lib.cieg_spmm(None, None, None, None, 4)
+    assert rc == 7 and b"null handle" in lib.cieg_last_error()
+
+
+def test_device_calls_fail_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(ci.CudaError):
+        ci.Device(0)
+    h = ci.generate_sector_matrix(500, 1, 64, 0.5, 0.5, precision=1, beta=500)
+    with pytest.raises(ci.CudaError):
+        ci.spmm(h, np.zeros((500, 2)))
+
+
+def test_choose_shifts_matches_reference_library(ref_lib):
+    rng = np.random.default_rng(5)
+    for _ in range(50):
+        k = int(rng.integers(1, 16))
+        theta = np.sort(rng.normal(0, 4, k))
+        relres = 10.0 ** rng.uniform(-10, 0, k)
+        rn = relres * rng.uniform(1, 20)
+        it = int(rng.integers(1, 9))
+        tol = 10.0 ** rng.uniform(-9, -5)
+        cfg = ci.PrecondConfig(engage_after=int(rng.integers(0, 5)), far_threshold=10.0 ** rng.uniform(-3, -1))
+        mu, en = ref_lib.choose_shifts(theta, rn, np.ones(k), relres, it, tol, cfg)
+        plan = ci.choose_shifts(theta, rn, np.ones(k), relres, it, tol, cfg)
+        assert np.array_equal(plan.mu, mu) and np.array_equal(plan.engage, en)
+
+
+def test_csb1_roundtrip_with_reference_reader(tmp_path, ref_lib):
+    """Our CSB1 writer is readable by ci::load_csb and vice versa
+    (csb.cpp:256-331); the round trip is lossless."""
+    h = ci.generate_sector_matrix(2500, 2, 64, 0.2, 0.5, seed=3, precision=0, beta=700)
+    p = tmp_path / "h.csb"
+    ci.save_csb(h, str(p))
+    rm = ref_lib.RefMatrix.load(p)
+    assert rm.summary() == (h.dim, h.nnz_lower, h.block_count(), 0)
+    x = ci.random_block(h.dim, 3, 8)
+    assert np.array_equal(rm.spmm_dim(x), ref_lib.RefMatrix(h).spmm(x, serial=True))
+    p2 = tmp_path / "h2.csb"
+    rm.save(p2)
+    h2 = ci.load_csb(str(p2))
+    for f in ("block_boundaries", "entry_offsets", "rows", "cols", "values"):
+        assert np.array_equal(getattr(h, f), getattr(h2, f)), f
+
+
+def test_csb1_rejects_malformed(tmp_path):
+    p = tmp_path / "bad.csb"
+    p.write_bytes(b"NOPE" + b"\0" * 40)
+    with pytest.raises(ci.FormatError):
+        ci.load_csb(str(p))
+    h = ci.generate_sector_matrix(300, 1, 64, 0.5, 0.5, precision=1, beta=300)
+    ci.save_csb(h, str(p))
+    data = p.read_bytes()
+    p.write_bytes(data[:-5])
+    with pytest.raises(ci.FormatError):
+        ci.load_csb(str(p))
+
+
+def test_write_history_csv_schema():
+    import io
+
+    rep = ci.SolveReport(eigenvalues=np.zeros(1), eigenvectors=np.zeros((1, 1)), trial_vectors=np.zeros((1, 1)),
+                         history=[ci.HistoryRow(0, 0, 0.1, -1.25), ci.HistoryRow(1, 0, 1e-9, -1.5)],
+                         counters=ci.OperationCounters(), converged=True, iterations=1, norm_estimate=1.5,
+                         timing_ms={})
+    s = io.StringIO()
+    ci.write_history_csv(rep, s)
+    assert s.getvalue() == "iter,col,relres,theta\n0,0,0.10000000000000001,-1.25\n1,0,1.0000000000000001e-09,-1.5\n"

@@ -1,0 +1,141 @@
+"""K1 parity on the GPU: the CUDA SpMM (through the C ABI) against the
+reference's spmm_serial (golden fixtures; live oracle/_ref when present), the
+SPEC.md:229-242 properties, determinism, and size-independent properties at
+the BASELINE config-2 scale."""
+import numpy as np
+import pytest
+
+from conftest import gen_from
+from oracle import ci_oracle as O
+from paper_1609_01689_b200 import ci, configs
+
+pytestmark = pytest.mark.gpu
+
+# fp64 H: different summation order only -> ~1e-16 relative; fp32 H promoted
+# exactly, fp64 accumulation -> same bound.
+TOL = 1e-13
+
+
+def rel(a, b):
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.parametrize("name", ["f64", "f32", "f32_t256"])
+@pytest.mark.parametrize("m", [1, 5, 16])
+def test_spmm_matches_reference_golden(golden, name, m):
+    g = golden("spmm")
+    h = gen_from(g[f"gen_{name}_params"])
+    x = ci.random_block(h.dim, m, 100 + m)
+    assert rel(ci.spmm(h, x), g[f"spmm_{name}_m{m}"]) < TOL
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 7, 8, 13, 16, 17, 32, 48, 64])
+def test_spmm_block_widths(m):
+    """Config-1 matrix (fp64, 64-row tiles) at every LOBPCG width and the
+    config-3 sweep widths."""
+    h = configs.CFG1.generate()
+    x = ci.random_block(h.dim, m, 7 + m)
+    assert rel(ci.spmm(h, x), O.spmm(h, x)) < TOL
+
+
+def test_spmm_live_reference(ref_lib):
+    h = gen_from((30000, 3, 256, 0.02, 0.4, 77, 0, 2000))
+    x = ci.random_block(h.dim, 16, 3)
+    assert rel(ci.spmm(h, x), ref_lib.RefMatrix(h).spmm(x, serial=True)) < TOL
+
+
+def test_spmm_diagonal_and_zero():
+    n = 1000
+    d = np.linspace(-2, 7, n)
+    h = ci.CsbMatrix(dim=n, precision=1, block_boundaries=np.array([0, 500, n], np.uint32),
+                     entry_offsets=np.array([0, 500, 500, n], np.uint64),
+                     rows=np.concatenate([np.arange(500), np.arange(500)]).astype(np.uint16),
+                     cols=np.concatenate([np.arange(500), np.arange(500)]).astype(np.uint16), values=d.copy())
+    x = ci.random_block(n, 6, 1)
+    assert np.array_equal(ci.spmm(h, x), d[:, None] * x)
+    hs = configs.CFG1.generate()
+    assert not ci.spmm(hs, np.zeros((hs.dim, 4))).any()
+
+
+def test_spmm_linearity_symmetry_and_columns():
+    """linearity, u^T(Hv) = v^T(Hu), width-k == k width-1
+    products, deterministic run to run (bitwise)."""
+    h = gen_from((20000, 4, 64, 0.05, 0.5, 5, 0, 2000))
+    x = ci.random_block(h.dim, 8, 1)
+    y = ci.random_block(h.dim, 8, 2)
+    a, b = 0.75, -1.5
+    lhs = ci.spmm(h, a * x + b * y)
+    rhs = a * ci.spmm(h, x) + b * ci.spmm(h, y)
+    assert rel(lhs, rhs) < 1e-12
+    u, v = x[:, :1], y[:, :1]
+    s1 = float(u[:, 0] @ ci.spmm(h, v)[:, 0])
+    s2 = float(v[:, 0] @ ci.spmm(h, u)[:, 0])
+    assert abs(s1 - s2) <= 1e-12 * abs(s1)
+    full = ci.spmm(h, x)
+    for j in range(8):
+        assert np.array_equal(ci.spmm(h, x[:, j:j + 1])[:, 0], full[:, j])
+    assert np.array_equal(ci.spmm(h, x), full)
+
+
+def test_spmm_dimension_mismatch():
+    h = configs.CFG1.generate()
+    with pytest.raises(ci.DimensionMismatch):
+        ci.spmm(h, np.zeros((h.dim + 1, 2)))
+
+
+def test_spmm_small_groups_merge_into_panels():
+    """Physics-style small groups (the 6Li-like partition) are merged into
+    <= 64/128-row panels; result unchanged."""
+    h = gen_from((2000, 2, 64, 0.2, 0.5, 8, 1, 500))
+    rng = np.random.default_rng(0)
+    cuts = np.unique(np.concatenate([[0, 2000], rng.integers(1, 2000, 300)])).astype(np.uint32)
+    h.groups = cuts
+    x = ci.random_block(h.dim, 8, 2)
+    assert rel(ci.DeviceMatrix(h).spmm_host(x), O.spmm(h, x)) < TOL
+
+
+@pytest.mark.slow
+def test_spmm_config2_scale_properties():
+    """BASELINE config 2 (n = 2e6, ~0.8e9 stored nnz, m = 16): oracle-free,
+    size-independent checks -- symmetry of the bilinear form, linearity, the
+    exact diagonal contribution, bitwise determinism -- plus exact parity on
+    a row sample against a CPU product restricted to those rows."""
+    h = configs.CFG2.generate()
+    dm = ci.DeviceMatrix(h)
+    x = ci.random_block(h.dim, 16, 1)
+    y = ci.random_block(h.dim, 16, 2)
+    hx = dm.spmm_host(x)
+    assert np.array_equal(hx, dm.spmm_host(x))
+    hy = dm.spmm_host(y)
+    s1 = np.einsum("ij,ij->j", y, hx)
+    s2 = np.einsum("ij,ij->j", x, hy)
+    assert np.abs(s1 - s2).max() <= 1e-11 * np.abs(s1).max()
+    assert rel(dm.spmm_host(x + 2.0 * y), hx + 2.0 * hy) < 1e-12
+    # row sample: U[rows] from the stored entries touching those rows
+    rows = [0, 1, 99_999, 100_000, 1_234_567, h.dim - 1]
+    want = np.array([_row_product(h, row, x) for row in rows])
+    assert rel(hx[rows], want) < 1e-12
+
+
+def _row_product(h, row, x):
+    """(H X)[row] from the CSB blocks: row part from block row B(row), the
+    transposed part from block column B(row) (the reference's two phases)."""
+    bb = h.block_boundaries.astype(np.int64)
+    offs = h.entry_offsets.astype(np.int64)
+    b = int(np.searchsorted(bb, row, side="right") - 1)
+    loc = row - bb[b]
+    out = np.zeros(x.shape[1])
+    for j in range(b + 1):  # phase one: blocks (b, j)
+        k = b * (b + 1) // 2 + j
+        e0, e1 = offs[k], offs[k + 1]
+        sel = np.nonzero(h.rows[e0:e1] == loc)[0] + e0
+        out += (h.values[sel].astype(np.float64)[:, None] * x[bb[j] + h.cols[sel].astype(np.int64)]).sum(0)
+    for i in range(b, len(bb) - 1):  # phase two: blocks (i, b), strict on the diagonal
+        k = i * (i + 1) // 2 + b
+        e0, e1 = offs[k], offs[k + 1]
+        m = h.cols[e0:e1] == loc
+        if i == b:
+            m &= h.rows[e0:e1] != loc
+        sel = np.nonzero(m)[0] + e0
+        out += (h.values[sel].astype(np.float64)[:, None] * x[bb[i] + h.rows[sel].astype(np.int64)]).sum(0)
+    return out
