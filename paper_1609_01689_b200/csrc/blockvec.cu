@@ -110,15 +110,18 @@ __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R,
     partials[static_cast<std::size_t>(blockIdx.x) * MA * NB + e] = red[e];
 }
 
-// out[a + kx*b] (column major) = sum over blocks, in block order.
+// out[a + kx*b] (column major) = sum over block partials: one warp per
+// element, lane-strided partial sums then a fixed xor tree (deterministic).
 __global__ void gram_reduce_kernel(const double* partials, int nblocks, int MA, int NB, int kx,
                                    int ky, double* out) {
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (e >= kx * ky) return;
   const int a = e % kx, b = e / kx;
   double s = 0.0;
-  for (int k = 0; k < nblocks; ++k) s += partials[static_cast<std::size_t>(k) * MA * NB + a * NB + b];
-  out[e] = s;
+  for (int k = lane; k < nblocks; k += 32) s += partials[static_cast<std::size_t>(k) * MA * NB + a * NB + b];
+  s = warp_sum(s);
+  if (lane == 0) out[e] = s;
 }
 
 template <int MT, int NT>
@@ -301,7 +304,7 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
     const int e = static_cast<int>(kx * ky);
-    gram_reduce_kernel<<<(e + 127) / 128, 128, 0, ctx->stream>>>(partials, blocks, MA, NB,
+    gram_reduce_kernel<<<(e + 3) / 4, 128, 0, ctx->stream>>>(partials, blocks, MA, NB,
                                                                   static_cast<int>(kx), static_cast<int>(ky), dout);
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;

@@ -36,6 +36,8 @@ cieg_mat::~cieg_mat() {
   cudaFree(work_tile);
   cudaFree(work_other);
   cudaFree(work_kind);
+  cudaFree(sched_off);
+  cudaFree(sched);
 }
 
 extern "C" {
@@ -108,6 +110,7 @@ int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* 
     std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te);
     cieg::HostTiles ht;
     cieg::build_tiles(*csb, panels, te, ht);
+    cieg::build_schedule(ht, static_cast<std::uint32_t>(ctx->sm_count));
 
     auto* m = new cieg_mat;
     try {
@@ -130,6 +133,9 @@ int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* 
       m->work_tile = cieg::upload_vec(ht.work_tile);
       m->work_other = cieg::upload_vec(ht.work_other);
       m->work_kind = cieg::upload_vec(ht.work_kind);
+      m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
+      m->sched_off = cieg::upload_vec(ht.sched_off);
+      m->sched = cieg::upload_vec(ht.sched);
       m->tile_bytes = ht.tile_off.back() * (4 + (ht.precision == 0 ? 4 : 8));
     } catch (...) {
       delete m;

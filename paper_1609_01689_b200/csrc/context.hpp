@@ -87,6 +87,9 @@ struct cieg_mat {
   std::uint32_t* work_tile = nullptr;
   std::uint32_t* work_other = nullptr;
   std::uint32_t* work_kind = nullptr;
+  std::uint32_t sched_ctas = 0;
+  std::uint32_t* sched_off = nullptr;
+  std::uint32_t* sched = nullptr;
   ~cieg_mat();
 };
 

@@ -39,6 +39,8 @@ struct SpmmArgs {
   const std::uint32_t* work_tile;
   const std::uint32_t* work_other;
   const std::uint32_t* work_kind;
+  const std::uint32_t* sched_off;
+  const uint4* sched;  // 2 x uint4 per item
   const std::uint64_t* tile_off;
   const std::uint32_t* idx;
   const void* val;
@@ -74,66 +76,28 @@ struct Shape {
 };
 
 struct Item {
-  std::uint32_t kind, o0;
-  int orow;
   std::uint64_t q0, q1;  // entry quads [q0, q1)
+  std::uint32_t flags;   // kind | first << 8 | last << 9
+  std::uint32_t o0;      // partner panel start row
+  int orow;              // partner panel rows
+  std::uint32_t panel;   // owner panel
+  __device__ __forceinline__ std::uint32_t kind() const { return flags & 0xffu; }
+  __device__ __forceinline__ bool first() const { return (flags >> 8) & 1u; }
+  __device__ __forceinline__ bool last() const { return (flags >> 9) & 1u; }
 };
 
-__device__ __forceinline__ void fetch_item(const SpmmArgs& a, std::uint32_t w, Item& it) {
-  const std::uint32_t tile = __ldg(a.work_tile + w);
-  const std::uint32_t other = __ldg(a.work_other + w);
-  it.kind = __ldg(a.work_kind + w);
-  it.o0 = __ldg(a.panel_start + other);
-  it.orow = static_cast<int>(__ldg(a.panel_start + other + 1) - it.o0);
-  it.q0 = __ldg(a.tile_off + tile) >> 2;
-  it.q1 = __ldg(a.tile_off + tile + 1) >> 2;
-}
-
-// Walks the CTA's (panel, item, chunk) sequence.
-struct Cursor {
-  std::uint32_t P, w;
+__device__ __forceinline__ Item load_item(const SpmmArgs& a, std::uint32_t i) {
+  const uint4 u = __ldg(a.sched + 2 * static_cast<std::size_t>(i));
+  const uint4 v = __ldg(a.sched + 2 * static_cast<std::size_t>(i) + 1);
   Item it;
-  std::uint64_t q;  // first quad of the current chunk
-  bool valid;
-
-  __device__ __forceinline__ bool seek_panel(const SpmmArgs& a) {
-    while (w >= a.work_off[P + 1]) {
-      P += gridDim.x;
-      if (P >= a.npanels) return false;
-      w = a.work_off[P];
-    }
-    return true;
-  }
-  __device__ __forceinline__ void init(const SpmmArgs& a) {
-    P = blockIdx.x;
-    valid = P < a.npanels;
-    if (!valid) return;
-    w = a.work_off[P];
-    valid = seek_panel(a);
-    if (valid) {
-      fetch_item(a, w, it);
-      q = it.q0;
-    }
-  }
-  // next item after the current one (for slab prefetch); false at the end
-  __device__ __forceinline__ bool peek_next(const SpmmArgs& a, Item& nit) const {
-    Cursor c = *this;
-    ++c.w;
-    if (!c.seek_panel(a)) return false;
-    fetch_item(a, c.w, nit);
-    return true;
-  }
-  __device__ __forceinline__ void next_chunk(const SpmmArgs& a) {
-    q += kChunkQuads;
-    if (q < it.q1) return;
-    ++w;
-    valid = seek_panel(a);
-    if (valid) {
-      fetch_item(a, w, it);
-      q = it.q0;
-    }
-  }
-};
+  it.q0 = (static_cast<std::uint64_t>(u.y) << 32) | u.x;
+  it.q1 = (static_cast<std::uint64_t>(u.w) << 32) | u.z;
+  it.flags = v.x;
+  it.o0 = v.y;
+  it.orow = static_cast<int>(v.z);
+  it.panel = v.w;
+  return it;
+}
 
 template <typename V, int TD, int NT>
 __device__ __forceinline__ void load_slab(const SpmmArgs& a, const Item& it, int pt,
@@ -205,44 +169,44 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
 
-  // Total work items of this CTA (to balance the EMPTY barrier arrivals).
-  std::uint32_t total = 0;
-  for (std::uint32_t P = blockIdx.x; P < a.npanels; P += gridDim.x) total += a.work_off[P + 1] - a.work_off[P];
+  const std::uint32_t i_beg = a.sched_off[blockIdx.x], i_end = a.sched_off[blockIdx.x + 1];
+  const std::uint32_t total = i_end - i_beg;
+  if (total == 0) return;
 
   if (warp < kProducerWarps) {
     // ------------------------------------------------------------ producer
-    // Register double buffer: the next batch of entry quads (possibly the
-    // first batch of the next work item) is in flight while the current one
-    // is scattered; the next item's X slab is prefetched a whole item ahead.
+    // Register double buffer: the next batch of entry quads (or the first
+    // batch of the next work item) is in flight while the current batch is
+    // placed; item descriptors are prefetched two items ahead and the next
+    // item's X slab a whole item ahead.
     const int pt = tid;  // 0 .. 255
-    Cursor issue, use;
-    issue.init(a);
-    if (!issue.valid) return;
-    use = issue;
-    Quad<V> cur[kQuads], nxt[kQuads];
-    auto load_batch = [&](Quad<V>(&out)[kQuads]) {
+    const V* val = static_cast<const V*>(a.val);
+    auto load_batch = [&](const Item& it, std::uint64_t qb, Quad<V>(&out)[kQuads]) {
 #pragma unroll
       for (int j = 0; j < kQuads; ++j) {
-        const std::uint64_t q = issue.q + pt + static_cast<std::uint64_t>(j) * kProducerThreads;
-        if (issue.valid && q < issue.it.q1)
-          load_quad(a, static_cast<const V*>(a.val), q, out[j]);
+        const std::uint64_t q = qb + pt + static_cast<std::uint64_t>(j) * kProducerThreads;
+        if (q < it.q1)
+          load_quad(a, val, q, out[j]);
         else
           out[j].id.x = kNoQuad;
       }
-      if (issue.valid) issue.next_chunk(a);
     };
-    load_batch(cur);
+    Item cur = load_item(a, i_beg);
+    Item nxt = (i_beg + 1 < i_end) ? load_item(a, i_beg + 1) : cur;
+    Quad<V> qa[kQuads], qb[kQuads];
+    load_batch(cur, cur.q0, qa);
     double xv[S::kSlabPer];
-    load_slab<V, TD, NT>(a, use.it, pt, xv);
+    load_slab<V, TD, NT>(a, cur, pt, xv);
     int buf = 0;
-    while (use.valid) {
+    for (std::uint32_t i = i_beg; i < i_end; ++i) {
+      const bool has_next = i + 1 < i_end;
       bar_sync(kBarEmpty0 + buf, kThreads);
       V* A = tile_buf(buf);
       {
         float4* p4 = reinterpret_cast<float4*>(A);
         constexpr int n4 = static_cast<int>(S::kTileBytes / 16);
 #pragma unroll 4
-        for (int i = pt; i < n4; i += kProducerThreads) p4[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = pt; k < n4; k += kProducerThreads) p4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       double* X = slab_buf(buf);
 #pragma unroll
@@ -251,32 +215,34 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         const int k = e / (8 * NT), t = e - k * (8 * NT);
         X[k * S::kSX + t] = xv[j];
       }
-      {
-        Item nit;
-        if (use.peek_next(a, nit)) load_slab<V, TD, NT>(a, nit, pt, xv);
-      }
+      if (has_next) load_slab<V, TD, NT>(a, nxt, pt, xv);
+      const Item after = (i + 2 < i_end) ? load_item(a, i + 2) : nxt;
       bar_sync(kBarProducers, kProducerThreads);  // clear before scatter
-      const std::uint32_t kind = use.it.kind;
-      for (;;) {
-        load_batch(nxt);
+      const std::uint32_t kind = cur.kind();
+      for (std::uint64_t q = cur.q0;; q += kChunkQuads) {
+        const bool more = q + kChunkQuads < cur.q1;
+        if (more)
+          load_batch(cur, q + kChunkQuads, qb);
+        else if (has_next)
+          load_batch(nxt, nxt.q0, qb);
 #pragma unroll
         for (int j = 0; j < kQuads; ++j) {
-          if (cur[j].id.x == kNoQuad) continue;
+          if (qa[j].id.x == kNoQuad) continue;
           if (kind == 0u)
-            put4<0>(A, cur[j]);
+            put4<0>(A, qa[j]);
           else if (kind == 1u)
-            put4<1>(A, cur[j]);
-          else
-            put4<2>(A, cur[j]);
+            put4<1>(A, qa[j]);
+          else if (kind == 2u)
+            put4<2>(A, qa[j]);
         }
 #pragma unroll
-        for (int j = 0; j < kQuads; ++j) cur[j] = nxt[j];
-        const std::uint32_t w_before = use.w, p_before = use.P;
-        use.next_chunk(a);
-        if (!use.valid || use.w != w_before || use.P != p_before) break;
+        for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
+        if (!more) break;
       }
       bar_arrive(kBarFull0 + buf, kThreads);
       buf ^= 1;
+      cur = nxt;
+      nxt = after;
     }
   } else {
     // ------------------------------------------------------------ consumer
@@ -286,47 +252,47 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
     bar_arrive(kBarEmpty0 + 0, kThreads);
     bar_arrive(kBarEmpty0 + 1, kThreads);
     int buf = 0;
-    std::uint32_t done = 0;
-    for (std::uint32_t P = blockIdx.x; P < a.npanels; P += gridDim.x) {
-      const std::uint32_t r0 = __ldg(a.panel_start + P);
-      const int prow = static_cast<int>(__ldg(a.panel_start + P + 1) - r0);
-      double acc[S::kMT][NT][2];
+    double acc[S::kMT][NT][2];
+    Item it = load_item(a, i_beg);
+    for (std::uint32_t i = i_beg; i < i_end; ++i) {
+      const Item nit = (i + 1 < i_end) ? load_item(a, i + 1) : it;
+      if (it.first()) {
 #pragma unroll
-      for (int j = 0; j < S::kMT; ++j)
+        for (int j = 0; j < S::kMT; ++j)
 #pragma unroll
-        for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
-      const bool live = m_base < prow;
-      for (std::uint32_t w = a.work_off[P]; w < a.work_off[P + 1]; ++w) {
-        bar_sync(kBarFull0 + buf, kThreads);
-        if (live) {
-          // Rows >= orow of the slab and of the tile are zero: all TD/4
-          // k-steps run. Groups of 4 k-steps load every fragment into its own
-          // register before the group's DMMAs issue.
-          const V* A = tile_buf(buf) + (m_base + g) * S::kSA + q;
-          const double* xb = slab_buf(buf) + q * S::kSX + g;
-#pragma unroll 1
-          for (int k0 = 0; k0 < TD / 4; k0 += 4) {
-            double af[4][S::kMT], bf[4][NT];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-#pragma unroll
-              for (int j = 0; j < S::kMT; ++j) af[u][j] = static_cast<double>(A[j * 8 * S::kSA + 4 * (k0 + u)]);
-#pragma unroll
-              for (int n = 0; n < NT; ++n) bf[u][n] = xb[4 * (k0 + u) * S::kSX + 8 * n];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-#pragma unroll
-              for (int n = 0; n < NT; ++n)
-#pragma unroll
-                for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], af[u][j], bf[u][n]);
-          }
-        }
-        ++done;
-        if (done + 2 <= total) bar_arrive(kBarEmpty0 + buf, kThreads);
-        buf ^= 1;
+          for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
       }
+      const std::uint32_t r0 = __ldg(a.panel_start + it.panel);
+      const int prow = static_cast<int>(__ldg(a.panel_start + it.panel + 1) - r0);
+      const bool live = m_base < prow;
+      bar_sync(kBarFull0 + buf, kThreads);
       if (live) {
+        // Rows >= orow of the slab and of the tile are zero: all TD/4
+        // k-steps run. Groups of 4 k-steps load every fragment into its own
+        // register before the group's DMMAs issue.
+        const V* A = tile_buf(buf) + (m_base + g) * S::kSA + q;
+        const double* xb = slab_buf(buf) + q * S::kSX + g;
+#pragma unroll 1
+        for (int k0 = 0; k0 < TD / 4; k0 += 4) {
+          double af[4][S::kMT], bf[4][NT];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+#pragma unroll
+            for (int j = 0; j < S::kMT; ++j) af[u][j] = static_cast<double>(A[j * 8 * S::kSA + 4 * (k0 + u)]);
+#pragma unroll
+            for (int n = 0; n < NT; ++n) bf[u][n] = xb[4 * (k0 + u) * S::kSX + 8 * n];
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int n = 0; n < NT; ++n)
+#pragma unroll
+              for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], af[u][j], bf[u][n]);
+        }
+      }
+      if (i + 2 < i_end) bar_arrive(kBarEmpty0 + buf, kThreads);
+      buf ^= 1;
+      if (it.last() && live) {
 #pragma unroll
         for (int j = 0; j < S::kMT; ++j) {
           const int row = m_base + 8 * j + g;
@@ -344,6 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
           }
         }
       }
+      it = nit;
     }
   }
 }
@@ -354,12 +321,7 @@ void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   static_assert(S::kSmem <= 227 * 1024, "shared memory budget");
   auto kern = spmm_ws_kernel<V, TD, NT>;
   CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::kSmem)));
-  int per_sm = 0;
-  CIEG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, S::kSmem));
-  per_sm = std::max(1, per_sm);
-  const unsigned grid =
-      static_cast<unsigned>(std::min<std::uint64_t>(m->npanels, static_cast<std::uint64_t>(per_sm) * ctx->sm_count));
-  kern<<<grid, kThreads, S::kSmem, ctx->stream>>>(args);
+  kern<<<m->sched_ctas, kThreads, S::kSmem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
 }
@@ -379,9 +341,22 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
   if (mcols == 0 || m->dim == 0) return;
   for (std::uint32_t c0 = 0; c0 < mcols; c0 += 16) {
     const std::uint32_t mc = std::min<std::uint32_t>(16, mcols - c0);
-    SpmmArgs args{m->panel_start, m->work_off, m->work_tile, m->work_other, m->work_kind,
-                  m->tile_off,    m->idx,      m->val,       x + c0,        y + c0,
-                  ldx,            ldy,         mc,           m->npanels};
+    SpmmArgs args{m->panel_start,
+                  m->work_off,
+                  m->work_tile,
+                  m->work_other,
+                  m->work_kind,
+                  m->sched_off,
+                  reinterpret_cast<const uint4*>(m->sched),
+                  m->tile_off,
+                  m->idx,
+                  m->val,
+                  x + c0,
+                  y + c0,
+                  ldx,
+                  ldy,
+                  mc,
+                  m->npanels};
     if (m->precision == 0) {
       if (m->tile_edge == 64)
         dispatch_nt<float, 64>(ctx, m, args, mc);

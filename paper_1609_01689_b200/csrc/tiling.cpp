@@ -200,4 +200,61 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
   if (nt >= (1ull << 32)) fail(CIEG_ERR_CONFIG, "tile count exceeds 2^32");
 }
 
+void build_schedule(HostTiles& t, std::uint32_t ctas) {
+  const std::uint32_t np = t.npanels();
+  ctas = std::max<std::uint32_t>(1, std::min<std::uint32_t>(ctas, np));
+  // cost of a panel = entry quads of its work items + a fixed per-item charge
+  std::vector<std::pair<std::uint64_t, std::uint32_t>> cost(np);
+  for (std::uint32_t P = 0; P < np; ++P) {
+    std::uint64_t c = 0;
+    for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w) {
+      const std::uint32_t tile = t.work_tile[w];
+      c += (t.tile_off[tile + 1] - t.tile_off[tile]) / 4 + 256;
+    }
+    cost[P] = {c, P};
+  }
+  std::vector<std::uint32_t> order(np);
+  std::iota(order.begin(), order.end(), 0u);
+  std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
+    return cost[a].first > cost[b].first;
+  });
+  // min-heap of (load, cta)
+  std::vector<std::pair<std::uint64_t, std::uint32_t>> heap;
+  for (std::uint32_t b = 0; b < ctas; ++b) heap.push_back({0, b});
+  auto cmp = [](const auto& x, const auto& y) { return x.first != y.first ? x.first > y.first : x.second > y.second; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  std::vector<std::vector<std::uint32_t>> panels_of(ctas);
+  for (std::uint32_t P : order) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    auto& top = heap.back();
+    panels_of[top.second].push_back(P);
+    top.first += cost[P].first;
+    std::push_heap(heap.begin(), heap.end(), cmp);
+  }
+  t.sched_off.assign(ctas + 1, 0);
+  t.sched.clear();
+  for (std::uint32_t b = 0; b < ctas; ++b) {
+    std::sort(panels_of[b].begin(), panels_of[b].end());
+    for (std::uint32_t P : panels_of[b]) {
+      const std::uint32_t w0 = t.work_off[P], w1 = t.work_off[P + 1];
+      if (w0 == w1) {  // empty panel: one no-op item so the owner still writes zeros
+        const std::uint32_t d[8] = {0, 0, 0, 0, 3u | (1u << 8) | (1u << 9), t.panel_start[P],
+                                    t.panel_start[P + 1] - t.panel_start[P], P};
+        t.sched.insert(t.sched.end(), d, d + 8);
+        continue;
+      }
+      for (std::uint32_t w = w0; w < w1; ++w) {
+        const std::uint32_t tile = t.work_tile[w], other = t.work_other[w];
+        const std::uint64_t q0 = t.tile_off[tile] / 4, q1 = t.tile_off[tile + 1] / 4;
+        const std::uint32_t flags = t.work_kind[w] | ((w == w0) ? 1u << 8 : 0u) | ((w + 1 == w1) ? 1u << 9 : 0u);
+        const std::uint32_t d[8] = {static_cast<std::uint32_t>(q0), static_cast<std::uint32_t>(q0 >> 32),
+                                    static_cast<std::uint32_t>(q1), static_cast<std::uint32_t>(q1 >> 32),
+                                    flags, t.panel_start[other], t.panel_start[other + 1] - t.panel_start[other], P};
+        t.sched.insert(t.sched.end(), d, d + 8);
+      }
+    }
+    t.sched_off[b + 1] = static_cast<std::uint32_t>(t.sched.size() / 8);
+  }
+}
+
 }  // namespace cieg

@@ -41,6 +41,11 @@ struct HostTiles {
   std::vector<std::uint32_t> work_off;
   std::vector<std::uint32_t> work_tile, work_other, work_kind;
 
+  // Static per-CTA schedule for the persistent SpMM kernel (one CTA per SM):
+  // CTA b runs sched[sched_off[b] .. sched_off[b+1]) in order.
+  std::vector<std::uint32_t> sched_off;
+  std::vector<std::uint32_t> sched;  // 8 words per item, see ItemDesc in spmm.cu
+
   std::uint32_t npanels() const { return static_cast<std::uint32_t>(panel_start.size() - 1); }
   std::uint64_t ntiles() const { return tile_pi.size(); }
 };
@@ -54,5 +59,11 @@ std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* g
 
 void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& panels,
                  std::uint32_t tile_edge, HostTiles& out);
+
+// Assign owner panels to `ctas` persistent CTAs (longest-first greedy on the
+// entry count, ties by panel id, so the result is deterministic) and emit
+// each CTA's item descriptors: {q0 lo/hi, q1 lo/hi, kind | first << 8 |
+// last << 9, other-panel start row, other-panel rows, owner panel}.
+void build_schedule(HostTiles& t, std::uint32_t ctas);
 
 }  // namespace cieg

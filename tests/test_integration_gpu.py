@@ -1,0 +1,37 @@
+"""The reference-side drop-in (integration/ci_gpu_dropin.cpp): the reference's
+own ci::lobpcg_solve signature, compiled against the reference headers, now
+running on the GPU -- same iteration count and eigenvalues as the
+reference's CPU solve (golden fixture)."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, gen_from
+from paper_1609_01689_b200 import ci
+
+pytestmark = pytest.mark.gpu
+LIB = os.path.join(ROOT, "integration", "_build", "libcieigen_gpu.so")
+
+
+@pytest.mark.parametrize("name", ["sector_f64", "sector_f64_prec"])
+def test_dropin_lobpcg_matches_reference(golden, name):
+    if not os.path.exists(LIB):
+        pytest.skip("integration/_build not built (needs the reference headers at build time)")
+    lib = C.CDLL(LIB)
+    g = golden("lobpcg")
+    k, kt, tol, pre, seed = g[f"{name}_meta"]
+    h = gen_from(g[f"{name}_params"])
+    x0 = ci.random_block(h.dim, int(kt), int(seed))
+    v = h.view()
+    groups = np.ascontiguousarray(h.groups, dtype=np.uint32)
+    eig = np.zeros(int(k))
+    iters = C.c_int()
+    rc = lib.dropin_lobpcg(C.byref(v), groups.ctypes.data_as(C.POINTER(C.c_uint32)), C.c_uint32(len(groups) - 1),
+                           x0.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint32(int(kt)), C.c_int(int(k)),
+                           C.c_double(float(tol)), C.c_int(int(pre)), eig.ctypes.data_as(C.POINTER(C.c_double)),
+                           C.byref(iters))
+    assert rc == 0
+    assert iters.value == int(g[f"{name}_iterations"])
+    np.testing.assert_allclose(eig, g[f"{name}_eigenvalues"], rtol=1e-10)
