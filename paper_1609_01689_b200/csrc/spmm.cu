@@ -22,8 +22,12 @@
 //   * fp32 values are promoted to fp64 exactly on fragment load (F2F runs on
 //     its own unit, measured not to slow DMMA); products and sums are fp64,
 //     the reference's precision contract (csb.hpp:79-82).
-//   * padding makes fragment loads conflict-free: tile row stride TD+4 words
-//     (bank 4g+q), X slab row stride 8*NT+4 doubles.
+//   * fragment loads are conflict-free and wide: tile columns are stored
+//     k-step-pair interleaved (upload-time permutation folded into the packed
+//     indices) with row stride TD+8, so one 64-bit (fp32) / 128-bit (fp64)
+//     load per lane yields the A fragments of two k-steps; X slab row stride
+//     8*NT+4 doubles. The consumer double-buffers fragments across groups of
+//     4 k-steps so loads and conversions overlap the previous group's DMMAs.
 #include <algorithm>
 #include <cstdint>
 
@@ -66,7 +70,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 template <typename V, int TD, int NT>
 struct Shape {
-  static constexpr int kSA = TD + 4;                    // row stride (elements), 4 mod 16
+  static constexpr int kSA = TD + 8;                    // row stride (elements), 8 mod 32 banks (f32)
   static constexpr int kSX = 8 * NT + 4;                // doubles
   static constexpr int kMT = TD / 8 / kConsumerWarps;   // m-tiles per consumer warp
   static constexpr std::size_t kTileBytes = ((sizeof(V) * TD * kSA + 15) / 16) * 16;
@@ -268,26 +272,50 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       bar_sync(kBarFull0 + buf, kThreads);
       if (live) {
         // Rows >= orow of the slab and of the tile are zero: all TD/4
-        // k-steps run. Groups of 4 k-steps load every fragment into its own
-        // register before the group's DMMAs issue.
-        const V* A = tile_buf(buf) + (m_base + g) * S::kSA + q;
+        // k-steps run, in groups of 4 (two interleaved k-step pairs), with
+        // the next group's fragments loaded and converted while the current
+        // group's DMMAs issue.
+        const V* A = tile_buf(buf) + (m_base + g) * S::kSA + 2 * q;
         const double* xb = slab_buf(buf) + q * S::kSX + g;
-#pragma unroll 1
-        for (int k0 = 0; k0 < TD / 4; k0 += 4) {
-          double af[4][S::kMT], bf[4][NT];
+        double af[2][4][S::kMT], bf[2][4][NT];
+        auto load_group = [&](int grp, double (&fa)[4][S::kMT], double (&fb)[4][NT]) {
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
+          for (int p = 0; p < 2; ++p) {
 #pragma unroll
-            for (int j = 0; j < S::kMT; ++j) af[u][j] = static_cast<double>(A[j * 8 * S::kSA + 4 * (k0 + u)]);
-#pragma unroll
-            for (int n = 0; n < NT; ++n) bf[u][n] = xb[4 * (k0 + u) * S::kSX + 8 * n];
+            for (int j = 0; j < S::kMT; ++j) {
+              const V* src = A + j * 8 * S::kSA + 8 * (2 * grp + p);
+              if constexpr (sizeof(V) == 4) {
+                const float2 v2 = *reinterpret_cast<const float2*>(src);
+                fa[2 * p][j] = static_cast<double>(v2.x);
+                fa[2 * p + 1][j] = static_cast<double>(v2.y);
+              } else {
+                const double2 v2 = *reinterpret_cast<const double2*>(src);
+                fa[2 * p][j] = v2.x;
+                fa[2 * p + 1][j] = v2.y;
+              }
+            }
           }
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int n = 0; n < NT; ++n) fb[u][n] = xb[4 * (4 * grp + u) * S::kSX + 8 * n];
+        };
+        auto mma_group = [&](const double (&fa)[4][S::kMT], const double (&fb)[4][NT]) {
 #pragma unroll
           for (int u = 0; u < 4; ++u)
 #pragma unroll
             for (int n = 0; n < NT; ++n)
 #pragma unroll
-              for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], af[u][j], bf[u][n]);
+              for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], fa[u][j], fb[u][n]);
+        };
+        constexpr int kGroups = TD / 16;
+        load_group(0, af[0], bf[0]);
+#pragma unroll 1
+        for (int grp = 0; grp < kGroups; grp += 2) {
+          load_group(grp + 1, af[1], bf[1]);
+          mma_group(af[0], bf[0]);
+          if (grp + 2 < kGroups) load_group(grp + 2, af[0], bf[0]);
+          mma_group(af[1], bf[1]);
         }
       }
       if (i + 2 < i_end) bar_arrive(kBarEmpty0 + buf, kThreads);

@@ -45,8 +45,12 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
     if (panels[p + 1] <= panels[p] || panels[p + 1] - panels[p] > te)
       fail(CIEG_ERR_CONFIG, "panel plan violates the tile edge");
 
-  const std::uint32_t sa = te + 4;
+  const std::uint32_t sa = te + 8;
   const std::uint32_t sentinel = te | (te << 16);  // row 0, pad column te: never read
+  // Within every 8 columns, k-step j's column 4j' + q and k-step j'+1's
+  // column 4j' + 4 + q are stored side by side, so one 64-bit (fp32) or
+  // 128-bit (fp64) shared load yields the A fragments of two k-steps.
+  auto kperm = [](std::uint32_t k) { return (k & ~7u) | ((k & 3u) << 1) | ((k >> 2) & 1u); };
   std::vector<std::uint32_t> panel_of(dim);
   for (std::uint32_t p = 0; p < np; ++p)
     for (std::uint32_t r = panels[p]; r < panels[p + 1]; ++r) panel_of[r] = p;
@@ -111,9 +115,10 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
           }
           const std::uint32_t rl = a - r0, cl = b - panels[pj];
           // Packed tile-local index: the entry's shared-memory offset in the
-          // row-part orientation (r * SA + c) and in the transposed one
-          // (c * SA + r), SA = tile_edge + 4 (the kernels' padded row stride).
-          tb->idx.push_back((rl * sa + cl) | ((cl * sa + rl) << 16));
+          // row-part orientation (r * SA + perm(c)) and in the transposed one
+          // (c * SA + perm(r)), SA = tile_edge + 8 (the kernels' padded row
+          // stride, 8 mod 32 banks).
+          tb->idx.push_back((rl * sa + kperm(cl)) | ((cl * sa + kperm(rl)) << 16));
           tb->v.push_back(single ? static_cast<double>(v32[e]) : v64[e]);
         }
       }

@@ -8,9 +8,10 @@
 //   * one stored tile per nonzero (PI >= PJ) panel pair, entries as a packed
 //     32-bit tile-local index plus the value (f32 or f64), tiles back to back
 //     with 64-bit offsets, each list padded to a multiple of 4. The index
-//     holds the entry's two shared-memory offsets, r*SA+c (low 16 bits) and
-//     c*SA+r (high 16 bits), SA = tile_edge + 4, so the SpMM scatter is a
-//     single store in either orientation;
+//     holds the entry's two shared-memory offsets, r*SA+perm(c) (low 16
+//     bits) and c*SA+perm(r) (high 16 bits), SA = tile_edge + 8, perm pairing
+//     the columns of consecutive k-steps, so the SpMM scatter is a single
+//     store in either orientation;
 //   * an owner work list per panel P: the tiles whose product lands in P's
 //     rows -- (P, J) row parts, (I, P) transposed parts, (P, P) symmetric --
 //     so one CTA computes all of Y[P] and writes it exactly once
@@ -34,7 +35,7 @@ struct HostTiles {
   std::vector<std::uint32_t> panel_start;      // npanels + 1
   std::vector<std::uint64_t> tile_off;         // ntiles + 1
   std::vector<std::uint32_t> tile_pi, tile_pj; // panel pair of each tile
-  std::vector<std::uint32_t> idx;              // packed (r*SA+c) | (c*SA+r) << 16
+  std::vector<std::uint32_t> idx;              // packed (r*SA+perm c) | (c*SA+perm r) << 16
   std::vector<float> val32;
   std::vector<double> val64;
   // owner work lists: items [work_off[P], work_off[P+1]) of (tile, other, kind)
