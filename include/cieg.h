@@ -108,6 +108,44 @@ int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y
 int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
                    uint32_t m);
 
+/* ---- row-block sharding over several GPUs ------------ */
+/* Partition the rows over nranks at group boundaries (a group never straddles
+ * two ranks, so each rank's tile diagonal is local), balanced by the stored
+ * entries each owner streams (owner-computes: a rank reads its rows' tiles and
+ * the tiles (I > P, P) whose transposed part lands in its rows).
+ * row_bounds: nranks + 1 entries. halo_lo/halo_hi: the X rows rank r's SpMM
+ * reads. Host-only (no device needed). The planner of the reference only
+ * models this (planner.cpp:88-139). */
+int cieg_shard_plan(const cieg_csb_view* csb, const uint32_t* group_bounds, uint32_t ngroups,
+                    uint32_t tile_edge, uint32_t nranks, uint32_t* row_bounds, uint32_t* halo_lo,
+                    uint32_t* halo_hi);
+/* Upload the part of H that owner rows [row_lo, row_hi) need. cieg_spmm on
+ * the result reads a full-length X (only rows [halo_lo, halo_hi) are touched)
+ * and writes rows [row_lo, row_hi) of U into a LOCAL buffer (row_lo -> row 0). */
+int cieg_matrix_upload_shard(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                             uint32_t ngroups, uint32_t tile_edge, uint32_t row_lo, uint32_t row_hi,
+                             cieg_mat** out);
+/* Rows owned by a (shard) matrix: [row_lo, row_hi); the full matrix owns all. */
+int cieg_matrix_rows(const cieg_mat* mat, uint32_t* row_lo, uint32_t* row_hi, uint32_t* halo_lo,
+                     uint32_t* halo_hi);
+/* Tile diagonal of the groups inside [row_lo, row_hi) (local row numbering). */
+int cieg_precond_from_csb_range(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                                uint32_t ngroups, uint32_t row_lo, uint32_t row_hi, cieg_prec** out);
+/* Run the context's work on a caller-owned stream (e.g. torch's current
+ * stream) so it orders with the caller's collectives; NULL restores the
+ * context's own stream. */
+int cieg_ctx_set_stream(cieg_ctx* ctx, void* stream);
+
+/* Collective hooks for the sharded solver (one process per GPU). */
+typedef struct {
+  void* user;
+  /* in-place sum over ranks of `count` doubles in host memory (Gram partials) */
+  int (*allreduce_sum)(void* user, double* host_buf, uint64_t count);
+  /* all-gather: every rank's local rows of a row-distributed block (device,
+   * local_rows x m) into the full-length block x_full (device, dim x m) */
+  int (*allgather_rows)(void* user, const double* x_local_dev, uint32_t m, double* x_full_dev);
+} cieg_dist_hooks;
+
 /* ---- tall-skinny block kernels (proj/include/ci/block_vectors.hpp) ----- */
 /* X^T Y (kx x ky, column major, written to out_host) -- ci::block_inner
  * (block_vectors.hpp:60, block_vectors.cpp:74-85). Partials are reduced in a
@@ -187,6 +225,13 @@ typedef void (*cieg_observer_fn)(void* user, int iteration, const double* x_host
 int cieg_lobpcg_solve(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
                       const cieg_prec* prec, const cieg_lobpcg_options* opt,
                       cieg_observer_fn observer, void* observer_user, cieg_report** out);
+/* Sharded ci::lobpcg_solve: mat from cieg_matrix_upload_shard, x0_host and
+ * prec local to the rank's rows; every Gram is all-reduced and the SpMM input
+ * all-gathered through `hooks`; identical control flow on every rank. The
+ * report's trial vectors are the rank's local rows. */
+int cieg_lobpcg_solve_dist(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
+                           const cieg_prec* prec, const cieg_lobpcg_options* opt, const cieg_dist_hooks* hooks,
+                           cieg_report** out);
 int cieg_report_destroy(cieg_report* rep);
 /* SolveReport fields (lobpcg.hpp:34-43). */
 int cieg_report_summary(const cieg_report* rep, int* converged, int* iterations,

@@ -493,24 +493,25 @@ def _llt_rinv(a):
     return scipy.linalg.solve_triangular(L.T, np.eye(a.shape[0]), lower=False)
 
 
-def orthonormalize(y, drop_tol=1e-8, against=None):
-    """lobpcg.cpp:89-119."""
+def orthonormalize(y, drop_tol=1e-8, against=None, inner=block_inner):
+    """lobpcg.cpp:89-119. `inner` computes X^T Y (a sharded run passes a
+    local-partial + all-reduce)."""
     v = np.array(y, dtype=np.float64, copy=True)
     if v.shape[1] == 0:
         return v
-    orig_sq = np.diag(block_inner(y, y)).copy()
+    orig_sq = np.diag(inner(y, y)).copy()
     if against is not None and against.shape[1] > 0:
         for _ in range(2):
-            c = block_inner(against, v)
+            c = inner(against, v)
             v = add_linear_combination(v, against, -c)
-    gram = block_inner(v, v)
+    gram = inner(v, v)
     kept = _rank_revealing_select(gram, orig_sq, drop_tol)
     while kept:
         q = v[:, kept]
         rinv = _llt_rinv(gram[np.ix_(kept, kept)])
         if rinv is not None:
             q = linear_combination(q, rinv)
-            r2 = _llt_rinv(block_inner(q, q))
+            r2 = _llt_rinv(inner(q, q))
             if r2 is not None:
                 q = linear_combination(q, r2)
             return q
@@ -534,15 +535,19 @@ class Report:
     active_sets: list
 
 
-def lobpcg_solve(h, x0, k_want, tol, max_iter=500, tiles=None, bounds=None, cfg=PrecondConfig(), matvec=None):
+def lobpcg_solve(h, x0, k_want, tol, max_iter=500, tiles=None, bounds=None, cfg=PrecondConfig(), matvec=None,
+                 inner=block_inner):
     """lobpcg.cpp:216-387, verbatim control flow. `tiles`/`bounds` give the
-    dense tile diagonal (None = unpreconditioned); `matvec` overrides the SpMM."""
+    dense tile diagonal (None = unpreconditioned); `matvec` overrides the SpMM;
+    `inner` overrides X^T Y -- together they run the same loop on a row shard
+    (local rows, all-gathered SpMM input, all-reduced Grams)."""
+    block_inner = inner  # noqa: N806 -- every Gram below goes through the hook
     if x0.shape[1] < k_want:
         raise ValueError("ConfigError: lobpcg: trial width below k_want")
     apply = matvec or (lambda v: spmm(h, v))
     counters = [0, 0, 0, 0]
     drop_tol = 1e-8
-    x = orthonormalize(x0, drop_tol)
+    x = orthonormalize(x0, drop_tol, inner=inner)
     counters[3] += 1
     if x.shape[1] < k_want:
         raise ValueError("SubspaceCollapse: initial block has fewer than k_want independent columns")
@@ -567,7 +572,7 @@ def lobpcg_solve(h, x0, k_want, tol, max_iter=500, tiles=None, bounds=None, cfg=
     it = 0
     while True:
         r = hx - x * theta[None, :]
-        res_norm = column_norms(r)
+        res_norm = np.sqrt(np.diag(block_inner(r, r)))
         relres = res_norm / max(norm_est, K_TINY_DIAG)
         for j in range(kt):
             history.append((it, j, float(relres[j]), float(theta[j])))
@@ -586,7 +591,7 @@ def lobpcg_solve(h, x0, k_want, tol, max_iter=500, tiles=None, bounds=None, cfg=
             wsrc = r
         active = [j for j in range(kt) if relres[j] > tol]
         active_sets.append(active)
-        w = orthonormalize(wsrc[:, active], drop_tol, np.hstack([x, p]))
+        w = orthonormalize(wsrc[:, active], drop_tol, np.hstack([x, p]), inner=inner)
         counters[3] += 1
         if w.shape[1] == 0:
             break

@@ -72,6 +72,14 @@ class LobpcgOptionsC(C.Structure):
     ]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_uint64)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p)
+
+
+class DistHooks(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE_FN), ("allgather_rows", ALLGATHER_FN)]
+
+
 OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_uint32,
                        C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double))
 
@@ -113,6 +121,13 @@ SIGNATURES = {
     "cieg_lobpcg_solve": (_i, [_vp, _vp, _pd, _u32, _vp, C.POINTER(LobpcgOptionsC), OBSERVER, _vp,
                                C.POINTER(_vp)]),
     "cieg_report_destroy": (_i, [_vp]),
+    "cieg_lobpcg_solve_dist": (_i, [_vp, _vp, _pd, _u32, _vp, C.POINTER(LobpcgOptionsC), C.POINTER(DistHooks),
+                                    C.POINTER(_vp)]),
+    "cieg_shard_plan": (_i, [C.POINTER(CsbView), _pu32, _u32, _u32, _u32, _pu32, _pu32, _pu32]),
+    "cieg_matrix_upload_shard": (_i, [_vp, C.POINTER(CsbView), _pu32, _u32, _u32, _u32, _u32, C.POINTER(_vp)]),
+    "cieg_matrix_rows": (_i, [_vp, _pu32, _pu32, _pu32, _pu32]),
+    "cieg_precond_from_csb_range": (_i, [_vp, C.POINTER(CsbView), _pu32, _u32, _u32, _u32, C.POINTER(_vp)]),
+    "cieg_ctx_set_stream": (_i, [_vp, _vp]),
     "cieg_report_summary": (_i, [_vp, _pi, _pi, _pd, _pu32, _pu32, _pu64]),
     "cieg_report_counters": (_i, [_vp, _pu64]),
     "cieg_report_eigenvalues": (_i, [_vp, _pd]),

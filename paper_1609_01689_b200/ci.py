@@ -629,6 +629,10 @@ def lobpcg_solve(h: CsbMatrix, x0: np.ndarray, options: LobpcgOptions = LobpcgOp
     prec = options.preconditioner.handle if options.preconditioner is not None else None
     _check(lib.cieg_lobpcg_solve(dev.handle, dm.handle, _ptr(x0), x0.shape[1], prec, C.byref(opt), cb, None,
                                  C.byref(rep)))
+    return _read_report(lib, rep, h.dim)
+
+
+def _read_report(lib, rep, nrows: int) -> SolveReport:
     try:
         conv, iters, kw, kt = C.c_int(), C.c_int(), C.c_uint32(), C.c_uint32()
         ne, nh = C.c_double(), C.c_uint64()
@@ -638,7 +642,7 @@ def lobpcg_solve(h: CsbMatrix, x0: np.ndarray, options: LobpcgOptions = LobpcgOp
         _check(lib.cieg_report_counters(rep, _ptr(cnt, C.c_uint64)))
         ev = np.zeros(kw.value)
         _check(lib.cieg_report_eigenvalues(rep, _ptr(ev)))
-        trial = np.zeros((h.dim, kt.value))
+        trial = np.zeros((nrows, kt.value))
         _check(lib.cieg_report_trial_vectors(rep, _ptr(trial)))
         n = nh.value
         hi, hc = np.zeros(n, np.int32), np.zeros(n, np.int32)

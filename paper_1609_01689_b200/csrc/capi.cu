@@ -59,7 +59,8 @@ int cieg_ctx_create(int device, cieg_ctx** out) {
     if (prop.major != 10)
       cieg::fail(CIEG_ERR_CUDA, std::string("libcieg is built for sm_100a; device is ") + prop.name);
     c->sm_count = prop.multiProcessorCount;
-    CIEG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CIEG_CUDA(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
     *out = c;
   });
 }
@@ -73,7 +74,8 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   ctx->scratch_red.release();
   ctx->scratch_small.release();
   ctx->pinned_small.release();
-  cudaStreamDestroy(ctx->stream);
+  cudaStreamSynchronize(ctx->own_stream);
+  cudaStreamDestroy(ctx->own_stream);
   delete ctx;
   return CIEG_OK;
 }
@@ -88,60 +90,124 @@ int cieg_ctx_synchronize(cieg_ctx* ctx) {
 void* cieg_ctx_stream(cieg_ctx* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+}  // extern "C"
+
+namespace {
+
+std::uint32_t choose_tile_edge(const cieg_csb_view* csb, const uint32_t* group_bounds, uint32_t ngroups,
+                               uint32_t tile_edge) {
+  std::uint32_t te = tile_edge;
+  if (te == 0) {
+    // Tile edge follows the group size: 64-row groups -> 64, else 128.
+    te = 128;
+    if (group_bounds && ngroups > 0) {
+      std::uint32_t mx = 0;
+      for (std::uint32_t g = 0; g < ngroups; ++g) mx = std::max(mx, group_bounds[g + 1] - group_bounds[g]);
+      if (mx <= 64) te = 64;
+    }
+  }
+  if (te != 64 && te != 128) cieg::fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
+  if (csb->precision == 1) te = 64;  // fp64 dense tiles: 64 rows keep two buffers in shared memory
+  return te;
+}
+
+cieg_mat* upload_tiles(cieg_ctx* ctx, cieg::HostTiles& ht) {
+  cieg::build_schedule(ht, static_cast<std::uint32_t>(ctx->sm_count));
+  auto* m = new cieg_mat;
+  try {
+    m->ctx = ctx;
+    m->dim = ht.dim;
+    m->tile_edge = ht.tile_edge;
+    m->precision = ht.precision;
+    m->nnz = ht.nnz;
+    m->npanels = ht.npanels();
+    m->ntiles = ht.ntiles();
+    m->row_lo = ht.row_lo;
+    m->row_hi = ht.row_hi;
+    m->halo_lo = ht.halo_lo;
+    m->halo_hi = ht.halo_hi;
+    m->panel_start_host = ht.panel_start;
+    m->panel_start = cieg::upload_vec(ht.panel_start);
+    m->tile_off = cieg::upload_vec(ht.tile_off);
+    m->idx = cieg::upload_vec(ht.idx);
+    if (ht.precision == 0)
+      m->val = cieg::upload_vec(ht.val32);
+    else
+      m->val = cieg::upload_vec(ht.val64);
+    m->work_off = cieg::upload_vec(ht.work_off);
+    m->work_tile = cieg::upload_vec(ht.work_tile);
+    m->work_other = cieg::upload_vec(ht.work_other);
+    m->work_kind = cieg::upload_vec(ht.work_kind);
+    m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
+    m->sched_off = cieg::upload_vec(ht.sched_off);
+    m->sched = cieg::upload_vec(ht.sched);
+    m->tile_bytes = ht.tile_off.back() * (4 + (ht.precision == 0 ? 4 : 8));
+  } catch (...) {
+    delete m;
+    throw;
+  }
+  return m;
+}
+
+}  // namespace
+
+extern "C" {
+
 int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
                        uint32_t ngroups, uint32_t tile_edge, cieg_mat** out) {
   return cieg::guarded([&] {
     if (!ctx || !csb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_upload: null argument");
-    if (csb->precision != 0 && csb->precision != 1)
-      cieg::fail(CIEG_ERR_FORMAT, "bad precision tag");
+    if (csb->precision != 0 && csb->precision != 1) cieg::fail(CIEG_ERR_FORMAT, "bad precision tag");
     CIEG_CUDA(cudaSetDevice(ctx->device));
-    std::uint32_t te = tile_edge;
-    if (te == 0) {
-      // Tile edge follows the group size: 64-row groups -> 64, else 128.
-      te = 128;
-      if (group_bounds && ngroups > 0) {
-        std::uint32_t mx = 0;
-        for (std::uint32_t g = 0; g < ngroups; ++g) mx = std::max(mx, group_bounds[g + 1] - group_bounds[g]);
-        if (mx <= 64) te = 64;
-      }
-    }
-    if (te != 64 && te != 128) cieg::fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
-    if (csb->precision == 1) te = 64;  // fp64 dense tiles: 64 rows keep two buffers in shared memory
+    const std::uint32_t te = choose_tile_edge(csb, group_bounds, ngroups, tile_edge);
     std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te);
     cieg::HostTiles ht;
     cieg::build_tiles(*csb, panels, te, ht);
-    cieg::build_schedule(ht, static_cast<std::uint32_t>(ctx->sm_count));
+    *out = upload_tiles(ctx, ht);
+  });
+}
 
-    auto* m = new cieg_mat;
-    try {
-      m->ctx = ctx;
-      m->dim = ht.dim;
-      m->tile_edge = te;
-      m->precision = ht.precision;
-      m->nnz = ht.nnz;
-      m->npanels = ht.npanels();
-      m->ntiles = ht.ntiles();
-      m->panel_start_host = ht.panel_start;
-      m->panel_start = cieg::upload_vec(ht.panel_start);
-      m->tile_off = cieg::upload_vec(ht.tile_off);
-      m->idx = cieg::upload_vec(ht.idx);
-      if (ht.precision == 0)
-        m->val = cieg::upload_vec(ht.val32);
-      else
-        m->val = cieg::upload_vec(ht.val64);
-      m->work_off = cieg::upload_vec(ht.work_off);
-      m->work_tile = cieg::upload_vec(ht.work_tile);
-      m->work_other = cieg::upload_vec(ht.work_other);
-      m->work_kind = cieg::upload_vec(ht.work_kind);
-      m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
-      m->sched_off = cieg::upload_vec(ht.sched_off);
-      m->sched = cieg::upload_vec(ht.sched);
-      m->tile_bytes = ht.tile_off.back() * (4 + (ht.precision == 0 ? 4 : 8));
-    } catch (...) {
-      delete m;
-      throw;
-    }
-    *out = m;
+int cieg_matrix_upload_shard(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                             uint32_t ngroups, uint32_t tile_edge, uint32_t row_lo, uint32_t row_hi,
+                             cieg_mat** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !csb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_upload_shard: null argument");
+    if (csb->precision != 0 && csb->precision != 1) cieg::fail(CIEG_ERR_FORMAT, "bad precision tag");
+    if (row_lo >= row_hi || row_hi > csb->dim) cieg::fail(CIEG_ERR_DIMENSION, "shard rows outside [0, dim)");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    const std::uint32_t te = choose_tile_edge(csb, group_bounds, ngroups, tile_edge);
+    std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te);
+    cieg::HostTiles ht;
+    cieg::build_tiles(*csb, panels, te, ht);
+    cieg::restrict_to_rows(ht, row_lo, row_hi);
+    *out = upload_tiles(ctx, ht);
+  });
+}
+
+int cieg_matrix_rows(const cieg_mat* m, uint32_t* row_lo, uint32_t* row_hi, uint32_t* halo_lo, uint32_t* halo_hi) {
+  return cieg::guarded([&] {
+    if (!m) cieg::fail(CIEG_ERR_ARGUMENT, "null matrix");
+    if (row_lo) *row_lo = m->row_lo;
+    if (row_hi) *row_hi = m->row_hi;
+    if (halo_lo) *halo_lo = m->halo_lo;
+    if (halo_hi) *halo_hi = m->halo_hi;
+  });
+}
+
+int cieg_shard_plan(const cieg_csb_view* csb, const uint32_t* group_bounds, uint32_t ngroups, uint32_t tile_edge,
+                    uint32_t nranks, uint32_t* row_bounds, uint32_t* halo_lo, uint32_t* halo_hi) {
+  return cieg::guarded([&] {
+    if (!csb || !row_bounds || !halo_lo || !halo_hi) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_shard_plan: null argument");
+    const std::uint32_t te = choose_tile_edge(csb, group_bounds, ngroups, tile_edge);
+    cieg::shard_plan(*csb, group_bounds, ngroups, te, nranks, row_bounds, halo_lo, halo_hi);
+  });
+}
+
+int cieg_ctx_set_stream(cieg_ctx* ctx, void* stream) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
   });
 }
 
@@ -177,18 +243,20 @@ int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y
   });
 }
 
+
 int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
                    uint32_t m) {
   return cieg::guarded([&] {
     if (!ctx || !mat) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host: null handle");
-    const std::size_t bytes = static_cast<std::size_t>(mat->dim) * m * sizeof(double);
-    if (bytes == 0) return;
+    const std::size_t xbytes = static_cast<std::size_t>(mat->dim) * m * sizeof(double);
+    const std::size_t ybytes = static_cast<std::size_t>(mat->row_hi - mat->row_lo) * m * sizeof(double);
+    if (xbytes == 0) return;
     if (!x_host || !y_host) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host: null vector");
-    double* dx = static_cast<double*>(ctx->scratch_x.get(bytes));
-    double* dy = static_cast<double*>(ctx->scratch_y.get(bytes));
-    CIEG_CUDA(cudaMemcpyAsync(dx, x_host, bytes, cudaMemcpyHostToDevice, ctx->stream));
+    double* dx = static_cast<double*>(ctx->scratch_x.get(xbytes));
+    double* dy = static_cast<double*>(ctx->scratch_y.get(ybytes));
+    CIEG_CUDA(cudaMemcpyAsync(dx, x_host, xbytes, cudaMemcpyHostToDevice, ctx->stream));
     cieg::launch_spmm(ctx, mat, dx, m, dy, m, m);
-    CIEG_CUDA(cudaMemcpyAsync(y_host, dy, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaMemcpyAsync(y_host, dy, ybytes, cudaMemcpyDeviceToHost, ctx->stream));
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

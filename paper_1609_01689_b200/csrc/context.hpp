@@ -61,7 +61,8 @@ struct PinnedBuf {
 
 struct cieg_ctx {
   int device = 0;
-  cudaStream_t stream = nullptr;
+  cudaStream_t stream = nullptr;      // stream all work is enqueued on
+  cudaStream_t own_stream = nullptr;  // the context's own stream
   std::uint64_t launches = 0;
   int sm_count = 148;
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
@@ -87,6 +88,7 @@ struct cieg_mat {
   std::uint32_t* work_tile = nullptr;
   std::uint32_t* work_other = nullptr;
   std::uint32_t* work_kind = nullptr;
+  std::uint32_t row_lo = 0, row_hi = 0, halo_lo = 0, halo_hi = 0;  // owner rows / X rows read
   std::uint32_t sched_ctas = 0;
   std::uint32_t* sched_off = nullptr;
   std::uint32_t* sched = nullptr;

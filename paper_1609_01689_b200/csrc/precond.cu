@@ -570,42 +570,75 @@ int cieg_precond_upload(cieg_ctx* ctx, const cieg_tilediag_view* t, cieg_prec** 
   });
 }
 
+}  // extern "C"
+
+namespace {
+
 // ci::extract_tile_diagonal (hamiltonian.cpp:178-203): dense f64 blocks from
-// the diagonal CSB blocks, mirrored.
+// the diagonal CSB blocks, mirrored; restricted to the groups inside
+// [row_lo, row_hi) with local row numbering (a shard's preconditioner).
+cieg_prec* prec_from_csb(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* gb, uint32_t ng, uint32_t row_lo,
+                         uint32_t row_hi) {
+  const std::uint32_t dim = csb->dim;
+  if (gb[0] != 0 || gb[ng] != dim) cieg::fail(CIEG_ERR_DIMENSION, "group bounds do not cover [0, dim)");
+  std::uint32_t g0 = 0, g1 = 0;
+  while (g0 < ng && gb[g0] < row_lo) ++g0;
+  g1 = g0;
+  while (g1 < ng && gb[g1 + 1] <= row_hi) ++g1;
+  if (gb[g0] != row_lo || gb[g1] != row_hi) cieg::fail(CIEG_ERR_CONFIG, "shard rows are not group boundaries");
+  const std::uint32_t lng = g1 - g0;
+  std::vector<std::uint32_t> lb(lng + 1);
+  for (std::uint32_t g = 0; g <= lng; ++g) lb[g] = gb[g0 + g] - row_lo;
+  std::vector<std::uint32_t> group_of(dim, 0xffffffffu);
+  std::vector<std::uint64_t> off(lng + 1, 0);
+  for (std::uint32_t g = 0; g < lng; ++g) {
+    const std::uint64_t sz = lb[g + 1] - lb[g];
+    off[g + 1] = off[g] + sz * sz;
+    for (std::uint32_t r = gb[g0 + g]; r < gb[g0 + g + 1]; ++r) group_of[r] = g;
+  }
+  std::vector<double> blocks(off[lng], 0.0);
+  const float* v32 = static_cast<const float*>(csb->values);
+  const double* v64 = static_cast<const double*>(csb->values);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (std::int64_t i64 = 0; i64 < static_cast<std::int64_t>(csb->nb); ++i64) {
+    const std::uint32_t i = static_cast<std::uint32_t>(i64);
+    const std::uint32_t base = csb->block_boundaries[i];
+    if (csb->block_boundaries[i + 1] <= row_lo || base >= row_hi) continue;
+    const std::uint64_t bid = static_cast<std::uint64_t>(i) * (i + 1) / 2 + i;
+    for (std::uint64_t e = csb->entry_offsets[bid]; e < csb->entry_offsets[bid + 1]; ++e) {
+      const std::uint32_t r = base + csb->rows[e], c = base + csb->cols[e];
+      const std::uint32_t g = group_of[r];
+      if (g == 0xffffffffu || group_of[c] != g) continue;
+      const std::uint32_t s = gb[g0 + g];
+      const std::uint64_t n = lb[g + 1] - lb[g];
+      const double v = csb->precision == 0 ? static_cast<double>(v32[e]) : v64[e];
+      blocks[off[g] + (r - s) + (c - s) * n] = v;
+      blocks[off[g] + (c - s) + (r - s) * n] = v;
+    }
+  }
+  return make_prec(ctx, row_hi - row_lo, lng, lb.data(), blocks.data());
+}
+
+}  // namespace
+
+extern "C" {
+
 int cieg_precond_from_csb(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* gb, uint32_t ng,
                           cieg_prec** out) {
   return cieg::guarded([&] {
     if (!ctx || !csb || !gb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_precond_from_csb: null argument");
     CIEG_CUDA(cudaSetDevice(ctx->device));
-    const std::uint32_t dim = csb->dim;
-    if (gb[0] != 0 || gb[ng] != dim) cieg::fail(CIEG_ERR_DIMENSION, "group bounds do not cover [0, dim)");
-    std::vector<std::uint32_t> group_of(dim);
-    std::vector<std::uint64_t> off(ng + 1, 0);
-    for (std::uint32_t g = 0; g < ng; ++g) {
-      const std::uint64_t sz = gb[g + 1] - gb[g];
-      off[g + 1] = off[g] + sz * sz;
-      for (std::uint32_t r = gb[g]; r < gb[g + 1]; ++r) group_of[r] = g;
-    }
-    std::vector<double> blocks(off[ng], 0.0);
-    const float* v32 = static_cast<const float*>(csb->values);
-    const double* v64 = static_cast<const double*>(csb->values);
-#pragma omp parallel for schedule(dynamic, 1)
-    for (std::int64_t i64 = 0; i64 < static_cast<std::int64_t>(csb->nb); ++i64) {
-      const std::uint32_t i = static_cast<std::uint32_t>(i64);
-      const std::uint64_t bid = static_cast<std::uint64_t>(i) * (i + 1) / 2 + i;
-      const std::uint32_t base = csb->block_boundaries[i];
-      for (std::uint64_t e = csb->entry_offsets[bid]; e < csb->entry_offsets[bid + 1]; ++e) {
-        const std::uint32_t r = base + csb->rows[e], c = base + csb->cols[e];
-        const std::uint32_t g = group_of[r];
-        if (group_of[c] != g) continue;
-        const std::uint32_t s = gb[g];
-        const std::uint64_t n = gb[g + 1] - s;
-        const double v = csb->precision == 0 ? static_cast<double>(v32[e]) : v64[e];
-        blocks[off[g] + (r - s) + (c - s) * n] = v;
-        blocks[off[g] + (c - s) + (r - s) * n] = v;
-      }
-    }
-    *out = make_prec(ctx, dim, ng, gb, blocks.data());
+    *out = prec_from_csb(ctx, csb, gb, ng, 0, csb->dim);
+  });
+}
+
+int cieg_precond_from_csb_range(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* gb, uint32_t ng,
+                                uint32_t row_lo, uint32_t row_hi, cieg_prec** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !csb || !gb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_precond_from_csb_range: null argument");
+    if (row_lo >= row_hi || row_hi > csb->dim) cieg::fail(CIEG_ERR_DIMENSION, "range outside [0, dim)");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    *out = prec_from_csb(ctx, csb, gb, ng, row_lo, row_hi);
   });
 }
 

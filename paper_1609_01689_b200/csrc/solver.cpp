@@ -145,12 +145,13 @@ enum Phase { kSpmm = 0, kRR = 1, kOrtho = 2, kPrecond = 3, kResid = 4, kOther = 
 class Solver {
  public:
   Solver(cieg_ctx* ctx, const cieg_mat* mat, const cieg_prec* prec, const cieg_lobpcg_options& opt,
-         cieg_report& rep)
-      : ctx_(ctx), mat_(mat), prec_(prec), opt_(opt), rep_(rep), n_(mat->dim) {
+         cieg_report& rep, const cieg_dist_hooks* hooks = nullptr)
+      : ctx_(ctx), mat_(mat), prec_(prec), opt_(opt), rep_(rep), n_(mat->row_hi - mat->row_lo), hooks_(hooks) {
     ws_.n = n_;
   }
 
   void run(const double* x0_host, std::uint32_t kt0, cieg_observer_fn obs, void* user);
+  ~Solver() { xfull_.release(); }
 
  private:
   // orthonormalize (lobpcg.cpp:89-119). `v` holds the input (width v.w) and is
@@ -161,10 +162,22 @@ class Solver {
     Clock c(ctx_, &rep_.timing_ms[kSpmm]);
     ++rep_.counters[0];
     rep_.counters[1] += x.w;
-    launch_spmm(ctx_, mat_, x.p, x.w, hx.p, x.w, x.w);
+    const double* xin = x.p;
+    if (hooks_) {  // sharded: gather every rank's rows of X (the owner kernel reads its halo)
+      double* full = static_cast<double*>(xfull_.get(sizeof(double) * mat_->dim * std::max<std::uint32_t>(x.w, 1)));
+      if (hooks_->allgather_rows(hooks_->user, x.p, x.w, full) != 0)
+        fail(CIEG_ERR_ARGUMENT, "allgather_rows hook failed");
+      xin = full;
+    }
+    launch_spmm(ctx_, mat_, xin, x.w, hx.p, x.w, x.w);
     hx.w = x.w;
   }
-  Mat gram(const View3& l, const View3& r) { return cieg::gram(ctx_, n_, l, r); }
+  Mat gram(const View3& l, const View3& r) {
+    Mat g = cieg::gram(ctx_, n_, l, r);
+    if (hooks_ && !g.empty() && hooks_->allreduce_sum(hooks_->user, g.data(), g.size()) != 0)
+      fail(CIEG_ERR_ARGUMENT, "allreduce_sum hook failed");
+    return g;
+  }
   void clean_p_block(double drop_tol);
 
   cieg_ctx* ctx_;
@@ -172,7 +185,9 @@ class Solver {
   const cieg_prec* prec_;
   cieg_lobpcg_options opt_;
   cieg_report& rep_;
-  std::uint32_t n_;
+  std::uint32_t n_;  // local rows (all rows unless sharded)
+  const cieg_dist_hooks* hooks_;
+  DevBuf xfull_;
   Workspace ws_;
   Block x_, hx_, p_, hp_, x2_, hx2_, p2_, hp2_, w_, hw_, wtmp_, r_, wsrc_;
   std::vector<double> theta_;
@@ -455,13 +470,33 @@ int cieg_lobpcg_solve(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host,
                       void* observer_user, cieg_report** out) {
   return cieg::guarded([&] {
     if (!ctx || !mat || !x0_host || !opt || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_lobpcg_solve: null argument");
-    if (prec && prec->dim != mat->dim)
+    if (prec && prec->dim != mat->row_hi - mat->row_lo)
       cieg::fail(CIEG_ERR_DIMENSION, "apply_preconditioner: tiles do not cover the basis");
+    if (mat->row_lo != 0 || mat->row_hi != mat->dim)
+      cieg::fail(CIEG_ERR_CONFIG, "cieg_lobpcg_solve needs the whole matrix; use cieg_lobpcg_solve_dist for a shard");
     CIEG_CUDA(cudaSetDevice(ctx->device));
     auto rep = std::make_unique<cieg_report>();
     {
       cieg::Solver s(ctx, mat, prec, *opt, *rep);
       s.run(x0_host, kt, observer, observer_user);
+    }
+    *out = rep.release();
+  });
+}
+
+int cieg_lobpcg_solve_dist(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
+                           const cieg_prec* prec, const cieg_lobpcg_options* opt, const cieg_dist_hooks* hooks,
+                           cieg_report** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat || !x0_host || !opt || !hooks || !out || !hooks->allreduce_sum || !hooks->allgather_rows)
+      cieg::fail(CIEG_ERR_ARGUMENT, "cieg_lobpcg_solve_dist: null argument");
+    if (prec && prec->dim != mat->row_hi - mat->row_lo)
+      cieg::fail(CIEG_ERR_DIMENSION, "apply_preconditioner: tiles do not cover the basis");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    auto rep = std::make_unique<cieg_report>();
+    {
+      cieg::Solver s(ctx, mat, prec, *opt, *rep, hooks);
+      s.run(x0_host, kt, nullptr, nullptr);
     }
     *out = rep.release();
   });

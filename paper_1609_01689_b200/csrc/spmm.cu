@@ -51,6 +51,7 @@ struct SpmmArgs {
   const double* x;
   double* y;
   std::uint32_t ldx, ldy, mcols, npanels;
+  std::uint32_t row_base;  // first owner row of a shard (U is written shard-local)
 };
 
 constexpr int kProducerWarps = 8;
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         for (int j = 0; j < S::kMT; ++j) {
           const int row = m_base + 8 * j + g;
           if (row >= prow) continue;
-          double* yr = a.y + static_cast<std::size_t>(r0 + row) * a.ldy;
+          double* yr = a.y + static_cast<std::size_t>(r0 - a.row_base + row) * a.ldy;
 #pragma unroll
           for (int n = 0; n < NT; ++n) {
             const int c = 8 * n + 2 * q;
@@ -384,7 +385,8 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   ldx,
                   ldy,
                   mc,
-                  m->npanels};
+                  m->npanels,
+                  m->row_lo};
     if (m->precision == 0) {
       if (m->tile_edge == 64)
         dispatch_nt<float, 64>(ctx, m, args, mc);

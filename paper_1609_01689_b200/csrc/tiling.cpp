@@ -128,6 +128,10 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
 
   out = HostTiles{};
   out.dim = dim;
+  out.row_lo = 0;
+  out.row_hi = dim;
+  out.halo_lo = 0;
+  out.halo_hi = dim;
   out.tile_edge = te;
   out.precision = csb.precision;
   out.panel_start = panels;
@@ -206,34 +210,40 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
 }
 
 void build_schedule(HostTiles& t, std::uint32_t ctas) {
-  const std::uint32_t np = t.npanels();
+  // owner panels of this tiling (all of them unless restricted to a shard)
+  const std::uint32_t p_lo = static_cast<std::uint32_t>(
+      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), t.row_lo) - t.panel_start.begin());
+  const std::uint32_t p_hi = static_cast<std::uint32_t>(
+      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), t.row_hi) - t.panel_start.begin());
+  const std::uint32_t np = p_hi - p_lo;
   ctas = std::max<std::uint32_t>(1, std::min<std::uint32_t>(ctas, np));
   // cost of a panel = entry quads of its work items + a fixed per-item charge
   std::vector<std::pair<std::uint64_t, std::uint32_t>> cost(np);
-  for (std::uint32_t P = 0; P < np; ++P) {
+  for (std::uint32_t i = 0; i < np; ++i) {
+    const std::uint32_t P = p_lo + i;
     std::uint64_t c = 0;
     for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w) {
       const std::uint32_t tile = t.work_tile[w];
       c += (t.tile_off[tile + 1] - t.tile_off[tile]) / 4 + 256;
     }
-    cost[P] = {c, P};
+    cost[i] = {c, P};
   }
   std::vector<std::uint32_t> order(np);
   std::iota(order.begin(), order.end(), 0u);
   std::stable_sort(order.begin(), order.end(), [&](std::uint32_t a, std::uint32_t b) {
     return cost[a].first > cost[b].first;
-  });
+  });  // order holds local indices i; panel = p_lo + i
   // min-heap of (load, cta)
   std::vector<std::pair<std::uint64_t, std::uint32_t>> heap;
   for (std::uint32_t b = 0; b < ctas; ++b) heap.push_back({0, b});
   auto cmp = [](const auto& x, const auto& y) { return x.first != y.first ? x.first > y.first : x.second > y.second; };
   std::make_heap(heap.begin(), heap.end(), cmp);
   std::vector<std::vector<std::uint32_t>> panels_of(ctas);
-  for (std::uint32_t P : order) {
+  for (std::uint32_t i : order) {
     std::pop_heap(heap.begin(), heap.end(), cmp);
     auto& top = heap.back();
-    panels_of[top.second].push_back(P);
-    top.first += cost[P].first;
+    panels_of[top.second].push_back(p_lo + i);
+    top.first += cost[i].first;
     std::push_heap(heap.begin(), heap.end(), cmp);
   }
   t.sched_off.assign(ctas + 1, 0);
@@ -259,6 +269,143 @@ void build_schedule(HostTiles& t, std::uint32_t ctas) {
       }
     }
     t.sched_off[b + 1] = static_cast<std::uint32_t>(t.sched.size() / 8);
+  }
+}
+
+void restrict_to_rows(HostTiles& t, std::uint32_t row_lo, std::uint32_t row_hi) {
+  const std::uint32_t np = t.npanels();
+  const std::uint32_t p_lo = static_cast<std::uint32_t>(
+      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), row_lo) - t.panel_start.begin());
+  const std::uint32_t p_hi = static_cast<std::uint32_t>(
+      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), row_hi) - t.panel_start.begin());
+  if (p_lo > np || p_hi > np || t.panel_start[p_lo] != row_lo || t.panel_start[p_hi] != row_hi)
+    fail(CIEG_ERR_CONFIG, "shard bounds are not panel boundaries");
+  // tiles referenced by owned work items, in first-use order
+  std::vector<std::int64_t> remap(t.ntiles(), -1);
+  std::vector<std::uint64_t> keep;
+  std::uint32_t hlo = row_lo, hhi = row_hi;
+  for (std::uint32_t P = p_lo; P < p_hi; ++P)
+    for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w) {
+      const std::uint32_t tile = t.work_tile[w];
+      if (remap[tile] < 0) {
+        remap[tile] = static_cast<std::int64_t>(keep.size());
+        keep.push_back(tile);
+      }
+      const std::uint32_t o = t.work_other[w];
+      hlo = std::min(hlo, t.panel_start[o]);
+      hhi = std::max(hhi, t.panel_start[o + 1]);
+    }
+  HostTiles r;
+  r.dim = t.dim;
+  r.tile_edge = t.tile_edge;
+  r.precision = t.precision;
+  r.panel_start = t.panel_start;
+  r.tile_off.assign(1, 0);
+  for (std::uint64_t k : keep) {
+    r.tile_pi.push_back(t.tile_pi[k]);
+    r.tile_pj.push_back(t.tile_pj[k]);
+    r.tile_off.push_back(r.tile_off.back() + (t.tile_off[k + 1] - t.tile_off[k]));
+  }
+  const std::uint64_t slots = r.tile_off.back();
+  r.idx.resize(slots);
+  if (t.precision == 0)
+    r.val32.resize(slots);
+  else
+    r.val64.resize(slots);
+  r.nnz = 0;
+#pragma omp parallel for schedule(dynamic, 64)
+  for (std::int64_t j = 0; j < static_cast<std::int64_t>(keep.size()); ++j) {
+    const std::uint64_t k = keep[j];
+    const std::uint64_t n = t.tile_off[k + 1] - t.tile_off[k];
+    std::memcpy(r.idx.data() + r.tile_off[j], t.idx.data() + t.tile_off[k], n * sizeof(std::uint32_t));
+    if (t.precision == 0)
+      std::memcpy(r.val32.data() + r.tile_off[j], t.val32.data() + t.tile_off[k], n * sizeof(float));
+    else
+      std::memcpy(r.val64.data() + r.tile_off[j], t.val64.data() + t.tile_off[k], n * sizeof(double));
+  }
+  for (std::uint64_t k : keep) {
+    // count real (non-sentinel) entries
+    const std::uint32_t te = t.tile_edge;
+    const std::uint32_t sentinel = te | (te << 16);
+    for (std::uint64_t e = t.tile_off[k]; e < t.tile_off[k + 1]; ++e) r.nnz += t.idx[e] != sentinel;
+  }
+  r.work_off.assign(np + 1, 0);
+  for (std::uint32_t P = 0; P < np; ++P) {
+    const std::uint32_t cnt = (P >= p_lo && P < p_hi) ? t.work_off[P + 1] - t.work_off[P] : 0;
+    r.work_off[P + 1] = r.work_off[P] + cnt;
+  }
+  for (std::uint32_t P = p_lo; P < p_hi; ++P)
+    for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w) {
+      r.work_tile.push_back(static_cast<std::uint32_t>(remap[t.work_tile[w]]));
+      r.work_other.push_back(t.work_other[w]);
+      r.work_kind.push_back(t.work_kind[w]);
+    }
+  r.row_lo = row_lo;
+  r.row_hi = row_hi;
+  r.halo_lo = hlo;
+  r.halo_hi = hhi;
+  t = std::move(r);
+}
+
+void shard_plan(const cieg_csb_view& csb, const std::uint32_t* gb, std::uint32_t ng, std::uint32_t te,
+                std::uint32_t nranks, std::uint32_t* row_bounds, std::uint32_t* halo_lo, std::uint32_t* halo_hi) {
+  if (nranks == 0) fail(CIEG_ERR_CONFIG, "shard_plan: nranks must be positive");
+  const std::uint32_t dim = csb.dim;
+  // per-row streamed entries: row part + transposed part
+  std::vector<std::uint64_t> cost(dim + 1, 0);
+  const float* v32 = nullptr;
+  (void)v32;
+  for (std::uint32_t bi = 0; bi < csb.nb; ++bi) {
+    const std::uint32_t rb = csb.block_boundaries[bi];
+    for (std::uint32_t bj = 0; bj <= bi; ++bj) {
+      const std::uint64_t b = static_cast<std::uint64_t>(bi) * (bi + 1) / 2 + bj;
+      const std::uint32_t cb = csb.block_boundaries[bj];
+      for (std::uint64_t e = csb.entry_offsets[b]; e < csb.entry_offsets[b + 1]; ++e) {
+        const std::uint32_t r = rb + csb.rows[e], c = cb + csb.cols[e];
+        ++cost[r];
+        if (c != r) ++cost[c];
+      }
+    }
+  }
+  std::vector<std::uint32_t> cuts;  // candidate cut rows = group boundaries
+  if (gb && ng) {
+    if (gb[0] != 0 || gb[ng] != dim) fail(CIEG_ERR_DIMENSION, "group bounds do not cover [0, dim)");
+    cuts.assign(gb, gb + ng + 1);
+  } else {
+    for (std::uint32_t r = 0; r <= dim; r += te) cuts.push_back(r);
+    if (cuts.back() != dim) cuts.push_back(dim);
+  }
+  std::vector<std::uint64_t> pre(dim + 1, 0);
+  for (std::uint32_t r = 0; r < dim; ++r) pre[r + 1] = pre[r] + cost[r];
+  const std::uint64_t total = pre[dim];
+  row_bounds[0] = 0;
+  std::size_t ci = 0;
+  for (std::uint32_t k = 1; k < nranks; ++k) {
+    const long double target = static_cast<long double>(total) * k / nranks;
+    while (ci + 1 < cuts.size() && pre[cuts[ci + 1]] <= target) ++ci;
+    std::uint32_t cut = cuts[ci];
+    if (ci + 1 < cuts.size() && (target - pre[cuts[ci]]) > (pre[cuts[ci + 1]] - target)) cut = cuts[ci + 1];
+    cut = std::max(cut, row_bounds[k - 1]);
+    row_bounds[k] = cut;
+  }
+  row_bounds[nranks] = dim;
+  // halos from the device panel grid of a full tiling
+  std::vector<std::uint32_t> panels = plan_panels(dim, gb, ng, te);
+  HostTiles t;
+  build_tiles(csb, panels, te, t);
+  for (std::uint32_t k = 0; k < nranks; ++k) {
+    const std::uint32_t lo = row_bounds[k], hi = row_bounds[k + 1];
+    std::uint32_t hl = lo, hh = hi;
+    for (std::uint32_t P = 0; P < t.npanels(); ++P) {
+      if (t.panel_start[P] < lo || t.panel_start[P + 1] > hi) continue;
+      for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w) {
+        const std::uint32_t o = t.work_other[w];
+        hl = std::min(hl, t.panel_start[o]);
+        hh = std::max(hh, t.panel_start[o + 1]);
+      }
+    }
+    halo_lo[k] = hl;
+    halo_hi[k] = hh;
   }
 }
 

@@ -47,6 +47,9 @@ struct HostTiles {
   std::vector<std::uint32_t> sched_off;
   std::vector<std::uint32_t> sched;  // 8 words per item, see ItemDesc in spmm.cu
 
+  // owner rows of this (shard) tiling and the X rows its SpMM reads
+  std::uint32_t row_lo = 0, row_hi = 0, halo_lo = 0, halo_hi = 0;
+
   std::uint32_t npanels() const { return static_cast<std::uint32_t>(panel_start.size() - 1); }
   std::uint64_t ntiles() const { return tile_pi.size(); }
 };
@@ -66,5 +69,16 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
 // each CTA's item descriptors: {q0 lo/hi, q1 lo/hi, kind | first << 8 |
 // last << 9, other-panel start row, other-panel rows, owner panel}.
 void build_schedule(HostTiles& t, std::uint32_t ctas);
+
+// Keep only what owner rows [row_lo, row_hi) need (panel-aligned bounds):
+// their work lists and the tiles those reference (re-indexed), and record the
+// X halo. Other panels keep empty work lists.
+void restrict_to_rows(HostTiles& t, std::uint32_t row_lo, std::uint32_t row_hi);
+
+// Row partition over nranks at group boundaries balanced by the entries each
+// owner streams (row part + transposed part); panel-expanded X halos.
+void shard_plan(const cieg_csb_view& csb, const std::uint32_t* group_bounds, std::uint32_t ngroups,
+                std::uint32_t tile_edge, std::uint32_t nranks, std::uint32_t* row_bounds,
+                std::uint32_t* halo_lo, std::uint32_t* halo_hi);
 
 }  // namespace cieg

@@ -1,0 +1,102 @@
+"""The sharded GPU solver (cieg_lobpcg_solve_dist via dist.py): world 1 over
+NCCL, and world 2 as two processes sharing the one available B200 with gloo
+collectives (host-mediated: no kernel waits on another rank's kernel). Same
+iteration count and eigenvalues as the reference."""
+import os
+import socket
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, backend, name, out_q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    from conftest import gen_from
+    from paper_1609_01689_b200 import ci
+    from paper_1609_01689_b200 import dist as D
+
+    torch.cuda.set_device(0)
+    if backend == "nccl":
+        dist.init_process_group("nccl", rank=rank, world_size=world, device_id=torch.device("cuda", 0))
+    else:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        g = dict(np.load(os.path.join(ROOT, "tests", "golden", "lobpcg.npz")))
+        h = gen_from(g[f"{name}_params"])
+        k, kt, tol, pre, seed = g[f"{name}_meta"]
+        dev = ci.Device(0)
+        sm = D.ShardedMatrix(h, rank, world, dev)
+        x0 = ci.random_block(h.dim, int(kt), int(seed))[sm.row_lo:sm.row_hi]
+        prec = D.local_tile_diagonal(h, sm.row_lo, sm.row_hi, dev) if pre else None
+        # sharded SpMM against the single-GPU kernel
+        x = ci.random_block(h.dim, 7, 3)
+        y = sm.spmm(torch.from_numpy(x[sm.row_lo:sm.row_hi].copy()).cuda()).cpu().numpy()
+        yf = ci.spmm(h, x)[sm.row_lo:sm.row_hi]
+        res["spmm_rel"] = float(np.abs(y - yf).max() / np.abs(yf).max())
+        rep = D.lobpcg_solve_dist(sm, x0, ci.LobpcgOptions(k_want=int(k), tol=float(tol)), prec)
+        res["iterations"] = rep.iterations
+        res["eigenvalues"] = rep.eigenvalues.tolist()
+        res["counters"] = [rep.counters.spmm_calls, rep.counters.spmv_equivalents,
+                           rep.counters.precond_applications, rep.counters.orthogonalizations]
+        res["rows"] = rep.trial_vectors.shape[0]
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        res["error"] = repr(e) + traceback.format_exc()
+    finally:
+        dist.destroy_process_group()
+    out_q.put((rank, res))
+
+
+def _run(world, backend, name):
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, backend, name, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    return out
+
+
+@pytest.mark.timeout(400)
+@pytest.mark.parametrize("world,backend", [(1, "nccl"), (2, "gloo")])
+@pytest.mark.parametrize("name", ["sector_f64", "sector_f64_prec"])
+def test_sharded_solver_matches_reference(golden, world, backend, name):
+    out = _run(world, backend, name)
+    g = golden("lobpcg")
+    rows = 0
+    for rank in range(world):
+        res = out[rank]
+        assert "error" not in res, res.get("error")
+        assert res["spmm_rel"] < 1e-13
+        assert res["iterations"] == int(g[f"{name}_iterations"])
+        assert res["counters"] == g[f"{name}_counters"].tolist()
+        np.testing.assert_allclose(res["eigenvalues"], g[f"{name}_eigenvalues"], rtol=1e-10)
+        rows += res["rows"]
+    assert rows == int(g[f"{name}_params"][0])
+    assert all(out[r]["eigenvalues"] == out[0]["eigenvalues"] for r in range(world))
