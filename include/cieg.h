@@ -276,6 +276,23 @@ int cieg_host_csb_destroy(cieg_host_csb* h);
 int cieg_host_csb_view(const cieg_host_csb* h, cieg_csb_view* view, uint64_t* nnz);
 int cieg_host_csb_groups(const cieg_host_csb* h, const uint32_t** bounds, uint32_t* ngroups);
 
+/* The same generator run on the GPU, writing the device tile stream directly
+ * (no host CSB; bit-identical tile stream to cieg_matrix_upload of
+ * cieg_generate_csb). Owner rows [row_lo, row_hi) (0, 0 = all) for a shard;
+ * tile_edge 0 = choose. SURVEY.md 8(f) rank 1. */
+int cieg_generate_device(cieg_ctx* ctx, const cieg_gen_params* prm, uint32_t tile_edge, uint32_t row_lo,
+                         uint32_t row_hi, cieg_mat** out);
+/* Tile-diagonal preconditioner built on the device from the matrix's own
+ * diagonal tiles (groups = generator tiles) -- ci::extract_tile_diagonal
+ * (hamiltonian.cpp:178-203) without a host TileDiagonal; shard-local. */
+int cieg_precond_from_matrix(cieg_ctx* ctx, const cieg_mat* mat, cieg_prec** out);
+/* Borrowed group partition of a matrix (ngroups + 1 bounds; 0 groups when unknown). */
+int cieg_matrix_groups(const cieg_mat* mat, const uint32_t** bounds, uint32_t* ngroups);
+/* Copy the device tile stream to the host (tile_off: ntiles + 1; tile_pi/pj:
+ * ntiles; idx/val: tile_off[ntiles] slots); any pointer may be NULL. */
+int cieg_matrix_export(const cieg_mat* mat, uint64_t* tile_off, uint32_t* tile_pi, uint32_t* tile_pj,
+                       uint32_t* idx, void* val);
+
 /* ci::random_block (block_vectors.cpp:162-174): out n x k row-major,
  * entries 2*unit(hash3(seed, i, j)) - 1. */
 int cieg_random_block(uint32_t n, uint32_t k, uint64_t seed, double* out_host);

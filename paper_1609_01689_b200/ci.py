@@ -315,28 +315,68 @@ def load_csb(path: str) -> CsbMatrix:
 class DeviceMatrix:
     """H re-tiled and resident in HBM (cieg_mat)."""
 
-    def __init__(self, h: CsbMatrix, device: Optional[Device] = None, tile_edge: int = 0):
+    def __init__(self, h: Optional[CsbMatrix], device: Optional[Device] = None, tile_edge: int = 0,
+                 _handle: Optional[C.c_void_p] = None):
         self.device = device or Device.default()
         lib = _lib.load()
-        v = h.view()
-        handle = C.c_void_p()
-        gptr, ng = None, 0
-        if h.groups is not None:
-            g = np.ascontiguousarray(h.groups, dtype=np.uint32)
-            gptr, ng = _ptr(g, C.c_uint32), len(g) - 1
-        _check(lib.cieg_matrix_upload(self.device.handle, C.byref(v), gptr, ng, tile_edge, C.byref(handle)))
+        if _handle is None:
+            v = h.view()
+            handle = C.c_void_p()
+            gptr, ng = None, 0
+            if h.groups is not None:
+                g = np.ascontiguousarray(h.groups, dtype=np.uint32)
+                gptr, ng = _ptr(g, C.c_uint32), len(g) - 1
+            _check(lib.cieg_matrix_upload(self.device.handle, C.byref(v), gptr, ng, tile_edge, C.byref(handle)))
+        else:
+            handle = _handle
         self.handle = handle
         self._fin = weakref.finalize(self, lib.cieg_matrix_destroy, handle)
         info = [C.c_uint32(), C.c_uint64(), C.c_uint32(), C.c_uint64(), C.c_uint32(), C.c_int(), C.c_uint64()]
         _check(lib.cieg_matrix_info(handle, *[C.byref(x) for x in info]))
         (self.dim, self.nnz, self.npanels, self.ntiles, self.tile_edge, self.precision,
          self.tile_bytes) = [x.value for x in info]
+        rows = [C.c_uint32() for _ in range(4)]
+        _check(lib.cieg_matrix_rows(handle, *[C.byref(x) for x in rows]))
+        self.row_lo, self.row_hi, self.halo_lo, self.halo_hi = [x.value for x in rows]
+
+    @classmethod
+    def generate(cls, n, sectors, tile, p, q, seed=1, precision=0, beta=2000, band=2,
+                 device: Optional[Device] = None, tile_edge: int = 0, rows=None) -> "DeviceMatrix":
+        """The BASELINE generator run on the GPU (cieg_generate_device): the
+        tile stream is written in HBM directly, bit-identical to uploading
+        generate_sector_matrix(...). `rows` = (row_lo, row_hi) for a shard."""
+        dev = device or Device.default()
+        prm = gen_params(n, sectors, tile, p, q, seed, precision, beta, band)
+        lo, hi = (0, 0) if rows is None else rows
+        handle = C.c_void_p()
+        _check(_lib.load().cieg_generate_device(dev.handle, C.byref(prm), tile_edge, lo, hi, C.byref(handle)))
+        return cls(None, dev, _handle=handle)
+
+    def groups(self) -> np.ndarray:
+        b = C.POINTER(C.c_uint32)()
+        ng = C.c_uint32()
+        _check(_lib.load().cieg_matrix_groups(self.handle, C.byref(b), C.byref(ng)))
+        return np.ctypeslib.as_array(b, (ng.value + 1,)).copy() if ng.value else np.zeros(0, np.uint32)
+
+    def export(self):
+        """(tile_off, tile_pi, tile_pj, idx, val) of the device tile stream."""
+        to = np.zeros(self.ntiles + 1, np.uint64)
+        pi = np.zeros(self.ntiles, np.uint32)
+        pj = np.zeros(self.ntiles, np.uint32)
+        _check(_lib.load().cieg_matrix_export(self.handle, _ptr(to, C.c_uint64), None, None, None, None))
+        slots = int(to[-1])
+        idx = np.zeros(slots, np.uint32)
+        val = np.zeros(slots, np.float32 if self.precision == 0 else np.float64)
+        _check(_lib.load().cieg_matrix_export(self.handle, _ptr(to, C.c_uint64), _ptr(pi, C.c_uint32),
+                                              _ptr(pj, C.c_uint32), _ptr(idx, C.c_uint32),
+                                              val.ctypes.data_as(C.c_void_p)))
+        return to, pi, pj, idx, val
 
     def spmm_host(self, x: np.ndarray) -> np.ndarray:
         x = _f64(x)
         if x.ndim != 2 or x.shape[0] != self.dim:
             raise DimensionMismatch("spmm: vector dim != matrix dim")
-        y = np.empty_like(x)
+        y = np.empty((self.row_hi - self.row_lo, x.shape[1]))  # a shard returns its own rows
         _check(_lib.load().cieg_spmm_host(self.device.handle, self.handle, _ptr(x), _ptr(y), x.shape[1]))
         return y
 
@@ -525,6 +565,16 @@ def extract_tile_diagonal(h: CsbMatrix, groups=None, device: Optional[Device] = 
     return TileDiagonal(handle, g, dev)
 
 
+def tile_diagonal_from_matrix(dm: DeviceMatrix) -> TileDiagonal:
+    """Tile diagonal built on the device from the matrix's diagonal tiles
+    (cieg_precond_from_matrix; shard-local for a shard)."""
+    handle = C.c_void_p()
+    _check(_lib.load().cieg_precond_from_matrix(dm.device.handle, dm.handle, C.byref(handle)))
+    g = dm.groups().astype(np.int64)
+    lb = g[(g >= dm.row_lo) & (g <= dm.row_hi)] - dm.row_lo
+    return TileDiagonal(handle, lb.astype(np.uint32), dm.device)
+
+
 def apply_preconditioner(tiles: TileDiagonal, r: np.ndarray, plan: ShiftPlan,
                          config: PrecondConfig = PrecondConfig()) -> np.ndarray:
     """ci::apply_preconditioner (precond.cpp:160-207)."""
@@ -600,16 +650,17 @@ class LobpcgOptions:
 _TIMING_KEYS = ("spmm", "rayleigh_ritz", "orthonormalization", "preconditioner", "residual", "other", "total")
 
 
-def lobpcg_solve(h: CsbMatrix, x0: np.ndarray, options: LobpcgOptions = LobpcgOptions(),
+def lobpcg_solve(h, x0: np.ndarray, options: LobpcgOptions = LobpcgOptions(),
                  device: Optional[Device] = None) -> SolveReport:
-    """ci::lobpcg_solve (lobpcg.cpp:216-387) on the GPU."""
+    """ci::lobpcg_solve (lobpcg.cpp:216-387) on the GPU. `h` is a CsbMatrix
+    (uploaded once) or an already resident DeviceMatrix."""
     x0 = _f64(x0)
     if x0.shape[0] != h.dim:
         raise DimensionMismatch("lobpcg: X0 dim != matrix dim")
     if x0.shape[1] < options.k_want:
         raise ConfigError("lobpcg: trial width below k_want")
     lib = _lib.load()
-    dm = device_matrix(h, device)
+    dm = h if isinstance(h, DeviceMatrix) else device_matrix(h, device)
     dev = dm.device
     opt = _lib.LobpcgOptionsC()
     opt.k_want, opt.tol, opt.max_iter = options.k_want, options.tol, options.max_iter

@@ -40,6 +40,12 @@ class Config:
     def expected_nnz(self) -> float:
         return ci.expected_nnz(self.n, self.sectors, self.tile, self.p(), self.q)
 
+    def generate_device(self, device=None, rows=None, seed: int | None = None) -> "ci.DeviceMatrix":
+        """Generated on the GPU straight into the device tile stream."""
+        return ci.DeviceMatrix.generate(self.n, self.sectors, self.tile, self.p(), self.q,
+                                        self.seed if seed is None else seed, self.precision, self.beta,
+                                        device=device, rows=rows)
+
     def generate(self, seed: int | None = None) -> "ci.CsbMatrix":
         return ci.generate_sector_matrix(self.n, self.sectors, self.tile, self.p(), self.q,
                                          self.seed if seed is None else seed, self.precision, self.beta)

@@ -127,6 +127,9 @@ cieg_mat* upload_tiles(cieg_ctx* ctx, cieg::HostTiles& ht) {
     m->halo_lo = ht.halo_lo;
     m->halo_hi = ht.halo_hi;
     m->panel_start_host = ht.panel_start;
+    m->tile_pi_host = ht.tile_pi;
+    m->tile_pj_host = ht.tile_pj;
+    m->tile_off_host = ht.tile_off;
     m->panel_start = cieg::upload_vec(ht.panel_start);
     m->tile_off = cieg::upload_vec(ht.tile_off);
     m->idx = cieg::upload_vec(ht.idx);
@@ -164,6 +167,7 @@ int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* 
     cieg::HostTiles ht;
     cieg::build_tiles(*csb, panels, te, ht);
     *out = upload_tiles(ctx, ht);
+    if (group_bounds && ngroups) (*out)->group_bounds_host.assign(group_bounds, group_bounds + ngroups + 1);
   });
 }
 
@@ -181,6 +185,7 @@ int cieg_matrix_upload_shard(cieg_ctx* ctx, const cieg_csb_view* csb, const uint
     cieg::build_tiles(*csb, panels, te, ht);
     cieg::restrict_to_rows(ht, row_lo, row_hi);
     *out = upload_tiles(ctx, ht);
+    if (group_bounds && ngroups) (*out)->group_bounds_host.assign(group_bounds, group_bounds + ngroups + 1);
   });
 }
 

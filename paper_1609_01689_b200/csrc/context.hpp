@@ -79,6 +79,9 @@ struct cieg_mat {
   std::uint64_t ntiles = 0;
   std::uint64_t tile_bytes = 0;
   std::vector<std::uint32_t> panel_start_host;
+  std::vector<std::uint32_t> group_bounds_host;  // group (= tile) partition, when known
+  std::vector<std::uint32_t> tile_pi_host, tile_pj_host;
+  std::vector<std::uint64_t> tile_off_host;
   // device arrays
   std::uint32_t* panel_start = nullptr;
   std::uint64_t* tile_off = nullptr;

@@ -21,18 +21,10 @@
 #include <cstring>
 #include <numeric>
 
-#include "cieg_internal.hpp"
 #include "gen_common.h"
+#include "generator.hpp"
 
 namespace cieg {
-namespace {
-
-struct TileGrid {
-  std::vector<std::uint32_t> start;   // tile t covers [start[t], start[t+1])
-  std::vector<std::uint32_t> sector;  // sector of tile t
-  std::vector<std::uint32_t> sector_start;  // sectors + 1
-  std::uint32_t count() const { return static_cast<std::uint32_t>(sector.size()); }
-};
 
 TileGrid make_grid(const cieg_gen_params& p) {
   TileGrid g;
@@ -50,7 +42,9 @@ TileGrid make_grid(const cieg_gen_params& p) {
   return g;
 }
 
-void validate(const cieg_gen_params& p) {
+namespace {
+
+void validate_impl(const cieg_gen_params& p) {
   if (p.n == 0) fail(CIEG_ERR_CONFIG, "generator: n must be positive");
   if (p.sectors == 0 || p.sectors > p.n) fail(CIEG_ERR_CONFIG, "generator: bad sector count");
   if (p.tile == 0 || p.tile > 4096) fail(CIEG_ERR_CONFIG, "generator: bad tile edge");
@@ -59,6 +53,12 @@ void validate(const cieg_gen_params& p) {
   if (p.beta >= (1u << 16)) fail(CIEG_ERR_BETA, "beta must stay below 2^16");
   if (p.beta < p.tile) fail(CIEG_ERR_CONFIG, "generator: beta below the tile edge");
 }
+
+}  // namespace
+
+void validate(const cieg_gen_params& p) { validate_impl(p); }
+
+namespace {
 
 struct Expect {
   double diag_off;   // expected off-diagonal stored nnz inside diagonal tiles
@@ -96,15 +96,9 @@ double avg_row_nnz(const cieg_gen_params& p) {
   return 2.0 * (e.diag_off + p.p * p.q * e.cand_pairs) / static_cast<double>(p.n);
 }
 
-void generate(const cieg_gen_params& p, HostCsb& out) {
-  validate(p);
-  const TileGrid g = make_grid(p);
+std::vector<std::vector<std::uint32_t>> kept_tiles(const cieg_gen_params& p, const TileGrid& g) {
   const std::uint32_t ntiles = g.count();
   const cieg_gen::Seeds sd = cieg_gen::derive_seeds(p.seed);
-  const double avg = avg_row_nnz(p);
-  const double scale = avg > 0.0 ? 1.0 / std::sqrt(avg) : 0.0;
-
-  // Kept column tiles per tile row (ascending).
   std::vector<std::vector<std::uint32_t>> kept(ntiles);
 #pragma omp parallel for schedule(dynamic, 16)
   for (std::int64_t ti = 0; ti < static_cast<std::int64_t>(ntiles); ++ti) {
@@ -117,6 +111,21 @@ void generate(const cieg_gen_params& p, HostCsb& out) {
       if (cieg_gen::unit_double(cieg_gen::hash3(sd.tile, I, J)) < p.p) kept[I].push_back(J);
     kept[I].push_back(I);
   }
+  return kept;
+}
+
+double value_scale(const cieg_gen_params& p) {
+  const double avg = avg_row_nnz(p);
+  return avg > 0.0 ? 1.0 / std::sqrt(avg) : 0.0;
+}
+
+void generate(const cieg_gen_params& p, HostCsb& out) {
+  validate(p);
+  const TileGrid g = make_grid(p);
+  const std::uint32_t ntiles = g.count();
+  const cieg_gen::Seeds sd = cieg_gen::derive_seeds(p.seed);
+  const double scale = value_scale(p);
+  const std::vector<std::vector<std::uint32_t>> kept = kept_tiles(p, g);
 
   // CSB blocks: consecutive tiles up to beta rows, cut at sector starts.
   std::vector<std::uint32_t> bb{0};

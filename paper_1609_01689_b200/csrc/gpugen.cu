@@ -1,0 +1,408 @@
+// gpugen.cu -- the BASELINE sector generator run on the GPU, writing the
+// device tile stream of the SpMM directly: no host
+// CSB, no host re-tiling. Same hash streams and portable Box-Muller as the
+// host generator (gen_common.h), same panel plan, same entry order inside a
+// tile (row-major), so the tile stream is bit-identical to
+// cieg_matrix_upload(cieg_generate_csb(...)) -- checked by the GPU tests.
+// Also builds the tile-diagonal preconditioner on the device from a matrix's
+// diagonal tiles (ci::extract_tile_diagonal, hamiltonian.cpp:178-203).
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+#include "context.hpp"
+#include "device_common.cuh"
+#include "gen_common.h"
+#include "generator.hpp"
+#include "precond.hpp"
+#include "tiling.hpp"
+
+namespace cieg {
+namespace {
+
+struct GenTile {
+  std::uint32_t a0, nr;  // global first row / rows of panel PI
+  std::uint32_t b0, nc;  // global first column / columns of panel PJ
+  std::uint32_t diag;    // PI == PJ (lower part only, incl. the diagonal)
+  std::uint32_t sector;  // sector of the rows (diagonal values)
+};
+
+struct GenArgs {
+  const GenTile* tiles;
+  std::uint64_t q_seed, v1_seed, v2_seed, d_seed;
+  double q, scale;
+  std::uint32_t sa, te;
+};
+
+__device__ __forceinline__ bool entry_exists(const GenArgs& g, const GenTile& t, std::uint32_t a, std::uint32_t b) {
+  if (t.diag && b > a) return false;
+  if (a == b) return true;
+  return cieg_gen::unit_double(cieg_gen::hash3(g.q_seed, a, b)) < g.q;
+}
+
+__global__ void __launch_bounds__(256) gen_count_kernel(GenArgs g, std::uint32_t* counts) {
+  const GenTile t = g.tiles[blockIdx.x];
+  const std::uint32_t total = t.nr * t.nc;
+  std::uint32_t cnt = 0;
+  for (std::uint32_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const std::uint32_t r = e / t.nc, c = e - r * t.nc;
+    cnt += entry_exists(g, t, t.a0 + r, t.b0 + c) ? 1u : 0u;
+  }
+  __shared__ std::uint32_t red[8];
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    std::uint32_t s = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) s += red[w];
+    counts[blockIdx.x] = s;
+  }
+}
+
+__device__ __forceinline__ std::uint32_t kperm(std::uint32_t k) { return (k & ~7u) | ((k & 3u) << 1) | ((k >> 2) & 1u); }
+
+// One CTA (128 threads, one column each) per tile, rows in order: entries are
+// written row-major, exactly the order of the host CSB re-tiling.
+template <typename V>
+__global__ void __launch_bounds__(128) gen_fill_kernel(GenArgs g, const std::uint64_t* tile_off, std::uint32_t* idx,
+                                                       V* val) {
+  const GenTile t = g.tiles[blockIdx.x];
+  __shared__ std::uint32_t wcount[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const std::uint32_t c = threadIdx.x;
+  std::uint64_t pos = tile_off[blockIdx.x];
+  for (std::uint32_t r = 0; r < t.nr; ++r) {
+    const std::uint32_t a = t.a0 + r, b = t.b0 + c;
+    const bool ex = c < t.nc && entry_exists(g, t, a, b);
+    const unsigned ballot = __ballot_sync(0xffffffffu, ex);
+    if (lane == 0) wcount[warp] = __popc(ballot);
+    __syncthreads();
+    std::uint32_t before = 0, rowtot = 0;
+    for (int w = 0; w < 4; ++w) {
+      if (w < warp) before += wcount[w];
+      rowtot += wcount[w];
+    }
+    if (ex) {
+      const std::uint64_t e = pos + before + __popc(ballot & ((1u << lane) - 1u));
+      idx[e] = (r * g.sa + kperm(c)) | ((c * g.sa + kperm(r)) << 16);
+      double v;
+      if (a == b) {
+        const double u = cieg_gen::unit_double(cieg_gen::hash3(g.d_seed, a, a));
+        v = 10.0 * static_cast<double>(t.sector) + 4.0 * u - 2.0;
+      } else {
+        v = cieg_gen::normal_from(cieg_gen::hash3(g.v1_seed, a, b), cieg_gen::hash3(g.v2_seed, a, b)) * g.scale;
+      }
+      val[e] = static_cast<V>(v);
+    }
+    pos += rowtot;
+    __syncthreads();
+  }
+}
+
+__global__ void fill_u32(std::uint32_t* p, std::uint64_t n, std::uint32_t v) {
+  for (std::uint64_t i = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<std::uint64_t>(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
+template <typename T>
+T* dev_upload(const std::vector<T>& v) {
+  T* d = nullptr;
+  CIEG_CUDA(cudaMalloc(&d, std::max<std::size_t>(1, v.size()) * sizeof(T)));
+  if (!v.empty()) CIEG_CUDA(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return d;
+}
+
+}  // namespace
+
+cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t te, std::uint32_t row_lo,
+                          std::uint32_t row_hi) {
+  validate(p);
+  if (te == 0) te = p.precision == 1 ? 64 : (p.tile <= 64 ? 64 : 128);
+  if (p.precision == 1) te = 64;
+  if (te != 64 && te != 128) fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
+  if (row_hi == 0) row_hi = p.n;
+  const TileGrid grid = make_grid(p);
+  const std::uint32_t ng = grid.count();
+  const std::vector<std::vector<std::uint32_t>> kept = kept_tiles(p, grid);
+  const double scale = value_scale(p);
+
+  HostTiles ht;
+  ht.dim = p.n;
+  ht.tile_edge = te;
+  ht.precision = p.precision;
+  ht.panel_start = plan_panels(p.n, grid.start.data(), ng, te);
+  const std::uint32_t np = static_cast<std::uint32_t>(ht.panel_start.size() - 1);
+  // generator tile -> its panel range (panels never span two generator tiles)
+  std::vector<std::uint32_t> tp0(ng + 1);
+  for (std::uint32_t t = 0, P = 0; t <= ng; ++t) {
+    const std::uint32_t r = t < ng ? grid.start[t] : p.n;
+    while (P < np && ht.panel_start[P] < r) ++P;
+    if (P <= np && ht.panel_start[P] != r) fail(CIEG_ERR_CONFIG, "panel plan does not follow the generator tiles");
+    tp0[t] = P;
+  }
+  const std::uint32_t p_lo = static_cast<std::uint32_t>(
+      std::lower_bound(ht.panel_start.begin(), ht.panel_start.end(), row_lo) - ht.panel_start.begin());
+  const std::uint32_t p_hi = static_cast<std::uint32_t>(
+      std::lower_bound(ht.panel_start.begin(), ht.panel_start.end(), row_hi) - ht.panel_start.begin());
+  if (p_hi > np || ht.panel_start[p_lo] != row_lo || ht.panel_start[p_hi] != row_hi || row_lo >= row_hi)
+    fail(CIEG_ERR_CONFIG, "shard rows are not panel boundaries");
+  auto owned = [&](std::uint32_t P) { return P >= p_lo && P < p_hi; };
+
+  struct Key {
+    std::uint32_t pi, pj, I;
+  };
+  std::vector<Key> keys;
+  for (std::uint32_t I = 0; I < ng; ++I)
+    for (std::uint32_t J : kept[I])
+      for (std::uint32_t PI = tp0[I]; PI < tp0[I + 1]; ++PI)
+        for (std::uint32_t PJ = tp0[J]; PJ < tp0[J + 1]; ++PJ) {
+          if (I == J && PJ > PI) continue;
+          if (!owned(PI) && !owned(PJ)) continue;
+          keys.push_back({PI, PJ, I});
+        }
+  std::sort(keys.begin(), keys.end(), [](const Key& x, const Key& y) { return x.pi != y.pi ? x.pi < y.pi : x.pj < y.pj; });
+  const std::uint64_t nt = keys.size();
+  std::vector<GenTile> gt(nt);
+  ht.tile_pi.resize(nt);
+  ht.tile_pj.resize(nt);
+  for (std::uint64_t k = 0; k < nt; ++k) {
+    const Key& q = keys[k];
+    ht.tile_pi[k] = q.pi;
+    ht.tile_pj[k] = q.pj;
+    gt[k] = GenTile{ht.panel_start[q.pi], ht.panel_start[q.pi + 1] - ht.panel_start[q.pi], ht.panel_start[q.pj],
+                    ht.panel_start[q.pj + 1] - ht.panel_start[q.pj], q.pi == q.pj ? 1u : 0u, grid.sector[q.I]};
+  }
+  const cieg_gen::Seeds sd = cieg_gen::derive_seeds(p.seed);
+  CIEG_CUDA(cudaSetDevice(ctx->device));
+  GenTile* d_tiles = dev_upload(gt);
+  std::uint32_t* d_counts = nullptr;
+  CIEG_CUDA(cudaMalloc(&d_counts, std::max<std::uint64_t>(1, nt) * sizeof(std::uint32_t)));
+  GenArgs ga{d_tiles, sd.q, sd.v1, sd.v2, sd.d, p.q, scale, te + 8, te};
+  cieg_mat* m = nullptr;
+  try {
+    if (nt) {
+      gen_count_kernel<<<static_cast<unsigned>(nt), 256, 0, ctx->stream>>>(ga, d_counts);
+      CIEG_CUDA(cudaGetLastError());
+      ++ctx->launches;
+    }
+    std::vector<std::uint32_t> counts(nt);
+    if (nt) CIEG_CUDA(cudaMemcpyAsync(counts.data(), d_counts, nt * sizeof(std::uint32_t), cudaMemcpyDeviceToHost,
+                                      ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    ht.tile_off.assign(nt + 1, 0);
+    ht.nnz = 0;
+    for (std::uint64_t k = 0; k < nt; ++k) {
+      ht.nnz += counts[k];
+      ht.tile_off[k + 1] = ht.tile_off[k] + ((counts[k] + 3u) & ~3u);
+    }
+    ht.row_lo = row_lo;
+    ht.row_hi = row_hi;
+    build_work_lists(ht, p_lo, p_hi);
+    std::uint32_t hlo = row_lo, hhi = row_hi;
+    for (std::uint32_t P = p_lo; P < p_hi; ++P)
+      for (std::uint32_t w = ht.work_off[P]; w < ht.work_off[P + 1]; ++w) {
+        hlo = std::min(hlo, ht.panel_start[ht.work_other[w]]);
+        hhi = std::max(hhi, ht.panel_start[ht.work_other[w] + 1]);
+      }
+    ht.halo_lo = hlo;
+    ht.halo_hi = hhi;
+    build_schedule(ht, static_cast<std::uint32_t>(ctx->sm_count));
+
+    m = new cieg_mat;
+    m->ctx = ctx;
+    m->dim = p.n;
+    m->tile_edge = te;
+    m->precision = p.precision;
+    m->nnz = ht.nnz;
+    m->npanels = np;
+    m->ntiles = nt;
+    m->row_lo = row_lo;
+    m->row_hi = row_hi;
+    m->halo_lo = hlo;
+    m->halo_hi = hhi;
+    m->panel_start_host = ht.panel_start;
+    m->group_bounds_host.assign(grid.start.begin(), grid.start.end());
+    m->panel_start = dev_upload(ht.panel_start);
+    m->tile_off = dev_upload(ht.tile_off);
+    m->tile_pi_host = ht.tile_pi;
+    m->tile_pj_host = ht.tile_pj;
+    m->tile_off_host = ht.tile_off;
+    const std::uint64_t slots = ht.tile_off[nt];
+    CIEG_CUDA(cudaMalloc(&m->idx, std::max<std::uint64_t>(1, slots) * sizeof(std::uint32_t)));
+    CIEG_CUDA(cudaMalloc(&m->val, std::max<std::uint64_t>(1, slots) * (p.precision == 0 ? 4 : 8)));
+    if (slots) {
+      fill_u32<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(m->idx, slots, te | (te << 16));
+      CIEG_CUDA(cudaMemsetAsync(m->val, 0, slots * (p.precision == 0 ? 4 : 8), ctx->stream));
+      if (p.precision == 0)
+        gen_fill_kernel<float><<<static_cast<unsigned>(nt), 128, 0, ctx->stream>>>(ga, m->tile_off, m->idx,
+                                                                                   static_cast<float*>(m->val));
+      else
+        gen_fill_kernel<double><<<static_cast<unsigned>(nt), 128, 0, ctx->stream>>>(ga, m->tile_off, m->idx,
+                                                                                    static_cast<double*>(m->val));
+      CIEG_CUDA(cudaGetLastError());
+      ctx->launches += 2;
+    }
+    m->work_off = dev_upload(ht.work_off);
+    m->work_tile = dev_upload(ht.work_tile);
+    m->work_other = dev_upload(ht.work_other);
+    m->work_kind = dev_upload(ht.work_kind);
+    m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
+    m->sched_off = dev_upload(ht.sched_off);
+    m->sched = dev_upload(ht.sched);
+    m->tile_bytes = slots * (4 + (p.precision == 0 ? 4 : 8));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  } catch (...) {
+    cudaFree(d_tiles);
+    cudaFree(d_counts);
+    delete m;
+    throw;
+  }
+  cudaFree(d_tiles);
+  cudaFree(d_counts);
+  return m;
+}
+
+namespace {
+
+__device__ __forceinline__ std::uint32_t kunperm(std::uint32_t p) {
+  return (p & ~7u) | ((p & 1u) << 2) | ((p >> 1) & 3u);
+}
+
+struct DiagTile {
+  std::uint64_t e0, e1;      // entry slots
+  std::uint32_t a0, b0;      // global first row / column of the tile's panels
+  std::uint32_t gs, gn;      // group start row (shard-local numbering) and size
+  std::uint64_t block_off;   // doubles
+};
+
+// Scatter the tile's entries into its group's dense block, mirrored
+// (ci::extract_tile_diagonal, hamiltonian.cpp:178-203).
+template <typename V>
+__global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx, const V* val, std::uint32_t sa,
+                                   std::uint32_t te, std::uint32_t row_lo, double* blocks) {
+  const DiagTile t = dt[blockIdx.x];
+  for (std::uint64_t e = t.e0 + threadIdx.x; e < t.e1; e += blockDim.x) {
+    const std::uint32_t off = idx[e] & 0xffffu;
+    const std::uint32_t r = off / sa, pc = off - r * sa;
+    if (pc >= te) continue;  // sentinel
+    const std::uint32_t c = kunperm(pc);
+    const std::uint32_t ia = t.a0 + r - row_lo - t.gs, ib = t.b0 + c - row_lo - t.gs;
+    const double v = static_cast<double>(val[e]);
+    blocks[t.block_off + ia + static_cast<std::uint64_t>(ib) * t.gn] = v;
+    blocks[t.block_off + ib + static_cast<std::uint64_t>(ia) * t.gn] = v;
+  }
+}
+
+}  // namespace
+
+cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
+  if (m->group_bounds_host.empty() || m->tile_pi_host.empty())
+    fail(CIEG_ERR_CONFIG, "precond_from_matrix needs a matrix made by cieg_generate_device");
+  const std::vector<std::uint32_t>& gb = m->group_bounds_host;
+  const std::uint32_t ng = static_cast<std::uint32_t>(gb.size() - 1);
+  std::uint32_t g0 = 0;
+  while (g0 < ng && gb[g0] < m->row_lo) ++g0;
+  std::uint32_t g1 = g0;
+  while (g1 < ng && gb[g1 + 1] <= m->row_hi) ++g1;
+  const std::uint32_t lng = g1 - g0;
+  std::vector<std::uint32_t> lb(lng + 1);
+  for (std::uint32_t g = 0; g <= lng; ++g) lb[g] = gb[g0 + g] - m->row_lo;
+  std::vector<std::uint64_t> off(lng + 1, 0);
+  for (std::uint32_t g = 0; g < lng; ++g) {
+    const std::uint64_t sz = lb[g + 1] - lb[g];
+    off[g + 1] = off[g] + sz * sz;
+  }
+  // group of every owned panel
+  const std::vector<std::uint32_t>& ps = m->panel_start_host;
+  std::vector<std::int64_t> gpanel(m->npanels, -1);
+  for (std::uint32_t P = 0, g = 0; P < m->npanels; ++P) {
+    if (ps[P] < m->row_lo || ps[P + 1] > m->row_hi) continue;
+    while (g < lng && lb[g + 1] + m->row_lo <= ps[P]) ++g;
+    gpanel[P] = g;
+  }
+  std::vector<DiagTile> dts;
+  for (std::uint64_t t = 0; t < m->ntiles; ++t) {
+    const std::uint32_t pi = m->tile_pi_host[t], pj = m->tile_pj_host[t];
+    if (gpanel[pi] < 0 || gpanel[pi] != gpanel[pj]) continue;
+    const std::uint32_t g = static_cast<std::uint32_t>(gpanel[pi]);
+    dts.push_back(DiagTile{m->tile_off_host[t], m->tile_off_host[t + 1], ps[pi], ps[pj], lb[g], lb[g + 1] - lb[g],
+                           off[g]});
+  }
+  auto* pr = new cieg_prec;
+  try {
+    pr->ctx = ctx;
+    pr->dim = m->row_hi - m->row_lo;
+    pr->ngroups = lng;
+    pr->bounds_host = lb;
+    pr->block_off_host = off;
+    for (std::uint32_t g = 0; g < lng; ++g) pr->max_group = std::max(pr->max_group, lb[g + 1] - lb[g]);
+    pr->bounds = dev_upload(lb);
+    pr->block_off = dev_upload(off);
+    CIEG_CUDA(cudaMalloc(&pr->blocks, sizeof(double) * std::max<std::uint64_t>(1, off[lng])));
+    CIEG_CUDA(cudaMemsetAsync(pr->blocks, 0, sizeof(double) * off[lng], ctx->stream));
+    if (!dts.empty()) {
+      DiagTile* d = dev_upload(dts);
+      if (m->precision == 0)
+        diag_blocks_kernel<float><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
+            d, m->idx, static_cast<const float*>(m->val), m->tile_edge + 8, m->tile_edge, m->row_lo, pr->blocks);
+      else
+        diag_blocks_kernel<double><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
+            d, m->idx, static_cast<const double*>(m->val), m->tile_edge + 8, m->tile_edge, m->row_lo, pr->blocks);
+      CIEG_CUDA(cudaGetLastError());
+      ++ctx->launches;
+      CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(d);
+    }
+  } catch (...) {
+    delete pr;
+    throw;
+  }
+  return pr;
+}
+
+}  // namespace cieg
+
+extern "C" {
+
+int cieg_generate_device(cieg_ctx* ctx, const cieg_gen_params* prm, uint32_t tile_edge, uint32_t row_lo,
+                         uint32_t row_hi, cieg_mat** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !prm || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_generate_device: null argument");
+    *out = cieg::generate_device(ctx, *prm, tile_edge, row_lo, row_hi);
+  });
+}
+
+int cieg_precond_from_matrix(cieg_ctx* ctx, const cieg_mat* mat, cieg_prec** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_precond_from_matrix: null argument");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    *out = cieg::precond_from_matrix(ctx, mat);
+  });
+}
+
+int cieg_matrix_groups(const cieg_mat* mat, const uint32_t** bounds, uint32_t* ngroups) {
+  return cieg::guarded([&] {
+    if (!mat || !bounds || !ngroups) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_groups: null argument");
+    *bounds = mat->group_bounds_host.data();
+    *ngroups = mat->group_bounds_host.empty() ? 0 : static_cast<uint32_t>(mat->group_bounds_host.size() - 1);
+  });
+}
+
+// Copy the device tile stream back (tests: bit-identity with the host path).
+int cieg_matrix_export(const cieg_mat* m, uint64_t* tile_off, uint32_t* tile_pi, uint32_t* tile_pj, uint32_t* idx,
+                       void* val) {
+  return cieg::guarded([&] {
+    if (!m) cieg::fail(CIEG_ERR_ARGUMENT, "null matrix");
+    std::vector<std::uint64_t> to(m->ntiles + 1);
+    CIEG_CUDA(cudaMemcpy(to.data(), m->tile_off, to.size() * sizeof(std::uint64_t), cudaMemcpyDeviceToHost));
+    if (tile_off) std::memcpy(tile_off, to.data(), to.size() * sizeof(std::uint64_t));
+    if (tile_pi && !m->tile_pi_host.empty()) std::memcpy(tile_pi, m->tile_pi_host.data(), m->ntiles * 4);
+    if (tile_pj && !m->tile_pj_host.empty()) std::memcpy(tile_pj, m->tile_pj_host.data(), m->ntiles * 4);
+    const std::uint64_t slots = to.back();
+    if (idx && slots) CIEG_CUDA(cudaMemcpy(idx, m->idx, slots * 4, cudaMemcpyDeviceToHost));
+    if (val && slots) CIEG_CUDA(cudaMemcpy(val, m->val, slots * (m->precision == 0 ? 4 : 8), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -180,32 +180,7 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
     }
   }
 
-  // Owner work lists: row parts and the diagonal tile of P (ascending J),
-  // then transposed parts of tiles (I, P), I > P (ascending I).
-  std::vector<std::vector<std::uint64_t>> trans(np);
-  for (std::uint64_t t = 0; t < nt; ++t)
-    if (out.tile_pi[t] != out.tile_pj[t]) trans[out.tile_pj[t]].push_back(t);
-  out.work_off.assign(np + 1, 0);
-  for (std::uint32_t P = 0; P < np; ++P)
-    out.work_off[P + 1] = out.work_off[P] + static_cast<std::uint32_t>(rowtiles[P].size() + trans[P].size());
-  const std::uint32_t nw = out.work_off[np];
-  out.work_tile.resize(nw);
-  out.work_other.resize(nw);
-  out.work_kind.resize(nw);
-  for (std::uint32_t P = 0; P < np; ++P) {
-    std::uint32_t w = out.work_off[P];
-    for (std::uint64_t t = tiles_before[P]; t < tiles_before[P + 1]; ++t, ++w) {
-      out.work_tile[w] = static_cast<std::uint32_t>(t);
-      out.work_other[w] = out.tile_pj[t];
-      out.work_kind[w] = out.tile_pj[t] == P ? kDiagonal : kRowPart;
-    }
-    for (std::uint64_t t : trans[P]) {
-      out.work_tile[w] = static_cast<std::uint32_t>(t);
-      out.work_other[w] = out.tile_pi[t];
-      out.work_kind[w] = kTransposed;
-      ++w;
-    }
-  }
+  build_work_lists(out, 0, np);
   if (nt >= (1ull << 32)) fail(CIEG_ERR_CONFIG, "tile count exceeds 2^32");
 }
 
@@ -269,6 +244,42 @@ void build_schedule(HostTiles& t, std::uint32_t ctas) {
       }
     }
     t.sched_off[b + 1] = static_cast<std::uint32_t>(t.sched.size() / 8);
+  }
+}
+
+void build_work_lists(HostTiles& out, std::uint32_t p_lo, std::uint32_t p_hi) {
+  // Owner work lists for panels [p_lo, p_hi): row parts and the diagonal tile
+  // of P (ascending J), then transposed parts of tiles (I, P), I > P
+  // (ascending I). Tiles must be sorted by (pi, pj).
+  const std::uint32_t np = static_cast<std::uint32_t>(out.panel_start.size() - 1);
+  const std::uint64_t nt = out.tile_pi.size();
+  std::vector<std::vector<std::uint32_t>> rowt(np), trans(np);
+  for (std::uint64_t t = 0; t < nt; ++t) {
+    const std::uint32_t pi = out.tile_pi[t], pj = out.tile_pj[t];
+    if (pi >= p_lo && pi < p_hi) rowt[pi].push_back(static_cast<std::uint32_t>(t));
+    if (pi != pj && pj >= p_lo && pj < p_hi) trans[pj].push_back(static_cast<std::uint32_t>(t));
+  }
+  out.work_off.assign(np + 1, 0);
+  for (std::uint32_t P = 0; P < np; ++P)
+    out.work_off[P + 1] = out.work_off[P] + static_cast<std::uint32_t>(rowt[P].size() + trans[P].size());
+  const std::uint32_t nw = out.work_off[np];
+  out.work_tile.resize(nw);
+  out.work_other.resize(nw);
+  out.work_kind.resize(nw);
+  for (std::uint32_t P = 0; P < np; ++P) {
+    std::uint32_t w = out.work_off[P];
+    for (std::uint32_t t : rowt[P]) {
+      out.work_tile[w] = t;
+      out.work_other[w] = out.tile_pj[t];
+      out.work_kind[w] = out.tile_pj[t] == P ? kDiagonal : kRowPart;
+      ++w;
+    }
+    for (std::uint32_t t : trans[P]) {
+      out.work_tile[w] = t;
+      out.work_other[w] = out.tile_pi[t];
+      out.work_kind[w] = kTransposed;
+      ++w;
+    }
   }
 }
 

@@ -64,6 +64,9 @@ std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* g
 void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& panels,
                  std::uint32_t tile_edge, HostTiles& out);
 
+// Owner work lists of panels [p_lo, p_hi) from tiles sorted by (pi, pj).
+void build_work_lists(HostTiles& t, std::uint32_t p_lo, std::uint32_t p_hi);
+
 // Assign owner panels to `ctas` persistent CTAs (longest-first greedy on the
 // entry count, ties by panel id, so the result is deterministic) and emit
 // each CTA's item descriptors: {q0 lo/hi, q1 lo/hi, kind | first << 8 |
