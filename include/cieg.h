@@ -63,6 +63,11 @@ int cieg_ctx_synchronize(cieg_ctx* ctx);
 /* cudaStream_t of the context, as void* (for callers that enqueue their own
  * work, e.g. torch.cuda.ExternalStream). */
 void* cieg_ctx_stream(cieg_ctx* ctx);
+/* 1: the preconditioner's FOM reproduces the reference's operation order
+ * bit for bit (sequential dots, un-fused products); 0 (default): DMMA block
+ * products and parallel fixed-order reductions (deterministic, ~1e-16
+ * relative difference). Direct LU solves are reference-order in both. */
+int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact);
 /* Number of kernels this context has launched (instrumentation). */
 uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx);
 

@@ -119,6 +119,12 @@ class Device:
     def synchronize(self) -> None:
         _check(_lib.load().cieg_ctx_synchronize(self.handle))
 
+    def set_exact_order(self, exact: bool) -> None:
+        """True: the preconditioner's FOM follows the reference's operation
+        order bit for bit; False (default): tensor-core products and parallel
+        fixed-order reductions."""
+        _check(_lib.load().cieg_ctx_set_exact_order(self.handle, 1 if exact else 0))
+
     @property
     def stream(self) -> int:
         return int(_lib.load().cieg_ctx_stream(self.handle) or 0)

@@ -208,6 +208,13 @@ int cieg_shard_plan(const cieg_csb_view* csb, const uint32_t* group_bounds, uint
   });
 }
 
+int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");
+    ctx->exact_order = exact ? 1 : 0;
+  });
+}
+
 int cieg_ctx_set_stream(cieg_ctx* ctx, void* stream) {
   return cieg::guarded([&] {
     if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");

@@ -64,6 +64,7 @@ struct cieg_ctx {
   cudaStream_t stream = nullptr;      // stream all work is enqueued on
   cudaStream_t own_stream = nullptr;  // the context's own stream
   std::uint64_t launches = 0;
+  int exact_order = 0;  // 1: K5 reproduces the reference's operation order bit for bit
   int sm_count = 148;
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
   cieg::PinnedBuf pinned_small;

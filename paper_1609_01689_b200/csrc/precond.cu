@@ -17,6 +17,7 @@
 #include <cstring>
 #include <map>
 
+#include "device_common.cuh"
 #include "precond.hpp"
 
 #define DMUL __dmul_rn
@@ -310,15 +311,37 @@ __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant_
   for (int m = 0; m < mmax; ++m) {
     // z = block * v_m for active columns (sequential k order per element)
     for (int i = tid; i < n; i += blockDim.x) {
-      double z[kMaxCols > 16 ? 16 : kMaxCols];
-      for (int c = 0; c < cc; ++c) z[c] = 0.0;
-      for (int kk = 0; kk < n; ++kk) {
-        const double a = blk[i + static_cast<std::size_t>(kk) * n];
-        for (int c = 0; c < cc; ++c)
-          if (active[c]) z[c] = DADD(z[c], DMUL(a, B(m, kk, c)));
+      // z = block * v_m, k ascending per element (the reference's order);
+      // 16 block entries are loaded ahead so the L2 latency is paid once per
+      // 16 k. Columns are computed whether active or not (inactive ones are
+      // never read), keeping the inner loop branch free.
+      double z[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) z[c] = 0.0;
+      const double* brow = blk + i;
+      int kk = 0;
+      for (; kk + 16 <= n; kk += 16) {
+        double a[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) a[u] = __ldg(brow + static_cast<std::size_t>(kk + u) * n);
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const double* bv = &B(m, kk + u, 0);
+#pragma unroll
+          for (int c = 0; c < 16; ++c)
+            if (c < cc) z[c] = DADD(z[c], DMUL(a[u], bv[c]));
+        }
       }
-      for (int c = 0; c < cc; ++c)
-        if (active[c]) wv[i * CC + c] = DSUB(z[c], DMUL(p.mu[cbeg + c], B(m, i, c)));
+      for (; kk < n; ++kk) {
+        const double a = __ldg(brow + static_cast<std::size_t>(kk) * n);
+        const double* bv = &B(m, kk, 0);
+#pragma unroll
+        for (int c = 0; c < 16; ++c)
+          if (c < cc) z[c] = DADD(z[c], DMUL(a, bv[c]));
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        if (c < cc && active[c]) wv[i * CC + c] = DSUB(z[c], DMUL(p.mu[cbeg + c], B(m, i, c)));
     }
     __syncthreads();
     // scale = max(beta, ||w||)
@@ -406,6 +429,201 @@ __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant_
   }
 }
 
+
+// ------------------------------------------------------------ fast FOM
+// Same algorithm (fom_solve, precond.cpp:87-158) with the block products on
+// the FP64 tensor pipe (DMMA m8n8k4, block entries streamed from L2/HBM with
+// 4 k-steps of loads in flight) and every dot product / norm a parallel
+// fixed-order reduction. Deterministic, but the summation order differs from
+// the reference's sequential loops (results agree to ~1e-16 relative); the
+// reference-order kernel above is selected with cieg_ctx_set_exact_order.
+constexpr int kFastSC = 20;  // smem row stride of basis / w (doubles), 4 mod 16
+
+__device__ __forceinline__ double fom_col_reduce(double part, double* red, int c_of_t, int rsub, int cc) {
+  // part: this thread's partial for column c_of_t (t & 15), row lane rsub (t >> 4)
+  red[rsub * 16 + c_of_t] = part;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 16) {
+    for (int k = 0; k < 16; ++k) s += red[k * 16 + threadIdx.x];
+    red[256 + threadIdx.x] = s;
+  }
+  __syncthreads();
+  const double out = red[256 + c_of_t];
+  __syncthreads();
+  (void)cc;
+  return out;
+}
+
+__global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_constant__ FomParams p) {
+  extern __shared__ double sm[];
+  const std::uint32_t grp = p.groups[blockIdx.x];
+  const std::uint32_t r0 = p.bounds[grp];
+  const int n = static_cast<int>(p.bounds[grp + 1] - r0);
+  const int NP = (n + 7) & ~7;
+  const int cbeg = blockIdx.y * p.chunk;
+  const int cc = min(p.chunk, p.ncols - cbeg);
+  const int mmax = min(p.iters, n);
+  double* basis = sm;                                                  // (mmax+1) x NP x SC
+  double* wv = basis + static_cast<std::size_t>(mmax + 1) * NP * kFastSC;  // NP x SC
+  double* red = wv + static_cast<std::size_t>(NP) * kFastSC;          // 256 + 16
+  double* hess = red + 272;                                            // 16 x 16
+  double* beta = hess + 256;                                           // 16
+  double* scal = beta + 16;                                            // 16
+  double* hcol = scal + 16;                                            // 16
+  int* state = reinterpret_cast<int*>(hcol + 16);                      // active[16], steps[16], done[16]
+  int* active = state;
+  int* steps = state + 16;
+  int* done = state + 32;
+  const double* blk = p.blocks + p.block_off[grp];
+  const int tid = threadIdx.x;
+  const int tc = tid & 15, trow = tid >> 4;
+  auto B = [&](int m, int i, int c) -> double& { return basis[(static_cast<std::size_t>(m) * NP + i) * kFastSC + c]; };
+  auto W = [&](int i, int c) -> double& { return wv[i * kFastSC + c]; };
+  const bool tcol = tc < cc;
+  const int jcol = tcol ? p.cols[cbeg + tc] : 0;
+
+  // beta_j = ||rhs_j||; basis_0 = rhs / beta (rows >= n zero)
+  double part = 0.0;
+  for (int i = trow; i < n; i += 16) {
+    const double v = tcol ? p.r[static_cast<std::size_t>(r0 + i) * p.k + jcol] : 0.0;
+    part = fma(v, v, part);
+  }
+  const double bsq = fom_col_reduce(part, red, tc, trow, cc);
+  if (tid < 16) {
+    beta[tid] = sqrt(bsq);
+    active[tid] = (tid < cc && beta[tid] != 0.0) ? 1 : 0;
+    steps[tid] = 0;
+    done[tid] = 0;
+  }
+  for (int e = tid; e < 256; e += blockDim.x) hess[e] = 0.0;
+  __syncthreads();
+  for (int e = tid; e < NP * 16; e += blockDim.x) {
+    const int i = e >> 4, c = e & 15;
+    double v = 0.0;
+    if (i < n && c < cc && beta[c] != 0.0) v = p.r[static_cast<std::size_t>(r0 + i) * p.k + p.cols[cbeg + c]] / beta[c];
+    B(0, i, c) = v;
+  }
+  __syncthreads();
+
+  const int warp = tid >> 5, lane = tid & 31, g = lane >> 2, q = lane & 3;
+  const int mtiles = NP / 8;
+  for (int m = 0; m < mmax; ++m) {
+    // z = block * v_m on the tensor pipe; warp w owns m-tiles w, w+8, w+16, w+24
+    double acc[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int k0 = 0; k0 < NP; k0 += 16) {
+      double af[4][4], bf[4][2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int kk = k0 + 4 * u + q;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const int mt = warp + 8 * a;
+          const int i = 8 * mt + g;
+          af[u][a] = (mt < mtiles && i < n && kk < n) ? __ldg(blk + i + static_cast<std::size_t>(kk) * n) : 0.0;
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) bf[u][b] = (k0 + 4 * u < NP) ? B(m, k0 + 4 * u + q, 8 * b + g) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[u][a], bf[u][b]);
+    }
+    // w = z - mu v_m
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int mt = warp + 8 * a;
+      if (mt >= mtiles) continue;
+      const int i = 8 * mt + g;
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 8 * b + 2 * q + h;
+          const double mu = c < cc ? p.mu[cbeg + c] : 0.0;
+          W(i, c) = (i < n) ? acc[a][b][h] - mu * B(m, i, c) : 0.0;
+        }
+    }
+    __syncthreads();
+    // scale = max(beta, ||w||)
+    part = 0.0;
+    for (int i = trow; i < n; i += 16) part = fma(W(i, tc), W(i, tc), part);
+    const double wn = sqrt(fom_col_reduce(part, red, tc, trow, cc));
+    if (tid < 16) scal[tid] = beta[tid] > wn ? beta[tid] : wn;
+    // two-pass modified Gram-Schmidt
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int ib = 0; ib <= m; ++ib) {
+        part = 0.0;
+        for (int i = trow; i < n; i += 16) part = fma(B(ib, i, tc), W(i, tc), part);
+        const double hv = fom_col_reduce(part, red, tc, trow, cc);
+        if (tid < 16 && active[tid]) {
+          double& hh = hess[tid * 16 + ib + m * 4];
+          hh = pass == 0 ? hv : hh + hv;
+          hcol[tid] = hv;
+        }
+        __syncthreads();
+        for (int e = tid; e < n * 16; e += blockDim.x) {
+          const int i = e >> 4, c = e & 15;
+          if (c < cc && active[c]) W(i, c) -= hcol[c] * B(ib, i, c);
+        }
+        __syncthreads();
+      }
+    }
+    part = 0.0;
+    for (int i = trow; i < n; i += 16) part = fma(W(i, tc), W(i, tc), part);
+    const double nrm = sqrt(fom_col_reduce(part, red, tc, trow, cc));
+    if (tid < 16 && active[tid]) {
+      steps[tid] = m + 1;
+      const double sc = scal[tid] > 1.0 ? scal[tid] : 1.0;
+      if (nrm <= 1e-12 * sc) {
+        hess[tid * 16 + (m + 1) + m * 4] = 0.0;
+        active[tid] = 0;
+        done[tid] = m + 1;
+      } else {
+        hess[tid * 16 + (m + 1) + m * 4] = nrm;
+        scal[tid] = nrm;
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < NP * 16; e += blockDim.x) {
+      const int i = e >> 4, c = e & 15;
+      if (c < cc && active[c]) B(m + 1, i, c) = (i < n) ? W(i, c) / scal[c] : 0.0;
+    }
+    __syncthreads();
+  }
+  __shared__ double ycoef[16][kFomMaxSteps];
+  if (tid < 16) {
+    const int c = tid;
+    const int m = c < cc ? (done[c] ? done[c] : (active[c] ? steps[c] : 0)) : 0;
+    if (m > 0) {
+      double hm[kFomMaxSteps * kFomMaxSteps];
+      for (int a = 0; a < m; ++a)
+        for (int b = 0; b < m; ++b) hm[a + b * m] = hess[c * 16 + a + b * 4];
+      double rhs[kFomMaxSteps] = {0.0, 0.0, 0.0};
+      rhs[0] = beta[c];
+      tiny_lu_solve(hm, m, rhs);
+      for (int a = 0; a < m; ++a) ycoef[c][a] = rhs[a];
+    }
+    done[c] = m;
+  }
+  __syncthreads();
+  for (int e = tid; e < n * 16; e += blockDim.x) {
+    const int i = e >> 4, c = e & 15;
+    if (c >= cc) continue;
+    const int m = done[c];
+    double x = 0.0;
+    for (int a = 0; a < m; ++a) x = fma(B(a, i, c), ycoef[c][a], x);
+    p.w[static_cast<std::size_t>(r0 + i) * p.k + p.cols[cbeg + c]] = x;
+  }
+}
+
 }  // namespace
 
 int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::uint32_t k,
@@ -486,19 +704,32 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
     }
     const int mmax = std::min<int>(cfg.inner_iters, static_cast<int>(prec->max_group));
     if (mmax > kFomMaxSteps) fail(CIEG_ERR_CONFIG, "fom_solve: inner_iters above 3 is not supported");
-    // chunk so that shared memory stays below ~200 KB
     const std::size_t n = prec->max_group;
-    int chunk = 16;
-    auto smem_for = [&](int cc) {
-      return sizeof(double) * ((mmax + 1) * n * cc + n * cc + cc * 16 + 2 * cc) + sizeof(int) * 3 * cc;
-    };
-    while (chunk > 1 && smem_for(chunk) > 200 * 1024) chunk /= 2;
-    if (smem_for(chunk) > 220 * 1024) fail(CIEG_ERR_CONFIG, "FOM tile too large for shared memory");
-    fp.chunk = chunk;
-    const std::size_t smem = smem_for(chunk);
-    CIEG_CUDA(cudaFuncSetAttribute(fom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
-    fom_kernel<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+    if (!ctx->exact_order && n <= 256) {
+      // fast path: DMMA block products, parallel fixed-order reductions
+      const int chunk = 16;
+      fp.chunk = chunk;
+      const std::size_t np8 = (n + 7) & ~std::size_t{7};
+      const std::size_t smem = sizeof(double) * ((mmax + 1) * np8 * kFastSC + np8 * kFastSC + 272 + 256 + 48) +
+                               sizeof(int) * 48;
+      CIEG_CUDA(cudaFuncSetAttribute(fom_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(smem)));
+      dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
+      fom_fast_kernel<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+    } else {
+      // reference-order path: chunk so that shared memory stays below ~200 KB
+      int chunk = 16;
+      auto smem_for = [&](int cc) {
+        return sizeof(double) * ((mmax + 1) * n * cc + n * cc + cc * 16 + 2 * cc) + sizeof(int) * 3 * cc;
+      };
+      while (chunk > 1 && smem_for(chunk) > 200 * 1024) chunk /= 2;
+      if (smem_for(chunk) > 220 * 1024) fail(CIEG_ERR_CONFIG, "FOM tile too large for shared memory");
+      fp.chunk = chunk;
+      const std::size_t smem = smem_for(chunk);
+      CIEG_CUDA(cudaFuncSetAttribute(fom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
+      fom_kernel<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+    }
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
   }

@@ -53,8 +53,16 @@ def test_gram_deterministic():
     assert np.array_equal(a, a.T)  # same fixed-order sums for (a,b) and (b,a)
 
 
+@pytest.fixture
+def exact_order():
+    dev = ci.Device.default()
+    dev.set_exact_order(True)
+    yield
+    dev.set_exact_order(False)
+
+
 @pytest.mark.parametrize("name", ["lu", "fom"])
-def test_preconditioner_bitwise_vs_reference(golden, name):
+def test_preconditioner_bitwise_vs_reference(golden, name, exact_order):
     g = golden("precond")
     h = gen_from(g[f"{name}_params"])
     td = ci.extract_tile_diagonal(h)
@@ -63,7 +71,18 @@ def test_preconditioner_bitwise_vs_reference(golden, name):
     assert np.array_equal(w, g[f"{name}_w"])
 
 
-def test_preconditioner_live_reference(ref_lib):
+@pytest.mark.parametrize("name", ["lu", "fom"])
+def test_preconditioner_fast_path_vs_reference(golden, name):
+    """Default (tensor-core FOM) path: same result to rounding."""
+    g = golden("precond")
+    h = gen_from(g[f"{name}_params"])
+    td = ci.extract_tile_diagonal(h)
+    r = ci.random_block(h.dim, 8, 31)
+    w = ci.apply_preconditioner(td, r, ci.ShiftPlan(g[f"{name}_mu"], g[f"{name}_engage"]))
+    assert rel(w, g[f"{name}_w"]) < 1e-12
+
+
+def test_preconditioner_live_reference(ref_lib, exact_order):
     h = gen_from((6144, 3, 256, 0.1, 0.4, 5, 0, 2000))
     rm = ref_lib.RefMatrix(h)
     rtd = ref_lib.RefTileDiagonal(rm, h.groups)
