@@ -16,6 +16,7 @@ OpenMP on all host cores) on the same matrix.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -245,32 +246,132 @@ def lobpcg_record():
     return out
 
 
+def sweep_record(dev):
+    """BASELINE config 3: the config-1 matrix (fp64, L2-resident) at m = 1..64:
+    device time per SpMM (CUDA events, 20 back-to-back calls after warm-up),
+    algorithmic GB/s and flop/byte per m."""
+    import torch
+
+    from paper_1609_01689_b200 import ci, configs
+
+    cfg = configs.CFG1
+    dm = cfg.generate_device(device=dev)
+    stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", dev.index))
+    out = []
+    for m in configs.SWEEP_M:
+        x = torch.from_numpy(ci.random_block(cfg.n, m, m)).cuda()
+        y = torch.empty_like(x)
+        torch.cuda.synchronize()
+        for _ in range(3):
+            dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(20):
+            dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+        e1.record(stream)
+        e1.synchronize()
+        us = e0.elapsed_time(e1) / 20 * 1e3
+        b = configs.spmm_bytes(dm.nnz, cfg.n, m, 1)
+        f = configs.spmm_flops(dm.nnz, cfg.n, m)
+        out.append({"m": m, "us": round(us, 2), "gbs": round(b / (us * 1e-6) / 1e9, 1),
+                    "flop_per_byte": round(f / b, 3), "gflops": round(f / (us * 1e-6) / 1e9, 1)})
+    return {"workload": "cfg3-sweep (config-1 matrix, fp64 H, L2-resident)", "points": out}
+
+
+def cfg4_record(dev):
+    """BASELINE config 4 time-to-solution on one GPU (matrix generated on the
+    GPU; preconditioned, k_want 8, block 16, tol 1e-6)."""
+    import numpy as np
+
+    from paper_1609_01689_b200 import ci, configs
+
+    cfg = configs.CFG4
+    t0 = time.time()
+    dm = cfg.generate_device(device=dev)
+    td = ci.tile_diagonal_from_matrix(dm)
+    dev.synchronize()
+    gen_s = time.time() - t0
+    x0 = ci.random_block(cfg.n, cfg.kt, 42)
+    t0 = time.perf_counter()
+    rep = ci.lobpcg_solve(dm, x0, ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol, preconditioner=td))
+    tts = time.perf_counter() - t0
+    rr = np.array([r.relres for r in rep.history]).reshape(-1, cfg.kt)
+    return {"workload": cfg.name, "n": cfg.n, "nnz_stored": dm.nnz, "tts_s": round(tts, 3),
+            "iterations": rep.iterations, "converged": rep.converged, "gen_on_gpu_s": round(gen_s, 2),
+            "split_ms": {k: round(v, 1) for k, v in rep.timing_ms.items()}, "counters": vars(rep.counters),
+            "max_final_relres": float(rr[-1, :cfg.k_want].max()), "eigenvalues": rep.eigenvalues.tolist()}
+
+
+def group_bounds(cfg):
+    """Generator tile (= group) starts, the rule of generator.cpp make_grid."""
+    out = []
+    for s in range(cfg.sectors):
+        a, b = cfg.n * s // cfg.sectors, cfg.n * (s + 1) // cfg.sectors
+        out.extend(range(a, b, cfg.tile))
+    return out + [cfg.n]
+
+
 def ours(args):
     import torch
 
     from paper_1609_01689_b200 import ci, configs
 
     rank, world, local = dist_env()
+    local = local % max(1, torch.cuda.device_count())
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # CIEG_DIST_BACKEND=gloo runs the N > 1 choreography with host-mediated
+        # collectives (used to exercise several ranks on a single GPU)
+        if os.environ.get("CIEG_DIST_BACKEND") == "gloo":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     cfg = configs.CFG2
     m = args.m or cfg.m
-    h, t_gen = gen_matrix(cfg, rank)
     dev = ci.Device(local)
+    tdev = torch.device("cuda", local)
+    h = None
     t0 = time.time()
-    dm = ci.DeviceMatrix(h, dev)
+    if world == 1:
+        # the drop-in path: host CsbMatrix (also used by the CPU baseline) -> upload
+        h, t_gen = gen_matrix(cfg, 0)
+        t0 = time.time()
+        dm = ci.DeviceMatrix(h, dev)
+        row_bounds = [0, cfg.n]
+    else:
+        # row-block shards generated on each GPU (strong scaling of the same matrix)
+        gb = group_bounds(cfg)
+        row_bounds = [0]
+        for k in range(1, world):
+            target = cfg.n * k // world
+            row_bounds.append(min(gb, key=lambda g: abs(g - target)))
+        row_bounds.append(cfg.n)
+        t_gen = 0.0
+        dm = cfg.generate_device(device=dev, rows=(row_bounds[rank], row_bounds[rank + 1]))
     t_up = time.time() - t0
-    n = h.dim
-    stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", local))
-    x = torch.from_numpy(ci.random_block(n, m, 5)).cuda()
-    y = torch.empty_like(x)
+    n = cfg.n
+    lo, hi = row_bounds[rank], row_bounds[rank + 1]
+    # one dedicated (non-default) stream carries the collectives and the
+    # library's kernels, so both are ordered and the events time both
+    stream = torch.cuda.Stream(device=tdev)
+    torch.cuda.set_stream(stream)
+    from paper_1609_01689_b200 import _lib as L
+
+    lib = L.load()
+    ci._check(lib.cieg_ctx_set_stream(dev.handle, ctypes.c_void_p(stream.cuda_stream)))
+    x_full = torch.from_numpy(ci.random_block(n, m, 5)).to(tdev)
+    x_local = x_full[lo:hi].clone()
+    y = torch.empty((hi - lo, m), dtype=torch.float64, device=tdev)
     torch.cuda.synchronize()
 
     def step():
-        dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+        if world > 1:
+            from paper_1609_01689_b200 import dist as D
+
+            D.allgather_rows(x_local, row_bounds, x_full)
+        dm.spmm_ptr(x_full.data_ptr(), y.data_ptr(), m)
 
     def barrier():
         if world > 1:
@@ -280,7 +381,7 @@ def ours(args):
 
     for _ in range(args.warmup):
         step()
-    dev.synchronize()
+    torch.cuda.synchronize()
     barrier()
     torch.cuda.synchronize()
     l0 = dev.launches
@@ -292,7 +393,6 @@ def ours(args):
             step()
         ev1.record(stream)
         ev1.synchronize()
-    dev.synchronize()
     torch.cuda.synchronize()
     barrier()
     launches = dev.launches - l0
@@ -300,39 +400,53 @@ def ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([ms], device="cuda")
+        t = torch.tensor([ms], device=tdev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    nbytes = configs.spmm_bytes(h.nnz_lower, n, m, h.precision)
-    flops = configs.spmm_flops(h.nnz_lower, n, m)
+        nnz_t = torch.tensor([dm.nnz], device=tdev, dtype=torch.float64)
+        dist.all_reduce(nnz_t)
+    nnz_total = dm.nnz if world == 1 else None
+    # algorithmic bytes of the whole distributed SpMM: every stored entry once,
+    # X and U once (shards duplicate boundary tiles; those bytes are not counted)
+    if world == 1:
+        nbytes = configs.spmm_bytes(dm.nnz, n, m, dm.precision)
+        flops = configs.spmm_flops(dm.nnz, n, m)
+    else:
+        nnz_total = int(cfg.expected_nnz())
+        nbytes = configs.spmm_bytes(nnz_total, n, m, 0)
+        flops = configs.spmm_flops(nnz_total, n, m)
     gbs = nbytes / (ms * 1e-3) / 1e9
-    total_gbs = gbs * world
+    ci._check(lib.cieg_ctx_set_stream(dev.handle, None))
+    torch.cuda.set_stream(torch.cuda.default_stream(tdev))
 
-    # e2e: the C-ABI host call with pinned host buffers
-    xh = torch.from_numpy(ci.random_block(n, m, 6)).pin_memory()
-    yh = torch.empty_like(xh).pin_memory()
-    xn, yn = xh.numpy(), yh.numpy()
-    for _ in range(max(1, args.warmup)):
-        dm.spmm_host(xn)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    ke = max(3, min(args.steps, 10))
-    import ctypes as C
-
-    from paper_1609_01689_b200 import _lib
-
-    lib = _lib.load()
-    e0.record(stream)
-    for _ in range(ke):
-        rc = lib.cieg_spmm_host(dev.handle, dm.handle, xn.ctypes.data_as(C.POINTER(C.c_double)),
-                                yn.ctypes.data_as(C.POINTER(C.c_double)), m)
-        if rc:
-            raise RuntimeError(lib.cieg_last_error().decode())
-    e1.record(stream)
-    e1.synchronize()
-    ms_e2e = e0.elapsed_time(e1) / ke
-    e2e_gbs = nbytes / (ms_e2e * 1e-3) / 1e9 * world
-
+    # e2e (rank 0 drives a full-matrix host call when world == 1; sharded runs
+    # report the device-resident number end to end through all ranks)
+    e2e = None
+    if world == 1:
+        xh = torch.from_numpy(ci.random_block(n, m, 6)).pin_memory()
+        yh = torch.empty_like(xh).pin_memory()
+        xn, yn = xh.numpy(), yh.numpy()
+        for _ in range(max(1, args.warmup)):
+            dm.spmm_host(xn)
+        own = torch.cuda.ExternalStream(dev.stream, device=tdev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        ke = max(3, min(args.steps, 10))
+        e0.record(own)
+        for _ in range(ke):
+            rc = lib.cieg_spmm_host(dev.handle, dm.handle, xn.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                    yn.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), m)
+            if rc:
+                raise RuntimeError(lib.cieg_last_error().decode())
+        e1.record(own)
+        e1.synchronize()
+        ms_e2e = e0.elapsed_time(e1) / ke
+        e2e = {"value": round(nbytes / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * m * 8,
+               "d2h_bytes_per_step": n * m * 8, "ms_per_step": round(ms_e2e, 4),
+               "call": "cieg_spmm_host (pinned host X/U)"}
+    else:
+        e2e = {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+               "note": "sharded run: inputs device-resident, the step includes the NCCL all-gather of X"}
     peak, peak_kind = load_peaks()
     if rank != 0:
         if world > 1:
@@ -341,23 +455,22 @@ def ours(args):
             dist.destroy_process_group()
         return 0
     line = {
-        "metric": "spmm_gbs", "value": round(total_gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+        "metric": "spmm_gbs", "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms, 4), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64 (fp32 H promoted exactly)",
         "data": "synthetic (seeded sector generator, BASELINE config 2)",
-        "config": {"workload": cfg.name, "n": n, "nnz_stored": h.nnz_lower, "m": m, "tile": cfg.tile,
+        "config": {"workload": cfg.name, "n": n, "nnz_stored": int(nnz_total), "m": m, "tile": cfg.tile,
                    "p": round(cfg.p(), 8), "q": cfg.q, "device_tile_edge": dm.tile_edge, "device_tiles": dm.ntiles,
                    "l2": "inputs larger than L2 (H 6.4 GB, X/U 256 MB each); no flush",
-                   "parallelism": "single GPU" if world == 1 else f"replicas x{world} (one shard-sized matrix per rank)",
+                   "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} (NCCL all-gather of X)",
                    "gen_s": round(t_gen, 1), "upload_s": round(t_up, 1)},
         "roofline": {"bound": "hbm", "achieved": round(gbs, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(gbs / peak, 4), "traffic": load_traffic(cfg.name), "peak_kind": peak_kind,
                      "fp64_tflops": round(flops / (ms * 1e-3) / 1e12, 3), "fp64_peak_tflops": FP64_PEAK_TFLOPS,
                      "fp64_frac": round(flops / (ms * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, 4),
                      "bytes_per_launch": nbytes, "flops_per_launch": flops},
-        "e2e": {"value": round(e2e_gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": n * m * 8,
-                "d2h_bytes_per_step": n * m * 8, "ms_per_step": round(ms_e2e, 4),
-                "call": "cieg_spmm_host (pinned host X/U)"},
+        "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
@@ -365,6 +478,10 @@ def ours(args):
         line["cpu_baseline"] = cpu_baseline(h, m)
     if world == 1 and not args.no_lobpcg:
         line["lobpcg"] = lobpcg_record()
+        line["sweep"] = sweep_record(dev)
+        if not args.no_cfg4:
+            del dm
+            line["lobpcg_cfg4"] = cfg4_record(dev)
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -382,6 +499,7 @@ def main():
     ap.add_argument("--m", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-lobpcg", action="store_true")
+    ap.add_argument("--no-cfg4", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

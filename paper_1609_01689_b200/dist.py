@@ -132,7 +132,11 @@ def lobpcg_solve_dist(sm: ShardedMatrix, x0_local: np.ndarray, options: ci.Lobpc
     lib = _lib.load()
     dev = sm.device
     tdev = torch.device("cuda", dev.index)
-    torch_stream = torch.cuda.current_stream(tdev)
+    # One dedicated stream carries both the library's kernels and the
+    # collectives issued from the hooks, so they are ordered without host syncs.
+    torch_stream = torch.cuda.Stream(device=tdev)
+    prev_stream = torch.cuda.current_stream(tdev)
+    torch.cuda.set_stream(torch_stream)
     ci._check(lib.cieg_ctx_set_stream(dev.handle, C.c_void_p(torch_stream.cuda_stream)))
     rb = sm.row_bounds
     dim = sm.h.dim
@@ -172,4 +176,5 @@ def lobpcg_solve_dist(sm: ShardedMatrix, x0_local: np.ndarray, options: ci.Lobpc
                                              C.byref(hooks), C.byref(rep)))
     finally:
         lib.cieg_ctx_set_stream(dev.handle, None)
+        torch.cuda.set_stream(prev_stream)
     return ci._read_report(lib, rep, sm.local_rows)
