@@ -20,13 +20,19 @@
 namespace cieg {
 namespace {
 
-constexpr int kGramWarps = 4;
+constexpr int kGramWarps = 8;
+
+template <int MT, int NT>
+struct GramUnroll {
+  static constexpr int kU = (MT + NT) <= 4 ? 8 : ((MT + NT) <= 8 ? 4 : ((MT + NT) <= 10 ? 2 : 1));
+};
 
 template <int MT, int NT>
 __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R, std::uint32_t n,
                                                                std::uint32_t rows_per_warp,
                                                                double* partials) {
   constexpr int MA = 8 * MT, NB = 8 * NT;
+  constexpr int U = GramUnroll<MT, NT>::kU;
   __shared__ double red[MA * NB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -73,18 +79,24 @@ __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R,
   const std::uint64_t gw = static_cast<std::uint64_t>(blockIdx.x) * kGramWarps + warp;
   const std::uint64_t r0 = gw * rows_per_warp;
   const std::uint64_t r1 = std::min<std::uint64_t>(n, r0 + rows_per_warp);
-  for (std::uint64_t i0 = r0; i0 < r1; i0 += 4) {
-    const std::uint64_t i = i0 + q;
-    const bool ok = i < r1;
-    double a[MT], b[NT];
+  // U k-steps (4 rows each) of fragments are loaded before their DMMAs issue
+  for (std::uint64_t i0 = r0; i0 < r1; i0 += 4 * U) {
+    double a[U][MT], b[U][NT];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt) a[mt] = (ok && pa[mt]) ? __ldg(pa[mt] + i * la[mt]) : 0.0;
+    for (int u = 0; u < U; ++u) {
+      const std::uint64_t i = i0 + 4 * u + q;
+      const bool ok = i < r1;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) b[nt] = (ok && pb[nt]) ? __ldg(pb[nt] + i * lb[nt]) : 0.0;
+      for (int mt = 0; mt < MT; ++mt) a[u][mt] = (ok && pa[mt]) ? __ldg(pa[mt] + i * la[mt]) : 0.0;
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+      for (int nt = 0; nt < NT; ++nt) b[u][nt] = (ok && pb[nt]) ? __ldg(pb[nt] + i * lb[nt]) : 0.0;
+    }
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+    for (int u = 0; u < U; ++u)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[u][mt], b[u][nt]);
   }
 
   // warps fold their partials into one buffer in warp order (deterministic)
@@ -216,15 +228,23 @@ __global__ void __launch_bounds__(32 * kCombineWarps)
     }
     const std::uint64_t arow = i0 + g;
     for (int s = 0; s < p.in.nseg; ++s) {
-      const double* base = p.in.s[s].p;
-      const std::uint32_t ld = p.in.s[s].ld, w = p.in.s[s].w;
+      const double* base = p.in.s[s].p + arow * p.in.s[s].ld;
+      const std::uint32_t w = p.in.s[s].w;
       const int ksteps = static_cast<int>((w + 3) / 4);
       const double* gsb = gs + (poff[s] + q) * SG + g;
-      for (int ks = 0; ks < ksteps; ++ks) {
-        const std::uint32_t k = 4 * ks + q;
-        const double a = (arow < p.n && k < w) ? base[arow * ld + k] : 0.0;
+      const bool rok = arow < p.n;
+      // all A fragments of the segment (<= 12 k-steps) are loaded before the DMMAs
+      double a[12];
 #pragma unroll
-        for (int nt = 0; nt < OT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a, gsb[4 * ks * SG + 8 * nt]);
+      for (int ks = 0; ks < 12; ++ks) {
+        const std::uint32_t k = 4 * ks + q;
+        a[ks] = (ks < ksteps && rok && k < w) ? base[k] : 0.0;
+      }
+#pragma unroll
+      for (int ks = 0; ks < 12; ++ks) {
+        if (ks >= ksteps) break;
+#pragma unroll
+        for (int nt = 0; nt < OT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a[ks], gsb[4 * ks * SG + 8 * nt]);
       }
     }
     if (crow < p.n) {
@@ -291,8 +311,8 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
   if (kx == 0 || ky == 0) return out;
   if (kx > 48 || ky > 48) fail(CIEG_ERR_CONFIG, "gram: block width above 48");
   const int MT = static_cast<int>((kx + 7) / 8), NT = static_cast<int>((ky + 7) / 8);
-  // fixed decomposition: rows_per_warp multiple of 4, at most 2 blocks per SM
-  const int max_blocks = 2 * ctx->sm_count;
+  // fixed decomposition: rows_per_warp multiple of 4, at most 4 blocks per SM
+  const int max_blocks = 4 * ctx->sm_count;
   std::uint64_t rpw = (static_cast<std::uint64_t>(n) + max_blocks * kGramWarps - 1) / (max_blocks * kGramWarps);
   rpw = std::max<std::uint64_t>(64, (rpw + 3) & ~3ull);
   const int blocks = static_cast<int>(std::max<std::uint64_t>(1, (n + rpw * kGramWarps - 1) / (rpw * kGramWarps)));
@@ -320,6 +340,8 @@ void combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_ho
              const Out2& out, bool accumulate) {
   if (n == 0 || kout == 0) return;
   if (kout > 48) fail(CIEG_ERR_CONFIG, "combine: output width above 48");
+  for (int k = 0; k < in.nseg; ++k)
+    if (in.s[k].w > 48) fail(CIEG_ERR_CONFIG, "combine: input segment wider than 48");
   if (out.w0 + out.w1 != kout) fail(CIEG_ERR_DIMENSION, "combine: output split mismatch");
   const std::uint32_t kin = in.width;
   if (kin == 0) {
