@@ -12,7 +12,7 @@ import os
 import pathlib
 
 _HERE = pathlib.Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libcieg.so"
+LIB_PATH = pathlib.Path(os.environ["CIEG_LIB"]) if os.environ.get("CIEG_LIB") else _HERE / "libcieg.so"  # override: experiments
 
 
 class CsbView(C.Structure):

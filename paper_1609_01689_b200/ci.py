@@ -119,6 +119,11 @@ class Device:
     def synchronize(self) -> None:
         _check(_lib.load().cieg_ctx_synchronize(self.handle))
 
+    def set_stream(self, stream: int) -> None:
+        """Launch on an external CUDA stream (a cudaStream_t as int; 0 or
+        None = back to the context's own stream). cieg_ctx_set_stream."""
+        _check(_lib.load().cieg_ctx_set_stream(self.handle, C.c_void_p(stream) if stream else None))
+
     def set_exact_order(self, exact: bool) -> None:
         """True: the preconditioner's FOM follows the reference's operation
         order bit for bit; False (default): tensor-core products and parallel

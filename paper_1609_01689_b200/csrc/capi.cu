@@ -145,6 +145,7 @@ cieg_mat* upload_tiles(cieg_ctx* ctx, cieg::HostTiles& ht) {
     m->sched_off = cieg::upload_vec(ht.sched_off);
     m->sched = cieg::upload_vec(ht.sched);
     m->tile_bytes = ht.tile_off.back() * (4 + (ht.precision == 0 ? 4 : 8));
+    cieg::order_tile_entries(ctx, m);
   } catch (...) {
     delete m;
     throw;

@@ -101,6 +101,10 @@ struct cieg_mat {
 
 namespace cieg {
 
+// Bank-aware ordering of the entries inside every tile (reorder.cu); run
+// once on every freshly built device tile stream.
+void order_tile_entries(cieg_ctx* ctx, cieg_mat* m);
+
 // Launch the owner-computes SpMM over device X/Y (row-major, ld = ldx/ldy).
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
                  std::uint32_t ldy, std::uint32_t mcols);

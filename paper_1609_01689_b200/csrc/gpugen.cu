@@ -12,6 +12,7 @@
 
 #include "context.hpp"
 #include "device_common.cuh"
+#include "tile_layout.h"
 #include "gen_common.h"
 #include "generator.hpp"
 #include "precond.hpp"
@@ -32,6 +33,7 @@ struct GenArgs {
   std::uint64_t q_seed, v1_seed, v2_seed, d_seed;
   double q, scale;
   std::uint32_t sa, te;
+  int precision;
 };
 
 __device__ __forceinline__ bool entry_exists(const GenArgs& g, const GenTile& t, std::uint32_t a, std::uint32_t b) {
@@ -59,7 +61,6 @@ __global__ void __launch_bounds__(256) gen_count_kernel(GenArgs g, std::uint32_t
   }
 }
 
-__device__ __forceinline__ std::uint32_t kperm(std::uint32_t k) { return (k & ~7u) | ((k & 3u) << 1) | ((k >> 2) & 1u); }
 
 // One CTA (128 threads, one column each) per tile, rows in order: entries are
 // written row-major, exactly the order of the host CSB re-tiling.
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(128) gen_fill_kernel(GenArgs g, const std::uin
     }
     if (ex) {
       const std::uint64_t e = pos + before + __popc(ballot & ((1u << lane) - 1u));
-      idx[e] = (r * g.sa + kperm(c)) | ((c * g.sa + kperm(r)) << 16);
+      idx[e] = cieg_tl::pack(r, c, g.sa, g.precision);
       double v;
       if (a == b) {
         const double u = cieg_gen::unit_double(cieg_gen::hash3(g.d_seed, a, a));
@@ -178,7 +179,7 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
   GenTile* d_tiles = dev_upload(gt);
   std::uint32_t* d_counts = nullptr;
   CIEG_CUDA(cudaMalloc(&d_counts, std::max<std::uint64_t>(1, nt) * sizeof(std::uint32_t)));
-  GenArgs ga{d_tiles, sd.q, sd.v1, sd.v2, sd.d, p.q, scale, te + 8, te};
+  GenArgs ga{d_tiles, sd.q, sd.v1, sd.v2, sd.d, p.q, scale, cieg_tl::stride(te, p.precision), te, p.precision};
   cieg_mat* m = nullptr;
   try {
     if (nt) {
@@ -251,6 +252,7 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
     m->sched_off = dev_upload(ht.sched_off);
     m->sched = dev_upload(ht.sched);
     m->tile_bytes = slots * (4 + (p.precision == 0 ? 4 : 8));
+    order_tile_entries(ctx, m);
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
   } catch (...) {
     cudaFree(d_tiles);
@@ -265,9 +267,6 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
 
 namespace {
 
-__device__ __forceinline__ std::uint32_t kunperm(std::uint32_t p) {
-  return (p & ~7u) | ((p & 1u) << 2) | ((p >> 1) & 3u);
-}
 
 struct DiagTile {
   std::uint64_t e0, e1;      // entry slots
@@ -279,14 +278,15 @@ struct DiagTile {
 // Scatter the tile's entries into its group's dense block, mirrored
 // (ci::extract_tile_diagonal, hamiltonian.cpp:178-203).
 template <typename V>
-__global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx, const V* val, std::uint32_t sa,
-                                   std::uint32_t te, std::uint32_t row_lo, double* blocks) {
+__global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx, const V* val, std::uint32_t te, std::uint32_t row_lo, double* blocks) {
   const DiagTile t = dt[blockIdx.x];
   for (std::uint64_t e = t.e0 + threadIdx.x; e < t.e1; e += blockDim.x) {
     const std::uint32_t off = idx[e] & 0xffffu;
+    constexpr int prec = sizeof(V) == 4 ? 0 : 1;
+    const std::uint32_t sa = cieg_tl::stride(te, prec);
     const std::uint32_t r = off / sa, pc = off - r * sa;
     if (pc >= te) continue;  // sentinel
-    const std::uint32_t c = kunperm(pc);
+    const std::uint32_t c = cieg_tl::unperm(pc, prec);
     const std::uint32_t ia = t.a0 + r - row_lo - t.gs, ib = t.b0 + c - row_lo - t.gs;
     const double v = static_cast<double>(val[e]);
     blocks[t.block_off + ia + static_cast<std::uint64_t>(ib) * t.gn] = v;
@@ -345,10 +345,10 @@ cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
       DiagTile* d = dev_upload(dts);
       if (m->precision == 0)
         diag_blocks_kernel<float><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
-            d, m->idx, static_cast<const float*>(m->val), m->tile_edge + 8, m->tile_edge, m->row_lo, pr->blocks);
+            d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->blocks);
       else
         diag_blocks_kernel<double><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
-            d, m->idx, static_cast<const double*>(m->val), m->tile_edge + 8, m->tile_edge, m->row_lo, pr->blocks);
+            d, m->idx, static_cast<const double*>(m->val), m->tile_edge, m->row_lo, pr->blocks);
       CIEG_CUDA(cudaGetLastError());
       ++ctx->launches;
       CIEG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -22,12 +22,18 @@
 //   * fp32 values are promoted to fp64 exactly on fragment load (F2F runs on
 //     its own unit, measured not to slow DMMA); products and sums are fp64,
 //     the reference's precision contract (csb.hpp:79-82).
-//   * fragment loads are conflict-free and wide: tile columns are stored
-//     k-step-pair interleaved (upload-time permutation folded into the packed
-//     indices) with row stride TD+8, so one 64-bit (fp32) / 128-bit (fp64)
-//     load per lane yields the A fragments of two k-steps; X slab row stride
-//     8*NT+4 doubles. The consumer double-buffers fragments across groups of
-//     4 k-steps so loads and conversions overlap the previous group's DMMAs.
+//   * fragment loads are conflict-free and wide (tile_layout.h): fp32 tile
+//     columns are interleaved in 16-column groups with row stride TD+16, so
+//     one float4 per lane yields the A fragments of 4 k-steps (fp64: stride
+//     TD+8, one double2 = 2 k-steps); the X slab stores the two n-tiles'
+//     columns side by side, so one double2 yields both B fragments of a
+//     k-step. The consumer double-buffers fragments across groups of 4
+//     k-steps so loads and conversions overlap the previous group's DMMAs.
+//   * scatter stores are (nearly) bank-conflict-free: reorder.cu orders every
+//     tile's entries at upload so each warp-wide store hits distinct banks in
+//     both orientations; only the TD data columns of a tile are zeroed.
+//   * the next item's entry stream is bulk-prefetched into L2
+//     (cp.async.bulk.prefetch.L2) a whole item ahead of the register batches.
 #include <algorithm>
 #include <cstdint>
 
@@ -71,7 +77,7 @@ __device__ __forceinline__ void bar_arrive(int id, int n) {
 }
 template <typename V, int TD, int NT>
 struct Shape {
-  static constexpr int kSA = TD + 8;                    // row stride (elements), 8 mod 32 banks (f32)
+  static constexpr int kSA = sizeof(V) == 4 ? TD + 16 : TD + 8;  // row stride (elements), tile_layout.h
   static constexpr int kSX = 8 * NT + 4;                // doubles
   static constexpr int kMT = TD / 8 / kConsumerWarps;   // m-tiles per consumer warp
   static constexpr std::size_t kTileBytes = ((sizeof(V) * TD * kSA + 15) / 16) * 16;
@@ -82,13 +88,14 @@ struct Shape {
 
 struct Item {
   std::uint64_t q0, q1;  // entry quads [q0, q1)
-  std::uint32_t flags;   // kind | first << 8 | last << 9
+  std::uint32_t flags;   // kind | first << 8 | last << 9 | owner rows << 16
   std::uint32_t o0;      // partner panel start row
   int orow;              // partner panel rows
-  std::uint32_t panel;   // owner panel
+  std::uint32_t r0;      // owner panel start row
   __device__ __forceinline__ std::uint32_t kind() const { return flags & 0xffu; }
   __device__ __forceinline__ bool first() const { return (flags >> 8) & 1u; }
   __device__ __forceinline__ bool last() const { return (flags >> 9) & 1u; }
+  __device__ __forceinline__ int prow() const { return static_cast<int>(flags >> 16); }
 };
 
 __device__ __forceinline__ Item load_item(const SpmmArgs& a, std::uint32_t i) {
@@ -100,7 +107,7 @@ __device__ __forceinline__ Item load_item(const SpmmArgs& a, std::uint32_t i) {
   it.flags = v.x;
   it.o0 = v.y;
   it.orow = static_cast<int>(v.z);
-  it.panel = v.w;
+  it.r0 = v.w;
   return it;
 }
 
@@ -114,6 +121,28 @@ __device__ __forceinline__ void load_slab(const SpmmArgs& a, const Item& it, int
     xv[j] = (k < it.orow && t < static_cast<int>(a.mcols)) ? __ldg(a.x + static_cast<std::size_t>(it.o0 + k) * a.ldx + t)
                                                             : 0.0;
   }
+}
+
+// Bulk L2 prefetch of a byte range (no registers, no shared memory): keeps
+// the DRAM stream of the items ahead in flight while the producer warps'
+// register batches only see L2 latency.
+__device__ __forceinline__ void prefetch_l2(const void* p, std::uint64_t bytes) {
+  const std::uint64_t a0 = reinterpret_cast<std::uint64_t>(p) & ~15ull;
+  const std::uint64_t a1 = (reinterpret_cast<std::uint64_t>(p) + bytes + 15) & ~15ull;
+  for (std::uint64_t a = a0; a < a1; a += (1u << 20)) {
+    const std::uint32_t n = static_cast<std::uint32_t>(a1 - a < (1u << 20) ? a1 - a : (1u << 20));
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(n) : "memory");
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ void prefetch_item(const SpmmArgs& a, const Item& it) {
+  const std::uint64_t nq = it.q1 - it.q0;
+  if (nq) {
+    prefetch_l2(a.idx + 4 * it.q0, 16 * nq);
+    prefetch_l2(static_cast<const V*>(a.val) + 4 * it.q0, 4 * sizeof(V) * nq);
+  }
+  if (it.orow) prefetch_l2(a.x + static_cast<std::size_t>(it.o0) * a.ldx, sizeof(double) * it.orow * a.ldx);
 }
 
 template <int KIND, typename V>
@@ -205,20 +234,27 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
     int buf = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i) {
       const bool has_next = i + 1 < i_end;
+      // the item after this one: its entries (and X slab) are bulk-prefetched
+      // into L2 a whole item ahead of the register batches (measured best at
+      // distance 1; deeper prefetch loses)
+      if (pt == 0 && has_next) prefetch_item<V>(a, nxt);
       bar_sync(kBarEmpty0 + buf, kThreads);
       V* A = tile_buf(buf);
       {
+        // zero the TD data columns of every row (the pad columns are never read)
         float4* p4 = reinterpret_cast<float4*>(A);
-        constexpr int n4 = static_cast<int>(S::kTileBytes / 16);
+        constexpr int kRow4 = TD * static_cast<int>(sizeof(V)) / 16, kStride4 = S::kSA * static_cast<int>(sizeof(V)) / 16;
 #pragma unroll 4
-        for (int k = pt; k < n4; k += kProducerThreads) p4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = pt; k < TD * kRow4; k += kProducerThreads)
+          p4[(k / kRow4) * kStride4 + k % kRow4] = make_float4(0.f, 0.f, 0.f, 0.f);
       }
       double* X = slab_buf(buf);
 #pragma unroll
       for (int j = 0; j < S::kSlabPer; ++j) {
         const int e = pt + j * kProducerThreads;
         const int k = e / (8 * NT), t = e - k * (8 * NT);
-        X[k * S::kSX + t] = xv[j];
+        // NT == 2: columns g and 8 + g side by side (one 128-bit B load)
+        X[k * S::kSX + (NT == 2 ? 2 * (t & 7) + (t >> 3) : t)] = xv[j];
       }
       if (has_next) load_slab<V, TD, NT>(a, nxt, pt, xv);
       const Item after = (i + 2 < i_end) ? load_item(a, i + 2) : nxt;
@@ -267,8 +303,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 #pragma unroll
           for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
       }
-      const std::uint32_t r0 = __ldg(a.panel_start + it.panel);
-      const int prow = static_cast<int>(__ldg(a.panel_start + it.panel + 1) - r0);
+      const std::uint32_t r0 = it.r0;
+      const int prow = it.prow();
       const bool live = m_base < prow;
       bar_sync(kBarFull0 + buf, kThreads);
       if (live) {
@@ -276,30 +312,42 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         // k-steps run, in groups of 4 (two interleaved k-step pairs), with
         // the next group's fragments loaded and converted while the current
         // group's DMMAs issue.
-        const V* A = tile_buf(buf) + (m_base + g) * S::kSA + 2 * q;
-        const double* xb = slab_buf(buf) + q * S::kSX + g;
+        // fp32: one float4 = the A fragments of the group's 4 k-steps;
+        // fp64: two double2 (tile_layout.h). NT == 2: one double2 = both
+        // n-tiles' B fragments of a k-step.
+        const V* A = tile_buf(buf) + (m_base + g) * S::kSA + (sizeof(V) == 4 ? 4 : 2) * q;
+        const double* xb = slab_buf(buf) + q * S::kSX + (NT == 2 ? 2 * g : g);
         double af[2][4][S::kMT], bf[2][4][NT];
         auto load_group = [&](int grp, double (&fa)[4][S::kMT], double (&fb)[4][NT]) {
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
+          for (int j = 0; j < S::kMT; ++j) {
+            if constexpr (sizeof(V) == 4) {
+              const float4 v4 = *reinterpret_cast<const float4*>(A + j * 8 * S::kSA + 16 * grp);
+              fa[0][j] = static_cast<double>(v4.x);
+              fa[1][j] = static_cast<double>(v4.y);
+              fa[2][j] = static_cast<double>(v4.z);
+              fa[3][j] = static_cast<double>(v4.w);
+            } else {
 #pragma unroll
-            for (int j = 0; j < S::kMT; ++j) {
-              const V* src = A + j * 8 * S::kSA + 8 * (2 * grp + p);
-              if constexpr (sizeof(V) == 4) {
-                const float2 v2 = *reinterpret_cast<const float2*>(src);
-                fa[2 * p][j] = static_cast<double>(v2.x);
-                fa[2 * p + 1][j] = static_cast<double>(v2.y);
-              } else {
-                const double2 v2 = *reinterpret_cast<const double2*>(src);
+              for (int p = 0; p < 2; ++p) {
+                const double2 v2 = *reinterpret_cast<const double2*>(A + j * 8 * S::kSA + 8 * (2 * grp + p));
                 fa[2 * p][j] = v2.x;
                 fa[2 * p + 1][j] = v2.y;
               }
             }
           }
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < 4; ++u) {
+            const double* xr = xb + 4 * (4 * grp + u) * S::kSX;
+            if constexpr (NT == 2) {
+              const double2 v2 = *reinterpret_cast<const double2*>(xr);
+              fb[u][0] = v2.x;
+              fb[u][1] = v2.y;
+            } else {
 #pragma unroll
-            for (int n = 0; n < NT; ++n) fb[u][n] = xb[4 * (4 * grp + u) * S::kSX + 8 * n];
+              for (int n = 0; n < NT; ++n) fb[u][n] = xr[8 * n];
+            }
+          }
         };
         auto mma_group = [&](const double (&fa)[4][S::kMT], const double (&fb)[4][NT]) {
 #pragma unroll

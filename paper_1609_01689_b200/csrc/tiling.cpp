@@ -1,5 +1,6 @@
 // tiling.cpp -- see tiling.hpp.
 #include "tiling.hpp"
+#include "tile_layout.h"
 
 #include <algorithm>
 #include <cstring>
@@ -45,12 +46,9 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
     if (panels[p + 1] <= panels[p] || panels[p + 1] - panels[p] > te)
       fail(CIEG_ERR_CONFIG, "panel plan violates the tile edge");
 
-  const std::uint32_t sa = te + 8;
+  const int prec = csb.precision;
+  const std::uint32_t sa = cieg_tl::stride(te, prec);  // tile_layout.h
   const std::uint32_t sentinel = te | (te << 16);  // row 0, pad column te: never read
-  // Within every 8 columns, k-step j's column 4j' + q and k-step j'+1's
-  // column 4j' + 4 + q are stored side by side, so one 64-bit (fp32) or
-  // 128-bit (fp64) shared load yields the A fragments of two k-steps.
-  auto kperm = [](std::uint32_t k) { return (k & ~7u) | ((k & 3u) << 1) | ((k >> 2) & 1u); };
   std::vector<std::uint32_t> panel_of(dim);
   for (std::uint32_t p = 0; p < np; ++p)
     for (std::uint32_t r = panels[p]; r < panels[p + 1]; ++r) panel_of[r] = p;
@@ -115,10 +113,8 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
           }
           const std::uint32_t rl = a - r0, cl = b - panels[pj];
           // Packed tile-local index: the entry's shared-memory offset in the
-          // row-part orientation (r * SA + perm(c)) and in the transposed one
-          // (c * SA + perm(r)), SA = tile_edge + 8 (the kernels' padded row
-          // stride, 8 mod 32 banks).
-          tb->idx.push_back((rl * sa + kperm(cl)) | ((cl * sa + kperm(rl)) << 16));
+          // row-part orientation and in the transposed one (tile_layout.h).
+          tb->idx.push_back(cieg_tl::pack(rl, cl, sa, prec));
           tb->v.push_back(single ? static_cast<double>(v32[e]) : v64[e]);
         }
       }
@@ -227,19 +223,22 @@ void build_schedule(HostTiles& t, std::uint32_t ctas) {
     std::sort(panels_of[b].begin(), panels_of[b].end());
     for (std::uint32_t P : panels_of[b]) {
       const std::uint32_t w0 = t.work_off[P], w1 = t.work_off[P + 1];
+      const std::uint32_t prows = t.panel_start[P + 1] - t.panel_start[P];
       if (w0 == w1) {  // empty panel: one no-op item so the owner still writes zeros
-        const std::uint32_t d[8] = {0, 0, 0, 0, 3u | (1u << 8) | (1u << 9), t.panel_start[P],
-                                    t.panel_start[P + 1] - t.panel_start[P], P};
+        const std::uint32_t d[8] = {0, 0, 0, 0, 3u | (1u << 8) | (1u << 9) | (prows << 16), t.panel_start[P],
+                                    prows, t.panel_start[P]};
         t.sched.insert(t.sched.end(), d, d + 8);
         continue;
       }
       for (std::uint32_t w = w0; w < w1; ++w) {
         const std::uint32_t tile = t.work_tile[w], other = t.work_other[w];
         const std::uint64_t q0 = t.tile_off[tile] / 4, q1 = t.tile_off[tile + 1] / 4;
-        const std::uint32_t flags = t.work_kind[w] | ((w == w0) ? 1u << 8 : 0u) | ((w + 1 == w1) ? 1u << 9 : 0u);
+        const std::uint32_t flags = t.work_kind[w] | ((w == w0) ? 1u << 8 : 0u) | ((w + 1 == w1) ? 1u << 9 : 0u) |
+                                    (prows << 16);
         const std::uint32_t d[8] = {static_cast<std::uint32_t>(q0), static_cast<std::uint32_t>(q0 >> 32),
                                     static_cast<std::uint32_t>(q1), static_cast<std::uint32_t>(q1 >> 32),
-                                    flags, t.panel_start[other], t.panel_start[other + 1] - t.panel_start[other], P};
+                                    flags, t.panel_start[other], t.panel_start[other + 1] - t.panel_start[other],
+                                    t.panel_start[P]};
         t.sched.insert(t.sched.end(), d, d + 8);
       }
     }

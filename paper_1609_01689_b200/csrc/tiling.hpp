@@ -70,7 +70,8 @@ void build_work_lists(HostTiles& t, std::uint32_t p_lo, std::uint32_t p_hi);
 // Assign owner panels to `ctas` persistent CTAs (longest-first greedy on the
 // entry count, ties by panel id, so the result is deterministic) and emit
 // each CTA's item descriptors: {q0 lo/hi, q1 lo/hi, kind | first << 8 |
-// last << 9, other-panel start row, other-panel rows, owner panel}.
+// last << 9 | owner rows << 16, other-panel start row, other-panel rows,
+// owner start row} -- everything the consumer needs without a dependent load.
 void build_schedule(HostTiles& t, std::uint32_t ctas);
 
 // Keep only what owner rows [row_lo, row_hi) need (panel-aligned bounds):

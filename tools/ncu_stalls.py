@@ -34,3 +34,18 @@ def summarise(sub, name):
         print(f"   {k:22s} {v:8d} {100*v/max(s,1):5.1f}%")
 summarise(recs[:split - 5], "producer (+prologue)")
 summarise(recs[split - 5:], "consumer")
+if len(sys.argv) > 2:
+    top = int(sys.argv[2])
+    def tot(r):
+        s = 0
+        for k in reasons:
+            try:
+                s += int(r[ix[k]] or 0)
+            except ValueError:
+                pass
+        return s
+    print("== top instructions (addr, total, long_sb, wait, barrier, source)")
+    for i, r in sorted(enumerate(recs), key=lambda x: -tot(x[1]))[:top]:
+        g = lambda k: r[ix[k]] if k in ix else "?"
+        print(f"  {i:5d} {tot(r):7d} lsb={g('stall_long_sb'):>6s} wait={g('stall_wait'):>6s} bar={g('stall_barrier'):>6s} "
+              f"ssb={g('stall_short_sb'):>6s} {'P' if i < split - 5 else 'C'} {r[ix['Source']][:70]}")
