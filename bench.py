@@ -48,7 +48,8 @@ def load_traffic(workload):
     p = os.path.join(REPO, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(workload)
+            e = json.load(f).get(workload)
+        return int(e["traffic_per_launch"]) if e else None
     except Exception:
         return None
 
