@@ -253,6 +253,35 @@ int cieg_report_history(const cieg_report* rep, int* iteration, int* column, dou
  * [spmm, rayleigh_ritz, orthonormalization, preconditioner, residual, other, total]. */
 int cieg_report_timing(const cieg_report* rep, double* ms7);
 
+/* ---- Lanczos baseline (proj/include/ci/lanczos.hpp) -------------------- */
+/* Checkpoint hook (LanczosOptions::observer, lanczos.hpp:18-21): step count,
+ * the tridiagonal coefficients alpha[0..m) / beta[0..m), and the Lanczos
+ * basis (column-major n x m) copied to the host only when an observer is
+ * installed; pointers are valid during the call only. */
+typedef void (*cieg_lanczos_observer_fn)(void* user, int m, const double* alpha, const double* beta,
+                                         const double* basis_host, uint32_t n);
+typedef struct {
+  int k_want;   /* lanczos.hpp:15 */
+  double tol;   /* lanczos.hpp:16 */
+  int max_iter; /* lanczos.hpp:17 */
+  cieg_lanczos_observer_fn observer;
+  void* observer_user;
+} cieg_lanczos_options;
+void cieg_lanczos_options_default(cieg_lanczos_options* opt);
+/* ci::lanczos_checkpoint (lanczos.hpp:26, lanczos.cpp:11-15): 1 on the
+ * staggered grid (every 10 steps to 100, 20 to 200, then 40). */
+int cieg_lanczos_checkpoint(int m);
+/* ci::lanczos_default_start (lanczos.hpp:30, lanczos.cpp:17-22) given the end
+ * of the lowest stratum: ones on [0, stratum_end), normalised; out: n doubles. */
+int cieg_lanczos_default_start(uint32_t n, uint32_t stratum_end, double* out);
+/* ci::lanczos_solve (lanczos.hpp:35-36, lanczos.cpp:24-136): v0 host vector
+ * of length n. Same report schema as cieg_lobpcg_solve (k_want = kt = the
+ * number of Ritz pairs returned; counters: spmm_calls, spmv_equivalents, 0,
+ * orthogonalizations; timing: spmm, ritz analysis, reorthogonalisation,
+ * 0, 0, other, total). */
+int cieg_lanczos_solve(cieg_ctx* ctx, const cieg_mat* mat, const double* v0_host, const cieg_lanczos_options* opt,
+                       cieg_report** out);
+
 /* ---- synthetic sector generator (BASELINE.json configs) ---------------- */
 /* Deterministic sector/tile matrix of SURVEY.md 8(d): ns equal sectors,
  * tile grid restarting at every sector, tiles kept for |ds| <= band with

@@ -657,3 +657,100 @@ def lobpcg_solve(h, x0, k_want, tol, max_iter=500, tiles=None, bounds=None, cfg=
         counters[3] += 1
         it += 1
     return Report(theta[:k_want].copy(), x, history, counters, converged, iterations, norm_est, active_sets)
+
+
+# ------------------------------------------------------------- lanczos.cpp
+
+def lanczos_checkpoint(m):
+    """lanczos.cpp:11-15: every 10 steps to 100, every 20 to 200, then 40."""
+    if m <= 100:
+        return m % 10 == 0
+    if m <= 200:
+        return m % 20 == 0
+    return m % 40 == 0
+
+
+def symmetric_double(seed, i, j):
+    """rng.hpp:33-36."""
+    return 2.0 * unit_double(hash3(seed, i, j)) - 1.0
+
+
+def lanczos_solve(matvec, v0, k_want, tol, max_iter=500):
+    """lanczos.cpp:24-136: Lanczos with two-pass full reorthogonalisation,
+    seeded random restart on breakdown, Ritz analysis on the checkpoint grid.
+    `matvec(v)` applies H to an (n, 1) block (spmm with m = 1). numpy's
+    LAPACK eigh stands in for Eigen's tridiagonal QL (tolerance-level)."""
+    v0 = np.asarray(v0, dtype=np.float64).reshape(-1)
+    dim = v0.shape[0]
+    nrm0 = np.linalg.norm(v0)
+    if nrm0 == 0.0:
+        raise ValueError("lanczos: v0 must be nonzero")
+    max_steps = min(max_iter, dim)
+    basis = np.zeros((dim, max_steps + 1))
+    basis[:, 0] = v0 / nrm0  # :36
+    alpha, beta = [], []
+    counters = [0, 0, 0, 0]
+    history = []
+    norm_est = 0.0
+    ritz = ritz_vecs = None
+    factorized = 0
+    converged = False
+    iterations = 0
+
+    def factorize(m):  # :54-63
+        t = np.diag(np.array(alpha[:m])) + np.diag(np.array(beta[: m - 1]), -1) + np.diag(np.array(beta[: m - 1]), 1)
+        w, z = np.linalg.eigh(t)
+        return w, z, m
+
+    restart_counter = 0
+    for m in range(1, max_steps + 1):
+        w = matvec(basis[:, m - 1 : m]).reshape(-1)  # :67
+        counters[0] += 1
+        counters[1] += 1
+        a = float(basis[:, m - 1] @ w)  # :68
+        alpha.append(a)
+        w = w - a * basis[:, m - 1]  # :70
+        if m >= 2:
+            w = w - beta[m - 2] * basis[:, m - 2]  # :71
+        for _ in range(2):  # :73-76
+            coeff = basis[:, :m].T @ w
+            w = w - basis[:, :m] @ coeff
+        counters[3] += 1
+        b = float(np.linalg.norm(w))
+        scale = max(abs(a), 1.0)
+        if b <= 1e-13 * scale:  # :81-96
+            r = np.array([symmetric_double(0x4C414E43 + restart_counter, i, m) for i in range(dim)])
+            restart_counter += 1
+            for _ in range(2):
+                coeff = basis[:, :m].T @ r
+                r = r - basis[:, :m] @ coeff
+            rn = float(np.linalg.norm(r))
+            if rn == 0.0:
+                break
+            basis[:, m] = r / rn
+            beta.append(0.0)
+        else:
+            basis[:, m] = w / b
+            beta.append(b)
+        last = m == max_steps
+        if not lanczos_checkpoint(m) and not last:  # :102-103
+            continue
+        ritz, ritz_vecs, factorized = factorize(m)
+        norm_est = max(norm_est, abs(ritz[0]), abs(ritz[m - 1]))  # :106-107
+        k = min(k_want, m)
+        all_conv = k >= k_want
+        for j in range(k):  # :111-118
+            res = abs(beta[m - 1]) * abs(ritz_vecs[m - 1, j])
+            relres = res / max(norm_est, 1e-300)
+            history.append((m, j, relres, ritz[j]))
+            if relres > tol:
+                all_conv = False
+        iterations = m
+        if all_conv:
+            converged = True
+            break
+    if factorized == 0:
+        ritz, ritz_vecs, factorized = factorize(len(alpha))
+    k = min(k_want, factorized)
+    x = basis[:, :factorized] @ ritz_vecs[:, :k]  # :131-132
+    return Report(ritz[:k].copy(), x, history, counters, converged, iterations, norm_est, [])

@@ -83,6 +83,20 @@ class DistHooks(C.Structure):
 OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_uint32,
                        C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double))
 
+# cieg_lanczos_observer_fn(user, m, alpha, beta, basis_host (n x m col-major), n)
+LANCZOS_OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                               C.POINTER(C.c_double), C.c_uint32)
+
+
+class LanczosOptionsC(C.Structure):
+    _fields_ = [
+        ("k_want", C.c_int),
+        ("tol", C.c_double),
+        ("max_iter", C.c_int),
+        ("observer", LANCZOS_OBSERVER),
+        ("observer_user", C.c_void_p),
+    ]
+
 _vp = C.c_void_p
 _u32 = C.c_uint32
 _u64 = C.c_uint64
@@ -121,6 +135,10 @@ SIGNATURES = {
     "cieg_lobpcg_solve": (_i, [_vp, _vp, _pd, _u32, _vp, C.POINTER(LobpcgOptionsC), OBSERVER, _vp,
                                C.POINTER(_vp)]),
     "cieg_report_destroy": (_i, [_vp]),
+    "cieg_lanczos_options_default": (None, [C.POINTER(LanczosOptionsC)]),
+    "cieg_lanczos_checkpoint": (_i, [C.c_int]),
+    "cieg_lanczos_default_start": (_i, [_u32, _u32, _pd]),
+    "cieg_lanczos_solve": (_i, [_vp, _vp, _pd, C.POINTER(LanczosOptionsC), C.POINTER(_vp)]),
     "cieg_lobpcg_solve_dist": (_i, [_vp, _vp, _pd, _u32, _vp, C.POINTER(LobpcgOptionsC), C.POINTER(DistHooks),
                                     C.POINTER(_vp)]),
     "cieg_shard_plan": (_i, [C.POINTER(CsbView), _pu32, _u32, _u32, _u32, _pu32, _pu32, _pu32]),

@@ -721,6 +721,63 @@ def _read_report(lib, rep, nrows: int) -> SolveReport:
                        timing_ms=dict(zip(_TIMING_KEYS, tm.tolist())))
 
 
+@dataclasses.dataclass
+class LanczosOptions:
+    """ci::LanczosOptions (lanczos.hpp:14-22); observer(m, basis (n x m),
+    alpha, beta) at every checkpoint."""
+    k_want: int = 8
+    tol: float = 1e-6
+    max_iter: int = 500
+    observer: Optional[Callable] = None
+
+
+def lanczos_checkpoint(m: int) -> bool:
+    """ci::lanczos_checkpoint (lanczos.cpp:11-15)."""
+    return bool(_lib.load().cieg_lanczos_checkpoint(int(m)))
+
+
+def lanczos_default_start(n: int, stratum_end: int) -> np.ndarray:
+    """ci::lanczos_default_start (lanczos.cpp:17-22) for a basis whose lowest
+    stratum is rows [0, stratum_end)."""
+    out = np.zeros(n)
+    _check(_lib.load().cieg_lanczos_default_start(n, stratum_end, _ptr(out)))
+    return out
+
+
+def lanczos_solve(h, v0: np.ndarray, options: LanczosOptions = LanczosOptions(),
+                  device: Optional[Device] = None) -> SolveReport:
+    """ci::lanczos_solve (lanczos.cpp:24-136) on the GPU: K1 SpMV per step,
+    two-pass full reorthogonalisation against the HBM-resident basis. `h` is
+    a CsbMatrix (uploaded once) or a resident DeviceMatrix. The observer is
+    called at every checkpoint as observer(m, basis, alpha, beta) with the
+    (n x m) Lanczos basis, like LanczosOptions::observer."""
+    v0 = np.ascontiguousarray(v0, dtype=np.float64).reshape(-1)
+    if v0.shape[0] != h.dim:
+        raise DimensionMismatch("lanczos: v0 dim != matrix dim")
+    if not np.any(v0):
+        raise ConfigError("lanczos: v0 must be nonzero")
+    if options.k_want < 1:
+        raise ConfigError("lanczos: k_want must be >= 1")
+    lib = _lib.load()
+    dm = h if isinstance(h, DeviceMatrix) else device_matrix(h, device)
+    opt = _lib.LanczosOptionsC()
+    lib.cieg_lanczos_options_default(C.byref(opt))
+    opt.k_want, opt.tol, opt.max_iter = options.k_want, options.tol, options.max_iter
+    if options.observer is not None:
+        user_obs = options.observer
+
+        def _obs(_user, m, ap, bp, basis_ptr, n):
+            a = np.ctypeslib.as_array(ap, (m,)).copy()
+            b = np.ctypeslib.as_array(bp, (m,)).copy()
+            basis = np.ctypeslib.as_array(basis_ptr, (m, n)).T.copy()  # column-major n x m
+            user_obs(m, basis, a, b)
+
+        opt.observer = _lib.LANCZOS_OBSERVER(_obs)
+    rep = C.c_void_p()
+    _check(lib.cieg_lanczos_solve(dm.device.handle, dm.handle, _ptr(v0), C.byref(opt), C.byref(rep)))
+    return _read_report(lib, rep, h.dim)
+
+
 def write_history_csv(report: SolveReport, os: io.TextIOBase) -> None:
     """ci::write_history_csv (lobpcg.cpp:389-397): ``iter,col,relres,theta`` %.17g."""
     os.write("iter,col,relres,theta\n")

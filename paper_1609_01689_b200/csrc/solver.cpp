@@ -17,22 +17,8 @@
 #include "blockvec.hpp"
 #include "dense_small.hpp"
 #include "precond.hpp"
+#include "report.hpp"
 
-struct cieg_report {
-  std::vector<double> eigenvalues;
-  std::vector<double> trial;  // n x kt row-major
-  std::uint32_t n = 0, kt = 0, k_want = 0;
-  struct Row {
-    int iteration, column;
-    double relres, theta;
-  };
-  std::vector<Row> history;
-  std::uint64_t counters[4] = {0, 0, 0, 0};
-  bool converged = false;
-  int iterations = 0;
-  double norm_estimate = 0.0;
-  double timing_ms[7] = {0, 0, 0, 0, 0, 0, 0};
-};
 
 namespace cieg {
 namespace {
@@ -129,18 +115,6 @@ double dev_from_identity(const Mat& g, int m) {
   return d;
 }
 
-struct Clock {
-  cieg_ctx* ctx;
-  double* slot;
-  std::chrono::steady_clock::time_point t0;
-  Clock(cieg_ctx* c, double* s) : ctx(c), slot(s), t0(std::chrono::steady_clock::now()) {}
-  ~Clock() {
-    cudaStreamSynchronize(ctx->stream);
-    *slot += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-  }
-};
-
-enum Phase { kSpmm = 0, kRR = 1, kOrtho = 2, kPrecond = 3, kResid = 4, kOther = 5, kTotal = 6 };
 
 class Solver {
  public:

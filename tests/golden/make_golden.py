@@ -30,6 +30,56 @@ LOBPCG_CASES = {
 }
 
 
+LANCZOS_CASES = {
+    # name: (gen params or None = diag(1..100), v0 kind, k_want, tol, max_iter)
+    "diag100_restart": (None, "e0+e1", 3, 1e-10, 100),
+    "sector_f64": ((2000, 4, 64, 0.1, 0.5, 11, 1, 500), "stratum", 4, 1e-8, 300),
+    "sector_f32": ((3072, 3, 256, 0.2, 0.4, 13, 0, 2000), "stratum", 4, 1e-6, 300),
+}
+
+
+def diag100():
+    n = 100
+    return ci.CsbMatrix(dim=n, precision=1, block_boundaries=np.array([0, n], np.uint32),
+                        entry_offsets=np.array([0, n], np.uint64), rows=np.arange(n, dtype=np.uint16),
+                        cols=np.arange(n, dtype=np.uint16), values=np.arange(1, n + 1, dtype=np.float64),
+                        groups=np.array([0, 50, n], np.uint32))
+
+
+def lanczos_start(kind, n, sectors):
+    v = np.zeros(n)
+    if kind == "e0+e1":
+        v[0] = v[1] = 1.0
+    else:  # lanczos_default_start on the first sector (the lowest stratum)
+        v[: n // sectors] = 1.0
+    return v
+
+
+def make_lanczos():
+    la = {}
+    for name, (p, kind, k, tol, max_iter) in LANCZOS_CASES.items():
+        h = diag100() if p is None else gen(p)
+        v0 = lanczos_start(kind, h.dim, 1 if p is None else int(p[1]))
+        rm = ref.RefMatrix(h)
+        r = ref.lanczos_solve(rm, v0, k, tol, max_iter)
+        if p is not None:
+            la[f"{name}_params"] = np.array(p, dtype=np.float64)
+        la[f"{name}_meta"] = np.array([k, tol, max_iter, 0.0 if kind == "e0+e1" else 1.0])
+        la[f"{name}_v0"] = v0
+        la[f"{name}_eigenvalues"] = r.eigenvalues
+        la[f"{name}_eigenvectors"] = r.trial_vectors
+        la[f"{name}_iterations"] = np.array(r.iterations)
+        la[f"{name}_converged"] = np.array(r.converged)
+        la[f"{name}_counters"] = r.counters
+        la[f"{name}_relres"] = r.history.relres
+        la[f"{name}_theta"] = r.history.theta
+        la[f"{name}_hist_iter"] = r.history.iteration
+        la[f"{name}_norm_estimate"] = np.array(r.norm_estimate)
+        la[f"{name}_dense_eigs"] = np.linalg.eigvalsh(rm.to_dense())[:k]
+        print("lanczos", name, "iterations", r.iterations, "converged", r.converged, r.eigenvalues)
+    np.savez_compressed(os.path.join(OUT, "lanczos.npz"), **la)
+
+
 def digest(h):
     m = hashlib.sha256()
     for a in (h.block_boundaries, h.entry_offsets, h.rows, h.cols, h.values, h.groups):
@@ -145,4 +195,8 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["lanczos"]:
+        make_lanczos()
+    else:
+        main()
+        make_lanczos()

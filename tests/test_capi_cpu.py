@@ -111,3 +111,17 @@ def test_write_history_csv_schema():
     s = io.StringIO()
     ci.write_history_csv(rep, s)
     assert s.getvalue() == "iter,col,relres,theta\n0,0,0.10000000000000001,-1.25\n1,0,1.0000000000000001e-09,-1.5\n"
+
+
+def test_lanczos_host_helpers():
+    """ci::lanczos_checkpoint (lanczos.cpp:11-15) and lanczos_default_start
+    (lanczos.cpp:17-22) -- host logic, no GPU needed."""
+    from oracle import ci_oracle as O
+
+    for m in list(range(1, 400)):
+        assert ci.lanczos_checkpoint(m) == O.lanczos_checkpoint(m)
+    v = ci.lanczos_default_start(10, 4)
+    np.testing.assert_array_equal(v, np.r_[np.full(4, 1.0 / np.sqrt(4.0)), np.zeros(6)])
+    assert np.linalg.norm(v) == pytest.approx(1.0, abs=1e-15)
+    with pytest.raises(ci.ConfigError):
+        ci.lanczos_default_start(10, 0)

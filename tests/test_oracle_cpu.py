@@ -167,6 +167,37 @@ def test_oracle_lobpcg(golden, name):
     np.testing.assert_allclose(r.eigenvalues, g[f"{name}_dense_eigs"], rtol=1e-8)
 
 
+def _diag100():
+    n = 100
+    return ci.CsbMatrix(dim=n, precision=1, block_boundaries=np.array([0, n], np.uint32),
+                        entry_offsets=np.array([0, n], np.uint64), rows=np.arange(n, dtype=np.uint16),
+                        cols=np.arange(n, dtype=np.uint16), values=np.arange(1, n + 1, dtype=np.float64),
+                        groups=np.array([0, 50, n], np.uint32))
+
+
+@pytest.mark.parametrize("name", ["diag100_restart", "sector_f64", "sector_f32"])
+def test_oracle_lanczos(golden, name):
+    """lanczos.cpp:24-136 restated in numpy vs the compiled reference: same
+    step count, convergence, counters and per-checkpoint convergence pattern;
+    Ritz values to 1e-10 relative (LAPACK vs Eigen tridiagonal QL), Ritz
+    vectors to 1e-6 up to sign. diag100_restart exercises the breakdown restart."""
+    g = golden("lanczos")
+    k, tol, max_iter, _ = g[f"{name}_meta"]
+    h = _diag100() if name.startswith("diag") else gen_from(g[f"{name}_params"])
+    r = O.lanczos_solve(lambda x: O.spmm(h, x), g[f"{name}_v0"], int(k), float(tol), int(max_iter))
+    assert r.converged == bool(g[f"{name}_converged"])
+    assert r.iterations == int(g[f"{name}_iterations"])
+    assert r.counters == g[f"{name}_counters"].tolist()
+    hist = np.array([[it, rr > tol] for it, _, rr, _ in r.history])
+    assert hist[:, 0].tolist() == g[f"{name}_hist_iter"].tolist()
+    assert hist[:, 1].tolist() == (g[f"{name}_relres"] > tol).tolist()
+    np.testing.assert_allclose([t for *_, t in r.history], g[f"{name}_theta"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(r.eigenvalues, g[f"{name}_eigenvalues"], rtol=1e-10)
+    np.testing.assert_allclose(r.eigenvalues, g[f"{name}_dense_eigs"], rtol=1e-7)
+    ov = np.abs(np.sum(r.trial_vectors * g[f"{name}_eigenvectors"], axis=0))
+    np.testing.assert_allclose(ov, 1.0, atol=1e-6)
+
+
 # ------------------------------------------------------- SPEC known answers
 
 def test_spec_spmm_known_answers():
