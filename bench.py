@@ -270,6 +270,38 @@ def lobpcg_record():
     return out
 
 
+def lanczos_record():
+    """Config-1 Lanczos baseline (lanczos.cpp:24-136) on the GPU vs the
+    reference's CPU Lanczos, same start (ones on the first sector, the
+    generator's lowest stratum), k_want 4, tol 1e-8."""
+    from paper_1609_01689_b200 import ci, configs
+
+    cfg = configs.CFG1
+    h = cfg.generate()
+    v0 = ci.lanczos_default_start(h.dim, h.dim // cfg.sectors)
+    opt = ci.LanczosOptions(k_want=cfg.k_want, tol=cfg.tol, max_iter=500)
+    ci.lanczos_solve(h, v0, opt)  # warm
+    t0 = time.perf_counter()
+    rep = ci.lanczos_solve(h, v0, opt)
+    ms = (time.perf_counter() - t0) * 1e3
+    out = {"workload": cfg.name + " (Lanczos)", "iterations": rep.iterations, "converged": rep.converged,
+           "ms": round(ms, 2), "split_ms": {k: round(v, 2) for k, v in rep.timing_ms.items()},
+           "eigenvalues": [float(v) for v in rep.eigenvalues]}
+    try:
+        from oracle import ref
+
+        if ref.available():
+            rm = ref.RefMatrix(h)
+            t0 = time.perf_counter()
+            rr = ref.lanczos_solve(rm, v0, cfg.k_want, cfg.tol, 500)
+            out["reference"] = {"iterations": rr.iterations, "ms": round((time.perf_counter() - t0) * 1e3, 2),
+                                "cores": ref.max_threads()}
+            out["max_rel_eig_diff"] = float(np.max(np.abs(rep.eigenvalues - rr.eigenvalues) / np.abs(rr.eigenvalues)))
+    except Exception as e:  # the record is informative only
+        out["reference_error"] = str(e)
+    return out
+
+
 def sweep_record(dev):
     """BASELINE config 3: the config-1 matrix (fp64, L2-resident) at m = 1..64:
     device time per SpMM (CUDA events, 20 back-to-back calls after warm-up),
@@ -320,10 +352,22 @@ def cfg4_record(dev):
     rep = ci.lobpcg_solve(dm, x0, ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol, preconditioner=td))
     tts = time.perf_counter() - t0
     rr = np.array([r.relres for r in rep.history]).reshape(-1, cfg.kt)
-    return {"workload": cfg.name, "n": cfg.n, "nnz_stored": dm.nnz, "tts_s": round(tts, 3),
-            "iterations": rep.iterations, "converged": rep.converged, "gen_on_gpu_s": round(gen_s, 2),
-            "split_ms": {k: round(v, 1) for k, v in rep.timing_ms.items()}, "counters": vars(rep.counters),
-            "max_final_relres": float(rr[-1, :cfg.k_want].max()), "eigenvalues": rep.eigenvalues.tolist()}
+    out = {"workload": cfg.name, "n": cfg.n, "nnz_stored": dm.nnz, "tts_s": round(tts, 3),
+           "iterations": rep.iterations, "converged": rep.converged, "gen_on_gpu_s": round(gen_s, 2),
+           "split_ms": {k: round(v, 1) for k, v in rep.timing_ms.items()}, "counters": vars(rep.counters),
+           "max_final_relres": float(rr[-1, :cfg.k_want].max()), "eigenvalues": rep.eigenvalues.tolist()}
+    # the paper's comparison: the Lanczos baseline on the same matrix
+    # (ones on the first sector, k_want 8, tol 1e-6, <= 500 steps)
+    del td
+    t0 = time.perf_counter()
+    la = ci.lanczos_solve(dm, ci.lanczos_default_start(cfg.n, cfg.n // cfg.sectors),
+                          ci.LanczosOptions(k_want=cfg.k_want, tol=cfg.tol, max_iter=500))
+    out["lanczos"] = {"tts_s": round(time.perf_counter() - t0, 3), "iterations": la.iterations,
+                      "converged": la.converged, "split_ms": {k: round(v, 1) for k, v in la.timing_ms.items()},
+                      "spmv_equivalents": la.counters.spmv_equivalents,
+                      "max_rel_eig_diff_vs_lobpcg": float(np.max(np.abs(la.eigenvalues - rep.eigenvalues) /
+                                                                 np.abs(rep.eigenvalues)))}
+    return out
 
 
 def group_bounds(cfg):
@@ -498,6 +542,7 @@ def ours(args):
         line["cpu_baseline"] = cpu_baseline(h, m)
     if world == 1 and not args.no_lobpcg:
         line["lobpcg"] = lobpcg_record()
+        line["lanczos"] = lanczos_record()
         line["sweep"] = sweep_record(dev)
         if not args.no_cfg4:
             del dm

@@ -24,6 +24,7 @@
 #include "ci/csb.hpp"
 #include "ci/errors.hpp"
 #include "ci/hamiltonian.hpp"
+#include "ci/lanczos.hpp"
 #include "ci/lobpcg.hpp"
 #include "ci/precond.hpp"
 #include "cieg.h"
@@ -193,14 +194,68 @@ SolveReport lobpcg_solve(const CsbMatrix& h, const BlockVectors& x0, const Lobpc
   return out;
 }
 
+// lanczos.hpp:26 -- host logic.
+bool lanczos_checkpoint(int m) { return cieg_lanczos_checkpoint(m) != 0; }
+
+// lanczos.hpp:30 -- ones on the lowest stratum, normalised.
+Eigen::VectorXd lanczos_default_start(const BasisTable& basis) {
+  Eigen::VectorXd v(basis.dimension());
+  check(cieg_lanczos_default_start(basis.dimension(), basis.stratum_end(0), v.data()));
+  return v;
+}
+
+// lanczos.hpp:35-36 -- ci::lanczos_solve on the GPU.
+SolveReport lanczos_solve(const CsbMatrix& h, const Eigen::VectorXd& v0, const LanczosOptions& opt) {
+  if (static_cast<std::uint32_t>(v0.size()) != h.dim) throw DimensionMismatch("lanczos: v0 dim != matrix dim");
+  if (v0.norm() == 0.0) throw ConfigError("lanczos: v0 must be nonzero");
+  if (opt.k_want < 1) throw ConfigError("lanczos: k_want must be >= 1");
+  cieg_lanczos_options o;
+  cieg_lanczos_options_default(&o);
+  o.k_want = opt.k_want;
+  o.tol = opt.tol;
+  o.max_iter = opt.max_iter;
+  if (opt.observer) {
+    o.observer = [](void* user, int m, const double* a, const double* b, const double* basis_host, std::uint32_t n) {
+      const auto* op = static_cast<const LanczosOptions*>(user);
+      Eigen::MatrixXd basis(n, m);
+      std::memcpy(basis.data(), basis_host, sizeof(double) * static_cast<std::size_t>(n) * m);
+      op->observer(m, basis, std::vector<double>(a, a + m), std::vector<double>(b, b + m));
+    };
+    o.observer_user = const_cast<LanczosOptions*>(&opt);
+  }
+  cieg_report* rep = nullptr;
+  check(cieg_lanczos_solve(dev().ctx, matrix(h), v0.data(), &o, &rep));
+  SolveReport out;
+  int conv = 0, iters = 0;
+  double ne = 0.0;
+  std::uint32_t kw = 0, kt = 0;
+  std::uint64_t nh = 0, cnt[4];
+  cieg_report_summary(rep, &conv, &iters, &ne, &kw, &kt, &nh);
+  cieg_report_counters(rep, cnt);
+  out.converged = conv != 0;
+  out.iterations = iters;
+  out.norm_estimate = ne;
+  out.counters = OperationCounters{cnt[0], cnt[1], cnt[2], cnt[3]};
+  out.eigenvalues.resize(kw);
+  cieg_report_eigenvalues(rep, out.eigenvalues.data());
+  out.eigenvectors = BlockVectors(h.dim, kw);
+  cieg_report_trial_vectors(rep, out.eigenvectors.values().data());
+  out.trial_vectors = out.eigenvectors;
+  std::vector<int> hi(nh), hc(nh);
+  std::vector<double> hr(nh), ht(nh);
+  cieg_report_history(rep, hi.data(), hc.data(), hr.data(), ht.data());
+  for (std::uint64_t i = 0; i < nh; ++i) out.history.push_back({hi[i], hc[i], hr[i], ht[i]});
+  cieg_report_destroy(rep);
+  return out;
+}
+
 }  // namespace ci
 
 // C entry for the test harness: run the reference-API call sequence of the
 // CLI's run_solver (ci_eigen.cpp:139-151) through the drop-in.
-extern "C" int dropin_lobpcg(const cieg_csb_view* v, const std::uint32_t* groups, std::uint32_t ng,
-                             const double* x0, std::uint32_t kt, int k_want, double tol, int use_prec,
-                             double* eig_out, int* iters_out) {
-  try {
+namespace {
+// cieg_csb_view -> ci::CsbMatrix (the caller-side object the drop-in receives)
+ci::CsbMatrix from_view(const cieg_csb_view* v) {
     ci::CsbMatrix h;
     h.dim = v->dim;
     h.precision = v->precision == 0 ? ci::Precision::Single : ci::Precision::Double;
@@ -217,6 +272,15 @@ extern "C" int dropin_lobpcg(const cieg_csb_view* v, const std::uint32_t* groups
         blk.values64.assign(static_cast<const double*>(v->values) + e0, static_cast<const double*>(v->values) + e1);
       h.nnz_lower += blk.size();
     }
+    return h;
+}
+}  // namespace
+
+extern "C" int dropin_lobpcg(const cieg_csb_view* v, const std::uint32_t* groups, std::uint32_t ng,
+                             const double* x0, std::uint32_t kt, int k_want, double tol, int use_prec,
+                             double* eig_out, int* iters_out) {
+  try {
+    ci::CsbMatrix h = from_view(v);
     ci::TileDiagonal td;
     if (use_prec) {
       for (std::uint32_t g = 0; g < ng; ++g) {
@@ -249,6 +313,26 @@ extern "C" int dropin_lobpcg(const cieg_csb_view* v, const std::uint32_t* groups
     opt.preconditioner = use_prec ? &td : nullptr;
     ci::SolveReport rep = ci::lobpcg_solve(h, X0, opt);
     for (int j = 0; j < k_want; ++j) eig_out[j] = rep.eigenvalues[j];
+    *iters_out = rep.iterations;
+    return 0;
+  } catch (const ci::Error& e) {
+    return 1;
+  }
+}
+
+// Lanczos through the reference API (lanczos.hpp:35-36).
+extern "C" int dropin_lanczos(const cieg_csb_view* v, const double* v0, int k_want, double tol, int max_iter,
+                              double* eig_out, int* iters_out) {
+  try {
+    ci::CsbMatrix h = from_view(v);
+    Eigen::VectorXd x(h.dim);
+    std::memcpy(x.data(), v0, sizeof(double) * h.dim);
+    ci::LanczosOptions opt;
+    opt.k_want = k_want;
+    opt.tol = tol;
+    opt.max_iter = max_iter;
+    ci::SolveReport rep = ci::lanczos_solve(h, x, opt);
+    for (int j = 0; j < k_want && j < static_cast<int>(rep.eigenvalues.size()); ++j) eig_out[j] = rep.eigenvalues[j];
     *iters_out = rep.iterations;
     return 0;
   } catch (const ci::Error& e) {

@@ -32,6 +32,84 @@ namespace cieg_dense {
 
 using Index = std::ptrdiff_t;
 
+// Implicit QL on a symmetric tridiagonal (tql2): d diagonal, e[i] the entry
+// coupling i-1 and i (e[0] unused); the rotations are accumulated into V
+// (rows x n col-major: the tridiagonalising transform, the identity, or any
+// subset of its rows -- every row is updated independently, so tracking one
+// row yields exactly that row of the full result). Writes ascending
+// eigenvalues w and the rows x n eigenvector rows z (stable order on ties).
+inline bool tql2_sorted(Index n, std::vector<double>& d, std::vector<double>& e, std::vector<double>& V, double* w,
+                        double* z, Index rows = -1) {
+  if (rows < 0) rows = n;
+  auto v = [&](Index i, Index j) -> double& { return V[static_cast<size_t>(i + j * rows)]; };
+  for (Index i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  double f = 0.0, tst1 = 0.0;
+  const double eps = std::ldexp(1.0, -52);
+  for (Index l = 0; l < n; ++l) {
+    tst1 = std::max(tst1, std::fabs(d[l]) + std::fabs(e[l]));
+    Index m = l;
+    while (m < n) {
+      if (std::fabs(e[m]) <= eps * tst1) break;
+      ++m;
+    }
+    if (m == n) m = n - 1;
+    if (m > l) {
+      int iter = 0;
+      do {
+        if (++iter > 60) return false;
+        double g = d[l];
+        double p = (d[l + 1] - g) / (2.0 * e[l]);
+        double r = std::hypot(p, 1.0);
+        if (p < 0) r = -r;
+        d[l] = e[l] / (p + r);
+        d[l + 1] = e[l] * (p + r);
+        double dl1 = d[l + 1];
+        double h = g - d[l];
+        for (Index i = l + 2; i < n; ++i) d[i] -= h;
+        f += h;
+        p = d[m];
+        double c = 1.0, c2 = c, c3 = c;
+        double el1 = e[l + 1];
+        double s = 0.0, s2 = 0.0;
+        for (Index i = m - 1; i >= l; --i) {
+          c3 = c2;
+          c2 = c;
+          s2 = s;
+          g = c * e[i];
+          h = c * p;
+          r = std::hypot(p, e[i]);
+          e[i + 1] = s * r;
+          s = e[i] / r;
+          c = p / r;
+          p = c * d[i] - s * g;
+          d[i + 1] = h + s * (c * g + s * d[i]);
+          for (Index k = 0; k < rows; ++k) {
+            h = v(k, i + 1);
+            v(k, i + 1) = s * v(k, i) + c * h;
+            v(k, i) = c * v(k, i) - s * h;
+          }
+          if (i == 0) break;
+        }
+        p = -s * s2 * c3 * el1 * e[l] / dl1;
+        e[l] = s * p;
+        d[l] = c * p;
+      } while (std::fabs(e[l]) > eps * tst1);
+    }
+    d[l] = d[l] + f;
+    e[l] = 0.0;
+  }
+  // Stable ascending sort of eigenpairs.
+  std::vector<Index> order(static_cast<size_t>(n));
+  std::iota(order.begin(), order.end(), Index{0});
+  std::stable_sort(order.begin(), order.end(), [&](Index x, Index y) { return d[x] < d[y]; });
+  for (Index j = 0; j < n; ++j) {
+    w[j] = d[order[j]];
+    for (Index i = 0; i < rows; ++i) z[i + j * rows] = v(i, order[j]);
+  }
+  return true;
+}
+
 // a: n x n column-major symmetric (only the lower triangle is read).
 // On return: w ascending eigenvalues, z (n x n col-major) eigenvectors.
 // Returns false if the QL iteration fails to converge.
@@ -116,83 +194,30 @@ inline bool sym_eig(Index n, const double* a, double* w, double* z) {
   v(n - 1, n - 1) = 1.0;
   e[0] = 0.0;
 
-  // Implicit QL on the tridiagonal (tql2).
-  for (Index i = 1; i < n; ++i) e[i - 1] = e[i];
-  e[n - 1] = 0.0;
-  double f = 0.0, tst1 = 0.0;
-  const double eps = std::ldexp(1.0, -52);
-  for (Index l = 0; l < n; ++l) {
-    tst1 = std::max(tst1, std::fabs(d[l]) + std::fabs(e[l]));
-    Index m = l;
-    while (m < n) {
-      if (std::fabs(e[m]) <= eps * tst1) break;
-      ++m;
-    }
-    if (m == n) m = n - 1;
-    if (m > l) {
-      int iter = 0;
-      do {
-        if (++iter > 60) return false;
-        double g = d[l];
-        double p = (d[l + 1] - g) / (2.0 * e[l]);
-        double r = std::hypot(p, 1.0);
-        if (p < 0) r = -r;
-        d[l] = e[l] / (p + r);
-        d[l + 1] = e[l] * (p + r);
-        double dl1 = d[l + 1];
-        double h = g - d[l];
-        for (Index i = l + 2; i < n; ++i) d[i] -= h;
-        f += h;
-        p = d[m];
-        double c = 1.0, c2 = c, c3 = c;
-        double el1 = e[l + 1];
-        double s = 0.0, s2 = 0.0;
-        for (Index i = m - 1; i >= l; --i) {
-          c3 = c2;
-          c2 = c;
-          s2 = s;
-          g = c * e[i];
-          h = c * p;
-          r = std::hypot(p, e[i]);
-          e[i + 1] = s * r;
-          s = e[i] / r;
-          c = p / r;
-          p = c * d[i] - s * g;
-          d[i + 1] = h + s * (c * g + s * d[i]);
-          for (Index k = 0; k < n; ++k) {
-            h = v(k, i + 1);
-            v(k, i + 1) = s * v(k, i) + c * h;
-            v(k, i) = c * v(k, i) - s * h;
-          }
-          if (i == 0) break;
-        }
-        p = -s * s2 * c3 * el1 * e[l] / dl1;
-        e[l] = s * p;
-        d[l] = c * p;
-      } while (std::fabs(e[l]) > eps * tst1);
-    }
-    d[l] = d[l] + f;
-    e[l] = 0.0;
-  }
-  // Stable ascending sort of eigenpairs.
-  std::vector<Index> order(static_cast<size_t>(n));
-  std::iota(order.begin(), order.end(), Index{0});
-  std::stable_sort(order.begin(), order.end(), [&](Index x, Index y) { return d[x] < d[y]; });
-  for (Index j = 0; j < n; ++j) {
-    w[j] = d[order[j]];
-    for (Index i = 0; i < n; ++i) z[i + j * n] = v(i, order[j]);
-  }
-  return true;
+  return tql2_sorted(n, d, e, V, w, z);
 }
 
 // Symmetric tridiagonal eigenproblem (diag n, sub n-1); QL with eigenvectors
 // accumulated from the identity. Used by Lanczos (lanczos.cpp:54-63).
 inline bool tridiag_eig(Index n, const double* diag, const double* sub, double* w, double* z) {
+  // Eigen's computeFromTridiagonal: the QL iteration straight on the
+  // tridiagonal, rotations accumulated from the identity (no reduction step).
   if (n == 0) return true;
-  std::vector<double> a(static_cast<size_t>(n * n), 0.0);
-  for (Index i = 0; i < n; ++i) a[i + i * n] = diag[i];
-  for (Index i = 0; i + 1 < n; ++i) a[(i + 1) + i * n] = sub[i];
-  return sym_eig(n, a.data(), w, z);
+  std::vector<double> d(diag, diag + n), e(static_cast<size_t>(n), 0.0), V(static_cast<size_t>(n * n), 0.0);
+  for (Index i = 1; i < n; ++i) e[i] = sub[i - 1];
+  for (Index i = 0; i < n; ++i) V[static_cast<size_t>(i + i * n)] = 1.0;
+  return tql2_sorted(n, d, e, V, w, z);
+}
+
+// Eigenvalues and the BOTTOM row of the eigenvector matrix of a tridiagonal
+// (what the Lanczos residual test reads, lanczos.cpp:112-114) in O(n^2):
+// bitwise equal to the last row of tridiag_eig's z.
+inline bool tridiag_eig_bottom(Index n, const double* diag, const double* sub, double* w, double* zlast) {
+  if (n == 0) return true;
+  std::vector<double> d(diag, diag + n), e(static_cast<size_t>(n), 0.0), V(static_cast<size_t>(n), 0.0);
+  for (Index i = 1; i < n; ++i) e[i] = sub[i - 1];
+  V[static_cast<size_t>(n - 1)] = 1.0;
+  return tql2_sorted(n, d, e, V, w, zlast, 1);
 }
 
 // In-place Cholesky a = L L^T of the lower triangle (column major); on success

@@ -30,15 +30,16 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kColsPerPass = 8;
-constexpr int kCoeffChunk = 2048;  // coefficients staged in shared memory per pass of the update
+constexpr int kUpdCols = 64;  // basis columns per CTA of the GEMV update
 
-// Fixed CTA count for the n-length reductions: a function of n only, so the
-// summation order (and the result) does not depend on the device.
+// Fixed row-chunk count for the n-length reductions: a function of n only,
+// so the summation order (and the result) does not depend on the device.
 std::uint32_t reduction_ctas(std::uint32_t n) {
-  return std::max<std::uint32_t>(1, std::min<std::uint32_t>(1024, (n + 2047) / 2048));
+  return std::max<std::uint32_t>(1, std::min<std::uint32_t>(1024, (n + 511) / 512));
 }
 
-// partial[g * m + j] = sum over CTA g's rows of V[r, j] * w[r]  (V column-major, ld)
+// partial[g * m + j] = sum over row chunk g of V[r, j] * w[r]  (V column-major, ld);
+// grid (row chunks, column groups of kColsPerPass)
 __global__ void __launch_bounds__(kThreads) gemvt_partial_kernel(const double* __restrict__ v, std::size_t ld,
                                                                  std::uint32_t n, std::uint32_t m,
                                                                  const double* __restrict__ w,
@@ -47,29 +48,27 @@ __global__ void __launch_bounds__(kThreads) gemvt_partial_kernel(const double* _
   const std::uint32_t chunk = (n + gridDim.x - 1) / gridDim.x;
   const std::uint32_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (std::uint32_t j0 = 0; j0 < m; j0 += kColsPerPass) {
-    double acc[kColsPerPass];
+  const std::uint32_t j0 = blockIdx.y * kColsPerPass;
+  double acc[kColsPerPass];
 #pragma unroll
-    for (int c = 0; c < kColsPerPass; ++c) acc[c] = 0.0;
-    for (std::uint32_t r = r0 + threadIdx.x; r < r1; r += kThreads) {
-      const double wr = w[r];
-#pragma unroll
-      for (int c = 0; c < kColsPerPass; ++c)
-        if (j0 + c < m) acc[c] = fma(v[(j0 + c) * ld + r], wr, acc[c]);
-    }
+  for (int c = 0; c < kColsPerPass; ++c) acc[c] = 0.0;
+  for (std::uint32_t r = r0 + threadIdx.x; r < r1; r += kThreads) {
+    const double wr = w[r];
 #pragma unroll
     for (int c = 0; c < kColsPerPass; ++c)
-      for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o);
-    if (lane == 0)
+      if (j0 + c < m) acc[c] = fma(v[(j0 + c) * ld + r], wr, acc[c]);
+  }
 #pragma unroll
-      for (int c = 0; c < kColsPerPass; ++c) red[warp][c] = acc[c];
-    __syncthreads();
-    if (threadIdx.x < kColsPerPass && j0 + threadIdx.x < m) {
-      double s = 0.0;
-      for (int k = 0; k < kThreads / 32; ++k) s += red[k][threadIdx.x];
-      partial[static_cast<std::size_t>(blockIdx.x) * m + j0 + threadIdx.x] = s;
-    }
-    __syncthreads();
+  for (int c = 0; c < kColsPerPass; ++c)
+    for (int o = 16; o > 0; o >>= 1) acc[c] += __shfl_down_sync(0xffffffffu, acc[c], o);
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < kColsPerPass; ++c) red[warp][c] = acc[c];
+  __syncthreads();
+  if (threadIdx.x < kColsPerPass && j0 + threadIdx.x < m) {
+    double s = 0.0;
+    for (int k = 0; k < kThreads / 32; ++k) s += red[k][threadIdx.x];
+    partial[static_cast<std::size_t>(blockIdx.x) * m + j0 + threadIdx.x] = s;
   }
 }
 
@@ -83,23 +82,31 @@ __global__ void reduce_partials_kernel(const double* __restrict__ partial, std::
   out[j] = s;
 }
 
-// w[r] -= sum_j V[r, j] * coeff[j]   (Eigen: tmp = V * coeff; w -= tmp)
-__global__ void __launch_bounds__(kThreads) gemv_update_kernel(const double* __restrict__ v, std::size_t ld,
-                                                               std::uint32_t n, std::uint32_t m,
-                                                               const double* __restrict__ coeff,
-                                                               double* __restrict__ w) {
-  __shared__ double c[kCoeffChunk];
+// tmp[c * n + r] = sum_{j in column chunk c} V[r, j] * coeff[j]; grid (row blocks, column chunks)
+__global__ void __launch_bounds__(kThreads) gemv_partial_kernel(const double* __restrict__ v, std::size_t ld,
+                                                                std::uint32_t n, std::uint32_t m,
+                                                                const double* __restrict__ coeff,
+                                                                double* __restrict__ tmp) {
+  __shared__ double c[kUpdCols];
+  const std::uint32_t j0 = blockIdx.y * kUpdCols;
+  const std::uint32_t jn = min(static_cast<std::uint32_t>(kUpdCols), m - j0);
+  for (std::uint32_t j = threadIdx.x; j < jn; j += kThreads) c[j] = coeff[j0 + j];
+  __syncthreads();
   const std::uint32_t r = blockIdx.x * kThreads + threadIdx.x;
+  if (r >= n) return;
   double s = 0.0;
-  for (std::uint32_t j0 = 0; j0 < m; j0 += kCoeffChunk) {
-    const std::uint32_t jn = min(static_cast<std::uint32_t>(kCoeffChunk), m - j0);
-    __syncthreads();
-    for (std::uint32_t j = threadIdx.x; j < jn; j += kThreads) c[j] = coeff[j0 + j];
-    __syncthreads();
-    if (r < n)
-      for (std::uint32_t j = 0; j < jn; ++j) s = fma(v[(j0 + j) * ld + r], c[j], s);
-  }
-  if (r < n) w[r] -= s;
+  for (std::uint32_t j = 0; j < jn; ++j) s = fma(v[(j0 + j) * ld + r], c[j], s);
+  tmp[static_cast<std::size_t>(blockIdx.y) * n + r] = s;
+}
+
+// w[r] -= sum_c tmp[c * n + r], chunks ascending   (Eigen: tmp = V * coeff; w -= tmp)
+__global__ void gemv_finish_kernel(const double* __restrict__ tmp, std::uint32_t chunks, std::uint32_t n,
+                                   double* __restrict__ w) {
+  const std::uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  double s = 0.0;
+  for (std::uint32_t c = 0; c < chunks; ++c) s += tmp[static_cast<std::size_t>(c) * n + r];
+  w[r] -= s;
 }
 
 // w = w - a * v1 - b * v2   (lanczos.cpp:70-71; v2 may be null)
@@ -166,7 +173,8 @@ class Lanczos {
   }
   // out[0..m) = V[:, :m]^T w   (device)
   void gemvt(const double* v, int m, const double* w, double* out) {
-    gemvt_partial_kernel<<<g_, kThreads, 0, ctx_->stream>>>(v, n_, n_, static_cast<std::uint32_t>(m), w, partial_);
+    const dim3 grid(g_, (m + kColsPerPass - 1) / kColsPerPass);
+    gemvt_partial_kernel<<<grid, kThreads, 0, ctx_->stream>>>(v, n_, n_, static_cast<std::uint32_t>(m), w, partial_);
     reduce_partials_kernel<<<(m + 127) / 128, 128, 0, ctx_->stream>>>(partial_, g_, static_cast<std::uint32_t>(m), out);
     launched(2);
   }
@@ -181,18 +189,32 @@ class Lanczos {
   void reorthogonalize(double* w, int m) {
     for (int pass = 0; pass < 2; ++pass) {
       gemvt(basis_, m, w, coeff_);
-      gemv_update_kernel<<<blocks_for(n_), kThreads, 0, ctx_->stream>>>(basis_, n_, n_, static_cast<std::uint32_t>(m),
-                                                                        coeff_, w);
-      launched();
+      const std::uint32_t chunks = (m + kUpdCols - 1) / kUpdCols;
+      gemv_partial_kernel<<<dim3(blocks_for(n_), chunks), kThreads, 0, ctx_->stream>>>(
+          basis_, n_, n_, static_cast<std::uint32_t>(m), coeff_, tmp_);
+      gemv_finish_kernel<<<blocks_for(n_), kThreads, 0, ctx_->stream>>>(tmp_, chunks, n_, w);
+      launched(2);
     }
   }
-  void factorize(int m) {  // lanczos.cpp:54-63
+  // lanczos.cpp:54-63. At checkpoints only the Ritz values and the bottom
+  // row of the eigenvector matrix are needed (the residual test): O(m^2),
+  // bitwise equal to the full factorisation's values; the full vectors are
+  // formed once, for the returned Ritz vectors.
+  void factorize(int m, bool full) {
     ritz_.assign(m, 0.0);
-    ritz_vecs_.assign(static_cast<std::size_t>(m) * m, 0.0);
     std::vector<double> sub(std::max(m - 1, 0));
     for (int i = 0; i + 1 < m; ++i) sub[i] = beta_[i];
-    if (!cieg_dense::tridiag_eig(m, alpha_.data(), sub.data(), ritz_.data(), ritz_vecs_.data()))
-      fail(CIEG_ERR_INDEFINITE, "lanczos: tridiagonal eigensolver did not converge");
+    bool ok;
+    if (full) {
+      ritz_vecs_.assign(static_cast<std::size_t>(m) * m, 0.0);
+      ok = cieg_dense::tridiag_eig(m, alpha_.data(), sub.data(), ritz_.data(), ritz_vecs_.data());
+      bottom_.resize(m);
+      for (int j = 0; j < m; ++j) bottom_[j] = ritz_vecs_[(m - 1) + static_cast<std::size_t>(j) * m];
+    } else {
+      bottom_.assign(m, 0.0);
+      ok = cieg_dense::tridiag_eig_bottom(m, alpha_.data(), sub.data(), ritz_.data(), bottom_.data());
+    }
+    if (!ok) fail(CIEG_ERR_INDEFINITE, "lanczos: tridiagonal eigensolver did not converge");
     factorized_ = m;
   }
 
@@ -208,7 +230,8 @@ class Lanczos {
   double* coeff_ = nullptr;
   double* partial_ = nullptr;
   double* scalar_ = nullptr;
-  std::vector<double> alpha_, beta_, ritz_, ritz_vecs_;
+  double* tmp_ = nullptr;  // GEMV partials: ceil(m / kUpdCols) x n
+  std::vector<double> alpha_, beta_, ritz_, ritz_vecs_, bottom_;
   int factorized_ = 0;
 };
 
@@ -230,6 +253,7 @@ void Lanczos::run(const double* v0_host) {
   coeff_ = alloc(max_steps + 1);
   partial_ = alloc(static_cast<std::size_t>(g_) * (max_steps + 1));
   scalar_ = alloc(1);
+  tmp_ = alloc(static_cast<std::size_t>(n_) * ((max_steps + kUpdCols) / kUpdCols));
   {
     std::vector<double> v(n_);
     for (std::uint32_t i = 0; i < n_; ++i) v[i] = v0_host[i] / v0n;
@@ -283,13 +307,13 @@ void Lanczos::run(const double* v0_host) {
     if (!checkpoint && !last) continue;
 
     Clock c(ctx_, &rep_.timing_ms[kRR]);
-    factorize(m);
+    factorize(m, false);
     rep_.norm_estimate = std::max({rep_.norm_estimate, std::fabs(ritz_[0]), std::fabs(ritz_[m - 1])});
     const int k = std::min(opt_.k_want, m);
     bool all_converged = k >= opt_.k_want;
     for (int j = 0; j < k; ++j) {
       // |beta_m| times the bottom eigenvector component (lanczos.cpp:112-116)
-      const double res = std::fabs(beta_[m - 1]) * std::fabs(ritz_vecs_[(m - 1) + static_cast<std::size_t>(j) * m]);
+      const double res = std::fabs(beta_[m - 1]) * std::fabs(bottom_[j]);
       const double relres = res / std::max(rep_.norm_estimate, 1e-300);
       rep_.history.push_back({m, j, relres, ritz_[j]});
       if (relres > opt_.tol) all_converged = false;
@@ -308,7 +332,7 @@ void Lanczos::run(const double* v0_host) {
   }
 
   Clock c(ctx_, &rep_.timing_ms[kOther]);
-  if (factorized_ == 0) factorize(static_cast<int>(alpha_.size()));
+  factorize(factorized_ == 0 ? static_cast<int>(alpha_.size()) : factorized_, true);
   const int k = std::min(opt_.k_want, factorized_);
   rep_.eigenvalues.assign(ritz_.begin(), ritz_.begin() + k);
   rep_.k_want = rep_.kt = static_cast<std::uint32_t>(k);

@@ -35,3 +35,24 @@ def test_dropin_lobpcg_matches_reference(golden, name):
     assert rc == 0
     assert iters.value == int(g[f"{name}_iterations"])
     np.testing.assert_allclose(eig, g[f"{name}_eigenvalues"], rtol=1e-10)
+
+
+@pytest.mark.parametrize("name", ["sector_f64", "sector_f32"])
+def test_dropin_lanczos_matches_reference(golden, name):
+    """ci::lanczos_solve through the reference-side drop-in on the GPU."""
+    if not os.path.exists(LIB):
+        pytest.skip("integration/_build not built (needs the reference headers at build time)")
+    lib = C.CDLL(LIB)
+    g = golden("lanczos")
+    k, tol, max_iter, _ = g[f"{name}_meta"]
+    h = gen_from(g[f"{name}_params"])
+    v0 = np.ascontiguousarray(g[f"{name}_v0"])
+    v = h.view()
+    eig = np.zeros(int(k))
+    iters = C.c_int()
+    rc = lib.dropin_lanczos(C.byref(v), v0.ctypes.data_as(C.POINTER(C.c_double)), C.c_int(int(k)),
+                            C.c_double(float(tol)), C.c_int(int(max_iter)), eig.ctypes.data_as(C.POINTER(C.c_double)),
+                            C.byref(iters))
+    assert rc == 0
+    assert iters.value == int(g[f"{name}_iterations"])
+    np.testing.assert_allclose(eig, g[f"{name}_eigenvalues"], rtol=1e-10)
