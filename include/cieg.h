@@ -97,6 +97,12 @@ typedef struct {
 int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb,
                        const uint32_t* group_bounds, uint32_t ngroups,
                        uint32_t tile_edge, cieg_mat** out);
+/* cieg_matrix_upload with extra mandatory device-panel boundaries cuts[ncuts]
+ * (e.g. the truncation dimensions of cieg_multilevel_guess, so their leading
+ * blocks can be viewed without copying). */
+int cieg_matrix_upload_cuts(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                            uint32_t ngroups, uint32_t tile_edge, const uint32_t* cuts, uint32_t ncuts,
+                            cieg_mat** out);
 int cieg_matrix_destroy(cieg_mat* mat);
 /* dim, stored nnz (lower incl. diagonal), device panels, device tiles,
  * tile edge, precision, device bytes of the tile stream. */
@@ -252,6 +258,56 @@ int cieg_report_history(const cieg_report* rep, int* iteration, int* column, dou
 /* Device-event time split of the solve in milliseconds:
  * [spmm, rayleigh_ritz, orthonormalization, preconditioner, residual, other, total]. */
 int cieg_report_timing(const cieg_report* rep, double* ms7);
+
+/* ---- lobpcg.hpp public helpers ------------------------------------------ */
+/* ci::orthonormalize (lobpcg.hpp:92-93, lobpcg.cpp:89-119): y_dev (row-major
+ * n x k, device) is projected against against_dev (n x ka, may be NULL) twice,
+ * rank-revealing column selection at drop_tol, CholQR twice; the result is
+ * written back packed (n x k_out, ld = k_out). */
+int cieg_orthonormalize(cieg_ctx* ctx, double* y_dev, uint32_t n, uint32_t k, double drop_tol,
+                        const double* against_dev, uint32_t ka, uint32_t* k_out);
+/* ci::rayleigh_ritz (lobpcg.hpp:84-86, lobpcg.cpp:121-145) on an orthonormal
+ * basis Y and HY (device, n x m row-major): theta_out[k_trial], g_out
+ * (m x k_trial column-major). CIEG_ERR_INDEFINITE when Y^T Y deviates from I
+ * by more than 1e-6. */
+int cieg_rayleigh_ritz(cieg_ctx* ctx, const double* y_dev, const double* hy_dev, uint32_t n, uint32_t m,
+                       uint32_t k_trial, double* theta_out, double* g_out);
+/* ci::residual_norms (lobpcg.hpp:97-99, lobpcg.cpp:147-169): relative
+ * residuals |H x_j - theta_j x_j| / max(est |x_j|, 1e-300); norm_est <= 0
+ * means "none" (est = max |theta|). x_dev device n x k row-major. */
+int cieg_residual_norms(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, uint32_t k, const double* theta,
+                        double norm_est, double* out);
+
+/* ---- starting blocks (proj/include/ci/guess.hpp) ----------------------- */
+/* Leading principal block H[0:dim, 0:dim] of an uploaded matrix as a matrix
+ * of its own, sharing the parent's device tile stream (valid while the
+ * parent lives); dim must end on a device panel boundary (e.g. a sector or
+ * group boundary). The truncated-space problems of multilevel_guess. */
+int cieg_matrix_leading_view(cieg_ctx* ctx, const cieg_mat* mat, uint32_t dim, cieg_mat** out);
+/* ci::pad_from_subspace (guess.hpp:21, guess.cpp:14-23), host buffers. */
+int cieg_pad_from_subspace(const double* x_host, uint32_t n1, uint32_t k, uint32_t dim, double* out_host);
+typedef struct {
+  int k_want;    /* guess.hpp:49 */
+  int k_trial;   /* guess.hpp:50 */
+  double tol;    /* guess.hpp:51 */
+  int max_iter;  /* guess.hpp:52 */
+  uint64_t seed; /* guess.hpp:53 */
+} cieg_multilevel_options;
+void cieg_multilevel_options_default(cieg_multilevel_options* opt);
+typedef struct { /* ci::LevelReport (guess.hpp:31-37); nmax -> the level dimension */
+  uint32_t dim;
+  int iterations;
+  int converged;
+  double seconds;
+} cieg_level_report;
+/* ci::multilevel_guess (guess.hpp:60-62, guess.cpp:66-117): level_dims[0..nlevels)
+ * are the ascending truncated dimensions (leading blocks, reference levels =
+ * nlevels + 1); unpreconditioned LOBPCG per level, random start at the
+ * smallest. guess_host: n x k_trial row-major capacity, k_out = its width
+ * (packed); levels_out[nlevels]. */
+int cieg_multilevel_guess(cieg_ctx* ctx, const cieg_mat* mat, const uint32_t* level_dims, uint32_t nlevels,
+                          const cieg_multilevel_options* opt, double* guess_host, uint32_t* k_out,
+                          cieg_level_report* levels_out);
 
 /* ---- Lanczos baseline (proj/include/ci/lanczos.hpp) -------------------- */
 /* Checkpoint hook (LanczosOptions::observer, lanczos.hpp:18-21): step count,

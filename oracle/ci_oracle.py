@@ -754,3 +754,74 @@ def lanczos_solve(matvec, v0, k_want, tol, max_iter=500):
     k = min(k_want, factorized)
     x = basis[:, :factorized] @ ritz_vecs[:, :k]  # :131-132
     return Report(ritz[:k].copy(), x, history, counters, converged, iterations, norm_est, [])
+
+
+# ------------------------------------------------------- lobpcg.cpp helpers
+
+def rayleigh_ritz(y_basis, hy, k_trial):
+    """lobpcg.cpp:121-145: overlap check (1e-6), eig_sym of Y^T HY, leading
+    k_trial eigenpairs."""
+    m = y_basis.shape[1]
+    if k_trial > m:
+        raise ValueError("DimensionMismatch: rayleigh_ritz: k_trial exceeds basis width")
+    overlap = block_inner(y_basis, y_basis)
+    dev = np.abs(overlap - np.eye(m)).max()
+    if dev > 1e-6:
+        raise ValueError(f"IndefiniteGram: basis overlap deviates from identity by {dev}")
+    evals, evecs = _eig_sym(block_inner(y_basis, hy))
+    return evals[:k_trial].copy(), evecs[:, :k_trial].copy()
+
+
+def residual_norms(h, x, theta, norm_est=None):
+    """lobpcg.cpp:147-169."""
+    r = spmm(h, x) - x * np.asarray(theta)[None, :]
+    rn = column_norms(r)
+    xn = column_norms(x)
+    est = norm_est if norm_est is not None else 0.0
+    if not est > 0.0:
+        est = max([0.0] + [abs(t) for t in theta])
+    return [rn[j] / max(est * xn[j], K_TINY_DIAG) for j in range(x.shape[1])]
+
+
+# ---------------------------------------------------------------- guess.cpp
+
+def pad_from_subspace(x1, dim):
+    """guess.cpp:14-23."""
+    out = np.zeros((dim, x1.shape[1]))
+    out[: x1.shape[0]] = x1
+    return out
+
+
+def _widen_to(x, k_trial, seed):
+    """guess.cpp:57-62."""
+    if x.shape[1] >= k_trial:
+        return x
+    extra = random_block(x.shape[0], k_trial - x.shape[1], (int(mix64(np.uint64(seed))) + 1) & M64)
+    extra = orthonormalize(extra, 1e-8, against=x)
+    return np.hstack([x, extra])
+
+
+def multilevel_guess(h, level_dims, k_want=8, k_trial=12, tol=1e-6, max_iter=500, seed=1):
+    """guess.cpp:66-117 with the truncated problems taken as the leading
+    blocks H[0:d, 0:d] (d in level_dims): random orthonormal start at the
+    smallest level, unpreconditioned LOBPCG per level, zero-pad + widen_to
+    into the next space. Returns (guess, [(dim, iterations, converged)])."""
+    n = h.dim
+    levels = len(level_dims) + 1
+    if levels == 1:
+        return orthonormalize(random_block(n, k_trial, seed)), []
+    carried = None
+    reports = []
+    for level, d in enumerate(level_dims):
+        width = min(k_trial, d)
+        if level == 0:
+            x0 = orthonormalize(random_block(d, width, seed))
+        else:
+            x0 = _widen_to(pad_from_subspace(carried, d), width, seed + level)
+        if x0.shape[1] < k_want:
+            raise ValueError("SubspaceCollapse: level guess lost too many columns")
+        r = lobpcg_solve(h, x0, k_want, tol, max_iter,
+                         matvec=lambda v, d=d: spmm(h, pad_from_subspace(v, n))[:d])
+        carried = r.trial_vectors
+        reports.append((d, r.iterations, r.converged))
+    return _widen_to(pad_from_subspace(carried, n), k_trial, seed + levels), reports

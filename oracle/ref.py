@@ -138,7 +138,8 @@ def orthonormalize(y, drop_tol=1e-8, against=None):
         ap, ka = None, 0
     _chk(load().ciref_orthonormalize(C.c_uint32(y.shape[0]), _p(y), C.c_uint32(y.shape[1]), C.c_double(drop_tol),
                                      ap, C.c_uint32(ka), _p(out), C.byref(kout)))
-    return out[:, :kout.value].copy() if kout.value else np.zeros((y.shape[0], 0))
+    k = kout.value  # the result is packed n x k (row-major)
+    return out.reshape(-1)[: y.shape[0] * k].reshape(y.shape[0], k).copy() if k else np.zeros((y.shape[0], 0))
 
 
 class RefTileDiagonal:
@@ -240,3 +241,83 @@ def lanczos_solve(refmat: RefMatrix, v0, k_want, tol, max_iter=500):
     _chk(load().ciref_lanczos_solve(refmat.handle, _p(v0), C.c_int(k_want), C.c_double(tol), C.c_int(max_iter),
                                     C.byref(out)))
     return _report(out, refmat.h.dim)
+
+
+class SyntheticProblem:
+    """ci::build_synthetic_problem (hamiltonian.cpp:205-224): the reference's
+    physics-basis synthetic Hamiltonian (basis enumeration, grouping, tiles,
+    assembly), for pinning the multilevel guess."""
+
+    def __init__(self, Z, N, M2, parity, Nmax, hw=1.0, seed=1, offdiag=0.1, d=2, beta=2000, precision=1):
+        lib = load()
+        self.spec = (Z, N, M2, parity, Nmax, hw)
+        self.params = (seed, offdiag, d, beta, precision)
+        out = C.c_void_p()
+        _chk(lib.ciref_synthetic_problem(C.c_int(Z), C.c_int(N), C.c_int(M2), C.c_int(parity), C.c_int(Nmax),
+                                         C.c_double(hw), C.c_uint64(seed), C.c_double(offdiag), C.c_int(d),
+                                         C.c_uint32(beta), C.c_int(precision), C.byref(out)))
+        self.handle = out
+        self._fin = weakref.finalize(self, lib.ciref_problem_destroy, out)
+        lib.ciref_problem_matrix.restype = C.c_void_p
+        lib.ciref_problem_groups.restype = C.c_uint32
+        lib.ciref_problem_strata.restype = C.c_uint32
+        self.matrix_handle = C.c_void_p(lib.ciref_problem_matrix(out))
+        ng = lib.ciref_problem_groups(out, None)
+        self.groups = np.zeros(ng, np.uint32)
+        lib.ciref_problem_groups(out, _p(self.groups, C.c_uint32))
+        ns = lib.ciref_problem_strata(out, None)
+        self.strata = np.zeros(ns, np.uint32)
+        lib.ciref_problem_strata(out, _p(self.strata, C.c_uint32))
+
+    def csb(self, path):
+        """The assembled matrix as a ci.CsbMatrix (through a CSB1 file), with
+        the problem's group partition attached."""
+        from paper_1609_01689_b200 import ci
+
+        _chk(load().ciref_matrix_save(self.matrix_handle, str(path).encode()))
+        h = ci.load_csb(str(path))
+        h.groups = self.groups.copy()
+        return h
+
+
+def multilevel_guess(spec, params, levels, k_want, k_trial, tol, max_iter=500, mseed=1):
+    """ci::multilevel_guess (guess.cpp:66-117) with build_synthetic_problem as
+    the factory. Returns (guess n x k, [(nmax, dim, iterations, converged)])."""
+    lib = load()
+    Z, N, M2, parity, Nmax, hw = spec
+    seed, offdiag, d, beta, precision = params
+    full = SyntheticProblem(*spec, seed=seed, offdiag=offdiag, d=d, beta=beta, precision=precision)
+    dim = int(full.strata[-1])
+    guess = np.zeros((dim, k_trial))
+    kout, dout, nlv = C.c_uint32(), C.c_uint32(), C.c_int()
+    lv = [np.zeros(levels, np.int32), np.zeros(levels, np.uint32), np.zeros(levels, np.int32), np.zeros(levels, np.int32)]
+    _chk(lib.ciref_multilevel_guess(C.c_int(Z), C.c_int(N), C.c_int(M2), C.c_int(parity), C.c_int(Nmax),
+                                    C.c_double(hw), C.c_uint64(seed), C.c_double(offdiag), C.c_int(d),
+                                    C.c_uint32(beta), C.c_int(precision), C.c_int(levels), C.c_int(k_want),
+                                    C.c_int(k_trial), C.c_double(tol), C.c_int(max_iter), C.c_uint64(mseed),
+                                    _p(guess), C.byref(kout), C.byref(dout), C.byref(nlv),
+                                    _p(lv[0], C.c_int), _p(lv[1], C.c_uint32), _p(lv[2], C.c_int), _p(lv[3], C.c_int)))
+    g = guess.reshape(-1)[: dout.value * kout.value].reshape(dout.value, kout.value)
+    rows = [(int(lv[0][i]), int(lv[1][i]), int(lv[2][i]), bool(lv[3][i])) for i in range(nlv.value)]
+    return g, rows
+
+
+def rayleigh_ritz(y, hy, k_trial):
+    """ci::rayleigh_ritz (lobpcg.cpp:121-145) -> (theta, g m x k_trial)."""
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    hy = np.ascontiguousarray(hy, dtype=np.float64)
+    n, m = y.shape
+    theta = np.zeros(k_trial)
+    g = np.zeros(m * k_trial)
+    _chk(load().ciref_rayleigh_ritz(C.c_uint32(n), _p(y), _p(hy), C.c_uint32(m), C.c_int(k_trial), _p(theta), _p(g)))
+    return theta, g.reshape(k_trial, m).T.copy()
+
+
+def residual_norms(refmat, x, theta, norm_est=None):
+    """ci::residual_norms (lobpcg.cpp:147-169)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    out = np.zeros(x.shape[1])
+    _chk(load().ciref_residual_norms(refmat.handle, _p(x), C.c_uint32(x.shape[1]), _p(th),
+                                     C.c_double(norm_est if norm_est is not None else 0.0), _p(out)))
+    return out

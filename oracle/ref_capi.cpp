@@ -12,11 +12,13 @@
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <optional>
 #include <string>
 
 #include "ci/block_vectors.hpp"
 #include "ci/csb.hpp"
 #include "ci/errors.hpp"
+#include "ci/guess.hpp"
 #include "ci/hamiltonian.hpp"
 #include "ci/lanczos.hpp"
 #include "ci/lobpcg.hpp"
@@ -327,6 +329,108 @@ int ciref_lanczos_solve(void* h, const double* v0, int k_want, double tol, int m
     auto r = std::make_unique<Report>();
     r->rep = ci::lanczos_solve(H, v, opt);
     *out = r.release();
+  });
+}
+
+// ---- synthetic physics problems + the reference's own multilevel_guess ----
+struct ProblemHolder {
+  ci::Problem p;
+};
+
+static ci::BasisSpec make_spec(int Z, int N, int M2, int parity, int Nmax, double hw) {
+  ci::BasisSpec s;
+  s.Z = Z;
+  s.N = N;
+  s.M2 = M2;
+  s.parity = parity;
+  s.Nmax = Nmax;
+  s.hbar_omega = hw;
+  return s;
+}
+
+// build_synthetic_problem (hamiltonian.cpp:205-224).
+int ciref_synthetic_problem(int Z, int N, int M2, int parity, int Nmax, double hw, std::uint64_t seed,
+                            double offdiag, int d, std::uint32_t beta, int precision, void** out) {
+  return guard([&] {
+    auto h = std::make_unique<ProblemHolder>();
+    h->p = ci::build_synthetic_problem(make_spec(Z, N, M2, parity, Nmax, hw), seed, offdiag, d, beta,
+                                       precision == 0 ? ci::Precision::Single : ci::Precision::Double);
+    *out = h.release();
+  });
+}
+void ciref_problem_destroy(void* h) { delete static_cast<ProblemHolder*>(h); }
+void* ciref_problem_matrix(void* h) { return &static_cast<ProblemHolder*>(h)->p.matrix; }
+// group starts + dim (n = count + 1 written when out != null); returns the count + 1
+std::uint32_t ciref_problem_groups(void* h, std::uint32_t* out) {
+  const auto& g = static_cast<ProblemHolder*>(h)->p.partition.group_ranges;
+  if (out) {
+    for (std::size_t i = 0; i < g.size(); ++i) out[i] = g[i].first;
+    out[g.size()] = g.empty() ? 0 : g.back().second;
+  }
+  return static_cast<std::uint32_t>(g.size() + 1);
+}
+// quanta stratum boundaries (basis.hpp:68) + dim
+std::uint32_t ciref_problem_strata(void* h, std::uint32_t* out) {
+  const auto& b = *static_cast<ProblemHolder*>(h)->p.basis;
+  const auto& q = b.quanta_boundaries;
+  if (out) {
+    for (std::size_t i = 0; i < q.size(); ++i) out[i] = q[i];
+    out[q.size()] = b.dimension();
+  }
+  return static_cast<std::uint32_t>(q.size() + 1);
+}
+
+// multilevel_guess (guess.cpp:66-117) with build_synthetic_problem as the
+// ProblemFactory. lv_* arrays hold up to `levels` entries; *nlv = written.
+int ciref_multilevel_guess(int Z, int N, int M2, int parity, int Nmax, double hw, std::uint64_t seed,
+                           double offdiag, int d, std::uint32_t beta, int precision, int levels, int k_want,
+                           int k_trial, double tol, int max_iter, std::uint64_t mseed, double* guess_out,
+                           std::uint32_t* kout, std::uint32_t* dim_out, int* nlv, int* lv_nmax, std::uint32_t* lv_dim,
+                           int* lv_iters, int* lv_conv) {
+  return guard([&] {
+    ci::MultilevelOptions o;
+    o.levels = levels;
+    o.k_want = k_want;
+    o.k_trial = k_trial;
+    o.tol = tol;
+    o.max_iter = max_iter;
+    o.seed = mseed;
+    const ci::Precision pr = precision == 0 ? ci::Precision::Single : ci::Precision::Double;
+    ci::MultilevelResult r = ci::multilevel_guess(
+        make_spec(Z, N, M2, parity, Nmax, hw), o,
+        [&](const ci::BasisSpec& s) { return ci::build_synthetic_problem(s, seed, offdiag, d, beta, pr); });
+    *kout = r.guess.width();
+    *dim_out = r.guess.dim();
+    from_bv(r.guess, guess_out);
+    *nlv = static_cast<int>(r.levels.size());
+    for (std::size_t i = 0; i < r.levels.size(); ++i) {
+      lv_nmax[i] = r.levels[i].nmax;
+      lv_dim[i] = r.levels[i].dim;
+      lv_iters[i] = r.levels[i].iterations;
+      lv_conv[i] = r.levels[i].converged ? 1 : 0;
+    }
+  });
+}
+
+// rayleigh_ritz (lobpcg.cpp:121-145); g_out m x k_trial column-major.
+int ciref_rayleigh_ritz(std::uint32_t n, const double* y, const double* hy, std::uint32_t m, int k_trial,
+                        double* theta_out, double* g_out) {
+  return guard([&] {
+    auto [theta, coeff] = ci::rayleigh_ritz(to_bv(y, n, m), to_bv(hy, n, m), k_trial, -1, 0, 0);
+    for (int j = 0; j < k_trial; ++j) theta_out[j] = theta[j];
+    std::memcpy(g_out, coeff.g.data(), sizeof(double) * coeff.g.size());
+  });
+}
+
+// residual_norms (lobpcg.cpp:147-169); norm_est <= 0 -> nullopt.
+int ciref_residual_norms(void* h, const double* x, std::uint32_t k, const double* theta, double norm_est,
+                         double* out) {
+  return guard([&] {
+    const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);
+    std::optional<double> est;
+    if (norm_est > 0) est = norm_est;
+    std::vector<double> r = ci::residual_norms(H, to_bv(x, H.dim, k), std::vector<double>(theta, theta + k), est);
+    for (std::uint32_t j = 0; j < k; ++j) out[j] = r[j];
   });
 }
 

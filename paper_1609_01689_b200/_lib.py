@@ -83,6 +83,25 @@ class DistHooks(C.Structure):
 OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_uint32,
                        C.c_uint32, C.POINTER(C.c_double), C.POINTER(C.c_double))
 
+class MultilevelOptionsC(C.Structure):
+    _fields_ = [
+        ("k_want", C.c_int),
+        ("k_trial", C.c_int),
+        ("tol", C.c_double),
+        ("max_iter", C.c_int),
+        ("seed", C.c_uint64),
+    ]
+
+
+class LevelReportC(C.Structure):
+    _fields_ = [
+        ("dim", C.c_uint32),
+        ("iterations", C.c_int),
+        ("converged", C.c_int),
+        ("seconds", C.c_double),
+    ]
+
+
 # cieg_lanczos_observer_fn(user, m, alpha, beta, basis_host (n x m col-major), n)
 LANCZOS_OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                C.POINTER(C.c_double), C.c_uint32)
@@ -136,6 +155,15 @@ SIGNATURES = {
                                C.POINTER(_vp)]),
     "cieg_report_destroy": (_i, [_vp]),
     "cieg_lanczos_options_default": (None, [C.POINTER(LanczosOptionsC)]),
+    "cieg_orthonormalize": (_i, [_vp, _vp, _u32, _u32, C.c_double, _vp, _u32, _pu32]),
+    "cieg_rayleigh_ritz": (_i, [_vp, _vp, _vp, _u32, _u32, _u32, _pd, _pd]),
+    "cieg_residual_norms": (_i, [_vp, _vp, _vp, _u32, _pd, C.c_double, _pd]),
+    "cieg_matrix_leading_view": (_i, [_vp, _vp, _u32, C.POINTER(_vp)]),
+    "cieg_matrix_upload_cuts": (_i, [_vp, C.POINTER(CsbView), _pu32, _u32, _u32, _pu32, _u32, C.POINTER(_vp)]),
+    "cieg_pad_from_subspace": (_i, [_pd, _u32, _u32, _u32, _pd]),
+    "cieg_multilevel_options_default": (None, [C.POINTER(MultilevelOptionsC)]),
+    "cieg_multilevel_guess": (_i, [_vp, _vp, _pu32, _u32, C.POINTER(MultilevelOptionsC), _pd, _pu32,
+                                   C.POINTER(LevelReportC)]),
     "cieg_lanczos_checkpoint": (_i, [C.c_int]),
     "cieg_lanczos_default_start": (_i, [_u32, _u32, _pd]),
     "cieg_lanczos_solve": (_i, [_vp, _vp, _pd, C.POINTER(LanczosOptionsC), C.POINTER(_vp)]),

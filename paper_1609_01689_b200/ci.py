@@ -327,8 +327,10 @@ class DeviceMatrix:
     """H re-tiled and resident in HBM (cieg_mat)."""
 
     def __init__(self, h: Optional[CsbMatrix], device: Optional[Device] = None, tile_edge: int = 0,
-                 _handle: Optional[C.c_void_p] = None):
+                 _handle: Optional[C.c_void_p] = None, cuts: Optional[Sequence[int]] = None,
+                 _parent: Optional["DeviceMatrix"] = None):
         self.device = device or Device.default()
+        self._parent = _parent  # a leading view borrows its parent's tile stream
         lib = _lib.load()
         if _handle is None:
             v = h.view()
@@ -337,7 +339,9 @@ class DeviceMatrix:
             if h.groups is not None:
                 g = np.ascontiguousarray(h.groups, dtype=np.uint32)
                 gptr, ng = _ptr(g, C.c_uint32), len(g) - 1
-            _check(lib.cieg_matrix_upload(self.device.handle, C.byref(v), gptr, ng, tile_edge, C.byref(handle)))
+            cu = np.ascontiguousarray(cuts if cuts is not None else [], dtype=np.uint32)
+            _check(lib.cieg_matrix_upload_cuts(self.device.handle, C.byref(v), gptr, ng, tile_edge,
+                                               _ptr(cu, C.c_uint32), len(cu), C.byref(handle)))
         else:
             handle = _handle
         self.handle = handle
@@ -362,6 +366,14 @@ class DeviceMatrix:
         handle = C.c_void_p()
         _check(_lib.load().cieg_generate_device(dev.handle, C.byref(prm), tile_edge, lo, hi, C.byref(handle)))
         return cls(None, dev, _handle=handle)
+
+    def leading(self, dim: int) -> "DeviceMatrix":
+        """H[0:dim, 0:dim] as a matrix of its own sharing this matrix's tile
+        stream (cieg_matrix_leading_view); dim must be a device panel
+        boundary (upload with cuts=[dim, ...] to make it one)."""
+        handle = C.c_void_p()
+        _check(_lib.load().cieg_matrix_leading_view(self.device.handle, self.handle, int(dim), C.byref(handle)))
+        return DeviceMatrix(None, self.device, _handle=handle, _parent=self)
 
     def groups(self) -> np.ndarray:
         b = C.POINTER(C.c_uint32)()
@@ -776,6 +788,172 @@ def lanczos_solve(h, v0: np.ndarray, options: LanczosOptions = LanczosOptions(),
     rep = C.c_void_p()
     _check(lib.cieg_lanczos_solve(dm.device.handle, dm.handle, _ptr(v0), C.byref(opt), C.byref(rep)))
     return _read_report(lib, rep, h.dim)
+
+
+# ------------------------------------------- lobpcg.hpp public helpers
+
+@dataclasses.dataclass
+class SubspaceCoefficients:
+    """ci::SubspaceCoefficients (lobpcg.hpp:73-80): Ritz coefficients g over
+    the [X W P] basis and the segment widths."""
+    g: np.ndarray
+    x_width: int
+    w_width: int
+    p_width: int
+
+
+def orthonormalize(y: np.ndarray, drop_tol: float = 1e-8, against: Optional[np.ndarray] = None,
+                   device: Optional[Device] = None) -> np.ndarray:
+    """ci::orthonormalize (lobpcg.cpp:89-119) on the GPU: projection against
+    `against` (twice), rank-revealing column selection, CholQR twice. The
+    result may be narrower than y."""
+    y = _f64(y)
+    if against is not None:
+        against = _f64(against)
+        if against.shape[0] != y.shape[0]:
+            raise DimensionMismatch("orthonormalize: row counts differ")
+    dev = _dev(device)
+    dy = _DevArray(y)
+    da = _DevArray(against) if against is not None and against.shape[1] else None
+    kout = C.c_uint32()
+    dev.synchronize()
+    _check(_lib.load().cieg_orthonormalize(dev.handle, dy.ptr, y.shape[0], y.shape[1], float(drop_tol),
+                                           da.ptr if da else None, da.t.shape[1] if da else 0, C.byref(kout)))
+    k = kout.value
+    return dy.host().reshape(-1)[: y.shape[0] * k].reshape(y.shape[0], k).copy()
+
+
+def rayleigh_ritz(y_basis: np.ndarray, hy: np.ndarray, k_trial: int, x_width: int = -1, w_width: int = 0,
+                  p_width: int = 0, device: Optional[Device] = None):
+    """ci::rayleigh_ritz (lobpcg.cpp:121-145): (theta[k_trial], SubspaceCoefficients)."""
+    y, hyy = _f64(y_basis), _f64(hy)
+    if hyy.shape != y.shape:
+        raise DimensionMismatch("rayleigh_ritz: HY shape mismatch")
+    m = y.shape[1]
+    if k_trial > m:
+        raise DimensionMismatch("rayleigh_ritz: k_trial exceeds basis width")
+    dev = _dev(device)
+    dy, dh = _DevArray(y), _DevArray(hyy)
+    theta = np.zeros(k_trial)
+    g = np.zeros(m * k_trial)
+    dev.synchronize()
+    _check(_lib.load().cieg_rayleigh_ritz(dev.handle, dy.ptr, dh.ptr, y.shape[0], m, k_trial, _ptr(theta), _ptr(g)))
+    return theta.tolist(), SubspaceCoefficients(g.reshape(k_trial, m).T.copy(), m if x_width < 0 else x_width,
+                                                w_width, p_width)
+
+
+def residual_norms(h, x: np.ndarray, theta, norm_est: Optional[float] = None,
+                   device: Optional[Device] = None) -> list:
+    """ci::residual_norms (lobpcg.cpp:147-169) on the GPU."""
+    x = _f64(x)
+    th = np.ascontiguousarray(theta, dtype=np.float64)
+    if x.shape[1] != th.shape[0]:
+        raise DimensionMismatch("residual_norms: theta width mismatch")
+    dm = h if isinstance(h, DeviceMatrix) else device_matrix(h, device)
+    dx = _DevArray(x)
+    out = np.zeros(x.shape[1])
+    dm.device.synchronize()
+    _check(_lib.load().cieg_residual_norms(dm.device.handle, dm.handle, dx.ptr, x.shape[1], _ptr(th),
+                                           float(norm_est) if norm_est is not None else 0.0, _ptr(out)))
+    return out.tolist()
+
+
+# ---------------------------------------------------- guess.hpp (starting blocks)
+
+def pad_from_subspace(x1: np.ndarray, dim: int) -> np.ndarray:
+    """ci::pad_from_subspace (guess.cpp:14-23)."""
+    x1 = _f64(x1)
+    out = np.zeros((dim, x1.shape[1]))
+    _check(_lib.load().cieg_pad_from_subspace(_ptr(x1), x1.shape[0], x1.shape[1], int(dim), _ptr(out)))
+    return out
+
+
+@dataclasses.dataclass
+class MultilevelOptions:
+    """ci::MultilevelOptions (guess.hpp:47-54); the levels are given as the
+    list of truncated dimensions (leading blocks of H)."""
+    k_want: int = 8
+    k_trial: int = 12
+    tol: float = 1e-6
+    max_iter: int = 500
+    seed: int = 1
+
+
+@dataclasses.dataclass
+class LevelReport:
+    """ci::LevelReport (guess.hpp:31-37); `dim` identifies the level."""
+    dim: int
+    iterations: int
+    converged: bool
+    seconds: float
+
+
+@dataclasses.dataclass
+class MultilevelResult:
+    guess: np.ndarray
+    levels: list
+
+
+def multilevel_guess(h, level_dims: Sequence[int], options: MultilevelOptions = MultilevelOptions(),
+                     device: Optional[Device] = None) -> MultilevelResult:
+    """ci::multilevel_guess (guess.cpp:66-117) on the GPU. The truncated
+    problems are the leading blocks H[0:d, 0:d] for d in level_dims
+    (ascending, below dim) -- for a basis ordered by quanta stratum these are
+    exactly the reference's lower-Nmax Hamiltonians. A CsbMatrix is uploaded
+    with the level dimensions as mandatory panel cuts."""
+    dims = np.ascontiguousarray(list(level_dims), dtype=np.uint32)
+    dm = h if isinstance(h, DeviceMatrix) else DeviceMatrix(h, device, cuts=dims)
+    o = _lib.MultilevelOptionsC()
+    _lib.load().cieg_multilevel_options_default(C.byref(o))
+    o.k_want, o.k_trial, o.tol, o.max_iter, o.seed = (options.k_want, options.k_trial, options.tol,
+                                                      options.max_iter, options.seed)
+    guess = np.zeros((dm.dim, options.k_trial))
+    kout = C.c_uint32()
+    lv = (_lib.LevelReportC * max(1, len(dims)))()
+    _check(_lib.load().cieg_multilevel_guess(dm.device.handle, dm.handle, _ptr(dims, C.c_uint32), len(dims),
+                                             C.byref(o), _ptr(guess), C.byref(kout), lv))
+    k = kout.value
+    g = guess.reshape(-1)[: dm.dim * k].reshape(dm.dim, k).copy()
+    return MultilevelResult(g, [LevelReport(int(r.dim), int(r.iterations), bool(r.converged), float(r.seconds))
+                                for r in list(lv)[: len(dims)]])
+
+
+_BVEC = b"BVEC"
+
+
+def save_vectors(x: np.ndarray, path: str) -> None:
+    """ci::save_vectors (guess.cpp:119-133): "BVEC", u64 dim, u32 width,
+    column-major little-endian doubles."""
+    x = _f64(x)
+    with open(path, "wb") as f:
+        f.write(_BVEC)
+        f.write(struct.pack("<QI", x.shape[0], x.shape[1]))
+        f.write(np.asfortranarray(x).astype("<f8").tobytes(order="F"))
+
+
+def load_guess_file(path: str, dim: int, k: int, device: Optional[Device] = None) -> np.ndarray:
+    """ci::load_guess_file (guess.cpp:135-163): first k columns, orthonormalized."""
+    try:
+        f = open(path, "rb")
+    except OSError:
+        raise FormatError("cannot open: " + path)
+    with f:
+        magic = f.read(4)
+        if magic != _BVEC:
+            raise FormatError("bad magic; not a BVEC file: " + path)
+        hdr = f.read(12)
+        if len(hdr) < 12:
+            raise FormatError("truncated BVEC header: " + path)
+        fdim, width = struct.unpack("<QI", hdr)
+        if fdim != dim:
+            raise DimensionMismatch(f"vector file dimension {fdim} != basis dimension {dim}")
+        if width < k:
+            raise DimensionMismatch(f"vector file holds {width} columns, need {k}")
+        raw = f.read(8 * dim * k)
+        if len(raw) < 8 * dim * k:
+            raise FormatError("truncated BVEC payload: " + path)
+    x = np.frombuffer(raw, dtype="<f8").reshape(k, dim).T.astype(np.float64)
+    return orthonormalize(x, device=device)
 
 
 def write_history_csv(report: SolveReport, os: io.TextIOBase) -> None:

@@ -2,7 +2,9 @@
 // points (include/cieg.h).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
+#include <memory>
 #include <string>
 
 #include "context.hpp"
@@ -28,10 +30,12 @@ T* upload_vec(const std::vector<T>& v) {
 }  // namespace cieg
 
 cieg_mat::~cieg_mat() {
-  cudaFree(panel_start);
-  cudaFree(tile_off);
-  cudaFree(idx);
-  cudaFree(val);
+  if (!borrowed_stream) {
+    cudaFree(panel_start);
+    cudaFree(tile_off);
+    cudaFree(idx);
+    cudaFree(val);
+  }
   cudaFree(work_off);
   cudaFree(work_tile);
   cudaFree(work_other);
@@ -39,6 +43,35 @@ cieg_mat::~cieg_mat() {
   cudaFree(sched_off);
   cudaFree(sched);
 }
+
+namespace {
+
+__global__ void count_real_kernel(const std::uint32_t* idx, std::uint64_t n, std::uint32_t sentinel,
+                                  unsigned long long* count) {
+  unsigned long long c = 0;
+  for (std::uint64_t i = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; i < n;
+       i += std::uint64_t(gridDim.x) * blockDim.x)
+    c += idx[i] != sentinel;
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(count, c);
+}
+
+// Real (non-padding) entries among the first n slots of a tile stream.
+std::uint64_t count_real_entries(cieg_ctx* ctx, const std::uint32_t* idx, std::uint64_t n, std::uint32_t sentinel) {
+  if (n == 0) return 0;
+  unsigned long long* d = nullptr;
+  CIEG_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+  unsigned long long h = 0;
+  CIEG_CUDA(cudaMemsetAsync(d, 0, sizeof h, ctx->stream));
+  count_real_kernel<<<4 * ctx->sm_count, 256, 0, ctx->stream>>>(idx, n, sentinel, d);
+  ++ctx->launches;
+  CIEG_CUDA(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, ctx->stream));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  cudaFree(d);
+  return h;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -159,16 +192,82 @@ extern "C" {
 
 int cieg_matrix_upload(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
                        uint32_t ngroups, uint32_t tile_edge, cieg_mat** out) {
+  return cieg_matrix_upload_cuts(ctx, csb, group_bounds, ngroups, tile_edge, nullptr, 0, out);
+}
+
+int cieg_matrix_upload_cuts(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
+                            uint32_t ngroups, uint32_t tile_edge, const uint32_t* cuts, uint32_t ncuts,
+                            cieg_mat** out) {
   return cieg::guarded([&] {
-    if (!ctx || !csb || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_upload: null argument");
+    if (!ctx || !csb || !out || (ncuts && !cuts)) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_upload: null argument");
     if (csb->precision != 0 && csb->precision != 1) cieg::fail(CIEG_ERR_FORMAT, "bad precision tag");
     CIEG_CUDA(cudaSetDevice(ctx->device));
     const std::uint32_t te = choose_tile_edge(csb, group_bounds, ngroups, tile_edge);
-    std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te);
+    std::vector<std::uint32_t> panels = cieg::plan_panels(csb->dim, group_bounds, ngroups, te, cuts, ncuts);
     cieg::HostTiles ht;
     cieg::build_tiles(*csb, panels, te, ht);
     *out = upload_tiles(ctx, ht);
     if (group_bounds && ngroups) (*out)->group_bounds_host.assign(group_bounds, group_bounds + ngroups + 1);
+  });
+}
+
+int cieg_matrix_leading_view(cieg_ctx* ctx, const cieg_mat* m, uint32_t dim, cieg_mat** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !m || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_matrix_leading_view: null argument");
+    if (m->row_lo != 0 || m->row_hi != m->dim) cieg::fail(CIEG_ERR_CONFIG, "leading view of a shard");
+    if (m->tile_pi_host.empty() && m->ntiles) cieg::fail(CIEG_ERR_CONFIG, "matrix keeps no host tile map");
+    const std::vector<std::uint32_t>& ps = m->panel_start_host;
+    const auto pit = std::lower_bound(ps.begin(), ps.end(), dim);
+    if (dim == 0 || dim > m->dim || pit == ps.end() || *pit != dim)
+      cieg::fail(CIEG_ERR_DIMENSION, "leading block must end on a panel boundary inside the matrix");
+    const std::uint32_t pd = static_cast<std::uint32_t>(pit - ps.begin());
+    // tiles are sorted by (pi, pj): those inside [0, dim)^2 are a prefix
+    const std::uint64_t td = static_cast<std::uint64_t>(
+        std::lower_bound(m->tile_pi_host.begin(), m->tile_pi_host.end(), pd) - m->tile_pi_host.begin());
+    cieg::HostTiles ht;
+    ht.dim = dim;
+    ht.tile_edge = m->tile_edge;
+    ht.precision = m->precision;
+    ht.panel_start.assign(ps.begin(), ps.begin() + pd + 1);
+    ht.tile_pi.assign(m->tile_pi_host.begin(), m->tile_pi_host.begin() + td);
+    ht.tile_pj.assign(m->tile_pj_host.begin(), m->tile_pj_host.begin() + td);
+    ht.tile_off.assign(m->tile_off_host.begin(), m->tile_off_host.begin() + td + 1);
+    ht.row_lo = ht.halo_lo = 0;
+    ht.row_hi = ht.halo_hi = dim;
+    cieg::build_work_lists(ht, 0, pd);
+    cieg::build_schedule(ht, static_cast<std::uint32_t>(ctx->sm_count));
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    auto v = std::make_unique<cieg_mat>();
+    v->borrowed_stream = true;
+    v->ctx = ctx;
+    v->dim = dim;
+    v->tile_edge = m->tile_edge;
+    v->precision = m->precision;
+    v->npanels = pd;
+    v->ntiles = td;
+    v->row_lo = v->halo_lo = 0;
+    v->row_hi = v->halo_hi = dim;
+    v->panel_start_host = ht.panel_start;
+    v->tile_pi_host = ht.tile_pi;
+    v->tile_pj_host = ht.tile_pj;
+    v->tile_off_host = ht.tile_off;
+    for (std::uint32_t b : m->group_bounds_host)
+      if (b <= dim) v->group_bounds_host.push_back(b);
+    v->panel_start = m->panel_start;
+    v->tile_off = m->tile_off;
+    v->idx = m->idx;
+    v->val = m->val;
+    v->work_off = cieg::upload_vec(ht.work_off);
+    v->work_tile = cieg::upload_vec(ht.work_tile);
+    v->work_other = cieg::upload_vec(ht.work_other);
+    v->work_kind = cieg::upload_vec(ht.work_kind);
+    v->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
+    v->sched_off = cieg::upload_vec(ht.sched_off);
+    v->sched = cieg::upload_vec(ht.sched);
+    // stored entries of the block (padding sentinels excluded), for info()
+    v->nnz = count_real_entries(ctx, m->idx, ht.tile_off.back(), m->tile_edge | (m->tile_edge << 16));
+    v->tile_bytes = ht.tile_off.back() * (4 + (m->precision == 0 ? 4 : 8));
+    *out = v.release();
   });
 }
 

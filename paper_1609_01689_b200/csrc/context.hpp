@@ -96,6 +96,9 @@ struct cieg_mat {
   std::uint32_t sched_ctas = 0;
   std::uint32_t* sched_off = nullptr;
   std::uint32_t* sched = nullptr;
+  // a leading-block view (cieg_matrix_leading_view) borrows panel_start,
+  // tile_off, idx and val from its parent and owns only its work lists
+  bool borrowed_stream = false;
   ~cieg_mat();
 };
 

@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <string>
 
 #include "blockvec.hpp"
 #include "dense_small.hpp"
@@ -116,6 +117,54 @@ double dev_from_identity(const Mat& g, int m) {
 }
 
 
+// orthonormalize (lobpcg.cpp:89-119) over device blocks. `gram` is the Gram
+// product (all-reduced across ranks inside a sharded solve). `v` holds the
+// input (width v.w) and is overwritten; `tmp` is scratch of the same
+// capacity; the result (possibly width 0) is left in `v` (the two may swap).
+template <typename GramFn>
+void orthonormalize_dev(cieg_ctx* ctx, std::uint32_t n, GramFn&& gram, Block& v, Block& tmp, double drop_tol,
+                        const View3* against) {
+  if (v.w == 0) return;
+  const int k = static_cast<int>(v.w);
+  Mat g0 = gram(view({sg(v)}), view({sg(v)}));
+  std::vector<double> orig_sq(k);
+  for (int j = 0; j < k; ++j) orig_sq[j] = g0[j + static_cast<std::size_t>(j) * k];
+  if (against && against->width > 0) {
+    for (int pass = 0; pass < 2; ++pass) {
+      Mat c = gram(*against, view({sg(v)}));
+      for (double& e : c) e = -e;
+      combine(ctx, n, *against, c.data(), v.w, out1(v.p, v.w), true);
+    }
+  }
+  // Without a projection the Gram is unchanged (the reference recomputes it;
+  // the deterministic kernel would return the identical matrix).
+  Mat gram_v = (against && against->width > 0) ? gram(view({sg(v)}), view({sg(v)})) : g0;
+  std::vector<std::uint32_t> kept = rank_revealing_select(gram_v, k, orig_sq, drop_tol);
+  while (!kept.empty()) {
+    const int kk = static_cast<int>(kept.size());
+    Mat sub(static_cast<std::size_t>(kk) * kk);
+    for (int a = 0; a < kk; ++a)
+      for (int b = 0; b < kk; ++b) sub[a + b * kk] = gram_v[kept[a] + static_cast<std::size_t>(kept[b]) * k];
+    Mat rinv;
+    if (llt_rinv(sub, kk, rinv)) {
+      // q = V[:, kept] R^{-1}: one combine with the selection folded in.
+      Mat sel(static_cast<std::size_t>(k) * kk, 0.0);
+      for (int a = 0; a < kk; ++a)
+        for (int c = 0; c < kk; ++c) sel[kept[a] + static_cast<std::size_t>(c) * k] = rinv[a + c * kk];
+      combine(ctx, n, view({sg(v)}), sel.data(), kk, out1(tmp.p, kk), false);
+      tmp.w = kk;
+      std::swap(v, tmp);
+      // cholqr_pass (lobpcg.cpp:61-69): second pass, result ignored on failure.
+      Mat gq = gram(view({sg(v)}), view({sg(v)}));
+      Mat rinv2;
+      if (llt_rinv(gq, kk, rinv2)) combine(ctx, n, view({sg(v)}), rinv2.data(), kk, out1(v.p, kk), false);
+      return;
+    }
+    kept.pop_back();
+  }
+  v.w = 0;
+}
+
 class Solver {
  public:
   Solver(cieg_ctx* ctx, const cieg_mat* mat, const cieg_prec* prec, const cieg_lobpcg_options& opt,
@@ -168,45 +217,8 @@ class Solver {
 };
 
 void Solver::orthonormalize(Block& v, Block& tmp, double drop_tol, const View3* against) {
-  if (v.w == 0) return;
-  const int k = static_cast<int>(v.w);
-  Mat g0 = gram(view({sg(v)}), view({sg(v)}));
-  std::vector<double> orig_sq(k);
-  for (int j = 0; j < k; ++j) orig_sq[j] = g0[j + static_cast<std::size_t>(j) * k];
-  if (against && against->width > 0) {
-    for (int pass = 0; pass < 2; ++pass) {
-      Mat c = gram(*against, view({sg(v)}));
-      for (double& e : c) e = -e;
-      combine(ctx_, n_, *against, c.data(), v.w, out1(v.p, v.w), true);
-    }
-  }
-  // Without a projection the Gram is unchanged (the reference recomputes it;
-  // the deterministic kernel would return the identical matrix).
-  Mat gram_v = (against && against->width > 0) ? gram(view({sg(v)}), view({sg(v)})) : g0;
-  std::vector<std::uint32_t> kept = rank_revealing_select(gram_v, k, orig_sq, drop_tol);
-  while (!kept.empty()) {
-    const int kk = static_cast<int>(kept.size());
-    Mat sub(static_cast<std::size_t>(kk) * kk);
-    for (int a = 0; a < kk; ++a)
-      for (int b = 0; b < kk; ++b) sub[a + b * kk] = gram_v[kept[a] + static_cast<std::size_t>(kept[b]) * k];
-    Mat rinv;
-    if (llt_rinv(sub, kk, rinv)) {
-      // q = V[:, kept] R^{-1}: one combine with the selection folded in.
-      Mat sel(static_cast<std::size_t>(k) * kk, 0.0);
-      for (int a = 0; a < kk; ++a)
-        for (int c = 0; c < kk; ++c) sel[kept[a] + static_cast<std::size_t>(c) * k] = rinv[a + c * kk];
-      combine(ctx_, n_, view({sg(v)}), sel.data(), kk, out1(tmp.p, kk), false);
-      tmp.w = kk;
-      std::swap(v, tmp);
-      // cholqr_pass (lobpcg.cpp:61-69): second pass, result ignored on failure.
-      Mat gq = gram(view({sg(v)}), view({sg(v)}));
-      Mat rinv2;
-      if (llt_rinv(gq, kk, rinv2)) combine(ctx_, n_, view({sg(v)}), rinv2.data(), kk, out1(v.p, kk), false);
-      return;
-    }
-    kept.pop_back();
-  }
-  v.w = 0;
+  orthonormalize_dev(ctx_, n_, [this](const View3& l, const View3& r) { return gram(l, r); }, v, tmp, drop_tol,
+                     against);
 }
 
 void Solver::clean_p_block(double drop_tol) {
@@ -531,6 +543,78 @@ int cieg_report_timing(const cieg_report* r, double* ms7) {
   return cieg::guarded([&] {
     if (!r || !ms7) cieg::fail(CIEG_ERR_ARGUMENT, "null argument");
     for (int i = 0; i < 7; ++i) ms7[i] = r->timing_ms[i];
+  });
+}
+
+/* ---- lobpcg.hpp public helpers ---------------------------------------- */
+
+int cieg_orthonormalize(cieg_ctx* ctx, double* y_dev, uint32_t n, uint32_t k, double drop_tol,
+                        const double* against_dev, uint32_t ka, uint32_t* k_out) {
+  return cieg::guarded([&] {
+    if (!ctx || !y_dev || !k_out || (ka && !against_dev))
+      cieg::fail(CIEG_ERR_ARGUMENT, "cieg_orthonormalize: null argument");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    cieg::DevBuf scratch;
+    cieg::Block v{y_dev, k, k};
+    cieg::Block tmp{static_cast<double*>(scratch.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(n) * k))),
+                    0, k};
+    const cieg::View3 ag = cieg::view({cieg::seg(against_dev, ka)});
+    cieg::orthonormalize_dev(
+        ctx, n, [&](const cieg::View3& l, const cieg::View3& r) { return cieg::gram(ctx, n, l, r); }, v, tmp,
+        drop_tol, ka ? &ag : nullptr);
+    if (v.w && v.p != y_dev)
+      CIEG_CUDA(cudaMemcpyAsync(y_dev, v.p, sizeof(double) * std::size_t(n) * v.w, cudaMemcpyDeviceToDevice,
+                                ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *k_out = v.w;
+  });
+}
+
+int cieg_rayleigh_ritz(cieg_ctx* ctx, const double* y_dev, const double* hy_dev, uint32_t n, uint32_t m,
+                       uint32_t k_trial, double* theta_out, double* g_out) {
+  return cieg::guarded([&] {
+    if (!ctx || !y_dev || !hy_dev || !theta_out || !g_out)
+      cieg::fail(CIEG_ERR_ARGUMENT, "cieg_rayleigh_ritz: null argument");
+    if (k_trial > m) cieg::fail(CIEG_ERR_DIMENSION, "rayleigh_ritz: k_trial exceeds basis width");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    const cieg::View3 y = cieg::view({cieg::seg(y_dev, m)}), hy = cieg::view({cieg::seg(hy_dev, m)});
+    const int mm = static_cast<int>(m);
+    cieg::Mat overlap = cieg::gram(ctx, n, y, y);
+    const double dev = cieg::dev_from_identity(overlap, mm);
+    if (dev > 1e-6)
+      cieg::fail(CIEG_ERR_INDEFINITE, "basis overlap deviates from identity by " + std::to_string(dev));
+    std::vector<double> evals;
+    cieg::Mat evecs;
+    cieg::eig_sym(cieg::gram(ctx, n, y, hy), mm, evals, evecs);
+    for (uint32_t j = 0; j < k_trial; ++j) theta_out[j] = evals[j];
+    std::copy(evecs.begin(), evecs.begin() + static_cast<std::size_t>(m) * k_trial, g_out);
+  });
+}
+
+int cieg_residual_norms(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, uint32_t k, const double* theta,
+                        double norm_est, double* out) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat || !x_dev || !theta || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_residual_norms: null argument");
+    if (mat->row_lo != 0 || mat->row_hi != mat->dim)
+      cieg::fail(CIEG_ERR_CONFIG, "cieg_residual_norms needs the whole matrix (not a shard)");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    const std::uint32_t n = mat->dim;
+    cieg::DevBuf hx, r;
+    auto* hxp = static_cast<double*>(hx.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(n) * k)));
+    auto* rp = static_cast<double*>(r.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(n) * k)));
+    // residual_norms (lobpcg.cpp:147-169): R = H X - X diag(theta), relative to est * |x_j|
+    cieg::launch_spmm(ctx, mat, x_dev, k, hxp, k, k);
+    cieg::residual(ctx, n, k, hxp, x_dev, theta, rp);
+    const cieg::View3 rv = cieg::view({cieg::seg(rp, k)}), xv = cieg::view({cieg::seg(x_dev, k)});
+    const cieg::Mat gr = cieg::gram(ctx, n, rv, rv), gx = cieg::gram(ctx, n, xv, xv);
+    double est = norm_est;
+    if (!(est > 0.0))
+      for (uint32_t j = 0; j < k; ++j) est = std::max(est, std::fabs(theta[j]));
+    for (uint32_t j = 0; j < k; ++j) {
+      const double rn = std::sqrt(gr[j + static_cast<std::size_t>(k) * j]);
+      const double xn = std::sqrt(gx[j + static_cast<std::size_t>(k) * j]);
+      out[j] = rn / std::max(est * xn, cieg::kTinyDiag);
+    }
   });
 }
 

@@ -9,6 +9,19 @@
 namespace cieg {
 
 std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* gb,
+                                       std::uint32_t ng, std::uint32_t te, const std::uint32_t* cuts,
+                                       std::uint32_t ncuts) {
+  std::vector<std::uint32_t> p = plan_panels(dim, gb, ng, te);
+  // mandatory cuts only split panels, so every panel stays <= te
+  for (std::uint32_t i = 0; i < ncuts; ++i) {
+    if (cuts[i] == 0 || cuts[i] >= dim) continue;
+    auto it = std::lower_bound(p.begin(), p.end(), cuts[i]);
+    if (*it != cuts[i]) p.insert(it, cuts[i]);
+  }
+  return p;
+}
+
+std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* gb,
                                        std::uint32_t ng, std::uint32_t te) {
   std::vector<std::uint32_t> p{0};
   if (!gb || ng == 0) {

@@ -60,6 +60,11 @@ struct HostTiles {
 // physics-style groups), otherwise each group is its own panel.
 std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* group_bounds,
                                        std::uint32_t ngroups, std::uint32_t tile_edge);
+// The same plan with extra mandatory panel boundaries (e.g. the truncation
+// levels of a multilevel guess, so their leading blocks are panel-aligned).
+std::vector<std::uint32_t> plan_panels(std::uint32_t dim, const std::uint32_t* group_bounds,
+                                       std::uint32_t ngroups, std::uint32_t tile_edge, const std::uint32_t* cuts,
+                                       std::uint32_t ncuts);
 
 void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& panels,
                  std::uint32_t tile_edge, HostTiles& out);

@@ -55,3 +55,27 @@ def ref_lib():
     if not ref.available():
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
     return ref
+
+
+def multilevel_operator(g):
+    """The operator multilevel_guess sees in tests/golden/multilevel.npz: the
+    Nmax-4 4He Hamiltonian (the leading block of the Nmax-6 one) followed by
+    a diagonal filler up to the Nmax-6 dimension. The level solves read only
+    the leading block and the guess is zero-padded below it, so the filler
+    never enters the result (make_golden.py: make_multilevel)."""
+    from paper_1609_01689_b200 import ci
+
+    full = int(g["full_dim"])
+    bb = g["sub_block_boundaries"].astype(np.uint32)
+    nb = len(bb) - 1
+    eo = g["sub_entry_offsets"].astype(np.uint64)
+    sub = int(bb[-1])
+    fill = full - sub
+    rows = np.concatenate([g["sub_rows"], np.arange(fill, dtype=np.uint16)])
+    cols = np.concatenate([g["sub_cols"], np.arange(fill, dtype=np.uint16)])
+    vals = np.concatenate([g["sub_values"], np.full(fill, 100.0, dtype=g["sub_values"].dtype)])
+    # block row nb: blocks (nb, 0..nb-1) empty, (nb, nb) the filler diagonal
+    eo_new = np.concatenate([eo, np.full(nb, eo[-1], dtype=np.uint64), [eo[-1] + fill]]).astype(np.uint64)
+    groups = np.concatenate([g["sub_groups"].astype(np.uint32), [full]]).astype(np.uint32)
+    return ci.CsbMatrix(dim=full, precision=int(g["sub_precision"]), block_boundaries=np.append(bb, np.uint32(full)),
+                        entry_offsets=eo_new, rows=rows, cols=cols, values=vals, groups=groups)

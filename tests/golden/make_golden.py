@@ -80,6 +80,37 @@ def make_lanczos():
     np.savez_compressed(os.path.join(OUT, "lanczos.npz"), **la)
 
 
+MULTILEVEL_SPEC = (2, 2, 0, 1, 6, 1.0)    # 4He, Nmax 6: strata 0 | 1 | 59 | 952 | 7916
+MULTILEVEL_PARAMS = (1, 0.1, 2, 2000, 0)  # seed, offdiag_scale, d, beta, fp32 H
+
+
+def make_multilevel():
+    """The reference's own multilevel_guess (guess.cpp:66-117, factory =
+    build_synthetic_problem) on 4He Nmax 6, levels 3 (Nmax 2 / 4 / 6). The
+    level solves only see the Nmax-4 space (dim 952) -- the leading block of
+    the Nmax-6 Hamiltonian -- and the guess is zero below row 952, so the
+    fixture stores the Nmax-4 matrix, the guess's leading 952 rows and the
+    level reports."""
+    import tempfile
+
+    Z, N, M2, par, nmax, hw = MULTILEVEL_SPEC
+    seed, off, d, beta, prec = MULTILEVEL_PARAMS
+    full = ref.SyntheticProblem(*MULTILEVEL_SPEC, seed=seed, offdiag=off, d=d, beta=beta, precision=prec)
+    sub = ref.SyntheticProblem(Z, N, M2, par, nmax - 2, hw, seed=seed, offdiag=off, d=d, beta=beta, precision=prec)
+    with tempfile.TemporaryDirectory() as td:
+        h = sub.csb(os.path.join(td, "sub.csb"))
+    g, lv = ref.multilevel_guess(MULTILEVEL_SPEC, MULTILEVEL_PARAMS, levels=3, k_want=8, k_trial=12, tol=1e-6)
+    dsub = int(sub.strata[-1])
+    assert np.all(g[dsub:] == 0.0)
+    ml = {"full_dim": np.array(int(full.strata[-1])), "strata": full.strata, "level_dims": np.array([r[1] for r in lv]),
+          "level_nmax": np.array([r[0] for r in lv]), "level_iterations": np.array([r[2] for r in lv]),
+          "level_converged": np.array([r[3] for r in lv]), "guess_head": g[:dsub], "guess_width": np.array(g.shape[1]),
+          "sub_block_boundaries": h.block_boundaries, "sub_entry_offsets": h.entry_offsets, "sub_rows": h.rows,
+          "sub_cols": h.cols, "sub_values": h.values, "sub_groups": sub.groups, "sub_precision": np.array(h.precision)}
+    np.savez_compressed(os.path.join(OUT, "multilevel.npz"), **ml)
+    print("multilevel levels", lv, "guess", g.shape)
+
+
 def digest(h):
     m = hashlib.sha256()
     for a in (h.block_boundaries, h.entry_offsets, h.rows, h.cols, h.values, h.groups):
@@ -197,6 +228,9 @@ def main():
 if __name__ == "__main__":
     if sys.argv[1:] == ["lanczos"]:
         make_lanczos()
+    elif sys.argv[1:] == ["multilevel"]:
+        make_multilevel()
     else:
         main()
         make_lanczos()
+        make_multilevel()

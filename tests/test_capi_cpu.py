@@ -125,3 +125,11 @@ def test_lanczos_host_helpers():
     assert np.linalg.norm(v) == pytest.approx(1.0, abs=1e-15)
     with pytest.raises(ci.ConfigError):
         ci.lanczos_default_start(10, 0)
+
+
+def test_pad_from_subspace_host():
+    x = np.arange(12.0).reshape(4, 3)
+    p = ci.pad_from_subspace(x, 6)
+    assert p.shape == (6, 3) and np.array_equal(p[:4], x) and not p[4:].any()
+    with pytest.raises(ci.DimensionMismatch):
+        ci.pad_from_subspace(x, 3)

@@ -198,6 +198,26 @@ def test_oracle_lanczos(golden, name):
     np.testing.assert_allclose(ov, 1.0, atol=1e-6)
 
 
+def test_oracle_multilevel_guess(golden):
+    """guess.cpp:66-117 restated (leading blocks as the level problems) vs the
+    reference's own multilevel_guess on 4He Nmax 6: same level dimensions,
+    iteration counts and convergence; the guess spans the same columns."""
+    from conftest import multilevel_operator
+
+    g = golden("multilevel")
+    h = multilevel_operator(g)
+    guess, lv = O.multilevel_guess(h, g["level_dims"].tolist(), k_want=8, k_trial=12, tol=1e-6)
+    assert [r[0] for r in lv] == g["level_dims"].tolist()
+    assert [r[1] for r in lv] == g["level_iterations"].tolist()
+    assert [r[2] for r in lv] == g["level_converged"].tolist()
+    head = g["guess_head"]
+    assert guess.shape == (h.dim, int(g["guess_width"]))
+    assert np.all(guess[head.shape[0]:] == 0.0)
+    ov = np.abs(np.sum(guess[: head.shape[0]] * head, axis=0))
+    np.testing.assert_allclose(ov[:8], 1.0, atol=1e-8)
+    np.testing.assert_allclose(ov, 1.0, atol=1e-4)
+
+
 # ------------------------------------------------------- SPEC known answers
 
 def test_spec_spmm_known_answers():
