@@ -57,6 +57,13 @@ typedef struct cieg_host_csb cieg_host_csb;
 /* ---- context --------------------------------------------------------- */
 /* Bind a context (one CUDA stream) to a device. No reference analogue: the
  * reference is host-only. */
+/* Device buffers on the context's GPU for integrators that hold host data
+ * (the reference-side drop-in stages ci::BlockVectors through these).
+ * cieg_memcpy kind: 0 host->device, 1 device->host, 2 device->device;
+ * ordered on the context stream and synchronous. */
+int cieg_device_alloc(cieg_ctx* ctx, uint64_t bytes, void** out);
+int cieg_device_free(cieg_ctx* ctx, void* p);
+int cieg_memcpy(cieg_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind);
 int cieg_ctx_create(int device, cieg_ctx** out);
 int cieg_ctx_destroy(cieg_ctx* ctx);
 int cieg_ctx_synchronize(cieg_ctx* ctx);

@@ -15,6 +15,8 @@
 // Built by integration/Makefile (needs the reference headers; Eigen comes from
 // oracle/eigen_shim in this image).
 #include <cstring>
+#include <fstream>
+#include <optional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -24,6 +26,7 @@
 #include "ci/csb.hpp"
 #include "ci/errors.hpp"
 #include "ci/hamiltonian.hpp"
+#include "ci/guess.hpp"
 #include "ci/lanczos.hpp"
 #include "ci/lobpcg.hpp"
 #include "ci/precond.hpp"
@@ -121,6 +124,20 @@ cieg_precond_config config(const ci::PrecondConfig& c) {
   return cieg_precond_config{c.inner_iters, c.small_block_cutoff, c.engage_after, c.relres_gate,
                              c.near_converged_factor, c.far_threshold, c.column_floor_factor};
 }
+
+// Device staging of host ci::BlockVectors (row-major, the layout the C ABI uses).
+struct DevBlock {
+  void* p = nullptr;
+  DevBlock(const double* host, std::size_t count) {
+    check(cieg_device_alloc(dev().ctx, sizeof(double) * count, &p));
+    if (host && count) check(cieg_memcpy(dev().ctx, p, host, sizeof(double) * count, 0));
+  }
+  ~DevBlock() { cieg_device_free(dev().ctx, p); }
+  double* d() const { return static_cast<double*>(p); }
+  void to_host(double* host, std::size_t count) const {
+    if (count) check(cieg_memcpy(dev().ctx, host, p, sizeof(double) * count, 1));
+  }
+};
 
 }  // namespace
 
@@ -249,6 +266,100 @@ SolveReport lanczos_solve(const CsbMatrix& h, const Eigen::VectorXd& v0, const L
   return out;
 }
 
+// lobpcg.hpp:92-93 -- ci::orthonormalize on the GPU.
+BlockVectors orthonormalize(const BlockVectors& y, double drop_tol, const BlockVectors* against) {
+  if (against && against->dim() != y.dim()) throw DimensionMismatch("orthonormalize: row counts differ");
+  DevBlock dy(y.values().data(), y.values().size());
+  std::unique_ptr<DevBlock> da;
+  if (against && against->width()) da = std::make_unique<DevBlock>(against->values().data(), against->values().size());
+  std::uint32_t k = 0;
+  check(cieg_orthonormalize(dev().ctx, dy.d(), y.dim(), y.width(), drop_tol, da ? da->d() : nullptr,
+                            da ? against->width() : 0, &k));
+  BlockVectors out(y.dim(), k);
+  dy.to_host(out.values().data(), out.values().size());
+  return out;
+}
+
+// lobpcg.hpp:84-86 -- ci::rayleigh_ritz on the GPU.
+std::pair<std::vector<double>, SubspaceCoefficients> rayleigh_ritz(const BlockVectors& y_basis,
+                                                                   const BlockVectors& hy, int k_trial, int x_width,
+                                                                   int w_width, int p_width) {
+  const int m = static_cast<int>(y_basis.width());
+  if (k_trial > m) throw DimensionMismatch("rayleigh_ritz: k_trial exceeds basis width");
+  if (hy.width() != y_basis.width() || hy.dim() != y_basis.dim())
+    throw DimensionMismatch("rayleigh_ritz: HY shape mismatch");
+  DevBlock dy(y_basis.values().data(), y_basis.values().size()), dh(hy.values().data(), hy.values().size());
+  std::vector<double> theta(k_trial);
+  SubspaceCoefficients c;
+  c.g.resize(m, k_trial);
+  check(cieg_rayleigh_ritz(dev().ctx, dy.d(), dh.d(), y_basis.dim(), m, k_trial, theta.data(), c.g.data()));
+  c.x_width = x_width < 0 ? m : x_width;
+  c.w_width = w_width;
+  c.p_width = p_width;
+  return {std::move(theta), std::move(c)};
+}
+
+// lobpcg.hpp:97-99 -- ci::residual_norms on the GPU.
+std::vector<double> residual_norms(const CsbMatrix& h, const BlockVectors& x, const std::vector<double>& theta,
+                                   std::optional<double> norm_est) {
+  if (x.width() != theta.size()) throw DimensionMismatch("residual_norms: theta width mismatch");
+  DevBlock dx(x.values().data(), x.values().size());
+  std::vector<double> out(x.width());
+  check(cieg_residual_norms(dev().ctx, matrix(h), dx.d(), x.width(), theta.data(), norm_est.value_or(0.0),
+                            out.data()));
+  return out;
+}
+
+// guess.hpp:21 -- host logic.
+BlockVectors pad_from_subspace(const BlockVectors& x1, std::uint32_t dim) {
+  BlockVectors out(dim, x1.width());
+  check(cieg_pad_from_subspace(x1.values().data(), x1.dim(), x1.width(), dim, out.values().data()));
+  return out;
+}
+
+// guess.hpp:66-69 -- BVEC files (host I/O), the load orthonormalized on the GPU.
+void save_vectors(const BlockVectors& x, const std::string& path) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw FormatError("cannot open for writing: " + path);
+  os.write("BVEC", 4);
+  const std::uint64_t dim = x.dim();
+  const std::uint32_t width = x.width();
+  os.write(reinterpret_cast<const char*>(&dim), sizeof dim);
+  os.write(reinterpret_cast<const char*>(&width), sizeof width);
+  for (std::uint32_t j = 0; j < width; ++j)
+    for (std::uint32_t i = 0; i < x.dim(); ++i) {
+      const double v = x.at(i, j);
+      os.write(reinterpret_cast<const char*>(&v), sizeof v);
+    }
+}
+
+BlockVectors load_guess_file(const std::string& path, std::uint32_t dim, std::uint32_t k) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw FormatError("cannot open: " + path);
+  char magic[4];
+  is.read(magic, 4);
+  if (!is || std::memcmp(magic, "BVEC", 4) != 0) throw FormatError("bad magic; not a BVEC file: " + path);
+  std::uint64_t file_dim = 0;
+  std::uint32_t width = 0;
+  is.read(reinterpret_cast<char*>(&file_dim), sizeof file_dim);
+  is.read(reinterpret_cast<char*>(&width), sizeof width);
+  if (!is) throw FormatError("truncated BVEC header: " + path);
+  if (file_dim != dim)
+    throw DimensionMismatch("vector file dimension " + std::to_string(file_dim) + " != basis dimension " +
+                            std::to_string(dim));
+  if (width < k)
+    throw DimensionMismatch("vector file holds " + std::to_string(width) + " columns, need " + std::to_string(k));
+  BlockVectors out(dim, k);
+  for (std::uint32_t j = 0; j < k; ++j)
+    for (std::uint32_t i = 0; i < dim; ++i) {
+      double v;
+      is.read(reinterpret_cast<char*>(&v), sizeof v);
+      if (!is) throw FormatError("truncated BVEC payload: " + path);
+      out.at(i, j) = v;
+    }
+  return orthonormalize(out);
+}
+
 }  // namespace ci
 
 // C entry for the test harness: run the reference-API call sequence of the
@@ -336,6 +447,35 @@ extern "C" int dropin_lanczos(const cieg_csb_view* v, const double* v0, int k_wa
     *iters_out = rep.iterations;
     return 0;
   } catch (const ci::Error& e) {
+    return 1;
+  }
+}
+
+// ci::orthonormalize / ci::residual_norms through the drop-in (test harness).
+extern "C" int dropin_orthonormalize(std::uint32_t n, std::uint32_t k, const double* y, double drop_tol, double* out,
+                                     std::uint32_t* kout) {
+  try {
+    ci::BlockVectors Y(n, k);
+    std::memcpy(Y.values().data(), y, sizeof(double) * n * k);
+    ci::BlockVectors Q = ci::orthonormalize(Y, drop_tol);
+    *kout = Q.width();
+    std::memcpy(out, Q.values().data(), sizeof(double) * Q.values().size());
+    return 0;
+  } catch (const ci::Error&) {
+    return 1;
+  }
+}
+
+extern "C" int dropin_residual_norms(const cieg_csb_view* v, const double* x, std::uint32_t k, const double* theta,
+                                     double* out) {
+  try {
+    ci::CsbMatrix h = from_view(v);
+    ci::BlockVectors X(h.dim, k);
+    std::memcpy(X.values().data(), x, sizeof(double) * h.dim * k);
+    std::vector<double> r = ci::residual_norms(h, X, std::vector<double>(theta, theta + k));
+    std::memcpy(out, r.data(), sizeof(double) * k);
+    return 0;
+  } catch (const ci::Error&) {
     return 1;
   }
 }

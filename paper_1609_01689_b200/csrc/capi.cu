@@ -78,6 +78,34 @@ extern "C" {
 const char* cieg_last_error(void) { return cieg::g_last_error.c_str(); }
 const char* cieg_version(void) { return "cieg 0.1 (sm_100a)"; }
 
+int cieg_device_alloc(cieg_ctx* ctx, uint64_t bytes, void** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_device_alloc: null argument");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    *out = nullptr;
+    CIEG_CUDA(cudaMalloc(out, std::max<uint64_t>(1, bytes)));
+  });
+}
+
+int cieg_device_free(cieg_ctx* ctx, void* p) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_device_free: null context");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    if (p) CIEG_CUDA(cudaFree(p));
+  });
+}
+
+int cieg_memcpy(cieg_ctx* ctx, void* dst, const void* src, uint64_t bytes, int kind) {
+  return cieg::guarded([&] {
+    if (!ctx || (bytes && (!dst || !src))) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_memcpy: null argument");
+    static const cudaMemcpyKind kinds[3] = {cudaMemcpyHostToDevice, cudaMemcpyDeviceToHost, cudaMemcpyDeviceToDevice};
+    if (kind < 0 || kind > 2) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_memcpy: kind must be 0 (H2D), 1 (D2H) or 2 (D2D)");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    if (bytes) CIEG_CUDA(cudaMemcpyAsync(dst, src, bytes, kinds[kind], ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int cieg_ctx_create(int device, cieg_ctx** out) {
   return cieg::guarded([&] {
     if (!out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_ctx_create: null output");

@@ -56,3 +56,25 @@ def test_dropin_lanczos_matches_reference(golden, name):
     assert rc == 0
     assert iters.value == int(g[f"{name}_iterations"])
     np.testing.assert_allclose(eig, g[f"{name}_eigenvalues"], rtol=1e-10)
+
+
+def test_dropin_orthonormalize_and_residual_norms(ref_lib):
+    """ci::orthonormalize / ci::residual_norms through the drop-in vs the reference."""
+    if not os.path.exists(LIB):
+        pytest.skip("integration/_build not built (needs the reference headers at build time)")
+    lib = C.CDLL(LIB)
+    y = ci.random_block(1500, 6, 4)
+    out = np.zeros_like(y)
+    kout = C.c_uint32()
+    pd = lambda a: a.ctypes.data_as(C.POINTER(C.c_double))  # noqa: E731
+    assert lib.dropin_orthonormalize(C.c_uint32(1500), C.c_uint32(6), pd(y), C.c_double(1e-8), pd(out),
+                                     C.byref(kout)) == 0
+    assert kout.value == 6
+    np.testing.assert_allclose(out, ref_lib.orthonormalize(y), atol=1e-12)
+    h = gen_from((2000, 4, 64, 0.1, 0.5, 11, 1, 500))
+    x = ci.random_block(2000, 3, 8)
+    th = np.array([0.5, -1.0, 2.0])
+    r = np.zeros(3)
+    v = h.view()
+    assert lib.dropin_residual_norms(C.byref(v), pd(x), C.c_uint32(3), pd(th), pd(r)) == 0
+    np.testing.assert_allclose(r, ref_lib.residual_norms(ref_lib.RefMatrix(h), x, th), rtol=1e-12)
