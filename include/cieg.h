@@ -159,8 +159,11 @@ typedef struct {
   void* user;
   /* in-place sum over ranks of `count` doubles in host memory (Gram partials) */
   int (*allreduce_sum)(void* user, double* host_buf, uint64_t count);
-  /* all-gather: every rank's local rows of a row-distributed block (device,
-   * local_rows x m) into the full-length block x_full (device, dim x m) */
+  /* gather before each SpMM: every rank's local rows of a row-distributed
+   * block (device, local_rows x m) into the full-length block x_full
+   * (device, dim x m). The shard's kernel reads x_full only on its halo rows
+   * [halo_lo, halo_hi) (cieg_matrix_rows), so filling those suffices -- a
+   * point-to-point halo exchange instead of an all-gather (dist.py). */
   int (*allgather_rows)(void* user, const double* x_local_dev, uint32_t m, double* x_full_dev);
 } cieg_dist_hooks;
 

@@ -7,9 +7,14 @@ one process per GPU with torch.distributed for the plumbing.
   (I, P) landing in its rows -- owner-computes needs no reduce-scatter of
   transposed partials; tiles on a shard boundary are held by both owners) and
   its rows of every block vector and tile-diagonal group.
-* SpMM: the rank's rows of X are all-gathered (one NCCL broadcast per rank
-  into the full-length X; uneven row counts), then the local owner-computes
-  kernel writes the rank's rows of U.
+* SpMM: each rank's owner kernel reads X only on its halo rows
+  [halo_lo, halo_hi) (cieg_matrix_rows), so before K1 every rank receives
+  exactly the rows of its halo that other ranks own, point to point
+  (``halo_exchange``: batched isend/irecv, SURVEY.md 8(e) "optimised
+  variant"), then writes its rows of U. For the block-banded sector matrices
+  the halo is the +-2-sector band, so the exchanged volume stays flat as the
+  rank count grows, where an all-gather (``allgather_rows``, kept for
+  comparison) moves (G-1)/G of X to every rank.
 * Grams: a local partial over the rank's rows, then an all-reduce; all ranks
   then take identical control-flow decisions (the solver loop is the same
   C++ code as the single-GPU path, driven through cieg_lobpcg_solve_dist's
@@ -59,6 +64,75 @@ def allgather_rows(x_local: torch.Tensor, row_bounds, out: torch.Tensor, group=N
     return out
 
 
+class ExchangePlan:
+    """Who sends which owned rows to whom: recvs[(peer, a, b)] = peer's rows
+    [a, b) inside this rank's halo, sends[(peer, a, b)] = this rank's rows
+    inside peer's halo. Built from every rank's row bounds and halo."""
+
+    def __init__(self, row_bounds, halo_lo, halo_hi, rank: int):
+        world = len(row_bounds) - 1
+        self.rank = rank
+        self.lo, self.hi = int(row_bounds[rank]), int(row_bounds[rank + 1])
+        self.sends, self.recvs = [], []
+        for s in range(world):
+            if s == rank:
+                continue
+            a, b = max(self.lo, int(halo_lo[s])), min(self.hi, int(halo_hi[s]))
+            if b > a:
+                self.sends.append((s, a, b))
+            a, b = max(int(row_bounds[s]), int(halo_lo[rank])), min(int(row_bounds[s + 1]), int(halo_hi[rank]))
+            if b > a:
+                self.recvs.append((s, a, b))
+
+    def recv_rows(self) -> int:
+        return sum(b - a for _, a, b in self.recvs)
+
+    def send_rows(self) -> int:
+        return sum(b - a for _, a, b in self.sends)
+
+
+def gather_halos(halo_lo: int, halo_hi: int, device, group=None):
+    """Every rank's (halo_lo, halo_hi), from each rank's own matrix."""
+    world = dist.get_world_size(group)
+    mine = torch.tensor([halo_lo, halo_hi], dtype=torch.int64, device=device)
+    allh = [torch.zeros(2, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(allh, mine, group=group)
+    hs = torch.stack(allh).cpu().numpy()
+    return hs[:, 0], hs[:, 1]
+
+
+def halo_exchange(x_local: torch.Tensor, plan: ExchangePlan, out: torch.Tensor, group=None) -> torch.Tensor:
+    """out[a:b] = X[a:b] for every row this rank's SpMM reads: own rows copied,
+    peers' rows received point to point (one batched isend/irecv round)."""
+    out[plan.lo:plan.hi].copy_(x_local)
+    if out.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host tensors only (single-GPU multi-rank runs): stage
+        xh = x_local.cpu()
+        hb = {(a, b): torch.empty((b - a,) + tuple(out.shape[1:]), dtype=out.dtype) for _, a, b in plan.recvs}
+        ops = [dist.P2POp(dist.irecv, hb[(a, b)], peer if group is None else dist.get_global_rank(group, peer), group)
+               for peer, a, b in plan.recvs]
+        ops += [dist.P2POp(dist.isend, xh[a - plan.lo:b - plan.lo].contiguous(),
+                           peer if group is None else dist.get_global_rank(group, peer), group)
+                for peer, a, b in plan.sends]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        for (a, b), t in hb.items():
+            out[a:b].copy_(t)
+        return out
+    ops = []
+    for peer, a, b in plan.recvs:
+        g = peer if group is None else dist.get_global_rank(group, peer)
+        ops.append(dist.P2POp(dist.irecv, out[a:b], g, group))
+    for peer, a, b in plan.sends:
+        g = peer if group is None else dist.get_global_rank(group, peer)
+        ops.append(dist.P2POp(dist.isend, x_local[a - plan.lo:b - plan.lo], g, group))
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return out
+
+
 def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
@@ -97,16 +171,22 @@ class ShardedMatrix:
         import weakref
 
         self._fin = weakref.finalize(self, lib.cieg_matrix_destroy, handle)
+        self.plan = ExchangePlan(self.row_bounds, self.halo_lo, self.halo_hi, rank)
 
     @property
     def local_rows(self) -> int:
         return self.row_hi - self.row_lo
 
-    def spmm(self, x_local: torch.Tensor, group=None) -> torch.Tensor:
-        """Rows [row_lo, row_hi) of H X from the rank's rows of X."""
+    def spmm(self, x_local: torch.Tensor, group=None, exchange: str = "halo") -> torch.Tensor:
+        """Rows [row_lo, row_hi) of H X from the rank's rows of X (the halo
+        rows of X arrive point to point; exchange="allgather" for the
+        all-gather variant)."""
         m = x_local.shape[1]
         full = torch.empty((self.h.dim, m), dtype=torch.float64, device=x_local.device)
-        allgather_rows(x_local, self.row_bounds, full, group)
+        if exchange == "halo":
+            halo_exchange(x_local, self.plan, full, group)
+        else:
+            allgather_rows(x_local, self.row_bounds, full, group)
         y = torch.empty((self.local_rows, m), dtype=torch.float64, device=x_local.device)
         torch.cuda.current_stream().synchronize()
         ci._check(_lib.load().cieg_spmm(self.device.handle, self.handle, C.c_void_p(full.data_ptr()),
@@ -152,11 +232,12 @@ def lobpcg_solve_dist(sm: ShardedMatrix, x0_local: np.ndarray, options: ci.Lobpc
             return 1
 
     def _allgather(_user, xptr, m, fullptr):
+        # the hook need only fill the rank's halo rows: point-to-point exchange
         try:
             nloc = sm.local_rows
             xl = _view(xptr, (nloc, m), tdev)
             full = _view(fullptr, (dim, m), tdev)
-            allgather_rows(xl, rb, full, group)
+            halo_exchange(xl, sm.plan, full, group)
             return 0
         except Exception:  # noqa: BLE001
             return 1

@@ -59,6 +59,13 @@ def _worker(rank, world, port, golden_path, out_q):
         np.add.at(y, c[mine_col] - lo, v[mine_col, None] * xp[r[mine_col]])
         res["halo_ok"] = bool(np.isfinite(y).all())
         res["shard_rows_ok"] = bool(np.allclose(y, O.spmm(h, x)[lo:hi], rtol=0, atol=1e-13))
+        # (2b) the point-to-point halo exchange fills exactly the halo
+        plan = D.ExchangePlan(rb, hl, hh, rank)
+        hx = torch.full((h.dim, 5), float("nan"), dtype=torch.float64)
+        D.halo_exchange(torch.from_numpy(x[lo:hi].copy()), plan, hx)
+        hxn = hx.numpy()
+        res["halo_exchange_ok"] = bool(np.array_equal(hxn[hl[rank]:hh[rank]], x[hl[rank]:hh[rank]]))
+        res["halo_rows"] = plan.recv_rows()
 
         # (3) sharded LOBPCG: local rows, all-gathered SpMM input, all-reduced Grams
         def inner(a, b):
@@ -66,9 +73,9 @@ def _worker(rank, world, port, golden_path, out_q):
             D.allreduce_sum_(t)
             return t.numpy()
 
-        def matvec(vloc):
+        def matvec(vloc):  # halo rows only, as the device path does
             f = torch.zeros((h.dim, vloc.shape[1]), dtype=torch.float64)
-            D.allgather_rows(torch.from_numpy(np.ascontiguousarray(vloc)), rb, f)
+            D.halo_exchange(torch.from_numpy(np.ascontiguousarray(vloc)), plan, f)
             return O.spmm(h, f.numpy())[lo:hi]
 
         k, kt, tol, pre, seed = g["sector_f64_prec_meta"]
@@ -124,8 +131,65 @@ def test_gloo_world2_sharded_path(golden):
     for rank in (0, 1):
         res = out[rank]
         assert "error" not in res, res.get("error")
-        assert res["allgather_ok"] and res["halo_ok"] and res["shard_rows_ok"]
+        assert res["allgather_ok"] and res["halo_ok"] and res["shard_rows_ok"] and res["halo_exchange_ok"]
         assert res["iterations"] == int(g["sector_f64_prec_iterations"])
         assert res["counters"] == g["sector_f64_prec_counters"].tolist()
         np.testing.assert_allclose(res["eigenvalues"], g["sector_f64_prec_eigenvalues"], rtol=1e-10)
     assert out[0]["eigenvalues"] == out[1]["eigenvalues"]  # identical decisions on every rank
+
+
+def _exchange_worker(rank, world, port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01689_b200 import ci, configs
+    from paper_1609_01689_b200 import dist as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        h = configs.CFG1.generate()
+        rb, hl, hh = D.row_partition(h, world)
+        lo, hi = int(rb[rank]), int(rb[rank + 1])
+        x = ci.random_block(h.dim, 3, 21)
+        plan = D.ExchangePlan(rb, hl, hh, rank)
+        gl, gh = D.gather_halos(int(hl[rank]), int(hh[rank]), torch.device("cpu"))
+        res["gather_ok"] = gl.tolist() == hl.tolist() and gh.tolist() == hh.tolist()
+        out = torch.full((h.dim, 3), float("nan"), dtype=torch.float64)
+        D.halo_exchange(torch.from_numpy(x[lo:hi].copy()), plan, out)
+        o = out.numpy()
+        res["halo_ok"] = bool(np.array_equal(o[hl[rank]:hh[rank]], x[hl[rank]:hh[rank]]))
+        res["outside_untouched"] = bool(np.isnan(o[: hl[rank]]).all() and np.isnan(o[hh[rank]:]).all())
+        res["recv_rows"] = plan.recv_rows()
+        res["send_rows"] = plan.send_rows()
+    except Exception as e:  # pragma: no cover
+        res["error"] = repr(e)
+    finally:
+        dist.destroy_process_group()
+    out_q.put((rank, res))
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_gloo_halo_exchange(world):
+    """Point-to-point halo exchange (SURVEY.md 8(e) optimised variant) with
+    several peers: every rank ends up with exactly X on its halo rows, rows
+    outside the halo are never written, and the sent rows match the received
+    ones across ranks."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert "error" not in out[r], out[r].get("error")
+        assert out[r]["gather_ok"] and out[r]["halo_ok"] and out[r]["outside_untouched"]
+    assert sum(out[r]["recv_rows"] for r in range(world)) == sum(out[r]["send_rows"] for r in range(world))
