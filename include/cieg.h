@@ -125,6 +125,12 @@ int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y
  * synchronous on return. This is the call a ci::spmm drop-in makes. */
 int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
                    uint32_t m);
+/* `count` independent products U_i = H X_i through host buffers (pinned for
+ * full overlap), pipelined: the upload of X_{i+1} and the download of
+ * U_{i-1} run on the copy engines while K1 computes U_i. Same results as
+ * `count` calls of cieg_spmm_host. */
+int cieg_spmm_host_batch(cieg_ctx* ctx, const cieg_mat* mat, const double* const* x_hosts, double* const* y_hosts,
+                         uint32_t m, uint32_t count);
 
 /* ---- row-block sharding over several GPUs ------------ */
 /* Partition the rows over nranks at group boundaries (a group never straddles

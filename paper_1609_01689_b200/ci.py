@@ -403,6 +403,23 @@ class DeviceMatrix:
         _check(_lib.load().cieg_spmm_host(self.device.handle, self.handle, _ptr(x), _ptr(y), x.shape[1]))
         return y
 
+    def spmm_host_batch(self, xs: Sequence[np.ndarray]) -> list:
+        """Independent products H X_i through host memory with the copies of
+        neighbouring products overlapping K1 (cieg_spmm_host_batch). Pass
+        pinned arrays for full overlap."""
+        xs = [_f64(x) for x in xs]
+        if not xs:
+            return []
+        m = xs[0].shape[1]
+        if any(x.shape != (self.dim, m) for x in xs):
+            raise DimensionMismatch("spmm: vector dim != matrix dim")
+        ys = [np.empty((self.row_hi - self.row_lo, m)) for _ in xs]
+        pd = C.POINTER(C.c_double)
+        xa = (pd * len(xs))(*[_ptr(x) for x in xs])
+        ya = (pd * len(ys))(*[_ptr(y) for y in ys])
+        _check(_lib.load().cieg_spmm_host_batch(self.device.handle, self.handle, xa, ya, m, len(xs)))
+        return ys
+
     def spmm_ptr(self, x_ptr: int, y_ptr: int, m: int) -> None:
         """Device-pointer SpMM on the device's stream (row-major n x m)."""
         _check(_lib.load().cieg_spmm(self.device.handle, self.handle, C.c_void_p(x_ptr), C.c_void_p(y_ptr), m))

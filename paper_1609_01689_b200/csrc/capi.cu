@@ -401,4 +401,68 @@ int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, dou
   });
 }
 
+int cieg_spmm_host_batch(cieg_ctx* ctx, const cieg_mat* mat, const double* const* x_hosts, double* const* y_hosts,
+                         uint32_t m, uint32_t count) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat || (count && (!x_hosts || !y_hosts)))
+      cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host_batch: null argument");
+    const std::size_t xbytes = static_cast<std::size_t>(mat->dim) * m * sizeof(double);
+    const std::size_t ybytes = static_cast<std::size_t>(mat->row_hi - mat->row_lo) * m * sizeof(double);
+    if (xbytes == 0 || count == 0) return;
+    for (uint32_t i = 0; i < count; ++i)
+      if (!x_hosts[i] || !y_hosts[i]) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host_batch: null vector");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    double* dx[2] = {static_cast<double*>(ctx->scratch_x.get(xbytes)), static_cast<double*>(ctx->scratch_x2.get(xbytes))};
+    double* dy[2] = {static_cast<double*>(ctx->scratch_y.get(ybytes)), static_cast<double*>(ctx->scratch_y2.get(ybytes))};
+    // Three-stage pipeline over independent products: the upload of X_{i+1}
+    // and the download of U_{i-1} run on the two copy engines while K1
+    // computes U_i on the context stream; device X / U are double-buffered.
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t uploaded[2] = {}, computed[2] = {}, downloaded[2] = {};
+    auto cleanup = [&] {
+      for (int b = 0; b < 2; ++b) {
+        if (uploaded[b]) cudaEventDestroy(uploaded[b]);
+        if (computed[b]) cudaEventDestroy(computed[b]);
+        if (downloaded[b]) cudaEventDestroy(downloaded[b]);
+      }
+      if (up) cudaStreamDestroy(up);
+      if (down) cudaStreamDestroy(down);
+    };
+    try {
+      CIEG_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+      CIEG_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+      for (int b = 0; b < 2; ++b) {
+        CIEG_CUDA(cudaEventCreateWithFlags(&uploaded[b], cudaEventDisableTiming));
+        CIEG_CUDA(cudaEventCreateWithFlags(&computed[b], cudaEventDisableTiming));
+        CIEG_CUDA(cudaEventCreateWithFlags(&downloaded[b], cudaEventDisableTiming));
+      }
+      // nothing may touch the buffers before work already queued on the context stream
+      CIEG_CUDA(cudaEventRecord(computed[0], ctx->stream));
+      CIEG_CUDA(cudaEventRecord(computed[1], ctx->stream));
+      CIEG_CUDA(cudaEventRecord(downloaded[0], ctx->stream));
+      CIEG_CUDA(cudaEventRecord(downloaded[1], ctx->stream));
+      for (uint32_t i = 0; i < count; ++i) {
+        const int b = static_cast<int>(i & 1u);
+        CIEG_CUDA(cudaStreamWaitEvent(up, computed[b], 0));  // K1 of step i-2 has read X[b]
+        CIEG_CUDA(cudaMemcpyAsync(dx[b], x_hosts[i], xbytes, cudaMemcpyHostToDevice, up));
+        CIEG_CUDA(cudaEventRecord(uploaded[b], up));
+        CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, uploaded[b], 0));
+        CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, downloaded[b], 0));  // U[b] of step i-2 is home
+        cieg::launch_spmm(ctx, mat, dx[b], m, dy[b], m, m);
+        CIEG_CUDA(cudaEventRecord(computed[b], ctx->stream));
+        CIEG_CUDA(cudaStreamWaitEvent(down, computed[b], 0));
+        CIEG_CUDA(cudaMemcpyAsync(y_hosts[i], dy[b], ybytes, cudaMemcpyDeviceToHost, down));
+        CIEG_CUDA(cudaEventRecord(downloaded[b], down));
+      }
+      CIEG_CUDA(cudaStreamSynchronize(down));
+      CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+      CIEG_CUDA(cudaStreamSynchronize(up));
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 }  // extern "C"

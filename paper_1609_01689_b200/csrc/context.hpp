@@ -67,6 +67,7 @@ struct cieg_ctx {
   int exact_order = 0;  // 1: K5 reproduces the reference's operation order bit for bit
   int sm_count = 148;
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
+  cieg::DevBuf scratch_x2, scratch_y2;  // second buffers of the pipelined host batch
   cieg::PinnedBuf pinned_small;
 };
 

@@ -139,3 +139,14 @@ def _row_product(h, row, x):
         sel = np.nonzero(m)[0] + e0
         out += (h.values[sel].astype(np.float64)[:, None] * x[bb[i] + h.rows[sel].astype(np.int64)]).sum(0)
     return out
+
+
+def test_spmm_host_batch_matches_single_calls():
+    """cieg_spmm_host_batch (pipelined copies) = cieg_spmm_host per product, bitwise."""
+    h = gen_from((3072, 3, 256, 0.2, 0.4, 13, 0, 2000))
+    dm = ci.DeviceMatrix(h)
+    xs = [ci.random_block(h.dim, 16, s) for s in range(5)]
+    ys = dm.spmm_host_batch(xs)
+    for x, y in zip(xs, ys):
+        assert np.array_equal(y, dm.spmm_host(x))
+    assert dm.spmm_host_batch([]) == []
