@@ -27,12 +27,16 @@ struct GramUnroll {
   static constexpr int kU = (MT + NT) <= 4 ? 8 : ((MT + NT) <= 8 ? 4 : ((MT + NT) <= 10 ? 2 : 1));
 };
 
-template <int MT, int NT>
+// SYM (L and R the same view, MT == NT): the B fragments are the A
+// fragments and only tiles nt >= mt are computed; the reduction mirrors the
+// rest (tile (n, m) is the exact transpose of tile (m, n): same products,
+// same accumulation order).
+template <int MT, int NT, bool SYM = false>
 __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R, std::uint32_t n,
                                                                std::uint32_t rows_per_warp,
                                                                double* partials) {
   constexpr int MA = 8 * MT, NB = 8 * NT;
-  constexpr int U = GramUnroll<MT, NT>::kU;
+  constexpr int U = SYM ? GramUnroll<MT, 0>::kU : GramUnroll<MT, NT>::kU;  // SYM loads A only
   __shared__ double red[MA * NB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -60,6 +64,7 @@ __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R,
     std::uint32_t c = 8 * nt + g;
     pb[nt] = nullptr;
     lb[nt] = 0;
+    if (SYM) continue;
     for (int s = 0; s < R.nseg; ++s) {
       if (c < R.s[s].w) {
         pb[nt] = R.s[s].p + c;
@@ -88,15 +93,20 @@ __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R,
       const bool ok = i < r1;
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt) a[u][mt] = (ok && pa[mt]) ? __ldg(pa[mt] + i * la[mt]) : 0.0;
+      if (!SYM) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[u][nt] = (ok && pb[nt]) ? __ldg(pb[nt] + i * lb[nt]) : 0.0;
+        for (int nt = 0; nt < NT; ++nt) b[u][nt] = (ok && pb[nt]) ? __ldg(pb[nt] + i * lb[nt]) : 0.0;
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u)
 #pragma unroll
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[u][mt], b[u][nt]);
+        for (int nt = 0; nt < NT; ++nt) {
+          if (SYM && nt < mt) continue;
+          dmma_8x8x4(acc[mt][nt][0], acc[mt][nt][1], a[u][mt], SYM ? a[u][nt] : b[u][nt]);
+        }
   }
 
   // warps fold their partials into one buffer in warp order (deterministic)
@@ -106,6 +116,7 @@ __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R,
       for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
+          if (SYM && nt < mt) continue;
           const int row = 8 * mt + g, col = 8 * nt + 2 * q;
           if (w == 0) {
             red[row * NB + col] = acc[mt][nt][0];
@@ -125,11 +136,16 @@ __global__ void __launch_bounds__(32 * kGramWarps) gram_kernel(View3 L, View3 R,
 // out[a + kx*b] (column major) = sum over block partials: one warp per
 // element, lane-strided partial sums then a fixed xor tree (deterministic).
 __global__ void gram_reduce_kernel(const double* partials, int nblocks, int MA, int NB, int kx,
-                                   int ky, double* out) {
+                                   int ky, int sym, double* out) {
   const int e = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (e >= kx * ky) return;
-  const int a = e % kx, b = e / kx;
+  int a = e % kx, b = e / kx;
+  if (sym && (a >> 3) > (b >> 3)) {  // lower tile: read the mirrored upper entry
+    const int t = a;
+    a = b;
+    b = t;
+  }
   double s = 0.0;
   for (int k = lane; k < nblocks; k += 32) s += partials[static_cast<std::size_t>(k) * MA * NB + a * NB + b];
   s = warp_sum(s);
@@ -140,6 +156,19 @@ template <int MT, int NT>
 void launch_gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R, int blocks,
                  std::uint32_t rpw, double* partials) {
   gram_kernel<MT, NT><<<blocks, 32 * kGramWarps, 0, ctx->stream>>>(L, R, n, rpw, partials);
+}
+
+template <int MT>
+void launch_gram_sym(cieg_ctx* ctx, std::uint32_t n, const View3& L, int blocks, std::uint32_t rpw,
+                     double* partials) {
+  gram_kernel<MT, MT, true><<<blocks, 32 * kGramWarps, 0, ctx->stream>>>(L, L, n, rpw, partials);
+}
+
+bool same_view(const View3& a, const View3& b) {
+  if (a.nseg != b.nseg || a.width != b.width) return false;
+  for (int s = 0; s < a.nseg; ++s)
+    if (a.s[s].p != b.s[s].p || a.s[s].ld != b.s[s].ld || a.s[s].w != b.s[s].w) return false;
+  return true;
 }
 
 using GramLauncher = void (*)(cieg_ctx*, std::uint32_t, const View3&, const View3&, int,
@@ -319,13 +348,25 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
   const int MA = 8 * MT, NB = 8 * NT;
   double* partials = static_cast<double*>(ctx->scratch_red.get(sizeof(double) * blocks * MA * NB + 64));
   double* dout = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 48 * 48));
+  const bool sym = same_view(L, R);  // X^T X: upper tiles only, mirrored
   if (n > 0) {
-    gram_launcher(MT, NT)(ctx, n, L, R, blocks, static_cast<std::uint32_t>(rpw), partials);
+    if (sym) {
+      switch (MT) {
+        case 1: launch_gram_sym<1>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+        case 2: launch_gram_sym<2>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+        case 3: launch_gram_sym<3>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+        case 4: launch_gram_sym<4>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+        case 5: launch_gram_sym<5>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+        default: launch_gram_sym<6>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+      }
+    } else {
+      gram_launcher(MT, NT)(ctx, n, L, R, blocks, static_cast<std::uint32_t>(rpw), partials);
+    }
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
     const int e = static_cast<int>(kx * ky);
-    gram_reduce_kernel<<<(e + 3) / 4, 128, 0, ctx->stream>>>(partials, blocks, MA, NB,
-                                                                  static_cast<int>(kx), static_cast<int>(ky), dout);
+    gram_reduce_kernel<<<(e + 3) / 4, 128, 0, ctx->stream>>>(partials, blocks, MA, NB, static_cast<int>(kx),
+                                                                  static_cast<int>(ky), sym ? 1 : 0, dout);
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
     double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
