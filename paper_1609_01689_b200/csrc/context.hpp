@@ -68,6 +68,7 @@ struct cieg_ctx {
   int sm_count = 148;
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
   cieg::DevBuf scratch_x2, scratch_y2;  // second buffers of the pipelined host batch
+  cieg::DevBuf scratch_flag;            // K1 non-finite-input flag
   cieg::PinnedBuf pinned_small;
 };
 

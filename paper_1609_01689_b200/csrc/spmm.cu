@@ -39,6 +39,7 @@
 
 #include "context.hpp"
 #include "device_common.cuh"
+#include "tile_layout.h"
 
 namespace cieg {
 namespace {
@@ -58,6 +59,7 @@ struct SpmmArgs {
   double* y;
   std::uint32_t ldx, ldy, mcols, npanels;
   std::uint32_t row_base;  // first owner row of a shard (U is written shard-local)
+  unsigned* nonfinite;     // set when an X value is Inf/NaN (staged as 0; fixed up after the launch)
 };
 
 constexpr int kProducerWarps = 8;
@@ -231,6 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
     load_batch(cur, cur.q0, qa);
     double xv[S::kSlabPer];
     load_slab<V, TD, NT>(a, cur, pt, xv);
+    bool nonfinite = false;
     int buf = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i) {
       const bool has_next = i + 1 < i_end;
@@ -253,8 +256,15 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       for (int j = 0; j < S::kSlabPer; ++j) {
         const int e = pt + j * kProducerThreads;
         const int k = e / (8 * NT), t = e - k * (8 * NT);
+        // A non-finite X value would meet the dense tile's explicit zeros
+        // (0 * Inf = NaN) where the reference multiplies stored entries
+        // only: it is staged as 0 and nonfinite_fix_kernel adds its terms.
+        // (Checked here, a whole item after the load was issued.)
+        const bool bad = !isfinite(xv[j]);
+        const double v = bad ? 0.0 : xv[j];
+        nonfinite |= bad;
         // NT == 2: columns g and 8 + g side by side (one 128-bit B load)
-        X[k * S::kSX + (NT == 2 ? 2 * (t & 7) + (t >> 3) : t)] = xv[j];
+        X[k * S::kSX + (NT == 2 ? 2 * (t & 7) + (t >> 3) : t)] = v;
       }
       if (has_next) load_slab<V, TD, NT>(a, nxt, pt, xv);
       const Item after = (i + 2 < i_end) ? load_item(a, i + 2) : nxt;
@@ -285,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       cur = nxt;
       nxt = after;
     }
+    if (nonfinite) *a.nonfinite = 1u;
   } else {
     // ------------------------------------------------------------ consumer
     const int cw = warp - kProducerWarps;
@@ -392,6 +403,53 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
   }
 }
 
+// Exact terms of non-finite X values (rare; exits at once when K1 saw none):
+// for every Inf/NaN x[j][c] on the shard's halo rows, every stored entry in
+// row or column j adds h * x[j][c] to the owner output it feeds -- the same
+// owner-computes terms K1 would have produced, now without the dense
+// tile's zeros. Inf/NaN absorb, so the non-finite results do not depend on
+// the order of the (atomic) additions.
+template <typename V>
+__global__ void nonfinite_fix_kernel(const SpmmArgs a, std::uint32_t te, int precision, std::uint32_t p_lo,
+                                     std::uint32_t p_hi, std::uint32_t halo_lo, std::uint32_t halo_hi) {
+  if (*a.nonfinite == 0u) return;
+  const std::uint32_t sa = cieg_tl::stride(te, precision);
+  const V* val = static_cast<const V*>(a.val);
+  const std::uint64_t total = static_cast<std::uint64_t>(halo_hi - halo_lo) * a.mcols;
+  for (std::uint64_t e = blockIdx.x * std::uint64_t(blockDim.x) + threadIdx.x; e < total;
+       e += std::uint64_t(gridDim.x) * blockDim.x) {
+    const std::uint32_t j = halo_lo + static_cast<std::uint32_t>(e / a.mcols);
+    const std::uint32_t c = static_cast<std::uint32_t>(e % a.mcols);
+    const double xv = a.x[static_cast<std::size_t>(j) * a.ldx + c];
+    if (isfinite(xv)) continue;
+    std::uint32_t lo = 0, hi = a.npanels;  // panel of row j
+    while (hi - lo > 1) {
+      const std::uint32_t mid = (lo + hi) / 2;
+      if (a.panel_start[mid] <= j) lo = mid; else hi = mid;
+    }
+    const std::uint32_t pjx = lo;
+    for (std::uint32_t P = p_lo; P < p_hi; ++P)
+      for (std::uint32_t w = a.work_off[P]; w < a.work_off[P + 1]; ++w) {
+        const std::uint32_t o = a.work_other[w], kind = a.work_kind[w];
+        if (P != pjx && o != pjx) continue;
+        const std::uint32_t pi = kind == 1 ? o : P, pj = kind == 0 ? o : P;
+        const std::uint32_t r0 = a.panel_start[pi], q0 = a.panel_start[pj];
+        const std::uint32_t t = a.work_tile[w];
+        for (std::uint64_t q = a.tile_off[t]; q < a.tile_off[t + 1]; ++q) {
+          const std::uint32_t off = a.idx[q] & 0xffffu;
+          const std::uint32_t r = off / sa, pc = off - r * sa;
+          if (pc >= te) continue;  // padding
+          const std::uint32_t gr = r0 + r, gc = q0 + cieg_tl::unperm(pc, precision);
+          const double h = static_cast<double>(val[q]);
+          // kind 0: Y[gr] += h x[gc]; kind 1: Y[gc] += h x[gr]; kind 2: both (gr != gc)
+          if (kind != 1 && gc == j) atomicAdd(&a.y[static_cast<std::size_t>(gr - a.row_base) * a.ldy + c], h * xv);
+          if (kind != 0 && gr == j && (kind == 1 || gr != gc))
+            atomicAdd(&a.y[static_cast<std::size_t>(gc - a.row_base) * a.ldy + c], h * xv);
+        }
+      }
+  }
+}
+
 template <typename V, int TD, int NT>
 void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   using S = Shape<V, TD, NT>;
@@ -434,7 +492,9 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   ldy,
                   mc,
                   m->npanels,
-                  m->row_lo};
+                  m->row_lo,
+                  static_cast<unsigned*>(ctx->scratch_flag.get(sizeof(unsigned)))};
+    CIEG_CUDA(cudaMemsetAsync(args.nonfinite, 0, sizeof(unsigned), ctx->stream));
     if (m->precision == 0) {
       if (m->tile_edge == 64)
         dispatch_nt<float, 64>(ctx, m, args, mc);
@@ -443,6 +503,19 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
     } else {  // fp64 values: 64-row tiles (a 128-row fp64 tile pair exceeds shared memory)
       dispatch_nt<double, 64>(ctx, m, args, mc);
     }
+    // owned panels of this (shard) matrix
+    const auto& ps = m->panel_start_host;
+    const std::uint32_t p_lo = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_lo) - ps.begin());
+    const std::uint32_t p_hi = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_hi) - ps.begin());
+    const int prec = m->precision;
+    if (prec == 0)
+      nonfinite_fix_kernel<float><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
+                                                                          m->halo_lo, m->halo_hi);
+    else
+      nonfinite_fix_kernel<double><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
+                                                                           m->halo_lo, m->halo_hi);
+    CIEG_CUDA(cudaGetLastError());
+    ++ctx->launches;
   }
 }
 

@@ -150,3 +150,60 @@ def test_spmm_host_batch_matches_single_calls():
     for x, y in zip(xs, ys):
         assert np.array_equal(y, dm.spmm_host(x))
     assert dm.spmm_host_batch([]) == []
+
+
+@pytest.mark.parametrize("prec", [0, 1])
+@pytest.mark.parametrize("m", [1, 4, 16, 20])
+def test_spmm_nonfinite_inputs_match_reference(prec, m):
+    """Inf / NaN in X: the dense tile's explicit zeros must not turn into
+    NaN (0 * Inf); only stored entries multiply, as in spmm (csb.cpp:118-193).
+    Same non-finite pattern (NaN / +Inf / -Inf per element) as the oracle's
+    sequential restatement, finite elements to rounding."""
+    from oracle import ci_oracle as O
+
+    h = gen_from((3072, 3, 256, 0.2, 0.4, 13, prec, 2000)) if prec == 0 else gen_from((2000, 4, 64, 0.1, 0.5, 11, 1, 500))
+    x = ci.random_block(h.dim, m, 3)
+    x[100, 0] = np.inf
+    x[777, m - 1] = -np.inf
+    x[1500, m // 2] = np.nan
+    y = ci.spmm(h, x)
+    yo = O.spmm(h, x)
+    for mask in (np.isnan, np.isposinf, np.isneginf):
+        assert np.array_equal(mask(y), mask(yo))
+    fin = np.isfinite(yo)
+    np.testing.assert_allclose(y[fin], yo[fin], rtol=1e-12, atol=1e-12)
+    # finite inputs afterwards: the flag is per launch
+    x2 = ci.random_block(h.dim, m, 4)
+    np.testing.assert_allclose(ci.spmm(h, x2), O.spmm(h, x2), rtol=1e-12, atol=1e-12)
+
+
+def test_spmm_nonfinite_on_a_shard():
+    from oracle import ci_oracle as O
+
+    h = gen_from((3072, 3, 256, 0.2, 0.4, 13, 0, 2000))
+    x = ci.random_block(h.dim, 8, 5)
+    x[1030, 2] = np.inf  # a halo row of the second shard's neighbour
+    x[2100, 5] = np.nan
+    yo = O.spmm(h, x)
+    from paper_1609_01689_b200 import dist as D
+
+    rb, hl, hh = D.row_partition(h, 2)
+    for r in range(2):
+        dm = ci.DeviceMatrix.__new__(ci.DeviceMatrix)
+        import ctypes as C
+
+        from paper_1609_01689_b200 import _lib
+
+        lib = _lib.load()
+        v = h.view()
+        g = np.ascontiguousarray(h.groups, dtype=np.uint32)
+        handle = C.c_void_p()
+        ci._check(lib.cieg_matrix_upload_shard(ci.Device.default().handle, C.byref(v), ci._ptr(g, C.c_uint32),
+                                               len(g) - 1, 0, int(rb[r]), int(rb[r + 1]), C.byref(handle)))
+        dm = ci.DeviceMatrix(None, ci.Device.default(), _handle=handle)
+        y = dm.spmm_host(x)
+        ref = yo[rb[r]:rb[r + 1]]
+        for mask in (np.isnan, np.isposinf, np.isneginf):
+            assert np.array_equal(mask(y), mask(ref))
+        fin = np.isfinite(ref)
+        np.testing.assert_allclose(y[fin], ref[fin], rtol=1e-12, atol=1e-12)
