@@ -165,11 +165,12 @@ typedef struct {
   void* user;
   /* in-place sum over ranks of `count` doubles in host memory (Gram partials) */
   int (*allreduce_sum)(void* user, double* host_buf, uint64_t count);
-  /* gather before each SpMM: every rank's local rows of a row-distributed
-   * block (device, local_rows x m) into the full-length block x_full
-   * (device, dim x m). The shard's kernel reads x_full only on its halo rows
-   * [halo_lo, halo_hi) (cieg_matrix_rows), so filling those suffices -- a
-   * point-to-point halo exchange instead of an all-gather (dist.py). */
+  /* gather before each SpMM: the rank's local rows of a row-distributed
+   * block (device, local_rows x m) plus its neighbours' into x_full, a block
+   * addressed with GLOBAL row indices (x_full + row * m) of which only the
+   * shard's halo rows [halo_lo, halo_hi) (cieg_matrix_rows) are backed by
+   * memory -- the only rows the shard's kernel reads. dist.py fills them by
+   * a point-to-point halo exchange. */
   int (*allgather_rows)(void* user, const double* x_local_dev, uint32_t m, double* x_full_dev);
 } cieg_dist_hooks;
 
@@ -402,6 +403,8 @@ int cieg_matrix_export(const cieg_mat* mat, uint64_t* tile_off, uint32_t* tile_p
 /* ci::random_block (block_vectors.cpp:162-174): out n x k row-major,
  * entries 2*unit(hash3(seed, i, j)) - 1. */
 int cieg_random_block(uint32_t n, uint32_t k, uint64_t seed, double* out_host);
+/* Rows [row_lo, row_hi) of the same block (a shard's rows of X0). */
+int cieg_random_block_rows(uint32_t row_lo, uint32_t row_hi, uint32_t k, uint64_t seed, double* out_host);
 
 #ifdef __cplusplus
 }

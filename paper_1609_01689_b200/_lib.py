@@ -156,6 +156,7 @@ SIGNATURES = {
     "cieg_report_destroy": (_i, [_vp]),
     "cieg_lanczos_options_default": (None, [C.POINTER(LanczosOptionsC)]),
     "cieg_device_alloc": (_i, [_vp, C.c_uint64, C.POINTER(_vp)]),
+    "cieg_random_block_rows": (_i, [_u32, _u32, _u32, C.c_uint64, _pd]),
     "cieg_spmm_host_batch": (_i, [_vp, _vp, C.POINTER(_pd), C.POINTER(_pd), _u32, _u32]),
     "cieg_device_free": (_i, [_vp, _vp]),
     "cieg_memcpy": (_i, [_vp, _vp, _vp, C.c_uint64, C.c_int]),

@@ -263,6 +263,13 @@ def random_block(dim: int, width: int, seed: int) -> np.ndarray:
     return out
 
 
+def random_block_rows(row_lo: int, row_hi: int, width: int, seed: int) -> np.ndarray:
+    """Rows [row_lo, row_hi) of random_block(dim, width, seed) (a shard's X0)."""
+    out = np.empty((row_hi - row_lo, width), dtype=np.float64)
+    _check(_lib.load().cieg_random_block_rows(row_lo, row_hi, width, seed, _ptr(out)))
+    return out
+
+
 # CSB1 binary format (csb.cpp:256-331)
 
 def save_csb(h: CsbMatrix, path: str) -> None:

@@ -226,13 +226,14 @@ void generate(const cieg_gen_params& p, HostCsb& out) {
   out.group_bounds.assign(g.start.begin(), g.start.end());
 }
 
-void random_block(std::uint32_t n, std::uint32_t k, std::uint64_t seed, double* out) {
-  // ci::random_block (proj/src/block_vectors.cpp:162-174): symmetric_double(seed, i, j).
+void random_block(std::uint32_t n, std::uint32_t k, std::uint64_t seed, double* out, std::uint32_t row0) {
+  // ci::random_block (proj/src/block_vectors.cpp:162-174): symmetric_double(seed, i, j),
+  // rows [row0, row0 + n) of the global block (a shard's rows).
 #pragma omp parallel for schedule(static)
   for (std::int64_t i = 0; i < static_cast<std::int64_t>(n); ++i)
     for (std::uint32_t j = 0; j < k; ++j)
       out[static_cast<std::size_t>(i) * k + j] =
-          2.0 * cieg_gen::unit_double(cieg_gen::hash3(seed, static_cast<std::uint64_t>(i), j)) - 1.0;
+          2.0 * cieg_gen::unit_double(cieg_gen::hash3(seed, static_cast<std::uint64_t>(row0 + i), j)) - 1.0;
 }
 
 }  // namespace cieg
@@ -294,7 +295,15 @@ int cieg_host_csb_groups(const cieg_host_csb* hc, const uint32_t** bounds, uint3
 int cieg_random_block(uint32_t n, uint32_t k, uint64_t seed, double* out_host) {
   return cieg::guarded([&] {
     if (!out_host && n && k) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_random_block: null output");
-    cieg::random_block(n, k, seed, out_host);
+    cieg::random_block(n, k, seed, out_host, 0);
+  });
+}
+
+int cieg_random_block_rows(uint32_t row_lo, uint32_t row_hi, uint32_t k, uint64_t seed, double* out_host) {
+  return cieg::guarded([&] {
+    if (row_hi < row_lo) cieg::fail(CIEG_ERR_DIMENSION, "cieg_random_block_rows: row_hi < row_lo");
+    if (!out_host && row_hi > row_lo && k) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_random_block_rows: null output");
+    cieg::random_block(row_hi - row_lo, k, seed, out_host, row_lo);
   });
 }
 

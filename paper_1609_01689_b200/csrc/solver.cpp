@@ -186,8 +186,12 @@ class Solver {
     ++rep_.counters[0];
     rep_.counters[1] += x.w;
     const double* xin = x.p;
-    if (hooks_) {  // sharded: gather every rank's rows of X (the owner kernel reads its halo)
-      double* full = static_cast<double*>(xfull_.get(sizeof(double) * mat_->dim * std::max<std::uint32_t>(x.w, 1)));
+    if (hooks_) {
+      // sharded: the owner kernel reads X only on the shard's halo rows, so
+      // only those are allocated; `full` is addressed with global row indices
+      const std::size_t rows = mat_->halo_hi - mat_->halo_lo, w = std::max<std::uint32_t>(x.w, 1);
+      double* buf = static_cast<double*>(xfull_.get(sizeof(double) * std::max<std::size_t>(1, rows) * w));
+      double* full = buf - static_cast<std::ptrdiff_t>(mat_->halo_lo) * x.w;
       if (hooks_->allgather_rows(hooks_->user, x.p, x.w, full) != 0)
         fail(CIEG_ERR_ARGUMENT, "allgather_rows hook failed");
       xin = full;

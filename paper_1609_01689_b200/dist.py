@@ -101,9 +101,19 @@ def gather_halos(halo_lo: int, halo_hi: int, device, group=None):
     return hs[:, 0], hs[:, 1]
 
 
-def halo_exchange(x_local: torch.Tensor, plan: ExchangePlan, out: torch.Tensor, group=None) -> torch.Tensor:
-    """out[a:b] = X[a:b] for every row this rank's SpMM reads: own rows copied,
-    peers' rows received point to point (one batched isend/irecv round)."""
+def halo_exchange(x_local: torch.Tensor, plan: ExchangePlan, out: torch.Tensor, group=None,
+                  out_row0: int = 0) -> torch.Tensor:
+    """X[a:b] into out for every row this rank's SpMM reads: own rows copied,
+    peers' rows received point to point (one batched isend/irecv round).
+    out[i] holds global row out_row0 + i (a halo-sized buffer: out_row0 =
+    halo_lo; a full-length one: 0)."""
+    if out_row0:
+        lo = plan.lo - out_row0
+        sub = ExchangePlan.__new__(ExchangePlan)
+        sub.rank, sub.lo, sub.hi = plan.rank, lo, lo + (plan.hi - plan.lo)
+        sub.sends = [(p, a - out_row0, b - out_row0) for p, a, b in plan.sends]
+        sub.recvs = [(p, a - out_row0, b - out_row0) for p, a, b in plan.recvs]
+        plan = sub
     out[plan.lo:plan.hi].copy_(x_local)
     if out.is_cuda and dist.get_backend(group) == "gloo":
         # gloo moves host tensors only (single-GPU multi-rank runs): stage
@@ -177,6 +187,14 @@ class ShardedMatrix:
     def local_rows(self) -> int:
         return self.row_hi - self.row_lo
 
+    @property
+    def dim(self) -> int:
+        return self.h.dim
+
+    @property
+    def halo(self):
+        return int(self.halo_lo[self.rank]), int(self.halo_hi[self.rank])
+
     def spmm(self, x_local: torch.Tensor, group=None, exchange: str = "halo") -> torch.Tensor:
         """Rows [row_lo, row_hi) of H X from the rank's rows of X (the halo
         rows of X arrive point to point; exchange="allgather" for the
@@ -195,6 +213,62 @@ class ShardedMatrix:
         return y
 
 
+class DeviceShard:
+    """This rank's shard generated on its GPU (cieg_generate_device with a
+    row range): no host CSB anywhere -- the config-5 path (2e10 entries).
+    Collective: every rank must construct its shard (halos are exchanged)."""
+
+    def __init__(self, dm: ci.DeviceMatrix, row_bounds, group=None):
+        self.dm = dm
+        self.device = dm.device
+        self.handle = dm.handle
+        self.dim = dm.dim
+        self.rank = dist.get_rank(group)
+        self.row_bounds = np.asarray(row_bounds, dtype=np.int64)
+        self.row_lo, self.row_hi = dm.row_lo, dm.row_hi
+        assert self.row_lo == self.row_bounds[self.rank] and self.row_hi == self.row_bounds[self.rank + 1]
+        tdev = torch.device("cuda", dm.device.index)
+        self.halo_lo_all, self.halo_hi_all = gather_halos(dm.halo_lo, dm.halo_hi, tdev, group)
+        self.plan = ExchangePlan(self.row_bounds, self.halo_lo_all, self.halo_hi_all, self.rank)
+
+    @classmethod
+    def generate(cls, cfg, row_bounds, device: ci.Device, group=None, seed: Optional[int] = None) -> "DeviceShard":
+        rank = dist.get_rank(group)
+        dm = cfg.generate_device(device=device, rows=(int(row_bounds[rank]), int(row_bounds[rank + 1])), seed=seed)
+        return cls(dm, row_bounds, group)
+
+    @property
+    def local_rows(self) -> int:
+        return self.row_hi - self.row_lo
+
+    @property
+    def halo(self):
+        return int(self.dm.halo_lo), int(self.dm.halo_hi)
+
+
+def generated_row_bounds(cfg, world: int):
+    """Group-aligned row cuts for GPU-generated shards, balanced by the
+    generator's expected streamed entries per row (edge sectors couple to
+    fewer neighbours than interior ones)."""
+    gb = []
+    for s in range(cfg.sectors):
+        a, b = cfg.n * s // cfg.sectors, cfg.n * (s + 1) // cfg.sectors
+        gb.extend(range(a, b, cfg.tile))
+    gb.append(cfg.n)
+    gb = np.asarray(gb, dtype=np.int64)
+    # expected row weight: sectors within the +-2 band around the row's sector
+    sec = np.minimum((gb[:-1] * cfg.sectors) // cfg.n, cfg.sectors - 1)
+    neigh = np.array([min(s + 2, cfg.sectors - 1) - max(s - 2, 0) + 1 for s in sec], dtype=np.float64)
+    w = neigh * np.diff(gb)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    bounds = [0]
+    for k in range(1, world):
+        i = int(np.argmin(np.abs(cum - cum[-1] * k / world)))
+        bounds.append(max(int(gb[i]), bounds[-1] + 1))
+    bounds.append(cfg.n)
+    return np.asarray(bounds, dtype=np.int64)
+
+
 def local_tile_diagonal(h: ci.CsbMatrix, row_lo: int, row_hi: int, device: ci.Device) -> ci.TileDiagonal:
     g = np.ascontiguousarray(h.groups, dtype=np.uint32)
     v = h.view()
@@ -205,10 +279,12 @@ def local_tile_diagonal(h: ci.CsbMatrix, row_lo: int, row_hi: int, device: ci.De
     return ci.TileDiagonal(handle, lb.astype(np.uint32), device)
 
 
-def lobpcg_solve_dist(sm: ShardedMatrix, x0_local: np.ndarray, options: ci.LobpcgOptions,
+def lobpcg_solve_dist(sm, x0_local: np.ndarray, options: ci.LobpcgOptions,
                       precond: Optional[ci.TileDiagonal] = None, group=None) -> ci.SolveReport:
-    """Sharded ci::lobpcg_solve. x0_local = the rank's rows of X0. The report's
-    trial vectors are the rank's rows; eigenvalues/history are global."""
+    """Sharded ci::lobpcg_solve on a ShardedMatrix (host CSB uploaded by
+    rows) or a DeviceShard (generated on the GPU). x0_local = the rank's rows
+    of X0. The report's trial vectors are the rank's rows; eigenvalues,
+    history and counters are global (identical on every rank)."""
     lib = _lib.load()
     dev = sm.device
     tdev = torch.device("cuda", dev.index)
@@ -218,8 +294,7 @@ def lobpcg_solve_dist(sm: ShardedMatrix, x0_local: np.ndarray, options: ci.Lobpc
     prev_stream = torch.cuda.current_stream(tdev)
     torch.cuda.set_stream(torch_stream)
     ci._check(lib.cieg_ctx_set_stream(dev.handle, C.c_void_p(torch_stream.cuda_stream)))
-    rb = sm.row_bounds
-    dim = sm.h.dim
+    hlo, hhi = sm.halo
 
     def _allreduce(_user, buf, count):
         try:
@@ -232,12 +307,13 @@ def lobpcg_solve_dist(sm: ShardedMatrix, x0_local: np.ndarray, options: ci.Lobpc
             return 1
 
     def _allgather(_user, xptr, m, fullptr):
-        # the hook need only fill the rank's halo rows: point-to-point exchange
+        # fullptr is globally indexed and backed on the halo rows only:
+        # view exactly those and exchange point to point
         try:
             nloc = sm.local_rows
             xl = _view(xptr, (nloc, m), tdev)
-            full = _view(fullptr, (dim, m), tdev)
-            halo_exchange(xl, sm.plan, full, group)
+            halo_buf = _view(fullptr + 8 * hlo * m, (hhi - hlo, m), tdev)
+            halo_exchange(xl, sm.plan, halo_buf, group, out_row0=hlo)
             return 0
         except Exception:  # noqa: BLE001
             return 1

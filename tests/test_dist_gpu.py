@@ -100,3 +100,69 @@ def test_sharded_solver_matches_reference(golden, world, backend, name):
         rows += res["rows"]
     assert rows == int(g[f"{name}_params"][0])
     assert all(out[r]["eigenvalues"] == out[0]["eigenvalues"] for r in range(world))
+
+
+def _gen_worker(rank, world, port, out_q):
+    """GPU-generated shards (no host CSB), halo exchange, sharded solve."""
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01689_b200 import ci, configs
+    from paper_1609_01689_b200 import dist as D
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        cfg = configs.CFG1
+        dev = ci.Device(0)
+        rb = D.generated_row_bounds(cfg, world)
+        sh = D.DeviceShard.generate(cfg, rb, dev)
+        td = ci.tile_diagonal_from_matrix(sh.dm)
+        x0 = ci.random_block_rows(sh.row_lo, sh.row_hi, cfg.kt, 42)
+        rep = D.lobpcg_solve_dist(sh, x0, ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol), td)
+        res["iterations"] = rep.iterations
+        res["eigenvalues"] = rep.eigenvalues.tolist()
+        res["rows"] = rep.trial_vectors.shape[0]
+        res["halo"] = sh.halo
+        res["bounds"] = rb.tolist()
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        res["error"] = repr(e) + traceback.format_exc()
+    finally:
+        dist.destroy_process_group()
+    out_q.put((rank, res))
+
+
+@pytest.mark.timeout(400)
+def test_generated_shards_solver_matches_single_gpu():
+    """The config-5 path at config-1 size: every rank generates its rows on
+    the GPU, builds its local preconditioner from them, and the sharded solve
+    reproduces the single-GPU solve from the same start."""
+    import multiprocessing as mp
+
+    from paper_1609_01689_b200 import ci, configs
+
+    cfg = configs.CFG1
+    single = ci.lobpcg_solve(cfg.generate_device(), ci.random_block(cfg.n, cfg.kt, 42),
+                             ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol,
+                                              preconditioner=ci.tile_diagonal_from_matrix(cfg.generate_device())))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gen_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert "error" not in out[r], out[r].get("error")
+        assert out[r]["iterations"] == single.iterations
+        np.testing.assert_allclose(out[r]["eigenvalues"], single.eigenvalues, rtol=1e-10)
+    assert out[0]["rows"] + out[1]["rows"] == cfg.n
+    assert out[0]["eigenvalues"] == out[1]["eigenvalues"]
