@@ -370,6 +370,120 @@ def cfg4_record(dev):
     return out
 
 
+def cfg5_record(dev, rank, world):
+    """BASELINE config 5 (n = 4e7, S = 2e10, k_want 8, block 16, tol 1e-6)
+    sharded over the ranks: every rank generates its row block on its GPU
+    (DeviceShard) and its local tile-diagonal preconditioner; X halos move
+    point to point before each SpMM, Grams are all-reduced. Collective: all
+    ranks call it. Times are max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01689_b200 import ci, configs
+    from paper_1609_01689_b200 import dist as D
+
+    cfg = configs.CFG5
+    scale = float(os.environ.get("CIEG_CFG5_SCALE", "1"))  # < 1 only to exercise the path on one GPU
+    if scale != 1.0:
+        import dataclasses
+
+        n = int(cfg.n * scale) // cfg.sectors * cfg.sectors
+        cfg = dataclasses.replace(cfg, name=f"{cfg.name} (scaled x{scale}, functional check)", n=n,
+                                  target_nnz=cfg.target_nnz * scale)
+    tdev = torch.device("cuda", dev.index)
+    out = {"workload": cfg.name, "n": cfg.n, "gpus": world, "k_want": cfg.k_want, "block": cfg.kt, "tol": cfg.tol}
+    try:
+        # per-rank footprint: tile stream (8 B/entry, boundary tiles duplicated),
+        # dense fp64 256 x 256 diagonal blocks, ~15 local n x 16 blocks
+        local = cfg.n / world
+        est = cfg.expected_nnz() / world * 8 * 1.06 + local * 256 * 8 + 15 * local * cfg.kt * 8
+        free, _ = torch.cuda.mem_get_info(tdev)
+        ok = torch.tensor([1 if est < 0.92 * free else 0], device=tdev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if not int(ok.item()):
+            out["skipped"] = f"needs ~{est / 1e9:.0f} GB per GPU, {free / 1e9:.0f} GB free"
+            return out
+        dist.barrier()
+        t0 = time.time()
+        rb = D.generated_row_bounds(cfg, world)
+        sh = D.DeviceShard.generate(cfg, rb, dev)
+        td = ci.tile_diagonal_from_matrix(sh.dm)
+        dev.synchronize()
+        dist.barrier()
+        gen_s = time.time() - t0
+        x0 = ci.random_block_rows(sh.row_lo, sh.row_hi, cfg.kt, 42)
+        dist.barrier()
+        t0 = time.perf_counter()
+        rep = D.lobpcg_solve_dist(sh, x0, ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol), td)
+        dist.barrier()
+        tts = time.perf_counter() - t0
+        del td
+        # standalone sharded SpMMs at m = 16: K1 alone vs K1 + halo exchange
+        m = 16
+        xl = torch.from_numpy(ci.random_block_rows(sh.row_lo, sh.row_hi, m, 7)).to(tdev)
+        hl, hh = sh.halo
+        buf = torch.empty((hh - hl, m), dtype=torch.float64, device=tdev)
+        y = torch.empty((sh.local_rows, m), dtype=torch.float64, device=tdev)
+        stream = torch.cuda.Stream(device=tdev)
+        torch.cuda.set_stream(stream)
+        from paper_1609_01689_b200 import _lib as L
+
+        lib = L.load()
+        ci._check(lib.cieg_ctx_set_stream(dev.handle, ctypes.c_void_p(stream.cuda_stream)))
+        xfull_ptr = buf.data_ptr() - 8 * hl * m
+
+        def k1():
+            sh.dm.spmm_ptr(xfull_ptr, y.data_ptr(), m)
+
+        def step():
+            D.halo_exchange(xl, sh.plan, buf, out_row0=hl)
+            k1()
+
+        def timed(fn, k=5):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(k):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / k], device=tdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        ms_step, ms_k1 = timed(step), timed(k1)
+        ci._check(lib.cieg_ctx_set_stream(dev.handle, None))
+        torch.cuda.set_stream(torch.cuda.default_stream(tdev))
+        nnz_t = torch.tensor([float(sh.dm.nnz)], device=tdev, dtype=torch.float64)
+        dist.all_reduce(nnz_t)
+        nnz_max = torch.tensor([float(sh.dm.nnz)], device=tdev, dtype=torch.float64)
+        dist.all_reduce(nnz_max, op=dist.ReduceOp.MAX)
+        split = torch.tensor([rep.timing_ms[k] for k in ("spmm", "rayleigh_ritz", "orthonormalization",
+                                                          "preconditioner", "residual", "other", "total")],
+                             device=tdev, dtype=torch.float64)
+        dist.all_reduce(split, op=dist.ReduceOp.MAX)
+        per_gpu_bytes = configs.spmm_bytes(int(nnz_max.item()), sh.local_rows, m, 0)
+        peak, _ = load_peaks()
+        per_gpu_gbs = per_gpu_bytes / (ms_k1 * 1e-3) / 1e9
+        out.update({"tts_s": round(tts, 3), "iterations": rep.iterations, "converged": rep.converged,
+                    "gen_on_gpu_s": round(gen_s, 2), "nnz_stored_total": int(nnz_t.item()),
+                    "split_ms_max_over_ranks": dict(zip(("spmm", "rayleigh_ritz", "orthonormalization",
+                                                         "preconditioner", "residual", "other", "total"),
+                                                        [round(v, 1) for v in split.tolist()])),
+                    "counters": vars(rep.counters), "eigenvalues": rep.eigenvalues.tolist(),
+                    "spmm_m16": {"ms_k1": round(ms_k1, 3), "ms_with_halo_exchange": round(ms_step, 3),
+                                 "comm_fraction": round(1 - ms_k1 / ms_step, 3),
+                                 "per_gpu_gbs": round(per_gpu_gbs, 1),
+                                 "per_gpu_hbm_frac": round(per_gpu_gbs / peak, 4),
+                                 "halo_rows": hh - hl, "rows_per_gpu": sh.local_rows}})
+    except Exception as e:  # reported in the line; the headline stands
+        out["error"] = repr(e)[:400]
+    return out
+
+
 def group_bounds(cfg):
     """Generator tile (= group) starts, the rule of generator.cpp make_grid."""
     out = []
@@ -550,7 +664,13 @@ def ours(args):
                                "call": "cieg_spmm_host per step"}}
     else:
         e2e = {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-               "note": "sharded run: inputs device-resident, the step includes the NCCL all-gather of X"}
+               "note": "sharded run: inputs device-resident, the step includes the X halo exchange"}
+    tile_edge, ntiles = dm.tile_edge, dm.ntiles
+    del dm  # the records below build their own matrices
+    torch.cuda.empty_cache()
+    cfg5 = None
+    if world > 1 and not args.no_cfg5:
+        cfg5 = cfg5_record(dev, rank, world)  # collective: every rank
     peak, peak_kind = load_peaks()
     if rank != 0:
         if world > 1:
@@ -565,7 +685,7 @@ def ours(args):
         "vs_baseline": None, "dtype": "f64 (fp32 H promoted exactly)",
         "data": "synthetic (seeded sector generator, BASELINE config 2)",
         "config": {"workload": cfg.name, "n": n, "nnz_stored": int(nnz_total), "m": m, "tile": cfg.tile,
-                   "p": round(cfg.p(), 8), "q": cfg.q, "device_tile_edge": dm.tile_edge, "device_tiles": dm.ntiles,
+                   "p": round(cfg.p(), 8), "q": cfg.q, "device_tile_edge": tile_edge, "device_tiles": ntiles,
                    "l2": "inputs larger than L2 (H 6.4 GB, X/U 256 MB each); no flush",
                    "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} (X halo exchange)",
                    "exchange": exchange,
@@ -582,8 +702,9 @@ def ours(args):
         line["lanczos"] = lanczos_record()
         line["sweep"] = sweep_record(dev)
         if not args.no_cfg4:
-            del dm
             line["lobpcg_cfg4"] = cfg4_record(dev)
+    if cfg5 is not None:
+        line["lobpcg_cfg5"] = cfg5
     print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
@@ -602,6 +723,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-lobpcg", action="store_true")
     ap.add_argument("--no-cfg4", action="store_true")
+    ap.add_argument("--no-cfg5", action="store_true", help="skip the sharded config-5 LOBPCG record (N > 1)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
