@@ -396,8 +396,12 @@ def cfg5_record(dev, rank, world):
         # per-rank footprint: tile stream (8 B/entry, boundary tiles duplicated),
         # dense fp64 256 x 256 diagonal blocks, ~15 local n x 16 blocks
         local = cfg.n / world
-        est = cfg.expected_nnz() / world * 8 * 1.06 + local * 256 * 8 + 15 * local * cfg.kt * 8
         free, _ = torch.cuda.mem_get_info(tdev)
+        tiles = cfg.expected_nnz() / world * 8 * 1.06
+        blocks = local * 256 * 8
+        if blocks > (free - tiles) / 4:  # the library then stores the diagonal blocks in fp32 (exact)
+            blocks /= 2
+        est = tiles + blocks + 15 * local * cfg.kt * 8
         ok = torch.tensor([1 if est < 0.92 * free else 0], device=tdev)
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
         if not int(ok.item()):

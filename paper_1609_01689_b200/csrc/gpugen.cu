@@ -8,6 +8,8 @@
 // diagonal tiles (ci::extract_tile_diagonal, hamiltonian.cpp:178-203).
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
+#include <string>
 #include <numeric>
 
 #include "context.hpp"
@@ -277,8 +279,11 @@ struct DiagTile {
 
 // Scatter the tile's entries into its group's dense block, mirrored
 // (ci::extract_tile_diagonal, hamiltonian.cpp:178-203).
-template <typename V>
-__global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx, const V* val, std::uint32_t te, std::uint32_t row_lo, double* blocks) {
+// Blocks are stored in the tile stream's own value type: fp32 values of an
+// fp32 H widen to fp64 exactly when the preconditioner reads them.
+template <typename V, typename B = V>
+__global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx, const V* val, std::uint32_t te,
+                                   std::uint32_t row_lo, B* blocks) {
   const DiagTile t = dt[blockIdx.x];
   for (std::uint64_t e = t.e0 + threadIdx.x; e < t.e1; e += blockDim.x) {
     const std::uint32_t off = idx[e] & 0xffffu;
@@ -288,7 +293,7 @@ __global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx,
     if (pc >= te) continue;  // sentinel
     const std::uint32_t c = cieg_tl::unperm(pc, prec);
     const std::uint32_t ia = t.a0 + r - row_lo - t.gs, ib = t.b0 + c - row_lo - t.gs;
-    const double v = static_cast<double>(val[e]);
+    const B v = static_cast<B>(val[e]);
     blocks[t.block_off + ia + static_cast<std::uint64_t>(ib) * t.gn] = v;
     blocks[t.block_off + ib + static_cast<std::uint64_t>(ia) * t.gn] = v;
   }
@@ -339,12 +344,31 @@ cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
     for (std::uint32_t g = 0; g < lng; ++g) pr->max_group = std::max(pr->max_group, lb[g + 1] - lb[g]);
     pr->bounds = dev_upload(lb);
     pr->block_off = dev_upload(off);
-    CIEG_CUDA(cudaMalloc(&pr->blocks, sizeof(double) * std::max<std::uint64_t>(1, off[lng])));
-    CIEG_CUDA(cudaMemsetAsync(pr->blocks, 0, sizeof(double) * off[lng], ctx->stream));
+    // storage: fp64 (fastest FOM reads) unless the blocks would take more
+    // than a quarter of the free HBM, then fp32 for an fp32 H (exact: the
+    // values are fp32); the preconditioner's results are identical either way
+    bool f32 = false;
+    if (m->precision == 0) {
+      std::size_t free_b = 0, total_b = 0;
+      CIEG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      f32 = sizeof(double) * off[lng] > free_b / 4;
+      if (const char* e = std::getenv("CIEG_PREC_STORAGE")) f32 = std::string(e) == "fp32";
+    }
+    const std::size_t vb = f32 ? sizeof(float) : sizeof(double);
+    void* blocks = nullptr;
+    CIEG_CUDA(cudaMalloc(&blocks, vb * std::max<std::uint64_t>(1, off[lng])));
+    if (f32)
+      pr->blocks32 = static_cast<float*>(blocks);
+    else
+      pr->blocks = static_cast<double*>(blocks);
+    CIEG_CUDA(cudaMemsetAsync(blocks, 0, vb * off[lng], ctx->stream));
     if (!dts.empty()) {
       DiagTile* d = dev_upload(dts);
-      if (m->precision == 0)
+      if (f32)
         diag_blocks_kernel<float><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
+            d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->blocks32);
+      else if (m->precision == 0)
+        diag_blocks_kernel<float, double><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
             d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->blocks);
       else
         diag_blocks_kernel<double><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(

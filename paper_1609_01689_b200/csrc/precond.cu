@@ -14,6 +14,7 @@
 // reference's sequential order, so for identical inputs the result is
 // bitwise identical to the reference compiled on the host.
 #include <cstdio>
+#include <type_traits>
 #include <cstring>
 #include <map>
 
@@ -29,6 +30,7 @@ cieg_prec::~cieg_prec() {
   cudaFree(bounds);
   cudaFree(block_off);
   cudaFree(blocks);
+  cudaFree(blocks32);
 }
 
 namespace cieg {
@@ -67,6 +69,24 @@ ShiftPlan choose_shifts(const std::vector<double>& theta, const std::vector<doub
 
 namespace {
 
+// Dense tile-diagonal blocks, fp64 or (for an fp32 H, whose values are
+// exactly fp32) fp32 storage; read as fp64 either way (exact widening).
+struct BlockRef {
+  const double* d;
+  const float* f;
+  __device__ __forceinline__ BlockRef at(std::uint64_t off) const {
+    return BlockRef{d ? d + off : nullptr, f ? f + off : nullptr};
+  }
+};
+// the kernels are instantiated per storage type (no per-element branch)
+template <bool F32>
+__device__ __forceinline__ double ldb(const BlockRef& b, std::size_t i) {
+  if constexpr (F32)
+    return static_cast<double>(__ldg(b.f + i));
+  else
+    return __ldg(b.d + i);
+}
+
 constexpr int kMaxDirect = 64;
 constexpr int kLuThreads = 128;
 constexpr int kMaxCols = 64;
@@ -74,7 +94,7 @@ constexpr int kMaxCols = 64;
 struct LuParams {
   const std::uint32_t* bounds;
   const std::uint64_t* block_off;
-  const double* blocks;
+  BlockRef blocks;
   const std::uint32_t* groups;  // small group ids
   const double* r;
   double* w;
@@ -86,12 +106,13 @@ struct LuParams {
   int* singular_count;
 };
 
-__device__ bool lu_factor(double* A, int n, int ld, int* perm, double mu, const double* src,
+template <bool F32>
+__device__ bool lu_factor(double* A, int n, int ld, int* perm, double mu, const BlockRef src,
                           double* red_v, int* red_i) {
   const int tid = threadIdx.x;
   for (int e = tid; e < n * n; e += blockDim.x) {
     const int i = e % n, j = e / n;
-    double v = src[e];
+    double v = ldb<F32>(src, e);
     if (i == j) v = DSUB(v, mu);
     A[i + j * ld] = v;
   }
@@ -152,6 +173,7 @@ __device__ bool lu_factor(double* A, int n, int ld, int* perm, double mu, const 
   return red_i[1] == 0;
 }
 
+template <bool F32>
 __global__ void __launch_bounds__(kLuThreads) lu_direct_kernel(const __grid_constant__ LuParams p) {
   __shared__ double A[kMaxDirect * (kMaxDirect + 1)];
   extern __shared__ double tmp_dyn[];  // [columns of this shift][kMaxDirect]
@@ -163,12 +185,12 @@ __global__ void __launch_bounds__(kLuThreads) lu_direct_kernel(const __grid_cons
   const std::uint32_t r0 = p.bounds[grp];
   const int n = static_cast<int>(p.bounds[grp + 1] - r0);
   const int ld = n + 1;
-  const double* src = p.blocks + p.block_off[grp];
+  const BlockRef src = p.blocks.at(p.block_off[grp]);
   double mu = p.shift[s];
-  bool ok = lu_factor(A, n, ld, perm, mu, src, red_v, red_i);
+  bool ok = lu_factor<F32>(A, n, ld, perm, mu, src, red_v, red_i);
   if (!ok) {
     mu = mu + 1e-8 * (1.0 + fabs(mu));
-    ok = lu_factor(A, n, ld, perm, mu, src, red_v, red_i);
+    ok = lu_factor<F32>(A, n, ld, perm, mu, src, red_v, red_i);
   }
   if (!ok) {  // pass-through: W keeps R for these columns
     if (threadIdx.x == 0) {
@@ -202,7 +224,7 @@ constexpr int kFomMaxSteps = 3;
 struct FomParams {
   const std::uint32_t* bounds;
   const std::uint64_t* block_off;
-  const double* blocks;
+  BlockRef blocks;
   const std::uint32_t* groups;  // large group ids
   const double* r;
   double* w;
@@ -262,6 +284,7 @@ __device__ void tiny_lu_solve(double* hm, int m, double* rhs) {
   for (int i = 0; i < m; ++i) rhs[i] = t[i];
 }
 
+template <bool F32>
 __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant__ FomParams p) {
   extern __shared__ double sm[];
   const std::uint32_t grp = p.groups[blockIdx.x];
@@ -280,7 +303,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant_
   int* active = reinterpret_cast<int*>(scal + CC);                      // CC
   int* steps = active + CC;                                             // CC
   int* done = steps + CC;                                               // CC: finished with m = done
-  const double* blk = p.blocks + p.block_off[grp];
+  const BlockRef blk = p.blocks.at(p.block_off[grp]);
   const int tid = threadIdx.x;
   auto B = [&](int m, int i, int c) -> double& { return basis[(static_cast<std::size_t>(m) * n + i) * CC + c]; };
 
@@ -318,12 +341,12 @@ __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant_
       double z[16];
 #pragma unroll
       for (int c = 0; c < 16; ++c) z[c] = 0.0;
-      const double* brow = blk + i;
+      const BlockRef brow = blk.at(i);
       int kk = 0;
       for (; kk + 16 <= n; kk += 16) {
         double a[16];
 #pragma unroll
-        for (int u = 0; u < 16; ++u) a[u] = __ldg(brow + static_cast<std::size_t>(kk + u) * n);
+        for (int u = 0; u < 16; ++u) a[u] = ldb<F32>(brow, static_cast<std::size_t>(kk + u) * n);
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const double* bv = &B(m, kk + u, 0);
@@ -333,7 +356,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant_
         }
       }
       for (; kk < n; ++kk) {
-        const double a = __ldg(brow + static_cast<std::size_t>(kk) * n);
+        const double a = ldb<F32>(brow, static_cast<std::size_t>(kk) * n);
         const double* bv = &B(m, kk, 0);
 #pragma unroll
         for (int c = 0; c < 16; ++c)
@@ -455,6 +478,7 @@ __device__ __forceinline__ double fom_col_reduce(double part, double* red, int c
   return out;
 }
 
+template <bool F32>
 __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_constant__ FomParams p) {
   extern __shared__ double sm[];
   const std::uint32_t grp = p.groups[blockIdx.x];
@@ -475,7 +499,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
   int* active = state;
   int* steps = state + 16;
   int* done = state + 32;
-  const double* blk = p.blocks + p.block_off[grp];
+  const BlockRef blk = p.blocks.at(p.block_off[grp]);
   const int tid = threadIdx.x;
   const int tc = tid & 15, trow = tid >> 4;
   auto B = [&](int m, int i, int c) -> double& { return basis[(static_cast<std::size_t>(m) * NP + i) * kFastSC + c]; };
@@ -515,8 +539,12 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    for (int k0 = 0; k0 < NP; k0 += 16) {
-      double af[4][4], bf[4][2];
+    // A fragments (raw storage type) are prefetched one 16-wide k chunk
+    // ahead and widened at use, so global latency overlaps the DMMAs
+    using Raw = typename std::conditional<F32, float, double>::type;
+    const Raw* blk_raw = F32 ? reinterpret_cast<const Raw*>(blk.f) : reinterpret_cast<const Raw*>(blk.d);
+    Raw a0[4][4], a1[4][4];
+    auto load_a = [&](int k0, Raw (&dst)[4][4]) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int kk = k0 + 4 * u + q;
@@ -524,17 +552,33 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
         for (int a = 0; a < 4; ++a) {
           const int mt = warp + 8 * a;
           const int i = 8 * mt + g;
-          af[u][a] = (mt < mtiles && i < n && kk < n) ? __ldg(blk + i + static_cast<std::size_t>(kk) * n) : 0.0;
+          dst[u][a] = (k0 < NP && mt < mtiles && i < n && kk < n) ? __ldg(blk_raw + i + static_cast<std::size_t>(kk) * n)
+                                                                  : Raw(0);
         }
-#pragma unroll
-        for (int b = 0; b < 2; ++b) bf[u][b] = (k0 + 4 * u < NP) ? B(m, k0 + 4 * u + q, 8 * b + g) : 0.0;
       }
+    };
+    auto mma_chunk = [&](int k0, const Raw (&src)[4][4]) {
+      if (k0 >= NP) return;
+      double bf[4][2];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 2; ++b) bf[u][b] = (k0 + 4 * u < NP) ? B(m, k0 + 4 * u + q, 8 * b + g) : 0.0;
 #pragma unroll
-          for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], af[u][a], bf[u][b]);
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const double av = static_cast<double>(src[u][a]);
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], av, bf[u][b]);
+        }
+    };
+    load_a(0, a0);
+    for (int k0 = 0; k0 < NP; k0 += 32) {
+      load_a(k0 + 16, a1);
+      mma_chunk(k0, a0);
+      load_a(k0 + 32, a0);
+      mma_chunk(k0 + 16, a1);
     }
     // w = z - mu v_m
 #pragma unroll
@@ -660,7 +704,7 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
     static thread_local LuParams lp;
     lp.bounds = prec->bounds;
     lp.block_off = prec->block_off;
-    lp.blocks = prec->blocks;
+    lp.blocks = BlockRef{prec->blocks, prec->blocks32};
     lp.groups = dgroups;
     lp.r = r;
     lp.w = w;
@@ -680,10 +724,10 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
     int maxcols = 0;
     for (int t = 0; t < lp.nshift; ++t) maxcols = std::max(maxcols, lp.col_start[t + 1] - lp.col_start[t]);
     const std::size_t smem = sizeof(double) * static_cast<std::size_t>(maxcols) * kMaxDirect;
-    CIEG_CUDA(cudaFuncSetAttribute(lu_direct_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
     dim3 grid(static_cast<unsigned>(small.size()), static_cast<unsigned>(lp.nshift));
-    lu_direct_kernel<<<grid, kLuThreads, smem, ctx->stream>>>(lp);
+    auto lu = prec->blocks32 ? lu_direct_kernel<true> : lu_direct_kernel<false>;
+    CIEG_CUDA(cudaFuncSetAttribute(lu, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    lu<<<grid, kLuThreads, smem, ctx->stream>>>(lp);
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
   }
@@ -691,7 +735,7 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
     static thread_local FomParams fp;
     fp.bounds = prec->bounds;
     fp.block_off = prec->block_off;
-    fp.blocks = prec->blocks;
+    fp.blocks = BlockRef{prec->blocks, prec->blocks32};
     fp.groups = dgroups + small.size();
     fp.r = r;
     fp.w = w;
@@ -712,10 +756,10 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
       const std::size_t np8 = (n + 7) & ~std::size_t{7};
       const std::size_t smem = sizeof(double) * ((mmax + 1) * np8 * kFastSC + np8 * kFastSC + 272 + 256 + 48) +
                                sizeof(int) * 48;
-      CIEG_CUDA(cudaFuncSetAttribute(fom_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(smem)));
+      auto fom = prec->blocks32 ? fom_fast_kernel<true> : fom_fast_kernel<false>;
+      CIEG_CUDA(cudaFuncSetAttribute(fom, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
-      fom_fast_kernel<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+      fom<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
     } else {
       // reference-order path: chunk so that shared memory stays below ~200 KB
       int chunk = 16;
@@ -726,9 +770,10 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
       if (smem_for(chunk) > 220 * 1024) fail(CIEG_ERR_CONFIG, "FOM tile too large for shared memory");
       fp.chunk = chunk;
       const std::size_t smem = smem_for(chunk);
-      CIEG_CUDA(cudaFuncSetAttribute(fom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      auto fom = prec->blocks32 ? fom_kernel<true> : fom_kernel<false>;
+      CIEG_CUDA(cudaFuncSetAttribute(fom, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
-      fom_kernel<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+      fom<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
     }
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;

@@ -14,7 +14,8 @@ struct cieg_prec {
   std::vector<std::uint64_t> block_off_host;  // offsets (doubles) of each dense block
   std::uint32_t* bounds = nullptr;            // device
   std::uint64_t* block_off = nullptr;         // device
-  double* blocks = nullptr;                   // device, column-major per group
+  double* blocks = nullptr;                   // device, column-major per group (fp64) ...
+  float* blocks32 = nullptr;                  // ... or fp32 (blocks of an fp32 H; exact)
   std::uint32_t max_group = 0;
   ~cieg_prec();
 };
