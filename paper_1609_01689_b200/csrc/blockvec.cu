@@ -201,16 +201,25 @@ struct CombineParams {
   std::uint32_t n, kin, kout;
   int accumulate;
   const double* g_dev;  // used when kin*kout > kCombineMaxG
+  View3 L;              // fused Gram L^T out (combine_gram; unused for SYM)
+  double* partials;     // fused Gram: per-CTA partials (8 LT x 8 OT)
   double g[kCombineMaxG];
 };
 
 constexpr int kCombineWarps = 8;
 
-template <int OT>
+// LT > 0 fuses a Gram of the freshly computed output into the pass:
+// L^T out (L a view over the same rows, LT = ceil(L.width / 8)) or, SYM,
+// out^T out (upper tiles; mirrored by gram_reduce_kernel). Each warp stages
+// its 8 output rows in shared memory to re-read them in fragment layout;
+// per-warp partials are folded in warp order, per-CTA partials reduced in a
+// fixed order (deterministic).
+template <int OT, int LT = 0, bool SYM = false>
 __global__ void __launch_bounds__(32 * kCombineWarps)
     combine_kernel(const __grid_constant__ CombineParams p) {
   constexpr int SG = 8 * OT + 4;
-  extern __shared__ double gs[];  // [padded kin rows][SG]
+  constexpr int SO = 8 * OT + 4;  // staged output row stride
+  extern __shared__ double gs[];  // [padded kin rows][SG] | LT: [warps][8][SO] | fold [8 LT][8 OT]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, q = lane & 3;
   const double* gsrc = p.g_dev ? p.g_dev : p.g;
@@ -232,6 +241,33 @@ __global__ void __launch_bounds__(32 * kCombineWarps)
     }
   }
   __syncthreads();
+  int gsrows = 0;
+  for (int s = 0; s < p.in.nseg; ++s) gsrows += (static_cast<int>(p.in.s[s].w) + 3) & ~3;
+  double* ostage = gs + (gsrows > 4 ? gsrows : 4) * SG + warp * 8 * SO;
+  constexpr int LTX = LT > 0 ? LT : 1;
+  double gacc[LTX][OT][2];
+  const double* pl[LTX];
+  std::uint32_t ll[LTX];
+  if constexpr (LT > 0) {
+#pragma unroll
+    for (int lt = 0; lt < LT; ++lt) {
+#pragma unroll
+      for (int nt = 0; nt < OT; ++nt) gacc[lt][nt][0] = gacc[lt][nt][1] = 0.0;
+      pl[lt] = nullptr;
+      ll[lt] = 0;
+      if (!SYM) {
+        std::uint32_t c = 8 * lt + g;
+        for (int s = 0; s < p.L.nseg; ++s) {
+          if (c < p.L.s[s].w) {
+            pl[lt] = p.L.s[s].p + c;
+            ll[lt] = p.L.s[s].ld;
+            break;
+          }
+          c -= p.L.s[s].w;
+        }
+      }
+    }
+  }
 
   const std::uint64_t ngroups = (p.n + 7) / 8;
   for (std::uint64_t grp = static_cast<std::uint64_t>(blockIdx.x) * kCombineWarps + warp; grp < ngroups;
@@ -289,19 +325,76 @@ __global__ void __launch_bounds__(32 * kCombineWarps)
             p.out.o1[crow * p.out.ld1 + (c - p.out.w0)] = acc[nt][h];
         }
     }
+    if constexpr (LT > 0) {
+      // stage the 8 output rows (zero beyond n / kout), then accumulate
+      // L^T out over them: two k-steps of 4 rows
+#pragma unroll
+      for (int nt = 0; nt < OT; ++nt)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const std::uint32_t c = 8 * nt + 2 * q + h;
+          ostage[g * SO + 8 * nt + 2 * q + h] = (crow < p.n && c < p.kout) ? acc[nt][h] : 0.0;
+        }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = 4 * u + q;
+        const std::uint64_t row = i0 + r;
+        double bfr[OT], afr[LTX];
+#pragma unroll
+        for (int nt = 0; nt < OT; ++nt) bfr[nt] = ostage[r * SO + 8 * nt + g];
+#pragma unroll
+        for (int lt = 0; lt < LT; ++lt)
+          afr[lt] = SYM ? ostage[r * SO + 8 * lt + g] : ((row < p.n && pl[lt]) ? __ldg(pl[lt] + row * ll[lt]) : 0.0);
+#pragma unroll
+        for (int lt = 0; lt < LT; ++lt)
+#pragma unroll
+          for (int nt = 0; nt < OT; ++nt) {
+            if (SYM && nt < lt) continue;
+            dmma_8x8x4(gacc[lt][nt][0], gacc[lt][nt][1], afr[lt], bfr[nt]);
+          }
+      }
+      __syncwarp();
+    }
+  }
+  if constexpr (LT > 0) {
+    constexpr int MA = 8 * LT, NB = 8 * OT;
+    double* red = gs + (gsrows > 4 ? gsrows : 4) * SG + kCombineWarps * 8 * SO;
+    for (int w = 0; w < kCombineWarps; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int lt = 0; lt < LT; ++lt)
+#pragma unroll
+          for (int nt = 0; nt < OT; ++nt) {
+            if (SYM && nt < lt) continue;
+            const int row = 8 * lt + g, col = 8 * nt + 2 * q;
+            if (w == 0) {
+              red[row * NB + col] = gacc[lt][nt][0];
+              red[row * NB + col + 1] = gacc[lt][nt][1];
+            } else {
+              red[row * NB + col] += gacc[lt][nt][0];
+              red[row * NB + col + 1] += gacc[lt][nt][1];
+            }
+          }
+      }
+      __syncthreads();
+    }
+    for (int e = threadIdx.x; e < MA * NB; e += 32 * kCombineWarps)
+      p.partials[static_cast<std::size_t>(blockIdx.x) * MA * NB + e] = red[e];
   }
 }
 
-template <int OT>
+template <int OT, int LT = 0, bool SYM = false>
 void launch_combine(cieg_ctx* ctx, const CombineParams& prm, int blocks) {
-  constexpr int SG = 8 * OT + 4;
+  constexpr int SG = 8 * OT + 4, SO = 8 * OT + 4;
   int rows = 0;
   for (int s = 0; s < prm.in.nseg; ++s) rows += (static_cast<int>(prm.in.s[s].w) + 3) & ~3;
-  const std::size_t smem = sizeof(double) * static_cast<std::size_t>(std::max(rows, 4)) * SG;
+  std::size_t smem = sizeof(double) * static_cast<std::size_t>(std::max(rows, 4)) * SG;
+  if (LT > 0) smem += sizeof(double) * (static_cast<std::size_t>(kCombineWarps) * 8 * SO + 64 * LT * OT);
+  auto kern = combine_kernel<OT, LT, SYM>;
   if (smem > 48 * 1024)
-    CIEG_CUDA(cudaFuncSetAttribute(combine_kernel<OT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(smem)));
-  combine_kernel<OT><<<blocks, 32 * kCombineWarps, smem, ctx->stream>>>(prm);
+    CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<blocks, 32 * kCombineWarps, smem, ctx->stream>>>(prm);
 }
 
 // ---------------------------------------------------------------- residual
@@ -377,6 +470,37 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
   return out;
 }
 
+namespace {
+
+// Shared parameter setup of combine / combine_gram (G as a kernel parameter
+// when it fits, else staged in device scratch).
+CombineParams& setup_combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_host,
+                             std::uint32_t kout, const Out2& out, bool accumulate) {
+  static thread_local CombineParams prm;  // ~30 KB: keep off the stack
+  const std::uint32_t kin = in.width;
+  prm.in = in;
+  prm.out = out;
+  prm.n = n;
+  prm.kin = kin;
+  prm.kout = kout;
+  prm.accumulate = accumulate ? 1 : 0;
+  prm.L = View3{};
+  prm.partials = nullptr;
+  const std::size_t ng = static_cast<std::size_t>(kin) * kout;
+  if (ng <= static_cast<std::size_t>(kCombineMaxG)) {
+    std::memcpy(prm.g, g_host, sizeof(double) * ng);
+    prm.g_dev = nullptr;
+  } else {
+    double* d = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * ng));
+    CIEG_CUDA(cudaMemcpyAsync(d, g_host, sizeof(double) * ng, cudaMemcpyHostToDevice, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    prm.g_dev = d;
+  }
+  return prm;
+}
+
+}  // namespace
+
 void combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_host, std::uint32_t kout,
              const Out2& out, bool accumulate) {
   if (n == 0 || kout == 0) return;
@@ -396,25 +520,7 @@ void combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_ho
     }
     return;
   }
-  static thread_local CombineParams prm;  // ~30 KB: keep off the stack
-  prm.in = in;
-  prm.out = out;
-  prm.n = n;
-  prm.kin = kin;
-  prm.kout = kout;
-  prm.accumulate = accumulate ? 1 : 0;
-  const std::size_t ng = static_cast<std::size_t>(kin) * kout;
-  DevBuf* gbuf = nullptr;
-  if (ng <= static_cast<std::size_t>(kCombineMaxG)) {
-    std::memcpy(prm.g, g_host, sizeof(double) * ng);
-    prm.g_dev = nullptr;
-  } else {
-    gbuf = &ctx->scratch_small;
-    double* d = static_cast<double*>(gbuf->get(sizeof(double) * ng));
-    CIEG_CUDA(cudaMemcpyAsync(d, g_host, sizeof(double) * ng, cudaMemcpyHostToDevice, ctx->stream));
-    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
-    prm.g_dev = d;
-  }
+  CombineParams& prm = setup_combine(ctx, n, in, g_host, kout, out, accumulate);
   const int OT = static_cast<int>((kout + 7) / 8);
   const int blocks = grid_for(ctx, (n + 7) / 8, kCombineWarps * 4);
   switch (OT) {
@@ -427,6 +533,71 @@ void combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_ho
   }
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
+}
+
+namespace {
+
+template <int OT, int... LTs>
+void launch_fused_lt(cieg_ctx* ctx, const CombineParams& prm, int blocks, int lt, std::integer_sequence<int, LTs...>) {
+  using L = void (*)(cieg_ctx*, const CombineParams&, int);
+  L table[] = {&launch_combine<OT, LTs + 1, false>...};
+  table[lt - 1](ctx, prm, blocks);
+}
+
+void launch_fused(cieg_ctx* ctx, const CombineParams& prm, int blocks, int ot, int lt, bool sym) {
+  using S = std::make_integer_sequence<int, 4>;
+  if (sym) {
+    switch (ot) {
+      case 1: launch_combine<1, 1, true>(ctx, prm, blocks); break;
+      case 2: launch_combine<2, 2, true>(ctx, prm, blocks); break;
+      case 3: launch_combine<3, 3, true>(ctx, prm, blocks); break;
+      default: launch_combine<4, 4, true>(ctx, prm, blocks); break;
+    }
+    return;
+  }
+  switch (ot) {
+    case 1: launch_fused_lt<1>(ctx, prm, blocks, lt, S{}); break;
+    case 2: launch_fused_lt<2>(ctx, prm, blocks, lt, S{}); break;
+    case 3: launch_fused_lt<3>(ctx, prm, blocks, lt, S{}); break;
+    default: launch_fused_lt<4>(ctx, prm, blocks, lt, S{}); break;
+  }
+}
+
+}  // namespace
+
+std::vector<double> combine_gram(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_host,
+                                 std::uint32_t kout, const Out2& out, bool accumulate, const View3* L) {
+  const std::uint32_t kx = L ? L->width : kout;
+  const int OT = static_cast<int>((kout + 7) / 8), LT = static_cast<int>((kx + 7) / 8);
+  const bool fusable = n > 0 && kout > 0 && in.width > 0 && kx > 0 && OT <= 4 && LT <= 4;
+  if (!fusable) {  // the two passes separately
+    combine(ctx, n, in, g_host, kout, out, accumulate);
+    const View3 ov = view({Seg{out.o0, out.ld0, out.w0}, Seg{out.o1, out.ld1, out.w1}});
+    return gram(ctx, n, L ? *L : ov, ov);
+  }
+  for (int k = 0; k < in.nseg; ++k)
+    if (in.s[k].w > 48) fail(CIEG_ERR_CONFIG, "combine: input segment wider than 48");
+  if (out.w0 + out.w1 != kout) fail(CIEG_ERR_DIMENSION, "combine: output split mismatch");
+  CombineParams& prm = setup_combine(ctx, n, in, g_host, kout, out, accumulate);
+  const int blocks = grid_for(ctx, (n + 7) / 8, kCombineWarps * 4);
+  const int MA = 8 * (L ? LT : OT), NB = 8 * OT;
+  prm.L = L ? *L : View3{};
+  prm.partials = static_cast<double*>(ctx->scratch_red.get(sizeof(double) * blocks * MA * NB + 64));
+  launch_fused(ctx, prm, blocks, OT, LT, L == nullptr);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  double* dout = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 48 * 48));
+  const int e = static_cast<int>(kx * kout);
+  gram_reduce_kernel<<<(e + 3) / 4, 128, 0, ctx->stream>>>(prm.partials, blocks, MA, NB, static_cast<int>(kx),
+                                                                static_cast<int>(kout), L ? 0 : 1, dout);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  std::vector<double> res(static_cast<std::size_t>(e));
+  double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
+  CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(res.data(), pin, sizeof(double) * e);
+  return res;
 }
 
 void residual(cieg_ctx* ctx, std::uint32_t n, std::uint32_t k, const double* hx, const double* x,

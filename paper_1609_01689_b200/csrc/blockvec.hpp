@@ -55,6 +55,14 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
 void combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_host,
              std::uint32_t kout, const Out2& out, bool accumulate);
 
+// combine followed by a Gram of its output in the same pass: returns
+// L^T out (L.width x kout) or, for L == nullptr, out^T out (kout x kout),
+// column major on the host. Same values as combine + gram up to the Gram's
+// summation order; falls back to the two separate passes outside the fused
+// instantiations (out and L up to 32 columns).
+std::vector<double> combine_gram(cieg_ctx* ctx, std::uint32_t n, const View3& in, const double* g_host,
+                                 std::uint32_t kout, const Out2& out, bool accumulate, const View3* L);
+
 // R = HX - X diag(theta) (n x k, contiguous).
 void residual(cieg_ctx* ctx, std::uint32_t n, std::uint32_t k, const double* hx, const double* x,
               const double* theta_host, double* r);

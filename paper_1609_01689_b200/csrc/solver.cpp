@@ -117,28 +117,47 @@ double dev_from_identity(const Mat& g, int m) {
 }
 
 
-// orthonormalize (lobpcg.cpp:89-119) over device blocks. `gram` is the Gram
-// product (all-reduced across ranks inside a sharded solve). `v` holds the
-// input (width v.w) and is overwritten; `tmp` is scratch of the same
-// capacity; the result (possibly width 0) is left in `v` (the two may swap).
-template <typename GramFn>
-void orthonormalize_dev(cieg_ctx* ctx, std::uint32_t n, GramFn&& gram, Block& v, Block& tmp, double drop_tol,
-                        const View3* against) {
+// Gram products of a (possibly row-sharded) solve: local partials, then the
+// all-reduce hook when sharded -- for plain Grams and for Grams fused into a
+// combine pass alike.
+struct GramOps {
+  cieg_ctx* ctx;
+  std::uint32_t n;
+  const cieg_dist_hooks* hooks;
+  Mat reduce(Mat g) const {
+    if (hooks && !g.empty() && hooks->allreduce_sum(hooks->user, g.data(), g.size()) != 0)
+      fail(CIEG_ERR_ARGUMENT, "allreduce_sum hook failed");
+    return g;
+  }
+  Mat gram(const View3& l, const View3& r) const { return reduce(cieg::gram(ctx, n, l, r)); }
+  // out = [out] + in G, returning L^T out (or out^T out for L == nullptr)
+  Mat combine_gram(const View3& in, const double* g, std::uint32_t kout, const Out2& out, bool acc,
+                   const View3* L) const {
+    return reduce(cieg::combine_gram(ctx, n, in, g, kout, out, acc, L));
+  }
+};
+
+// orthonormalize (lobpcg.cpp:89-119) over device blocks. `v` holds the input
+// (width v.w) and is overwritten; `tmp` is scratch of the same capacity; the
+// result (possibly width 0) is left in `v` (the two may swap). The second
+// projection pass's Gram and the Gram of the projected block are fused into
+// the combine passes that produce them.
+void orthonormalize_dev(const GramOps& ops, Block& v, Block& tmp, double drop_tol, const View3* against) {
   if (v.w == 0) return;
+  cieg_ctx* ctx = ops.ctx;
+  const std::uint32_t n = ops.n;
   const int k = static_cast<int>(v.w);
-  Mat g0 = gram(view({sg(v)}), view({sg(v)}));
+  Mat g0 = ops.gram(view({sg(v)}), view({sg(v)}));
   std::vector<double> orig_sq(k);
   for (int j = 0; j < k; ++j) orig_sq[j] = g0[j + static_cast<std::size_t>(j) * k];
+  Mat gram_v = g0;  // without a projection the Gram is unchanged
   if (against && against->width > 0) {
-    for (int pass = 0; pass < 2; ++pass) {
-      Mat c = gram(*against, view({sg(v)}));
-      for (double& e : c) e = -e;
-      combine(ctx, n, *against, c.data(), v.w, out1(v.p, v.w), true);
-    }
+    Mat c = ops.gram(*against, view({sg(v)}));
+    for (double& e : c) e = -e;
+    Mat c2 = ops.combine_gram(*against, c.data(), v.w, out1(v.p, v.w), true, against);  // pass 1 + pass-2 Gram
+    for (double& e : c2) e = -e;
+    gram_v = ops.combine_gram(*against, c2.data(), v.w, out1(v.p, v.w), true, nullptr);  // pass 2 + V^T V
   }
-  // Without a projection the Gram is unchanged (the reference recomputes it;
-  // the deterministic kernel would return the identical matrix).
-  Mat gram_v = (against && against->width > 0) ? gram(view({sg(v)}), view({sg(v)})) : g0;
   std::vector<std::uint32_t> kept = rank_revealing_select(gram_v, k, orig_sq, drop_tol);
   while (!kept.empty()) {
     const int kk = static_cast<int>(kept.size());
@@ -147,15 +166,15 @@ void orthonormalize_dev(cieg_ctx* ctx, std::uint32_t n, GramFn&& gram, Block& v,
       for (int b = 0; b < kk; ++b) sub[a + b * kk] = gram_v[kept[a] + static_cast<std::size_t>(kept[b]) * k];
     Mat rinv;
     if (llt_rinv(sub, kk, rinv)) {
-      // q = V[:, kept] R^{-1}: one combine with the selection folded in.
+      // q = V[:, kept] R^{-1}: one combine with the selection folded in,
+      // fused with the Gram of q for the second CholQR pass
       Mat sel(static_cast<std::size_t>(k) * kk, 0.0);
       for (int a = 0; a < kk; ++a)
         for (int c = 0; c < kk; ++c) sel[kept[a] + static_cast<std::size_t>(c) * k] = rinv[a + c * kk];
-      combine(ctx, n, view({sg(v)}), sel.data(), kk, out1(tmp.p, kk), false);
+      Mat gq = ops.combine_gram(view({sg(v)}), sel.data(), kk, out1(tmp.p, kk), false, nullptr);
       tmp.w = kk;
       std::swap(v, tmp);
       // cholqr_pass (lobpcg.cpp:61-69): second pass, result ignored on failure.
-      Mat gq = gram(view({sg(v)}), view({sg(v)}));
       Mat rinv2;
       if (llt_rinv(gq, kk, rinv2)) combine(ctx, n, view({sg(v)}), rinv2.data(), kk, out1(v.p, kk), false);
       return;
@@ -169,7 +188,8 @@ class Solver {
  public:
   Solver(cieg_ctx* ctx, const cieg_mat* mat, const cieg_prec* prec, const cieg_lobpcg_options& opt,
          cieg_report& rep, const cieg_dist_hooks* hooks = nullptr)
-      : ctx_(ctx), mat_(mat), prec_(prec), opt_(opt), rep_(rep), n_(mat->row_hi - mat->row_lo), hooks_(hooks) {
+      : ctx_(ctx), mat_(mat), prec_(prec), opt_(opt), rep_(rep), n_(mat->row_hi - mat->row_lo), hooks_(hooks),
+        ops_{ctx, mat->row_hi - mat->row_lo, hooks} {
     ws_.n = n_;
   }
 
@@ -199,13 +219,9 @@ class Solver {
     launch_spmm(ctx_, mat_, xin, x.w, hx.p, x.w, x.w);
     hx.w = x.w;
   }
-  Mat gram(const View3& l, const View3& r) {
-    Mat g = cieg::gram(ctx_, n_, l, r);
-    if (hooks_ && !g.empty() && hooks_->allreduce_sum(hooks_->user, g.data(), g.size()) != 0)
-      fail(CIEG_ERR_ARGUMENT, "allreduce_sum hook failed");
-    return g;
-  }
-  void clean_p_block(double drop_tol);
+  Mat gram(const View3& l, const View3& r) { return ops_.gram(l, r); }
+  // c1: X^T P when already known (fused into the Rayleigh-Ritz update), else empty
+  void clean_p_block(double drop_tol, const Mat& c1);
 
   cieg_ctx* ctx_;
   const cieg_mat* mat_;
@@ -214,6 +230,7 @@ class Solver {
   cieg_report& rep_;
   std::uint32_t n_;  // local rows (all rows unless sharded)
   const cieg_dist_hooks* hooks_;
+  GramOps ops_;
   DevBuf xfull_;
   Workspace ws_;
   Block x_, hx_, p_, hp_, x2_, hx2_, p2_, hp2_, w_, hw_, wtmp_, r_, wsrc_;
@@ -221,21 +238,22 @@ class Solver {
 };
 
 void Solver::orthonormalize(Block& v, Block& tmp, double drop_tol, const View3* against) {
-  orthonormalize_dev(ctx_, n_, [this](const View3& l, const View3& r) { return gram(l, r); }, v, tmp, drop_tol,
-                     against);
+  orthonormalize_dev(ops_, v, tmp, drop_tol, against);
 }
 
-void Solver::clean_p_block(double drop_tol) {
-  // lobpcg.cpp:180-212
+void Solver::clean_p_block(double drop_tol, const Mat& c1) {
+  // lobpcg.cpp:180-212; the second pass's X^T P and the final P^T P are fused
+  // into the combine passes that produce P
   if (p_.w == 0) return;
-  for (int pass = 0; pass < 2; ++pass) {
-    Mat c = gram(view({sg(x_)}), view({sg(p_)}));
-    for (double& e : c) e = -e;
-    combine(ctx_, n_, view({sg(x_)}), c.data(), p_.w, out1(p_.p, p_.w), true);
-    combine(ctx_, n_, view({sg(hx_)}), c.data(), hp_.w, out1(hp_.p, hp_.w), true);
-  }
+  const View3 xv = view({sg(x_)});
+  Mat c = c1.empty() ? gram(xv, view({sg(p_)})) : c1;
+  for (double& e : c) e = -e;
+  Mat c2 = ops_.combine_gram(xv, c.data(), p_.w, out1(p_.p, p_.w), true, &xv);
+  combine(ctx_, n_, view({sg(hx_)}), c.data(), hp_.w, out1(hp_.p, hp_.w), true);
+  for (double& e : c2) e = -e;
+  Mat g = ops_.combine_gram(xv, c2.data(), p_.w, out1(p_.p, p_.w), true, nullptr);
+  combine(ctx_, n_, view({sg(hx_)}), c2.data(), hp_.w, out1(hp_.p, hp_.w), true);
   const int k = static_cast<int>(p_.w);
-  Mat g = gram(view({sg(p_)}), view({sg(p_)}));
   std::vector<double> orig_sq(k);
   for (int j = 0; j < k; ++j) orig_sq[j] = g[j + static_cast<std::size_t>(j) * k];
   std::vector<std::uint32_t> kept = rank_revealing_select(g, k, orig_sq, drop_tol);
@@ -416,16 +434,27 @@ void Solver::run(const double* x0_host, std::uint32_t kt0, cieg_observer_fn obs,
     }
     {
       Clock c(ctx_, &rep_.timing_ms[kOrtho]);
-      Mat xg = gram(view({sg(x_)}), view({sg(x_)}));
+      // X guard (lobpcg.cpp:363-375): X^T X and clean_p's first X^T P from
+      // one read of X and P
+      Mat g_xp = gram(view({sg(x_), sg(p_)}), view({sg(x_), sg(p_)}));
+      const int k2 = static_cast<int>(x_.w + p_.w);
+      Mat xg(static_cast<std::size_t>(kt) * kt), xp(static_cast<std::size_t>(kt) * p_.w);
+      for (int a = 0; a < kt; ++a) {
+        for (int b = 0; b < kt; ++b) xg[a + static_cast<std::size_t>(b) * kt] = g_xp[a + static_cast<std::size_t>(b) * k2];
+        for (std::uint32_t b = 0; b < p_.w; ++b)
+          xp[a + static_cast<std::size_t>(b) * kt] = g_xp[a + static_cast<std::size_t>(kt + b) * k2];
+      }
+      bool rescaled = false;
       if (dev_from_identity(xg, kt) > 1e-12) {
         Mat rinv;
         if (llt_rinv(xg, kt, rinv)) {
           combine(ctx_, n_, view({sg(x_)}), rinv.data(), kt, out1(x_.p, kt), false);
           combine(ctx_, n_, view({sg(hx_)}), rinv.data(), kt, out1(hx_.p, kt), false);
           ++rep_.counters[3];
+          rescaled = true;
         }
       }
-      clean_p_block(drop_tol);
+      clean_p_block(drop_tol, rescaled ? Mat{} : xp);
     }
     ++rep_.counters[3];
   }
@@ -563,9 +592,7 @@ int cieg_orthonormalize(cieg_ctx* ctx, double* y_dev, uint32_t n, uint32_t k, do
     cieg::Block tmp{static_cast<double*>(scratch.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(n) * k))),
                     0, k};
     const cieg::View3 ag = cieg::view({cieg::seg(against_dev, ka)});
-    cieg::orthonormalize_dev(
-        ctx, n, [&](const cieg::View3& l, const cieg::View3& r) { return cieg::gram(ctx, n, l, r); }, v, tmp,
-        drop_tol, ka ? &ag : nullptr);
+    cieg::orthonormalize_dev(cieg::GramOps{ctx, n, nullptr}, v, tmp, drop_tol, ka ? &ag : nullptr);
     if (v.w && v.p != y_dev)
       CIEG_CUDA(cudaMemcpyAsync(y_dev, v.p, sizeof(double) * std::size_t(n) * v.w, cudaMemcpyDeviceToDevice,
                                 ctx->stream));
