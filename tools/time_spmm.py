@@ -9,6 +9,7 @@ ap.add_argument("--cfg", default="cfg2-spmm")
 ap.add_argument("--m", type=int, nargs="+", default=[16])
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--scale", type=float, default=1.0)
+ap.add_argument("--te", type=int, default=0)
 a = ap.parse_args()
 cfg = configs.ALL[a.cfg]
 if a.scale != 1.0:
@@ -20,7 +21,8 @@ s = torch.cuda.Stream()
 torch.cuda.set_stream(s)
 dev.set_stream(s.cuda_stream)
 import time; _t = time.time()
-dm = cfg.generate_device(device=dev)
+dm = ci.DeviceMatrix.generate(cfg.n, cfg.sectors, cfg.tile, cfg.p(), cfg.q, cfg.seed, cfg.precision, cfg.beta,
+                             device=dev, tile_edge=a.te)
 print(f"generate_device {time.time() - _t:.2f} s", flush=True)
 S = dm.nnz
 for m in a.m:
