@@ -305,33 +305,63 @@ def lanczos_record():
 def sweep_record(dev):
     """BASELINE config 3: the config-1 matrix (fp64, L2-resident) at m = 1..64:
     device time per SpMM (CUDA events, 20 back-to-back calls after warm-up),
-    algorithmic GB/s and flop/byte per m."""
+    algorithmic GB/s and flop/byte per m. The problem is L2-resident and
+    launch-bound, so the same 20 calls are also captured in a CUDA graph and
+    replayed (`graph_us`, launch overhead removed); both are labelled."""
     import torch
 
+    from paper_1609_01689_b200 import _lib as L
     from paper_1609_01689_b200 import ci, configs
 
     cfg = configs.CFG1
     dm = cfg.generate_device(device=dev)
-    stream = torch.cuda.ExternalStream(dev.stream, device=torch.device("cuda", dev.index))
+    tdev = torch.device("cuda", dev.index)
+    lib = L.load()
+    stream = torch.cuda.Stream(device=tdev)
+    ci._check(lib.cieg_ctx_set_stream(dev.handle, ctypes.c_void_p(stream.cuda_stream)))
     out = []
-    for m in configs.SWEEP_M:
-        x = torch.from_numpy(ci.random_block(cfg.n, m, m)).cuda()
-        y = torch.empty_like(x)
-        torch.cuda.synchronize()
-        for _ in range(3):
-            dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(20):
-            dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
-        e1.record(stream)
-        e1.synchronize()
-        us = e0.elapsed_time(e1) / 20 * 1e3
-        b = configs.spmm_bytes(dm.nnz, cfg.n, m, 1)
-        f = configs.spmm_flops(dm.nnz, cfg.n, m)
-        out.append({"m": m, "us": round(us, 2), "gbs": round(b / (us * 1e-6) / 1e9, 1),
-                    "flop_per_byte": round(f / b, 3), "gflops": round(f / (us * 1e-6) / 1e9, 1)})
-    return {"workload": "cfg3-sweep (config-1 matrix, fp64 H, L2-resident)", "points": out}
+    try:
+        for m in configs.SWEEP_M:
+            x = torch.from_numpy(ci.random_block(cfg.n, m, m)).to(tdev)
+            y = torch.empty_like(x)
+            torch.cuda.synchronize()
+            with torch.cuda.stream(stream):
+                for _ in range(3):
+                    dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(20):
+                    dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+                e1.record(stream)
+            e1.synchronize()
+            us = e0.elapsed_time(e1) / 20 * 1e3
+            graph_us = None
+            try:
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=stream):
+                    for _ in range(20):
+                        dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+                g.replay()
+                torch.cuda.synchronize()
+                e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    e2.record(stream)
+                    g.replay()
+                    e3.record(stream)
+                e3.synchronize()
+                graph_us = round(e2.elapsed_time(e3) / 20 * 1e3, 2)
+            except Exception:  # capture unsupported here: report the plain number only
+                graph_us = None
+            b = configs.spmm_bytes(dm.nnz, cfg.n, m, 1)
+            f = configs.spmm_flops(dm.nnz, cfg.n, m)
+            out.append({"m": m, "us": round(us, 2), "graph_us": graph_us,
+                        "gbs": round(b / (us * 1e-6) / 1e9, 1),
+                        "graph_gbs": round(b / (graph_us * 1e-6) / 1e9, 1) if graph_us else None,
+                        "flop_per_byte": round(f / b, 3), "gflops": round(f / (us * 1e-6) / 1e9, 1)})
+    finally:
+        ci._check(lib.cieg_ctx_set_stream(dev.handle, None))
+    return {"workload": "cfg3-sweep (config-1 matrix, fp64 H, L2-resident; us = back-to-back launches, "
+                        "graph_us = CUDA-graph replay)", "points": out}
 
 
 def cfg4_record(dev):

@@ -69,6 +69,7 @@ struct cieg_ctx {
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
   cieg::DevBuf scratch_x2, scratch_y2;  // second buffers of the pipelined host batch
   cieg::DevBuf scratch_flag;            // K1 non-finite-input flag
+  unsigned spmm_launch_id = 0;          // tags the flag per K1 launch
   cieg::PinnedBuf pinned_small;
 };
 

@@ -59,7 +59,8 @@ struct SpmmArgs {
   double* y;
   std::uint32_t ldx, ldy, mcols, npanels;
   std::uint32_t row_base;  // first owner row of a shard (U is written shard-local)
-  unsigned* nonfinite;     // set when an X value is Inf/NaN (staged as 0; fixed up after the launch)
+  unsigned* nonfinite;     // = launch_id when an X value is Inf/NaN (staged as 0; fixed up after the launch)
+  unsigned launch_id;      // per-launch tag: no reset of the flag between launches
 };
 
 constexpr int kProducerWarps = 8;
@@ -228,8 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
   // Producer layout: with one n-tile (m <= 8) the consumers are quick and the
   // producers' per-item memory round trips dominate, so two producer groups
   // fill alternating items concurrently; with two n-tiles the DMMA work per
-  // item covers them and one 8-warp group (twice the placement rate) wins.
-  constexpr bool kTwoGroups = NT == 1;
+  // item (128-row tiles) covers them and one 8-warp group (twice the
+  // placement rate) wins.
+  constexpr bool kTwoGroups = NT == 1 || TD == 64;  // 64-row tiles: little DMMA work per item
   constexpr int kHandoff = (kTwoGroups ? kGroupThreads : kProducerThreads) + kConsumerThreads;
 
   if (warp < kProducerWarps && !kTwoGroups) {
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       cur = nxt;
       nxt = after;
     }
-    if (nonfinite) *a.nonfinite = 1u;
+    if (nonfinite) *a.nonfinite = a.launch_id;
   } else if (warp < kProducerWarps) {
     // ------------------------------------------------------------ producers
     // Two producer groups of 4 warps fill alternating items -- group G the
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         cur = nxt;
         nxt = after;
       }
-      if (nonfinite) *a.nonfinite = 1u;
+      if (nonfinite) *a.nonfinite = a.launch_id;
     }
   } else {
     // ------------------------------------------------------------ consumer
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 template <typename V>
 __global__ void nonfinite_fix_kernel(const SpmmArgs a, std::uint32_t te, int precision, std::uint32_t p_lo,
                                      std::uint32_t p_hi, std::uint32_t halo_lo, std::uint32_t halo_hi) {
-  if (*a.nonfinite == 0u) return;
+  if (*a.nonfinite != a.launch_id) return;
   const std::uint32_t sa = cieg_tl::stride(te, precision);
   const V* val = static_cast<const V*>(a.val);
   const std::uint64_t total = static_cast<std::uint64_t>(halo_hi - halo_lo) * a.mcols;
@@ -585,6 +587,15 @@ void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::ui
 
 }  // namespace
 
+// The non-finite flag: zeroed once when allocated; each K1 launch tags it
+// with its own launch id, so it never needs a reset (launch ids start at 1).
+unsigned* nonfinite_flag(cieg_ctx* ctx) {
+  const bool fresh = ctx->scratch_flag.bytes == 0;
+  auto* f = static_cast<unsigned*>(ctx->scratch_flag.get(sizeof(unsigned)));
+  if (fresh) CIEG_CUDA(cudaMemsetAsync(f, 0, sizeof(unsigned), ctx->stream));
+  return f;
+}
+
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
                  std::uint32_t ldy, std::uint32_t mcols) {
   if (mcols == 0 || m->dim == 0) return;
@@ -607,8 +618,8 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   mc,
                   m->npanels,
                   m->row_lo,
-                  static_cast<unsigned*>(ctx->scratch_flag.get(sizeof(unsigned)))};
-    CIEG_CUDA(cudaMemsetAsync(args.nonfinite, 0, sizeof(unsigned), ctx->stream));
+                  nonfinite_flag(ctx),
+                  ++ctx->spmm_launch_id};
     if (m->precision == 0) {
       if (m->tile_edge == 64)
         dispatch_nt<float, 64>(ctx, m, args, mc);
