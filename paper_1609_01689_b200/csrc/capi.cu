@@ -132,8 +132,12 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   cudaStreamSynchronize(ctx->stream);
   ctx->scratch_x.release();
   ctx->scratch_y.release();
+  ctx->scratch_x2.release();
+  ctx->scratch_y2.release();
   ctx->scratch_red.release();
   ctx->scratch_small.release();
+  ctx->scratch_flag.release();
+  for (auto& b : ctx->solver_pool) b.release();
   ctx->pinned_small.release();
   cudaStreamSynchronize(ctx->own_stream);
   cudaStreamDestroy(ctx->own_stream);

@@ -5,6 +5,7 @@
 
 #include <cstdint>
 #include <string>
+#include <deque>
 #include <vector>
 
 #include "cieg_internal.hpp"
@@ -70,6 +71,7 @@ struct cieg_ctx {
   cieg::DevBuf scratch_x2, scratch_y2;  // second buffers of the pipelined host batch
   cieg::DevBuf scratch_flag;            // K1 non-finite-input flag
   unsigned spmm_launch_id = 0;          // tags the flag per K1 launch
+  std::deque<cieg::DevBuf> solver_pool; // LOBPCG work blocks, reused across solves
   cieg::PinnedBuf pinned_small;
 };
 

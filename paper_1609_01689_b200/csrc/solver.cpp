@@ -34,18 +34,19 @@ struct Block {
   std::uint32_t cap = 0;
 };
 
+// Solver work blocks come from a pool kept in the context, so back-to-back
+// solves reuse their allocations (no cudaMalloc / synchronising cudaFree per
+// solve); buffers only grow.
 struct Workspace {
+  cieg_ctx* ctx = nullptr;
   std::uint32_t n = 0;
-  std::vector<double*> owned;
-  ~Workspace() {
-    for (double* p : owned) cudaFree(p);
-  }
+  std::size_t next = 0;
   Block alloc(std::uint32_t cap) {
     Block b;
     b.cap = cap;
     const std::size_t bytes = sizeof(double) * std::max<std::size_t>(1, static_cast<std::size_t>(n) * cap);
-    CIEG_CUDA(cudaMalloc(&b.p, bytes));
-    owned.push_back(b.p);
+    if (ctx->solver_pool.size() <= next) ctx->solver_pool.emplace_back();
+    b.p = static_cast<double*>(ctx->solver_pool[next++].get(bytes));
     return b;
   }
 };
@@ -190,6 +191,7 @@ class Solver {
          cieg_report& rep, const cieg_dist_hooks* hooks = nullptr)
       : ctx_(ctx), mat_(mat), prec_(prec), opt_(opt), rep_(rep), n_(mat->row_hi - mat->row_lo), hooks_(hooks),
         ops_{ctx, mat->row_hi - mat->row_lo, hooks} {
+    ws_.ctx = ctx;
     ws_.n = n_;
   }
 
