@@ -671,7 +671,7 @@ def ours(args):
         pd = ctypes.POINTER(ctypes.c_double)
         xp = [ctypes.cast(t.data_ptr(), pd) for t in xhs]
         yp = [ctypes.cast(t.data_ptr(), pd) for t in yhs]
-        ke = max(3, min(args.steps, 10))
+        ke = max(3, min(args.steps, 20))  # pipeline fill + drain amortised over the batch
         xs = (pd * ke)(*[xp[i % 2] for i in range(ke)])
         ys = (pd * ke)(*[yp[i % 2] for i in range(ke)])
         own = torch.cuda.ExternalStream(dev.stream, device=tdev)

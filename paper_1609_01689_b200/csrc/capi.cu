@@ -134,6 +134,8 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   ctx->scratch_y.release();
   ctx->scratch_x2.release();
   ctx->scratch_y2.release();
+  ctx->scratch_x3.release();
+  ctx->scratch_y3.release();
   ctx->scratch_red.release();
   ctx->scratch_small.release();
   ctx->scratch_flag.release();
@@ -416,15 +418,19 @@ int cieg_spmm_host_batch(cieg_ctx* ctx, const cieg_mat* mat, const double* const
     for (uint32_t i = 0; i < count; ++i)
       if (!x_hosts[i] || !y_hosts[i]) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host_batch: null vector");
     CIEG_CUDA(cudaSetDevice(ctx->device));
-    double* dx[2] = {static_cast<double*>(ctx->scratch_x.get(xbytes)), static_cast<double*>(ctx->scratch_x2.get(xbytes))};
-    double* dy[2] = {static_cast<double*>(ctx->scratch_y.get(ybytes)), static_cast<double*>(ctx->scratch_y2.get(ybytes))};
-    // Three-stage pipeline over independent products: the upload of X_{i+1}
-    // and the download of U_{i-1} run on the two copy engines while K1
-    // computes U_i on the context stream; device X / U are double-buffered.
+    // Three device X / U buffers: the upload of X_{i+1}, K1 on U_i and the
+    // download of U_{i-1} run concurrently without waiting on each other's
+    // buffer reuse (the download of a U takes longer than K1 when both copy
+    // directions are busy).
+    constexpr int kB = 3;
+    double* dx[kB] = {static_cast<double*>(ctx->scratch_x.get(xbytes)), static_cast<double*>(ctx->scratch_x2.get(xbytes)),
+                      static_cast<double*>(ctx->scratch_x3.get(xbytes))};
+    double* dy[kB] = {static_cast<double*>(ctx->scratch_y.get(ybytes)), static_cast<double*>(ctx->scratch_y2.get(ybytes)),
+                      static_cast<double*>(ctx->scratch_y3.get(ybytes))};
     cudaStream_t up = nullptr, down = nullptr;
-    cudaEvent_t uploaded[2] = {}, computed[2] = {}, downloaded[2] = {};
+    cudaEvent_t uploaded[kB] = {}, computed[kB] = {}, downloaded[kB] = {};
     auto cleanup = [&] {
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < kB; ++b) {
         if (uploaded[b]) cudaEventDestroy(uploaded[b]);
         if (computed[b]) cudaEventDestroy(computed[b]);
         if (downloaded[b]) cudaEventDestroy(downloaded[b]);
@@ -435,23 +441,21 @@ int cieg_spmm_host_batch(cieg_ctx* ctx, const cieg_mat* mat, const double* const
     try {
       CIEG_CUDA(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
       CIEG_CUDA(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
-      for (int b = 0; b < 2; ++b) {
+      for (int b = 0; b < kB; ++b) {
         CIEG_CUDA(cudaEventCreateWithFlags(&uploaded[b], cudaEventDisableTiming));
         CIEG_CUDA(cudaEventCreateWithFlags(&computed[b], cudaEventDisableTiming));
         CIEG_CUDA(cudaEventCreateWithFlags(&downloaded[b], cudaEventDisableTiming));
+        // nothing may touch the buffers before work already queued on the context stream
+        CIEG_CUDA(cudaEventRecord(computed[b], ctx->stream));
+        CIEG_CUDA(cudaEventRecord(downloaded[b], ctx->stream));
       }
-      // nothing may touch the buffers before work already queued on the context stream
-      CIEG_CUDA(cudaEventRecord(computed[0], ctx->stream));
-      CIEG_CUDA(cudaEventRecord(computed[1], ctx->stream));
-      CIEG_CUDA(cudaEventRecord(downloaded[0], ctx->stream));
-      CIEG_CUDA(cudaEventRecord(downloaded[1], ctx->stream));
       for (uint32_t i = 0; i < count; ++i) {
-        const int b = static_cast<int>(i & 1u);
-        CIEG_CUDA(cudaStreamWaitEvent(up, computed[b], 0));  // K1 of step i-2 has read X[b]
+        const int b = static_cast<int>(i % kB);
+        CIEG_CUDA(cudaStreamWaitEvent(up, computed[b], 0));  // K1 of step i-3 has read X[b]
         CIEG_CUDA(cudaMemcpyAsync(dx[b], x_hosts[i], xbytes, cudaMemcpyHostToDevice, up));
         CIEG_CUDA(cudaEventRecord(uploaded[b], up));
         CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, uploaded[b], 0));
-        CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, downloaded[b], 0));  // U[b] of step i-2 is home
+        CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, downloaded[b], 0));  // U[b] of step i-3 is home
         cieg::launch_spmm(ctx, mat, dx[b], m, dy[b], m, m);
         CIEG_CUDA(cudaEventRecord(computed[b], ctx->stream));
         CIEG_CUDA(cudaStreamWaitEvent(down, computed[b], 0));

@@ -68,7 +68,7 @@ struct cieg_ctx {
   int exact_order = 0;  // 1: K5 reproduces the reference's operation order bit for bit
   int sm_count = 148;
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
-  cieg::DevBuf scratch_x2, scratch_y2;  // second buffers of the pipelined host batch
+  cieg::DevBuf scratch_x2, scratch_y2, scratch_x3, scratch_y3;  // ring buffers of the pipelined host batch
   cieg::DevBuf scratch_flag;            // K1 non-finite-input flag
   unsigned spmm_launch_id = 0;          // tags the flag per K1 launch
   std::deque<cieg::DevBuf> solver_pool; // LOBPCG work blocks, reused across solves
