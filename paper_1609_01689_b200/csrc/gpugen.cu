@@ -27,7 +27,8 @@ struct GenTile {
   std::uint32_t a0, nr;  // global first row / rows of panel PI
   std::uint32_t b0, nc;  // global first column / columns of panel PJ
   std::uint32_t diag;    // PI == PJ (lower part only, incl. the diagonal)
-  std::uint32_t sector;  // sector of the rows (diagonal values)
+  std::uint32_t sector;  // sector of the rows (diagonal values), when not `general`
+  std::uint32_t general; // a panel merges several generator tiles: per-entry tile lookup
 };
 
 struct GenArgs {
@@ -36,11 +37,37 @@ struct GenArgs {
   double q, scale;
   std::uint32_t sa, te;
   int precision;
+  // generator tile grid, for `general` device tiles (small generator tiles
+  // merged into one panel): tile starts (ntiles + 1), sectors, first kept-
+  // candidate tile J0 of the band, and the tile-keep hash (generator.cpp:
+  // kept_tiles)
+  const std::uint32_t* tstart;
+  const std::uint32_t* tsector;
+  const std::uint32_t* tj0;
+  std::uint32_t ntiles;
+  std::uint64_t tile_seed;
+  double p;
 };
+
+__device__ __forceinline__ std::uint32_t tile_of(const GenArgs& g, std::uint32_t r) {
+  std::uint32_t lo = 0, hi = g.ntiles;  // largest t with tstart[t] <= r
+  while (hi - lo > 1) {
+    const std::uint32_t mid = (lo + hi) / 2;
+    if (g.tstart[mid] <= r) lo = mid; else hi = mid;
+  }
+  return lo;
+}
 
 __device__ __forceinline__ bool entry_exists(const GenArgs& g, const GenTile& t, std::uint32_t a, std::uint32_t b) {
   if (t.diag && b > a) return false;
   if (a == b) return true;
+  if (t.general) {  // the generator tile pair of this entry must be kept
+    const std::uint32_t I = tile_of(g, a), J = tile_of(g, b);
+    if (I != J) {
+      if (J > I || J < g.tj0[I]) return false;
+      if (!(cieg_gen::unit_double(cieg_gen::hash3(g.tile_seed, I, J)) < g.p)) return false;
+    }
+  }
   return cieg_gen::unit_double(cieg_gen::hash3(g.q_seed, a, b)) < g.q;
 }
 
@@ -91,7 +118,8 @@ __global__ void __launch_bounds__(128) gen_fill_kernel(GenArgs g, const std::uin
       double v;
       if (a == b) {
         const double u = cieg_gen::unit_double(cieg_gen::hash3(g.d_seed, a, a));
-        v = 10.0 * static_cast<double>(t.sector) + 4.0 * u - 2.0;
+        const std::uint32_t sec = t.general ? g.tsector[tile_of(g, a)] : t.sector;
+        v = 10.0 * static_cast<double>(sec) + 4.0 * u - 2.0;
       } else {
         v = cieg_gen::normal_from(cieg_gen::hash3(g.v1_seed, a, b), cieg_gen::hash3(g.v2_seed, a, b)) * g.scale;
       }
@@ -121,11 +149,15 @@ T* dev_upload(const std::vector<T>& v) {
 cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t te, std::uint32_t row_lo,
                           std::uint32_t row_hi) {
   validate(p);
-  if (te == 0) te = p.precision == 1 ? 64 : (p.tile <= 64 ? 64 : 128);
-  if (p.precision == 1) te = 64;
-  if (te != 64 && te != 128) fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
   if (row_hi == 0) row_hi = p.n;
   const TileGrid grid = make_grid(p);
+  if (te == 0) {  // the rule of cieg_matrix_upload (capi.cu: choose_tile_edge) on the generator's groups
+    std::uint32_t mx = 0;
+    for (std::uint32_t t = 0; t < grid.count(); ++t) mx = std::max(mx, grid.start[t + 1] - grid.start[t]);
+    te = mx <= 64 ? 64 : 128;
+  }
+  if (p.precision == 1) te = 64;
+  if (te != 64 && te != 128) fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
   const std::uint32_t ng = grid.count();
   const std::vector<std::vector<std::uint32_t>> kept = kept_tiles(p, grid);
   const double scale = value_scale(p);
@@ -136,13 +168,17 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
   ht.precision = p.precision;
   ht.panel_start = plan_panels(p.n, grid.start.data(), ng, te);
   const std::uint32_t np = static_cast<std::uint32_t>(ht.panel_start.size() - 1);
-  // generator tile -> its panel range (panels never span two generator tiles)
-  std::vector<std::uint32_t> tp0(ng + 1);
-  for (std::uint32_t t = 0, P = 0; t <= ng; ++t) {
-    const std::uint32_t r = t < ng ? grid.start[t] : p.n;
-    while (P < np && ht.panel_start[P] < r) ++P;
-    if (P <= np && ht.panel_start[P] != r) fail(CIEG_ERR_CONFIG, "panel plan does not follow the generator tiles");
-    tp0[t] = P;
+  // generator tile -> its panel range [tpa, tpb): a chunked large tile spans
+  // several panels; small tiles merged by the planner share one panel, whose
+  // device tiles then decide per entry which generator tile pair it is in
+  std::vector<std::uint32_t> tpa(ng), tpb(ng), tiles_in_panel(np, 0);
+  for (std::uint32_t t = 0; t < ng; ++t) {
+    const std::uint32_t r0 = grid.start[t], r1 = grid.start[t + 1];
+    tpa[t] = static_cast<std::uint32_t>(std::upper_bound(ht.panel_start.begin(), ht.panel_start.end(), r0) -
+                                        ht.panel_start.begin()) - 1;
+    tpb[t] = static_cast<std::uint32_t>(std::lower_bound(ht.panel_start.begin(), ht.panel_start.end(), r1) -
+                                        ht.panel_start.begin());
+    for (std::uint32_t P = tpa[t]; P < tpb[t]; ++P) ++tiles_in_panel[P];
   }
   const std::uint32_t p_lo = static_cast<std::uint32_t>(
       std::lower_bound(ht.panel_start.begin(), ht.panel_start.end(), row_lo) - ht.panel_start.begin());
@@ -158,13 +194,15 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
   std::vector<Key> keys;
   for (std::uint32_t I = 0; I < ng; ++I)
     for (std::uint32_t J : kept[I])
-      for (std::uint32_t PI = tp0[I]; PI < tp0[I + 1]; ++PI)
-        for (std::uint32_t PJ = tp0[J]; PJ < tp0[J + 1]; ++PJ) {
-          if (I == J && PJ > PI) continue;
+      for (std::uint32_t PI = tpa[I]; PI < tpb[I]; ++PI)
+        for (std::uint32_t PJ = tpa[J]; PJ < tpb[J]; ++PJ) {
+          if (PJ > PI) continue;  // lower triangle of panels (diagonal tiles: lower part)
           if (!owned(PI) && !owned(PJ)) continue;
           keys.push_back({PI, PJ, I});
         }
   std::sort(keys.begin(), keys.end(), [](const Key& x, const Key& y) { return x.pi != y.pi ? x.pi < y.pi : x.pj < y.pj; });
+  keys.erase(std::unique(keys.begin(), keys.end(), [](const Key& x, const Key& y) { return x.pi == y.pi && x.pj == y.pj; }),
+             keys.end());
   const std::uint64_t nt = keys.size();
   std::vector<GenTile> gt(nt);
   ht.tile_pi.resize(nt);
@@ -173,15 +211,28 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
     const Key& q = keys[k];
     ht.tile_pi[k] = q.pi;
     ht.tile_pj[k] = q.pj;
+    const std::uint32_t general = (tiles_in_panel[q.pi] > 1 || tiles_in_panel[q.pj] > 1) ? 1u : 0u;
     gt[k] = GenTile{ht.panel_start[q.pi], ht.panel_start[q.pi + 1] - ht.panel_start[q.pi], ht.panel_start[q.pj],
-                    ht.panel_start[q.pj + 1] - ht.panel_start[q.pj], q.pi == q.pj ? 1u : 0u, grid.sector[q.I]};
+                    ht.panel_start[q.pj + 1] - ht.panel_start[q.pj], q.pi == q.pj ? 1u : 0u, grid.sector[q.I], general};
+  }
+  // band start J0 per tile row (generator.cpp: kept_tiles)
+  std::vector<std::uint32_t> tj0(ng);
+  for (std::uint32_t I = 0; I < ng; ++I) {
+    const std::uint32_t sI = grid.sector[I];
+    const std::uint32_t s_lo = sI >= p.band ? sI - p.band : 0;
+    tj0[I] = static_cast<std::uint32_t>(std::lower_bound(grid.start.begin(), grid.start.end() - 1,
+                                                         grid.sector_start[s_lo]) - grid.start.begin());
   }
   const cieg_gen::Seeds sd = cieg_gen::derive_seeds(p.seed);
   CIEG_CUDA(cudaSetDevice(ctx->device));
   GenTile* d_tiles = dev_upload(gt);
+  std::uint32_t* d_tstart = dev_upload(grid.start);
+  std::uint32_t* d_tsector = dev_upload(grid.sector);
+  std::uint32_t* d_tj0 = dev_upload(tj0);
   std::uint32_t* d_counts = nullptr;
   CIEG_CUDA(cudaMalloc(&d_counts, std::max<std::uint64_t>(1, nt) * sizeof(std::uint32_t)));
-  GenArgs ga{d_tiles, sd.q, sd.v1, sd.v2, sd.d, p.q, scale, cieg_tl::stride(te, p.precision), te, p.precision};
+  GenArgs ga{d_tiles, sd.q, sd.v1, sd.v2, sd.d, p.q, scale, cieg_tl::stride(te, p.precision), te, p.precision,
+             d_tstart, d_tsector, d_tj0, ng, sd.tile, p.p};
   cieg_mat* m = nullptr;
   try {
     if (nt) {
@@ -259,11 +310,17 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
   } catch (...) {
     cudaFree(d_tiles);
     cudaFree(d_counts);
+    cudaFree(d_tstart);
+    cudaFree(d_tsector);
+    cudaFree(d_tj0);
     delete m;
     throw;
   }
   cudaFree(d_tiles);
   cudaFree(d_counts);
+  cudaFree(d_tstart);
+  cudaFree(d_tsector);
+  cudaFree(d_tj0);
   return m;
 }
 

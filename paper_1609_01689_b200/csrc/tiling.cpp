@@ -71,6 +71,7 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
     std::uint32_t pj;
     std::vector<std::uint32_t> idx;
     std::vector<double> v;
+    std::vector<std::uint16_t> key;  // row-major position in the tile (canonical order)
   };
   std::vector<std::vector<Bucket>> rowtiles(np);
   const bool single = csb.precision == 0;
@@ -120,7 +121,7 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
                 break;
               }
             if (!tb) {
-              bk.push_back(Bucket{pj, {}, {}});
+              bk.push_back(Bucket{pj, {}, {}, {}});
               tb = &bk.back();
             }
           }
@@ -128,11 +129,32 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
           // Packed tile-local index: the entry's shared-memory offset in the
           // row-part orientation and in the transposed one (tile_layout.h).
           tb->idx.push_back(cieg_tl::pack(rl, cl, sa, prec));
+          tb->key.push_back(static_cast<std::uint16_t>(rl * te + cl));
           tb->v.push_back(single ? static_cast<double>(v32[e]) : v64[e]);
         }
       }
     }
     std::sort(bk.begin(), bk.end(), [](const Bucket& x, const Bucket& y) { return x.pj < y.pj; });
+    // canonical row-major entry order inside every tile (a panel may straddle
+    // CSB blocks, which the walk above visits block by block): the GPU
+    // generator emits the same order, and the bank-aware reorder (reorder.cu)
+    // starts from it
+    for (Bucket& b : bk) {
+      if (!std::is_sorted(b.key.begin(), b.key.end())) {
+        std::vector<std::uint32_t> ord(b.key.size());
+        std::iota(ord.begin(), ord.end(), 0u);
+        std::sort(ord.begin(), ord.end(), [&](std::uint32_t x, std::uint32_t y) { return b.key[x] < b.key[y]; });
+        std::vector<std::uint32_t> idx(ord.size());
+        std::vector<double> v(ord.size());
+        for (std::size_t k = 0; k < ord.size(); ++k) {
+          idx[k] = b.idx[ord[k]];
+          v[k] = b.v[ord[k]];
+        }
+        b.idx.swap(idx);
+        b.v.swap(v);
+      }
+      std::vector<std::uint16_t>().swap(b.key);
+    }
   }
 
   out = HostTiles{};
