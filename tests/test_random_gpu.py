@@ -38,3 +38,39 @@ def test_random_generator_configs(c):
     host = ci.DeviceMatrix(h)
     for a, b in zip(dev.export(), host.export()):
         assert np.array_equal(a, b)
+
+
+rng2 = np.random.default_rng(7)
+LOBPCG_CASES = []
+for _ in range(16):
+    sectors = int(rng2.integers(2, 6))
+    tile = int(rng2.choice([32, 64, 128]))
+    n = int(rng2.integers(800, 4000)) // sectors * sectors
+    kt = int(rng2.choice([4, 6, 8]))
+    LOBPCG_CASES.append(dict(n=n, sectors=sectors, tile=tile, p=float(rng2.uniform(0.1, 0.6)),
+                             q=float(rng2.uniform(0.2, 0.6)), seed=int(rng2.integers(1, 1 << 30)),
+                             precision=int(rng2.integers(0, 2)), band=int(rng2.integers(1, 3)), kt=kt,
+                             k=int(rng2.integers(1, kt // 2 + 1)), prec=bool(rng2.integers(0, 2))))
+
+
+@pytest.mark.parametrize("c", LOBPCG_CASES,
+                         ids=[f"n{c['n']}t{c['tile']}k{c['k']}kt{c['kt']}p{c['precision']}{'P' if c['prec'] else ''}"
+                              for c in LOBPCG_CASES])
+def test_random_lobpcg_vs_live_reference(ref_lib, c):
+    """The north-star contract on random small problems: same iteration count
+    and counters as the reference's lobpcg_solve, eigenvalues to 1e-8 (fp64 H)
+    / 1e-5 (fp32 H) relative."""
+    h = ci.generate_sector_matrix(c["n"], c["sectors"], c["tile"], c["p"], c["q"], c["seed"], c["precision"], 2000,
+                                  band=c["band"])
+    tol = 1e-8 if c["precision"] == 1 else 1e-6
+    x0 = ci.random_block(h.dim, c["kt"], c["seed"] % 997)
+    td = ci.extract_tile_diagonal(h) if c["prec"] else None
+    rep = ci.lobpcg_solve(h, x0, ci.LobpcgOptions(k_want=c["k"], tol=tol, preconditioner=td))
+    rm = ref_lib.RefMatrix(h)
+    rtd = ref_lib.RefTileDiagonal(rm, h.groups) if c["prec"] else None
+    r = ref_lib.lobpcg_solve(rm, x0, c["k"], tol, 500, rtd)
+    assert rep.converged == r.converged
+    assert rep.iterations == r.iterations
+    assert [rep.counters.spmm_calls, rep.counters.spmv_equivalents, rep.counters.precond_applications,
+            rep.counters.orthogonalizations] == r.counters.tolist()
+    np.testing.assert_allclose(rep.eigenvalues, r.eigenvalues, rtol=1e-8 if c["precision"] == 1 else 1e-5)
