@@ -74,3 +74,24 @@ def test_random_lobpcg_vs_live_reference(ref_lib, c):
     assert [rep.counters.spmm_calls, rep.counters.spmv_equivalents, rep.counters.precond_applications,
             rep.counters.orthogonalizations] == r.counters.tolist()
     np.testing.assert_allclose(rep.eigenvalues, r.eigenvalues, rtol=1e-8 if c["precision"] == 1 else 1e-5)
+
+
+rng3 = np.random.default_rng(11)
+LANCZOS_CASES = []
+for _ in range(6):
+    sectors = int(rng3.integers(2, 6))
+    n = int(rng3.integers(600, 3000)) // sectors * sectors
+    LANCZOS_CASES.append(dict(n=n, sectors=sectors, tile=int(rng3.choice([32, 64, 128])),
+                              p=float(rng3.uniform(0.1, 0.6)), q=float(rng3.uniform(0.2, 0.6)),
+                              seed=int(rng3.integers(1, 1 << 30)), precision=int(rng3.integers(0, 2)),
+                              k=int(rng3.integers(1, 5))))
+
+
+@pytest.mark.parametrize("c", LANCZOS_CASES, ids=[f"n{c['n']}k{c['k']}p{c['precision']}" for c in LANCZOS_CASES])
+def test_random_lanczos_vs_live_reference(ref_lib, c):
+    h = ci.generate_sector_matrix(c["n"], c["sectors"], c["tile"], c["p"], c["q"], c["seed"], c["precision"], 2000)
+    v0 = ci.lanczos_default_start(h.dim, h.dim // c["sectors"])
+    rep = ci.lanczos_solve(h, v0, ci.LanczosOptions(k_want=c["k"], tol=1e-8, max_iter=300))
+    r = ref_lib.lanczos_solve(ref_lib.RefMatrix(h), v0, c["k"], 1e-8, 300)
+    assert rep.converged == r.converged and rep.iterations == r.iterations
+    np.testing.assert_allclose(rep.eigenvalues, r.eigenvalues, rtol=1e-10)
