@@ -254,8 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
     };
     Item cur = load_item(a, i_beg);
     Item nxt = (i_beg + 1 < i_end) ? load_item(a, i_beg + 1) : cur;
+    // qb carries each item's first batch across the item boundary: it is
+    // moved to qa only after the tile is cleared, so its memory round trip
+    // overlaps the clearing and the slab store instead of stalling them.
     Quad<V> qa[kQuads], qb[kQuads];
-    load_batch(cur, cur.q0, qa);
+    load_batch(cur, cur.q0, qb);
     double xv[S::kSlabPer];
     load_slab<V, TD, NT>(a, cur, pt, xv);
     bool nonfinite = false;
@@ -295,6 +298,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       const Item after = (i + 2 < i_end) ? load_item(a, i + 2) : nxt;
       bar_sync(kBarProducers, kProducerThreads);  // clear before scatter
       const std::uint32_t kind = cur.kind();
+#pragma unroll
+      for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
       for (std::uint64_t q = cur.q0;; q += kChunkQuads) {
         const bool more = q + kChunkQuads < cur.q1;
         if (more)
@@ -311,9 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
           else if (kind == 2u)
             put4<2>(A, qa[j]);
         }
+        if (!more) break;
 #pragma unroll
         for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
-        if (!more) break;
       }
       bar_arrive(kBarFull0 + buf, kThreads);
       buf ^= 1;
@@ -347,8 +352,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
     if (i0 < i_end) {
       Item cur = load_item(a, i0);
       Item nxt = (i0 + 2 < i_end) ? load_item(a, i0 + 2) : cur;
-      Quad<V> qa[kQuads], qb[kQuads];
-      load_batch(cur, cur.q0, qa);
+      Quad<V> qa[kQuads], qb[kQuads];  // qb: the item's first batch, as above
+      load_batch(cur, cur.q0, qb);
       double xv[S::kSlabPerG];
       load_slab_g<V, TD, NT>(a, cur, pt, xv);
       bool nonfinite = false;
@@ -386,6 +391,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         const Item after = (i + 4 < i_end) ? load_item(a, i + 4) : nxt;
         bar_sync(kBarProducers0 + grp, kGroupThreads);  // zeroing done before any scatter
         const std::uint32_t kind = cur.kind();
+#pragma unroll
+        for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
         for (std::uint64_t q = cur.q0;; q += kGroupChunkQuads) {
           const bool more = q + kGroupChunkQuads < cur.q1;
           if (more)
@@ -402,9 +409,9 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
             else if (kind == 2u)
               put4<2>(A, qa[j]);
           }
+          if (!more) break;
 #pragma unroll
           for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
-          if (!more) break;
         }
         bar_arrive(kBarFull0 + buf, kGroupThreads + kConsumerThreads);
         cur = nxt;
