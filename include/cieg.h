@@ -75,6 +75,15 @@ void* cieg_ctx_stream(cieg_ctx* ctx);
  * products and parallel fixed-order reductions (deterministic, ~1e-16
  * relative difference). Direct LU solves are reference-order in both. */
 int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact);
+/* SpMM (K1) mode: CIEG_SPMM_AUTO (default) = single pass for block widths
+ * <= 8 on unsharded matrices, owner-computes otherwise; CIEG_SPMM_OWNER =
+ * every stored tile streamed once per owner panel; CIEG_SPMM_SINGLE_PASS =
+ * one pass per stored tile, H·X and Hᵀ·X from the same shared tile, the
+ * transposed half reduced through per-tile partials (unsharded matrices;
+ * shards stay owner-computes). All modes are deterministic. Replaces no
+ * reference call: spmm (csb.cpp:118-193) has one code path. */
+enum { CIEG_SPMM_AUTO = 0, CIEG_SPMM_OWNER = 1, CIEG_SPMM_SINGLE_PASS = 2 };
+int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode);
 /* Number of kernels this context has launched (instrumentation). */
 uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx);
 

@@ -180,6 +180,7 @@ SIGNATURES = {
     "cieg_precond_from_csb_range": (_i, [_vp, C.POINTER(CsbView), _pu32, _u32, _u32, _u32, C.POINTER(_vp)]),
     "cieg_ctx_set_stream": (_i, [_vp, _vp]),
     "cieg_ctx_set_exact_order": (_i, [_vp, _i]),
+    "cieg_ctx_set_spmm_mode": (_i, [_vp, _i]),
     "cieg_report_summary": (_i, [_vp, _pi, _pi, _pd, _pu32, _pu32, _pu64]),
     "cieg_report_counters": (_i, [_vp, _pu64]),
     "cieg_report_eigenvalues": (_i, [_vp, _pd]),

@@ -130,6 +130,16 @@ class Device:
         fixed-order reductions."""
         _check(_lib.load().cieg_ctx_set_exact_order(self.handle, 1 if exact else 0))
 
+    SPMM_MODES = {"auto": 0, "owner": 1, "single": 2}
+
+    def set_spmm_mode(self, mode: str) -> None:
+        """SpMM mode: "auto" (default: single pass for widths <= 8 on
+        unsharded matrices), "owner" (owner-computes) or "single" (single
+        pass). cieg_ctx_set_spmm_mode."""
+        if mode not in self.SPMM_MODES:
+            raise ValueError(f"unknown SpMM mode {mode!r}")
+        _check(_lib.load().cieg_ctx_set_spmm_mode(self.handle, self.SPMM_MODES[mode]))
+
     @property
     def stream(self) -> int:
         return int(_lib.load().cieg_ctx_stream(self.handle) or 0)

@@ -36,6 +36,10 @@ cieg_mat::~cieg_mat() {
     cudaFree(idx);
     cudaFree(val);
   }
+  cudaFree(sp_sched_off);
+  cudaFree(sp_sched);
+  cudaFree(sp_col_off);
+  cudaFree(sp_col_items);
   cudaFree(work_off);
   cudaFree(work_tile);
   cudaFree(work_other);
@@ -139,6 +143,7 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   ctx->scratch_red.release();
   ctx->scratch_small.release();
   ctx->scratch_flag.release();
+  ctx->scratch_partial.release();
   for (auto& b : ctx->solver_pool) b.release();
   ctx->pinned_small.release();
   cudaStreamSynchronize(ctx->own_stream);
@@ -178,6 +183,30 @@ std::uint32_t choose_tile_edge(const cieg_csb_view* csb, const uint32_t* group_b
   return te;
 }
 
+}  // namespace
+
+namespace cieg {
+void upload_schedule(cieg_mat* m, const HostTiles& ht) {
+  m->work_off = upload_vec(ht.work_off);
+  m->work_tile = upload_vec(ht.work_tile);
+  m->work_other = upload_vec(ht.work_other);
+  m->work_kind = upload_vec(ht.work_kind);
+  m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
+  m->sched_off = upload_vec(ht.sched_off);
+  m->sched = upload_vec(ht.sched);
+  if (!ht.sp_sched_off.empty()) {
+    m->sp_ctas = static_cast<std::uint32_t>(ht.sp_sched_off.size() - 1);
+    m->sp_items = static_cast<std::uint32_t>(ht.sp_sched.size() / 8);
+    m->sp_sched_off = upload_vec(ht.sp_sched_off);
+    m->sp_sched = upload_vec(ht.sp_sched);
+    m->sp_col_off = upload_vec(ht.sp_col_off);
+    m->sp_col_items = upload_vec(ht.sp_col_items);
+  }
+}
+}  // namespace cieg
+
+namespace {
+
 cieg_mat* upload_tiles(cieg_ctx* ctx, cieg::HostTiles& ht) {
   cieg::build_schedule(ht, static_cast<std::uint32_t>(ctx->sm_count));
   auto* m = new cieg_mat;
@@ -204,13 +233,7 @@ cieg_mat* upload_tiles(cieg_ctx* ctx, cieg::HostTiles& ht) {
       m->val = cieg::upload_vec(ht.val32);
     else
       m->val = cieg::upload_vec(ht.val64);
-    m->work_off = cieg::upload_vec(ht.work_off);
-    m->work_tile = cieg::upload_vec(ht.work_tile);
-    m->work_other = cieg::upload_vec(ht.work_other);
-    m->work_kind = cieg::upload_vec(ht.work_kind);
-    m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
-    m->sched_off = cieg::upload_vec(ht.sched_off);
-    m->sched = cieg::upload_vec(ht.sched);
+    cieg::upload_schedule(m, ht);
     m->tile_bytes = ht.tile_off.back() * (4 + (ht.precision == 0 ? 4 : 8));
     cieg::order_tile_entries(ctx, m);
   } catch (...) {
@@ -291,13 +314,7 @@ int cieg_matrix_leading_view(cieg_ctx* ctx, const cieg_mat* m, uint32_t dim, cie
     v->tile_off = m->tile_off;
     v->idx = m->idx;
     v->val = m->val;
-    v->work_off = cieg::upload_vec(ht.work_off);
-    v->work_tile = cieg::upload_vec(ht.work_tile);
-    v->work_other = cieg::upload_vec(ht.work_other);
-    v->work_kind = cieg::upload_vec(ht.work_kind);
-    v->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
-    v->sched_off = cieg::upload_vec(ht.sched_off);
-    v->sched = cieg::upload_vec(ht.sched);
+    cieg::upload_schedule(v.get(), ht);
     // stored entries of the block (padding sentinels excluded), for info()
     v->nnz = count_real_entries(ctx, m->idx, ht.tile_off.back(), m->tile_edge | (m->tile_edge << 16));
     v->tile_bytes = ht.tile_off.back() * (4 + (m->precision == 0 ? 4 : 8));
@@ -346,6 +363,14 @@ int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact) {
   return cieg::guarded([&] {
     if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");
     ctx->exact_order = exact ? 1 : 0;
+  });
+}
+
+int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode) {
+  return cieg::guarded([&] {
+    if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");
+    if (mode < CIEG_SPMM_AUTO || mode > CIEG_SPMM_SINGLE_PASS) cieg::fail(CIEG_ERR_ARGUMENT, "unknown SpMM mode");
+    ctx->spmm_mode = mode;
   });
 }
 

@@ -65,11 +65,13 @@ struct cieg_ctx {
   cudaStream_t stream = nullptr;      // stream all work is enqueued on
   cudaStream_t own_stream = nullptr;  // the context's own stream
   std::uint64_t launches = 0;
-  int exact_order = 0;  // 1: K5 reproduces the reference's operation order bit for bit
+  int exact_order = 0;
+  int spmm_mode = -1;  // CIEG_SPMM_*; -1 = not set (CIEG_SPMM_MODE env, else auto)  // 1: K5 reproduces the reference's operation order bit for bit
   int sm_count = 148;
   cieg::DevBuf scratch_x, scratch_y, scratch_red, scratch_small;
   cieg::DevBuf scratch_x2, scratch_y2, scratch_x3, scratch_y3;  // ring buffers of the pipelined host batch
   cieg::DevBuf scratch_flag;            // K1 non-finite-input flag
+  cieg::DevBuf scratch_partial;         // single-pass K1: transposed partial products
   unsigned spmm_launch_id = 0;          // tags the flag per K1 launch
   std::deque<cieg::DevBuf> solver_pool; // LOBPCG work blocks, reused across solves
   cieg::PinnedBuf pinned_small;
@@ -101,6 +103,12 @@ struct cieg_mat {
   std::uint32_t sched_ctas = 0;
   std::uint32_t* sched_off = nullptr;
   std::uint32_t* sched = nullptr;
+  // single-pass schedule (full matrices; tiling.hpp): one item per stored tile
+  std::uint32_t sp_ctas = 0, sp_items = 0;
+  std::uint32_t* sp_sched_off = nullptr;
+  std::uint32_t* sp_sched = nullptr;
+  std::uint32_t* sp_col_off = nullptr;
+  std::uint32_t* sp_col_items = nullptr;
   // a leading-block view (cieg_matrix_leading_view) borrows panel_start,
   // tile_off, idx and val from its parent and owns only its work lists
   bool borrowed_stream = false;
@@ -112,6 +120,10 @@ namespace cieg {
 // Bank-aware ordering of the entries inside every tile (reorder.cu); run
 // once on every freshly built device tile stream.
 void order_tile_entries(cieg_ctx* ctx, cieg_mat* m);
+
+// Upload the work lists and both K1 schedules of a tiling.
+struct HostTiles;
+void upload_schedule(cieg_mat* m, const HostTiles& ht);
 
 // Launch the owner-computes SpMM over device X/Y (row-major, ld = ldx/ldy).
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,

@@ -297,13 +297,7 @@ cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t
       CIEG_CUDA(cudaGetLastError());
       ctx->launches += 2;
     }
-    m->work_off = dev_upload(ht.work_off);
-    m->work_tile = dev_upload(ht.work_tile);
-    m->work_other = dev_upload(ht.work_other);
-    m->work_kind = dev_upload(ht.work_kind);
-    m->sched_ctas = static_cast<std::uint32_t>(ht.sched_off.size() - 1);
-    m->sched_off = dev_upload(ht.sched_off);
-    m->sched = dev_upload(ht.sched);
+    upload_schedule(m, ht);
     m->tile_bytes = slots * (4 + (p.precision == 0 ? 4 : 8));
     order_tile_entries(ctx, m);
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -35,6 +35,8 @@
 //   * the next item's entry stream is bulk-prefetched into L2
 //     (cp.async.bulk.prefetch.L2) a whole item ahead of the register batches.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <cstdint>
 
 #include "context.hpp"
@@ -61,6 +63,7 @@ struct SpmmArgs {
   std::uint32_t row_base;  // first owner row of a shard (U is written shard-local)
   unsigned* nonfinite;     // = launch_id when an X value is Inf/NaN (staged as 0; fixed up after the launch)
   unsigned launch_id;      // per-launch tag: no reset of the flag between launches
+  double* partial;         // single pass: Aᵀ X_pi of item i at partial + i * TD * mcols (row-major, ld mcols)
 };
 
 constexpr int kProducerWarps = 8;
@@ -75,6 +78,7 @@ constexpr int kChunkQuads = kQuads * kProducerThreads;     // 1024 quads = 4096 
 constexpr int kGroupChunkQuads = kQuads * kGroupThreads;  // per producer group
 // named barrier ids (0 is __syncthreads)
 constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProducers = 5, kBarProducers0 = 5;  // groups: 5, 6
+constexpr int kBarConsumers = 7;  // single pass: the consumers' owner-slab refresh
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -90,6 +94,7 @@ struct Shape {
   static constexpr std::size_t kTileBytes = ((sizeof(V) * TD * kSA + 15) / 16) * 16;
   static constexpr std::size_t kSlabBytes = sizeof(double) * TD * kSX;
   static constexpr std::size_t kSmem = 2 * (kTileBytes + kSlabBytes);
+  static constexpr std::size_t kSmemSP = kSmem + kSlabBytes;  // + the owner panel's X slab
   static constexpr int kSlabPer = TD * 8 * NT / kProducerThreads;  // slab doubles per producer thread
   static constexpr int kSlabPerG = TD * 8 * NT / kGroupThreads;    // ... per producer-group thread
 };
@@ -214,7 +219,82 @@ __device__ __forceinline__ void put4(double* A, const Quad<double>& b) {
   put<KIND>(A, b.id.w, b.v1.y);
 }
 
+// Single pass, consumer warp cw: the transposed product D = Aᵀ X_P of an
+// off-diagonal item for tile columns [8 MT cw, 8 MT (cw + 1)) (D rows),
+// k over the tile rows, from the shared tile read column-wise, and its store
+// to the item's partial slot. fp32, 2 m-tiles: lane g takes columns
+// c0 = 16 cw + (g & 3) + 8 (g >> 2) and c0 + 4, adjacent in the permuted
+// row (tile_layout.h), so one float2 carries both m-tiles' A fragments.
 template <typename V, int TD, int NT>
+__device__ __forceinline__ void transposed_product(const SpmmArgs& a, const V* T, const double* oslab, std::uint32_t i,
+                                                   const Item& it, int cw, int lane) {
+  using S = Shape<V, TD, NT>;
+  constexpr int MT = S::kMT;
+  constexpr bool kPair = sizeof(V) == 4 && MT == 2;
+  const int g = lane >> 2, q = lane & 3;
+  const int prec = sizeof(V) == 4 ? 0 : 1;
+  int col[MT], pos[MT];
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    col[j] = kPair ? 16 * cw + (g & 3) + 8 * (g >> 2) + 4 * j : 8 * MT * cw + 8 * j + g;
+    pos[j] = static_cast<int>(cieg_tl::perm(static_cast<std::uint32_t>(col[j]), prec));
+  }
+  double acc[MT][NT][2];
+#pragma unroll
+  for (int j = 0; j < MT; ++j)
+#pragma unroll
+    for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+  const V* A = T + q * S::kSA;
+  const double* xb = oslab + q * S::kSX + (NT == 2 ? 2 * g : g);
+  const int ksteps = (it.prow() + 3) >> 2;  // tile rows >= prow are zero
+#pragma unroll 4
+  for (int s = 0; s < ksteps; ++s) {
+    double fa[MT], fb[NT];
+    const V* Ar = A + 4 * s * S::kSA;
+    if constexpr (kPair) {
+      const float2 v2 = *reinterpret_cast<const float2*>(Ar + pos[0]);
+      fa[0] = static_cast<double>(v2.x);
+      fa[1] = static_cast<double>(v2.y);
+    } else {
+#pragma unroll
+      for (int j = 0; j < MT; ++j) fa[j] = static_cast<double>(Ar[pos[j]]);
+    }
+    const double* xr = xb + 4 * s * S::kSX;
+    if constexpr (NT == 2) {
+      const double2 v2 = *reinterpret_cast<const double2*>(xr);
+      fb[0] = v2.x;
+      fb[1] = v2.y;
+    } else {
+      fb[0] = xr[0];
+    }
+#pragma unroll
+    for (int n = 0; n < NT; ++n)
+#pragma unroll
+      for (int j = 0; j < MT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], fa[j], fb[n]);
+  }
+  const int mc = static_cast<int>(a.mcols);
+  double* out = a.partial + static_cast<std::size_t>(i) * TD * mc;
+#pragma unroll
+  for (int j = 0; j < MT; ++j) {
+    if (col[j] >= it.orow) continue;
+    double* o = out + static_cast<std::size_t>(col[j]) * mc;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int c = 8 * n + 2 * q;
+      if (c < mc) o[c] = acc[j][n][0];
+      if (c + 1 < mc) o[c + 1] = acc[j][n][1];
+    }
+  }
+}
+
+// SP = false: owner-computes -- an off-diagonal tile is streamed twice, once
+// per owner panel (row part into P, transposed part into Q), each output
+// row summed in registers by its owner. SP = true: single pass -- one item
+// per stored tile; the consumers also form Aᵀ X_P from the same shared tile
+// (X_P, the owner panel's slab, staged once per owner) and store it to the
+// item's partial slot, added to block column Q by sp_reduce_kernel in a
+// fixed order. Both are deterministic.
+template <typename V, int TD, int NT, bool SP>
 __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) {
   using S = Shape<V, TD, NT>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -424,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
     const int cw = warp - kProducerWarps;
     const int g = lane >> 2, q = lane & 3;
     const int m_base = cw * 8 * S::kMT;
+    double* oslab = reinterpret_cast<double*>(smem + 2 * S::kTileBytes + 2 * S::kSlabBytes);  // SP only
     bar_arrive(kBarEmpty0 + 0, kHandoff);
     bar_arrive(kBarEmpty0 + 1, kHandoff);
     int buf = 0;
@@ -436,6 +517,24 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         for (int j = 0; j < S::kMT; ++j)
 #pragma unroll
           for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
+        if constexpr (SP) {
+          // the owner panel's X rows, for the transposed products of its items
+          bar_sync(kBarConsumers, kConsumerThreads);  // every warp is done with the previous owner's slab
+          bool bad = false;
+          for (int e = tid - kProducerThreads; e < TD * 8 * NT; e += kConsumerThreads) {
+            const int k = e / (8 * NT), t = e - k * (8 * NT);
+            double v = (k < it.prow() && t < static_cast<int>(a.mcols))
+                           ? __ldg(a.x + static_cast<std::size_t>(it.r0 + k) * a.ldx + t)
+                           : 0.0;
+            if (!isfinite(v)) {  // staged as 0; nonfinite_fix_kernel adds its terms
+              v = 0.0;
+              bad = true;
+            }
+            oslab[k * S::kSX + (NT == 2 ? 2 * (t & 7) + (t >> 3) : t)] = v;
+          }
+          if (bad) *a.nonfinite = a.launch_id;
+          bar_sync(kBarConsumers, kConsumerThreads);
+        }
       }
       const std::uint32_t r0 = it.r0;
       const int prow = it.prow();
@@ -500,6 +599,9 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
           if (grp + 2 < kGroups) load_group(grp + 2, af[0], bf[0]);
           mma_group(af[1], bf[1]);
         }
+      }
+      if constexpr (SP) {
+        if (it.kind() == 0u && m_base < it.orow) transposed_product<V, TD, NT>(a, tile_buf(buf), oslab, i, it, cw, lane);
       }
       if (i + 2 < i_end) bar_arrive(kBarEmpty0 + buf, kHandoff);
       buf ^= 1;
@@ -573,23 +675,68 @@ __global__ void nonfinite_fix_kernel(const SpmmArgs a, std::uint32_t te, int pre
   }
 }
 
-template <typename V, int TD, int NT>
+// Single pass: Y[rows of Q] += sum of the partial slots of block column Q,
+// in the fixed slot order of sp_col_items (deterministic). One CTA per panel.
+__global__ void sp_reduce_kernel(const double* partial, const std::uint32_t* col_off, const std::uint32_t* col_items,
+                                 const std::uint32_t* panel_start, double* y, std::uint32_t ldy, std::uint32_t mcols,
+                                 std::uint32_t td) {
+  const std::uint32_t Q = blockIdx.x;
+  const std::uint32_t k0 = col_off[Q], k1 = col_off[Q + 1];
+  if (k0 == k1) return;
+  const std::uint32_t q0 = panel_start[Q], rows = panel_start[Q + 1] - q0;
+  for (std::uint32_t e = threadIdx.x; e < rows * mcols; e += blockDim.x) {
+    const std::uint32_t r = e / mcols, c = e - r * mcols;
+    double sum = 0.0;
+    for (std::uint32_t k = k0; k < k1; ++k)
+      sum += partial[(static_cast<std::size_t>(col_items[k]) * td + r) * mcols + c];
+    y[static_cast<std::size_t>(q0 + r) * ldy + c] += sum;
+  }
+}
+
+template <typename V, int TD, int NT, bool SP>
 void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   using S = Shape<V, TD, NT>;
-  static_assert(S::kSmem <= 227 * 1024, "shared memory budget");
-  auto kern = spmm_ws_kernel<V, TD, NT>;
-  CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(S::kSmem)));
-  kern<<<m->sched_ctas, kThreads, S::kSmem, ctx->stream>>>(args);
+  constexpr std::size_t smem = SP ? S::kSmemSP : S::kSmem;
+  static_assert(smem <= 227 * 1024, "shared memory budget");
+  auto kern = spmm_ws_kernel<V, TD, NT, SP>;
+  CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  kern<<<SP ? m->sp_ctas : m->sched_ctas, kThreads, smem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
 }
 
 template <typename V, int TD>
-void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::uint32_t mc) {
-  if (mc <= 8)
-    launch_variant<V, TD, 1>(ctx, m, args);
-  else
-    launch_variant<V, TD, 2>(ctx, m, args);
+void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::uint32_t mc, bool sp) {
+  if (sp) {
+    if (mc <= 8)
+      launch_variant<V, TD, 1, true>(ctx, m, args);
+    else
+      launch_variant<V, TD, 2, true>(ctx, m, args);
+  } else {
+    if (mc <= 8)
+      launch_variant<V, TD, 1, false>(ctx, m, args);
+    else
+      launch_variant<V, TD, 2, false>(ctx, m, args);
+  }
+}
+
+// K1 mode (cieg_ctx_set_spmm_mode; else CIEG_SPMM_MODE=owner|single; else
+// auto): single pass for block widths <= kSinglePassMaxCols on full
+// (unsharded) matrices, owner-computes otherwise. Measured on config 2
+// (profiles/README.md): single pass 2.88 / 3.13 / 5.12 ms at m = 1 / 8 / 16
+// vs owner-computes 3.65 / 3.71 / 4.77 ms.
+constexpr std::uint32_t kSinglePassMaxCols = 8;
+bool use_single_pass(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
+  static const int env_mode = [] {
+    const char* e = std::getenv("CIEG_SPMM_MODE");
+    if (e && std::strcmp(e, "owner") == 0) return static_cast<int>(CIEG_SPMM_OWNER);
+    if (e && std::strcmp(e, "single") == 0) return static_cast<int>(CIEG_SPMM_SINGLE_PASS);
+    return static_cast<int>(CIEG_SPMM_AUTO);
+  }();
+  if (!m->sp_sched || m->row_lo != 0 || m->row_hi != m->dim) return false;
+  const int mode = ctx->spmm_mode >= 0 ? ctx->spmm_mode : env_mode;
+  if (mode != CIEG_SPMM_AUTO) return mode == CIEG_SPMM_SINGLE_PASS;
+  return mc <= kSinglePassMaxCols;
 }
 
 }  // namespace
@@ -626,14 +773,28 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   m->npanels,
                   m->row_lo,
                   nonfinite_flag(ctx),
-                  ++ctx->spmm_launch_id};
+                  ++ctx->spmm_launch_id,
+                  nullptr};
+    const bool sp = use_single_pass(ctx, m, mc);
+    if (sp) {
+      args.sched_off = m->sp_sched_off;
+      args.sched = reinterpret_cast<const uint4*>(m->sp_sched);
+      args.partial = static_cast<double*>(
+          ctx->scratch_partial.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(m->sp_items) * m->tile_edge * mc)));
+    }
     if (m->precision == 0) {
       if (m->tile_edge == 64)
-        dispatch_nt<float, 64>(ctx, m, args, mc);
+        dispatch_nt<float, 64>(ctx, m, args, mc, sp);
       else
-        dispatch_nt<float, 128>(ctx, m, args, mc);
+        dispatch_nt<float, 128>(ctx, m, args, mc, sp);
     } else {  // fp64 values: 64-row tiles (a 128-row fp64 tile pair exceeds shared memory)
-      dispatch_nt<double, 64>(ctx, m, args, mc);
+      dispatch_nt<double, 64>(ctx, m, args, mc, sp);
+    }
+    if (sp) {
+      sp_reduce_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
+                                                            m->panel_start, y + c0, ldy, mc, m->tile_edge);
+      CIEG_CUDA(cudaGetLastError());
+      ++ctx->launches;
     }
     // owned panels of this (shard) matrix
     const auto& ps = m->panel_start_host;

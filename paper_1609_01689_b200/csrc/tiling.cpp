@@ -215,20 +215,23 @@ void build_tiles(const cieg_csb_view& csb, const std::vector<std::uint32_t>& pan
   if (nt >= (1ull << 32)) fail(CIEG_ERR_CONFIG, "tile count exceeds 2^32");
 }
 
-void build_schedule(HostTiles& t, std::uint32_t ctas) {
-  // owner panels of this tiling (all of them unless restricted to a shard)
-  const std::uint32_t p_lo = static_cast<std::uint32_t>(
-      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), t.row_lo) - t.panel_start.begin());
-  const std::uint32_t p_hi = static_cast<std::uint32_t>(
-      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), t.row_hi) - t.panel_start.begin());
+namespace {
+
+// Greedy longest-first assignment of owner panels [p_lo, p_hi) to CTAs and
+// the per-CTA item lists. With single_pass the transposed items are left
+// out (their product comes from the row-part item of the same tile).
+void assign_items(const HostTiles& t, std::uint32_t ctas, std::uint32_t p_lo, std::uint32_t p_hi, bool single_pass,
+                  std::vector<std::uint32_t>& sched_off, std::vector<std::uint32_t>& sched) {
   const std::uint32_t np = p_hi - p_lo;
   ctas = std::max<std::uint32_t>(1, std::min<std::uint32_t>(ctas, np));
+  auto counted = [&](std::uint32_t w) { return !single_pass || t.work_kind[w] != kTransposed; };
   // cost of a panel = entry quads of its work items + a fixed per-item charge
   std::vector<std::pair<std::uint64_t, std::uint32_t>> cost(np);
   for (std::uint32_t i = 0; i < np; ++i) {
     const std::uint32_t P = p_lo + i;
     std::uint64_t c = 0;
     for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w) {
+      if (!counted(w)) continue;
       const std::uint32_t tile = t.work_tile[w];
       c += (t.tile_off[tile + 1] - t.tile_off[tile]) / 4 + 256;
     }
@@ -252,33 +255,72 @@ void build_schedule(HostTiles& t, std::uint32_t ctas) {
     top.first += cost[i].first;
     std::push_heap(heap.begin(), heap.end(), cmp);
   }
-  t.sched_off.assign(ctas + 1, 0);
-  t.sched.clear();
+  sched_off.assign(ctas + 1, 0);
+  sched.clear();
+  std::vector<std::uint32_t> ws;
   for (std::uint32_t b = 0; b < ctas; ++b) {
     std::sort(panels_of[b].begin(), panels_of[b].end());
     for (std::uint32_t P : panels_of[b]) {
-      const std::uint32_t w0 = t.work_off[P], w1 = t.work_off[P + 1];
+      ws.clear();
+      for (std::uint32_t w = t.work_off[P]; w < t.work_off[P + 1]; ++w)
+        if (counted(w)) ws.push_back(w);
       const std::uint32_t prows = t.panel_start[P + 1] - t.panel_start[P];
-      if (w0 == w1) {  // empty panel: one no-op item so the owner still writes zeros
+      if (ws.empty()) {  // empty panel: one no-op item so the owner still writes zeros
         const std::uint32_t d[8] = {0, 0, 0, 0, 3u | (1u << 8) | (1u << 9) | (prows << 16), t.panel_start[P],
                                     prows, t.panel_start[P]};
-        t.sched.insert(t.sched.end(), d, d + 8);
+        sched.insert(sched.end(), d, d + 8);
         continue;
       }
-      for (std::uint32_t w = w0; w < w1; ++w) {
+      for (std::size_t k = 0; k < ws.size(); ++k) {
+        const std::uint32_t w = ws[k];
         const std::uint32_t tile = t.work_tile[w], other = t.work_other[w];
         const std::uint64_t q0 = t.tile_off[tile] / 4, q1 = t.tile_off[tile + 1] / 4;
-        const std::uint32_t flags = t.work_kind[w] | ((w == w0) ? 1u << 8 : 0u) | ((w + 1 == w1) ? 1u << 9 : 0u) |
+        const std::uint32_t flags = t.work_kind[w] | (k == 0 ? 1u << 8 : 0u) | (k + 1 == ws.size() ? 1u << 9 : 0u) |
                                     (prows << 16);
         const std::uint32_t d[8] = {static_cast<std::uint32_t>(q0), static_cast<std::uint32_t>(q0 >> 32),
                                     static_cast<std::uint32_t>(q1), static_cast<std::uint32_t>(q1 >> 32),
                                     flags, t.panel_start[other], t.panel_start[other + 1] - t.panel_start[other],
                                     t.panel_start[P]};
-        t.sched.insert(t.sched.end(), d, d + 8);
+        sched.insert(sched.end(), d, d + 8);
       }
     }
-    t.sched_off[b + 1] = static_cast<std::uint32_t>(t.sched.size() / 8);
+    sched_off[b + 1] = static_cast<std::uint32_t>(sched.size() / 8);
   }
+}
+
+}  // namespace
+
+void build_schedule(HostTiles& t, std::uint32_t ctas) {
+  // owner panels of this tiling (all of them unless restricted to a shard)
+  const std::uint32_t p_lo = static_cast<std::uint32_t>(
+      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), t.row_lo) - t.panel_start.begin());
+  const std::uint32_t p_hi = static_cast<std::uint32_t>(
+      std::lower_bound(t.panel_start.begin(), t.panel_start.end(), t.row_hi) - t.panel_start.begin());
+  assign_items(t, ctas, p_lo, p_hi, false, t.sched_off, t.sched);
+  t.sp_sched_off.clear();
+  t.sp_sched.clear();
+  t.sp_col_off.clear();
+  t.sp_col_items.clear();
+  if (t.row_lo != 0 || t.row_hi != t.dim) return;  // shards: owner-computes only
+  assign_items(t, ctas, p_lo, p_hi, true, t.sp_sched_off, t.sp_sched);
+  // partial slots per block column, in item order (a fixed order: deterministic sums)
+  const std::uint32_t np = t.npanels();
+  const std::size_t nitems = t.sp_sched.size() / 8;
+  std::vector<std::uint32_t> q_of(nitems, np);
+  for (std::size_t i = 0; i < nitems; ++i) {
+    const std::uint32_t* d = t.sp_sched.data() + 8 * i;
+    if ((d[4] & 0xffu) != kRowPart) continue;
+    q_of[i] = static_cast<std::uint32_t>(
+        std::upper_bound(t.panel_start.begin(), t.panel_start.end(), d[5]) - t.panel_start.begin() - 1);
+  }
+  t.sp_col_off.assign(np + 1, 0);
+  for (std::uint32_t qv : q_of)
+    if (qv < np) ++t.sp_col_off[qv + 1];
+  for (std::uint32_t Q = 0; Q < np; ++Q) t.sp_col_off[Q + 1] += t.sp_col_off[Q];
+  t.sp_col_items.resize(t.sp_col_off[np]);
+  std::vector<std::uint32_t> fill(t.sp_col_off.begin(), t.sp_col_off.end() - 1);
+  for (std::size_t i = 0; i < nitems; ++i)
+    if (q_of[i] < np) t.sp_col_items[fill[q_of[i]]++] = static_cast<std::uint32_t>(i);
 }
 
 void build_work_lists(HostTiles& out, std::uint32_t p_lo, std::uint32_t p_hi) {

@@ -46,6 +46,11 @@ struct HostTiles {
   // CTA b runs sched[sched_off[b] .. sched_off[b+1]) in order.
   std::vector<std::uint32_t> sched_off;
   std::vector<std::uint32_t> sched;  // 8 words per item, see ItemDesc in spmm.cu
+  // Single-pass schedule (full matrices only; empty for shards): one item
+  // per stored tile, owned by its row panel. An off-diagonal item's
+  // transposed product Aᵀ X_pi goes to partial slot = its item index; the
+  // slots feeding block column Q are sp_col_items[sp_col_off[Q] .. sp_col_off[Q+1]).
+  std::vector<std::uint32_t> sp_sched_off, sp_sched, sp_col_off, sp_col_items;
 
   // owner rows of this (shard) tiling and the X rows its SpMM reads
   std::uint32_t row_lo = 0, row_hi = 0, halo_lo = 0, halo_hi = 0;

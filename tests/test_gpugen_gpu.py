@@ -51,7 +51,13 @@ def test_device_generator_shard_matches_upload_shard():
         x = ci.random_block(n, 8, 7)
         y = dev.spmm_host(x)
         assert y.shape == (hi - lo, 8)
-        np.testing.assert_array_equal(y, ci.DeviceMatrix(h).spmm_host(x)[lo:hi])
+        # shards are owner-computes: bitwise equal to the full matrix in that mode
+        full = ci.DeviceMatrix(h)
+        ci.Device.default().set_spmm_mode("owner")
+        try:
+            np.testing.assert_array_equal(y, full.spmm_host(x)[lo:hi])
+        finally:
+            ci.Device.default().set_spmm_mode("auto")
 
 
 def test_lobpcg_on_generated_config1():

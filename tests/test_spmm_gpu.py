@@ -207,3 +207,92 @@ def test_spmm_nonfinite_on_a_shard():
             assert np.array_equal(mask(y), mask(ref))
         fin = np.isfinite(ref)
         np.testing.assert_allclose(y[fin], ref[fin], rtol=1e-12, atol=1e-12)
+
+
+# ---------------------------------------------------------------- K1 modes
+# Single pass (one item per stored tile, H·X and Hᵀ·X from the same shared
+# tile, transposed half through per-tile partials) and owner-computes must
+# both match the oracle at every width and tile shape, and stay bitwise
+# deterministic run to run.
+_MODE_MATS = {
+    "f64_t64": (20_000, 10, 64, 0.05, 0.5, 1, 1, 2000),
+    "f32_t128": (30_000, 3, 256, 0.02, 0.4, 77, 0, 2000),
+    "f32_t64": (20_000, 4, 64, 0.05, 0.5, 5, 0, 2000),
+}
+
+
+@pytest.fixture
+def spmm_mode():
+    dev = ci.Device.default()
+    yield dev.set_spmm_mode
+    dev.set_spmm_mode("auto")
+
+
+@pytest.mark.parametrize("mode", ["single", "owner"])
+@pytest.mark.parametrize("mat", list(_MODE_MATS))
+@pytest.mark.parametrize("m", [1, 3, 8, 9, 16, 24])
+def test_spmm_modes_match_reference(spmm_mode, mode, mat, m):
+    spmm_mode(mode)
+    h = gen_from(_MODE_MATS[mat])
+    dm = ci.DeviceMatrix(h)
+    x = ci.random_block(h.dim, m, 40 + m)
+    y = dm.spmm_host(x)
+    assert rel(y, O.spmm(h, x)) < TOL
+    assert np.array_equal(y, dm.spmm_host(x))
+
+
+def test_spmm_single_pass_equals_owner_to_rounding(spmm_mode):
+    """The two modes sum in different orders: equal to ~1e-16, and each
+    column independent of the block width."""
+    h = gen_from(_MODE_MATS["f32_t128"])
+    dm = ci.DeviceMatrix(h)
+    x = ci.random_block(h.dim, 8, 9)
+    spmm_mode("single")
+    ys = dm.spmm_host(x)
+    for j in range(8):
+        assert np.array_equal(dm.spmm_host(x[:, j:j + 1])[:, 0], ys[:, j])
+    spmm_mode("owner")
+    yo = dm.spmm_host(x)
+    assert rel(ys, yo) < TOL
+
+
+@pytest.mark.parametrize("mode", ["single", "owner"])
+def test_spmm_modes_generated_and_leading_view(spmm_mode, mode):
+    """Device-generated matrix (cieg_generate_device) and a leading-block
+    view (own schedules over the parent's tile stream) in both modes."""
+    spmm_mode(mode)
+    p = _MODE_MATS["f32_t128"]
+    dm = ci.DeviceMatrix.generate(p[0], p[1], p[2], p[3], p[4], p[5], p[6], p[7])
+    h = gen_from(p)
+    x = ci.random_block(h.dim, 5, 2)
+    assert rel(dm.spmm_host(x), O.spmm(h, x)) < TOL
+    hc = gen_from(p)
+    dmc = ci.DeviceMatrix(hc, cuts=[12_288])
+    lead = dmc.leading(12_288)
+    xl = ci.random_block(12_288, 4, 3)
+    full = np.zeros((h.dim, 4))
+    full[:12_288] = xl
+    assert rel(lead.spmm_host(xl), O.spmm(h, full)[:12_288]) < TOL
+
+
+@pytest.mark.parametrize("m", [2, 16])
+def test_spmm_single_pass_nonfinite(spmm_mode, m):
+    """Inf / NaN in X under single pass: the owner slab (transposed half) is
+    sanitised like the partner slab and the exact terms added afterwards."""
+    spmm_mode("single")
+    h = gen_from((3072, 3, 256, 0.2, 0.4, 13, 0, 2000))
+    x = ci.random_block(h.dim, m, 3)
+    x[100, 0] = np.inf
+    x[777, m - 1] = -np.inf
+    x[1500, m // 2] = np.nan
+    y = ci.spmm(h, x)
+    yo = O.spmm(h, x)
+    for mask in (np.isnan, np.isposinf, np.isneginf):
+        assert np.array_equal(mask(y), mask(yo))
+    fin = np.isfinite(yo)
+    np.testing.assert_allclose(y[fin], yo[fin], rtol=1e-12, atol=1e-12)
+
+
+def test_spmm_mode_rejects_unknown():
+    with pytest.raises(ValueError):
+        ci.Device.default().set_spmm_mode("fast")
