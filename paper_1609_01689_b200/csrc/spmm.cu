@@ -246,9 +246,10 @@ __device__ __forceinline__ void transposed_product(const SpmmArgs& a, const V* T
     for (int n = 0; n < NT; ++n) acc[j][n][0] = acc[j][n][1] = 0.0;
   const V* A = T + q * S::kSA;
   const double* xb = oslab + q * S::kSX + (NT == 2 ? 2 * g : g);
-  const int ksteps = (it.prow() + 3) >> 2;  // tile rows >= prow are zero
-#pragma unroll 4
-  for (int s = 0; s < ksteps; ++s) {
+  // all TD/4 k-steps, fully unrolled (tile and slab rows >= prow are zero):
+  // measured faster than a prow-bounded loop (cfg2 m = 8: 2.99 vs 3.13 ms)
+#pragma unroll
+  for (int s = 0; s < TD / 4; ++s) {
     double fa[MT], fb[NT];
     const V* Ar = A + 4 * s * S::kSA;
     if constexpr (kPair) {
@@ -723,8 +724,8 @@ void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::ui
 // K1 mode (cieg_ctx_set_spmm_mode; else CIEG_SPMM_MODE=owner|single; else
 // auto): single pass for block widths <= kSinglePassMaxCols on full
 // (unsharded) matrices, owner-computes otherwise. Measured on config 2
-// (profiles/README.md): single pass 2.88 / 3.13 / 5.12 ms at m = 1 / 8 / 16
-// vs owner-computes 3.65 / 3.71 / 4.77 ms.
+// (profiles/README.md): single pass 2.73 / 2.99 / 5.03 ms at m = 1 / 8 / 16
+// vs owner-computes 3.65 / 3.71 / 4.72 ms.
 constexpr std::uint32_t kSinglePassMaxCols = 8;
 bool use_single_pass(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
   static const int env_mode = [] {
