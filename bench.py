@@ -524,6 +524,42 @@ def cfg5_record(dev, rank, world):
     return out
 
 
+def widths_record(dev, dm, stream, n):
+    """K1 on the config-2 matrix at the LOBPCG / Lanczos block widths, in the
+    default mode (single pass for m <= 8, owner-computes above) and in
+    owner-computes, device time per launch (median of 3 x 10 launches)."""
+    import torch
+
+    from paper_1609_01689_b200 import configs
+
+    out = []
+    for m in (1, 4, 8, 16):
+        x = torch.randn(n, m, dtype=torch.float64, device="cuda")
+        y = torch.empty_like(x)
+        row = {"m": m}
+        for mode in ("auto", "owner"):
+            dev.set_spmm_mode(mode)
+            for _ in range(3):
+                dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+            times = []
+            for _ in range(3):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(10):
+                    dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+                e1.record(stream)
+                e1.synchronize()
+                times.append(e0.elapsed_time(e1) / 10)
+            t = sorted(times)[1]
+            row[mode] = {"ms": round(t, 4),
+                         "gbs": round(configs.spmm_bytes(dm.nnz, n, m, dm.precision) / (t * 1e-3) / 1e9, 1)}
+        row["auto_mode"] = "single pass" if m <= 8 else "owner-computes"
+        out.append(row)
+        del x, y
+    dev.set_spmm_mode("auto")
+    return {"workload": "cfg2-spmm K1 by block width", "points": out}
+
+
 def group_bounds(cfg):
     """Generator tile (= group) starts, the rule of generator.cpp make_grid."""
     out = []
@@ -654,6 +690,7 @@ def ours(args):
         nbytes = configs.spmm_bytes(nnz_total, n, m, 0)
         flops = configs.spmm_flops(nnz_total, n, m)
     gbs = nbytes / (ms * 1e-3) / 1e9
+    widths = widths_record(dev, dm, stream, n) if world == 1 else None
     ci._check(lib.cieg_ctx_set_stream(dev.handle, None))
     torch.cuda.set_stream(torch.cuda.default_stream(tdev))
 
@@ -736,6 +773,8 @@ def ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if widths is not None:
+        line["widths"] = widths
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(h, m)
     if world == 1 and not args.no_lobpcg:
