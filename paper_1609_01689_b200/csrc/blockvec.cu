@@ -214,7 +214,7 @@ constexpr int kCombineWarps = 8;
 // its 8 output rows in shared memory to re-read them in fragment layout;
 // per-warp partials are folded in warp order, per-CTA partials reduced in a
 // fixed order (deterministic).
-template <int OT, int LT = 0, bool SYM = false>
+template <int OT, int LT = 0, bool SYM = false, int KS = 12>
 __global__ void __launch_bounds__(32 * kCombineWarps)
     combine_kernel(const __grid_constant__ CombineParams p) {
   constexpr int SG = 8 * OT + 4;
@@ -270,8 +270,24 @@ __global__ void __launch_bounds__(32 * kCombineWarps)
   }
 
   const std::uint64_t ngroups = (p.n + 7) / 8;
-  for (std::uint64_t grp = static_cast<std::uint64_t>(blockIdx.x) * kCombineWarps + warp; grp < ngroups;
-       grp += static_cast<std::uint64_t>(gridDim.x) * kCombineWarps) {
+  // A fragments of a group of 8 rows, every segment at once (KS k-steps per
+  // segment): thread (g, q) holds Y[row i0 + g][4 ks + q] of segment s.
+  auto load_a = [&](std::uint64_t grp, double (&a)[3][KS]) {
+    const std::uint64_t arow = grp * 8 + g;
+    const bool rok = arow < p.n;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      if (s >= p.in.nseg) break;
+      const double* base = p.in.s[s].p + arow * p.in.s[s].ld;
+      const std::uint32_t w = p.in.s[s].w;
+#pragma unroll
+      for (int ks = 0; ks < KS; ++ks) {
+        const std::uint32_t k = 4 * ks + q;
+        a[s][ks] = (rok && k < w) ? base[k] : 0.0;
+      }
+    }
+  };
+  auto process = [&](std::uint64_t grp, const double (&a)[3][KS]) {
     const std::uint64_t i0 = grp * 8;
     double acc[OT][2];
     // C fragment rows i0 + g, columns 8 nt + 2q (+1)
@@ -291,25 +307,16 @@ __global__ void __launch_bounds__(32 * kCombineWarps)
         acc[nt][h] = v;
       }
     }
-    const std::uint64_t arow = i0 + g;
-    for (int s = 0; s < p.in.nseg; ++s) {
-      const double* base = p.in.s[s].p + arow * p.in.s[s].ld;
-      const std::uint32_t w = p.in.s[s].w;
-      const int ksteps = static_cast<int>((w + 3) / 4);
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      if (s >= p.in.nseg) break;
+      const int ksteps = static_cast<int>((p.in.s[s].w + 3) / 4);
       const double* gsb = gs + (poff[s] + q) * SG + g;
-      const bool rok = arow < p.n;
-      // all A fragments of the segment (<= 12 k-steps) are loaded before the DMMAs
-      double a[12];
 #pragma unroll
-      for (int ks = 0; ks < 12; ++ks) {
-        const std::uint32_t k = 4 * ks + q;
-        a[ks] = (ks < ksteps && rok && k < w) ? base[k] : 0.0;
-      }
-#pragma unroll
-      for (int ks = 0; ks < 12; ++ks) {
+      for (int ks = 0; ks < KS; ++ks) {
         if (ks >= ksteps) break;
 #pragma unroll
-        for (int nt = 0; nt < OT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a[ks], gsb[4 * ks * SG + 8 * nt]);
+        for (int nt = 0; nt < OT; ++nt) dmma_8x8x4(acc[nt][0], acc[nt][1], a[s][ks], gsb[4 * ks * SG + 8 * nt]);
       }
     }
     if (crow < p.n) {
@@ -356,6 +363,13 @@ __global__ void __launch_bounds__(32 * kCombineWarps)
       }
       __syncwarp();
     }
+    };
+  const std::uint64_t stride = static_cast<std::uint64_t>(gridDim.x) * kCombineWarps;
+  std::uint64_t grp = static_cast<std::uint64_t>(blockIdx.x) * kCombineWarps + warp;
+  for (; grp < ngroups; grp += stride) {
+    double a[3][KS];
+    load_a(grp, a);
+    process(grp, a);
   }
   if constexpr (LT > 0) {
     constexpr int MA = 8 * LT, NB = 8 * OT;
@@ -391,7 +405,10 @@ void launch_combine(cieg_ctx* ctx, const CombineParams& prm, int blocks) {
   for (int s = 0; s < prm.in.nseg; ++s) rows += (static_cast<int>(prm.in.s[s].w) + 3) & ~3;
   std::size_t smem = sizeof(double) * static_cast<std::size_t>(std::max(rows, 4)) * SG;
   if (LT > 0) smem += sizeof(double) * (static_cast<std::size_t>(kCombineWarps) * 8 * SO + 64 * LT * OT);
-  auto kern = combine_kernel<OT, LT, SYM>;
+  // KS: k-steps per input segment (4 covers the <= 16-wide LOBPCG blocks)
+  bool narrow = true;
+  for (int s = 0; s < prm.in.nseg; ++s) narrow = narrow && prm.in.s[s].w <= 16;
+  auto kern = narrow ? combine_kernel<OT, LT, SYM, 4> : combine_kernel<OT, LT, SYM, 12>;
   if (smem > 48 * 1024)
     CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<blocks, 32 * kCombineWarps, smem, ctx->stream>>>(prm);
