@@ -158,6 +158,21 @@ int cieg_shard_plan(const cieg_csb_view* csb, const uint32_t* group_bounds, uint
 int cieg_matrix_upload_shard(cieg_ctx* ctx, const cieg_csb_view* csb, const uint32_t* group_bounds,
                              uint32_t ngroups, uint32_t tile_edge, uint32_t row_lo, uint32_t row_hi,
                              cieg_mat** out);
+/* Single-pass SpMM on a row shard (the transposed-half
+ * partials are reduce-scattered to the row owners): every stored tile of the
+ * shard's rows is read once; y_dev (local rows) gets the row parts and the
+ * transposed parts that land on owned rows, yhalo_dev (rows [lo, hi) of
+ * cieg_matrix_partial_rows, m columns, ld m) the transposed partial sums for
+ * rows owned by lower shards, which the caller sends to their owners and
+ * adds there (dist.py partial_reduce: point to point, added in rank order).
+ * x_dev as for cieg_spmm on a shard (globally addressed, halo rows backed).
+ * On an unsharded matrix: cieg_spmm in single-pass mode (no partial rows).
+ * Replaces the reference's fused-mode planner step (planner.cpp:116-122). */
+int cieg_spmm_partial(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y_dev, uint32_t m,
+                      double* yhalo_dev);
+/* Rows [lo, hi) of the partials cieg_spmm_partial writes (hi = row_lo of the
+ * shard; lo = hi when it has none). */
+int cieg_matrix_partial_rows(const cieg_mat* mat, uint32_t* lo, uint32_t* hi);
 /* Rows owned by a (shard) matrix: [row_lo, row_hi); the full matrix owns all. */
 int cieg_matrix_rows(const cieg_mat* mat, uint32_t* row_lo, uint32_t* row_hi, uint32_t* halo_lo,
                      uint32_t* halo_hi);

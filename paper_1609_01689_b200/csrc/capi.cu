@@ -202,6 +202,7 @@ void upload_schedule(cieg_mat* m, const HostTiles& ht) {
     m->sp_col_off = upload_vec(ht.sp_col_off);
     m->sp_col_items = upload_vec(ht.sp_col_items);
   }
+  m->sp_partial_lo = ht.sp_partial_lo;
 }
 }  // namespace cieg
 
@@ -347,6 +348,41 @@ int cieg_matrix_rows(const cieg_mat* m, uint32_t* row_lo, uint32_t* row_hi, uint
     if (row_hi) *row_hi = m->row_hi;
     if (halo_lo) *halo_lo = m->halo_lo;
     if (halo_hi) *halo_hi = m->halo_hi;
+  });
+}
+
+int cieg_matrix_partial_rows(const cieg_mat* m, uint32_t* lo, uint32_t* hi) {
+  return cieg::guarded([&] {
+    if (!m) cieg::fail(CIEG_ERR_ARGUMENT, "null matrix");
+    if (lo) *lo = m->sp_sched ? m->sp_partial_lo : m->row_lo;
+    if (hi) *hi = m->row_lo;
+  });
+}
+
+int cieg_spmm_partial(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y_dev, uint32_t m,
+                      double* yhalo_dev) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_partial: null handle");
+    if ((!x_dev || !y_dev) && m > 0 && mat->dim > 0) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_partial: null vector");
+    if (x_dev == y_dev && m > 0) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_partial: X and U must not alias");
+    if (!mat->sp_sched) cieg::fail(CIEG_ERR_CONFIG, "cieg_spmm_partial: matrix has no single-pass schedule");
+    const bool shard = mat->row_lo != 0 || mat->row_hi != mat->dim;
+    if (shard) {
+      if (!yhalo_dev && mat->row_lo > mat->sp_partial_lo && m > 0)
+        cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_partial: null partial buffer");
+      double dummy = 0.0;  // a shard without partial rows still takes the single pass
+      cieg::launch_spmm(ctx, mat, x_dev, m, y_dev, m, m, yhalo_dev ? yhalo_dev : &dummy, m);
+    } else {
+      const int saved = ctx->spmm_mode;
+      ctx->spmm_mode = CIEG_SPMM_SINGLE_PASS;
+      try {
+        cieg::launch_spmm(ctx, mat, x_dev, m, y_dev, m, m);
+      } catch (...) {
+        ctx->spmm_mode = saved;
+        throw;
+      }
+      ctx->spmm_mode = saved;
+    }
   });
 }
 

@@ -109,6 +109,7 @@ struct cieg_mat {
   std::uint32_t* sp_sched = nullptr;
   std::uint32_t* sp_col_off = nullptr;
   std::uint32_t* sp_col_items = nullptr;
+  std::uint32_t sp_partial_lo = 0;  // shards: partial rows [sp_partial_lo, row_lo) for lower shards
   // a leading-block view (cieg_matrix_leading_view) borrows panel_start,
   // tile_off, idx and val from its parent and owns only its work lists
   bool borrowed_stream = false;
@@ -126,7 +127,9 @@ struct HostTiles;
 void upload_schedule(cieg_mat* m, const HostTiles& ht);
 
 // Launch the owner-computes SpMM over device X/Y (row-major, ld = ldx/ldy).
+// On a shard, yhalo != nullptr selects the single pass and receives the
+// transposed partials for rows [sp_partial_lo, row_lo) (ld ldh).
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
-                 std::uint32_t ldy, std::uint32_t mcols);
+                 std::uint32_t ldy, std::uint32_t mcols, double* yhalo = nullptr, std::uint32_t ldh = 0);
 
 }  // namespace cieg

@@ -637,8 +637,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 // the order of the (atomic) additions.
 template <typename V>
 __global__ void nonfinite_fix_kernel(const SpmmArgs a, std::uint32_t te, int precision, std::uint32_t p_lo,
-                                     std::uint32_t p_hi, std::uint32_t halo_lo, std::uint32_t halo_hi) {
-  if (*a.nonfinite != a.launch_id) return;
+                                     std::uint32_t p_hi, std::uint32_t halo_lo, std::uint32_t halo_hi, int force) {
+  // force: a single-pass shard -- terms of another shard's tiles reach this
+  // shard's rows through its partials, so K1's flag here does not see them
+  if (!force && *a.nonfinite != a.launch_id) return;
   const std::uint32_t sa = cieg_tl::stride(te, precision);
   const V* val = static_cast<const V*>(a.val);
   const std::uint64_t total = static_cast<std::uint64_t>(halo_hi - halo_lo) * a.mcols;
@@ -678,19 +680,27 @@ __global__ void nonfinite_fix_kernel(const SpmmArgs a, std::uint32_t te, int pre
 
 // Single pass: Y[rows of Q] += sum of the partial slots of block column Q,
 // in the fixed slot order of sp_col_items (deterministic). One CTA per panel.
+// On a shard, block columns below the owned rows (q0 < row_lo) belong to
+// lower shards: their sums go to yhalo (rows from part_lo) for the
+// point-to-point reduction to their owners (dist.py).
 __global__ void sp_reduce_kernel(const double* partial, const std::uint32_t* col_off, const std::uint32_t* col_items,
                                  const std::uint32_t* panel_start, double* y, std::uint32_t ldy, std::uint32_t mcols,
-                                 std::uint32_t td) {
+                                 std::uint32_t td, std::uint32_t row_lo, double* yhalo, std::uint32_t ldh,
+                                 std::uint32_t part_lo) {
   const std::uint32_t Q = blockIdx.x;
   const std::uint32_t k0 = col_off[Q], k1 = col_off[Q + 1];
   if (k0 == k1) return;
   const std::uint32_t q0 = panel_start[Q], rows = panel_start[Q + 1] - q0;
+  const bool own = q0 >= row_lo;
   for (std::uint32_t e = threadIdx.x; e < rows * mcols; e += blockDim.x) {
     const std::uint32_t r = e / mcols, c = e - r * mcols;
     double sum = 0.0;
     for (std::uint32_t k = k0; k < k1; ++k)
       sum += partial[(static_cast<std::size_t>(col_items[k]) * td + r) * mcols + c];
-    y[static_cast<std::size_t>(q0 + r) * ldy + c] += sum;
+    if (own)
+      y[static_cast<std::size_t>(q0 + r - row_lo) * ldy + c] += sum;
+    else
+      yhalo[static_cast<std::size_t>(q0 + r - part_lo) * ldh + c] = sum;
   }
 }
 
@@ -734,7 +744,7 @@ bool use_single_pass(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
     if (e && std::strcmp(e, "single") == 0) return static_cast<int>(CIEG_SPMM_SINGLE_PASS);
     return static_cast<int>(CIEG_SPMM_AUTO);
   }();
-  if (!m->sp_sched || m->row_lo != 0 || m->row_hi != m->dim) return false;
+  if (!m->sp_sched) return false;
   const int mode = ctx->spmm_mode >= 0 ? ctx->spmm_mode : env_mode;
   if (mode != CIEG_SPMM_AUTO) return mode == CIEG_SPMM_SINGLE_PASS;
   return mc <= kSinglePassMaxCols;
@@ -752,8 +762,14 @@ unsigned* nonfinite_flag(cieg_ctx* ctx) {
 }
 
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
-                 std::uint32_t ldy, std::uint32_t mcols) {
+                 std::uint32_t ldy, std::uint32_t mcols, double* yhalo, std::uint32_t ldh) {
   if (mcols == 0 || m->dim == 0) return;
+  const bool shard = m->row_lo != 0 || m->row_hi != m->dim;
+  const bool shard_sp = shard && yhalo != nullptr;
+  if (shard_sp && !m->sp_sched) fail(CIEG_ERR_CONFIG, "single-pass SpMM: the shard has no single-pass schedule");
+  if (shard_sp && m->row_lo > m->sp_partial_lo)  // rows without partials read as zero
+    CIEG_CUDA(cudaMemset2DAsync(yhalo, sizeof(double) * ldh, 0, sizeof(double) * mcols, m->row_lo - m->sp_partial_lo,
+                                ctx->stream));
   for (std::uint32_t c0 = 0; c0 < mcols; c0 += 16) {
     const std::uint32_t mc = std::min<std::uint32_t>(16, mcols - c0);
     SpmmArgs args{m->panel_start,
@@ -776,7 +792,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   nonfinite_flag(ctx),
                   ++ctx->spmm_launch_id,
                   nullptr};
-    const bool sp = use_single_pass(ctx, m, mc);
+    const bool sp = shard ? shard_sp : use_single_pass(ctx, m, mc);
     if (sp) {
       args.sched_off = m->sp_sched_off;
       args.sched = reinterpret_cast<const uint4*>(m->sp_sched);
@@ -793,7 +809,8 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
     }
     if (sp) {
       sp_reduce_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
-                                                            m->panel_start, y + c0, ldy, mc, m->tile_edge);
+                                                            m->panel_start, y + c0, ldy, mc, m->tile_edge, m->row_lo,
+                                                            shard_sp ? yhalo + c0 : nullptr, ldh, m->sp_partial_lo);
       CIEG_CUDA(cudaGetLastError());
       ++ctx->launches;
     }
@@ -804,10 +821,10 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
     const int prec = m->precision;
     if (prec == 0)
       nonfinite_fix_kernel<float><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
-                                                                          m->halo_lo, m->halo_hi);
+                                                                          m->halo_lo, m->halo_hi, shard_sp ? 1 : 0);
     else
       nonfinite_fix_kernel<double><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
-                                                                           m->halo_lo, m->halo_hi);
+                                                                           m->halo_lo, m->halo_hi, shard_sp ? 1 : 0);
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
   }

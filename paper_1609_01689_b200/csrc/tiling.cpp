@@ -301,7 +301,7 @@ void build_schedule(HostTiles& t, std::uint32_t ctas) {
   t.sp_sched.clear();
   t.sp_col_off.clear();
   t.sp_col_items.clear();
-  if (t.row_lo != 0 || t.row_hi != t.dim) return;  // shards: owner-computes only
+  t.sp_partial_lo = t.row_lo;
   assign_items(t, ctas, p_lo, p_hi, true, t.sp_sched_off, t.sp_sched);
   // partial slots per block column, in item order (a fixed order: deterministic sums)
   const std::uint32_t np = t.npanels();
@@ -315,7 +315,10 @@ void build_schedule(HostTiles& t, std::uint32_t ctas) {
   }
   t.sp_col_off.assign(np + 1, 0);
   for (std::uint32_t qv : q_of)
-    if (qv < np) ++t.sp_col_off[qv + 1];
+    if (qv < np) {
+      ++t.sp_col_off[qv + 1];
+      t.sp_partial_lo = std::min(t.sp_partial_lo, t.panel_start[qv]);  // block columns below the shard
+    }
   for (std::uint32_t Q = 0; Q < np; ++Q) t.sp_col_off[Q + 1] += t.sp_col_off[Q];
   t.sp_col_items.resize(t.sp_col_off[np]);
   std::vector<std::uint32_t> fill(t.sp_col_off.begin(), t.sp_col_off.end() - 1);

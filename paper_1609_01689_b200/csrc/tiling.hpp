@@ -51,6 +51,9 @@ struct HostTiles {
   // transposed product Aᵀ X_pi goes to partial slot = its item index; the
   // slots feeding block column Q are sp_col_items[sp_col_off[Q] .. sp_col_off[Q+1]).
   std::vector<std::uint32_t> sp_sched_off, sp_sched, sp_col_off, sp_col_items;
+  // shards: first row of the transposed partials for rows of lower shards
+  // (rows [sp_partial_lo, row_lo); = row_lo when there are none)
+  std::uint32_t sp_partial_lo = 0;
 
   // owner rows of this (shard) tiling and the X rows its SpMM reads
   std::uint32_t row_lo = 0, row_hi = 0, halo_lo = 0, halo_hi = 0;

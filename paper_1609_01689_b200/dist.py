@@ -143,6 +143,87 @@ def halo_exchange(x_local: torch.Tensor, plan: ExchangePlan, out: torch.Tensor, 
     return out
 
 
+class PartialPlan:
+    """The reverse of the halo exchange for the single-pass SpMM
+    (cieg_spmm_partial): every rank holds transposed partial sums for rows
+    [part_lo, row_lo) owned by lower ranks. sends[(peer, a, b)] = rows of
+    peer inside this rank's partial range; recvs[(peer, a, b)] = this rank's
+    rows inside peer's partial range (peers above this rank)."""
+
+    def __init__(self, row_bounds, part_lo, rank: int):
+        world = len(row_bounds) - 1
+        self.rank = rank
+        self.lo, self.hi = int(row_bounds[rank]), int(row_bounds[rank + 1])
+        self.part_lo = int(part_lo[rank])
+        self.sends, self.recvs = [], []
+        for s in range(world):
+            if s < rank:  # rows of a lower owner inside my partial range
+                a, b = max(int(row_bounds[s]), self.part_lo), min(int(row_bounds[s + 1]), self.lo)
+                if b > a:
+                    self.sends.append((s, a, b))
+            elif s > rank:  # my rows inside a higher rank's partial range
+                a, b = max(self.lo, int(part_lo[s])), min(self.hi, int(row_bounds[s]))
+                if b > a:
+                    self.recvs.append((s, a, b))
+
+    def recv_rows(self) -> int:
+        return sum(b - a for _, a, b in self.recvs)
+
+    def send_rows(self) -> int:
+        return sum(b - a for _, a, b in self.sends)
+
+
+def gather_partial_lo(part_lo: int, device, group=None):
+    world = dist.get_world_size(group)
+    mine = torch.tensor([part_lo], dtype=torch.int64, device=device)
+    allp = [torch.zeros(1, dtype=torch.int64, device=device) for _ in range(world)]
+    dist.all_gather(allp, mine, group=group)
+    return torch.cat(allp).cpu().numpy()
+
+
+def partial_reduce(yhalo: torch.Tensor, plan: PartialPlan, y_local: torch.Tensor, group=None) -> torch.Tensor:
+    """Send this rank's partial rows to their owners and add the partials
+    received for its own rows: point to point (one batched isend/irecv
+    round), added in ascending peer order -- deterministic for a fixed
+    partition. yhalo[i] holds global row plan.part_lo + i."""
+    staged = y_local.is_cuda and dist.get_backend(group) == "gloo"  # gloo moves host tensors only
+    src = yhalo.cpu() if staged else yhalo
+    bufs = [(peer, a, b, torch.empty((b - a,) + tuple(y_local.shape[1:]), dtype=y_local.dtype,
+                                      device="cpu" if staged else y_local.device))
+            for peer, a, b in sorted(plan.recvs)]
+    ops = [dist.P2POp(dist.irecv, t, peer if group is None else dist.get_global_rank(group, peer), group)
+           for peer, a, b, t in bufs]
+    ops += [dist.P2POp(dist.isend, src[a - plan.part_lo:b - plan.part_lo].contiguous(),
+                       peer if group is None else dist.get_global_rank(group, peer), group)
+            for peer, a, b in plan.sends]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    for peer, a, b, t in bufs:  # ascending peer order
+        y_local[a - plan.lo:b - plan.lo] += t.to(y_local.device)
+    return y_local
+
+
+def spmm_single_pass(handle, device: ci.Device, x_full: torch.Tensor, y_local: torch.Tensor, plan: PartialPlan,
+                     group=None) -> torch.Tensor:
+    """H X on a shard in the single pass (cieg_spmm_partial): the local rows
+    plus the transposed partials the higher ranks send (x_full: globally
+    addressed, halo rows filled)."""
+    m = x_full.shape[1]
+    yhalo = torch.empty((max(plan.lo - plan.part_lo, 1), m), dtype=torch.float64, device=y_local.device)
+    torch.cuda.current_stream().synchronize()
+    ci._check(_lib.load().cieg_spmm_partial(device.handle, handle, C.c_void_p(x_full.data_ptr()),
+                                            C.c_void_p(y_local.data_ptr()), m, C.c_void_p(yhalo.data_ptr())))
+    device.synchronize()
+    return partial_reduce(yhalo, plan, y_local, group)
+
+
+def partial_rows(handle):
+    lo, hi = C.c_uint32(), C.c_uint32()
+    ci._check(_lib.load().cieg_matrix_partial_rows(handle, C.byref(lo), C.byref(hi)))
+    return lo.value, hi.value
+
+
 def allreduce_sum_(t: torch.Tensor, group=None) -> torch.Tensor:
     dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
     return t
@@ -195,10 +276,12 @@ class ShardedMatrix:
     def halo(self):
         return int(self.halo_lo[self.rank]), int(self.halo_hi[self.rank])
 
-    def spmm(self, x_local: torch.Tensor, group=None, exchange: str = "halo") -> torch.Tensor:
+    def spmm(self, x_local: torch.Tensor, group=None, exchange: str = "halo", mode: str = "owner") -> torch.Tensor:
         """Rows [row_lo, row_hi) of H X from the rank's rows of X (the halo
         rows of X arrive point to point; exchange="allgather" for the
-        all-gather variant)."""
+        all-gather variant). mode="single": the single pass, whose
+        transposed partials for lower ranks' rows go back point to point
+        (collective: every rank calls it)."""
         m = x_local.shape[1]
         full = torch.empty((self.h.dim, m), dtype=torch.float64, device=x_local.device)
         if exchange == "halo":
@@ -206,6 +289,11 @@ class ShardedMatrix:
         else:
             allgather_rows(x_local, self.row_bounds, full, group)
         y = torch.empty((self.local_rows, m), dtype=torch.float64, device=x_local.device)
+        if mode == "single":
+            if getattr(self, "partial_plan", None) is None:
+                plo = gather_partial_lo(partial_rows(self.handle)[0], x_local.device, group)
+                self.partial_plan = PartialPlan(self.row_bounds, plo, self.rank)
+            return spmm_single_pass(self.handle, self.device, full, y, self.partial_plan, group)
         torch.cuda.current_stream().synchronize()
         ci._check(_lib.load().cieg_spmm(self.device.handle, self.handle, C.c_void_p(full.data_ptr()),
                                         C.c_void_p(y.data_ptr()), m))

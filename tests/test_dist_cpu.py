@@ -193,3 +193,71 @@ def test_gloo_halo_exchange(world):
         assert "error" not in out[r], out[r].get("error")
         assert out[r]["gather_ok"] and out[r]["halo_ok"] and out[r]["outside_untouched"]
     assert sum(out[r]["recv_rows"] for r in range(world)) == sum(out[r]["send_rows"] for r in range(world))
+
+
+def _partial_worker(rank, world, port, out_q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01689_b200 import dist as D
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        # rows 0..99 in uneven shards; each rank's partial range reaches two shards down
+        rb = [0, 17, 40, 71, 100][: world + 1]
+        rb[-1] = 100
+        plo = [max(0, rb[r] - 30) if r > 0 else 0 for r in range(world)]
+        plan = D.PartialPlan(rb, plo, rank)
+        gl = D.gather_partial_lo(plo[rank], torch.device("cpu"))
+        res["gather_ok"] = gl.tolist() == plo
+        lo, hi = rb[rank], rb[rank + 1]
+
+        def f(r, rows, m=3):  # rank r's partial for global rows
+            rows = np.asarray(rows, dtype=np.float64)[:, None]
+            return r * 1000.0 + rows + 0.25 * np.arange(m)[None, :]
+
+        yhalo = torch.from_numpy(f(rank, range(plo[rank], lo))) if lo > plo[rank] else torch.zeros((1, 3))
+        y = torch.from_numpy(np.full((hi - lo, 3), 0.5))
+        D.partial_reduce(yhalo, plan, y)
+        want = np.full((hi - lo, 3), 0.5)
+        for t in range(rank + 1, world):  # ascending peers
+            a, b = max(lo, plo[t]), min(hi, rb[t])
+            if b > a:
+                want[a - lo:b - lo] += f(t, range(a, b))
+        res["ok"] = bool(np.array_equal(y.numpy(), want))
+        res["sent"] = plan.send_rows()
+        res["recv"] = plan.recv_rows()
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        res["error"] = repr(e) + traceback.format_exc()
+    finally:
+        dist.destroy_process_group()
+    out_q.put((rank, res))
+
+
+@pytest.mark.parametrize("world", [3, 4])
+def test_gloo_partial_reduce(world):
+    """Reverse exchange of the single-pass SpMM (transposed
+    partials back to the row owners): every owner ends with its rows plus
+    the partials of every higher rank, added in ascending rank order
+    (exactly reproducible), and sent rows equal received rows overall."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_partial_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert "error" not in out[r], out[r].get("error")
+        assert out[r]["gather_ok"] and out[r]["ok"]
+    assert sum(out[r]["sent"] for r in range(world)) == sum(out[r]["recv"] for r in range(world))

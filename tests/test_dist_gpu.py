@@ -53,6 +53,8 @@ def _worker(rank, world, port, backend, name, out_q):
         y = sm.spmm(torch.from_numpy(x[sm.row_lo:sm.row_hi].copy()).cuda()).cpu().numpy()
         yf = ci.spmm(h, x)[sm.row_lo:sm.row_hi]
         res["spmm_rel"] = float(np.abs(y - yf).max() / np.abs(yf).max())
+        ys = sm.spmm(torch.from_numpy(x[sm.row_lo:sm.row_hi].copy()).cuda(), mode="single").cpu().numpy()
+        res["spmm_single_rel"] = float(np.abs(ys - yf).max() / np.abs(yf).max())
         rep = D.lobpcg_solve_dist(sm, x0, ci.LobpcgOptions(k_want=int(k), tol=float(tol)), prec)
         res["iterations"] = rep.iterations
         res["eigenvalues"] = rep.eigenvalues.tolist()
@@ -94,6 +96,7 @@ def test_sharded_solver_matches_reference(golden, world, backend, name):
         res = out[rank]
         assert "error" not in res, res.get("error")
         assert res["spmm_rel"] < 1e-13
+        assert res["spmm_single_rel"] < 1e-13
         assert res["iterations"] == int(g[f"{name}_iterations"])
         assert res["counters"] == g[f"{name}_counters"].tolist()
         np.testing.assert_allclose(res["eigenvalues"], g[f"{name}_eigenvalues"], rtol=1e-10)
@@ -166,3 +169,84 @@ def test_generated_shards_solver_matches_single_gpu():
         np.testing.assert_allclose(out[r]["eigenvalues"], single.eigenvalues, rtol=1e-10)
     assert out[0]["rows"] + out[1]["rows"] == cfg.n
     assert out[0]["eigenvalues"] == out[1]["eigenvalues"]
+
+
+def _single_pass_shards(h, world, m, x):
+    """Every shard of a world-`world` partition in this process: the
+    single-pass kernel (cieg_spmm_partial) per shard, then the reverse
+    exchange done on the host exactly as dist.partial_reduce orders it."""
+    import ctypes as C
+
+    import torch
+
+    from paper_1609_01689_b200 import _lib, ci
+    from paper_1609_01689_b200 import dist as D
+
+    dev = ci.Device.default()
+    rb, hl, hh = D.row_partition(h, world)
+    xs = torch.from_numpy(x).cuda()
+    ys, halos = [], []
+    for r in range(world):
+        sm = D.ShardedMatrix(h, r, world, dev, plan=(rb, hl, hh))
+        plo, phi = D.partial_rows(sm.handle)
+        assert phi == sm.row_lo and plo <= phi
+        y = torch.empty((sm.local_rows, m), dtype=torch.float64, device="cuda")
+        yh = torch.full((max(phi - plo, 1), m), float("nan"), dtype=torch.float64, device="cuda")
+        ci._check(_lib.load().cieg_spmm_partial(dev.handle, sm.handle, C.c_void_p(xs.data_ptr()),
+                                                C.c_void_p(y.data_ptr()), m, C.c_void_p(yh.data_ptr())))
+        dev.synchronize()
+        ys.append(y.cpu().numpy())
+        halos.append((plo, yh.cpu().numpy()[: phi - plo]))
+    out = np.zeros((h.dim, m))
+    for r in range(world):
+        lo, hi = int(rb[r]), int(rb[r + 1])
+        yr = ys[r].copy()
+        for t in range(r + 1, world):
+            plo, yh = halos[t]
+            a, b = max(lo, plo), min(hi, int(rb[t]))
+            if b > a:
+                yr[a - lo:b - lo] += yh[a - plo:b - plo]
+        out[lo:hi] = yr
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("mat", ["f64_t64", "f32_t128"])
+@pytest.mark.parametrize("m", [1, 5, 16])
+def test_single_pass_shards_match_reference(world, mat, m):
+    """each shard reads its stored tiles once; the transposed
+    partials for lower shards' rows are reduced at their owners. The
+    assembled product equals the reference's spmm."""
+    from conftest import gen_from
+
+    from oracle import ci_oracle as O
+    from paper_1609_01689_b200 import ci
+
+    params = {"f64_t64": (20_000, 10, 64, 0.05, 0.5, 1, 1, 2000),
+              "f32_t128": (30_000, 3, 256, 0.02, 0.4, 77, 0, 2000)}[mat]
+    h = gen_from(params)
+    x = ci.random_block(h.dim, m, 11 + m)
+    y = _single_pass_shards(h, world, m, x)
+    want = O.spmm(h, x)
+    assert np.abs(y - want).max() / np.abs(want).max() < 1e-13
+
+
+def test_single_pass_shards_nonfinite():
+    """Inf / NaN rows feeding other shards' rows through the partials: the
+    receiving owner's fix-up adds those terms (same pattern as the reference)."""
+    from conftest import gen_from
+
+    from oracle import ci_oracle as O
+    from paper_1609_01689_b200 import ci
+
+    h = gen_from((3072, 3, 256, 0.2, 0.4, 13, 0, 2000))
+    x = ci.random_block(h.dim, 4, 5)
+    x[2100, 1] = np.inf
+    x[1030, 2] = np.nan
+    x[2900, 3] = -np.inf
+    y = _single_pass_shards(h, 2, 4, x)
+    yo = O.spmm(h, x)
+    for mask in (np.isnan, np.isposinf, np.isneginf):
+        assert np.array_equal(mask(y), mask(yo))
+    fin = np.isfinite(yo)
+    np.testing.assert_allclose(y[fin], yo[fin], rtol=1e-12, atol=1e-12)
