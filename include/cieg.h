@@ -196,6 +196,13 @@ typedef struct {
    * memory -- the only rows the shard's kernel reads. dist.py fills them by
    * a point-to-point halo exchange. */
   int (*allgather_rows)(void* user, const double* x_local_dev, uint32_t m, double* x_full_dev);
+  /* optional (NULL: owner-computes shards). After a single-pass SpMM (the
+   * SpMM mode's width rule, cieg_ctx_set_spmm_mode): send the transposed
+   * partials for lower ranks' rows (yhalo_dev, rows [lo, hi) of
+   * cieg_matrix_partial_rows, m columns) to their owners and add the ones
+   * received into y_local_dev (local_rows x m) in ascending rank order --
+   * the reduce-scatter of SURVEY.md 8(e), point to point. */
+  int (*reduce_partials)(void* user, const double* yhalo_dev, uint32_t m, double* y_local_dev);
 } cieg_dist_hooks;
 
 /* ---- tall-skinny block kernels (proj/include/ci/block_vectors.hpp) ----- */

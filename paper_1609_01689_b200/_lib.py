@@ -76,8 +76,12 @@ ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_uint6
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p)
 
 
+PARTIALS_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p)
+
+
 class DistHooks(C.Structure):
-    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE_FN), ("allgather_rows", ALLGATHER_FN)]
+    _fields_ = [("user", C.c_void_p), ("allreduce_sum", ALLREDUCE_FN), ("allgather_rows", ALLGATHER_FN),
+                ("reduce_partials", PARTIALS_FN)]
 
 
 OBSERVER = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.POINTER(C.c_double), C.c_uint32,

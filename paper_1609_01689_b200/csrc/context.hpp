@@ -122,6 +122,10 @@ namespace cieg {
 // once on every freshly built device tile stream.
 void order_tile_entries(cieg_ctx* ctx, cieg_mat* m);
 
+// The SpMM mode's choice for block width mc on a matrix with a single-pass
+// schedule (auto: single pass for mc <= 8).
+bool single_pass_default(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
+
 // Upload the work lists and both K1 schedules of a tiling.
 struct HostTiles;
 void upload_schedule(cieg_mat* m, const HostTiles& ht);

@@ -217,6 +217,17 @@ class Solver {
       if (hooks_->allgather_rows(hooks_->user, x.p, x.w, full) != 0)
         fail(CIEG_ERR_ARGUMENT, "allgather_rows hook failed");
       xin = full;
+      if (hooks_->reduce_partials && single_pass_default(ctx_, mat_, x.w)) {
+        // single pass: the transposed partials for lower ranks' rows travel
+        // back to their owners (SURVEY.md 8(e) reduce-scatter, point to point)
+        const std::size_t prow = mat_->row_lo - mat_->sp_partial_lo;
+        double* yh = static_cast<double*>(yhalo_.get(sizeof(double) * std::max<std::size_t>(1, prow) * w));
+        launch_spmm(ctx_, mat_, xin, x.w, hx.p, x.w, x.w, yh, x.w);
+        if (hooks_->reduce_partials(hooks_->user, yh, x.w, hx.p) != 0)
+          fail(CIEG_ERR_ARGUMENT, "reduce_partials hook failed");
+        hx.w = x.w;
+        return;
+      }
     }
     launch_spmm(ctx_, mat_, xin, x.w, hx.p, x.w, x.w);
     hx.w = x.w;
@@ -233,7 +244,7 @@ class Solver {
   std::uint32_t n_;  // local rows (all rows unless sharded)
   const cieg_dist_hooks* hooks_;
   GramOps ops_;
-  DevBuf xfull_;
+  DevBuf xfull_, yhalo_;
   Workspace ws_;
   Block x_, hx_, p_, hp_, x2_, hx2_, p2_, hp2_, w_, hw_, wtmp_, r_, wsrc_;
   std::vector<double> theta_;

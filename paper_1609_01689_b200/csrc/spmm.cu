@@ -737,7 +737,9 @@ void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::ui
 // (profiles/README.md): single pass 2.73 / 2.99 / 5.03 ms at m = 1 / 8 / 16
 // vs owner-computes 3.65 / 3.71 / 4.72 ms.
 constexpr std::uint32_t kSinglePassMaxCols = 8;
-bool use_single_pass(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
+}  // namespace
+
+bool single_pass_default(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
   static const int env_mode = [] {
     const char* e = std::getenv("CIEG_SPMM_MODE");
     if (e && std::strcmp(e, "owner") == 0) return static_cast<int>(CIEG_SPMM_OWNER);
@@ -750,7 +752,6 @@ bool use_single_pass(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
   return mc <= kSinglePassMaxCols;
 }
 
-}  // namespace
 
 // The non-finite flag: zeroed once when allocated; each K1 launch tags it
 // with its own launch id, so it never needs a reset (launch ids start at 1).
@@ -792,7 +793,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   nonfinite_flag(ctx),
                   ++ctx->spmm_launch_id,
                   nullptr};
-    const bool sp = shard ? shard_sp : use_single_pass(ctx, m, mc);
+    const bool sp = shard ? shard_sp : single_pass_default(ctx, m, mc);
     if (sp) {
       args.sched_off = m->sp_sched_off;
       args.sched = reinterpret_cast<const uint4*>(m->sp_sched);

@@ -368,11 +368,15 @@ def local_tile_diagonal(h: ci.CsbMatrix, row_lo: int, row_hi: int, device: ci.De
 
 
 def lobpcg_solve_dist(sm, x0_local: np.ndarray, options: ci.LobpcgOptions,
-                      precond: Optional[ci.TileDiagonal] = None, group=None) -> ci.SolveReport:
+                      precond: Optional[ci.TileDiagonal] = None, group=None,
+                      single_pass: bool = True) -> ci.SolveReport:
     """Sharded ci::lobpcg_solve on a ShardedMatrix (host CSB uploaded by
     rows) or a DeviceShard (generated on the GPU). x0_local = the rank's rows
     of X0. The report's trial vectors are the rank's rows; eigenvalues,
-    history and counters are global (identical on every rank)."""
+    history and counters are global (identical on every rank).
+    single_pass: SpMMs of the single-pass widths (the SpMM mode's rule) use
+    the single pass with the partials reduced at their owners; False keeps
+    every SpMM owner-computes."""
     lib = _lib.load()
     dev = sm.device
     tdev = torch.device("cuda", dev.index)
@@ -406,10 +410,24 @@ def lobpcg_solve_dist(sm, x0_local: np.ndarray, options: ci.LobpcgOptions,
         except Exception:  # noqa: BLE001
             return 1
 
+    # single-pass SpMM widths: transposed partials back to their owners
+    plo = gather_partial_lo(partial_rows(sm.handle)[0], tdev, group)
+    pplan = PartialPlan(sm.row_bounds, plo, dist.get_rank(group))
+
+    def _partials(_user, yhptr, m, yptr):
+        try:
+            yl = _view(yptr, (sm.local_rows, m), tdev)
+            yh = _view(yhptr, (max(pplan.lo - pplan.part_lo, 1), m), tdev)
+            partial_reduce(yh, pplan, yl, group)
+            return 0
+        except Exception:  # noqa: BLE001
+            return 1
+
     hooks = _lib.DistHooks()
     hooks.user = None
     hooks.allreduce_sum = _lib.ALLREDUCE_FN(_allreduce)
     hooks.allgather_rows = _lib.ALLGATHER_FN(_allgather)
+    hooks.reduce_partials = _lib.PARTIALS_FN(_partials) if single_pass else _lib.PARTIALS_FN()
     opt = _lib.LobpcgOptionsC()
     opt.k_want, opt.tol, opt.max_iter = options.k_want, options.tol, options.max_iter
     opt.precond_config = options.precond_config.c()
