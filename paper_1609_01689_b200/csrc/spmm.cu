@@ -37,6 +37,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <cstdint>
 
 #include "context.hpp"
@@ -288,6 +289,126 @@ __device__ __forceinline__ void transposed_product(const SpmmArgs& a, const V* T
   }
 }
 
+// Single pass at m <= 2 (SCM = m): a scalar FP64 consumer. The n8 DMMA
+// would spend 4-8x the useful flops on one or two columns; here every
+// consumer warp reads its TD / 8 tile rows once per item (one vector load
+// per row covers the row: PPL positions per lane) and forms both products
+// from the same registers: the row part into per-lane partials that persist
+// over the owner's items (lane-reduced in a fixed xor tree at the owner's
+// end), the transposed part against the owner slab (per-lane partials over
+// the warp's rows, combined across warps in warp order through shared
+// memory). Deterministic. Positions are the permuted tile columns
+// (tile_layout.h), so the partner slab is read at unperm(position).
+template <typename V, int TD, int NT, int SCM, int HANDOFF>
+__device__ __forceinline__ void scalar_consumer(const SpmmArgs& a, unsigned char* smem, std::uint32_t i_beg,
+                                                std::uint32_t i_end, int cw, int lane, int tid) {
+  using S = Shape<V, TD, NT>;
+  constexpr int RPW = TD / kConsumerWarps;  // tile rows per consumer warp
+  constexpr int PPL = TD / 32;              // tile positions per lane
+  constexpr int prec = sizeof(V) == 4 ? 0 : 1;
+  using VecT = typename std::conditional<sizeof(V) * PPL == 16, typename std::conditional<sizeof(V) == 4, float4, double2>::type, float2>::type;
+  static_assert(sizeof(VecT) == sizeof(V) * PPL, "one vector load per row and lane");
+  double* oslab = reinterpret_cast<double*>(smem + 2 * S::kTileBytes + 2 * S::kSlabBytes);
+  double* red = oslab + TD * S::kSX;  // [kConsumerWarps][TD][SCM]
+  const int p0 = PPL * lane;
+  int col[PPL];
+#pragma unroll
+  for (int k = 0; k < PPL; ++k) col[k] = static_cast<int>(cieg_tl::unperm(static_cast<std::uint32_t>(p0 + k), prec));
+  const int r_base = cw * RPW;
+  const int mc = static_cast<int>(a.mcols);
+  bar_arrive(kBarEmpty0 + 0, HANDOFF);
+  bar_arrive(kBarEmpty0 + 1, HANDOFF);
+  int buf = 0;
+  double racc[RPW][SCM];
+  Item it = load_item(a, i_beg);
+  for (std::uint32_t i = i_beg; i < i_end; ++i) {
+    const Item nit = (i + 1 < i_end) ? load_item(a, i + 1) : it;
+    if (it.first()) {
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+        for (int j = 0; j < SCM; ++j) racc[rr][j] = 0.0;
+      bar_sync(kBarConsumers, kConsumerThreads);  // every warp is done with the previous owner's slab
+      bool bad = false;
+      for (int e = tid - kProducerThreads; e < TD * 8 * NT; e += kConsumerThreads) {
+        const int k = e / (8 * NT), t = e - k * (8 * NT);
+        double v = (k < it.prow() && t < mc) ? __ldg(a.x + static_cast<std::size_t>(it.r0 + k) * a.ldx + t) : 0.0;
+        if (!isfinite(v)) {  // staged as 0; nonfinite_fix_kernel adds its terms
+          v = 0.0;
+          bad = true;
+        }
+        oslab[k * S::kSX + t] = v;
+      }
+      if (bad) *a.nonfinite = a.launch_id;
+      bar_sync(kBarConsumers, kConsumerThreads);
+    }
+    bar_sync(kBarFull0 + buf, HANDOFF);
+    const V* A = reinterpret_cast<const V*>(smem + buf * S::kTileBytes);
+    const double* X = reinterpret_cast<const double*>(smem + 2 * S::kTileBytes + buf * S::kSlabBytes);
+    const bool trans = it.kind() == 0u;
+    double xq[PPL][SCM], tacc[PPL][SCM];
+#pragma unroll
+    for (int k = 0; k < PPL; ++k)
+#pragma unroll
+      for (int j = 0; j < SCM; ++j) {
+        xq[k][j] = X[col[k] * S::kSX + j];
+        tacc[k][j] = 0.0;
+      }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      const int r = r_base + rr;
+      const VecT vv = *reinterpret_cast<const VecT*>(A + r * S::kSA + p0);
+      const V* av = reinterpret_cast<const V*>(&vv);
+      double ad[PPL];
+#pragma unroll
+      for (int k = 0; k < PPL; ++k) ad[k] = static_cast<double>(av[k]);
+#pragma unroll
+      for (int k = 0; k < PPL; ++k)
+#pragma unroll
+        for (int j = 0; j < SCM; ++j) racc[rr][j] = fma(ad[k], xq[k][j], racc[rr][j]);
+      if (trans) {
+#pragma unroll
+        for (int j = 0; j < SCM; ++j) {
+          const double xp = oslab[r * S::kSX + j];
+#pragma unroll
+          for (int k = 0; k < PPL; ++k) tacc[k][j] = fma(ad[k], xp, tacc[k][j]);
+        }
+      }
+    }
+    if (i + 2 < i_end) bar_arrive(kBarEmpty0 + buf, HANDOFF);
+    buf ^= 1;
+    if (trans) {
+#pragma unroll
+      for (int k = 0; k < PPL; ++k)
+#pragma unroll
+        for (int j = 0; j < SCM; ++j) red[(cw * TD + col[k]) * SCM + j] = tacc[k][j];
+      bar_sync(kBarConsumers, kConsumerThreads);
+      double* out = a.partial + static_cast<std::size_t>(i) * TD * mc;
+      for (int e = tid - kProducerThreads; e < TD * SCM; e += kConsumerThreads) {
+        const int c = e / SCM, j = e - c * SCM;
+        if (c >= it.orow || j >= mc) continue;
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) sum += red[(w * TD + c) * SCM + j];
+        out[c * mc + j] = sum;
+      }
+      bar_sync(kBarConsumers, kConsumerThreads);  // red free for the next item
+    }
+    if (it.last()) {
+#pragma unroll
+      for (int rr = 0; rr < RPW; ++rr)
+#pragma unroll
+        for (int j = 0; j < SCM; ++j) {
+          const double v = warp_sum(racc[rr][j]);
+          const int r = r_base + rr;
+          if (lane == 0 && r < it.prow() && j < mc)
+            a.y[static_cast<std::size_t>(it.r0 - a.row_base + r) * a.ldy + j] = v;
+        }
+    }
+    it = nit;
+  }
+}
+
 // SP = false: owner-computes -- an off-diagonal tile is streamed twice, once
 // per owner panel (row part into P, transposed part into Q), each output
 // row summed in registers by its owner. SP = true: single pass -- one item
@@ -295,7 +416,7 @@ __device__ __forceinline__ void transposed_product(const SpmmArgs& a, const V* T
 // (X_P, the owner panel's slab, staged once per owner) and store it to the
 // item's partial slot, added to block column Q by sp_reduce_kernel in a
 // fixed order. Both are deterministic.
-template <typename V, int TD, int NT, bool SP>
+template <typename V, int TD, int NT, bool SP, int SCM = 0>
 __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) {
   using S = Shape<V, TD, NT>;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -500,6 +621,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       }
       if (nonfinite) *a.nonfinite = a.launch_id;
     }
+  } else if constexpr (SCM > 0) {
+    scalar_consumer<V, TD, NT, SCM, kHandoff>(a, smem, i_beg, i_end, warp - kProducerWarps, lane, tid);
   } else {
     // ------------------------------------------------------------ consumer
     const int cw = warp - kProducerWarps;
@@ -704,12 +827,13 @@ __global__ void sp_reduce_kernel(const double* partial, const std::uint32_t* col
   }
 }
 
-template <typename V, int TD, int NT, bool SP>
+template <typename V, int TD, int NT, bool SP, int SCM = 0>
 void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   using S = Shape<V, TD, NT>;
-  constexpr std::size_t smem = SP ? S::kSmemSP : S::kSmem;
+  constexpr std::size_t smem =
+      (SP ? S::kSmemSP : S::kSmem) + sizeof(double) * kConsumerWarps * TD * SCM;  // SCM: warp partials
   static_assert(smem <= 227 * 1024, "shared memory budget");
-  auto kern = spmm_ws_kernel<V, TD, NT, SP>;
+  auto kern = spmm_ws_kernel<V, TD, NT, SP, SCM>;
   CIEG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   kern<<<SP ? m->sp_ctas : m->sched_ctas, kThreads, smem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
@@ -719,7 +843,11 @@ void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
 template <typename V, int TD>
 void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::uint32_t mc, bool sp) {
   if (sp) {
-    if (mc <= 8)
+    if (mc == 1)
+      launch_variant<V, TD, 1, true, 1>(ctx, m, args);
+    else if (mc == 2)
+      launch_variant<V, TD, 1, true, 2>(ctx, m, args);
+    else if (mc <= 8)
       launch_variant<V, TD, 1, true>(ctx, m, args);
     else
       launch_variant<V, TD, 2, true>(ctx, m, args);
@@ -734,8 +862,8 @@ void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::ui
 // K1 mode (cieg_ctx_set_spmm_mode; else CIEG_SPMM_MODE=owner|single; else
 // auto): single pass for block widths <= kSinglePassMaxCols on full
 // (unsharded) matrices, owner-computes otherwise. Measured on config 2
-// (profiles/README.md): single pass 2.73 / 2.99 / 5.03 ms at m = 1 / 8 / 16
-// vs owner-computes 3.65 / 3.71 / 4.72 ms.
+// (profiles/README.md): single pass 2.14 / 2.99 / 5.03 ms at m = 1 / 8 / 16
+// (scalar consumer at m <= 2) vs owner-computes 3.65 / 3.71 / 4.72 ms.
 constexpr std::uint32_t kSinglePassMaxCols = 8;
 }  // namespace
 
