@@ -560,6 +560,57 @@ def widths_record(dev, dm, stream, n):
     return {"workload": "cfg2-spmm K1 by block width", "points": out}
 
 
+def shard_modes_record(dev, dm, plan, row_bounds, rank, n, tdev, stream, m=8):
+    """N > 1, config 2 at m = 8 on the same shards: owner-computes K1 after
+    the X halo exchange vs the single pass, whose transposed partials for
+    lower ranks' rows go back point to point (SURVEY.md 8(e) reduce-scatter)
+    -- per step, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01689_b200 import ci, configs
+    from paper_1609_01689_b200 import dist as D
+
+    try:
+        lo, hi = int(row_bounds[rank]), int(row_bounds[rank + 1])
+        x_full = torch.from_numpy(ci.random_block(n, m, 8)).to(tdev)
+        x_local = x_full[lo:hi].clone()
+        y = torch.empty((hi - lo, m), dtype=torch.float64, device=tdev)
+        pplan = D.PartialPlan(row_bounds, D.gather_partial_lo(D.partial_rows(dm.handle)[0], tdev), rank)
+
+        def owner():
+            D.halo_exchange(x_local, plan, x_full)
+            dm.spmm_ptr(x_full.data_ptr(), y.data_ptr(), m)
+
+        def single():
+            D.halo_exchange(x_local, plan, x_full)
+            D.spmm_single_pass(dm.handle, dev, x_full, y, pplan)
+
+        def timed(fn, k=5):
+            for _ in range(2):
+                fn()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(k):
+                fn()
+            e1.record(stream)
+            e1.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) / k], device=tdev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            return float(t.item())
+
+        ms_o, ms_s = timed(owner), timed(single)
+        nnz = int(configs.CFG2.expected_nnz())
+        nb = configs.spmm_bytes(nnz, n, m, 0)
+        return {"m": m, "owner_ms": round(ms_o, 3), "single_pass_ms": round(ms_s, 3),
+                "owner_gbs": round(nb / (ms_o * 1e-3) / 1e9, 1), "single_pass_gbs": round(nb / (ms_s * 1e-3) / 1e9, 1),
+                "partial_rows_sent": pplan.send_rows(), "partial_rows_received": pplan.recv_rows()}
+    except Exception as e:  # reported in the line; the headline stands
+        return {"error": repr(e)[:400]}
+
+
 def group_bounds(cfg):
     """Generator tile (= group) starts, the rule of generator.cpp make_grid."""
     out = []
@@ -691,6 +742,7 @@ def ours(args):
         flops = configs.spmm_flops(nnz_total, n, m)
     gbs = nbytes / (ms * 1e-3) / 1e9
     widths = widths_record(dev, dm, stream, n) if world == 1 else None
+    shard_modes = shard_modes_record(dev, dm, plan, row_bounds, rank, n, tdev, stream) if world > 1 else None
     ci._check(lib.cieg_ctx_set_stream(dev.handle, None))
     torch.cuda.set_stream(torch.cuda.default_stream(tdev))
 
@@ -775,6 +827,8 @@ def ours(args):
     }
     if widths is not None:
         line["widths"] = widths
+    if shard_modes is not None:
+        line["shard_modes_m8"] = shard_modes
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(h, m)
     if world == 1 and not args.no_lobpcg:
