@@ -13,6 +13,16 @@ from paper_1609_01689_b200 import ci
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["auto", "owner", "single"])
+def spmm_mode(request):
+    """Every edge case in each K1 mode: owner-computes, single pass (DMMA;
+    the scalar consumer at m <= 2) and the default per-width choice."""
+    dev = ci.Device.default()
+    dev.set_spmm_mode(request.param)
+    yield request.param
+    dev.set_spmm_mode("auto")
+
+
 def csb_from_coo(n, r, c, v, block_rows, precision=1, groups=None):
     """Lower-triangle CSB (csb.hpp layout) from global (r >= c) triplets."""
     bb = np.asarray(block_rows, dtype=np.uint32)
@@ -51,8 +61,9 @@ def test_rows_and_panels_without_entries():
     rc = np.unique(np.stack([r, c], 1), axis=0)
     r, c = rc[:, 0], rc[:, 1]
     h = csb_from_coo(n, r, c, rng.standard_normal(len(r)), [0, 256, 512, 768, n], groups=np.arange(0, n + 1, 100))
-    y = check(h, 7)
-    assert not y[300:600].any()
+    for m in (1, 7):
+        y = check(h, m)
+        assert not y[300:600].any()
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 9, 67, 129])
@@ -61,8 +72,8 @@ def test_tiny_and_ragged_dimensions(n):
     r, c = np.tril_indices(n)
     keep = (rng.random(len(r)) < 0.5) | (r == c)
     h = csb_from_coo(n, r[keep], c[keep], rng.standard_normal(keep.sum()), [0, n], precision=0)
-    check(h, 3)
-    check(h, 17)
+    for m in (1, 2, 3, 17):
+        check(h, m)
 
 
 def test_zero_width_block():
