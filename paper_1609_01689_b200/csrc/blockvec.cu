@@ -415,26 +415,37 @@ void launch_combine(cieg_ctx* ctx, const CombineParams& prm, int blocks) {
 }
 
 // ---------------------------------------------------------------- residual
-__global__ void residual_kernel(std::uint64_t total, std::uint32_t k, const double* __restrict__ hx,
+// Index arithmetic in the element type I: 32-bit when the block has fewer
+// than 2^32 elements (config 4: 8e7), which keeps the per-element column
+// division off the 64-bit emulation path.
+template <typename I>
+__global__ void residual_kernel(I total, std::uint32_t k, const double* __restrict__ hx,
                                 const double* __restrict__ x, const double* __restrict__ theta,
                                 double* __restrict__ r) {
-  for (std::uint64_t e = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
+  for (I e = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<I>(gridDim.x) * blockDim.x) {
     const std::uint32_t j = static_cast<std::uint32_t>(e % k);
     r[e] = hx[e] - theta[j] * x[e];
   }
 }
 
-__global__ void gather_kernel(std::uint64_t n, std::uint32_t ksrc, const double* __restrict__ src,
-                              std::uint32_t kd, const std::uint32_t* __restrict__ cols,
-                              double* __restrict__ dst) {
-  const std::uint64_t total = n * kd;
-  for (std::uint64_t e = blockIdx.x * static_cast<std::uint64_t>(blockDim.x) + threadIdx.x; e < total;
-       e += static_cast<std::uint64_t>(gridDim.x) * blockDim.x) {
-    const std::uint64_t i = e / kd;
+template <typename I>
+__global__ void gather_kernel(I n, std::uint32_t ksrc, const double* __restrict__ src, std::uint32_t kd,
+                              const std::uint32_t* __restrict__ cols, double* __restrict__ dst) {
+  const I total = n * kd;
+  for (I e = blockIdx.x * static_cast<I>(blockDim.x) + threadIdx.x; e < total;
+       e += static_cast<I>(gridDim.x) * blockDim.x) {
+    const I i = e / kd;
     const std::uint32_t j = static_cast<std::uint32_t>(e - i * kd);
-    dst[e] = src[i * ksrc + cols[j]];
+    dst[e] = __ldg(src + static_cast<std::size_t>(i) * ksrc + cols[j]);
   }
+}
+
+// Streaming elementwise kernels: 8 resident 256-thread blocks per SM (full
+// occupancy) keep enough loads in flight for HBM.
+int elementwise_grid(cieg_ctx* ctx, std::uint64_t total) {
+  const std::uint64_t want = (total + 255) / 256;
+  return static_cast<int>(std::max<std::uint64_t>(1, std::min<std::uint64_t>(want, 8ull * ctx->sm_count)));
 }
 
 int grid_for(cieg_ctx* ctx, std::uint64_t work, int per_block) {
@@ -627,7 +638,11 @@ void residual(cieg_ctx* ctx, std::uint32_t n, std::uint32_t k, const double* hx,
   std::memcpy(pin, theta_host, sizeof(double) * k);
   CIEG_CUDA(cudaMemcpyAsync(th, pin, sizeof(double) * k, cudaMemcpyHostToDevice, ctx->stream));
   const std::uint64_t total = static_cast<std::uint64_t>(n) * k;
-  residual_kernel<<<grid_for(ctx, total, 1024), 256, 0, ctx->stream>>>(total, k, hx, x, th, r);
+  if (total < (1ull << 32))
+    residual_kernel<std::uint32_t><<<elementwise_grid(ctx, total), 256, 0, ctx->stream>>>(
+        static_cast<std::uint32_t>(total), k, hx, x, th, r);
+  else
+    residual_kernel<std::uint64_t><<<elementwise_grid(ctx, total), 256, 0, ctx->stream>>>(total, k, hx, x, th, r);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
 }
@@ -642,7 +657,10 @@ void gather_columns(cieg_ctx* ctx, std::uint32_t n, const double* src, std::uint
   std::memcpy(pin, cols.data(), sizeof(std::uint32_t) * kd);
   CIEG_CUDA(cudaMemcpyAsync(dc, pin, sizeof(std::uint32_t) * kd, cudaMemcpyHostToDevice, ctx->stream));
   const std::uint64_t total = static_cast<std::uint64_t>(n) * kd;
-  gather_kernel<<<grid_for(ctx, total, 1024), 256, 0, ctx->stream>>>(n, ksrc, src, kd, dc, dst);
+  if (total < (1ull << 32))
+    gather_kernel<std::uint32_t><<<elementwise_grid(ctx, total), 256, 0, ctx->stream>>>(n, ksrc, src, kd, dc, dst);
+  else
+    gather_kernel<std::uint64_t><<<elementwise_grid(ctx, total), 256, 0, ctx->stream>>>(n, ksrc, src, kd, dc, dst);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
 }
