@@ -214,8 +214,13 @@ constexpr int kCombineWarps = 8;
 // its 8 output rows in shared memory to re-read them in fragment layout;
 // per-warp partials are folded in warp order, per-CTA partials reduced in a
 // fixed order (deterministic).
+// Resident blocks per SM the register budget is capped for: the narrow
+// variants are latency-bound streams and gain from occupancy (ncu, config 4).
+// (0 = no constraint: the compiler's own register choice)
+constexpr int combine_min_blocks(int ot, int lt, int ks) { return lt == 0 && ot <= 2 && ks <= 4 ? 4 : 0; }
+
 template <int OT, int LT = 0, bool SYM = false, int KS = 12>
-__global__ void __launch_bounds__(32 * kCombineWarps)
+__global__ void __launch_bounds__(32 * kCombineWarps, combine_min_blocks(OT, LT, KS))
     combine_kernel(const __grid_constant__ CombineParams p) {
   constexpr int SG = 8 * OT + 4;
   constexpr int SO = 8 * OT + 4;  // staged output row stride
