@@ -22,6 +22,7 @@
 #include "cieg_internal.hpp"
 #include "context.hpp"
 #include "dense_small.hpp"
+#include "device_common.cuh"
 #include "gen_common.h"
 #include "report.hpp"
 
@@ -72,14 +73,18 @@ __global__ void __launch_bounds__(kThreads) gemvt_partial_kernel(const double* _
   }
 }
 
-// out[j] = sum_g partial[g * m + j], g ascending.
+// out[j] = sum_k partial[k * m + j]: one warp per output, lane-strided
+// partial sums then a fixed xor tree (deterministic; a serial loop over the
+// row blocks per output was latency-bound at ~50 us per call).
 __global__ void reduce_partials_kernel(const double* __restrict__ partial, std::uint32_t g, std::uint32_t m,
                                        double* __restrict__ out) {
-  const std::uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  const std::uint32_t j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const std::uint32_t lane = threadIdx.x & 31;
   if (j >= m) return;
   double s = 0.0;
-  for (std::uint32_t k = 0; k < g; ++k) s += partial[static_cast<std::size_t>(k) * m + j];
-  out[j] = s;
+  for (std::uint32_t k = lane; k < g; k += 32) s += partial[static_cast<std::size_t>(k) * m + j];
+  s = warp_sum(s);
+  if (lane == 0) out[j] = s;
 }
 
 // tmp[c * n + r] = sum_{j in column chunk c} V[r, j] * coeff[j]; grid (row blocks, column chunks)
@@ -175,7 +180,7 @@ class Lanczos {
   void gemvt(const double* v, int m, const double* w, double* out) {
     const dim3 grid(g_, (m + kColsPerPass - 1) / kColsPerPass);
     gemvt_partial_kernel<<<grid, kThreads, 0, ctx_->stream>>>(v, n_, n_, static_cast<std::uint32_t>(m), w, partial_);
-    reduce_partials_kernel<<<(m + 127) / 128, 128, 0, ctx_->stream>>>(partial_, g_, static_cast<std::uint32_t>(m), out);
+    reduce_partials_kernel<<<(m + 3) / 4, 128, 0, ctx_->stream>>>(partial_, g_, static_cast<std::uint32_t>(m), out);
     launched(2);
   }
   double dot(const double* a, const double* b) {
