@@ -40,24 +40,46 @@ std::uint32_t reduction_ctas(std::uint32_t n) {
 }
 
 // partial[g * m + j] = sum over row chunk g of V[r, j] * w[r]  (V column-major, ld);
-// grid (row chunks, column groups of kColsPerPass)
+// grid (row chunks, column groups of kColsPerPass). PAIRS (ld even, chunks
+// of even length): row pairs through 16-byte loads.
+template <bool PAIRS>
 __global__ void __launch_bounds__(kThreads) gemvt_partial_kernel(const double* __restrict__ v, std::size_t ld,
                                                                  std::uint32_t n, std::uint32_t m,
                                                                  const double* __restrict__ w,
                                                                  double* __restrict__ partial) {
   __shared__ double red[kThreads / 32][kColsPerPass];
-  const std::uint32_t chunk = (n + gridDim.x - 1) / gridDim.x;
+  const std::uint32_t chunk = PAIRS ? ((n + gridDim.x - 1) / gridDim.x + 1) & ~1u : (n + gridDim.x - 1) / gridDim.x;
   const std::uint32_t r0 = blockIdx.x * chunk, r1 = min(n, r0 + chunk);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const std::uint32_t j0 = blockIdx.y * kColsPerPass;
   double acc[kColsPerPass];
 #pragma unroll
   for (int c = 0; c < kColsPerPass; ++c) acc[c] = 0.0;
-  for (std::uint32_t r = r0 + threadIdx.x; r < r1; r += kThreads) {
-    const double wr = w[r];
+  if (PAIRS) {
+    // row pairs: one 16-byte load per column and pair (ld and r0 even)
+    const std::uint32_t p1 = r0 + ((r1 - r0) & ~1u);
+    for (std::uint32_t r = r0 + 2 * threadIdx.x; r < p1; r += 2 * kThreads) {
+      const double2 wr = *reinterpret_cast<const double2*>(w + r);
 #pragma unroll
-    for (int c = 0; c < kColsPerPass; ++c)
-      if (j0 + c < m) acc[c] = fma(v[(j0 + c) * ld + r], wr, acc[c]);
+      for (int c = 0; c < kColsPerPass; ++c)
+        if (j0 + c < m) {
+          const double2 vv = *reinterpret_cast<const double2*>(v + (j0 + c) * ld + r);
+          acc[c] = fma(vv.y, wr.y, fma(vv.x, wr.x, acc[c]));
+        }
+    }
+    if (p1 < r1 && threadIdx.x == 0) {  // odd tail row of the chunk
+      const double wr = w[p1];
+#pragma unroll
+      for (int c = 0; c < kColsPerPass; ++c)
+        if (j0 + c < m) acc[c] = fma(v[(j0 + c) * ld + p1], wr, acc[c]);
+    }
+  } else {
+    for (std::uint32_t r = r0 + threadIdx.x; r < r1; r += kThreads) {
+      const double wr = w[r];
+#pragma unroll
+      for (int c = 0; c < kColsPerPass; ++c)
+        if (j0 + c < m) acc[c] = fma(v[(j0 + c) * ld + r], wr, acc[c]);
+    }
   }
 #pragma unroll
   for (int c = 0; c < kColsPerPass; ++c)
@@ -179,7 +201,12 @@ class Lanczos {
   // out[0..m) = V[:, :m]^T w   (device)
   void gemvt(const double* v, int m, const double* w, double* out) {
     const dim3 grid(g_, (m + kColsPerPass - 1) / kColsPerPass);
-    gemvt_partial_kernel<<<grid, kThreads, 0, ctx_->stream>>>(v, n_, n_, static_cast<std::uint32_t>(m), w, partial_);
+    const bool pairs = n_ % 2 == 0 && reinterpret_cast<std::uintptr_t>(v) % 16 == 0 &&
+                       reinterpret_cast<std::uintptr_t>(w) % 16 == 0;
+    if (pairs)
+      gemvt_partial_kernel<true><<<grid, kThreads, 0, ctx_->stream>>>(v, n_, n_, static_cast<std::uint32_t>(m), w, partial_);
+    else
+      gemvt_partial_kernel<false><<<grid, kThreads, 0, ctx_->stream>>>(v, n_, n_, static_cast<std::uint32_t>(m), w, partial_);
     reduce_partials_kernel<<<(m + 3) / 4, 128, 0, ctx_->stream>>>(partial_, g_, static_cast<std::uint32_t>(m), out);
     launched(2);
   }
