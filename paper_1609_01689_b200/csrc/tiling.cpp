@@ -457,10 +457,12 @@ void shard_plan(const cieg_csb_view& csb, const std::uint32_t* gb, std::uint32_t
       }
     }
   }
-  std::vector<std::uint32_t> cuts;  // candidate cut rows = group boundaries
+  // candidate cut rows = the panel boundaries the shard upload will plan
+  // (small groups merge into panels, so not every group boundary is one)
+  std::vector<std::uint32_t> cuts;
   if (gb && ng) {
     if (gb[0] != 0 || gb[ng] != dim) fail(CIEG_ERR_DIMENSION, "group bounds do not cover [0, dim)");
-    cuts.assign(gb, gb + ng + 1);
+    cuts = plan_panels(dim, gb, ng, te);
   } else {
     for (std::uint32_t r = 0; r <= dim; r += te) cuts.push_back(r);
     if (cuts.back() != dim) cuts.push_back(dim);

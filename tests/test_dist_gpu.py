@@ -171,43 +171,7 @@ def test_generated_shards_solver_matches_single_gpu():
     assert out[0]["eigenvalues"] == out[1]["eigenvalues"]
 
 
-def _single_pass_shards(h, world, m, x):
-    """Every shard of a world-`world` partition in this process: the
-    single-pass kernel (cieg_spmm_partial) per shard, then the reverse
-    exchange done on the host exactly as dist.partial_reduce orders it."""
-    import ctypes as C
-
-    import torch
-
-    from paper_1609_01689_b200 import _lib, ci
-    from paper_1609_01689_b200 import dist as D
-
-    dev = ci.Device.default()
-    rb, hl, hh = D.row_partition(h, world)
-    xs = torch.from_numpy(x).cuda()
-    ys, halos = [], []
-    for r in range(world):
-        sm = D.ShardedMatrix(h, r, world, dev, plan=(rb, hl, hh))
-        plo, phi = D.partial_rows(sm.handle)
-        assert phi == sm.row_lo and plo <= phi
-        y = torch.empty((sm.local_rows, m), dtype=torch.float64, device="cuda")
-        yh = torch.full((max(phi - plo, 1), m), float("nan"), dtype=torch.float64, device="cuda")
-        ci._check(_lib.load().cieg_spmm_partial(dev.handle, sm.handle, C.c_void_p(xs.data_ptr()),
-                                                C.c_void_p(y.data_ptr()), m, C.c_void_p(yh.data_ptr())))
-        dev.synchronize()
-        ys.append(y.cpu().numpy())
-        halos.append((plo, yh.cpu().numpy()[: phi - plo]))
-    out = np.zeros((h.dim, m))
-    for r in range(world):
-        lo, hi = int(rb[r]), int(rb[r + 1])
-        yr = ys[r].copy()
-        for t in range(r + 1, world):
-            plo, yh = halos[t]
-            a, b = max(lo, plo), min(hi, int(rb[t]))
-            if b > a:
-                yr[a - lo:b - lo] += yh[a - plo:b - plo]
-        out[lo:hi] = yr
-    return out
+from conftest import single_pass_shards as _single_pass_shards  # noqa: E402
 
 
 @pytest.mark.parametrize("world", [2, 3])

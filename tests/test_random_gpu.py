@@ -7,6 +7,7 @@ shapes the fixed configs do not reach."""
 import numpy as np
 import pytest
 
+from conftest import single_pass_shards
 from oracle import ci_oracle as O
 from paper_1609_01689_b200 import ci
 
@@ -30,9 +31,21 @@ def test_random_generator_configs(c):
     h = ci.generate_sector_matrix(c["n"], c["sectors"], c["tile"], c["p"], c["q"], c["seed"], c["precision"],
                                   c["beta"], band=c["band"])
     x = ci.random_block(h.dim, c["m"], c["seed"] % 1000)
-    y = ci.DeviceMatrix(h).spmm_host(x)
+    dm = ci.DeviceMatrix(h)
+    y = dm.spmm_host(x)
     yo = O.spmm(h, x)
-    assert np.abs(y - yo).max() <= 1e-14 * max(np.abs(yo).max(), 1e-300)
+    scale = max(np.abs(yo).max(), 1e-300)
+    assert np.abs(y - yo).max() <= 1e-14 * scale
+    for mode in ("owner", "single"):  # both K1 modes, whatever auto chose
+        dm.device.set_spmm_mode(mode)
+        try:
+            assert np.abs(dm.spmm_host(x) - yo).max() <= 1e-14 * scale
+        finally:
+            dm.device.set_spmm_mode("auto")
+    # single-pass row shards (world 2), partials reduced at their owners
+    if len(h.groups) > 2:
+        ys = single_pass_shards(h, 2, c["m"], x)
+        assert np.abs(ys - yo).max() <= 1e-14 * scale
     dev = ci.DeviceMatrix.generate(c["n"], c["sectors"], c["tile"], c["p"], c["q"], c["seed"], c["precision"],
                                    c["beta"], band=c["band"])
     host = ci.DeviceMatrix(h)
