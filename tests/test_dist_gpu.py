@@ -214,3 +214,57 @@ def test_single_pass_shards_nonfinite():
         assert np.array_equal(mask(y), mask(yo))
     fin = np.isfinite(yo)
     np.testing.assert_allclose(y[fin], yo[fin], rtol=1e-12, atol=1e-12)
+
+
+def _small_groups_worker(rank, world, port, out_q):
+    """A matrix whose 16-row groups merge into device panels: the shard cuts
+    must fall on panel boundaries; the sharded solve matches one GPU."""
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch
+    import torch.distributed as dist
+
+    from paper_1609_01689_b200 import ci
+    from paper_1609_01689_b200 import dist as D
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    res = {}
+    try:
+        h = ci.generate_sector_matrix(1926, 2, 16, 0.3, 0.4, 91, 1, 256, band=1)
+        dev = ci.Device(0)
+        sm = D.ShardedMatrix(h, rank, world, dev)
+        x0 = ci.random_block(h.dim, 6, 5)
+        rep = D.lobpcg_solve_dist(sm, x0[sm.row_lo:sm.row_hi], ci.LobpcgOptions(k_want=3, tol=1e-8))
+        one = ci.lobpcg_solve(h, x0, ci.LobpcgOptions(k_want=3, tol=1e-8))
+        res["iterations"] = (rep.iterations, one.iterations)
+        res["eig_rel"] = float(np.abs(rep.eigenvalues - one.eigenvalues).max() / np.abs(one.eigenvalues).max())
+        res["bounds"] = [int(b) for b in sm.row_bounds]
+    except Exception as e:  # pragma: no cover
+        import traceback
+
+        res["error"] = repr(e) + traceback.format_exc()
+    finally:
+        dist.destroy_process_group()
+    out_q.put((rank, res))
+
+
+@pytest.mark.timeout(400)
+def test_sharded_solver_small_groups():
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_small_groups_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(2):
+        assert "error" not in out[r], out[r].get("error")
+        it, it1 = out[r]["iterations"]
+        assert it == it1
+        assert out[r]["eig_rel"] < 1e-10
