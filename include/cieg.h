@@ -418,6 +418,11 @@ int cieg_host_csb_groups(const cieg_host_csb* h, const uint32_t** bounds, uint32
  * (no host CSB; bit-identical tile stream to cieg_matrix_upload of
  * cieg_generate_csb). Owner rows [row_lo, row_hi) (0, 0 = all) for a shard;
  * tile_edge 0 = choose. SURVEY.md 8(f) rank 1. */
+/* The device panel grid cieg_generate_device plans for these parameters
+ * (panel_start[npanels + 1]; panel_start = NULL returns the count): shard
+ * row ranges must be unions of whole panels. */
+int cieg_generated_panels(const cieg_gen_params* prm, uint32_t tile_edge, uint32_t* panel_start, uint32_t cap,
+                          uint32_t* npanels);
 int cieg_generate_device(cieg_ctx* ctx, const cieg_gen_params* prm, uint32_t tile_edge, uint32_t row_lo,
                          uint32_t row_hi, cieg_mat** out);
 /* Tile-diagonal preconditioner built on the device from the matrix's own

@@ -201,6 +201,7 @@ SIGNATURES = {
     "cieg_host_csb_groups": (_i, [_vp, C.POINTER(_pu32), _pu32]),
     "cieg_random_block": (_i, [_u32, _u32, _u64, _pd]),
     "cieg_generate_device": (_i, [_vp, C.POINTER(GenParams), _u32, _u32, _u32, C.POINTER(_vp)]),
+    "cieg_generated_panels": (_i, [C.POINTER(GenParams), _u32, C.POINTER(_u32), _u32, C.POINTER(_u32)]),
     "cieg_precond_from_matrix": (_i, [_vp, _vp, C.POINTER(_vp)]),
     "cieg_matrix_groups": (_i, [_vp, C.POINTER(_pu32), _pu32]),
     "cieg_matrix_export": (_i, [_vp, _pu64, _pu32, _pu32, _pu32, _vp]),

@@ -256,6 +256,18 @@ def gen_params(n, sectors, tile, p, q, seed=1, precision=0, beta=2000, band=2) -
     return prm
 
 
+def generated_panels(n, sectors, tile, p=0.5, q=0.5, precision=0, beta=2000, band=2, tile_edge=0) -> np.ndarray:
+    """The device panel grid cieg_generate_device plans (panel starts, n
+    last): shard row ranges must be unions of whole panels."""
+    prm = gen_params(n, sectors, tile, p, q, precision=precision, beta=beta, band=band)
+    lib = _lib.load()
+    cnt = C.c_uint32()
+    _check(lib.cieg_generated_panels(C.byref(prm), tile_edge, None, 0, C.byref(cnt)))
+    out = np.zeros(cnt.value + 1, np.uint32)
+    _check(lib.cieg_generated_panels(C.byref(prm), tile_edge, _ptr(out, C.c_uint32), len(out), C.byref(cnt)))
+    return out.astype(np.int64)
+
+
 def expected_nnz(n, sectors, tile, p, q, band=2) -> float:
     prm = gen_params(n, sectors, tile, p, q, band=band)
     return float(_lib.load().cieg_gen_expected_nnz(C.byref(prm)))

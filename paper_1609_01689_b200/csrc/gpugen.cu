@@ -146,18 +146,25 @@ T* dev_upload(const std::vector<T>& v) {
 
 }  // namespace
 
-cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t te, std::uint32_t row_lo,
-                          std::uint32_t row_hi) {
-  validate(p);
-  if (row_hi == 0) row_hi = p.n;
-  const TileGrid grid = make_grid(p);
-  if (te == 0) {  // the rule of cieg_matrix_upload (capi.cu: choose_tile_edge) on the generator's groups
+// The device tile edge of a generated matrix: the rule of cieg_matrix_upload
+// (capi.cu: choose_tile_edge) on the generator's groups.
+std::uint32_t generated_tile_edge(const cieg_gen_params& p, const TileGrid& grid, std::uint32_t te) {
+  if (te == 0) {
     std::uint32_t mx = 0;
     for (std::uint32_t t = 0; t < grid.count(); ++t) mx = std::max(mx, grid.start[t + 1] - grid.start[t]);
     te = mx <= 64 ? 64 : 128;
   }
   if (p.precision == 1) te = 64;
   if (te != 64 && te != 128) fail(CIEG_ERR_CONFIG, "tile edge must be 64 or 128");
+  return te;
+}
+
+cieg_mat* generate_device(cieg_ctx* ctx, const cieg_gen_params& p, std::uint32_t te, std::uint32_t row_lo,
+                          std::uint32_t row_hi) {
+  validate(p);
+  if (row_hi == 0) row_hi = p.n;
+  const TileGrid grid = make_grid(p);
+  te = generated_tile_edge(p, grid, te);
   const std::uint32_t ng = grid.count();
   const std::vector<std::vector<std::uint32_t>> kept = kept_tiles(p, grid);
   const double scale = value_scale(p);
@@ -439,6 +446,22 @@ cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
 }  // namespace cieg
 
 extern "C" {
+
+int cieg_generated_panels(const cieg_gen_params* prm, uint32_t tile_edge, uint32_t* panel_start, uint32_t cap,
+                          uint32_t* npanels) {
+  return cieg::guarded([&] {
+    if (!prm || !npanels) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_generated_panels: null argument");
+    cieg::validate(*prm);
+    const cieg::TileGrid grid = cieg::make_grid(*prm);
+    const std::uint32_t te = cieg::generated_tile_edge(*prm, grid, tile_edge);
+    const std::vector<std::uint32_t> ps = cieg::plan_panels(prm->n, grid.start.data(), grid.count(), te);
+    *npanels = static_cast<uint32_t>(ps.size() - 1);
+    if (panel_start) {
+      if (cap < ps.size()) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_generated_panels: buffer too small");
+      std::copy(ps.begin(), ps.end(), panel_start);
+    }
+  });
+}
 
 int cieg_generate_device(cieg_ctx* ctx, const cieg_gen_params* prm, uint32_t tile_edge, uint32_t row_lo,
                          uint32_t row_hi, cieg_mat** out) {

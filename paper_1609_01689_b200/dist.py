@@ -335,15 +335,11 @@ class DeviceShard:
 
 
 def generated_row_bounds(cfg, world: int):
-    """Group-aligned row cuts for GPU-generated shards, balanced by the
+    """Row cuts for GPU-generated shards on the device panel grid
+    (cieg_generated_panels: small groups merge into panels), balanced by the
     generator's expected streamed entries per row (edge sectors couple to
     fewer neighbours than interior ones)."""
-    gb = []
-    for s in range(cfg.sectors):
-        a, b = cfg.n * s // cfg.sectors, cfg.n * (s + 1) // cfg.sectors
-        gb.extend(range(a, b, cfg.tile))
-    gb.append(cfg.n)
-    gb = np.asarray(gb, dtype=np.int64)
+    gb = ci.generated_panels(cfg.n, cfg.sectors, cfg.tile, precision=cfg.precision, beta=cfg.beta)
     # expected row weight: sectors within the +-2 band around the row's sector
     sec = np.minimum((gb[:-1] * cfg.sectors) // cfg.n, cfg.sectors - 1)
     neigh = np.array([min(s + 2, cfg.sectors - 1) - max(s - 2, 0) + 1 for s in sec], dtype=np.float64)

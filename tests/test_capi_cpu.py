@@ -133,3 +133,24 @@ def test_pad_from_subspace_host():
     assert p.shape == (6, 3) and np.array_equal(p[:4], x) and not p[4:].any()
     with pytest.raises(ci.DimensionMismatch):
         ci.pad_from_subspace(x, 3)
+
+
+def test_generated_panels_and_shard_cuts():
+    """cieg_generated_panels: the device panel grid of a generated matrix
+    (small groups merged into <= tile-edge panels); GPU-generated shard cuts
+    (dist.generated_row_bounds) always fall on it."""
+    import dataclasses
+
+    from paper_1609_01689_b200 import configs
+    from paper_1609_01689_b200 import dist as D
+
+    for tile, prec in ((16, 0), (33, 1), (64, 1), (256, 0)):
+        ps = ci.generated_panels(6000, 3, tile, precision=prec)
+        assert ps[0] == 0 and ps[-1] == 6000 and np.all(np.diff(ps) > 0)
+        te = 64 if prec == 1 or tile <= 64 else 128
+        assert np.diff(ps).max() <= te
+        cfg = dataclasses.replace(configs.CFG1, n=6000, sectors=3, tile=tile, precision=prec)
+        for world in (2, 3, 5):
+            rb = D.generated_row_bounds(cfg, world)
+            assert rb[0] == 0 and rb[-1] == 6000 and np.all(np.diff(rb) > 0)
+            assert set(rb.tolist()) <= set(ps.tolist())

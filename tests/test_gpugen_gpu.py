@@ -67,3 +67,28 @@ def test_lobpcg_on_generated_config1():
     rep = ci.lobpcg_solve(dm, ci.random_block(cfg.n, cfg.kt, 42),
                           ci.LobpcgOptions(k_want=cfg.k_want, tol=cfg.tol, preconditioner=td))
     assert rep.converged and rep.iterations == 84
+
+
+def test_generated_small_tile_shards():
+    """Shards of a generator with 16-row tiles (merged into device panels),
+    cut by dist.generated_row_bounds: every shard builds and its rows equal
+    the full matrix's, bitwise in owner-computes."""
+    import dataclasses
+
+    from paper_1609_01689_b200 import dist as D
+
+    cfg = dataclasses.replace(configs.CFG1, n=6000, sectors=3, tile=16, precision=0)
+    full = cfg.generate_device()
+    x = ci.random_block(cfg.n, 5, 3)
+    dev = ci.Device.default()
+    dev.set_spmm_mode("owner")
+    try:
+        yf = full.spmm_host(x)
+        rb = D.generated_row_bounds(cfg, 3)
+        for r in range(3):
+            lo, hi = int(rb[r]), int(rb[r + 1])
+            sh = cfg.generate_device(rows=(lo, hi))
+            np.testing.assert_array_equal(sh.spmm_host(x), yf[lo:hi])
+    finally:
+        dev.set_spmm_mode("auto")
+
