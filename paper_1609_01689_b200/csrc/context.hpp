@@ -122,9 +122,15 @@ namespace cieg {
 // once on every freshly built device tile stream.
 void order_tile_entries(cieg_ctx* ctx, cieg_mat* m);
 
-// The SpMM mode's choice for block width mc on a matrix with a single-pass
-// schedule (auto: single pass for mc <= 8).
+// The SpMM mode's rule for block width mc on a matrix with a single-pass
+// schedule (auto: single pass for mc <= 8); single_pass_default adds, in
+// auto mode, the memory check of single_pass_fits.
+bool single_pass_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
 bool single_pass_default(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
+// The per-tile partial slots of a single pass at width mc take at most a
+// quarter of the free device memory (or are already allocated).
+bool single_pass_fits(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
+constexpr std::uint32_t kSinglePassMaxCols = 8;
 
 // Upload the work lists and both K1 schedules of a tiling.
 struct HostTiles;

@@ -193,10 +193,21 @@ class Solver {
         ops_{ctx, mat->row_hi - mat->row_lo, hooks} {
     ws_.ctx = ctx;
     ws_.n = n_;
+    if (hooks_ && hooks_->reduce_partials && mat_->sp_sched) {
+      // single-pass SpMMs need room for their partial slots on every rank;
+      // one collective decision keeps the ranks' SpMM modes (and so their
+      // partial exchanges) in step
+      double no_room = single_pass_fits(ctx_, mat_, kSinglePassMaxCols) ? 0.0 : 1.0;
+      if (hooks_->allreduce_sum(hooks_->user, &no_room, 1) != 0) fail(CIEG_ERR_ARGUMENT, "allreduce_sum hook failed");
+      sp_ok_ = no_room == 0.0;
+    }
   }
 
   void run(const double* x0_host, std::uint32_t kt0, cieg_observer_fn obs, void* user);
-  ~Solver() { xfull_.release(); }
+  ~Solver() {
+    xfull_.release();
+    yhalo_.release();
+  }
 
  private:
   // orthonormalize (lobpcg.cpp:89-119). `v` holds the input (width v.w) and is
@@ -217,7 +228,7 @@ class Solver {
       if (hooks_->allgather_rows(hooks_->user, x.p, x.w, full) != 0)
         fail(CIEG_ERR_ARGUMENT, "allgather_rows hook failed");
       xin = full;
-      if (hooks_->reduce_partials && single_pass_default(ctx_, mat_, x.w)) {
+      if (sp_ok_ && single_pass_rule(ctx_, mat_, x.w)) {
         // single pass: the transposed partials for lower ranks' rows travel
         // back to their owners (SURVEY.md 8(e) reduce-scatter, point to point)
         const std::size_t prow = mat_->row_lo - mat_->sp_partial_lo;
@@ -245,6 +256,7 @@ class Solver {
   const cieg_dist_hooks* hooks_;
   GramOps ops_;
   DevBuf xfull_, yhalo_;
+  bool sp_ok_ = false;  // sharded single-pass SpMMs enabled (collective decision)
   Workspace ws_;
   Block x_, hx_, p_, hp_, x2_, hx2_, p2_, hp2_, w_, hw_, wtmp_, r_, wsrc_;
   std::vector<double> theta_;

@@ -864,10 +864,24 @@ void dispatch_nt(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, std::ui
 // (unsharded) matrices, owner-computes otherwise. Measured on config 2
 // (profiles/README.md): single pass 2.14 / 2.99 / 5.03 ms at m = 1 / 8 / 16
 // (scalar consumer at m <= 2) vs owner-computes 3.65 / 3.71 / 4.72 ms.
-constexpr std::uint32_t kSinglePassMaxCols = 8;
 }  // namespace
 
+bool single_pass_fits(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
+  const std::size_t need = sizeof(double) * static_cast<std::size_t>(m->sp_items) * m->tile_edge * mc;
+  if (need <= ctx->scratch_partial.bytes) return true;
+  std::size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) return false;
+  return need <= free_b / 4;
+}
+
 bool single_pass_default(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
+  if (!single_pass_rule(ctx, m, mc)) return false;
+  const int mode = ctx->spmm_mode;
+  // auto (and env-selected) mode: owner-computes when the partials would crowd HBM
+  return mode == CIEG_SPMM_SINGLE_PASS || single_pass_fits(ctx, m, mc);
+}
+
+bool single_pass_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
   static const int env_mode = [] {
     const char* e = std::getenv("CIEG_SPMM_MODE");
     if (e && std::strcmp(e, "owner") == 0) return static_cast<int>(CIEG_SPMM_OWNER);
