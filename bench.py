@@ -54,7 +54,7 @@ def load_traffic(workload):
         return None
 
 
-def roofline(gbs, tflops, hbm_peak, hbm_kind, nbytes, flops, workload):
+def roofline(gbs, tflops, hbm_peak, hbm_kind, nbytes, flops, workload, issued_flops=None, ms=None):
     """the roof is min(HBM, FP64). The bound is whichever
     the algorithmic intensity F/B selects against the ridge
     FP64_peak / HBM_peak (5.7 flop/B): cfg2 at m = 16 (7.4 flop/B) is
@@ -68,6 +68,12 @@ def roofline(gbs, tflops, hbm_peak, hbm_kind, nbytes, flops, workload):
          "fp64_achieved_tflops": round(tflops, 3), "fp64_peak_tflops": FP64_PEAK_TFLOPS,
          "fp64_peak_kind": "measured (tools/microbench/fp64_probe.cu: DFMA = DMMA m8n8k4 = 37.0 TF/s)",
          "fp64_frac": round(tflops / FP64_PEAK_TFLOPS, 4)}
+    if issued_flops and ms:
+        # what the FP64 tensor pipe actually executes: every work item is a
+        # dense TD x TD tile times TD x 8 ceil(m / 8) slab (DMMA), zeros included
+        it = issued_flops / (ms * 1e-3) / 1e12
+        r.update({"fp64_issued_flops_per_launch": int(issued_flops), "fp64_issued_tflops": round(it, 3),
+                  "fp64_issued_frac": round(it / FP64_PEAK_TFLOPS, 4)})
     if ai >= ridge:
         r.update({"bound": "tensor", "achieved": r["fp64_achieved_tflops"], "peak": FP64_PEAK_TFLOPS,
                   "unit": "TFLOP/s", "frac": r["fp64_frac"], "peak_kind": r["fp64_peak_kind"]})
@@ -795,13 +801,17 @@ def ours(args):
     else:
         e2e = {"value": round(gbs, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                "note": "sharded run: inputs device-resident, the step includes the X halo exchange"}
-    tile_edge, ntiles = dm.tile_edge, dm.ntiles
+    tile_edge, ntiles, npanels = dm.tile_edge, dm.ntiles, dm.npanels
     del dm  # the records below build their own matrices
     torch.cuda.empty_cache()
     cfg5 = None
     if world > 1 and not args.no_cfg5:
         cfg5 = cfg5_record(dev, rank, world)  # collective: every rank
     peak, peak_kind = load_peaks()
+    # owner-computes at m = 16: 2 items per off-diagonal tile + 1 per diagonal
+    # tile (one per panel), each a dense tile x (TD x 16) slab product
+    issued = ((2 * ntiles - npanels) * tile_edge * tile_edge * 8 * ((m + 7) // 8) * 2
+              if world == 1 and m > 8 else None)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -820,7 +830,8 @@ def ours(args):
                    "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} (X halo exchange)",
                    "exchange": exchange,
                    "gen_s": round(t_gen, 1), "upload_s": round(t_up, 1)},
-        "roofline": roofline(gbs, flops / (ms * 1e-3) / 1e12, peak, peak_kind, nbytes, flops, cfg.name),
+        "roofline": roofline(gbs, flops / (ms * 1e-3) / 1e12, peak, peak_kind, nbytes, flops, cfg.name,
+                             issued_flops=issued, ms=ms),
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
