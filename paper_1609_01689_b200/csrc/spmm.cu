@@ -78,7 +78,7 @@ constexpr int kQuads = 4;                                  // entry quads per pr
 constexpr int kChunkQuads = kQuads * kProducerThreads;     // 1024 quads = 4096 entries per batch
 constexpr int kGroupChunkQuads = kQuads * kGroupThreads;  // per producer group
 // named barrier ids (0 is __syncthreads)
-constexpr int kBarFull0 = 1, kBarEmpty0 = 3, kBarProducers = 5, kBarProducers0 = 5;  // groups: 5, 6
+constexpr int kBarProducers = 5, kBarProducers0 = 5;  // producer groups: 5, 6
 constexpr int kBarConsumers = 7;  // single pass: the consumers' owner-slab refresh
 
 __device__ __forceinline__ void bar_sync(int id, int n) {
@@ -86,6 +86,40 @@ __device__ __forceinline__ void bar_sync(int id, int n) {
 }
 __device__ __forceinline__ void bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Tile-buffer hand-off over shared-memory mbarriers: FULL[b] completes when
+// every thread of the filling producer group has arrived (release: its
+// shared stores are visible to the waiters), EMPTY[b] when every consumer
+// warp has released the buffer. Each consumer warp waits on FULL on its own
+// -- no barrier makes the consumer warps meet at every item, so one warp's
+// DMMAs keep the pipe busy while another crosses the item boundary.
+// Fill u of a buffer waits for EMPTY parity (u & 1) ^ 1 (fill 0 passes at
+// once) and is consumed at FULL parity u & 1.
+__device__ __forceinline__ std::uint32_t smem_addr(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(std::uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(std::uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(std::uint64_t* b, unsigned parity) {
+  const std::uint32_t addr = smem_addr(b);
+  std::uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+// consumer warp: release a tile buffer (after the warp's last read of it)
+__device__ __forceinline__ void release_buffer(std::uint64_t* empty, int lane) {
+  __syncwarp();
+  if (lane == 0) mbar_arrive(empty);
 }
 template <typename V, int TD, int NT>
 struct Shape {
@@ -299,9 +333,9 @@ __device__ __forceinline__ void transposed_product(const SpmmArgs& a, const V* T
 // the warp's rows, combined across warps in warp order through shared
 // memory). Deterministic. Positions are the permuted tile columns
 // (tile_layout.h), so the partner slab is read at unperm(position).
-template <typename V, int TD, int NT, int SCM, int HANDOFF>
-__device__ __forceinline__ void scalar_consumer(const SpmmArgs& a, unsigned char* smem, std::uint32_t i_beg,
-                                                std::uint32_t i_end, int cw, int lane, int tid) {
+template <typename V, int TD, int NT, int SCM>
+__device__ __forceinline__ void scalar_consumer(const SpmmArgs& a, unsigned char* smem, std::uint64_t* hand,
+                                                std::uint32_t i_beg, std::uint32_t i_end, int cw, int lane, int tid) {
   using S = Shape<V, TD, NT>;
   constexpr int RPW = TD / kConsumerWarps;  // tile rows per consumer warp
   constexpr int PPL = TD / 32;              // tile positions per lane
@@ -316,8 +350,6 @@ __device__ __forceinline__ void scalar_consumer(const SpmmArgs& a, unsigned char
   for (int k = 0; k < PPL; ++k) col[k] = static_cast<int>(cieg_tl::unperm(static_cast<std::uint32_t>(p0 + k), prec));
   const int r_base = cw * RPW;
   const int mc = static_cast<int>(a.mcols);
-  bar_arrive(kBarEmpty0 + 0, HANDOFF);
-  bar_arrive(kBarEmpty0 + 1, HANDOFF);
   int buf = 0;
   double racc[RPW][SCM];
   Item it = load_item(a, i_beg);
@@ -342,7 +374,7 @@ __device__ __forceinline__ void scalar_consumer(const SpmmArgs& a, unsigned char
       if (bad) *a.nonfinite = a.launch_id;
       bar_sync(kBarConsumers, kConsumerThreads);
     }
-    bar_sync(kBarFull0 + buf, HANDOFF);
+    mbar_wait(&hand[buf], ((i - i_beg) >> 1) & 1u);
     const V* A = reinterpret_cast<const V*>(smem + buf * S::kTileBytes);
     const double* X = reinterpret_cast<const double*>(smem + 2 * S::kTileBytes + buf * S::kSlabBytes);
     const bool trans = it.kind() == 0u;
@@ -375,7 +407,7 @@ __device__ __forceinline__ void scalar_consumer(const SpmmArgs& a, unsigned char
         }
       }
     }
-    if (i + 2 < i_end) bar_arrive(kBarEmpty0 + buf, HANDOFF);
+    release_buffer(&hand[2 + buf], lane);
     buf ^= 1;
     if (trans) {
 #pragma unroll
@@ -434,7 +466,16 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
   // item (128-row tiles) covers them and one 8-warp group (twice the
   // placement rate) wins.
   constexpr bool kTwoGroups = NT == 1 || TD == 64;  // 64-row tiles: little DMMA work per item
-  constexpr int kHandoff = (kTwoGroups ? kGroupThreads : kProducerThreads) + kConsumerThreads;
+  __shared__ __align__(8) std::uint64_t hand[4];     // FULL[0..1], EMPTY[0..1]
+  if (tid == 0) {
+    constexpr unsigned kFill = kTwoGroups ? kGroupThreads : kProducerThreads;
+    mbar_init(&hand[0], kFill);
+    mbar_init(&hand[1], kFill);
+    mbar_init(&hand[2], kConsumerWarps);
+    mbar_init(&hand[3], kConsumerWarps);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
   if (warp < kProducerWarps && !kTwoGroups) {
     // ------------------------------------------------------------ producer
@@ -471,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       // into L2 a whole item ahead of the register batches (measured best at
       // distance 1; deeper prefetch loses)
       if (pt == 0 && has_next) prefetch_item<V>(a, nxt);
-      bar_sync(kBarEmpty0 + buf, kThreads);
+      mbar_wait(&hand[2 + buf], (((i - i_beg) >> 1) & 1u) ^ 1u);
       V* A = tile_buf(buf);
       {
         // zero the TD data columns of every row (the pad columns are never read)
@@ -522,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 #pragma unroll
         for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
       }
-      bar_arrive(kBarFull0 + buf, kThreads);
+      mbar_arrive(&hand[buf]);
       buf ^= 1;
       cur = nxt;
       nxt = after;
@@ -564,7 +605,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
         const bool has_next = i + 2 < i_end;
         // the group's next item: entries and X slab bulk-prefetched into L2
         if (pt == 0 && has_next) prefetch_item<V>(a, nxt);
-        bar_sync(kBarEmpty0 + buf, kGroupThreads + kConsumerThreads);
+        mbar_wait(&hand[2 + buf], (((i - i0) >> 1) & 1u) ^ 1u);
         V* A = tile_buf(buf);
         {
           // zero the TD data columns of every row (the pad columns are never read)
@@ -615,22 +656,20 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
 #pragma unroll
           for (int j = 0; j < kQuads; ++j) qa[j] = qb[j];
         }
-        bar_arrive(kBarFull0 + buf, kGroupThreads + kConsumerThreads);
+        mbar_arrive(&hand[buf]);
         cur = nxt;
         nxt = after;
       }
       if (nonfinite) *a.nonfinite = a.launch_id;
     }
   } else if constexpr (SCM > 0) {
-    scalar_consumer<V, TD, NT, SCM, kHandoff>(a, smem, i_beg, i_end, warp - kProducerWarps, lane, tid);
+    scalar_consumer<V, TD, NT, SCM>(a, smem, hand, i_beg, i_end, warp - kProducerWarps, lane, tid);
   } else {
     // ------------------------------------------------------------ consumer
     const int cw = warp - kProducerWarps;
     const int g = lane >> 2, q = lane & 3;
     const int m_base = cw * 8 * S::kMT;
     double* oslab = reinterpret_cast<double*>(smem + 2 * S::kTileBytes + 2 * S::kSlabBytes);  // SP only
-    bar_arrive(kBarEmpty0 + 0, kHandoff);
-    bar_arrive(kBarEmpty0 + 1, kHandoff);
     int buf = 0;
     double acc[S::kMT][NT][2];
     Item it = load_item(a, i_beg);
@@ -663,7 +702,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       const std::uint32_t r0 = it.r0;
       const int prow = it.prow();
       const bool live = m_base < prow;
-      bar_sync(kBarFull0 + buf, kHandoff);
+      mbar_wait(&hand[buf], ((i - i_beg) >> 1) & 1u);
       if (live) {
         // Rows >= orow of the slab and of the tile are zero: all TD/4
         // k-steps run, in groups of 4 (two interleaved k-step pairs), with
@@ -727,7 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
       if constexpr (SP) {
         if (it.kind() == 0u && m_base < it.orow) transposed_product<V, TD, NT>(a, tile_buf(buf), oslab, i, it, cw, lane);
       }
-      if (i + 2 < i_end) bar_arrive(kBarEmpty0 + buf, kHandoff);
+      release_buffer(&hand[2 + buf], lane);
       buf ^= 1;
       if (it.last() && live) {
 #pragma unroll
