@@ -268,3 +268,38 @@ def test_sharded_solver_small_groups():
         it, it1 = out[r]["iterations"]
         assert it == it1
         assert out[r]["eig_rel"] < 1e-10
+
+
+def test_spmm_partial_arguments():
+    """cieg_spmm_partial: a shard with partial rows needs the partial buffer
+    (loud failure without it); on an unsharded matrix it is the single pass
+    with no partial rows (cieg_matrix_partial_rows gives an empty range)."""
+    import ctypes as C
+
+    import torch
+
+    from conftest import gen_from
+    from oracle import ci_oracle as O
+    from paper_1609_01689_b200 import _lib, ci
+    from paper_1609_01689_b200 import dist as D
+
+    h = gen_from((20_000, 10, 64, 0.05, 0.5, 1, 1, 2000))
+    dev = ci.Device.default()
+    lib = _lib.load()
+    rb, hl, hh = D.row_partition(h, 2)
+    sm = D.ShardedMatrix(h, 1, 2, dev, plan=(rb, hl, hh))
+    plo, phi = D.partial_rows(sm.handle)
+    assert plo < phi == sm.row_lo
+    x = torch.from_numpy(ci.random_block(h.dim, 3, 1)).cuda()
+    y = torch.empty((sm.local_rows, 3), dtype=torch.float64, device="cuda")
+    with pytest.raises(ci.Error):
+        ci._check(lib.cieg_spmm_partial(dev.handle, sm.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()),
+                                        3, None))
+    dm = ci.DeviceMatrix(h)
+    assert D.partial_rows(dm.handle) == (0, 0)
+    yf = torch.empty((h.dim, 3), dtype=torch.float64, device="cuda")
+    ci._check(lib.cieg_spmm_partial(dev.handle, dm.handle, C.c_void_p(x.data_ptr()), C.c_void_p(yf.data_ptr()), 3,
+                                    None))
+    dev.synchronize()
+    want = O.spmm(h, x.cpu().numpy())
+    assert np.abs(yf.cpu().numpy() - want).max() <= 1e-13 * np.abs(want).max()
