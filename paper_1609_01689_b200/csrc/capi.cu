@@ -370,8 +370,7 @@ int cieg_spmm_partial(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, d
     if (shard) {
       if (!yhalo_dev && mat->row_lo > mat->sp_partial_lo && m > 0)
         cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_partial: null partial buffer");
-      double dummy = 0.0;  // a shard without partial rows still takes the single pass
-      cieg::launch_spmm(ctx, mat, x_dev, m, y_dev, m, m, yhalo_dev ? yhalo_dev : &dummy, m);
+      cieg::launch_spmm(ctx, mat, x_dev, m, y_dev, m, m, yhalo_dev, m, true);
     } else {
       const int saved = ctx->spmm_mode;
       ctx->spmm_mode = CIEG_SPMM_SINGLE_PASS;

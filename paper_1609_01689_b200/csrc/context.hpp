@@ -137,9 +137,11 @@ struct HostTiles;
 void upload_schedule(cieg_mat* m, const HostTiles& ht);
 
 // Launch the owner-computes SpMM over device X/Y (row-major, ld = ldx/ldy).
-// On a shard, yhalo != nullptr selects the single pass and receives the
-// transposed partials for rows [sp_partial_lo, row_lo) (ld ldh).
+// On a shard, shard_single_pass selects the single pass; yhalo receives
+// the transposed partials for rows [sp_partial_lo, row_lo) (ld ldh; may be
+// null when the shard has no such rows).
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
-                 std::uint32_t ldy, std::uint32_t mcols, double* yhalo = nullptr, std::uint32_t ldh = 0);
+                 std::uint32_t ldy, std::uint32_t mcols, double* yhalo = nullptr, std::uint32_t ldh = 0,
+                 bool shard_single_pass = false);
 
 }  // namespace cieg

@@ -233,7 +233,7 @@ class Solver {
         // back to their owners (SURVEY.md 8(e) reduce-scatter, point to point)
         const std::size_t prow = mat_->row_lo - mat_->sp_partial_lo;
         double* yh = static_cast<double*>(yhalo_.get(sizeof(double) * std::max<std::size_t>(1, prow) * w));
-        launch_spmm(ctx_, mat_, xin, x.w, hx.p, x.w, x.w, yh, x.w);
+        launch_spmm(ctx_, mat_, xin, x.w, hx.p, x.w, x.w, yh, x.w, true);
         if (hooks_->reduce_partials(hooks_->user, yh, x.w, hx.p) != 0)
           fail(CIEG_ERR_ARGUMENT, "reduce_partials hook failed");
         hx.w = x.w;

@@ -944,11 +944,12 @@ unsigned* nonfinite_flag(cieg_ctx* ctx) {
 }
 
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
-                 std::uint32_t ldy, std::uint32_t mcols, double* yhalo, std::uint32_t ldh) {
+                 std::uint32_t ldy, std::uint32_t mcols, double* yhalo, std::uint32_t ldh, bool shard_single_pass) {
   if (mcols == 0 || m->dim == 0) return;
   const bool shard = m->row_lo != 0 || m->row_hi != m->dim;
-  const bool shard_sp = shard && yhalo != nullptr;
+  const bool shard_sp = shard && shard_single_pass;
   if (shard_sp && !m->sp_sched) fail(CIEG_ERR_CONFIG, "single-pass SpMM: the shard has no single-pass schedule");
+  if (shard_sp && !yhalo && m->row_lo > m->sp_partial_lo) fail(CIEG_ERR_ARGUMENT, "single-pass SpMM: null partial buffer");
   if (shard_sp && m->row_lo > m->sp_partial_lo)  // rows without partials read as zero
     CIEG_CUDA(cudaMemset2DAsync(yhalo, sizeof(double) * ldh, 0, sizeof(double) * mcols, m->row_lo - m->sp_partial_lo,
                                 ctx->stream));
@@ -992,7 +993,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
     if (sp) {
       sp_reduce_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
                                                             m->panel_start, y + c0, ldy, mc, m->tile_edge, m->row_lo,
-                                                            shard_sp ? yhalo + c0 : nullptr, ldh, m->sp_partial_lo);
+                                                            shard_sp && yhalo ? yhalo + c0 : nullptr, ldh, m->sp_partial_lo);
       CIEG_CUDA(cudaGetLastError());
       ++ctx->launches;
     }
