@@ -158,6 +158,8 @@ def reference_arm(args):
     cfg = configs.CFG2
     h, _ = gen_matrix(cfg, 0)
     m = cfg.m
+    # every host core the process may use (torchrun exports OMP_NUM_THREADS=1)
+    ref.set_threads(len(os.sched_getaffinity(0)))
     cores = ref.max_threads()
     # Bounded sample: the leading principal submatrix (whole CSB block rows) sized
     # so that warmup + steps stay within ~90 s of CPU time.
@@ -227,6 +229,7 @@ def cpu_baseline(h, m):
 
     if not ref.available():
         return None
+    ref.set_threads(len(os.sched_getaffinity(0)))
     cores = ref.max_threads()
     nbk = max(1, h.block_count() // 4)
     sample = _leading_block(h, nbk)
