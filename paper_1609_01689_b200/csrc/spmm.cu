@@ -754,13 +754,57 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_ws_kernel(const SpmmArgs a) 
               for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], fa[u][j], fb[u][n]);
         };
         constexpr int kGroups = TD / 16;
-        load_group(0, af[0], bf[0]);
+        if constexpr (sizeof(V) == 4) {
+          // A fragments held raw (float4 per m-tile) and widened right before
+          // their DMMAs: the conversions no longer wait on the next group's
+          // loads ahead of the current group's DMMAs
+          float4 ar[2][S::kMT];
+          auto load_raw = [&](int grp, float4 (&o)[S::kMT], double (&fb)[4][NT]) {
+#pragma unroll
+            for (int j = 0; j < S::kMT; ++j) o[j] = *reinterpret_cast<const float4*>(A + j * 8 * S::kSA + 16 * grp);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const double* xr = xb + 4 * (4 * grp + u) * S::kSX;
+              if constexpr (NT == 2) {
+                const double2 v2 = *reinterpret_cast<const double2*>(xr);
+                fb[u][0] = v2.x;
+                fb[u][1] = v2.y;
+              } else {
+#pragma unroll
+                for (int n = 0; n < NT; ++n) fb[u][n] = xr[8 * n];
+              }
+            }
+          };
+          auto mma_raw = [&](const float4 (&o)[S::kMT], const double (&fb)[4][NT]) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              double fa[S::kMT];
+#pragma unroll
+              for (int j = 0; j < S::kMT; ++j)
+                fa[j] = static_cast<double>(u == 0 ? o[j].x : u == 1 ? o[j].y : u == 2 ? o[j].z : o[j].w);
+#pragma unroll
+              for (int n = 0; n < NT; ++n)
+#pragma unroll
+                for (int j = 0; j < S::kMT; ++j) dmma_8x8x4(acc[j][n][0], acc[j][n][1], fa[j], fb[u][n]);
+            }
+          };
+          load_raw(0, ar[0], bf[0]);
 #pragma unroll 1
-        for (int grp = 0; grp < kGroups; grp += 2) {
-          load_group(grp + 1, af[1], bf[1]);
-          mma_group(af[0], bf[0]);
-          if (grp + 2 < kGroups) load_group(grp + 2, af[0], bf[0]);
-          mma_group(af[1], bf[1]);
+          for (int grp = 0; grp < kGroups; grp += 2) {
+            load_raw(grp + 1, ar[1], bf[1]);
+            mma_raw(ar[0], bf[0]);
+            if (grp + 2 < kGroups) load_raw(grp + 2, ar[0], bf[0]);
+            mma_raw(ar[1], bf[1]);
+          }
+        } else {
+          load_group(0, af[0], bf[0]);
+#pragma unroll 1
+          for (int grp = 0; grp < kGroups; grp += 2) {
+            load_group(grp + 1, af[1], bf[1]);
+            mma_group(af[0], bf[0]);
+            if (grp + 2 < kGroups) load_group(grp + 2, af[0], bf[0]);
+            mma_group(af[1], bf[1]);
+          }
         }
       }
       if constexpr (SP) {
