@@ -1,7 +1,8 @@
 """Randomised K1 stress (test infrastructure, not collected by pytest):
 random generator configs and widths, Inf/NaN injection, every SpMM mode and
 world-2 single-pass shards against the oracle's restatement of spmm.
-python tests/stress/spmm_stress.py <seed>   (B200; 120 configs, ~1 min)"""
+python tests/stress/spmm_stress.py <seed> [big]   (B200; 120 configs, ~1 min; "big": CSB
+block bounds up to 65535 rows, n up to 2e5)"""
 import sys, time; import os; sys.path.insert(0, os.path.join(os.path.dirname(__file__), "..", "..")); sys.path.insert(0, os.path.join(os.path.dirname(__file__), ".."))
 import numpy as np
 from conftest import single_pass_shards
@@ -11,11 +12,14 @@ rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 1)
 dev = ci.Device.default()
 bad = 0
 t0 = time.time()
-for it in range(120):
+for it in range(40 if len(sys.argv) > 2 and sys.argv[2] == 'big' else 120):
     sectors = int(rng.integers(1, 6)); tile = int(rng.choice([8, 16, 32, 50, 64, 96, 128, 256]))
-    n = int(rng.integers(max(sectors, 30), 5000)) // sectors * sectors
-    prm = dict(n=n, sectors=sectors, tile=tile, p=float(rng.uniform(0.05, 1.0)), q=float(rng.uniform(0.05, 1.0)),
-               seed=int(rng.integers(1, 1 << 30)), precision=int(rng.integers(0, 2)), beta=max(tile, 256), band=int(rng.integers(0, 4)))
+    big = len(sys.argv) > 2 and sys.argv[2] == "big"  # maximum CSB block bounds, larger dimensions
+    n = int(rng.integers(max(sectors, 30), 200_000 if big else 5000)) // sectors * sectors
+    beta = int(rng.choice([4096, 30000, 65535])) if big else max(tile, 256)
+    prm = dict(n=n, sectors=sectors, tile=tile, p=float(rng.uniform(0.05, 1.0)) * (0.02 if big else 1.0),
+               q=float(rng.uniform(0.05, 1.0)), seed=int(rng.integers(1, 1 << 30)),
+               precision=int(rng.integers(0, 2)), beta=max(beta, tile), band=int(rng.integers(0, 4)))
     m = int(rng.choice([1, 2, 3, 5, 8, 9, 13, 16, 17, 31]))
     h = ci.generate_sector_matrix(prm["n"], prm["sectors"], prm["tile"], prm["p"], prm["q"], prm["seed"], prm["precision"], prm["beta"], band=prm["band"])
     x = ci.random_block(h.dim, m, it)
