@@ -1,0 +1,89 @@
+// umma.cuh -- the few tcgen05 (5th-generation tensor core) primitives K1's
+// integer-slice path uses (spmm_i8.cu): shared-memory matrix descriptors for
+// the no-swizzle canonical layouts, the kind::i8 instruction descriptor,
+// TMEM allocation, MMA issue/commit and TMEM -> register loads. sm_100a only.
+//
+// Canonical no-swizzle layouts (8-bit elements): a "core matrix" is 8 rows x
+// 16 bytes, stored as 128 contiguous bytes.
+//   K-major operand  (rows = M or N, 16 K bytes per core row):
+//     LBO = byte stride between core matrices adjacent in K,
+//     SBO = byte stride between core matrices adjacent in M/N (8-row groups).
+//   MN-major operand (16 M/N bytes per core row, 8 K per core matrix):
+//     LBO = byte stride between core matrices adjacent in K (8-K groups),
+//     SBO = byte stride between core matrices adjacent in M/N (16-byte chunks).
+// A tile stored as 8-row x 16-column core matrices is therefore the K-major
+// A of H*X (M = tile row, K = tile column) and, with LBO/SBO swapped, the
+// MN-major A of H^T*X (M = tile column, K = tile row): one shared-memory copy
+// serves both orientations of a stored tile.
+#pragma once
+
+#include <cstdint>
+
+namespace cieg {
+namespace umma {
+
+__device__ __forceinline__ std::uint32_t smem_u32(const void* p) {
+  return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// Shared-memory matrix descriptor (tcgen05 "matrix descriptor"): start
+// address, LBO, SBO (all >> 4), version 1 (bits 46-47), no swizzle.
+__device__ __forceinline__ std::uint64_t sdesc(std::uint32_t saddr, std::uint32_t lbo, std::uint32_t sbo) {
+  return static_cast<std::uint64_t>((saddr >> 4) & 0x3fffu) | (static_cast<std::uint64_t>((lbo >> 4) & 0x3fffu) << 16) |
+         (static_cast<std::uint64_t>((sbo >> 4) & 0x3fffu) << 32) | (1ull << 46);
+}
+
+// Instruction descriptor, kind::i8, S32 accumulate: a/b signed (1) or
+// unsigned (0), a/b MN-major (1) or K-major (0), shape M x N.
+__host__ __device__ constexpr std::uint32_t idesc_i8(int a_signed, int b_signed, int a_mn, int b_mn, int m, int n) {
+  return (2u << 4) | (static_cast<std::uint32_t>(a_signed) << 7) | (static_cast<std::uint32_t>(b_signed) << 10) |
+         (static_cast<std::uint32_t>(a_mn) << 15) | (static_cast<std::uint32_t>(b_mn) << 16) |
+         (static_cast<std::uint32_t>(n >> 3) << 17) | (static_cast<std::uint32_t>(m >> 4) << 24);
+}
+
+// D[tmem] (+)= A[smem] * B[smem]; issued by one thread.
+__device__ __forceinline__ void mma_i8(std::uint32_t d_tmem, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                       std::uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// Arrive on an mbarrier once every MMA issued so far by this thread completes.
+__device__ __forceinline__ void commit(std::uint64_t* mbar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
+               : "memory");
+}
+
+// TMEM allocation by one full warp; the base address is written to *slot.
+template <int kCols>
+__device__ __forceinline__ void tmem_alloc(std::uint32_t* slot) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)), "n"(kCols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+template <int kCols>
+__device__ __forceinline__ void tmem_free(std::uint32_t base) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(base), "n"(kCols) : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// 16 consecutive 32-bit TMEM columns of this warp's 32 lanes -> 16 registers.
+__device__ __forceinline__ void ld16(std::uint32_t taddr, std::int32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+}  // namespace umma
+}  // namespace cieg
