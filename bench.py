@@ -147,55 +147,69 @@ def gen_matrix(cfg, rank):
     return h, time.time() - t
 
 
+# BASELINE config 2 (the headline workload). Raw parameters here so the
+# reference arm can build it without importing the product package;
+# ours() asserts that configs.CFG2 agrees.
+CFG2_RAW = {"name": "cfg2-spmm", "n": 2_000_000, "sectors": 20, "tile": 256, "q": 0.4, "target_nnz": 0.8e9,
+            "seed": 1, "m": 16, "precision": 0, "beta": 2000}
+
+
+def spmm_config(world, p, nnz):
+    """The config dict both arms print, byte for byte."""
+    c = CFG2_RAW
+    return {"workload": c["name"], "n": c["n"], "sectors": c["sectors"], "tile": c["tile"],
+            "p_calibrated": float(f"{p:.10g}"), "q": c["q"], "seed": c["seed"], "nnz_stored": int(nnz),
+            "m": c["m"], "h_values": "fp32", "x_y": "fp64",
+            "l2": "inputs larger than L2 (H 6.4 GB, X/U 256 MB each); no flush",
+            "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} (X halo exchange)"}
+
+
 def reference_arm(args):
-    """--impl reference: the reference's own ci::spmm on the host cores."""
+    """--impl reference: the reference's own ci::spmm (oracle/_ref, the
+    UNMODIFIED proj/src compiled here) on the host cores. The matrix is built
+    by the oracle's generator (oracle/ref_gen.cpp) straight into the
+    reference's ci::CsbMatrix -- the product library is never loaded."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
-    from paper_1609_01689_b200 import configs
-    from oracle import ref
+    from oracle import ci_oracle, ref
 
-    cfg = configs.CFG2
-    h, _ = gen_matrix(cfg, 0)
-    m = cfg.m
+    c = CFG2_RAW
+    m = c["m"]
+    p = ref.calibrated_p(c["n"], c["sectors"], c["tile"], c["q"], c["target_nnz"])
+    gen = lambda nbk: ref.generate(c["n"], c["sectors"], c["tile"], p, c["q"], c["seed"], c["precision"],
+                                   c["beta"], nbk=nbk)
     # every host core the process may use (torchrun exports OMP_NUM_THREADS=1)
     ref.set_threads(len(os.sched_getaffinity(0)))
     cores = ref.max_threads()
-    # Bounded sample: the leading principal submatrix (whole CSB block rows) sized
-    # so that warmup + steps stay within ~90 s of CPU time.
-    probe = _leading_block(h, max(1, h.block_count() // 16))
-    rp = ref.RefMatrix(probe)
-    xp = np.random.default_rng(0).standard_normal((probe.dim, m))
-    rp.spmm(xp)
-    t0 = time.perf_counter()
-    rp.spmm(xp)
-    t_probe = time.perf_counter() - t0
-    rate = probe.nnz_lower / max(t_probe, 1e-9)
+    nnz_full = ref.count_nnz(c["n"], c["sectors"], c["tile"], p, c["q"], c["seed"])
+    # Bounded sample: the leading principal submatrix (whole CSB block rows)
+    # sized so that warmup + steps stay within ~90 s of CPU time.
+    probe = gen(1)
+    nb = probe.nb_total
+    probe = gen(max(1, nb // 16))
+    xp = ci_oracle.random_block(probe.dim, m, 5)
+    secs, _ = ref.spmm_timed(probe, xp, 2)
+    rate = probe.nnz / max(secs[1], 1e-9)
     budget = 90.0 / max(1, args.steps + args.warmup)
-    frac_nnz = min(1.0, budget * rate / h.nnz_lower)
-    nbk = max(1, min(h.block_count(), int(round(h.block_count() * frac_nnz))))
-    sample = h if nbk == h.block_count() else _leading_block(h, nbk)
-    del rp, probe
-    rm = ref.RefMatrix(sample)
-    x = np.random.default_rng(1).standard_normal((sample.dim, m))
-    for _ in range(args.warmup):
-        rm.spmm(x)
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        rm.spmm(x)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.mean(ts)
-    nbytes = configs.spmm_bytes(sample.nnz_lower, sample.dim, m, sample.precision)
+    frac_nnz = min(1.0, budget * rate / nnz_full)
+    nbk = max(1, min(nb, int(round(nb * frac_nnz))))
+    del probe
+    rm = gen(nbk)
+    x = ci_oracle.random_block(rm.dim, m, 5)
+    secs, _ = ref.spmm_timed(rm, x, args.warmup + args.steps)
+    t = float(np.mean(secs[args.warmup:]))
+    v = 4 if c["precision"] == 0 else 8
+    nbytes = rm.nnz * (v + 4) + 2 * rm.dim * m * 8
     gbs = nbytes / t / 1e9
-    desc = (f"ci::spmm (reference, OpenMP {cores} threads) on the leading {sample.dim} rows "
-            f"({sample.nnz_lower} stored nnz, {100.0 * sample.nnz_lower / h.nnz_lower:.1f}% of config 2), m={m}")
+    desc = (f"ci::spmm (reference, OpenMP {cores} threads, timed inside the library) on the leading {rm.dim} rows "
+            f"({rm.nnz} stored nnz, {100.0 * rm.nnz / nnz_full:.1f}% of config 2), m={m}")
     line = {
         "metric": "spmm_gbs", "value": round(gbs, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64 (fp32 H promoted)", "data": "synthetic (seeded sector generator)",
-        "config": {"workload": cfg.name, "n": cfg.n, "nnz_stored": h.nnz_lower, "m": m, "tile": cfg.tile,
-                   "p": cfg.p(), "q": cfg.q, "sample_rows": sample.dim},
+        "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64 (fp32 H promoted)", "data": "synthetic (seeded sector generator, BASELINE config 2)",
+        "config": spmm_config(world, p, nnz_full),
         "impl": "reference",
         "cpu_baseline": {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
                          "sample": desc},
@@ -222,29 +236,30 @@ def _leading_block(h, nbk):
                         values=h.values[:e], groups=groups, beta=h.beta)
 
 
-def cpu_baseline(h, m):
-    """cpu_baseline record: reference ci::spmm on a bounded sample (~10-20 s)."""
-    from paper_1609_01689_b200 import configs
+def cpu_baseline(h, m, x, y_gpu):
+    """cpu_baseline record: the reference ci::spmm (oracle/_ref) on the FULL
+    config-2 matrix, timed inside the library (3 calls), and the parity check
+    of the GPU result against it (max relative difference)."""
     from oracle import ref
 
     if not ref.available():
-        return None
+        return None, None
     ref.set_threads(len(os.sched_getaffinity(0)))
     cores = ref.max_threads()
-    nbk = max(1, h.block_count() // 4)
-    sample = _leading_block(h, nbk)
-    rm = ref.RefMatrix(sample)
-    x = np.random.default_rng(2).standard_normal((sample.dim, m))
-    rm.spmm(x)
-    ts = []
-    for _ in range(3):
-        t0 = time.perf_counter()
-        rm.spmm(x)
-        ts.append(time.perf_counter() - t0)
-    t = statistics.mean(ts)
-    gbs = configs.spmm_bytes(sample.nnz_lower, sample.dim, m, sample.precision) / t / 1e9
-    return {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
-            "sample": f"ci::spmm x3 on the leading {sample.dim} rows ({sample.nnz_lower} nnz) of config 2, m={m}"}
+    rm = ref.RefMatrix(h)
+    secs, y_ref = ref.spmm_timed(rm, x, 3)
+    t = float(np.mean(secs[1:]))
+    v = 4 if h.precision == 0 else 8
+    gbs = (h.nnz_lower * (v + 4) + 2 * h.dim * m * 8) / t / 1e9
+    scale = np.abs(y_ref).max(axis=0)
+    max_rel = float((np.abs(y_gpu - y_ref).max(axis=0) / scale).max())
+    rec = {"value": round(gbs, 3), "unit": "GB/s", "cores": cores, "kind": "reference",
+           "sample": f"ci::spmm (oracle/_ref) on the full config-2 matrix ({h.dim} rows, {h.nnz_lower} nnz), m={m}, "
+                     f"mean of calls 2-3 timed inside the library"}
+    parity = {"max_rel": max_rel, "norm": "per column, relative to max |U_ref|",
+              "vs": "ci::spmm (unmodified reference, oracle/_ref) on the full config-2 matrix, same X",
+              "tolerance": 1e-13}
+    return rec, parity
 
 
 def lobpcg_record():
@@ -647,6 +662,10 @@ def ours(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     cfg = configs.CFG2
+    raw = CFG2_RAW
+    assert (cfg.name, cfg.n, cfg.sectors, cfg.tile, cfg.q, cfg.target_nnz, cfg.seed, cfg.m, cfg.precision,
+            cfg.beta) == (raw["name"], raw["n"], raw["sectors"], raw["tile"], raw["q"], raw["target_nnz"],
+                          raw["seed"], raw["m"], raw["precision"], raw["beta"]), "CFG2_RAW out of date"
     m = args.m or cfg.m
     dev = ci.Device(local)
     tdev = torch.device("cuda", local)
@@ -746,7 +765,7 @@ def ours(args):
         nbytes = configs.spmm_bytes(dm.nnz, n, m, dm.precision)
         flops = configs.spmm_flops(dm.nnz, n, m)
     else:
-        nnz_total = int(cfg.expected_nnz())
+        nnz_total = ci.count_nnz(cfg.n, cfg.sectors, cfg.tile, cfg.p(), cfg.q, cfg.seed)
         nbytes = configs.spmm_bytes(nnz_total, n, m, 0)
         flops = configs.spmm_flops(nnz_total, n, m)
     gbs = nbytes / (ms * 1e-3) / 1e9
@@ -759,22 +778,17 @@ def ours(args):
     # report the device-resident number end to end through all ranks)
     e2e = None
     if world == 1:
-        # K steps through the host: each step uploads its X from pinned host
-        # memory and downloads its U. cieg_spmm_host_batch pipelines them (the
-        # upload of X_{i+1} and the download of U_{i-1} overlap K1 on U_i);
-        # two pinned host X/U buffers alternate. The one-call-per-step number
-        # (cieg_spmm_host, nothing overlapped) is reported beside it.
-        xhs = [torch.from_numpy(ci.random_block(n, m, 6 + b)).pin_memory() for b in range(2)]
-        yhs = [torch.empty_like(xhs[0]).pin_memory() for _ in range(2)]
+        # The headline: ci::spmm's own host call (the drop-in binds
+        # cieg_spmm_host on the pageable std::vector of ci::BlockVectors):
+        # pageable numpy X/U, H2D + K1 + D2H inside each timed call. The
+        # pinned-buffer single call and the pipelined pinned batch
+        # (cieg_spmm_host_batch, copies of neighbouring steps overlapping K1)
+        # are reported beside it.
         pd = ctypes.POINTER(ctypes.c_double)
-        xp = [ctypes.cast(t.data_ptr(), pd) for t in xhs]
-        yp = [ctypes.cast(t.data_ptr(), pd) for t in yhs]
-        ke = max(3, min(args.steps, 20))  # pipeline fill + drain amortised over the batch
-        xs = (pd * ke)(*[xp[i % 2] for i in range(ke)])
-        ys = (pd * ke)(*[yp[i % 2] for i in range(ke)])
         own = torch.cuda.ExternalStream(dev.stream, device=tdev)
+        ke = max(3, min(args.steps, 20))
 
-        def timed(fn):
+        def timed(fn, reps):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
@@ -783,7 +797,25 @@ def ours(args):
             fn()
             e1.record(own)
             e1.synchronize()
-            return e0.elapsed_time(e1) / ke, (time.perf_counter() - w0) * 1e3 / ke
+            return e0.elapsed_time(e1) / reps, (time.perf_counter() - w0) * 1e3 / reps
+
+        xpg = [ci.random_block(n, m, 6 + b) for b in range(2)]
+        ypg = [np.empty_like(xpg[0]) for _ in range(2)]
+        xpp = [ctypes.cast(a.ctypes.data, pd) for a in xpg]
+        ypp = [ctypes.cast(a.ctypes.data, pd) for a in ypg]
+
+        def pageable():
+            for i in range(ke):
+                ci._check(lib.cieg_spmm_host(dev.handle, dm.handle, xpp[i % 2], ypp[i % 2], m))
+
+        pageable()  # warm (staging ring, page faults of the fresh numpy buffers)
+        ms_e2e, wall_e2e = timed(pageable, ke)
+        xhs = [torch.from_numpy(a).pin_memory() for a in xpg]
+        yhs = [torch.empty_like(xhs[0]).pin_memory() for _ in range(2)]
+        xp = [ctypes.cast(t.data_ptr(), pd) for t in xhs]
+        yp = [ctypes.cast(t.data_ptr(), pd) for t in yhs]
+        xs = (pd * ke)(*[xp[i % 2] for i in range(ke)])
+        ys = (pd * ke)(*[yp[i % 2] for i in range(ke)])
 
         def batch():
             ci._check(lib.cieg_spmm_host_batch(dev.handle, dm.handle, xs, ys, m, ke))
@@ -793,14 +825,17 @@ def ours(args):
                 ci._check(lib.cieg_spmm_host(dev.handle, dm.handle, xp[i % 2], yp[i % 2], m))
 
         batch()  # warm (allocates the second device buffers)
-        runs = sorted((timed(batch) for _ in range(3)), key=lambda t: t[0])
-        ms_e2e, wall_e2e = runs[1]  # median of three K-step batches
-        ms_single, _ = timed(single)
-        e2e = {"value": round(nbytes / (ms_e2e * 1e-3) / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": n * m * 8,
-               "d2h_bytes_per_step": n * m * 8, "ms_per_step": round(ms_e2e, 4), "wall_ms_per_step": round(wall_e2e, 4),
-               "steps": ke, "call": "cieg_spmm_host_batch (pinned host X/U; copies of neighbouring steps overlap K1)",
-               "unpipelined": {"value": round(nbytes / (ms_single * 1e-3) / 1e9, 3), "ms_per_step": round(ms_single, 4),
-                               "call": "cieg_spmm_host per step"}}
+        ms_batch, _ = sorted((timed(batch, ke) for _ in range(3)), key=lambda t: t[0])[1]
+        ms_single, _ = timed(single, ke)
+        gb = lambda t: round(nbytes / (t * 1e-3) / 1e9, 3)
+        e2e = {"value": gb(ms_e2e), "unit": "GB/s", "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": n * m * 8,
+               "ms_per_step": round(ms_e2e, 4), "wall_ms_per_step": round(wall_e2e, 4), "steps": ke,
+               "call": "cieg_spmm_host per step on pageable host X/U (ci::spmm's call in the drop-in; chunked "
+                       "pinned staging ring inside the library)",
+               "pinned": {"value": gb(ms_single), "ms_per_step": round(ms_single, 4),
+                          "call": "cieg_spmm_host per step, pinned host X/U"},
+               "pinned_batch": {"value": gb(ms_batch), "ms_per_step": round(ms_batch, 4),
+                                "call": "cieg_spmm_host_batch (pinned; copies of neighbouring steps overlap K1)"}}
     else:
         # every rank: its rows of X from pinned host memory, the halo exchange
         # and K1, its rows of U back to pinned host memory (max over ranks)
@@ -836,6 +871,8 @@ def ours(args):
                "call": "per rank: pinned host rows of X -> device, halo exchange + K1, rows of U -> pinned host "
                        "(bytes summed over ranks; time max over ranks)"}
     tile_edge, ntiles, npanels = dm.tile_edge, dm.ntiles, dm.npanels
+    if world == 1:  # the timed steps' input and output, for the parity check against the reference
+        x_host, y_host = x_full.cpu().numpy(), y.cpu().numpy()
     del dm  # the records below build their own matrices
     torch.cuda.empty_cache()
     cfg5 = None
@@ -858,12 +895,9 @@ def ours(args):
         "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f64 (fp32 H promoted exactly)",
         "data": "synthetic (seeded sector generator, BASELINE config 2)",
-        "config": {"workload": cfg.name, "n": n, "nnz_stored": int(nnz_total), "m": m, "tile": cfg.tile,
-                   "p": round(cfg.p(), 8), "q": cfg.q, "device_tile_edge": tile_edge, "device_tiles": ntiles,
-                   "l2": "inputs larger than L2 (H 6.4 GB, X/U 256 MB each); no flush",
-                   "parallelism": "single GPU" if world == 1 else f"row-block shards x{world} (X halo exchange)",
-                   "exchange": exchange,
-                   "gen_s": round(t_gen, 1), "upload_s": round(t_up, 1)},
+        "config": spmm_config(world, cfg.p(), nnz_total),
+        "setup": {"device_tile_edge": tile_edge, "device_tiles": ntiles, "exchange": exchange,
+                  "gen_s": round(t_gen, 1), "upload_s": round(t_up, 1)},
         "roofline": roofline(gbs, flops / (ms * 1e-3) / 1e12, peak, peak_kind, nbytes, flops, cfg.name,
                              issued_flops=issued, ms=ms),
         "e2e": e2e,
@@ -875,7 +909,7 @@ def ours(args):
     if shard_modes is not None:
         line["shard_modes_m8"] = shard_modes
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(h, m)
+        line["cpu_baseline"], line["parity"] = cpu_baseline(h, m, x_host, y_host)
     if world == 1 and not args.no_lobpcg:
         line["lobpcg"] = lobpcg_record()
         line["lanczos"] = lanczos_record()

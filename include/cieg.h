@@ -82,7 +82,12 @@ int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact);
  * transposed half reduced through per-tile partials (unsharded matrices;
  * shards stay owner-computes). All modes are deterministic. Replaces no
  * reference call: spmm (csb.cpp:118-193) has one code path. */
-enum { CIEG_SPMM_AUTO = 0, CIEG_SPMM_OWNER = 1, CIEG_SPMM_SINGLE_PASS = 2 };
+/* CIEG_SPMM_SLICED = the single pass on the int8 tensor cores (tcgen05):
+ * H and X split into exact 8-bit integer slices (Ozaki scheme), int32
+ * accumulators in TMEM, recombined in fp64 -- fp32 H with 128-row panels on
+ * unsharded matrices; agrees with the fp64 modes to rounding (~1e-16), not
+ * bit for bit. AUTO picks it for widths >= 9 where supported. */
+enum { CIEG_SPMM_AUTO = 0, CIEG_SPMM_OWNER = 1, CIEG_SPMM_SINGLE_PASS = 2, CIEG_SPMM_SLICED = 3 };
 int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode);
 /* Number of kernels this context has launched (instrumentation). */
 uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx);
@@ -408,6 +413,8 @@ typedef struct {
 double cieg_gen_expected_nnz(const cieg_gen_params* prm);
 /* Expected full-row off-diagonal count used for the value scale. */
 double cieg_gen_avg_row_nnz(const cieg_gen_params* prm);
+/* Exact stored-entry count of the generated matrix (0 on bad parameters). */
+uint64_t cieg_gen_count_nnz(const cieg_gen_params* prm);
 int cieg_generate_csb(const cieg_gen_params* prm, cieg_host_csb** out);
 int cieg_host_csb_destroy(cieg_host_csb* h);
 /* Borrowed views into the generated matrix (valid until destroy). */

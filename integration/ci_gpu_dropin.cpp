@@ -2,14 +2,21 @@
 // reference's own ci:: entry points (declared in
 // /root/reference/proj/include/ci/*.hpp, compiled against those headers) on
 // top of the C ABI in include/cieg.h. Linking this TU (plus libcieg.so) in
-// place of proj/src/{csb,block_vectors,lobpcg,precond}.cpp makes every caller
-// of ci::spmm / ci::lobpcg_solve / ci::apply_preconditioner run on the B200.
+// place of proj/src/{csb,block_vectors,lobpcg,precond,lanczos}.cpp (with
+// ci_host_companion.cpp for their non-hot symbols) makes every caller of
+// ci::spmm / ci::lobpcg_solve / ci::block_inner / ci::apply_preconditioner
+// ... run on the B200; basis, grouping, hamiltonian, guess, planner and config
+// stay the reference's own TUs (integration/Makefile links exactly that and
+// tests/test_integration_gpu.py runs it against the all-reference build).
 //
 // Contract mapping:
 //   * value semantics stay: inputs by const&, results by value;
-//   * H is uploaded once per CsbMatrix (cached by address + nnz_lower) and
-//     the TileDiagonal once per object -- the reference's non-owning
-//     LobpcgOptions::preconditioner pointer is the cache key;
+//   * uploaded H and tile diagonals are cached by object address AND a
+//     content fingerprint (dimensions, entry counts, buffer addresses and a
+//     spread sample of the stored entries / block values), re-uploaded when
+//     it changes -- a new matrix built at the same address (the CLI's
+//     `compare` loop, one Problem per seed) is never served stale;
+//     cieg_dropin_invalidate() drops every cached upload explicitly;
 //   * cieg_status != 0 is rethrown as the matching ci:: exception with the
 //     library's "<Type>: message" text; no exception crosses the C ABI.
 // Built by integration/Makefile (needs the reference headers; Eigen comes from
@@ -56,16 +63,80 @@ inline void check(int st) {
 
 struct Device {
   cieg_ctx* ctx = nullptr;
-  std::map<const ci::CsbMatrix*, std::pair<std::uint64_t, cieg_mat*>> mats;
-  std::map<const ci::TileDiagonal*, cieg_prec*> precs;
+  struct MatEntry {
+    std::uint64_t fp = 0;
+    cieg_mat* mat = nullptr;
+  };
+  struct PrecEntry {
+    std::uint64_t fp = 0;
+    cieg_prec* prec = nullptr;
+  };
+  std::map<const ci::CsbMatrix*, MatEntry> mats;
+  std::map<const ci::TileDiagonal*, PrecEntry> precs;
   Device() {
     const char* d = std::getenv("CIEG_DEVICE");
     check(cieg_ctx_create(d ? std::atoi(d) : 0, &ctx));
+  }
+  void clear() {
+    for (auto& [k, e] : mats) cieg_matrix_destroy(e.mat);
+    for (auto& [k, e] : precs) cieg_precond_destroy(e.prec);
+    mats.clear();
+    precs.clear();
   }
 };
 Device& dev() {
   static Device d;
   return d;
+}
+
+// FNV-1a over the fields that identify an upload's content.
+struct Fnv {
+  std::uint64_t h = 1469598103934665603ull;
+  template <typename T>
+  void add(const T& v) {
+    const auto* p = reinterpret_cast<const unsigned char*>(&v);
+    for (std::size_t i = 0; i < sizeof(T); ++i) h = (h ^ p[i]) * 1099511628211ull;
+  }
+};
+
+std::uint64_t fingerprint(const ci::CsbMatrix& h) {
+  Fnv f;
+  f.add(h.dim);
+  f.add(h.nnz_lower);
+  f.add(static_cast<int>(h.precision));
+  for (std::uint32_t b : h.layout.block_boundaries) f.add(b);
+  for (const ci::CoordinateBlock& b : h.blocks) {
+    const std::size_t n = b.size();
+    if (n == 0) continue;
+    f.add(n);
+    f.add(b.rows.data());
+    f.add(b.values32.data());
+    f.add(b.values64.data());
+    // up to 8 entries spread over the block
+    const std::size_t step = std::max<std::size_t>(1, n / 8);
+    for (std::size_t e = 0; e < n; e += step) {
+      f.add(b.rows[e]);
+      f.add(b.cols[e]);
+      if (!b.values32.empty()) f.add(b.values32[e]);
+      if (!b.values64.empty()) f.add(b.values64[e]);
+    }
+  }
+  return f.h;
+}
+
+std::uint64_t fingerprint(const ci::TileDiagonal& t) {
+  Fnv f;
+  f.add(t.blocks.size());
+  for (std::size_t g = 0; g < t.blocks.size(); ++g) {
+    const Eigen::MatrixXd& b = t.blocks[g];
+    f.add(t.ranges[g].first);
+    f.add(t.ranges[g].second);
+    f.add(b.data());
+    const long n = b.rows() * b.cols();
+    const long step = std::max<long>(1, n / 8);
+    for (long e = 0; e < n; e += step) f.add(b.data()[e]);
+  }
+  return f.h;
 }
 
 // Flatten the CsbMatrix block grid into the cieg_csb_view arrays.
@@ -95,29 +166,41 @@ std::unique_ptr<Flat> flatten(const ci::CsbMatrix& h) {
 }
 
 cieg_mat* matrix(const ci::CsbMatrix& h) {
+  const std::uint64_t fp = fingerprint(h);
   auto& m = dev().mats[&h];
-  if (!m.second || m.first != h.nnz_lower) {
-    if (m.second) cieg_matrix_destroy(m.second);
+  if (!m.mat || m.fp != fp) {
+    if (m.mat) cieg_matrix_destroy(m.mat);
+    m.mat = nullptr;
     auto f = flatten(h);
-    check(cieg_matrix_upload(dev().ctx, &f->view, nullptr, 0, 0, &m.second));
-    m.first = h.nnz_lower;
+    check(cieg_matrix_upload(dev().ctx, &f->view, nullptr, 0, 0, &m.mat));
+    m.fp = fp;
   }
-  return m.second;
+  return m.mat;
+}
+
+cieg_prec* upload_tiles(const ci::TileDiagonal& t) {
+  std::vector<std::uint32_t> bounds{t.ranges.empty() ? 0u : t.ranges.front().first};
+  std::vector<double> blocks;
+  for (std::size_t g = 0; g < t.blocks.size(); ++g) {
+    bounds.push_back(t.ranges[g].second);
+    blocks.insert(blocks.end(), t.blocks[g].data(), t.blocks[g].data() + t.blocks[g].size());
+  }
+  cieg_tilediag_view v{bounds.back(), static_cast<std::uint32_t>(t.blocks.size()), bounds.data(), blocks.data()};
+  cieg_prec* p = nullptr;
+  check(cieg_precond_upload(dev().ctx, &v, &p));
+  return p;
 }
 
 cieg_prec* precond(const ci::TileDiagonal& t) {
-  cieg_prec*& p = dev().precs[&t];
-  if (!p) {
-    std::vector<std::uint32_t> bounds{0};
-    std::vector<double> blocks;
-    for (std::size_t g = 0; g < t.blocks.size(); ++g) {
-      bounds.push_back(t.ranges[g].second);
-      blocks.insert(blocks.end(), t.blocks[g].data(), t.blocks[g].data() + t.blocks[g].size());
-    }
-    cieg_tilediag_view v{bounds.back(), static_cast<std::uint32_t>(t.blocks.size()), bounds.data(), blocks.data()};
-    check(cieg_precond_upload(dev().ctx, &v, &p));
+  const std::uint64_t fp = fingerprint(t);
+  auto& e = dev().precs[&t];
+  if (!e.prec || e.fp != fp) {
+    if (e.prec) cieg_precond_destroy(e.prec);
+    e.prec = nullptr;
+    e.prec = upload_tiles(t);
+    e.fp = fp;
   }
-  return p;
+  return e.prec;
 }
 
 cieg_precond_config config(const ci::PrecondConfig& c) {
@@ -310,54 +393,111 @@ std::vector<double> residual_norms(const CsbMatrix& h, const BlockVectors& x, co
   return out;
 }
 
-// guess.hpp:21 -- host logic.
-BlockVectors pad_from_subspace(const BlockVectors& x1, std::uint32_t dim) {
-  BlockVectors out(dim, x1.width());
-  check(cieg_pad_from_subspace(x1.values().data(), x1.dim(), x1.width(), dim, out.values().data()));
+
+// ---- block_vectors.hpp:60-75 -- the tall-skinny kernels (K2/K3) ------------
+// block_vectors.hpp:60 -- X^T Y, fixed-order device reduction (deterministic
+// like the reference's panel order, block_vectors.cpp:74-85).
+Eigen::MatrixXd block_inner(const BlockVectors& x, const BlockVectors& y) {
+  if (x.dim() != y.dim()) throw DimensionMismatch("block_inner: row counts differ");
+  Eigen::MatrixXd g = Eigen::MatrixXd::Zero(x.width(), y.width());
+  if (x.dim() == 0 || x.width() == 0 || y.width() == 0) return g;
+  DevBlock dx(x.values().data(), x.values().size()), dy(y.values().data(), y.values().size());
+  check(cieg_block_inner(dev().ctx, x.dim(), dx.d(), x.width(), dy.d(), y.width(), g.data()));
+  return g;
+}
+Eigen::MatrixXd block_inner_serial(const BlockVectors& x, const BlockVectors& y) { return block_inner(x, y); }
+
+// block_vectors.hpp:64 -- Y G.
+BlockVectors linear_combination(const BlockVectors& y, const Eigen::MatrixXd& g) {
+  if (static_cast<std::uint32_t>(g.rows()) != y.width())
+    throw DimensionMismatch("linear_combination: G rows != block width");
+  const auto kout = static_cast<std::uint32_t>(g.cols());
+  BlockVectors out(y.dim(), kout);
+  if (y.dim() == 0 || kout == 0) return out;
+  if (y.width() == 0) return out;  // empty sum
+  DevBlock dy(y.values().data(), y.values().size()), dout(nullptr, out.values().size());
+  check(cieg_linear_combination(dev().ctx, y.dim(), dy.d(), y.width(), g.data(), kout, dout.d()));
+  dout.to_host(out.values().data(), out.values().size());
+  return out;
+}
+BlockVectors linear_combination_serial(const BlockVectors& y, const Eigen::MatrixXd& g) {
+  return linear_combination(y, g);
+}
+
+// block_vectors.hpp:68 -- Y += X G.
+void add_linear_combination(BlockVectors& y, const BlockVectors& x, const Eigen::MatrixXd& g) {
+  if (x.dim() != y.dim()) throw DimensionMismatch("add_linear_combination: dims");
+  if (static_cast<std::uint32_t>(g.rows()) != x.width() || static_cast<std::uint32_t>(g.cols()) != y.width())
+    throw DimensionMismatch("add_linear_combination: G shape");
+  if (y.dim() == 0 || y.width() == 0 || x.width() == 0) return;
+  DevBlock dy(y.values().data(), y.values().size()), dx(x.values().data(), x.values().size());
+  check(cieg_add_linear_combination(dev().ctx, y.dim(), dy.d(), y.width(), dx.d(), x.width(), g.data()));
+  dy.to_host(y.values().data(), y.values().size());
+}
+
+// block_vectors.hpp:72 -- host (hash of (seed, row, col); rng.hpp).
+BlockVectors random_block(std::uint32_t dim, std::uint32_t width, std::uint64_t seed) {
+  BlockVectors out(dim, width);
+  if (dim && width) check(cieg_random_block(dim, width, seed, out.values().data()));
   return out;
 }
 
-// guess.hpp:66-69 -- BVEC files (host I/O), the load orthonormalized on the GPU.
-void save_vectors(const BlockVectors& x, const std::string& path) {
-  std::ofstream os(path, std::ios::binary);
-  if (!os) throw FormatError("cannot open for writing: " + path);
-  os.write("BVEC", 4);
-  const std::uint64_t dim = x.dim();
-  const std::uint32_t width = x.width();
-  os.write(reinterpret_cast<const char*>(&dim), sizeof dim);
-  os.write(reinterpret_cast<const char*>(&width), sizeof width);
-  for (std::uint32_t j = 0; j < width; ++j)
-    for (std::uint32_t i = 0; i < x.dim(); ++i) {
-      const double v = x.at(i, j);
-      os.write(reinterpret_cast<const char*>(&v), sizeof v);
-    }
+// block_vectors.hpp:75 -- only the Gram diagonal is formed on the device.
+std::vector<double> column_norms(const BlockVectors& x) {
+  std::vector<double> out(x.width(), 0.0);
+  if (x.dim() == 0 || x.width() == 0) return out;
+  DevBlock dx(x.values().data(), x.values().size());
+  check(cieg_column_norms(dev().ctx, x.dim(), dx.d(), x.width(), out.data()));
+  return out;
 }
 
-BlockVectors load_guess_file(const std::string& path, std::uint32_t dim, std::uint32_t k) {
-  std::ifstream is(path, std::ios::binary);
-  if (!is) throw FormatError("cannot open: " + path);
-  char magic[4];
-  is.read(magic, 4);
-  if (!is || std::memcmp(magic, "BVEC", 4) != 0) throw FormatError("bad magic; not a BVEC file: " + path);
-  std::uint64_t file_dim = 0;
-  std::uint32_t width = 0;
-  is.read(reinterpret_cast<char*>(&file_dim), sizeof file_dim);
-  is.read(reinterpret_cast<char*>(&width), sizeof width);
-  if (!is) throw FormatError("truncated BVEC header: " + path);
-  if (file_dim != dim)
-    throw DimensionMismatch("vector file dimension " + std::to_string(file_dim) + " != basis dimension " +
-                            std::to_string(dim));
-  if (width < k)
-    throw DimensionMismatch("vector file holds " + std::to_string(width) + " columns, need " + std::to_string(k));
-  BlockVectors out(dim, k);
-  for (std::uint32_t j = 0; j < k; ++j)
-    for (std::uint32_t i = 0; i < dim; ++i) {
-      double v;
-      is.read(reinterpret_cast<char*>(&v), sizeof v);
-      if (!is) throw FormatError("truncated BVEC payload: " + path);
-      out.at(i, j) = v;
-    }
-  return orthonormalize(out);
+// ---- precond.hpp:53-61 -- the tile preconditioner (K5) ---------------------
+BlockVectors apply_preconditioner(const TileDiagonal& tiles, const BlockVectors& r, const ShiftPlan& plan,
+                                  const PrecondConfig& cfg) {
+  if (plan.mu.size() != r.width() || plan.engage.size() != r.width())
+    throw DimensionMismatch("apply_preconditioner: plan width != residual width");
+  if (tiles.group_count() > 0 && tiles.ranges.back().second != r.dim())
+    throw DimensionMismatch("apply_preconditioner: tiles do not cover the basis");
+  if (tiles.group_count() == 0 || r.dim() == 0 || r.width() == 0) return r;  // nothing to solve: pass-through
+  BlockVectors w(r.dim(), r.width());
+  std::vector<int> en(plan.engage.begin(), plan.engage.end());
+  cieg_precond_config c = config(cfg);
+  DevBlock dr(r.values().data(), r.values().size()), dw(nullptr, w.values().size());
+  check(cieg_precond_apply(dev().ctx, precond(tiles), dr.d(), r.width(), plan.mu.data(), en.data(), &c, dw.d()));
+  dw.to_host(w.values().data(), w.values().size());
+  return w;
+}
+
+// precond.hpp:60-61 -- FOM on one dense block: a one-group tile diagonal
+// applied with the direct-solve cutoff at 0 (every group takes FOM) and
+// inner_iters = iters (the device FOM keeps PrecondConfig's 1..3 range).
+Eigen::MatrixXd fom_solve(const Eigen::MatrixXd& block, const std::vector<double>& mu, const Eigen::MatrixXd& rhs,
+                          int iters) {
+  if (iters < 1) throw ConfigError("fom_solve: iters must be >= 1");
+  const auto n = static_cast<std::uint32_t>(block.rows());
+  const auto k = static_cast<std::uint32_t>(rhs.cols());
+  if (mu.size() != k) throw DimensionMismatch("fom_solve: one shift per right-hand side");
+  Eigen::MatrixXd x = Eigen::MatrixXd::Zero(n, k);
+  if (n == 0 || k == 0) return x;
+  const std::uint32_t bounds[2] = {0, n};
+  cieg_tilediag_view v{n, 1, bounds, block.data()};
+  cieg_prec* p = nullptr;
+  check(cieg_precond_upload(dev().ctx, &v, &p));
+  std::unique_ptr<cieg_prec, int (*)(cieg_prec*)> guard(p, cieg_precond_destroy);
+  cieg_precond_config c;
+  cieg_precond_config_default(&c);
+  c.small_block_cutoff = 0;
+  c.inner_iters = iters;
+  std::vector<double> rrow(static_cast<std::size_t>(n) * k);  // row major
+  for (std::uint32_t i = 0; i < n; ++i)
+    for (std::uint32_t j = 0; j < k; ++j) rrow[static_cast<std::size_t>(i) * k + j] = rhs(i, j);
+  std::vector<int> en(k, 1);
+  DevBlock dr(rrow.data(), rrow.size()), dw(nullptr, rrow.size());
+  check(cieg_precond_apply(dev().ctx, p, dr.d(), k, mu.data(), en.data(), &c, dw.d()));
+  dw.to_host(rrow.data(), rrow.size());
+  for (std::uint32_t i = 0; i < n; ++i)
+    for (std::uint32_t j = 0; j < k; ++j) x(i, j) = rrow[static_cast<std::size_t>(i) * k + j];
+  return x;
 }
 
 }  // namespace ci
@@ -479,3 +619,7 @@ extern "C" int dropin_residual_norms(const cieg_csb_view* v, const double* x, st
     return 1;
   }
 }
+
+// Drop every cached upload (matrices and tile diagonals); the next call
+// re-uploads. For callers that mutate a CsbMatrix / TileDiagonal in place.
+extern "C" void cieg_dropin_invalidate() { dev().clear(); }

@@ -232,7 +232,7 @@ def lobpcg_solve(refmat: RefMatrix, x0, k_want, tol, max_iter=500, tilediag: Ref
     _chk(load().ciref_lobpcg_solve(refmat.handle, _p(x0), C.c_uint32(x0.shape[1]), C.c_int(k_want), C.c_double(tol),
                                    C.c_int(max_iter), None if tilediag is None else tilediag.handle,
                                    None if ca is None else _p(ca), C.byref(out)))
-    return _report(out, refmat.h.dim)
+    return _report(out, refmat.h.dim if refmat.h is not None else refmat.dim)
 
 
 def lanczos_solve(refmat: RefMatrix, v0, k_want, tol, max_iter=500):
@@ -321,3 +321,62 @@ def residual_norms(refmat, x, theta, norm_est=None):
     _chk(load().ciref_residual_norms(refmat.handle, _p(x), C.c_uint32(x.shape[1]), _p(th),
                                      C.c_double(norm_est if norm_est is not None else 0.0), _p(out)))
     return out
+
+
+# --------------------------------------------------------------- generator
+# ref_gen.cpp: the BASELINE sector generator restated for the oracle, building
+# the reference's own ci::CsbMatrix without the product library.
+
+def generate(n, sectors, tile, p, q, seed, precision, beta=2000, band=2, nbk=0):
+    """ci::CsbMatrix of the leading nbk CSB block rows (0: all) of the sector
+    matrix -> a handle-only RefMatrix (its .nnz / .nb_total are set)."""
+    lib = load()
+    out, nnz, nbt = C.c_void_p(), C.c_uint64(), C.c_uint32()
+    rc = lib.ciref_generate(C.c_uint64(n), C.c_uint32(sectors), C.c_uint32(tile), C.c_double(p), C.c_double(q),
+                            C.c_uint64(seed), C.c_int(precision), C.c_uint32(beta), C.c_uint32(band),
+                            C.c_uint32(nbk), C.c_int(0), C.byref(out), C.byref(nnz), C.byref(nbt))
+    if rc:
+        raise RefError("ciref_generate failed")
+    obj = RefMatrix.__new__(RefMatrix)
+    obj.h = None
+    obj.handle = out
+    obj._fin = weakref.finalize(obj, lib.ciref_matrix_destroy, out)
+    obj.nnz = nnz.value
+    obj.nb_total = nbt.value
+    obj.dim = obj.summary()[0]
+    return obj
+
+
+def count_nnz(n, sectors, tile, p, q, seed, band=2):
+    """Stored entries of the full sector matrix (no storage)."""
+    lib = load()
+    nnz, nbt = C.c_uint64(), C.c_uint32()
+    rc = lib.ciref_generate(C.c_uint64(n), C.c_uint32(sectors), C.c_uint32(tile), C.c_double(p), C.c_double(q),
+                            C.c_uint64(seed), C.c_int(0), C.c_uint32(2000), C.c_uint32(band), C.c_uint32(0),
+                            C.c_int(1), None, C.byref(nnz), C.byref(nbt))
+    if rc:
+        raise RefError("ciref_generate (count) failed")
+    return nnz.value
+
+
+def expected_nnz(n, sectors, tile, p, q, band=2):
+    lib = load()
+    lib.ciref_generate_expected_nnz.restype = C.c_double
+    return lib.ciref_generate_expected_nnz(C.c_uint64(n), C.c_uint32(sectors), C.c_uint32(tile), C.c_double(p),
+                                           C.c_double(q), C.c_uint32(band))
+
+
+def calibrated_p(n, sectors, tile, q, target_nnz, band=2):
+    """p giving target_nnz expected stored entries (configs.Config.p restated)."""
+    s0 = expected_nnz(n, sectors, tile, 0.0, q, band)
+    s1 = expected_nnz(n, sectors, tile, 1.0, q, band)
+    return (target_nnz - s0) / (s1 - s0)
+
+
+def spmm_timed(rm, x, reps):
+    """ci::spmm timed inside the reference library: per-call seconds and U."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty_like(x)
+    secs = np.empty(reps)
+    _chk(load().ciref_spmm_timed(rm.handle, _p(x), C.c_uint32(x.shape[1]), C.c_int(reps), _p(secs), _p(y)))
+    return secs, y

@@ -9,6 +9,7 @@
 // Never linked into the product.
 #include <omp.h>
 
+#include <chrono>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -134,6 +135,24 @@ int ciref_spmm(void* h, const double* x, std::uint32_t m, double* y, int serial)
     ci::BlockVectors X = to_bv(x, H.dim, m);
     ci::BlockVectors U = serial ? ci::spmm_serial(H, X) : ci::spmm(H, X);
     from_bv(U, y);
+  });
+}
+
+// ci::spmm timed on its own: X is built once outside the timed region, each
+// rep times exactly one ci::spmm call (csb.cpp:182-193: its own allocation of
+// U included, as every caller pays it), the last U is copied out afterwards.
+int ciref_spmm_timed(void* h, const double* x, std::uint32_t m, int reps, double* secs, double* y) {
+  return guard([&] {
+    const ci::CsbMatrix& H = *static_cast<ci::CsbMatrix*>(h);
+    const ci::BlockVectors X = to_bv(x, H.dim, m);
+    ci::BlockVectors U;
+    for (int r = 0; r < reps; ++r) {
+      const auto t0 = std::chrono::steady_clock::now();
+      U = ci::spmm(H, X);
+      const auto t1 = std::chrono::steady_clock::now();
+      secs[r] = std::chrono::duration<double>(t1 - t0).count();
+    }
+    if (y) from_bv(U, y);
   });
 }
 

@@ -195,6 +195,7 @@ SIGNATURES = {
     "cieg_report_timing": (_i, [_vp, _pd]),
     "cieg_gen_expected_nnz": (_d, [C.POINTER(GenParams)]),
     "cieg_gen_avg_row_nnz": (_d, [C.POINTER(GenParams)]),
+    "cieg_gen_count_nnz": (C.c_uint64, [C.POINTER(GenParams)]),
     "cieg_generate_csb": (_i, [C.POINTER(GenParams), C.POINTER(_vp)]),
     "cieg_host_csb_destroy": (_i, [_vp]),
     "cieg_host_csb_view": (_i, [_vp, C.POINTER(CsbView), _pu64]),

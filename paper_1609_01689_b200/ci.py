@@ -130,7 +130,7 @@ class Device:
         fixed-order reductions."""
         _check(_lib.load().cieg_ctx_set_exact_order(self.handle, 1 if exact else 0))
 
-    SPMM_MODES = {"auto": 0, "owner": 1, "single": 2}
+    SPMM_MODES = {"auto": 0, "owner": 1, "single": 2, "sliced": 3}
 
     def set_spmm_mode(self, mode: str) -> None:
         """SpMM mode: "auto" (default: single pass for widths <= 8 on
@@ -271,6 +271,12 @@ def generated_panels(n, sectors, tile, p=0.5, q=0.5, precision=0, beta=2000, ban
 def expected_nnz(n, sectors, tile, p, q, band=2) -> float:
     prm = gen_params(n, sectors, tile, p, q, band=band)
     return float(_lib.load().cieg_gen_expected_nnz(C.byref(prm)))
+
+
+def count_nnz(n, sectors, tile, p, q, seed, band=2) -> int:
+    """Exact stored-entry count of generate_sector_matrix(...) without building it."""
+    prm = gen_params(n, sectors, tile, p, q, seed=seed, band=band)
+    return int(_lib.load().cieg_gen_count_nnz(C.byref(prm)))
 
 
 def avg_row_nnz(n, sectors, tile, p, q, band=2) -> float:

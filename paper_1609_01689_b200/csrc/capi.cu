@@ -30,6 +30,7 @@ T* upload_vec(const std::vector<T>& v) {
 }  // namespace cieg
 
 cieg_mat::~cieg_mat() {
+  cieg::destroy_sliced(this);
   if (!borrowed_stream) {
     cudaFree(panel_start);
     cudaFree(tile_off);
@@ -146,6 +147,9 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   ctx->scratch_partial.release();
   for (auto& b : ctx->solver_pool) b.release();
   ctx->pinned_small.release();
+  ctx->pinned_stage.release();
+  for (auto& e : ctx->stage_ev)
+    if (e) cudaEventDestroy(e);
   cudaStreamSynchronize(ctx->own_stream);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;
@@ -404,7 +408,7 @@ int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact) {
 int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode) {
   return cieg::guarded([&] {
     if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");
-    if (mode < CIEG_SPMM_AUTO || mode > CIEG_SPMM_SINGLE_PASS) cieg::fail(CIEG_ERR_ARGUMENT, "unknown SpMM mode");
+    if (mode < CIEG_SPMM_AUTO || mode > CIEG_SPMM_SLICED) cieg::fail(CIEG_ERR_ARGUMENT, "unknown SpMM mode");
     ctx->spmm_mode = mode;
   });
 }
@@ -450,6 +454,81 @@ int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y
 }
 
 
+namespace {
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+// Host copy of one staging chunk, split over the OpenMP threads.
+void par_copy(void* dst, const void* src, std::size_t bytes) {
+  constexpr std::size_t kPiece = 1u << 20;
+  const std::int64_t pieces = static_cast<std::int64_t>((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) if (pieces > 1)
+  for (std::int64_t i = 0; i < pieces; ++i) {
+    const std::size_t o = static_cast<std::size_t>(i) * kPiece;
+    std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kPiece, bytes - o));
+  }
+}
+
+constexpr int kStageSlots = 4;
+constexpr std::size_t kStageChunk = 8u << 20;
+
+char* stage_ring(cieg_ctx* ctx) {
+  for (auto& e : ctx->stage_ev)
+    if (!e) CIEG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return static_cast<char*>(ctx->pinned_stage.get(kStageSlots * kStageChunk));
+}
+
+// Pageable host -> device through the pinned ring: the host copy of chunk c+1
+// (all threads) overlaps the DMA of chunk c.
+void upload_staged(cieg_ctx* ctx, void* dst, const void* src, std::size_t bytes) {
+  char* ring = stage_ring(ctx);
+  const std::size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+  for (std::size_t c = 0; c < chunks; ++c) {
+    const int slot = static_cast<int>(c % kStageSlots);
+    const std::size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    if (c >= kStageSlots) CIEG_CUDA(cudaEventSynchronize(ctx->stage_ev[slot]));
+    par_copy(ring + slot * kStageChunk, static_cast<const char*>(src) + off, len);
+    CIEG_CUDA(cudaMemcpyAsync(static_cast<char*>(dst) + off, ring + slot * kStageChunk, len, cudaMemcpyHostToDevice,
+                              ctx->stream));
+    CIEG_CUDA(cudaEventRecord(ctx->stage_ev[slot], ctx->stream));
+  }
+}
+
+// Device -> pageable host: kStageSlots chunk DMAs in flight ahead of the host
+// copies out of the ring.
+void download_staged(cieg_ctx* ctx, void* dst, const void* src, std::size_t bytes) {
+  char* ring = stage_ring(ctx);
+  const std::size_t chunks = (bytes + kStageChunk - 1) / kStageChunk;
+  auto issue = [&](std::size_t c) {
+    const int slot = static_cast<int>(c % kStageSlots);
+    const std::size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    CIEG_CUDA(cudaMemcpyAsync(ring + slot * kStageChunk, static_cast<const char*>(src) + off, len,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaEventRecord(ctx->stage_ev[slot], ctx->stream));
+  };
+  for (std::size_t c = 0; c < chunks && c < kStageSlots; ++c) issue(c);
+  for (std::size_t c = 0; c < chunks; ++c) {
+    const int slot = static_cast<int>(c % kStageSlots);
+    const std::size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
+    CIEG_CUDA(cudaEventSynchronize(ctx->stage_ev[slot]));
+    par_copy(static_cast<char*>(dst) + off, ring + slot * kStageChunk, len);
+    if (c + kStageSlots < chunks) issue(c + kStageSlots);
+  }
+}
+
+}  // namespace
+
+// ci::spmm's host call (the drop-in binds it, integration/ci_gpu_dropin.cpp):
+// pinned host buffers go straight to the copy engines; pageable ones (the
+// std::vector inside ci::BlockVectors) stream through a pinned chunk ring
+// with the host copies spread over the OpenMP threads.
 int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
                    uint32_t m) {
   return cieg::guarded([&] {
@@ -460,9 +539,15 @@ int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, dou
     if (!x_host || !y_host) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host: null vector");
     double* dx = static_cast<double*>(ctx->scratch_x.get(xbytes));
     double* dy = static_cast<double*>(ctx->scratch_y.get(ybytes));
-    CIEG_CUDA(cudaMemcpyAsync(dx, x_host, xbytes, cudaMemcpyHostToDevice, ctx->stream));
+    if (host_pinned(x_host))
+      CIEG_CUDA(cudaMemcpyAsync(dx, x_host, xbytes, cudaMemcpyHostToDevice, ctx->stream));
+    else
+      upload_staged(ctx, dx, x_host, xbytes);
     cieg::launch_spmm(ctx, mat, dx, m, dy, m, m);
-    CIEG_CUDA(cudaMemcpyAsync(y_host, dy, ybytes, cudaMemcpyDeviceToHost, ctx->stream));
+    if (host_pinned(y_host))
+      CIEG_CUDA(cudaMemcpyAsync(y_host, dy, ybytes, cudaMemcpyDeviceToHost, ctx->stream));
+    else
+      download_staged(ctx, y_host, dy, ybytes);
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

@@ -58,6 +58,8 @@ struct PinnedBuf {
   }
 };
 
+struct SlicedPlan;  // spmm_i8.cu
+
 }  // namespace cieg
 
 struct cieg_ctx {
@@ -75,6 +77,8 @@ struct cieg_ctx {
   unsigned spmm_launch_id = 0;          // tags the flag per K1 launch
   std::deque<cieg::DevBuf> solver_pool; // LOBPCG work blocks, reused across solves
   cieg::PinnedBuf pinned_small;
+  cieg::PinnedBuf pinned_stage;         // pageable host X/U: chunked staging ring (capi.cu)
+  cudaEvent_t stage_ev[4] = {};
 };
 
 struct cieg_mat {
@@ -113,6 +117,8 @@ struct cieg_mat {
   // a leading-block view (cieg_matrix_leading_view) borrows panel_start,
   // tile_off, idx and val from its parent and owns only its work lists
   bool borrowed_stream = false;
+  // integer-slice tensor-core K1 (spmm_i8.cu): digit records, built on first use
+  cieg::SlicedPlan* sliced = nullptr;
   ~cieg_mat();
 };
 
@@ -143,5 +149,21 @@ void upload_schedule(cieg_mat* m, const HostTiles& ht);
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
                  std::uint32_t ldy, std::uint32_t mcols, double* yhalo = nullptr, std::uint32_t ldh = 0,
                  bool shard_single_pass = false);
+
+// Integer-slice (Ozaki) K1 on tcgen05 (spmm_i8.cu): fp32 H, 128-row panels,
+// full (unsharded) matrices with a single-pass schedule.
+bool sliced_supported(const cieg_mat* m);
+// builds the slice records on first use; false when unsupported or H holds Inf/NaN
+bool sliced_ready(cieg_ctx* ctx, cieg_mat* m);
+// the mode's choice for width mc (auto: sliced for mc >= kSlicedMinCols)
+bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
+constexpr std::uint32_t kSlicedMinCols = 9;
+// Digitize X and run the sliced kernel: owner rows of Y written, every
+// off-diagonal item's transposed product stored to its partial slot (the
+// caller runs sp_reduce and the non-finite fix-up as for the single pass).
+void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
+                        std::uint32_t ldy, std::uint32_t mc, double* partial, unsigned* nonfinite,
+                        unsigned launch_id);
+void destroy_sliced(cieg_mat* m);
 
 }  // namespace cieg

@@ -226,6 +226,27 @@ void generate(const cieg_gen_params& p, HostCsb& out) {
   out.group_bounds.assign(g.start.begin(), g.start.end());
 }
 
+// Stored entries of the generated matrix without building it (same loops).
+std::uint64_t count_nnz(const cieg_gen_params& p) {
+  validate(p);
+  const TileGrid g = make_grid(p);
+  const cieg_gen::Seeds sd = cieg_gen::derive_seeds(p.seed);
+  const std::vector<std::vector<std::uint32_t>> kept = kept_tiles(p, g);
+  std::uint64_t total = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : total)
+  for (std::int64_t ti = 0; ti < static_cast<std::int64_t>(g.count()); ++ti) {
+    const std::uint32_t I = static_cast<std::uint32_t>(ti);
+    for (std::uint32_t a = g.start[I]; a < g.start[I + 1]; ++a)
+      for (std::uint32_t J : kept[I]) {
+        const std::uint32_t ce = (J == I) ? a : g.start[J + 1];
+        for (std::uint32_t b = g.start[J]; b < ce; ++b)
+          total += cieg_gen::unit_double(cieg_gen::hash3(sd.q, a, b)) < p.q;
+        total += J == I;
+      }
+  }
+  return total;
+}
+
 void random_block(std::uint32_t n, std::uint32_t k, std::uint64_t seed, double* out, std::uint32_t row0) {
   // ci::random_block (proj/src/block_vectors.cpp:162-174): symmetric_double(seed, i, j),
   // rows [row0, row0 + n) of the global block (a shard's rows).
@@ -242,6 +263,12 @@ extern "C" {
 
 double cieg_gen_expected_nnz(const cieg_gen_params* prm) {
   return prm ? cieg::expected_nnz(*prm) : 0.0;
+}
+
+uint64_t cieg_gen_count_nnz(const cieg_gen_params* prm) {
+  std::uint64_t n = 0;
+  if (cieg::guarded([&] { n = prm ? cieg::count_nnz(*prm) : 0; }) != CIEG_OK) return 0;
+  return n;
 }
 
 double cieg_gen_avg_row_nnz(const cieg_gen_params* prm) {

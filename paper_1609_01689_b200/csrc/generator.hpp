@@ -20,6 +20,7 @@ TileGrid make_grid(const cieg_gen_params& p);
 void validate(const cieg_gen_params& p);
 double expected_nnz(const cieg_gen_params& p);
 double avg_row_nnz(const cieg_gen_params& p);
+std::uint64_t count_nnz(const cieg_gen_params& p);  // stored entries, counted without storage
 double value_scale(const cieg_gen_params& p);  // 1 / sqrt(avg full-row off-diagonal count)
 // kept column tiles J <= I of every tile row I (ascending; the diagonal last)
 std::vector<std::vector<std::uint32_t>> kept_tiles(const cieg_gen_params& p, const TileGrid& g);

@@ -331,29 +331,45 @@ namespace {
 struct DiagTile {
   std::uint64_t e0, e1;      // entry slots
   std::uint32_t a0, b0;      // global first row / column of the tile's panels
-  std::uint32_t gs, gn;      // group start row (shard-local numbering) and size
-  std::uint64_t block_off;   // doubles
+  std::uint32_t g_lo, g_hi;  // groups overlapping the row panel (g_hi exclusive)
 };
 
-// Scatter the tile's entries into its group's dense block, mirrored
-// (ci::extract_tile_diagonal, hamiltonian.cpp:178-203).
+// Scatter the tile's entries into their group's dense block, mirrored
+// (ci::extract_tile_diagonal, hamiltonian.cpp:178-203). A panel may hold
+// several small groups (merged generator tiles) or be part of one larger
+// group: every entry looks up the groups of its row and its column and is
+// kept only when both lie in the same group, indexed relative to it.
 // Blocks are stored in the tile stream's own value type: fp32 values of an
 // fp32 H widen to fp64 exactly when the preconditioner reads them.
+__device__ __forceinline__ std::uint32_t group_of(const std::uint32_t* lb, std::uint32_t lo, std::uint32_t hi,
+                                                  std::uint32_t row) {
+  while (hi - lo > 1) {  // lb[lo] <= row < lb[hi]
+    const std::uint32_t mid = (lo + hi) >> 1;
+    if (lb[mid] <= row) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
 template <typename V, typename B = V>
 __global__ void diag_blocks_kernel(const DiagTile* dt, const std::uint32_t* idx, const V* val, std::uint32_t te,
-                                   std::uint32_t row_lo, B* blocks) {
+                                   std::uint32_t row_lo, const std::uint32_t* lb, const std::uint64_t* off,
+                                   std::uint32_t ngroups, B* blocks) {
   const DiagTile t = dt[blockIdx.x];
   for (std::uint64_t e = t.e0 + threadIdx.x; e < t.e1; e += blockDim.x) {
-    const std::uint32_t off = idx[e] & 0xffffu;
+    const std::uint32_t o = idx[e] & 0xffffu;
     constexpr int prec = sizeof(V) == 4 ? 0 : 1;
     const std::uint32_t sa = cieg_tl::stride(te, prec);
-    const std::uint32_t r = off / sa, pc = off - r * sa;
+    const std::uint32_t r = o / sa, pc = o - r * sa;
     if (pc >= te) continue;  // sentinel
     const std::uint32_t c = cieg_tl::unperm(pc, prec);
-    const std::uint32_t ia = t.a0 + r - row_lo - t.gs, ib = t.b0 + c - row_lo - t.gs;
+    const std::uint32_t ra = t.a0 + r - row_lo, cb = t.b0 + c - row_lo;  // shard-local row / column
+    if (ra >= lb[ngroups] || cb >= lb[ngroups]) continue;
+    const std::uint32_t g = group_of(lb, t.g_lo, t.g_hi + 1 > ngroups ? ngroups : t.g_hi + 1, ra);
+    if (ra < lb[g] || ra >= lb[g + 1] || cb < lb[g] || cb >= lb[g + 1]) continue;  // cross-group coupling
+    const std::uint32_t gn = lb[g + 1] - lb[g], ia = ra - lb[g], ib = cb - lb[g];
     const B v = static_cast<B>(val[e]);
-    blocks[t.block_off + ia + static_cast<std::uint64_t>(ib) * t.gn] = v;
-    blocks[t.block_off + ib + static_cast<std::uint64_t>(ia) * t.gn] = v;
+    blocks[off[g] + ia + static_cast<std::uint64_t>(ib) * gn] = v;
+    blocks[off[g] + ib + static_cast<std::uint64_t>(ia) * gn] = v;
   }
 }
 
@@ -376,21 +392,26 @@ cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
     const std::uint64_t sz = lb[g + 1] - lb[g];
     off[g + 1] = off[g] + sz * sz;
   }
-  // group of every owned panel
+  // groups overlapping every owned panel: [gfirst, glast]
   const std::vector<std::uint32_t>& ps = m->panel_start_host;
-  std::vector<std::int64_t> gpanel(m->npanels, -1);
+  std::vector<std::int64_t> gfirst(m->npanels, -1), glast(m->npanels, -1);
   for (std::uint32_t P = 0, g = 0; P < m->npanels; ++P) {
     if (ps[P] < m->row_lo || ps[P + 1] > m->row_hi) continue;
-    while (g < lng && lb[g + 1] + m->row_lo <= ps[P]) ++g;
-    gpanel[P] = g;
+    const std::uint32_t a = ps[P] - m->row_lo, b = ps[P + 1] - m->row_lo;
+    while (g < lng && lb[g + 1] <= a) ++g;
+    if (g >= lng) continue;
+    std::uint32_t h = g;
+    while (h + 1 < lng && lb[h + 1] < b) ++h;
+    gfirst[P] = g;
+    glast[P] = h;
   }
   std::vector<DiagTile> dts;
   for (std::uint64_t t = 0; t < m->ntiles; ++t) {
     const std::uint32_t pi = m->tile_pi_host[t], pj = m->tile_pj_host[t];
-    if (gpanel[pi] < 0 || gpanel[pi] != gpanel[pj]) continue;
-    const std::uint32_t g = static_cast<std::uint32_t>(gpanel[pi]);
-    dts.push_back(DiagTile{m->tile_off_host[t], m->tile_off_host[t + 1], ps[pi], ps[pj], lb[g], lb[g + 1] - lb[g],
-                           off[g]});
+    if (gfirst[pi] < 0 || gfirst[pj] < 0) continue;
+    if (glast[pi] < gfirst[pj] || glast[pj] < gfirst[pi]) continue;  // no group shared by the two panels
+    dts.push_back(DiagTile{m->tile_off_host[t], m->tile_off_host[t + 1], ps[pi], ps[pj],
+                           static_cast<std::uint32_t>(gfirst[pi]), static_cast<std::uint32_t>(glast[pi])});
   }
   auto* pr = new cieg_prec;
   try {
@@ -424,13 +445,16 @@ cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
       DiagTile* d = dev_upload(dts);
       if (f32)
         diag_blocks_kernel<float><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
-            d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->blocks32);
+            d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->bounds, pr->block_off, lng,
+            pr->blocks32);
       else if (m->precision == 0)
         diag_blocks_kernel<float, double><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
-            d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->blocks);
+            d, m->idx, static_cast<const float*>(m->val), m->tile_edge, m->row_lo, pr->bounds, pr->block_off, lng,
+            pr->blocks);
       else
         diag_blocks_kernel<double><<<static_cast<unsigned>(dts.size()), 256, 0, ctx->stream>>>(
-            d, m->idx, static_cast<const double*>(m->val), m->tile_edge, m->row_lo, pr->blocks);
+            d, m->idx, static_cast<const double*>(m->val), m->tile_edge, m->row_lo, pr->bounds, pr->block_off, lng,
+            pr->blocks);
       CIEG_CUDA(cudaGetLastError());
       ++ctx->launches;
       CIEG_CUDA(cudaStreamSynchronize(ctx->stream));

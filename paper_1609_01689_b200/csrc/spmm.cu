@@ -969,12 +969,33 @@ bool single_pass_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) 
     const char* e = std::getenv("CIEG_SPMM_MODE");
     if (e && std::strcmp(e, "owner") == 0) return static_cast<int>(CIEG_SPMM_OWNER);
     if (e && std::strcmp(e, "single") == 0) return static_cast<int>(CIEG_SPMM_SINGLE_PASS);
+    if (e && std::strcmp(e, "sliced") == 0) return static_cast<int>(CIEG_SPMM_SLICED);
     return static_cast<int>(CIEG_SPMM_AUTO);
   }();
   if (!m->sp_sched) return false;
   const int mode = ctx->spmm_mode >= 0 ? ctx->spmm_mode : env_mode;
+  if (mode == CIEG_SPMM_SLICED) return !sliced_supported(m);  // (the DMMA single pass where sliced cannot run)
   if (mode != CIEG_SPMM_AUTO) return mode == CIEG_SPMM_SINGLE_PASS;
   return mc <= kSinglePassMaxCols;
+}
+
+int effective_mode(const cieg_ctx* ctx) {
+  static const int env_mode = [] {
+    const char* e = std::getenv("CIEG_SPMM_MODE");
+    if (e && std::strcmp(e, "owner") == 0) return static_cast<int>(CIEG_SPMM_OWNER);
+    if (e && std::strcmp(e, "single") == 0) return static_cast<int>(CIEG_SPMM_SINGLE_PASS);
+    if (e && std::strcmp(e, "sliced") == 0) return static_cast<int>(CIEG_SPMM_SLICED);
+    return static_cast<int>(CIEG_SPMM_AUTO);
+  }();
+  return ctx->spmm_mode >= 0 ? ctx->spmm_mode : env_mode;
+}
+
+bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
+  if (!sliced_supported(m)) return false;
+  const int mode = effective_mode(ctx);
+  if (mode == CIEG_SPMM_SLICED) return true;
+  if (mode != CIEG_SPMM_AUTO) return false;
+  return mc >= kSlicedMinCols && single_pass_fits(ctx, m, mc);
 }
 
 
@@ -1019,14 +1040,18 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   nonfinite_flag(ctx),
                   ++ctx->spmm_launch_id,
                   nullptr};
-    const bool sp = shard ? shard_sp : single_pass_default(ctx, m, mc);
+    const bool sliced = !shard && sliced_rule(ctx, m, mc) && sliced_ready(ctx, const_cast<cieg_mat*>(m));
+    const bool sp = sliced || (shard ? shard_sp : single_pass_default(ctx, m, mc));
     if (sp) {
       args.sched_off = m->sp_sched_off;
       args.sched = reinterpret_cast<const uint4*>(m->sp_sched);
       args.partial = static_cast<double*>(
           ctx->scratch_partial.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(m->sp_items) * m->tile_edge * mc)));
     }
-    if (m->precision == 0) {
+    if (sliced) {
+      launch_spmm_sliced(ctx, const_cast<cieg_mat*>(m), x + c0, ldx, y + c0, ldy, mc, args.partial, args.nonfinite,
+                         args.launch_id);
+    } else if (m->precision == 0) {
       if (m->tile_edge == 64)
         dispatch_nt<float, 64>(ctx, m, args, mc, sp);
       else

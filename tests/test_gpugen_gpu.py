@@ -23,7 +23,12 @@ def test_device_generator_bit_identical(params):
         assert np.array_equal(a, b)
 
 
-@pytest.mark.parametrize("params", CASES[:2])
+# generator tiles smaller than half the device panel (16 / 24-row groups merged
+# into 128 / 64-row panels): a diagonal tile spans several groups
+SMALL_TILES = [(6000, 3, 16, 0.1, 0.5, 5, 0, 2000), (6000, 3, 24, 0.1, 0.5, 6, 1, 2000)]
+
+
+@pytest.mark.parametrize("params", CASES[:2] + SMALL_TILES)
 def test_device_generator_spmm_and_precond(params):
     n, s, t, p, q, seed, prec, beta = params
     h = gen_from(params)

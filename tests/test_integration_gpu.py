@@ -78,3 +78,69 @@ def test_dropin_orthonormalize_and_residual_norms(ref_lib):
     v = h.view()
     assert lib.dropin_residual_norms(C.byref(v), pd(x), C.c_uint32(3), pd(th), pd(r)) == 0
     np.testing.assert_allclose(r, ref_lib.residual_norms(ref_lib.RefMatrix(h), x, th), rtol=1e-12)
+
+
+SOLVE_GPU = os.path.join(ROOT, "integration", "_build", "ci_solve_gpu")
+SOLVE_REF = os.path.join(ROOT, "integration", "_build", "ci_solve_ref")
+
+
+def _run(exe, args):
+    import json
+    import subprocess
+
+    out = subprocess.run([exe] + [str(a) for a in args], check=True, capture_output=True, text=True, timeout=600)
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+# (Z, N, M2, parity, Nmax, seed, offdiag, d, beta, precision, k_want, k_trial, tol, max_iter)
+LINK_CASES = [(2, 2, 0, 1, 4, 1, 0.1, 2, 2000, 1, 4, 8, 1e-8, 500),
+              (2, 2, 0, 1, 6, 3, 0.1, 2, 2000, 0, 4, 6, 1e-6, 500),
+              (3, 3, 2, -1, 3, 5, 0.2, 2, 2000, 1, 3, 5, 1e-8, 500)]
+
+
+@pytest.mark.parametrize("case", LINK_CASES)
+def test_linked_dropin_build_matches_reference_build(case):
+    """The same run_solver-equivalent driver (integration/ci_solve_main.cpp),
+    linked once against all eleven reference TUs (CPU) and once with
+    csb/block_vectors/lobpcg/precond/lanczos.cpp replaced by the drop-in
+    (+ libcieg.so): identical iteration counts, counters and multilevel level
+    iterations; every operator-level result to rounding."""
+    if not (os.path.exists(SOLVE_GPU) and os.path.exists(SOLVE_REF)):
+        pytest.skip("integration/_build not built (needs /root/reference at build time)")
+    g, r = _run(SOLVE_GPU, case), _run(SOLVE_REF, case)
+    for key in ("dim", "nnz", "iterations", "converged", "counters", "stats", "history_csv_lines",
+                "multilevel_level_iterations", "multilevel_iterations"):
+        assert g[key] == r[key], key
+    tol_eig = 1e-5 if case[9] == 0 else 1e-9
+    np.testing.assert_allclose(g["eigenvalues"], r["eigenvalues"], rtol=tol_eig)
+    np.testing.assert_allclose(g["multilevel_eigenvalues"], r["multilevel_eigenvalues"], rtol=tol_eig)
+    for key in ("spmm", "block_inner", "linear_combination", "add_linear_combination", "apply_preconditioner",
+                "fom_solve", "csb_roundtrip_spmm"):
+        np.testing.assert_allclose(g[key], r[key], rtol=1e-12, err_msg=key)
+    np.testing.assert_allclose(g["column_norms"], r["column_norms"], rtol=1e-13)
+    np.testing.assert_allclose(g["residual_norms"], r["residual_norms"], rtol=1e-3, atol=1e-12)
+
+
+def test_dropin_cache_follows_content_not_address(ref_lib):
+    """two matrices with the same structure and different values
+    built at the same address (the CLI's `compare` loop) must not reuse the
+    first upload: dropin_lobpcg builds its CsbMatrix / TileDiagonal on the
+    stack, call after call."""
+    if not os.path.exists(LIB):
+        pytest.skip("integration/_build not built")
+    lib = C.CDLL(LIB)
+    for seed in (11, 12, 13):
+        h = gen_from((3000, 3, 64, 0.1, 0.5, seed, 1, 2000))
+        x0 = ci.random_block(h.dim, 6, 7)
+        v = h.view()
+        groups = np.ascontiguousarray(h.groups, dtype=np.uint32)
+        eig = np.zeros(3)
+        iters = C.c_int()
+        assert lib.dropin_lobpcg(C.byref(v), groups.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                 C.c_uint32(len(groups) - 1), x0.ctypes.data_as(C.POINTER(C.c_double)), C.c_uint32(6),
+                                 C.c_int(3), C.c_double(1e-8), C.c_int(1), eig.ctypes.data_as(C.POINTER(C.c_double)),
+                                 C.byref(iters)) == 0
+        rm = ref_lib.RefMatrix(h)
+        rr = ref_lib.lobpcg_solve(rm, x0, 3, 1e-8, 500, ref_lib.RefTileDiagonal(rm, h.groups))
+        assert iters.value == rr.iterations
+        np.testing.assert_allclose(eig, rr.eigenvalues, rtol=1e-10)

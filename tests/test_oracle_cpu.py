@@ -256,3 +256,23 @@ def test_spec_choose_shifts_examples():
     assert mu[0] == pytest.approx(-30.008) and en.all()
     mu, en = O.choose_shifts([-30.0], [5.0], [1.0], [0.5], 5, 1e-6)
     assert not en.any()
+
+
+@pytest.mark.parametrize("prec,beta", [(0, 100), (1, 100), (0, 2000)])
+def test_oracle_cpp_generator_matches_python_restatement(ref_lib, prec, beta):
+    """oracle/ref_gen.cpp (the generator the reference arm and the CPU
+    baselines build the reference's ci::CsbMatrix with) is bit for bit
+    ci_oracle.generate, and its leading-block sample is the leading principal
+    submatrix entry for entry."""
+    o = O.generate(600, 3, 32, 0.3, 0.5, 7, prec, beta=beta)
+    r = ref_lib.generate(600, 3, 32, 0.3, 0.5, 7, prec, beta=beta)
+    assert r.nnz == int(o.entry_offsets[-1]) == ref_lib.count_nnz(600, 3, 32, 0.3, 0.5, 7)
+    x = O.random_block(600, 3, 1)
+    np.testing.assert_array_equal(r.spmm_dim(x), O.spmm(o, x))
+    nb = r.nb_total
+    lead = ref_lib.generate(600, 3, 32, 0.3, 0.5, 7, prec, beta=beta, nbk=nb // 2)
+    d = lead.dim
+    dense = O.to_dense(o)[:d, :d]
+    xs = x[:d]
+    np.testing.assert_allclose(lead.spmm_dim(xs), dense @ xs, rtol=1e-12, atol=1e-12)
+    assert np.isclose(ref_lib.calibrated_p(600, 3, 32, 0.5, ref_lib.expected_nnz(600, 3, 32, 0.3, 0.5)), 0.3)

@@ -1,0 +1,155 @@
+"""The integer-slice K1 (CIEG_SPMM_SLICED, csrc/spmm_i8.cu: Ozaki slices on
+the tcgen05 int8 tensor cores) against the reference's spmm / the oracle:
+1e-13 relative at every width, under wide dynamic ranges of X (per-panel
+exponents) and of H (per-row exponents), zero columns, Inf/NaN inputs, the
+diagonal tiles and ragged sector tails, deterministic run to run; plus the
+fall-back when H holds non-finite values, and LOBPCG parity in this mode."""
+import numpy as np
+import pytest
+
+from conftest import gen_from
+from oracle import ci_oracle as O
+from paper_1609_01689_b200 import ci, configs
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-13
+
+
+def rel_cols(a, b):
+    """max over columns of max|a - b| / max|b| (column-wise scale)."""
+    s = np.maximum(np.abs(b).max(axis=0), 1e-300)
+    return float((np.abs(a - b).max(axis=0) / s).max())
+
+
+@pytest.fixture(scope="module")
+def sliced():
+    dev = ci.Device.default()
+    dev.set_spmm_mode("sliced")
+    yield dev
+    dev.set_spmm_mode("auto")
+
+
+# fp32 H, 256-row generator tiles -> 128-row panels (two per tile, sector tails)
+MATS = [(30000, 3, 256, 0.02, 0.4, 77, 0, 2000), (12000, 4, 200, 0.08, 0.4, 5, 0, 2000),
+        (9000, 3, 128, 0.1, 0.5, 9, 0, 2000)]
+
+
+@pytest.mark.parametrize("params", MATS)
+@pytest.mark.parametrize("m", [1, 3, 8, 9, 16, 24, 32])
+def test_sliced_matches_reference(sliced, ref_lib, params, m):
+    h = gen_from(params)
+    x = ci.random_block(h.dim, m, 100 + m)
+    y_ref = ref_lib.RefMatrix(h).spmm(x, serial=True)
+    y = ci.spmm(h, x)
+    assert rel_cols(y, y_ref) < TOL
+    assert np.array_equal(ci.spmm(h, x), y)  # deterministic
+
+
+def test_sliced_dynamic_range(sliced, ref_lib):
+    """X rows spanning 1e-200 .. 1e200 by panel and by row, zero columns,
+    and rows of H scaled over 1e-30 .. 1e30 (symmetrically)."""
+    h = gen_from(MATS[0])
+    rng = np.random.default_rng(3)
+    x = ci.random_block(h.dim, 16, 9)
+    x *= 10.0 ** rng.integers(-200, 200, size=(h.dim, 1))
+    x[:, 5] = 0.0
+    x[::7, 11] *= 1e-30
+    y_ref = ref_lib.RefMatrix(h).spmm(x, serial=True)
+    y = ci.spmm(h, x)
+    # relative per entry where the reference is well away from cancellation
+    rm = ref_lib.RefMatrix(h)
+    scale = rm.spmm(np.abs(x), serial=True)  # |H| |x| would need |H|; use the panel bound below instead
+    assert np.all(y[:, 5] == y_ref[:, 5])
+    err = np.abs(y - y_ref)
+    bound = 1e-13 * np.abs(y_ref).max(axis=0)
+    assert np.all(err.max(axis=0) <= bound + 0.0)
+    del scale
+    # a symmetric diagonal scaling D H D keeps the matrix symmetric: rows of very different size
+    d = 10.0 ** rng.integers(-30, 30, size=h.dim).astype(np.float64)
+    hv = h.values.astype(np.float64)
+    nb = h.block_count()
+    bi = np.concatenate([np.full(i + 1, i) for i in range(nb)])
+    bj = np.concatenate([np.arange(i + 1) for i in range(nb)])
+    counts = np.diff(h.entry_offsets.astype(np.int64))
+    r = h.block_boundaries[np.repeat(bi, counts)].astype(np.int64) + h.rows
+    c = h.block_boundaries[np.repeat(bj, counts)].astype(np.int64) + h.cols
+    vals = (hv * d[r] * d[c]).astype(np.float32)
+    hs = ci.CsbMatrix(dim=h.dim, precision=0, block_boundaries=h.block_boundaries, entry_offsets=h.entry_offsets,
+                      rows=h.rows, cols=h.cols, values=vals, groups=h.groups, beta=h.beta)
+    xs = ci.random_block(h.dim, 16, 4)
+    ys_ref = ref_lib.RefMatrix(hs).spmm(xs, serial=True)
+    ys = ci.spmm(hs, xs)
+    # entrywise against |H_s| |x| (the scale a row-scaled representation is exact to)
+    hsa = ci.CsbMatrix(dim=h.dim, precision=0, block_boundaries=h.block_boundaries, entry_offsets=h.entry_offsets,
+                       rows=h.rows, cols=h.cols, values=np.abs(vals), groups=h.groups, beta=h.beta)
+    mag = ref_lib.RefMatrix(hsa).spmm(np.abs(xs), serial=True)
+    assert np.all(np.abs(ys - ys_ref) <= 1e-13 * mag + 1e-300)
+
+
+def test_sliced_nonfinite_x_matches_reference(sliced, ref_lib):
+    h = gen_from(MATS[1])
+    x = ci.random_block(h.dim, 12, 8)
+    x[17, 3] = np.inf
+    x[4000, 0] = -np.inf
+    x[9000, 7] = np.nan
+    y_ref = ref_lib.RefMatrix(h).spmm(x, serial=True)
+    y = ci.spmm(h, x)
+    assert np.array_equal(np.isnan(y), np.isnan(y_ref))
+    assert np.array_equal(np.isposinf(y), np.isposinf(y_ref))
+    assert np.array_equal(np.isneginf(y), np.isneginf(y_ref))
+    fin = np.isfinite(y_ref)
+    assert np.abs(y[fin] - y_ref[fin]).max() <= 1e-13 * np.abs(y_ref[fin]).max()
+
+
+def test_sliced_nonfinite_h_falls_back_to_dmma(sliced, ref_lib):
+    """Inf/NaN stored values cannot be sliced: the matrix runs the fp64 DMMA
+    single pass instead (still on the GPU) and matches the reference."""
+    h = gen_from(MATS[2])
+    vals = h.values.copy()
+    vals[1234] = np.inf
+    hb = ci.CsbMatrix(dim=h.dim, precision=0, block_boundaries=h.block_boundaries, entry_offsets=h.entry_offsets,
+                      rows=h.rows, cols=h.cols, values=vals, groups=h.groups, beta=h.beta)
+    x = ci.random_block(h.dim, 16, 2)
+    y_ref = ref_lib.RefMatrix(hb).spmm(x, serial=True)
+    y = ci.spmm(hb, x)
+    assert np.array_equal(np.isnan(y), np.isnan(y_ref))
+    fin = np.isfinite(y_ref)
+    assert np.abs(y[fin] - y_ref[fin]).max() <= 1e-13 * np.abs(y_ref[fin]).max()
+
+
+def test_sliced_config2_properties(sliced):
+    """BASELINE config 2 (n = 2e6, S = 8e8) at m = 16: linearity and
+    u^T (H v) = v^T (H u) at full size, and agreement with the fp64 DMMA
+    owner-computes kernel to 1e-13."""
+    dm = configs.CFG2.generate_device()
+    x = ci.random_block(dm.dim, 16, 1)
+    z = ci.random_block(dm.dim, 16, 2)
+    y = dm.spmm_host(x)
+    yz = dm.spmm_host(z)
+    assert rel_cols(dm.spmm_host(0.5 * x - 2.0 * z), 0.5 * y - 2.0 * yz) < 1e-13
+    assert abs(float(z[:, 0] @ y[:, 0]) - float(x[:, 0] @ yz[:, 0])) < 1e-11 * abs(float(z[:, 0] @ y[:, 0]))
+    dev = ci.Device.default()
+    dev.set_spmm_mode("owner")
+    try:
+        y_dmma = dm.spmm_host(x)
+    finally:
+        dev.set_spmm_mode("sliced")
+    assert rel_cols(y, y_dmma) < TOL
+
+
+def test_sliced_lobpcg_matches_reference(sliced, ref_lib):
+    """The config-4 settings (kt 16, k 8, fp32 H, 256-row tiles, FOM/LU tile
+    preconditioner) with every SpMM on the int8 tensor cores: identical
+    iteration count, counters and active sets to ci::lobpcg_solve."""
+    cfg = configs.Config("cfg4-shape", 25 * 2368, 25, 256, None, 0.4, 0, 25 * 2368 * 400, k_want=8, kt=16,
+                         tol=1e-6, seed=3)
+    h = cfg.generate()
+    x0 = ci.random_block(h.dim, 16, 42)
+    rm = ref_lib.RefMatrix(h)
+    rr = ref_lib.lobpcg_solve(rm, x0, 8, 1e-6, 500, ref_lib.RefTileDiagonal(rm, h.groups))
+    rep = ci.lobpcg_solve(h, x0, ci.LobpcgOptions(k_want=8, tol=1e-6, preconditioner=ci.extract_tile_diagonal(h)))
+    assert rep.iterations == rr.iterations and rep.converged == rr.converged
+    assert [rep.counters.spmm_calls, rep.counters.spmv_equivalents, rep.counters.precond_applications,
+            rep.counters.orthogonalizations] == rr.counters.tolist()
+    np.testing.assert_allclose(rep.eigenvalues, rr.eigenvalues, rtol=1e-9)
