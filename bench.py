@@ -550,8 +550,9 @@ def cfg5_record(dev, rank, world):
 
 def widths_record(dev, dm, stream, n):
     """K1 on the config-2 matrix at the LOBPCG / Lanczos block widths, in the
-    default mode (single pass for m <= 8, owner-computes above) and in
-    owner-computes, device time per launch (median of 3 x 10 launches)."""
+    default mode and in each explicit kernel (owner-computes, DMMA single
+    pass, sliced int8 tensor-core), device time per launch (median of 3 x 10
+    launches)."""
     import torch
 
     from paper_1609_01689_b200 import configs
@@ -561,7 +562,7 @@ def widths_record(dev, dm, stream, n):
         x = torch.randn(n, m, dtype=torch.float64, device="cuda")
         y = torch.empty_like(x)
         row = {"m": m}
-        for mode in ("auto", "owner"):
+        for mode in ("auto", "owner", "single", "sliced"):
             dev.set_spmm_mode(mode)
             for _ in range(3):
                 dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
@@ -577,7 +578,8 @@ def widths_record(dev, dm, stream, n):
             t = sorted(times)[1]
             row[mode] = {"ms": round(t, 4),
                          "gbs": round(configs.spmm_bytes(dm.nnz, n, m, dm.precision) / (t * 1e-3) / 1e9, 1)}
-        row["auto_mode"] = "single pass" if m <= 8 else "owner-computes"
+        dev.set_spmm_mode("auto")
+        row["auto_mode"] = dm.spmm_kernel(m)
         out.append(row)
         del x, y
     dev.set_spmm_mode("auto")

@@ -89,6 +89,10 @@ int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact);
  * bit for bit. AUTO picks it for widths >= 9 where supported. */
 enum { CIEG_SPMM_AUTO = 0, CIEG_SPMM_OWNER = 1, CIEG_SPMM_SINGLE_PASS = 2, CIEG_SPMM_SLICED = 3 };
 int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode);
+/* The K1 kernel the current mode runs for a 16-column chunk of width m on
+ * this matrix: CIEG_SPMM_OWNER, CIEG_SPMM_SINGLE_PASS or CIEG_SPMM_SLICED
+ * (instrumentation; may build the sliced records on first use). */
+int cieg_spmm_effective_mode(cieg_ctx* ctx, cieg_mat* mat, uint32_t m, int* mode);
 /* Number of kernels this context has launched (instrumentation). */
 uint64_t cieg_ctx_launch_count(const cieg_ctx* ctx);
 

@@ -185,6 +185,7 @@ SIGNATURES = {
     "cieg_ctx_set_stream": (_i, [_vp, _vp]),
     "cieg_ctx_set_exact_order": (_i, [_vp, _i]),
     "cieg_ctx_set_spmm_mode": (_i, [_vp, _i]),
+    "cieg_spmm_effective_mode": (_i, [_vp, _vp, _u32, C.POINTER(C.c_int)]),
     "cieg_spmm_partial": (_i, [_vp, _vp, _vp, _vp, _u32, _vp]),
     "cieg_matrix_partial_rows": (_i, [_vp, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]),
     "cieg_report_summary": (_i, [_vp, _pi, _pi, _pd, _pu32, _pu32, _pu64]),

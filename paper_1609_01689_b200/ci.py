@@ -459,6 +459,14 @@ class DeviceMatrix:
         """Device-pointer SpMM on the device's stream (row-major n x m)."""
         _check(_lib.load().cieg_spmm(self.device.handle, self.handle, C.c_void_p(x_ptr), C.c_void_p(y_ptr), m))
 
+    SPMM_KERNELS = {1: "owner-computes", 2: "single pass", 3: "sliced"}
+
+    def spmm_kernel(self, m: int) -> str:
+        """The K1 kernel the device's current mode runs at width m here."""
+        out = C.c_int()
+        _check(_lib.load().cieg_spmm_effective_mode(self.device.handle, self.handle, m, C.byref(out)))
+        return self.SPMM_KERNELS.get(out.value, str(out.value))
+
 
 _UPLOADS: "weakref.WeakKeyDictionary[CsbMatrix, DeviceMatrix]" = weakref.WeakKeyDictionary()
 

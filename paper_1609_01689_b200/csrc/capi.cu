@@ -413,6 +413,13 @@ int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode) {
   });
 }
 
+int cieg_spmm_effective_mode(cieg_ctx* ctx, cieg_mat* mat, uint32_t m, int* mode) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat || !mode) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_effective_mode: null argument");
+    *mode = cieg::spmm_effective_mode(ctx, mat, std::min<std::uint32_t>(std::max<std::uint32_t>(m, 1), 16));
+  });
+}
+
 int cieg_ctx_set_stream(cieg_ctx* ctx, void* stream) {
   return cieg::guarded([&] {
     if (!ctx) cieg::fail(CIEG_ERR_ARGUMENT, "null context");

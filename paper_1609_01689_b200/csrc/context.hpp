@@ -165,5 +165,10 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
                         std::uint32_t ldy, std::uint32_t mc, double* partial, unsigned* nonfinite,
                         unsigned launch_id);
 void destroy_sliced(cieg_mat* m);
+// the K1 mode launch_spmm runs for width mc (CIEG_SPMM_OWNER / SINGLE_PASS / SLICED)
+int spmm_effective_mode(cieg_ctx* ctx, cieg_mat* m, std::uint32_t mc);
+// fp64 terms of the stored entries too small to slice exactly (after sp_reduce)
+void launch_sliced_tiny_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
+                            std::uint32_t ldy, std::uint32_t mc);
 
 }  // namespace cieg

@@ -990,6 +990,13 @@ int effective_mode(const cieg_ctx* ctx) {
   return ctx->spmm_mode >= 0 ? ctx->spmm_mode : env_mode;
 }
 
+int spmm_effective_mode(cieg_ctx* ctx, cieg_mat* m, std::uint32_t mc) {
+  const bool shard = m->row_lo != 0 || m->row_hi != m->dim;
+  if (!shard && sliced_rule(ctx, m, mc) && sliced_ready(ctx, m)) return CIEG_SPMM_SLICED;
+  if (!shard && single_pass_default(ctx, m, mc)) return CIEG_SPMM_SINGLE_PASS;
+  return CIEG_SPMM_OWNER;
+}
+
 bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
   if (!sliced_supported(m)) return false;
   const int mode = effective_mode(ctx);
@@ -1066,6 +1073,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
       CIEG_CUDA(cudaGetLastError());
       ++ctx->launches;
     }
+    if (sliced) launch_sliced_tiny_fix(ctx, m, x + c0, ldx, y + c0, ldy, mc);
     // owned panels of this (shard) matrix
     const auto& ps = m->panel_start_host;
     const std::uint32_t p_lo = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_lo) - ps.begin());

@@ -8,11 +8,11 @@
 // so the DMMA floor on config 2 at m = 16 is 3.46 ms = 31 % of HBM). The int8
 // tensor cores run ~120x that rate, so the same dense-tile products fit under
 // the HBM time once both operands are exact integer slices:
-//   * H: every stored value h of row r is a_int * 2^(e_r - 39) with
-//     |a_int| < 2^39 (e_r = exponent of the largest |h| touching index r, as
-//     row or column), so a_int is exact for every entry within 2^-16 of its
-//     row maximum and rounded at 2^-40 of it below that; a_int is split into
-//     five 8-bit slices, top signed, four unsigned (two's complement bytes).
+//   * H: every stored value h of row r is a_int * 2^(e_r - 38) with
+//     |a_int| < 2^38 (e_r = exponent of the largest |h| touching index r, as
+//     row or column), so a_int is exact for every entry within 2^-15 of its
+//     row maximum and rounded at 2^-39 of it below that; a_int is split into
+//     five balanced signed 8-bit digits.
 //     The diagonal is not sliced (its d_r x_r is added in fp64), so e_r is
 //     the off-diagonal scale of the row.
 //     Built once per matrix on the device (records_kernel): one 8-byte record
@@ -25,10 +25,11 @@
 //     one slice tile serves H X (K-major A) and H^T X (MN-major A).
 //   * the product a_int x_int = sum_d D_d 2^(8 (10 - d)), D_d = sum_{s+t=d}
 //     A_s X_t: one MMA per H slice s computes all its diagonals at once (B =
-//     digits 0 .. 6-s, D columns from 16 s), diagonals d <= 6 are kept (the
-//     dropped terms are below 2^-52 of max|a| max|x| per product), each D_d is
-//     an exact int32 over the 128-long tile dot product, and the epilogue
-//     recombines sum_d D_d 2^(-8 d) in fp64 and scales by 2^(e_r + ex - 13).
+//     digits 0 .. min(6, 7-s), D columns from 16 s), diagonals d <= 7 are kept
+//     (the dropped terms are below 2^-58 of max|a| max|x| per product), each
+//     D_d is an exact int32 over the 128-long tile dot product, and the
+//     epilogue recombines sum_d D_d 2^(-8 d) in fp64 and scales by
+//     2^(e_r + ex - 12).
 // The result agrees with the fp64 reference to rounding (tests compare at
 // 1e-13 relative), but its rounding is not the DMMA kernels': this mode is
 // selected per width (cieg_ctx_set_spmm_mode, CIEG_SPMM_SLICED).
@@ -53,6 +54,8 @@
 #include <algorithm>
 #include <climits>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -64,20 +67,22 @@ namespace cieg {
 
 constexpr int kTD = 128;                   // tile edge (fp32 H panels)
 constexpr int kAS = 5;                     // H slices
-constexpr int kXD = 7;                     // X digits = diagonals kept
+constexpr int kXD = 7;                     // X digits
+constexpr int kDiag = 8;                   // accumulated diagonals d = s + t (d <= 7 kept)
 constexpr int kNB = 16 * kXD;              // B rows per slab (digit-major, 16 columns each)
+constexpr int kND = 16 * kDiag;            // TMEM columns per orientation
 constexpr int kPlane = kTD * kTD;          // bytes per H slice plane
 constexpr int kPlanes = kAS * kPlane;      // 81920
 constexpr int kSlab = kNB * kTD;           // 14336: X digits of one panel
 constexpr int kSlabBytes = kSlab + 64;     // + 16 int32 exponents
-constexpr int kStageCols = 2 * kNB;        // TMEM columns per accumulator stage (row + transposed)
+constexpr int kStageCols = 2 * kND;        // TMEM columns per accumulator stage (row + transposed)
 constexpr int kThreads = 512;
 constexpr int kProducers = 7 * 32;         // warps 1..7
 constexpr std::uint16_t kNoEntry = 0xffff;
 
 struct OzItem {
   std::uint64_t rec0;   // first record
-  std::uint32_t nrec;   // records (even; sentinels included)
+  std::uint32_t nrec;   // records (a multiple of 64; sentinels included)
   std::uint32_t flags;  // kind | first << 8 | last << 9 | owner rows << 16
   std::uint32_t owner, partner;  // panel indices
   std::uint32_t r0;     // owner start row
@@ -93,6 +98,11 @@ struct SlicedPlan {
   float* diag = nullptr;  // stored diagonal of H (applied in fp64, not sliced)
   std::uint8_t* xd = nullptr;                 // per-call digit slabs, npanels * kSlabBytes
   std::uint8_t* xt = nullptr;
+  std::uint8_t* zeros = nullptr;  // kPlanes bytes of 0
+  // tiny entries (not exactly sliceable) as CSR over output rows, fp64
+  std::uint32_t ntiny_rows = 0;
+  std::uint32_t *tiny_rows = nullptr, *tiny_off = nullptr, *tiny_in = nullptr;
+  double* tiny_val = nullptr;
   std::uint64_t nrec = 0;
   bool finite = true;  // every stored value finite (else the DMMA kernels run)
   ~SlicedPlan() {
@@ -103,6 +113,11 @@ struct SlicedPlan {
     cudaFree(diag);
     cudaFree(xd);
     cudaFree(xt);
+    cudaFree(zeros);
+    cudaFree(tiny_rows);
+    cudaFree(tiny_off);
+    cudaFree(tiny_in);
+    cudaFree(tiny_val);
   }
 };
 
@@ -118,10 +133,13 @@ __host__ __device__ __forceinline__ std::uint32_t off_b(std::uint32_t n, std::ui
 // exponent E with |v| < 2^E (frexp), for finite nonzero v
 __device__ __forceinline__ int exp_of(double v) { return ilogb(v) + 1; }
 
-// 2^e as a double (normal range; exact)
+// 2^e as a double, exact and branchless for |e| <= 2044 (a product of two
+// normal powers of two; subnormal results are exact too)
 __device__ __forceinline__ double pow2(int e) {
-  if (e >= -1022 && e <= 1023) return __longlong_as_double(static_cast<long long>(e + 1023) << 52);
-  return ldexp(1.0, e);
+  e = max(-2044, min(2044, e));
+  const int h = e >> 1;
+  return __longlong_as_double(static_cast<long long>(h + 1023) << 52) *
+         __longlong_as_double(static_cast<long long>(e - h + 1023) << 52);
 }
 
 // exact int32 -> double without the conversion unit: 2^52 + 2^31 + v
@@ -157,10 +175,13 @@ __global__ void rowexp_kernel(const std::uint64_t* tile_off, const std::uint32_t
 }
 
 __device__ __forceinline__ uint2 make_record(float h, int er, std::uint32_t pos) {
-  // a_int = h 2^(39 - e_r), |a_int| < 2^39; two's complement bytes
-  const long long a = __double2ll_rn(ldexp(static_cast<double>(h), 39 - er));
-  const unsigned long long u = static_cast<unsigned long long>(a);
-  const std::uint32_t d0 = static_cast<std::uint32_t>(a >> 32) & 0xffu;  // signed top byte
+  // a_int = h 2^(38 - e_r), |a_int| < 2^38, as five balanced base-256 digits
+  // (all signed: no cancellation between diagonals in the fp64 recombination)
+  // via the carry-free bias: bytes of (a_int + B) ^ B, B = 0x8080808080
+  constexpr long long kBias = 0x8080808080ll;
+  const long long a = __double2ll_rn(ldexp(static_cast<double>(h), 38 - er));
+  const unsigned long long u = static_cast<unsigned long long>((a + kBias) ^ kBias);
+  const std::uint32_t d0 = static_cast<std::uint32_t>(u >> 32) & 0xffu;  // weight 2^32
   const std::uint32_t d1 = static_cast<std::uint32_t>(u >> 24) & 0xffu;
   const std::uint32_t d2 = static_cast<std::uint32_t>(u >> 16) & 0xffu;
   const std::uint32_t d3 = static_cast<std::uint32_t>(u >> 8) & 0xffu;
@@ -168,13 +189,34 @@ __device__ __forceinline__ uint2 make_record(float h, int er, std::uint32_t pos)
   return make_uint2(pos | (d0 << 16) | (d1 << 24), d2 | (d3 << 8) | (d4 << 16));
 }
 
+// Producer lane l of a warp loads the 16-byte pair of records (2 (32 w + l),
+// 2 (32 w + l) + 1) and stores the first of every pair in one warp-wide
+// pass, the second in the next: so rank-major record k = 64 w + 32 h + l is
+// kept at 64 w + 2 l + h, and each pass stores 32 consecutive ranks.
+__device__ __forceinline__ unsigned interleave(unsigned k) { return (k & ~63u) | ((k & 31u) << 1) | ((k >> 5) & 1u); }
+
 // One CTA per single-pass item: the item's entries as slice records, the
 // mirrored twin of every strictly lower entry of a diagonal tile, in an order
 // where every 32 consecutive records hit 32 distinct shared-memory banks of
 // the slice planes (bank = 4 (r & 7) + (c & 15) / 4): records are ranked
 // within their bank and emitted rank-major.
+// An entry is sliced only when its a_int is exact (|h| >= 2^(e_r - 15) for
+// a normal fp32 h); the few smaller ones go to the tiny list instead (output
+// row, input row, value), added in fp64 after the SpMM (tiny_fix_kernel), so
+// every stored value enters the product exactly.
+struct Tiny {
+  std::uint32_t out, in;
+  double v;
+};
+
+__device__ __forceinline__ bool sliceable(float h, int er) {
+  const double s = ldexp(static_cast<double>(h), 38 - er);
+  return s == rint(s);
+}
+
 __global__ void records_kernel(const OzItem* items, const std::uint32_t* sp_sched, const std::uint32_t* idx,
-                               const float* val, const int* rowexp, uint2* rec, float* diag_out) {
+                               const float* val, const int* rowexp, const std::uint32_t* panel_start, uint2* rec,
+                               float* diag_out, Tiny* tiny, unsigned* ntiny, unsigned tiny_cap) {
   __shared__ unsigned cnt[32], cnt2[32];
   const std::uint32_t i = blockIdx.x;
   const OzItem it = items[i];
@@ -198,6 +240,18 @@ __global__ void records_kernel(const OzItem* items, const std::uint32_t* sp_sche
       }
       for (int twin = 0; twin < (diag ? 2 : 1); ++twin) {
         const std::uint32_t rr = twin ? c : r, cc = twin ? r : c;
+        const int er = rowexp[it.r0 + rr];
+        if (!sliceable(h, er)) {
+          if (pass == 1) {
+            const std::uint32_t gr = it.r0 + rr, gc = (diag ? it.r0 : panel_start[it.partner]) + cc;
+            const unsigned t = atomicAdd(ntiny, diag ? 1u : 2u);
+            if (t + 1 < tiny_cap) {
+              tiny[t] = Tiny{gr, gc, static_cast<double>(h)};
+              if (!diag) tiny[t + 1] = Tiny{gc, gr, static_cast<double>(h)};
+            }
+          }
+          continue;
+        }
         const std::uint32_t pos = off_a(rr, cc);
         const std::uint32_t bank = (pos >> 2) & 31u;
         if (pass == 0) {
@@ -205,92 +259,137 @@ __global__ void records_kernel(const OzItem* items, const std::uint32_t* sp_sche
           continue;
         }
         const unsigned rank = atomicAdd(&cnt2[bank], 1u);
-        unsigned out = 0;
-        for (int b = 0; b < 32; ++b) out += min(cnt[b], rank) + ((static_cast<unsigned>(b) < bank && cnt[b] > rank) ? 1u : 0u);
-        rec[it.rec0 + out] = make_record(h, rowexp[it.r0 + rr], pos);
+        unsigned k = 0;  // rank-major position
+        for (int b = 0; b < 32; ++b) k += min(cnt[b], rank) + ((static_cast<unsigned>(b) < bank && cnt[b] > rank) ? 1u : 0u);
+        rec[it.rec0 + interleave(k)] = make_record(h, er, pos);
       }
     }
     __syncthreads();
   }
   unsigned total = 0;
   for (int b = 0; b < 32; ++b) total += cnt[b];
-  for (std::uint32_t k = total + threadIdx.x; k < it.nrec; k += blockDim.x) rec[it.rec0 + k] = make_uint2(kNoEntry, 0);
+  for (std::uint32_t k = total + threadIdx.x; k < it.nrec; k += blockDim.x)
+    rec[it.rec0 + interleave(k)] = make_uint2(kNoEntry, 0);  // (nrec is a multiple of 64)
 }
 
 // ----------------------------------------------------------------- per call
 
+// x = M 2^q with M a 53-bit integer (exact decomposition of a finite double)
+__device__ __forceinline__ void decompose(double x, long long& m, int& q) {
+  const long long bits = __double_as_longlong(x);
+  const int eb = static_cast<int>((bits >> 52) & 0x7ff);
+  const long long mant = bits & ((1ll << 52) - 1);
+  m = eb ? (mant | (1ll << 52)) : mant;
+  q = (eb ? eb : 1) - 1075;
+  if (bits < 0) m = -m;
+}
+// round(M 2^(q + s)) for |M 2^(q+s)| <= 2^54, integer arithmetic only
+__device__ __forceinline__ long long scaled(long long m, int sh) {
+  if (sh >= 0) return m << sh;
+  if (sh < -62) return 0;
+  const long long a = m < 0 ? -m : m;
+  const long long r = (a + (1ll << (-sh - 1))) >> -sh;
+  return m < 0 ? -r : r;
+}
+// exponent E with |x| < 2^E for M 2^q (M != 0)
+__device__ __forceinline__ int exp_mq(long long m, int q) {
+  const long long a = m < 0 ? -m : m;
+  return 64 - __clzll(a) + q;
+}
+
 // X digits of one panel: B-operand slabs for the row part (x) and the
 // transposed part (x 2^e_r), seven balanced digits per value, plus the
-// per-column exponents. Non-finite values are staged as 0 (flag set; the
-// caller's fix-up adds their exact terms).
+// per-column exponents, in integer arithmetic on the bit patterns. Thread
+// (column j, row group g) handles rows 4 (g + 8 u) .. +3, u = 0..3, so each
+// digit of four consecutive rows is one 32-bit shared store. Non-finite
+// values are staged as 0 (flag set; the caller's fix-up adds their exact
+// terms).
 __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uint32_t ldx, std::uint32_t mc,
                                                        const std::uint32_t* panel_start, const int* rowexp,
                                                        std::uint8_t* xd, std::uint8_t* xt, unsigned* nonfinite,
                                                        unsigned launch_id) {
   __shared__ __align__(16) std::uint8_t sd[2][kSlab];
-  __shared__ int wmax[2][4][16];
+  __shared__ int wmax[2][8][16];
   __shared__ int cmax[2][16];
   const std::uint32_t P = blockIdx.x, p0 = panel_start[P], rows = panel_start[P + 1] - p0;
-  const int r = threadIdx.x, w = r >> 5, lane = r & 31;
-  const int er = r < static_cast<int>(rows) ? rowexp[p0 + r] : 0;
-  double xv[16];
+  const int tid = threadIdx.x, j = tid & 15, g = tid >> 4;
+  long long mv[16];
+  int qv[16], er[16];
+  int E = INT_MIN / 4, Ep = INT_MIN / 4;
   bool bad = false;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    double v = (r < static_cast<int>(rows) && j < static_cast<int>(mc)) ? x[static_cast<std::size_t>(p0 + r) * ldx + j] : 0.0;
-    if (!isfinite(v)) {
-      v = 0.0;
-      bad = true;
-    }
-    xv[j] = v;
-    int E = v != 0.0 ? exp_of(v) : INT_MIN / 4, Ep = v != 0.0 ? E + er : INT_MIN / 4;
+  for (int u = 0; u < 4; ++u)
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) {
-      E = max(E, __shfl_xor_sync(0xffffffffu, E, s));
-      Ep = max(Ep, __shfl_xor_sync(0xffffffffu, Ep, s));
-    }
-    if (lane == 0) {
-      wmax[0][w][j] = E;
-      wmax[1][w][j] = Ep;
-    }
-  }
-  if (bad) *nonfinite = launch_id;
-  __syncthreads();
-  if (r < 32) {
-    const int k = r >> 4, j = r & 15;
-    int m = max(max(wmax[k][0][j], wmax[k][1][j]), max(wmax[k][2][j], wmax[k][3][j]));
-    cmax[k][j] = m < INT_MIN / 8 ? 0 : m;  // all-zero column: exponent 0, digits 0
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < 2; ++k)
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      long long v = __double2ll_rn(ldexp(xv[j], (k ? er : 0) + 54 - cmax[k][j]));
-      int dig[kXD];
-#pragma unroll
-      for (int t = kXD - 1; t > 0; --t) {
-        int dd = static_cast<int>(v & 0xff);
-        dd = dd >= 128 ? dd - 256 : dd;
-        dig[t] = dd;
-        v = (v - dd) >> 8;
+    for (int v = 0; v < 4; ++v) {
+      const int r = 4 * (g + 8 * u) + v, e = 4 * u + v;
+      const bool in = r < static_cast<int>(rows);
+      double xv = (in && j < static_cast<int>(mc)) ? x[static_cast<std::size_t>(p0 + r) * ldx + j] : 0.0;
+      er[e] = in ? rowexp[p0 + r] : 0;
+      if (!isfinite(xv)) {
+        xv = 0.0;
+        bad = true;
       }
-      dig[0] = static_cast<int>(v);
-#pragma unroll
-      for (int t = 0; t < kXD; ++t) sd[k][off_b(16 * t + j, r)] = static_cast<std::uint8_t>(dig[t]);
+      decompose(xv, mv[e], qv[e]);
+      if (mv[e] != 0) {
+        const int ee = exp_mq(mv[e], qv[e]);
+        E = max(E, ee);
+        Ep = max(Ep, ee + er[e]);
+      }
     }
+  if (bad) *nonfinite = launch_id;
+  E = max(E, __shfl_xor_sync(0xffffffffu, E, 16));
+  Ep = max(Ep, __shfl_xor_sync(0xffffffffu, Ep, 16));
+  if ((tid & 31) < 16) {
+    wmax[0][tid >> 5][j] = E;
+    wmax[1][tid >> 5][j] = Ep;
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int k = tid >> 4, jj = tid & 15;
+    const int m = max(max(wmax[k][0][jj], wmax[k][1][jj]), max(wmax[k][2][jj], wmax[k][3][jj]));
+    cmax[k][jj] = m < INT_MIN / 8 ? 0 : m;  // all-zero column: exponent 0, digits 0
+  }
+  __syncthreads();
+  // Balanced base-256 digits without carries: x_int + sum_t 128 256^t has
+  // the plain bytes X_t + 128, so the digit bytes (two's complement) are the
+  // bytes of (x_int + B) ^ B, B = 0x80808080808080; byte t weighs 256^t
+  // (digit index 6 - t). Four rows' bytes of one digit -> one word (PRMT).
+  constexpr long long kBias = 0x0080808080808080ll;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int cm = cmax[k][j];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      std::uint32_t lo[4], hi[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        const int e = 4 * u + v;
+        const long long w = (scaled(mv[e], qv[e] + (k ? er[e] : 0) + 54 - cm) + kBias) ^ kBias;
+        lo[v] = static_cast<std::uint32_t>(w);
+        hi[v] = static_cast<std::uint32_t>(w >> 32);
+      }
+#pragma unroll
+      for (int t = 0; t < kXD; ++t) {  // byte t of the values = digit kXD - 1 - t
+        const std::uint32_t* src = t < 4 ? lo : hi;
+        const std::uint32_t sel = static_cast<std::uint32_t>(t & 3) | (static_cast<std::uint32_t>(4 + (t & 3)) << 4);
+        const std::uint32_t p01 = __byte_perm(src[0], src[1], sel), p23 = __byte_perm(src[2], src[3], sel);
+        *reinterpret_cast<std::uint32_t*>(&sd[k][off_b(16 * (kXD - 1 - t) + j, 4 * (g + 8 * u))]) =
+            __byte_perm(p01, p23, 0x5410);
+      }
+    }
+  }
   __syncthreads();
   const uint4* s0 = reinterpret_cast<const uint4*>(sd[0]);
   const uint4* s1 = reinterpret_cast<const uint4*>(sd[1]);
   uint4* g0 = reinterpret_cast<uint4*>(xd + static_cast<std::size_t>(P) * kSlabBytes);
   uint4* g1 = reinterpret_cast<uint4*>(xt + static_cast<std::size_t>(P) * kSlabBytes);
-  for (int e = r; e < kSlab / 16; e += 128) {
+  for (int e = tid; e < kSlab / 16; e += 128) {
     g0[e] = s0[e];
     g1[e] = s1[e];
   }
-  if (r < 16) {
-    reinterpret_cast<int*>(xd + static_cast<std::size_t>(P) * kSlabBytes + kSlab)[r] = cmax[0][r];
-    reinterpret_cast<int*>(xt + static_cast<std::size_t>(P) * kSlabBytes + kSlab)[r] = cmax[1][r];
+  if (tid < 16) {
+    reinterpret_cast<int*>(xd + static_cast<std::size_t>(P) * kSlabBytes + kSlab)[tid] = cmax[0][tid];
+    reinterpret_cast<int*>(xt + static_cast<std::size_t>(P) * kSlabBytes + kSlab)[tid] = cmax[1][tid];
   }
 }
 
@@ -306,15 +405,33 @@ struct SlicedArgs {
   double* y;
   double* partial;
   std::uint32_t ldx, ldy, mc, row_base;
+  const std::uint8_t* zeros;  // kPlanes zero bytes (the slice buffers are cleared by a bulk copy)
+  long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
+  int ablate;        // timing-only (CIEG_SLICED_ABLATE=1): no clear/scatter -- results invalid
 };
 
+// (slabs hold the digits only -- the exponents are read from global memory --
+// so every operand starts on a 1024-byte boundary: whole 128-byte core matrices)
 struct Smem {
   std::uint8_t planes[2][kPlanes];
-  std::uint8_t xd[2][kSlabBytes];
-  std::uint8_t xt[2][kSlabBytes];
-  std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2];
+  std::uint8_t xd[2][kSlab];
+  std::uint8_t xt[2][kSlab];
+  std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2], zeroed[2];
   std::uint32_t tmem;
 };
+
+constexpr int kBatch = 8;  // 16-byte record pairs per producer thread per batch
+
+__device__ __forceinline__ void load_batch(const uint2* rec, const OzItem& it, std::uint32_t q0, int pt,
+                                           uint4 (&v)[kBatch]) {
+  const uint4* src = reinterpret_cast<const uint4*>(rec + it.rec0);
+  const std::uint32_t nq = it.nrec >> 1;
+#pragma unroll
+  for (int u = 0; u < kBatch; ++u) {
+    const std::uint32_t q = q0 + pt + u * kProducers;
+    v[u] = q < nq ? __ldg(src + q) : make_uint4(kNoEntry, 0, kNoEntry, 0);
+  }
+}
 
 __device__ __forceinline__ void scatter(std::uint8_t* pl, std::uint32_t x, std::uint32_t y) {
   const std::uint32_t pos = x & 0xffffu;
@@ -332,8 +449,9 @@ __device__ __forceinline__ void recombine(std::uint32_t taddr, double (&v)[16]) 
   std::int32_t hi[16], lo[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = 0.0;
-#pragma unroll
-  for (int d = kXD - 1; d >= 1; d -= 2) {
+  static_assert(kDiag % 2 == 0, "pairs of diagonals");
+#pragma unroll 1
+  for (int d = kDiag - 1; d >= 1; d -= 2) {  // rolled: a small instruction footprint
     umma::ld16(taddr + 16 * d, hi);
     umma::ld16(taddr + 16 * (d - 1), lo);
     umma::ld_wait();
@@ -343,13 +461,26 @@ __device__ __forceinline__ void recombine(std::uint32_t taddr, double (&v)[16]) 
       v[j] = fma(v[j], 0x1p-8, i2d(lo[j]));
     }
   }
-  if constexpr (kXD % 2 == 1) {
-    umma::ld16(taddr, lo);
-    umma::ld_wait();
+}
+
+// the 16 column exponents stored after a panel's digit slab
+__device__ __forceinline__ void load_exps(const std::uint8_t* slabs, std::uint32_t panel, int (&ex)[16]) {
+  const int4* p = reinterpret_cast<const int4*>(slabs + static_cast<std::size_t>(panel) * kSlabBytes + kSlab);
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = fma(v[j], 0x1p-8, i2d(lo[j]));
+  for (int j = 0; j < 4; ++j) {
+    const int4 e4 = __ldg(p + j);
+    ex[4 * j] = e4.x;
+    ex[4 * j + 1] = e4.y;
+    ex[4 * j + 2] = e4.z;
+    ex[4 * j + 3] = e4.w;
   }
 }
+
+#define TRACE(item, slot, cond)                                                                      \
+  do {                                                                                               \
+    if (a.trace && blockIdx.x == 0 && (cond) && (item) - i_beg < 256)                                \
+      a.trace[((item) - i_beg) * 16 + (slot)] = clock64();                                           \
+  } while (0)
 
 __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
@@ -364,113 +495,164 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       umma::mbar_init(&S.empty_t[b], 1);
       umma::mbar_init(&S.acc_full[b], 1);
       umma::mbar_init(&S.acc_empty[b], 8);
+      umma::mbar_init(&S.zeroed[b], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) umma::tmem_alloc<512>(&S.tmem);
   umma::fence_before();
   __syncthreads();
+  // Diagonal kDiag - 1 is first written by slice 1 (slice 0's MMA covers
+  // d < kXD only), so it accumulates onto TMEM that must start at zero: the
+  // epilogue warps clear those 16 columns of both stages here and again
+  // after reading each stage.
+  if (warp >= 8) {
+    umma::fence_after();
+    const std::uint32_t base = S.tmem + (static_cast<std::uint32_t>(32 * (warp & 3)) << 16) + (warp < 12 ? 0 : kND);
+    umma::st16_zero(base + 16 * (kDiag - 1));
+    umma::st16_zero(base + kStageCols + 16 * (kDiag - 1));
+    umma::st_wait();
+    umma::fence_before();
+  }
+  __syncthreads();
+  // The slice buffers are cleared by bulk copies from a zero page: here for
+  // the first two items, then by the row epilogue the moment the MMAs of the
+  // item that used a buffer complete (acc_full), two items ahead.
+  if (tid == 0 && !a.ablate)
+    for (std::uint32_t j = 0; j < 2 && i_beg + j < i_end; ++j) {
+      umma::mbar_arrive_tx(&S.zeroed[j], kPlanes);
+      umma::bulk_g2s(S.planes[j], a.zeros, kPlanes, &S.zeroed[j]);
+    }
   umma::fence_after();
   const std::uint32_t tbase = S.tmem;
 
   if (warp == 0) {
     // ------------------------------------------------------------ MMA issue
+    // The whole warp runs the issue loop converged, descriptors are
+    // warp-uniform (base descriptor + constant offsets, in uniform
+    // registers), one elected lane executes each tcgen05.mma: the tensor core
+    // needs a new MMA every ~50 cycles, which a per-MMA divergent issue path
+    // (R2UR + waterfall per instruction) cannot sustain.
     std::uint32_t k = 0, owners = 0;
     int o = 0;
-    const std::uint32_t pa[2] = {umma::smem_u32(S.planes[0]), umma::smem_u32(S.planes[1])};
-    const std::uint32_t pb[2] = {umma::smem_u32(S.xd[0]), umma::smem_u32(S.xd[1])};
-    const std::uint32_t pt[2] = {umma::smem_u32(S.xt[0]), umma::smem_u32(S.xt[1])};
+    const std::uint64_t a_k0 = umma::sdesc(umma::smem_u32(S.planes[0]), 128, 1024);   // A K-major (H X)
+    const std::uint64_t a_mn0 = umma::sdesc(umma::smem_u32(S.planes[0]), 1024, 128);  // A MN-major (H^T X)
+    const std::uint64_t b_d0 = umma::sdesc(umma::smem_u32(S.xd[0]), 128, 1024);
+    const std::uint64_t b_t0 = umma::sdesc(umma::smem_u32(S.xt[0]), 128, 1024);
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
       const OzItem it = a.items[i];
       const int b = k & 1;
+      TRACE(i, 0, lane == 0);
       if ((it.flags >> 8) & 1u) {
         o = owners & 1;
         umma::mbar_wait(&S.full_t[o], (owners >> 1) & 1u);
         ++owners;
       }
       umma::mbar_wait(&S.full_a[b], (k >> 1) & 1u);
+      TRACE(i, 1, lane == 0);
       umma::mbar_wait(&S.acc_empty[b], ((k >> 1) & 1u) ^ 1u);
+      TRACE(i, 2, lane == 0);
       umma::fence_after();
-      if (lane == 0) {
-        const std::uint32_t d_row = tbase + b * kStageCols, d_tr = d_row + kNB;
-        const bool trans = (it.flags & 0xffu) == 0u;
+      const std::uint32_t d_row = tbase + b * kStageCols, d_tr = d_row + kND;
+      const bool trans = (it.flags & 0xffu) == 0u;
+      // descriptor start-address field: (byte offset) >> 4, no carry out of 14 bits
+      const std::uint64_t ab = static_cast<std::uint64_t>(b * (kPlanes >> 4));
+      const std::uint64_t bd = b_d0 + static_cast<std::uint64_t>(b * (kSlab >> 4));
+      const std::uint64_t bt = b_t0 + static_cast<std::uint64_t>(o * (kSlab >> 4));
+#pragma unroll 1
+      for (int s = 0; s < kAS; ++s) {
+        const int n = 16 * min(kXD, kDiag - s);  // digits t with s + t < kDiag
+        const std::uint32_t id_row = umma::idesc_i8(1, 1, 0, 0, 128, n);  // balanced digits: all signed
+        const std::uint32_t id_tr = umma::idesc_i8(1, 1, 1, 0, 128, n);
 #pragma unroll
-        for (int s = 0; s < kAS; ++s) {
-          const int n = 16 * (kXD - s);
-          const std::uint32_t id_row = umma::idesc_i8(s == 0, 1, 0, 0, 128, n);
-          const std::uint32_t id_tr = umma::idesc_i8(s == 0, 1, 1, 0, 128, n);
-          const std::uint32_t ap = pa[b] + s * kPlane;
-#pragma unroll
-          for (int ks = 0; ks < kTD / 32; ++ks) {
-            umma::mma_i8(d_row + 16 * s, umma::sdesc(ap + 256 * ks, 128, 1024), umma::sdesc(pb[b] + 256 * ks, 128, 1024),
-                         id_row, (s | ks) != 0);
-            if (trans)
-              umma::mma_i8(d_tr + 16 * s, umma::sdesc(ap + 4096 * ks, 1024, 128),
-                           umma::sdesc(pt[o] + 256 * ks, 128, 1024), id_tr, (s | ks) != 0);
-          }
+        for (int ks = 0; ks < kTD / 32; ++ks) {
+          umma::mma_i8_warp(d_row + 16 * s, a_k0 + ab + ((s * kPlane + 256 * ks) >> 4), bd + ((256 * ks) >> 4), id_row,
+                            (s | ks) != 0);
+          if (trans)
+            umma::mma_i8_warp(d_tr + 16 * s, a_mn0 + ab + ((s * kPlane + 4096 * ks) >> 4), bt + ((256 * ks) >> 4),
+                              id_tr, (s | ks) != 0);
         }
-        umma::commit(&S.empty_a[b]);
-        umma::commit(&S.acc_full[b]);
-        if ((it.flags >> 9) & 1u) umma::commit(&S.empty_t[o]);
       }
-      __syncwarp();
+      umma::commit_warp(&S.empty_a[b]);
+      umma::commit_warp(&S.acc_full[b]);
+      if ((it.flags >> 9) & 1u) umma::commit_warp(&S.empty_t[o]);
+      TRACE(i, 3, lane == 0);
+
     }
   } else if (warp < 8) {
     // ------------------------------------------------------------ producers
+    // Records stream in batches of kBatch 16-byte pairs per thread, one batch
+    // in flight while the previous one is scattered; the first batch of the
+    // next item is loaded before this item's buffer wait and clear.
     const int pt = tid - 32;
     std::uint32_t k = 0, owners = 0;
+    constexpr std::uint32_t kStep = kBatch * kProducers;
+    uint4 cur[kBatch], nxt[kBatch];
+    OzItem it = a.items[i_beg < i_end ? i_beg : 0];
+    if (i_beg < i_end) load_batch(a.rec, it, 0, pt, cur);
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-      const OzItem it = a.items[i];
       const int b = k & 1;
+      TRACE(i, 8, pt == 0);
+      const OzItem nit = i + 1 < i_end ? a.items[i + 1] : it;
       if ((it.flags >> 8) & 1u) {
         const int o = owners & 1;
         if (pt == 0) {
           umma::mbar_wait(&S.empty_t[o], ((owners >> 1) & 1u) ^ 1u);
-          umma::mbar_arrive_tx(&S.full_t[o], kSlabBytes);
-          umma::bulk_g2s(S.xt[o], a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes, kSlabBytes, &S.full_t[o]);
+          umma::mbar_arrive_tx(&S.full_t[o], kSlab);
+          umma::bulk_g2s(S.xt[o], a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes, kSlab, &S.full_t[o]);
         }
         ++owners;
       }
       umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
+      TRACE(i, 4, pt == 0);
       if (pt == 0) {
-        umma::mbar_arrive_tx(&S.full_a[b], kSlabBytes);
-        umma::bulk_g2s(S.xd[b], a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes, kSlabBytes, &S.full_a[b]);
+        umma::mbar_arrive_tx(&S.full_a[b], kSlab);
+        umma::bulk_g2s(S.xd[b], a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes, kSlab, &S.full_a[b]);
         if (i + 1 < i_end) {  // next item's records into L2 while this one is placed
-          const OzItem nx = a.items[i + 1];
-          const std::uint8_t* p = reinterpret_cast<const std::uint8_t*>(a.rec + nx.rec0);
-          for (std::uint32_t off = 0; off < 8u * nx.nrec; off += 1u << 16)
-            umma::prefetch_l2(p + off, min(1u << 16, 8u * nx.nrec - off));
+          const std::uint8_t* p = reinterpret_cast<const std::uint8_t*>(a.rec + nit.rec0);
+          for (std::uint32_t off = 0; off < 8u * nit.nrec; off += 1u << 16)
+            umma::prefetch_l2(p + off, min(1u << 16, 8u * nit.nrec - off));
         }
       }
-      uint4* z = reinterpret_cast<uint4*>(S.planes[b]);
-      for (int e = pt; e < kPlanes / 16; e += kProducers) z[e] = make_uint4(0, 0, 0, 0);
-      asm volatile("bar.sync 1, %0;" ::"n"(kProducers) : "memory");
-      const uint4* src = reinterpret_cast<const uint4*>(a.rec + it.rec0);
-      const std::uint32_t nq = it.nrec >> 1;
+      if (!a.ablate) umma::mbar_wait(&S.zeroed[b], (k >> 1) & 1u);
+      TRACE(i, 5, pt == 0);
       std::uint8_t* pl = S.planes[b];
-      for (std::uint32_t q = pt; q < nq; q += 4 * kProducers) {
-        uint4 v[4];
+      const std::uint32_t nq = it.nrec >> 1;
+      for (std::uint32_t q0 = 0; q0 < nq; q0 += kStep) {
+        if (q0 + kStep < nq)
+          load_batch(a.rec, it, q0 + kStep, pt, nxt);
+        else if (i + 1 < i_end)
+          load_batch(a.rec, nit, 0, pt, nxt);
+        if (!a.ablate) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          v[u] = q + u * kProducers < nq ? __ldg(src + q + u * kProducers) : make_uint4(kNoEntry, 0, kNoEntry, 0);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          scatter(pl, v[u].x, v[u].y);
-          scatter(pl, v[u].z, v[u].w);
+          for (int u = 0; u < kBatch; ++u) {
+            scatter(pl, cur[u].x, cur[u].y);
+            scatter(pl, cur[u].z, cur[u].w);
+          }
         }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) cur[u] = nxt[u];
       }
+      TRACE(i, 6, pt == 0);
       umma::fence_async_smem();
       umma::mbar_arrive(&S.full_a[b]);
+      TRACE(i, 7, pt == 0);
+      it = nit;
     }
   } else if (warp < 12) {
     // ------------------------------------------------- row-part epilogue
+    // The next item's descriptor and column exponents are loaded one item
+    // ahead (global latency overlaps this item's wait and math).
     const int q = warp - 8, r = 32 * q + lane;
     const std::uint32_t lanes = static_cast<std::uint32_t>(32 * q) << 16;
     double yacc[16];
     int er = 0;
     std::uint32_t k = 0;
+    OzItem it = a.items[i_beg < i_end ? i_beg : 0];
+    int ex[16];
+    if (i_beg < i_end) load_exps(a.xd, it.partner, ex);
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-      const OzItem it = a.items[i];
+      const OzItem nit = i + 1 < i_end ? a.items[i + 1] : it;
       const int b = k & 1;
       const int prow = static_cast<int>(it.flags >> 16);
       if ((it.flags >> 8) & 1u) {
@@ -478,16 +660,27 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         for (int j = 0; j < 16; ++j) yacc[j] = 0.0;
         er = r < prow ? a.rowexp[it.r0 + r] : 0;
       }
+      TRACE(i, 9, lane == 0 && q == 0);
       umma::mbar_wait(&S.acc_full[b], (k >> 1) & 1u);
+      TRACE(i, 11, lane == 0 && q == 0);
+      if (q == 0 && lane == 0 && i + 2 < i_end && !a.ablate) {  // buffer b is free: clear it for item k + 2
+        umma::mbar_arrive_tx(&S.zeroed[b], kPlanes);
+        umma::bulk_g2s(S.planes[b], a.zeros, kPlanes, &S.zeroed[b]);
+      }
       umma::fence_after();
       double v[16];
       recombine(tbase + lanes + b * kStageCols, v);
+      umma::st16_zero(tbase + lanes + b * kStageCols + 16 * (kDiag - 1));
+      umma::st_wait();
+      TRACE(i, 12, lane == 0 && q == 0);
       umma::fence_before();
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
-      const int* ex = reinterpret_cast<const int*>(a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes + kSlab);
+      TRACE(i, 13, lane == 0 && q == 0);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) yacc[j] = fma(v[j], pow2(er + __ldg(ex + j) - 13), yacc[j]);
+      for (int j = 0; j < 16; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 12), yacc[j]);
+      TRACE(i, 10, lane == 0 && q == 0);
+      if (i + 1 < i_end) load_exps(a.xd, nit.partner, ex);
       if ((it.flags & 0xffu) == 2u && r < prow) {  // d_r x_r in fp64 (Inf/NaN x: the caller's fix-up adds it)
         const double dr = static_cast<double>(a.diag[it.r0 + r]);
         const double* xr = a.x + static_cast<std::size_t>(it.r0 + r) * a.ldx;
@@ -503,30 +696,47 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         for (int j = 0; j < 16; ++j)
           if (j < static_cast<int>(a.mc)) yr[j] = yacc[j];
       }
+      it = nit;
     }
   } else {
     // ------------------------------------------ transposed-part epilogue
     const int q = warp - 12, c = 32 * q + lane;
     const std::uint32_t lanes = static_cast<std::uint32_t>(32 * q) << 16;
     std::uint32_t k = 0;
+    OzItem it = a.items[i_beg < i_end ? i_beg : 0];
+    int ex[16];
+    if (i_beg < i_end) load_exps(a.xt, it.owner, ex);
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-      const OzItem it = a.items[i];
+      const OzItem nit = i + 1 < i_end ? a.items[i + 1] : it;
       const int b = k & 1;
       const bool trans = (it.flags & 0xffu) == 0u;
       umma::mbar_wait(&S.acc_full[b], (k >> 1) & 1u);
+      TRACE(i, 14, lane == 0 && q == 0);
       umma::fence_after();
       double v[16];
-      if (trans) recombine(tbase + lanes + b * kStageCols + kNB, v);
+      if (trans) {
+        recombine(tbase + lanes + b * kStageCols + kND, v);
+        umma::st16_zero(tbase + lanes + b * kStageCols + kND + 16 * (kDiag - 1));
+        umma::st_wait();
+      }
       umma::fence_before();
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
+      TRACE(i, 15, lane == 0 && q == 0);
       if (trans && c < static_cast<int>(it.orow)) {
-        const int* ex = reinterpret_cast<const int*>(a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes + kSlab);
         double* out = a.partial + (static_cast<std::size_t>(i) * kTD + c) * a.mc;
+        if (a.mc == 16) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (j < static_cast<int>(a.mc)) out[j] = v[j] * pow2(__ldg(ex + j) - 13);
+          for (int j = 0; j < 16; j += 2)
+            *reinterpret_cast<double2*>(out + j) = make_double2(v[j] * pow2(ex[j] - 12), v[j + 1] * pow2(ex[j + 1] - 12));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < static_cast<int>(a.mc)) out[j] = v[j] * pow2(ex[j] - 12);
+        }
       }
+      if (i + 1 < i_end && nit.owner != it.owner) load_exps(a.xt, nit.owner, ex);
+      it = nit;
     }
   }
   umma::fence_before();
@@ -567,7 +777,7 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     it.partner = panel_of(ps, d[5]);
     it.rec0 = total;
     std::uint64_t n = 4 * (q1 - q0) * (kind == 2 ? 2 : 1);
-    n += n & 1;
+    n = (n + 63) & ~63ull;  // whole 64-record interleave chunks
     it.nrec = static_cast<std::uint32_t>(n);
     total += n;
   }
@@ -599,16 +809,51 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     cudaFree(bad);
     pl->finite = bad_h == 0;
     std::uint32_t* dsched = m->sp_sched;
+    const unsigned tiny_cap = static_cast<unsigned>(std::min<std::uint64_t>(1u << 30, m->nnz / 512 + 4096));
+    Tiny* tiny = nullptr;
+    CIEG_CUDA(cudaMalloc(&tiny, sizeof(Tiny) * tiny_cap));
+    unsigned* ntiny = upload(std::vector<unsigned>{0u});
     if (nitems)
       records_kernel<<<nitems, 256, 0, ctx->stream>>>(pl->items, dsched, m->idx, static_cast<const float*>(m->val),
-                                                      pl->rowexp, pl->rec, pl->diag);
+                                                      pl->rowexp, m->panel_start, pl->rec, pl->diag, tiny, ntiny,
+                                                      tiny_cap);
     CIEG_CUDA(cudaGetLastError());
+    unsigned nt = 0;
+    CIEG_CUDA(cudaMemcpyAsync(&nt, ntiny, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (nt + 1 >= tiny_cap) {
+      pl->finite = false;  // too many unsliceable entries: this matrix runs the fp64 DMMA kernels
+    } else if (nt) {
+      std::vector<Tiny> th(nt);
+      CIEG_CUDA(cudaMemcpy(th.data(), tiny, sizeof(Tiny) * nt, cudaMemcpyDeviceToHost));
+      std::sort(th.begin(), th.end(), [](const Tiny& a, const Tiny& b) { return a.out < b.out || (a.out == b.out && a.in < b.in); });
+      std::vector<std::uint32_t> rows, off{0}, in(nt);
+      std::vector<double> v(nt);
+      for (unsigned t = 0; t < nt; ++t) {
+        if (t == 0 || th[t].out != th[t - 1].out) {
+          if (t) off.push_back(t);
+          rows.push_back(th[t].out);
+        }
+        in[t] = th[t].in;
+        v[t] = th[t].v;
+      }
+      off.push_back(nt);
+      pl->ntiny_rows = static_cast<std::uint32_t>(rows.size());
+      pl->tiny_rows = upload(rows);
+      pl->tiny_off = upload(off);
+      pl->tiny_in = upload(in);
+      pl->tiny_val = upload(v);
+    }
+    cudaFree(tiny);
+    cudaFree(ntiny);
     ctx->launches += 2;
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
     cudaFree(tpi);
     cudaFree(tpj);
     CIEG_CUDA(cudaMalloc(&pl->xd, static_cast<std::size_t>(m->npanels) * kSlabBytes));
     CIEG_CUDA(cudaMalloc(&pl->xt, static_cast<std::size_t>(m->npanels) * kSlabBytes));
+    CIEG_CUDA(cudaMalloc(&pl->zeros, kPlanes));
+    CIEG_CUDA(cudaMemset(pl->zeros, 0, kPlanes));
   } catch (...) {
     delete pl;
     throw;
@@ -616,7 +861,35 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
   return pl;
 }
 
+// y[out] += sum h x[in] over the tiny entries of each output row (fixed
+// order; non-finite x are left to the caller's non-finite fix-up).
+__global__ void tiny_fix_kernel(const std::uint32_t* rows, const std::uint32_t* off, const std::uint32_t* in,
+                                const double* val, std::uint32_t nrows, const double* x, std::uint32_t ldx, double* y,
+                                std::uint32_t ldy, std::uint32_t mc, std::uint32_t row_base) {
+  const std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
+  const std::uint32_t t = e >> 4, j = e & 15u;
+  if (t >= nrows || j >= mc) return;
+  double s = 0.0;
+  for (std::uint32_t k = off[t]; k < off[t + 1]; ++k) {
+    const double xv = x[static_cast<std::size_t>(in[k]) * ldx + j];
+    s = fma(val[k], isfinite(xv) ? xv : 0.0, s);
+  }
+  y[static_cast<std::size_t>(rows[t] - row_base) * ldy + j] += s;
+}
+
 }  // namespace
+
+void launch_sliced_tiny_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
+                            std::uint32_t ldy, std::uint32_t mc) {
+  const SlicedPlan* pl = m->sliced;
+  if (!pl || pl->ntiny_rows == 0) return;
+  const std::uint32_t threads = pl->ntiny_rows * 16;
+  tiny_fix_kernel<<<(threads + 255) / 256, 256, 0, ctx->stream>>>(pl->tiny_rows, pl->tiny_off, pl->tiny_in,
+                                                                  pl->tiny_val, pl->ntiny_rows, x, ldx, y, ldy, mc,
+                                                                  m->row_lo);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
 
 bool sliced_supported(const cieg_mat* m) {
   return m->precision == 0 && m->tile_edge == kTD && m->sp_sched != nullptr && m->row_lo == 0 &&
@@ -643,13 +916,34 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
   digitize_kernel<<<m->npanels, 128, 0, ctx->stream>>>(x, ldx, mc, m->panel_start, pl->rowexp, pl->xd, pl->xt,
                                                        nonfinite, launch_id);
   CIEG_CUDA(cudaGetLastError());
+  static const char* trace_path = std::getenv("CIEG_SLICED_TRACE");
+  long long* trace = nullptr;
+  if (trace_path) {
+    CIEG_CUDA(cudaMalloc(&trace, sizeof(long long) * 256 * 16));
+    CIEG_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 256 * 16, ctx->stream));
+  }
   SlicedArgs args{pl->items, pl->cta_off, pl->rec, pl->xd, pl->xt, pl->rowexp, pl->diag, x, y, partial,
-                  ldx, ldy, mc, m->row_lo};
+                  ldx, ldy, mc, m->row_lo, pl->zeros, trace, 0};
+  static const int ablate = [] {
+    const char* e = std::getenv("CIEG_SLICED_ABLATE");
+    return e ? std::atoi(e) : 0;
+  }();
+  args.ablate = ablate;
   constexpr std::size_t smem = sizeof(Smem) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   CIEG_CUDA(cudaFuncSetAttribute(spmm_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   spmm_sliced_kernel<<<m->sp_ctas, kThreads, smem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
+  if (trace) {  // debug: dump CTA 0's timeline
+    std::vector<long long> h(256 * 16);
+    CIEG_CUDA(cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(trace);
+    if (FILE* f = std::fopen(trace_path, "wb")) {
+      std::fwrite(h.data(), sizeof(long long), h.size(), f);
+      std::fclose(f);
+    }
+  }
   ctx->launches += 2;
 }
 

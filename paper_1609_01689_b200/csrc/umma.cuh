@@ -51,6 +51,24 @@ __device__ __forceinline__ void mma_i8(std::uint32_t d_tmem, std::uint64_t a, st
       : "memory");
 }
 
+// The same issued by one elected lane of a converged warp: every lane runs
+// the issue loop with warp-uniform descriptors (kept in uniform registers, no
+// per-MMA waterfall), one lane executes the MMA.
+__device__ __forceinline__ void mma_i8_warp(std::uint32_t d_tmem, std::uint64_t a, std::uint64_t b, std::uint32_t idesc,
+                                            std::uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, q;\n setp.ne.b32 p, %4, 0;\n elect.sync _|q, 0xffffffff;\n"
+      " @q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a), "l"(b), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_warp(std::uint64_t* mbar) {
+  asm volatile(
+      "{\n .reg .pred q;\n elect.sync _|q, 0xffffffff;\n"
+      " @q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(smem_u32(mbar))
+      : "memory");
+}
+
 // Arrive on an mbarrier once every MMA issued so far by this thread completes.
 __device__ __forceinline__ void commit(std::uint64_t* mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(mbar))
@@ -85,6 +103,16 @@ __device__ __forceinline__ void ld16(std::uint32_t taddr, std::int32_t (&v)[16])
 }
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// 16 consecutive 32-bit TMEM columns of this warp's 32 lanes <- 0
+__device__ __forceinline__ void st16_zero(std::uint32_t taddr) {
+  const std::uint32_t z = 0;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+      "r"(z)
+      : "memory");
+}
+__device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 
 // ---- mbarriers and bulk (TMA-engine) copies ---------------------------------
 __device__ __forceinline__ void mbar_init(std::uint64_t* b, unsigned count) {
@@ -107,6 +135,22 @@ __device__ __forceinline__ void mbar_wait(std::uint64_t* b, unsigned parity) {
         : "r"(a), "r"(parity)
         : "memory");
   } while (!ok);
+}
+// the same, backing off with nanosleep between polls: for warps that wait
+// long (epilogue, producers), so their polling does not compete with the
+// tensor core's shared-memory operand reads
+__device__ __forceinline__ void mbar_wait_sleep(std::uint64_t* b, unsigned parity, unsigned ns = 128) {
+  const std::uint32_t a = smem_u32(b);
+  std::uint32_t ok = 0;
+  for (;;) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
 }
 // global -> shared bulk copy (bytes % 16 == 0, both ends 16-byte aligned),
 // completing `bytes` transactions on the mbarrier

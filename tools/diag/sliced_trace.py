@@ -1,0 +1,31 @@
+"""Timeline of CTA 0 of the sliced K1 on config 2 (CIEG_SLICED_TRACE)."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+path = "/tmp/sliced_trace.bin"
+os.environ["CIEG_SLICED_TRACE"] = path
+import numpy as np
+import torch
+from paper_1609_01689_b200 import ci, configs
+dev = ci.Device.default()
+dev.set_spmm_mode("sliced")
+dm = configs.CFG2.generate_device()
+x = torch.from_numpy(ci.random_block(dm.dim, 16, 5)).cuda()
+y = torch.empty_like(x)
+for _ in range(3):
+    dm.spmm_ptr(x.data_ptr(), y.data_ptr(), 16)
+dev.synchronize()
+t = np.fromfile(path, dtype=np.int64).reshape(256, 16)
+n = int((t[:, 0] != 0).sum())
+t = t[:n]
+t0 = t[0, 0]
+names = {0: "M.start", 1: "M.fullA", 2: "M.accE", 3: "M.issued", 8: "P.start", 4: "P.emptyA", 5: "P.zeroed",
+         6: "P.scattered", 7: "P.arrived", 9: "R.top", 10: "R.acc", 11: "R.accF", 12: "R.recomb", 13: "R.done", 14: "T.accF", 15: "T.done"}
+print("items traced", n)
+print("item " + " ".join(f"{names[k]:>10s}" for k in sorted(names)))
+for i in range(min(n, 40)):
+    print(f"{i:4d} " + " ".join(f"{(t[i, k] - t0) if t[i, k] else -1:10d}" for k in sorted(names)))
+d = np.diff(t[:, 0])
+print("per item (cycles): M.start diff median", np.median(d))
+for a_, b_, lab in ((8, 4, "P wait emptyA"), (4, 5, "P zero+bar"), (5, 6, "P scatter"), (0, 1, "M wait fullA"),
+                    (1, 2, "M wait accE"), (2, 3, "M issue"), (11, 12, "R recombine"), (12, 13, "R rest"), (13, 10, "R yacc"), (9, 11, "R wait")):
+    print(f"{lab:16s} median {np.median(t[2:, b_] - t[2:, a_]):8.0f}")
