@@ -34,6 +34,17 @@ sys.path.insert(0, REPO)
 FP64_PEAK_TFLOPS = 37.0  # measured: tools/microbench/fp64_probe.cu (DFMA and DMMA both 37.0 TF/s)
 
 
+def _bf16_peak():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0
+
+
+BF16_PEAK_TFLOPS = _bf16_peak()
+
+
 def load_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -54,17 +65,20 @@ def load_traffic(workload):
         return None
 
 
-def roofline(gbs, tflops, hbm_peak, hbm_kind, nbytes, flops, workload, issued_flops=None, ms=None):
+def roofline(gbs, tflops, hbm_peak, hbm_kind, nbytes, flops, workload, issued_flops=None, ms=None, kernel=None,
+             int8_ops=None):
     """the roof is min(HBM, FP64). The bound is whichever
     the algorithmic intensity F/B selects against the ridge
     FP64_peak / HBM_peak (5.7 flop/B): cfg2 at m = 16 (7.4 flop/B) is
     FP64-bound, m <= 8 HBM-bound. Both fractions are reported."""
     ridge = FP64_PEAK_TFLOPS * 1e12 / (hbm_peak * 1e9)
     ai = flops / nbytes
-    r = {"traffic": load_traffic(workload), "bytes_per_launch": nbytes, "flops_per_launch": flops,
+    r = {"traffic": load_traffic(workload), "traffic_source": "profiles/traffic.json: ncu dram__bytes_read.sum + "
+         "dram__bytes_write.sum summed over the kernels of one SpMM call (committed capture, not this run)",
+         "bytes_per_launch": nbytes, "flops_per_launch": flops,
          "flop_per_byte": round(ai, 3), "ridge_flop_per_byte": round(ridge, 3),
          "hbm_achieved_gbs": round(gbs, 2), "hbm_peak_gbs": hbm_peak, "hbm_peak_kind": hbm_kind,
-         "hbm_frac": round(gbs / hbm_peak, 4),
+         "hbm_frac": round(gbs / hbm_peak, 4), "hbm_frac_nominal": round(gbs / 8000.0, 4),
          "fp64_achieved_tflops": round(tflops, 3), "fp64_peak_tflops": FP64_PEAK_TFLOPS,
          "fp64_peak_kind": "measured (tools/microbench/fp64_probe.cu: DFMA = DMMA m8n8k4 = 37.0 TF/s)",
          "fp64_frac": round(tflops / FP64_PEAK_TFLOPS, 4)}
@@ -74,6 +88,18 @@ def roofline(gbs, tflops, hbm_peak, hbm_kind, nbytes, flops, workload, issued_fl
         it = issued_flops / (ms * 1e-3) / 1e12
         r.update({"fp64_issued_flops_per_launch": int(issued_flops), "fp64_issued_tflops": round(it, 3),
                   "fp64_issued_frac": round(it / FP64_PEAK_TFLOPS, 4)})
+    if kernel == "sliced":
+        # the int8 tensor-core K1: no FP64 pipe in the product; the bound is
+        # HBM (its int8 tensor work is reported beside it)
+        r.update({"bound": "hbm", "achieved": r["hbm_achieved_gbs"], "peak": hbm_peak, "unit": "GB/s",
+                  "frac": r["hbm_frac"], "peak_kind": hbm_kind, "kernel": "sliced (int8 tcgen05, Ozaki slices)"})
+        if int8_ops and ms:
+            t = int8_ops / (ms * 1e-3) / 1e12
+            r.update({"int8_tensor_ops_per_launch": int(int8_ops), "int8_tensor_tops": round(t, 1),
+                      "int8_tensor_peak_tops": round(2 * BF16_PEAK_TFLOPS, 1),
+                      "int8_tensor_peak_kind": "2x MEASURED_PEAKS bf16 (dense int8 = 2x bf16 rate)",
+                      "int8_tensor_frac": round(t / (2 * BF16_PEAK_TFLOPS), 4)})
+        return r
     if ai >= ridge:
         r.update({"bound": "tensor", "achieved": r["fp64_achieved_tflops"], "peak": FP64_PEAK_TFLOPS,
                   "unit": "TFLOP/s", "frac": r["fp64_frac"], "peak_kind": r["fp64_peak_kind"]})
@@ -752,6 +778,7 @@ def ours(args):
     barrier()
     launches = dev.launches - l0
     ms = ev0.elapsed_time(ev1) / args.steps
+    kernel = dm.spmm_kernel(m) if world == 1 else "owner-computes shards"
     if world > 1:
         import torch.distributed as dist
 
@@ -884,7 +911,12 @@ def ours(args):
     # owner-computes at m = 16: 2 items per off-diagonal tile + 1 per diagonal
     # tile (one per panel), each a dense tile x (TD x 16) slab product
     issued = ((2 * ntiles - npanels) * tile_edge * tile_edge * 8 * ((m + 7) // 8) * 2
-              if world == 1 and m > 8 else None)
+              if world == 1 and m > 8 and kernel == "owner-computes" else None)
+    # sliced: per stored tile and orientation, sum_s 128 x N_s x 128 int8 MACs,
+    # N_s = 16 min(7, 8 - s) over the H slices s = 0..4 (sum 464); diagonal
+    # tiles one orientation; 2 ops per MAC
+    int8_ops = (2 * 128 * 464 * 128 * (2 * (ntiles - npanels) + npanels)
+                if world == 1 and kernel == "sliced" else None)
     if rank != 0:
         if world > 1:
             import torch.distributed as dist
@@ -901,7 +933,8 @@ def ours(args):
         "setup": {"device_tile_edge": tile_edge, "device_tiles": ntiles, "exchange": exchange,
                   "gen_s": round(t_gen, 1), "upload_s": round(t_up, 1)},
         "roofline": roofline(gbs, flops / (ms * 1e-3) / 1e12, peak, peak_kind, nbytes, flops, cfg.name,
-                             issued_flops=issued, ms=ms),
+                             issued_flops=issued, ms=ms, kernel=kernel, int8_ops=int8_ops),
+        "spmm_kernel": kernel,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

@@ -423,15 +423,13 @@ cieg_prec* precond_from_matrix(cieg_ctx* ctx, const cieg_mat* m) {
     for (std::uint32_t g = 0; g < lng; ++g) pr->max_group = std::max(pr->max_group, lb[g + 1] - lb[g]);
     pr->bounds = dev_upload(lb);
     pr->block_off = dev_upload(off);
-    // storage: fp64 (fastest FOM reads) unless the blocks would take more
-    // than a quarter of the free HBM, then fp32 for an fp32 H (exact: the
-    // values are fp32); the preconditioner's results are identical either way
+    // storage: an fp32 H's blocks are stored in fp32 -- exact (the values
+    // are fp32) and half the bytes the FOM products stream at every Krylov
+    // step; CIEG_PREC_STORAGE=fp64 keeps fp64 blocks (results identical)
     bool f32 = false;
     if (m->precision == 0) {
-      std::size_t free_b = 0, total_b = 0;
-      CIEG_CUDA(cudaMemGetInfo(&free_b, &total_b));
-      f32 = sizeof(double) * off[lng] > free_b / 4;
-      if (const char* e = std::getenv("CIEG_PREC_STORAGE")) f32 = std::string(e) == "fp32";
+      f32 = true;
+      if (const char* e = std::getenv("CIEG_PREC_STORAGE")) f32 = std::string(e) != "fp64";
     }
     const std::size_t vb = f32 ? sizeof(float) : sizeof(double);
     void* blocks = nullptr;
