@@ -707,12 +707,10 @@ def ours(args):
         row_bounds = [0, cfg.n]
     else:
         # row-block shards generated on each GPU (strong scaling of the same matrix)
-        gb = group_bounds(cfg)
-        row_bounds = [0]
-        for k in range(1, world):
-            target = cfg.n * k // world
-            row_bounds.append(min(gb, key=lambda g: abs(g - target)))
-        row_bounds.append(cfg.n)
+        from paper_1609_01689_b200 import dist as D
+
+        # panel-aligned cuts balanced by streamed entries (the documented sharding)
+        row_bounds = [int(v) for v in D.generated_row_bounds(cfg, world)]
         t_gen = 0.0
         dm = cfg.generate_device(device=dev, rows=(row_bounds[rank], row_bounds[rank + 1]))
     t_up = time.time() - t0

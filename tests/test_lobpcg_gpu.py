@@ -120,3 +120,13 @@ def test_smoke_entry():
     import __graft_entry__
 
     __graft_entry__.smoke()
+
+
+def test_trial_width_limit_is_a_config_error():
+    """trial widths above 16 (Rayleigh-Ritz bases above 48
+    columns) are not supported by the GPU solver -- a ConfigError with the
+    reason, before any work (documented in INTEGRATION.md); ci::lobpcg_solve
+    itself has no such limit."""
+    h = gen_from((2000, 4, 64, 0.1, 0.5, 11, 1, 500))
+    with pytest.raises(ci.ConfigError, match="above 16"):
+        ci.lobpcg_solve(h, ci.random_block(h.dim, 17, 1), ci.LobpcgOptions(k_want=3, tol=1e-8))
