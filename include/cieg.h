@@ -214,6 +214,17 @@ typedef struct {
   int (*reduce_partials)(void* user, const double* yhalo_dev, uint32_t m, double* y_local_dev);
 } cieg_dist_hooks;
 
+/* The same collectives inside the library, on an NCCL communicator owned by
+ * the context (libnccl.so.2 opened at run time): rank 0 creates the id,
+ * the caller distributes it (e.g. torch.distributed), every rank inits its
+ * context. cieg_lobpcg_solve_nccl then runs the sharded solve with the Gram
+ * all-reduces on the device before the single D2H, the X halo exchange and
+ * the single-pass partial reduction as grouped ncclSend/ncclRecv on the
+ * context's stream (the planner's fused mode, planner.cpp:116-122). */
+int cieg_nccl_unique_id(uint8_t* id_out /* 128 bytes */);
+int cieg_ctx_nccl_init(cieg_ctx* ctx, const uint8_t* id /* 128 bytes */, int nranks, int rank);
+int cieg_ctx_nccl_finalize(cieg_ctx* ctx);
+
 /* ---- tall-skinny block kernels (proj/include/ci/block_vectors.hpp) ----- */
 /* X^T Y (kx x ky, column major, written to out_host) -- ci::block_inner
  * (block_vectors.hpp:60, block_vectors.cpp:74-85). Partials are reduced in a
@@ -300,6 +311,10 @@ int cieg_lobpcg_solve(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host,
 int cieg_lobpcg_solve_dist(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
                            const cieg_prec* prec, const cieg_lobpcg_options* opt, const cieg_dist_hooks* hooks,
                            cieg_report** out);
+/* The sharded solve with its collectives inside the library (the context's
+ * NCCL communicator, cieg_ctx_nccl_init); same results as _dist. */
+int cieg_lobpcg_solve_nccl(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
+                           const cieg_prec* prec, const cieg_lobpcg_options* opt, cieg_report** out);
 int cieg_report_destroy(cieg_report* rep);
 /* SolveReport fields (lobpcg.hpp:34-43). */
 int cieg_report_summary(const cieg_report* rep, int* converged, int* iterations,

@@ -178,6 +178,10 @@ SIGNATURES = {
     "cieg_lanczos_solve": (_i, [_vp, _vp, _pd, C.POINTER(LanczosOptionsC), C.POINTER(_vp)]),
     "cieg_lobpcg_solve_dist": (_i, [_vp, _vp, _pd, _u32, _vp, C.POINTER(LobpcgOptionsC), C.POINTER(DistHooks),
                                     C.POINTER(_vp)]),
+    "cieg_lobpcg_solve_nccl": (_i, [_vp, _vp, _pd, _u32, _vp, C.POINTER(LobpcgOptionsC), C.POINTER(_vp)]),
+    "cieg_nccl_unique_id": (_i, [C.POINTER(C.c_uint8)]),
+    "cieg_ctx_nccl_init": (_i, [_vp, C.POINTER(C.c_uint8), _i, _i]),
+    "cieg_ctx_nccl_finalize": (_i, [_vp]),
     "cieg_shard_plan": (_i, [C.POINTER(CsbView), _pu32, _u32, _u32, _u32, _pu32, _pu32, _pu32]),
     "cieg_matrix_upload_shard": (_i, [_vp, C.POINTER(CsbView), _pu32, _u32, _u32, _u32, _u32, C.POINTER(_vp)]),
     "cieg_matrix_rows": (_i, [_vp, _pu32, _pu32, _pu32, _pu32]),

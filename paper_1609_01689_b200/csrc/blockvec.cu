@@ -495,10 +495,17 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
                                                                   static_cast<int>(ky), sym ? 1 : 0, dout);
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
+    if (nccl_active(ctx)) nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e));  // sharded: sum over ranks
     double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
     CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
     std::memcpy(out.data(), pin, sizeof(double) * e);
+  } else if (nccl_active(ctx)) {  // no local rows: still take part in the collective
+    const int e = static_cast<int>(kx * ky);
+    CIEG_CUDA(cudaMemsetAsync(dout, 0, sizeof(double) * e, ctx->stream));
+    nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e));
+    CIEG_CUDA(cudaMemcpyAsync(out.data(), dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
+    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   return out;
 }
@@ -626,6 +633,7 @@ std::vector<double> combine_gram(cieg_ctx* ctx, std::uint32_t n, const View3& in
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
   std::vector<double> res(static_cast<std::size_t>(e));
+  if (nccl_active(ctx)) nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e));  // sharded: sum over ranks
   double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
   CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
   CIEG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -148,6 +148,7 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   for (auto& b : ctx->solver_pool) b.release();
   ctx->pinned_small.release();
   ctx->pinned_stage.release();
+  cieg::destroy_nccl(ctx);
   for (auto& e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
   cudaStreamSynchronize(ctx->own_stream);

@@ -59,6 +59,7 @@ struct PinnedBuf {
 };
 
 struct SlicedPlan;  // spmm_i8.cu
+struct NcclPlane;   // nccl_plane.cu
 
 }  // namespace cieg
 
@@ -79,6 +80,8 @@ struct cieg_ctx {
   cieg::PinnedBuf pinned_small;
   cieg::PinnedBuf pinned_stage;         // pageable host X/U: chunked staging ring (capi.cu)
   cudaEvent_t stage_ev[4] = {};
+  cieg::NcclPlane* nccl = nullptr;      // communicator of a sharded solve (cieg_ctx_nccl_init)
+  bool nccl_grams = false;              // Grams all-reduced on the device inside gram()/combine_gram()
 };
 
 struct cieg_mat {
@@ -167,6 +170,16 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
 void destroy_sliced(cieg_mat* m);
 // the K1 mode launch_spmm runs for width mc (CIEG_SPMM_OWNER / SINGLE_PASS / SLICED)
 int spmm_effective_mode(cieg_ctx* ctx, cieg_mat* m, std::uint32_t mc);
+// NCCL data plane (nccl_plane.cu)
+struct NcclSolve;
+bool nccl_active(const cieg_ctx* ctx);
+void nccl_allreduce_sum(cieg_ctx* ctx, double* dev, std::size_t count);
+void destroy_nccl(cieg_ctx* ctx);
+NcclSolve* nccl_solve_begin(cieg_ctx* ctx, const cieg_mat* mat);
+void nccl_solve_end(NcclSolve* s);
+int nccl_hook_allreduce(void* user, double* host_buf, std::uint64_t count);
+int nccl_hook_gather(void* user, const double* x_local, std::uint32_t m, double* full);
+int nccl_hook_reduce_partials(void* user, const double* yhalo, std::uint32_t m, double* y_local);
 // fp64 terms of the stored entries too small to slice exactly (after sp_reduce)
 void launch_sliced_tiny_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
                             std::uint32_t ldy, std::uint32_t mc);

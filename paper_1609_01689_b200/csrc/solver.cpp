@@ -126,6 +126,7 @@ struct GramOps {
   std::uint32_t n;
   const cieg_dist_hooks* hooks;
   Mat reduce(Mat g) const {
+    if (nccl_active(ctx)) return g;  // already summed on the device (nccl_plane.cu)
     if (hooks && !g.empty() && hooks->allreduce_sum(hooks->user, g.data(), g.size()) != 0)
       fail(CIEG_ERR_ARGUMENT, "allreduce_sum hook failed");
     return g;
@@ -542,6 +543,29 @@ int cieg_lobpcg_solve_dist(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_
       cieg::Solver s(ctx, mat, prec, *opt, *rep, hooks);
       s.run(x0_host, kt, nullptr, nullptr);
     }
+    *out = rep.release();
+  });
+}
+
+int cieg_lobpcg_solve_nccl(cieg_ctx* ctx, const cieg_mat* mat, const double* x0_host, uint32_t kt,
+                           const cieg_prec* prec, const cieg_lobpcg_options* opt, cieg_report** out) {
+  return cieg::guarded([&] {
+    if (!ctx || !mat || !x0_host || !opt || !out) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_lobpcg_solve_nccl: null argument");
+    if (!ctx->nccl) cieg::fail(CIEG_ERR_CONFIG, "cieg_lobpcg_solve_nccl: no NCCL communicator (cieg_ctx_nccl_init)");
+    if (prec && prec->dim != mat->row_hi - mat->row_lo)
+      cieg::fail(CIEG_ERR_DIMENSION, "apply_preconditioner: tiles do not cover the basis");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    auto rep = std::make_unique<cieg_report>();
+    cieg::NcclSolve* ns = cieg::nccl_solve_begin(ctx, mat);
+    cieg_dist_hooks hooks{ns, cieg::nccl_hook_allreduce, cieg::nccl_hook_gather, cieg::nccl_hook_reduce_partials};
+    try {
+      cieg::Solver s(ctx, mat, prec, *opt, *rep, &hooks);
+      s.run(x0_host, kt, nullptr, nullptr);
+    } catch (...) {
+      cieg::nccl_solve_end(ns);
+      throw;
+    }
+    cieg::nccl_solve_end(ns);
     *out = rep.release();
   });
 }

@@ -437,3 +437,42 @@ def lobpcg_solve_dist(sm, x0_local: np.ndarray, options: ci.LobpcgOptions,
         lib.cieg_ctx_set_stream(dev.handle, None)
         torch.cuda.set_stream(prev_stream)
     return ci._read_report(lib, rep, sm.local_rows)
+
+
+def nccl_init(dev: "ci.Device", group=None) -> None:
+    """Give the device context its own NCCL communicator over the ranks of
+    `group` (rank 0 creates the id, torch.distributed broadcasts it): the
+    library's in-library data plane (cieg_lobpcg_solve_nccl)."""
+    lib = _lib.load()
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    uid = (C.c_uint8 * 128)()
+    if rank == 0:
+        ci._check(lib.cieg_nccl_unique_id(uid))
+    box = [bytes(uid)]
+    dist.broadcast_object_list(box, src=0, group=group)
+    uid = (C.c_uint8 * 128).from_buffer_copy(box[0])
+    ci._check(lib.cieg_ctx_nccl_init(dev.handle, uid, world, rank))
+
+
+def nccl_finalize(dev: "ci.Device") -> None:
+    ci._check(_lib.load().cieg_ctx_nccl_finalize(dev.handle))
+
+
+def lobpcg_solve_nccl(sm, x0_local: np.ndarray, options: ci.LobpcgOptions,
+                      precond: Optional[ci.TileDiagonal] = None) -> ci.SolveReport:
+    """lobpcg_solve_dist with the collectives inside the library (the
+    context's NCCL communicator, nccl_init): Gram all-reduces on the device
+    before the single D2H, the X halo exchange and the single-pass partial
+    reduction as grouped ncclSend/ncclRecv -- no Python callback in the
+    iteration. Same results as lobpcg_solve_dist."""
+    lib = _lib.load()
+    dev = sm.device
+    opt = _lib.LobpcgOptionsC()
+    opt.k_want, opt.tol, opt.max_iter = options.k_want, options.tol, options.max_iter
+    opt.precond_config = options.precond_config.c()
+    x0 = ci._f64(x0_local)
+    rep = C.c_void_p()
+    ci._check(lib.cieg_lobpcg_solve_nccl(dev.handle, sm.handle, ci._ptr(x0), x0.shape[1],
+                                         precond.handle if precond is not None else None, C.byref(opt),
+                                         C.byref(rep)))
+    return ci._read_report(lib, rep, sm.local_rows)

@@ -61,6 +61,18 @@ def _worker(rank, world, port, backend, name, out_q):
         res["counters"] = [rep.counters.spmm_calls, rep.counters.spmv_equivalents,
                            rep.counters.precond_applications, rep.counters.orthogonalizations]
         res["rows"] = rep.trial_vectors.shape[0]
+        if backend == "nccl":
+            # the same solve with the collectives inside the library (the
+            # context's own NCCL communicator, no Python hooks)
+            D.nccl_init(dev)
+            try:
+                rn = D.lobpcg_solve_nccl(sm, x0, ci.LobpcgOptions(k_want=int(k), tol=float(tol)), prec)
+            finally:
+                D.nccl_finalize(dev)
+            res["nccl_iterations"] = rn.iterations
+            res["nccl_eigenvalues"] = rn.eigenvalues.tolist()
+            res["nccl_counters"] = [rn.counters.spmm_calls, rn.counters.spmv_equivalents,
+                                    rn.counters.precond_applications, rn.counters.orthogonalizations]
     except Exception as e:  # pragma: no cover
         import traceback
 
@@ -100,6 +112,10 @@ def test_sharded_solver_matches_reference(golden, world, backend, name):
         assert res["iterations"] == int(g[f"{name}_iterations"])
         assert res["counters"] == g[f"{name}_counters"].tolist()
         np.testing.assert_allclose(res["eigenvalues"], g[f"{name}_eigenvalues"], rtol=1e-10)
+        if backend == "nccl":  # the in-library NCCL data plane
+            assert res["nccl_iterations"] == res["iterations"]
+            assert res["nccl_counters"] == res["counters"]
+            np.testing.assert_allclose(res["nccl_eigenvalues"], res["eigenvalues"], rtol=1e-13)
         rows += res["rows"]
     assert rows == int(g[f"{name}_params"][0])
     assert all(out[r]["eigenvalues"] == out[0]["eigenvalues"] for r in range(world))
