@@ -460,11 +460,13 @@ int grid_for(cieg_ctx* ctx, std::uint64_t work, int per_block) {
 
 }  // namespace
 
-std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R) {
+namespace {
+
+// Enqueue one Gram (partial kernel + fixed-order reduction) writing kx x ky
+// doubles to dout; `part` selects a private region of the partials scratch
+// so two Grams can be in flight before one D2H.
+int enqueue_gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R, double* partials, double* dout) {
   const std::uint32_t kx = L.width, ky = R.width;
-  std::vector<double> out(static_cast<std::size_t>(kx) * ky, 0.0);
-  if (kx == 0 || ky == 0) return out;
-  if (kx > 48 || ky > 48) fail(CIEG_ERR_CONFIG, "gram: block width above 48");
   const int MT = static_cast<int>((kx + 7) / 8), NT = static_cast<int>((ky + 7) / 8);
   // fixed decomposition: rows_per_warp multiple of 4, at most 4 blocks per SM
   const int max_blocks = 4 * ctx->sm_count;
@@ -472,43 +474,78 @@ std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const V
   rpw = std::max<std::uint64_t>(64, (rpw + 3) & ~3ull);
   const int blocks = static_cast<int>(std::max<std::uint64_t>(1, (n + rpw * kGramWarps - 1) / (rpw * kGramWarps)));
   const int MA = 8 * MT, NB = 8 * NT;
-  double* partials = static_cast<double*>(ctx->scratch_red.get(sizeof(double) * blocks * MA * NB + 64));
-  double* dout = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 48 * 48));
   const bool sym = same_view(L, R);  // X^T X: upper tiles only, mirrored
-  if (n > 0) {
-    if (sym) {
-      switch (MT) {
-        case 1: launch_gram_sym<1>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
-        case 2: launch_gram_sym<2>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
-        case 3: launch_gram_sym<3>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
-        case 4: launch_gram_sym<4>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
-        case 5: launch_gram_sym<5>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
-        default: launch_gram_sym<6>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
-      }
-    } else {
-      gram_launcher(MT, NT)(ctx, n, L, R, blocks, static_cast<std::uint32_t>(rpw), partials);
+  if (sym) {
+    switch (MT) {
+      case 1: launch_gram_sym<1>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+      case 2: launch_gram_sym<2>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+      case 3: launch_gram_sym<3>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+      case 4: launch_gram_sym<4>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+      case 5: launch_gram_sym<5>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
+      default: launch_gram_sym<6>(ctx, n, L, blocks, static_cast<std::uint32_t>(rpw), partials); break;
     }
-    CIEG_CUDA(cudaGetLastError());
-    ++ctx->launches;
-    const int e = static_cast<int>(kx * ky);
-    gram_reduce_kernel<<<(e + 3) / 4, 128, 0, ctx->stream>>>(partials, blocks, MA, NB, static_cast<int>(kx),
-                                                                  static_cast<int>(ky), sym ? 1 : 0, dout);
-    CIEG_CUDA(cudaGetLastError());
-    ++ctx->launches;
-    if (nccl_active(ctx)) nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e));  // sharded: sum over ranks
-    double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
-    CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
-    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
-    std::memcpy(out.data(), pin, sizeof(double) * e);
-  } else if (nccl_active(ctx)) {  // no local rows: still take part in the collective
-    const int e = static_cast<int>(kx * ky);
-    CIEG_CUDA(cudaMemsetAsync(dout, 0, sizeof(double) * e, ctx->stream));
-    nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e));
-    CIEG_CUDA(cudaMemcpyAsync(out.data(), dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
-    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  } else {
+    gram_launcher(MT, NT)(ctx, n, L, R, blocks, static_cast<std::uint32_t>(rpw), partials);
   }
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  const int e = static_cast<int>(kx * ky);
+  gram_reduce_kernel<<<(e + 3) / 4, 128, 0, ctx->stream>>>(partials, blocks, MA, NB, static_cast<int>(kx),
+                                                                static_cast<int>(ky), sym ? 1 : 0, dout);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+  return e;
+}
+
+std::size_t gram_partials_doubles(cieg_ctx* ctx, std::uint32_t n) {
+  const int max_blocks = 4 * ctx->sm_count;
+  (void)n;
+  return static_cast<std::size_t>(max_blocks) * 48 * 48 + 64;
+}
+
+}  // namespace
+
+std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R) {
+  const std::uint32_t kx = L.width, ky = R.width;
+  std::vector<double> out(static_cast<std::size_t>(kx) * ky, 0.0);
+  if (kx == 0 || ky == 0) return out;
+  if (kx > 48 || ky > 48) fail(CIEG_ERR_CONFIG, "gram: block width above 48");
+  double* partials = static_cast<double*>(ctx->scratch_red.get(sizeof(double) * gram_partials_doubles(ctx, n)));
+  double* dout = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 2 * 48 * 48));
+  const int e = static_cast<int>(kx * ky);
+  if (n > 0)
+    enqueue_gram(ctx, n, L, R, partials, dout);
+  else
+    CIEG_CUDA(cudaMemsetAsync(dout, 0, sizeof(double) * e, ctx->stream));
+  if (n == 0 && !nccl_active(ctx)) return out;
+  if (nccl_active(ctx)) nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e));  // sharded: sum over ranks
+  double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 2 * 48 * 48));
+  CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * e, cudaMemcpyDeviceToHost, ctx->stream));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::memcpy(out.data(), pin, sizeof(double) * e);
   return out;
 }
+
+// Two independent Grams with one D2H and one synchronisation.
+std::pair<std::vector<double>, std::vector<double>> gram_pair(cieg_ctx* ctx, std::uint32_t n, const View3& L1,
+                                                              const View3& R1, const View3& L2, const View3& R2) {
+  if (L1.width == 0 || R1.width == 0 || L2.width == 0 || R2.width == 0 || n == 0)
+    return {gram(ctx, n, L1, R1), gram(ctx, n, L2, R2)};
+  if (L1.width > 48 || R1.width > 48 || L2.width > 48 || R2.width > 48)
+    fail(CIEG_ERR_CONFIG, "gram: block width above 48");
+  const std::size_t pd = gram_partials_doubles(ctx, n);
+  double* partials = static_cast<double*>(ctx->scratch_red.get(sizeof(double) * 2 * pd));
+  double* dout = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * 2 * 48 * 48));
+  const int e1 = enqueue_gram(ctx, n, L1, R1, partials, dout);
+  const int e2 = enqueue_gram(ctx, n, L2, R2, partials + pd, dout + e1);
+  if (nccl_active(ctx)) nccl_allreduce_sum(ctx, dout, static_cast<std::size_t>(e1 + e2));
+  double* pin = static_cast<double*>(ctx->pinned_small.get(sizeof(double) * 2 * 48 * 48));
+  CIEG_CUDA(cudaMemcpyAsync(pin, dout, sizeof(double) * (e1 + e2), cudaMemcpyDeviceToHost, ctx->stream));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<double> a(pin, pin + e1), b(pin + e1, pin + e1 + e2);
+  return {std::move(a), std::move(b)};
+}
+
 
 namespace {
 
@@ -532,8 +569,9 @@ CombineParams& setup_combine(cieg_ctx* ctx, std::uint32_t n, const View3& in, co
     prm.g_dev = nullptr;
   } else {
     double* d = static_cast<double*>(ctx->scratch_small.get(sizeof(double) * ng));
+    // (a copy from pageable memory returns once the source is staged: no
+    // synchronisation needed before the caller reuses g_host)
     CIEG_CUDA(cudaMemcpyAsync(d, g_host, sizeof(double) * ng, cudaMemcpyHostToDevice, ctx->stream));
-    CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
     prm.g_dev = d;
   }
   return prm;

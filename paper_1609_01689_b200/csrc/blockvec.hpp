@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <vector>
 
 #include "context.hpp"
@@ -49,6 +50,9 @@ inline Out2 out2(double* p0, std::uint32_t w0, double* p1, std::uint32_t w1) {
 // L^T R (L.width x R.width), column major on the host; deterministic
 // fixed-order reduction. Synchronizes the stream.
 std::vector<double> gram(cieg_ctx* ctx, std::uint32_t n, const View3& L, const View3& R);
+// two independent Grams, one D2H + one synchronisation (same values as two gram() calls)
+std::pair<std::vector<double>, std::vector<double>> gram_pair(cieg_ctx* ctx, std::uint32_t n, const View3& L1,
+                                                              const View3& R1, const View3& L2, const View3& R2);
 
 // out = [accumulate ? out : 0] + in * G, G (in.width x kout) column major on
 // the host. Row-local: out may alias in when the widths match.

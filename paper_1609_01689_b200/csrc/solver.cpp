@@ -132,6 +132,11 @@ struct GramOps {
     return g;
   }
   Mat gram(const View3& l, const View3& r) const { return reduce(cieg::gram(ctx, n, l, r)); }
+  // two independent Grams, one host round trip
+  std::pair<Mat, Mat> gram_pair(const View3& l1, const View3& r1, const View3& l2, const View3& r2) const {
+    auto g = cieg::gram_pair(ctx, n, l1, r1, l2, r2);
+    return {reduce(std::move(g.first)), reduce(std::move(g.second))};
+  }
   // out = [out] + in G, returning L^T out (or out^T out for L == nullptr)
   Mat combine_gram(const View3& in, const double* g, std::uint32_t kout, const Out2& out, bool acc,
                    const View3* L) const {
@@ -149,12 +154,16 @@ void orthonormalize_dev(const GramOps& ops, Block& v, Block& tmp, double drop_to
   cieg_ctx* ctx = ops.ctx;
   const std::uint32_t n = ops.n;
   const int k = static_cast<int>(v.w);
-  Mat g0 = ops.gram(view({sg(v)}), view({sg(v)}));
+  const bool proj = against && against->width > 0;
+  Mat g0, c;
+  if (proj)  // V^T V and A^T V are independent: one host round trip
+    std::tie(g0, c) = ops.gram_pair(view({sg(v)}), view({sg(v)}), *against, view({sg(v)}));
+  else
+    g0 = ops.gram(view({sg(v)}), view({sg(v)}));
   std::vector<double> orig_sq(k);
   for (int j = 0; j < k; ++j) orig_sq[j] = g0[j + static_cast<std::size_t>(j) * k];
   Mat gram_v = g0;  // without a projection the Gram is unchanged
-  if (against && against->width > 0) {
-    Mat c = ops.gram(*against, view({sg(v)}));
+  if (proj) {
     for (double& e : c) e = -e;
     Mat c2 = ops.combine_gram(*against, c.data(), v.w, out1(v.p, v.w), true, against);  // pass 1 + pass-2 Gram
     for (double& e : c2) e = -e;
@@ -422,10 +431,11 @@ void Solver::run(const double* x0_host, std::uint32_t kt0, cieg_observer_fn obs,
       View3 hy = view({sg(hx_), sg(hw_), sg(hp_)});
       bool rescued = false;
       try {
-        Mat overlap = gram(y, y);
+        // the overlap check and Y^T HY are independent: one host round trip
+        auto [overlap, yhy] = ops_.gram_pair(y, y, y, hy);
         const double dev = dev_from_identity(overlap, static_cast<int>(y.width));
         if (dev > 1e-8) fail(CIEG_ERR_INDEFINITE, "basis drift " + std::to_string(dev));
-        eig_sym(gram(y, hy), static_cast<int>(y.width), evals, evecs);
+        eig_sym(yhy, static_cast<int>(y.width), evals, evecs);
       } catch (const Failure& f) {
         if (f.status != CIEG_ERR_INDEFINITE) throw;
         rescued = true;
