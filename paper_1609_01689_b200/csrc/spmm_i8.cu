@@ -76,8 +76,6 @@ constexpr int kPlanes = kAS * kPlane;      // 81920
 constexpr int kSlab = kNB * kTD;           // 14336: X digits of one panel
 constexpr int kSlabBytes = kSlab + 64;     // + 16 int32 exponents
 constexpr int kStageCols = 2 * kND;        // TMEM columns per accumulator stage (row + transposed)
-constexpr int kThreads = 512;
-constexpr int kProducers = 7 * 32;         // warps 1..7
 constexpr std::uint16_t kNoEntry = 0xffff;
 
 struct OzItem {
@@ -87,33 +85,36 @@ struct OzItem {
   std::uint32_t owner, partner;  // panel indices
   std::uint32_t r0;     // owner start row
   std::uint32_t orow;   // partner rows
+  std::uint32_t slot;   // the item's index in the single-pass schedule (its partial slot)
+  std::uint32_t pad;
 };
-static_assert(sizeof(OzItem) == 32, "item descriptor");
+static_assert(sizeof(OzItem) == 40, "item descriptor");
 
 struct SlicedPlan {
   OzItem* items = nullptr;
   std::uint32_t* cta_off = nullptr;
   uint2* rec = nullptr;
+  std::uint8_t* dense = nullptr;  // dense mode: every item's five slice planes (kPlanes bytes), TMA-loaded
   int* rowexp = nullptr;
   float* diag = nullptr;  // stored diagonal of H (applied in fp64, not sliced)
   std::uint8_t* xd = nullptr;                 // per-call digit slabs, npanels * kSlabBytes
   std::uint8_t* xt = nullptr;
-  std::uint8_t* zeros = nullptr;  // kPlanes bytes of 0
   // tiny entries (not exactly sliceable) as CSR over output rows, fp64
   std::uint32_t ntiny_rows = 0;
   std::uint32_t *tiny_rows = nullptr, *tiny_off = nullptr, *tiny_in = nullptr;
   double* tiny_val = nullptr;
   std::uint64_t nrec = 0;
-  bool finite = true;  // every stored value finite (else the DMMA kernels run)
+  std::uint32_t ctas = 0;
+  bool usable = true;  // every stored value finite and the planes fit (else the DMMA kernels run)
   ~SlicedPlan() {
     cudaFree(items);
     cudaFree(cta_off);
     cudaFree(rec);
+    cudaFree(dense);
     cudaFree(rowexp);
     cudaFree(diag);
     cudaFree(xd);
     cudaFree(xt);
-    cudaFree(zeros);
     cudaFree(tiny_rows);
     cudaFree(tiny_off);
     cudaFree(tiny_in);
@@ -272,6 +273,28 @@ __global__ void records_kernel(const OzItem* items, const std::uint32_t* sp_sche
     rec[it.rec0 + interleave(k)] = make_uint2(kNoEntry, 0);  // (nrec is a multiple of 64)
 }
 
+// Dense mode: every item's records scattered once into its five slice planes
+// in HBM (kPlanes bytes per item, zeros included), so the SpMM streams them
+// with bulk copies instead of scattering records every call.
+__global__ void dense_kernel(const OzItem* items, const uint2* rec, std::uint8_t* dense) {
+  const std::uint32_t i = blockIdx.x;
+  const OzItem it = items[i];
+  std::uint8_t* d = dense + static_cast<std::size_t>(i) * kPlanes;
+  uint4* d4 = reinterpret_cast<uint4*>(d);
+  for (int u = threadIdx.x; u < kPlanes / 16; u += blockDim.x) d4[u] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  for (std::uint32_t k = threadIdx.x; k < it.nrec; k += blockDim.x) {
+    const uint2 r = rec[it.rec0 + k];
+    const std::uint32_t pos = r.x & 0xffffu;
+    if (pos >= static_cast<std::uint32_t>(kPlane)) continue;
+    d[pos] = static_cast<std::uint8_t>(r.x >> 16);
+    d[pos + kPlane] = static_cast<std::uint8_t>(r.x >> 24);
+    d[pos + 2 * kPlane] = static_cast<std::uint8_t>(r.y);
+    d[pos + 3 * kPlane] = static_cast<std::uint8_t>(r.y >> 8);
+    d[pos + 4 * kPlane] = static_cast<std::uint8_t>(r.y >> 16);
+  }
+}
+
 // ----------------------------------------------------------------- per call
 
 // x = M 2^q with M a 53-bit integer (exact decomposition of a finite double)
@@ -396,7 +419,7 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
 struct SlicedArgs {
   const OzItem* items;
   const std::uint32_t* cta_off;
-  const uint2* rec;
+  const std::uint8_t* dense;  // every item's five slice planes (kPlanes bytes)
   const std::uint8_t* xd;
   const std::uint8_t* xt;
   const int* rowexp;
@@ -405,74 +428,53 @@ struct SlicedArgs {
   double* y;
   double* partial;
   std::uint32_t ldx, ldy, mc, row_base;
-  const std::uint8_t* zeros;  // kPlanes zero bytes (the slice buffers are cleared by a bulk copy)
   long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
-  int ablate;        // timing-only (CIEG_SLICED_ABLATE=1): no clear/scatter -- results invalid
 };
 
-// (slabs hold the digits only -- the exponents are read from global memory --
-// so every operand starts on a 1024-byte boundary: whole 128-byte core matrices)
+// (slabs hold the digits only -- every operand starts on a 1024-byte
+// boundary: whole 128-byte core matrices; the column exponents are staged
+// separately)
 struct Smem {
   std::uint8_t planes[2][kPlanes];
   std::uint8_t xd[2][kSlab];
   std::uint8_t xt[2][kSlab];
-  std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2], zeroed[2];
+  // the slabs' column exponents, staged with them (4 deep: an epilogue reads
+  // an item's exponents before it releases the item's accumulator stage)
+  int xd_exp[4][16];
+  int xt_exp[4][16];
+  std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2];
   std::uint32_t tmem;
 };
 
-constexpr int kBatch = 8;  // 16-byte record pairs per producer thread per batch
-
-__device__ __forceinline__ void load_batch(const uint2* rec, const OzItem& it, std::uint32_t q0, int pt,
-                                           uint4 (&v)[kBatch]) {
-  const uint4* src = reinterpret_cast<const uint4*>(rec + it.rec0);
-  const std::uint32_t nq = it.nrec >> 1;
-#pragma unroll
-  for (int u = 0; u < kBatch; ++u) {
-    const std::uint32_t q = q0 + pt + u * kProducers;
-    v[u] = q < nq ? __ldg(src + q) : make_uint4(kNoEntry, 0, kNoEntry, 0);
-  }
+// exact int64 -> double for |v| < 2^51 (the 2^52 + 2^51 bias; no conversion unit)
+__device__ __forceinline__ double l2d(long long v) {
+  return __longlong_as_double(v + 0x4338000000000000ll) - 6755399441055744.0;
 }
 
-__device__ __forceinline__ void scatter(std::uint8_t* pl, std::uint32_t x, std::uint32_t y) {
-  const std::uint32_t pos = x & 0xffffu;
-  if (pos >= static_cast<std::uint32_t>(kPlane)) return;
-  pl[pos] = static_cast<std::uint8_t>(x >> 16);
-  pl[pos + kPlane] = static_cast<std::uint8_t>(x >> 24);
-  pl[pos + 2 * kPlane] = static_cast<std::uint8_t>(y);
-  pl[pos + 3 * kPlane] = static_cast<std::uint8_t>(y >> 8);
-  pl[pos + 4 * kPlane] = static_cast<std::uint8_t>(y >> 16);
-}
-
-// sum_d D_d 2^(-8 d) over the kXD diagonal blocks at TMEM column col0 of this
-// warp's 32 lanes (Horner from the lowest diagonal; fp64, one rounding per step)
-__device__ __forceinline__ void recombine(std::uint32_t taddr, double (&v)[16]) {
-  std::int32_t hi[16], lo[16];
+// sum_d D_d 2^(24 - 8 d) over the kDiag diagonal blocks at TMEM address taddr
+// (8 columns of this warp's 32 lanes): the diagonals are combined exactly in
+// int64 in two groups of four (|D_d| < 2^24, so each group is below 2^49) and
+// the two groups are joined in fp64 with a single rounding.
+__device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8]) {
+  static_assert(kDiag == 8, "two groups of four diagonals");
+  std::int32_t d0[8], d1[8], d2[8], d3[8];
+  long long hi[8];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = 0.0;
-  static_assert(kDiag % 2 == 0, "pairs of diagonals");
-#pragma unroll 1
-  for (int d = kDiag - 1; d >= 1; d -= 2) {  // rolled: a small instruction footprint
-    umma::ld16(taddr + 16 * d, hi);
-    umma::ld16(taddr + 16 * (d - 1), lo);
+  for (int g = 0; g < 2; ++g) {
+    umma::ld8(taddr + 16 * (4 * g), d0);
+    umma::ld8(taddr + 16 * (4 * g + 1), d1);
+    umma::ld8(taddr + 16 * (4 * g + 2), d2);
+    umma::ld8(taddr + 16 * (4 * g + 3), d3);
     umma::ld_wait();
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      v[j] = fma(v[j], 0x1p-8, i2d(hi[j]));
-      v[j] = fma(v[j], 0x1p-8, i2d(lo[j]));
+    for (int j = 0; j < 8; ++j) {
+      const long long w = static_cast<long long>(d3[j]) + (static_cast<long long>(d2[j]) << 8) +
+                          (static_cast<long long>(d1[j]) << 16) + (static_cast<long long>(d0[j]) << 24);
+      if (g == 0)
+        hi[j] = w;
+      else
+        v[j] = fma(l2d(w), 0x1p-32, l2d(hi[j]));
     }
-  }
-}
-
-// the 16 column exponents stored after a panel's digit slab
-__device__ __forceinline__ void load_exps(const std::uint8_t* slabs, std::uint32_t panel, int (&ex)[16]) {
-  const int4* p = reinterpret_cast<const int4*>(slabs + static_cast<std::size_t>(panel) * kSlabBytes + kSlab);
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int4 e4 = __ldg(p + j);
-    ex[4 * j] = e4.x;
-    ex[4 * j + 1] = e4.y;
-    ex[4 * j + 2] = e4.z;
-    ex[4 * j + 3] = e4.w;
   }
 }
 
@@ -482,6 +484,13 @@ __device__ __forceinline__ void load_exps(const std::uint8_t* slabs, std::uint32
       a.trace[((item) - i_beg) * 16 + (slot)] = clock64();                                           \
   } while (0)
 
+// CTA: 18 warps (one per SM). Warp 0 issues the MMAs, warp 1 the bulk copies;
+// warps 2..17 are the epilogue, four per TMEM lane quarter (warp & 3):
+// row part columns 0-7 / 8-15, transposed part columns 0-7 / 8-15.
+constexpr int kWarps = 18;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kEpiWarps = 16;
+
 __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
@@ -489,13 +498,12 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
   const std::uint32_t i_beg = a.cta_off[blockIdx.x], i_end = a.cta_off[blockIdx.x + 1];
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      umma::mbar_init(&S.full_a[b], kProducers + 1);
+      umma::mbar_init(&S.full_a[b], 1);
       umma::mbar_init(&S.empty_a[b], 1);
       umma::mbar_init(&S.full_t[b], 1);
       umma::mbar_init(&S.empty_t[b], 1);
       umma::mbar_init(&S.acc_full[b], 1);
-      umma::mbar_init(&S.acc_empty[b], 8);
-      umma::mbar_init(&S.zeroed[b], 1);
+      umma::mbar_init(&S.acc_empty[b], kEpiWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -503,26 +511,19 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
   umma::fence_before();
   __syncthreads();
   // Diagonal kDiag - 1 is first written by slice 1 (slice 0's MMA covers
-  // d < kXD only), so it accumulates onto TMEM that must start at zero: the
-  // epilogue warps clear those 16 columns of both stages here and again
-  // after reading each stage.
-  if (warp >= 8) {
+  // d < kXD only), so it accumulates onto TMEM that must start at zero: each
+  // epilogue warp clears its 8 columns of it in both stages here and again
+  // after reading a stage.
+  const int eq = warp & 3, role = (warp - 2) >> 2, orient = role >> 1, half = role & 1;
+  const std::uint32_t ecol = (static_cast<std::uint32_t>(32 * eq) << 16) + orient * kND + 8 * half;
+  if (warp >= 2) {
     umma::fence_after();
-    const std::uint32_t base = S.tmem + (static_cast<std::uint32_t>(32 * (warp & 3)) << 16) + (warp < 12 ? 0 : kND);
-    umma::st16_zero(base + 16 * (kDiag - 1));
-    umma::st16_zero(base + kStageCols + 16 * (kDiag - 1));
+    umma::st8_zero(S.tmem + ecol + 16 * (kDiag - 1));
+    umma::st8_zero(S.tmem + ecol + kStageCols + 16 * (kDiag - 1));
     umma::st_wait();
     umma::fence_before();
   }
   __syncthreads();
-  // The slice buffers are cleared by bulk copies from a zero page: here for
-  // the first two items, then by the row epilogue the moment the MMAs of the
-  // item that used a buffer complete (acc_full), two items ahead.
-  if (tid == 0 && !a.ablate)
-    for (std::uint32_t j = 0; j < 2 && i_beg + j < i_end; ++j) {
-      umma::mbar_arrive_tx(&S.zeroed[j], kPlanes);
-      umma::bulk_g2s(S.planes[j], a.zeros, kPlanes, &S.zeroed[j]);
-    }
   umma::fence_after();
   const std::uint32_t tbase = S.tmem;
 
@@ -530,9 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     // ------------------------------------------------------------ MMA issue
     // The whole warp runs the issue loop converged, descriptors are
     // warp-uniform (base descriptor + constant offsets, in uniform
-    // registers), one elected lane executes each tcgen05.mma: the tensor core
-    // needs a new MMA every ~50 cycles, which a per-MMA divergent issue path
-    // (R2UR + waterfall per instruction) cannot sustain.
+    // registers), one elected lane executes each tcgen05.mma.
     std::uint32_t k = 0, owners = 0;
     int o = 0;
     const std::uint64_t a_k0 = umma::sdesc(umma::smem_u32(S.planes[0]), 128, 1024);   // A K-major (H X)
@@ -577,166 +576,131 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       umma::commit_warp(&S.acc_full[b]);
       if ((it.flags >> 9) & 1u) umma::commit_warp(&S.empty_t[o]);
       TRACE(i, 3, lane == 0);
-
     }
-  } else if (warp < 8) {
-    // ------------------------------------------------------------ producers
-    // Records stream in batches of kBatch 16-byte pairs per thread, one batch
-    // in flight while the previous one is scattered; the first batch of the
-    // next item is loaded before this item's buffer wait and clear.
-    const int pt = tid - 32;
-    std::uint32_t k = 0, owners = 0;
-    constexpr std::uint32_t kStep = kBatch * kProducers;
-    uint4 cur[kBatch], nxt[kBatch];
-    OzItem it = a.items[i_beg < i_end ? i_beg : 0];
-    if (i_beg < i_end) load_batch(a.rec, it, 0, pt, cur);
-    for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-      const int b = k & 1;
-      TRACE(i, 8, pt == 0);
-      const OzItem nit = i + 1 < i_end ? a.items[i + 1] : it;
-      if ((it.flags >> 8) & 1u) {
-        const int o = owners & 1;
-        if (pt == 0) {
+  } else if (warp == 1) {
+    // ------------------------------------------------------ bulk-copy issue
+    // One lane streams each item's five slice planes (built once per matrix;
+    // evict-first, so the X digit slabs of the sector band stay in L2) and
+    // the partner's X digit slab into a free buffer; the owner's slab when a
+    // new owner panel starts.
+    if (lane == 0) {
+      std::uint32_t k = 0, owners = 0;
+      const std::uint64_t stream = umma::createpolicy_evict_first();
+      for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
+        const OzItem it = a.items[i];
+        const int b = k & 1;
+        TRACE(i, 8, true);
+        if ((it.flags >> 8) & 1u) {
+          const int o = owners & 1;
           umma::mbar_wait(&S.empty_t[o], ((owners >> 1) & 1u) ^ 1u);
-          umma::mbar_arrive_tx(&S.full_t[o], kSlab);
-          umma::bulk_g2s(S.xt[o], a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes, kSlab, &S.full_t[o]);
+          umma::mbar_arrive_tx(&S.full_t[o], kSlab + 64);
+          const std::uint8_t* src = a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes;
+          umma::bulk_g2s(S.xt[o], src, kSlab, &S.full_t[o]);
+          umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t[o]);
+          ++owners;
         }
-        ++owners;
+        umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
+        TRACE(i, 4, true);
+        umma::mbar_arrive_tx(&S.full_a[b], kSlab + 64 + kPlanes);
+        const std::uint8_t* xsrc = a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes;
+        umma::bulk_g2s(S.xd[b], xsrc, kSlab, &S.full_a[b]);
+        umma::bulk_g2s(S.xd_exp[k & 3], xsrc + kSlab, 64, &S.full_a[b]);
+        const std::uint8_t* src = a.dense + static_cast<std::size_t>(i) * kPlanes;
+#pragma unroll 1
+        for (int s = 0; s < kAS; ++s)
+          umma::bulk_g2s_hint(S.planes[b] + s * kPlane, src + s * kPlane, kPlane, &S.full_a[b], stream);
+        TRACE(i, 7, true);
       }
-      umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
-      TRACE(i, 4, pt == 0);
-      if (pt == 0) {
-        umma::mbar_arrive_tx(&S.full_a[b], kSlab);
-        umma::bulk_g2s(S.xd[b], a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes, kSlab, &S.full_a[b]);
-        if (i + 1 < i_end) {  // next item's records into L2 while this one is placed
-          const std::uint8_t* p = reinterpret_cast<const std::uint8_t*>(a.rec + nit.rec0);
-          for (std::uint32_t off = 0; off < 8u * nit.nrec; off += 1u << 16)
-            umma::prefetch_l2(p + off, min(1u << 16, 8u * nit.nrec - off));
-        }
-      }
-      if (!a.ablate) umma::mbar_wait(&S.zeroed[b], (k >> 1) & 1u);
-      TRACE(i, 5, pt == 0);
-      std::uint8_t* pl = S.planes[b];
-      const std::uint32_t nq = it.nrec >> 1;
-      for (std::uint32_t q0 = 0; q0 < nq; q0 += kStep) {
-        if (q0 + kStep < nq)
-          load_batch(a.rec, it, q0 + kStep, pt, nxt);
-        else if (i + 1 < i_end)
-          load_batch(a.rec, nit, 0, pt, nxt);
-        if (!a.ablate) {
-#pragma unroll
-          for (int u = 0; u < kBatch; ++u) {
-            scatter(pl, cur[u].x, cur[u].y);
-            scatter(pl, cur[u].z, cur[u].w);
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) cur[u] = nxt[u];
-      }
-      TRACE(i, 6, pt == 0);
-      umma::fence_async_smem();
-      umma::mbar_arrive(&S.full_a[b]);
-      TRACE(i, 7, pt == 0);
-      it = nit;
     }
-  } else if (warp < 12) {
+  } else if (orient == 0) {
     // ------------------------------------------------- row-part epilogue
-    // The next item's descriptor and column exponents are loaded one item
-    // ahead (global latency overlaps this item's wait and math).
-    const int q = warp - 8, r = 32 * q + lane;
-    const std::uint32_t lanes = static_cast<std::uint32_t>(32 * q) << 16;
-    double yacc[16];
+    // (TMEM lanes = tile rows; 8 of the 16 columns per warp)
+    const int r = 32 * eq + lane, j0 = 8 * half;
+    double yacc[8];
     int er = 0;
     std::uint32_t k = 0;
-    OzItem it = a.items[i_beg < i_end ? i_beg : 0];
-    int ex[16];
-    if (i_beg < i_end) load_exps(a.xd, it.partner, ex);
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-      const OzItem nit = i + 1 < i_end ? a.items[i + 1] : it;
+      const OzItem it = a.items[i];
       const int b = k & 1;
       const int prow = static_cast<int>(it.flags >> 16);
       if ((it.flags >> 8) & 1u) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) yacc[j] = 0.0;
+        for (int j = 0; j < 8; ++j) yacc[j] = 0.0;
         er = r < prow ? a.rowexp[it.r0 + r] : 0;
       }
-      TRACE(i, 9, lane == 0 && q == 0);
+      TRACE(i, 9, lane == 0 && warp == 4);
       umma::mbar_wait(&S.acc_full[b], (k >> 1) & 1u);
-      TRACE(i, 11, lane == 0 && q == 0);
-      if (q == 0 && lane == 0 && i + 2 < i_end && !a.ablate) {  // buffer b is free: clear it for item k + 2
-        umma::mbar_arrive_tx(&S.zeroed[b], kPlanes);
-        umma::bulk_g2s(S.planes[b], a.zeros, kPlanes, &S.zeroed[b]);
-      }
+      TRACE(i, 11, lane == 0 && warp == 4);
       umma::fence_after();
-      double v[16];
-      recombine(tbase + lanes + b * kStageCols, v);
-      umma::st16_zero(tbase + lanes + b * kStageCols + 16 * (kDiag - 1));
+      int ex[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ex[j] = S.xd_exp[k & 3][j0 + j];
+      double v[8];
+      recombine8(tbase + ecol + b * kStageCols, v);
+      umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
       umma::st_wait();
-      TRACE(i, 12, lane == 0 && q == 0);
+      TRACE(i, 12, lane == 0 && warp == 4);
       umma::fence_before();
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
-      TRACE(i, 13, lane == 0 && q == 0);
+      TRACE(i, 13, lane == 0 && warp == 4);
 #pragma unroll
-      for (int j = 0; j < 16; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 12), yacc[j]);
-      TRACE(i, 10, lane == 0 && q == 0);
-      if (i + 1 < i_end) load_exps(a.xd, nit.partner, ex);
+      for (int j = 0; j < 8; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 36), yacc[j]);
+      TRACE(i, 10, lane == 0 && warp == 4);
       if ((it.flags & 0xffu) == 2u && r < prow) {  // d_r x_r in fp64 (Inf/NaN x: the caller's fix-up adds it)
         const double dr = static_cast<double>(a.diag[it.r0 + r]);
-        const double* xr = a.x + static_cast<std::size_t>(it.r0 + r) * a.ldx;
+        const double* xr = a.x + static_cast<std::size_t>(it.r0 + r) * a.ldx + j0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const double xv = j < static_cast<int>(a.mc) ? xr[j] : 0.0;
+        for (int j = 0; j < 8; ++j) {
+          const double xv = j0 + j < static_cast<int>(a.mc) ? xr[j] : 0.0;
           yacc[j] = fma(dr, isfinite(xv) ? xv : 0.0, yacc[j]);
         }
       }
       if (((it.flags >> 9) & 1u) && r < prow) {
-        double* yr = a.y + static_cast<std::size_t>(it.r0 + r - a.row_base) * a.ldy;
+        double* yr = a.y + static_cast<std::size_t>(it.r0 + r - a.row_base) * a.ldy + j0;
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (j < static_cast<int>(a.mc)) yr[j] = yacc[j];
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < static_cast<int>(a.mc)) yr[j] = yacc[j];
       }
-      it = nit;
     }
   } else {
     // ------------------------------------------ transposed-part epilogue
-    const int q = warp - 12, c = 32 * q + lane;
-    const std::uint32_t lanes = static_cast<std::uint32_t>(32 * q) << 16;
-    std::uint32_t k = 0;
-    OzItem it = a.items[i_beg < i_end ? i_beg : 0];
-    int ex[16];
-    if (i_beg < i_end) load_exps(a.xt, it.owner, ex);
+    // (TMEM lanes = tile columns): the item's partial slot, 8 columns per warp
+    const int c = 32 * eq + lane, j0 = 8 * half;
+    std::uint32_t k = 0, owners = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-      const OzItem nit = i + 1 < i_end ? a.items[i + 1] : it;
+      const OzItem it = a.items[i];
       const int b = k & 1;
       const bool trans = (it.flags & 0xffu) == 0u;
+      if ((it.flags >> 8) & 1u) ++owners;
       umma::mbar_wait(&S.acc_full[b], (k >> 1) & 1u);
-      TRACE(i, 14, lane == 0 && q == 0);
+      TRACE(i, 14, lane == 0 && warp == 12);
       umma::fence_after();
-      double v[16];
+      int ex[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) ex[j] = S.xt_exp[(owners - 1) & 3][j0 + j];
+      double v[8];
       if (trans) {
-        recombine(tbase + lanes + b * kStageCols + kND, v);
-        umma::st16_zero(tbase + lanes + b * kStageCols + kND + 16 * (kDiag - 1));
+        recombine8(tbase + ecol + b * kStageCols, v);
+        umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
         umma::st_wait();
       }
       umma::fence_before();
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
-      TRACE(i, 15, lane == 0 && q == 0);
+      TRACE(i, 15, lane == 0 && warp == 12);
       if (trans && c < static_cast<int>(it.orow)) {
-        double* out = a.partial + (static_cast<std::size_t>(i) * kTD + c) * a.mc;
+        double* out = a.partial + (static_cast<std::size_t>(it.slot) * kTD + c) * a.mc + j0;
         if (a.mc == 16) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 2)
-            *reinterpret_cast<double2*>(out + j) = make_double2(v[j] * pow2(ex[j] - 12), v[j + 1] * pow2(ex[j + 1] - 12));
+          for (int j = 0; j < 8; j += 2)
+            *reinterpret_cast<double2*>(out + j) = make_double2(v[j] * pow2(ex[j] - 36), v[j + 1] * pow2(ex[j + 1] - 36));
         } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (j < static_cast<int>(a.mc)) out[j] = v[j] * pow2(ex[j] - 12);
+          for (int j = 0; j < 8; ++j)
+            if (j0 + j < static_cast<int>(a.mc)) out[j] = v[j] * pow2(ex[j] - 36);
         }
       }
-      if (i + 1 < i_end && nit.owner != it.owner) load_exps(a.xt, nit.owner, ex);
-      it = nit;
     }
   }
   umma::fence_before();
@@ -758,10 +722,56 @@ std::uint32_t panel_of(const std::vector<std::uint32_t>& ps, std::uint32_t row) 
 
 SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
   const std::uint32_t nitems = m->sp_items;
-  std::vector<std::uint32_t> sched(8ull * nitems), cta_off(m->sp_ctas + 1);
-  CIEG_CUDA(cudaMemcpy(sched.data(), m->sp_sched, sizeof(std::uint32_t) * sched.size(), cudaMemcpyDeviceToHost));
-  CIEG_CUDA(cudaMemcpy(cta_off.data(), m->sp_sched_off, sizeof(std::uint32_t) * cta_off.size(), cudaMemcpyDeviceToHost));
+  std::vector<std::uint32_t> sp(8ull * nitems);
+  CIEG_CUDA(cudaMemcpy(sp.data(), m->sp_sched, sizeof(std::uint32_t) * sp.size(), cudaMemcpyDeviceToHost));
   const auto& ps = m->panel_start_host;
+  // The single-pass items grouped by owner panel (a panel's items are
+  // consecutive in the single-pass schedule), re-dealt in ascending panel
+  // order, each panel to the least-loaded CTA (cost: a per-item charge +
+  // a little per record): every CTA walks ascending panels and the grid sweeps the matrix
+  // front to back, so the partner panels' X digit slabs of concurrent items
+  // lie within one sector band and stay in L2.
+  struct Run {
+    std::uint32_t panel, first, count;
+    std::uint64_t cost;
+  };
+  std::vector<Run> runs;
+  for (std::uint32_t i = 0; i < nitems; ++i) {
+    const std::uint32_t* d = sp.data() + 8ull * i;
+    const std::uint32_t owner = panel_of(ps, d[7]);
+    const std::uint64_t q0 = (static_cast<std::uint64_t>(d[1]) << 32) | d[0];
+    const std::uint64_t q1 = (static_cast<std::uint64_t>(d[3]) << 32) | d[2];
+    // (dense mode: every item streams the same plane bytes and MMA work)
+    const std::uint64_t c = (4 * (q1 - q0) * ((d[4] & 0xffu) == 2u ? 2 : 1)) / 8 + 8192;
+    if (runs.empty() || runs.back().panel != owner || ((d[4] >> 8) & 1u)) runs.push_back(Run{owner, i, 0, 0});
+    ++runs.back().count;
+    runs.back().cost += c;
+  }
+  std::stable_sort(runs.begin(), runs.end(), [](const Run& x, const Run& y) { return x.panel < y.panel; });
+  const std::uint32_t ctas =
+      std::max<std::uint32_t>(1, std::min<std::uint32_t>(m->sp_ctas, static_cast<std::uint32_t>(runs.size())));
+  std::vector<std::pair<std::uint64_t, std::uint32_t>> heap;
+  for (std::uint32_t b = 0; b < ctas; ++b) heap.push_back({0, b});
+  auto cmp = [](const auto& x, const auto& y) { return x.first != y.first ? x.first > y.first : x.second > y.second; };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  std::vector<std::vector<std::uint32_t>> runs_of(ctas);
+  for (std::uint32_t r = 0; r < runs.size(); ++r) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    runs_of[heap.back().second].push_back(r);
+    heap.back().first += runs[r].cost;
+    std::push_heap(heap.begin(), heap.end(), cmp);
+  }
+  std::vector<std::uint32_t> order;  // new item -> single-pass item
+  order.reserve(nitems);
+  std::vector<std::uint32_t> cta_off(ctas + 1, 0);
+  for (std::uint32_t b = 0; b < ctas; ++b) {
+    for (std::uint32_t r : runs_of[b])
+      for (std::uint32_t i = runs[r].first; i < runs[r].first + runs[r].count; ++i) order.push_back(i);
+    cta_off[b + 1] = static_cast<std::uint32_t>(order.size());
+  }
+  std::vector<std::uint32_t> sched(8ull * nitems);  // the descriptors in the new order (records_kernel)
+  for (std::uint32_t i = 0; i < nitems; ++i)
+    std::copy(sp.begin() + 8ull * order[i], sp.begin() + 8ull * order[i] + 8, sched.begin() + 8ull * i);
   std::vector<OzItem> items(nitems);
   std::uint64_t total = 0;
   for (std::uint32_t i = 0; i < nitems; ++i) {
@@ -775,6 +785,8 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     it.orow = d[6];
     it.owner = panel_of(ps, d[7]);
     it.partner = panel_of(ps, d[5]);
+    it.slot = order[i];
+    it.pad = 0;
     it.rec0 = total;
     std::uint64_t n = 4 * (q1 - q0) * (kind == 2 ? 2 : 1);
     n = (n + 63) & ~63ull;  // whole 64-record interleave chunks
@@ -785,6 +797,7 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
   try {
     pl->nrec = total;
     pl->items = upload(items);
+    pl->ctas = ctas;
     pl->cta_off = upload(cta_off);
     CIEG_CUDA(cudaMalloc(&pl->rec, sizeof(uint2) * std::max<std::uint64_t>(1, total)));
     const std::uint32_t rows = ps.back() + kTD;
@@ -807,8 +820,8 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     unsigned bad_h = 0;
     CIEG_CUDA(cudaMemcpy(&bad_h, bad, sizeof(unsigned), cudaMemcpyDeviceToHost));
     cudaFree(bad);
-    pl->finite = bad_h == 0;
-    std::uint32_t* dsched = m->sp_sched;
+    pl->usable = bad_h == 0;
+    std::uint32_t* dsched = upload(sched);
     const unsigned tiny_cap = static_cast<unsigned>(std::min<std::uint64_t>(1u << 30, m->nnz / 512 + 4096));
     Tiny* tiny = nullptr;
     CIEG_CUDA(cudaMalloc(&tiny, sizeof(Tiny) * tiny_cap));
@@ -822,7 +835,7 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     CIEG_CUDA(cudaMemcpyAsync(&nt, ntiny, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
     if (nt + 1 >= tiny_cap) {
-      pl->finite = false;  // too many unsliceable entries: this matrix runs the fp64 DMMA kernels
+      pl->usable = false;  // too many unsliceable entries: this matrix runs the fp64 DMMA kernels
     } else if (nt) {
       std::vector<Tiny> th(nt);
       CIEG_CUDA(cudaMemcpy(th.data(), tiny, sizeof(Tiny) * nt, cudaMemcpyDeviceToHost));
@@ -846,14 +859,32 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     }
     cudaFree(tiny);
     cudaFree(ntiny);
+    cudaFree(dsched);
     ctx->launches += 2;
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
     cudaFree(tpi);
     cudaFree(tpj);
     CIEG_CUDA(cudaMalloc(&pl->xd, static_cast<std::size_t>(m->npanels) * kSlabBytes));
     CIEG_CUDA(cudaMalloc(&pl->xt, static_cast<std::size_t>(m->npanels) * kSlabBytes));
-    CIEG_CUDA(cudaMalloc(&pl->zeros, kPlanes));
-    CIEG_CUDA(cudaMemset(pl->zeros, 0, kPlanes));
+    // The slice planes of every item (kPlanes bytes each, 10 bytes per stored
+    // entry at the generator's 40 % tile density) when they fit in three
+    // quarters of the free memory; the records are dropped once scattered.
+    // Otherwise the matrix keeps the fp64 DMMA kernels.
+    const std::size_t dense_bytes = static_cast<std::size_t>(nitems) * kPlanes;
+    std::size_t free_b = 0, total_b = 0;
+    if (nitems && pl->usable && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && dense_bytes <= free_b / 4 * 3 &&
+        cudaMalloc(&pl->dense, dense_bytes) == cudaSuccess) {
+      dense_kernel<<<nitems, 256, 0, ctx->stream>>>(pl->items, pl->rec, pl->dense);
+      CIEG_CUDA(cudaGetLastError());
+      CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+      ++ctx->launches;
+    } else {
+      cudaGetLastError();  // (a failed allocation: the DMMA kernels run)
+      pl->dense = nullptr;
+      pl->usable = false;
+    }
+    cudaFree(pl->rec);
+    pl->rec = nullptr;
   } catch (...) {
     delete pl;
     throw;
@@ -893,13 +924,13 @@ void launch_sliced_tiny_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, s
 
 bool sliced_supported(const cieg_mat* m) {
   return m->precision == 0 && m->tile_edge == kTD && m->sp_sched != nullptr && m->row_lo == 0 &&
-         m->row_hi == m->dim && (!m->sliced || m->sliced->finite);
+         m->row_hi == m->dim && (!m->sliced || m->sliced->usable);
 }
 
 bool sliced_ready(cieg_ctx* ctx, cieg_mat* m) {
   if (!sliced_supported(m)) return false;
   if (!m->sliced) m->sliced = build_plan(ctx, m);
-  return m->sliced->finite;
+  return m->sliced->usable;
 }
 
 void destroy_sliced(cieg_mat* m) {
@@ -922,17 +953,12 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
     CIEG_CUDA(cudaMalloc(&trace, sizeof(long long) * 256 * 16));
     CIEG_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 256 * 16, ctx->stream));
   }
-  SlicedArgs args{pl->items, pl->cta_off, pl->rec, pl->xd, pl->xt, pl->rowexp, pl->diag, x, y, partial,
-                  ldx, ldy, mc, m->row_lo, pl->zeros, trace, 0};
-  static const int ablate = [] {
-    const char* e = std::getenv("CIEG_SLICED_ABLATE");
-    return e ? std::atoi(e) : 0;
-  }();
-  args.ablate = ablate;
+  SlicedArgs args{pl->items, pl->cta_off, pl->dense, pl->xd, pl->xt, pl->rowexp, pl->diag, x, y, partial,
+                  ldx,       ldy,         mc,        m->row_lo, trace};
   constexpr std::size_t smem = sizeof(Smem) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   CIEG_CUDA(cudaFuncSetAttribute(spmm_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  spmm_sliced_kernel<<<m->sp_ctas, kThreads, smem, ctx->stream>>>(args);
+  spmm_sliced_kernel<<<pl->ctas, kThreads, smem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
   if (trace) {  // debug: dump CTA 0's timeline
     std::vector<long long> h(256 * 16);

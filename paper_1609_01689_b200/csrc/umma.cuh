@@ -101,6 +101,13 @@ __device__ __forceinline__ void ld16(std::uint32_t taddr, std::int32_t (&v)[16])
       : "r"(taddr)
       : "memory");
 }
+// 8 consecutive 32-bit TMEM columns of this warp's 32 lanes -> 8 registers.
+__device__ __forceinline__ void ld8(std::uint32_t taddr, std::int32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr)
+               : "memory");
+}
 __device__ __forceinline__ void ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
 // 16 consecutive 32-bit TMEM columns of this warp's 32 lanes <- 0
@@ -110,6 +117,11 @@ __device__ __forceinline__ void st16_zero(std::uint32_t taddr) {
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
       "r"(z)
       : "memory");
+}
+// 8 consecutive 32-bit TMEM columns of this warp's 32 lanes <- 0
+__device__ __forceinline__ void st8_zero(std::uint32_t taddr) {
+  const std::uint32_t z = 0;
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(z) : "memory");
 }
 __device__ __forceinline__ void st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
@@ -159,6 +171,26 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, std::uint32
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+// the same with an L2 cache-policy hint (createpolicy_evict_first): streamed
+// data that should not displace the L2-resident working set
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, std::uint32_t bytes, std::uint64_t* bar,
+                                              std::uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ std::uint64_t createpolicy_evict_first() {
+  std::uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ std::uint64_t createpolicy_evict_last() {
+  std::uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 __device__ __forceinline__ void prefetch_l2(const void* p, std::uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");

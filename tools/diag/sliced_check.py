@@ -45,5 +45,8 @@ for mode in ("sliced", "owner", "single"):
     out = y.cpu().numpy()
     if mode == "sliced":
         ys = out
+        dm.spmm_ptr(x.data_ptr(), y.data_ptr(), m)
+        dev.synchronize()
+        print(f"cfg2 sliced run-to-run bitwise equal: {bool((y.cpu().numpy() == ys).all())}", flush=True)
     print(f"cfg2 m=16 {mode}: {ms:.3f} ms  {nbytes / ms / 1e6:.1f} GB/s  rel vs sliced {relc(ys, out):.3e}", flush=True)
 dev.set_spmm_mode("auto")
