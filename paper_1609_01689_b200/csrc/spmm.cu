@@ -910,6 +910,24 @@ __global__ void sp_reduce_kernel(const double* partial, const std::uint32_t* col
   }
 }
 
+// The same for the sliced K1's column-major slots (slot k, column c: rows at
+// partial + (k * mcols + c) * td): one fixed order per block column.
+__global__ void sp_reduce_cm_kernel(const double* partial, const std::uint32_t* col_off, const std::uint32_t* col_items,
+                                    const std::uint32_t* panel_start, double* y, std::uint32_t ldy, std::uint32_t mcols,
+                                    std::uint32_t td) {
+  const std::uint32_t Q = blockIdx.x;
+  const std::uint32_t k0 = col_off[Q], k1 = col_off[Q + 1];
+  if (k0 == k1) return;
+  const std::uint32_t q0 = panel_start[Q], rows = panel_start[Q + 1] - q0;
+  for (std::uint32_t e = threadIdx.x; e < td * mcols; e += blockDim.x) {
+    const std::uint32_t c = e / td, r = e - c * td;
+    if (r >= rows) continue;
+    double sum = 0.0;
+    for (std::uint32_t k = k0; k < k1; ++k) sum += partial[(static_cast<std::size_t>(col_items[k]) * mcols + c) * td + r];
+    y[static_cast<std::size_t>(q0 + r) * ldy + c] += sum;
+  }
+}
+
 template <typename V, int TD, int NT, bool SP, int SCM = 0>
 void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   using S = Shape<V, TD, NT>;
@@ -1066,7 +1084,12 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
     } else {  // fp64 values: 64-row tiles (a 128-row fp64 tile pair exceeds shared memory)
       dispatch_nt<double, 64>(ctx, m, args, mc, sp);
     }
-    if (sp) {
+    if (sliced) {
+      sp_reduce_cm_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
+                                                               m->panel_start, y + c0, ldy, mc, m->tile_edge);
+      CIEG_CUDA(cudaGetLastError());
+      ++ctx->launches;
+    } else if (sp) {
       sp_reduce_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
                                                             m->panel_start, y + c0, ldy, mc, m->tile_edge, m->row_lo,
                                                             shard_sp && yhalo ? yhalo + c0 : nullptr, ldh, m->sp_partial_lo);

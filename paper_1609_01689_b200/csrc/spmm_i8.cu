@@ -429,6 +429,7 @@ struct SlicedArgs {
   double* partial;
   std::uint32_t ldx, ldy, mc, row_base;
   long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
+  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no partial stores, 2 planes of item 0 only
 };
 
 // (slabs hold the digits only -- every operand starts on a 1024-byte
@@ -605,7 +606,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         const std::uint8_t* xsrc = a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes;
         umma::bulk_g2s(S.xd[b], xsrc, kSlab, &S.full_a[b]);
         umma::bulk_g2s(S.xd_exp[k & 3], xsrc + kSlab, 64, &S.full_a[b]);
-        const std::uint8_t* src = a.dense + static_cast<std::size_t>(i) * kPlanes;
+        const std::uint8_t* src = a.dense + static_cast<std::size_t>((a.ablate & 2) ? 0 : i) * kPlanes;
 #pragma unroll 1
         for (int s = 0; s < kAS; ++s)
           umma::bulk_g2s_hint(S.planes[b] + s * kPlane, src + s * kPlane, kPlane, &S.full_a[b], stream);
@@ -689,17 +690,13 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
       TRACE(i, 15, lane == 0 && warp == 12);
-      if (trans && c < static_cast<int>(it.orow)) {
-        double* out = a.partial + (static_cast<std::size_t>(it.slot) * kTD + c) * a.mc + j0;
-        if (a.mc == 16) {
+      if (trans && c < static_cast<int>(it.orow) && !(a.ablate & 1)) {
+        // the slot is column-major (128 rows per column): one warp store =
+        // 32 consecutive rows of one column, 256 contiguous bytes
+        double* out = a.partial + static_cast<std::size_t>(it.slot) * kTD * a.mc + c;
 #pragma unroll
-          for (int j = 0; j < 8; j += 2)
-            *reinterpret_cast<double2*>(out + j) = make_double2(v[j] * pow2(ex[j] - 36), v[j + 1] * pow2(ex[j + 1] - 36));
-        } else {
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (j0 + j < static_cast<int>(a.mc)) out[j] = v[j] * pow2(ex[j] - 36);
-        }
+        for (int j = 0; j < 8; ++j)
+          if (j0 + j < static_cast<int>(a.mc)) out[static_cast<std::size_t>(j0 + j) * kTD] = v[j] * pow2(ex[j] - 36);
       }
     }
   }
@@ -954,7 +951,12 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
     CIEG_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 256 * 16, ctx->stream));
   }
   SlicedArgs args{pl->items, pl->cta_off, pl->dense, pl->xd, pl->xt, pl->rowexp, pl->diag, x, y, partial,
-                  ldx,       ldy,         mc,        m->row_lo, trace};
+                  ldx,       ldy,         mc,        m->row_lo, trace, 0};
+  static const int ablate = [] {
+    const char* e = std::getenv("CIEG_SLICED_ABLATE");
+    return e ? std::atoi(e) : 0;
+  }();
+  args.ablate = ablate;
   constexpr std::size_t smem = sizeof(Smem) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
   CIEG_CUDA(cudaFuncSetAttribute(spmm_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
