@@ -467,6 +467,12 @@ class DeviceMatrix:
         _check(_lib.load().cieg_spmm_effective_mode(self.device.handle, self.handle, m, C.byref(out)))
         return self.SPMM_KERNELS.get(out.value, str(out.value))
 
+    def prepare(self, m: int = 16) -> str:
+        """Build the device data of the K1 kernel for width m now (the sliced
+        kernel's slice planes, otherwise built by the first SpMM); returns the
+        kernel's name."""
+        return self.spmm_kernel(m)
+
 
 _UPLOADS: "weakref.WeakKeyDictionary[CsbMatrix, DeviceMatrix]" = weakref.WeakKeyDictionary()
 

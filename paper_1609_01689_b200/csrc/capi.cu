@@ -151,6 +151,11 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   cieg::destroy_nccl(ctx);
   for (auto& e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& r : ctx->ev_pending) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   cudaStreamSynchronize(ctx->own_stream);
   cudaStreamDestroy(ctx->own_stream);
   delete ctx;

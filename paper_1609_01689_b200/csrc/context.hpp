@@ -80,6 +80,14 @@ struct cieg_ctx {
   cieg::PinnedBuf pinned_small;
   cieg::PinnedBuf pinned_stage;         // pageable host X/U: chunked staging ring (capi.cu)
   cudaEvent_t stage_ev[4] = {};
+  // phase timers (report.hpp Clock): event pairs read at the end of a solve,
+  // so timing a phase does not synchronise the host with the device
+  struct ClockRec {
+    cudaEvent_t a, b;
+    double* slot;
+  };
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<ClockRec> ev_pending;
   cieg::NcclPlane* nccl = nullptr;      // communicator of a sharded solve (cieg_ctx_nccl_init)
   bool nccl_grams = false;              // Grams all-reduced on the device inside gram()/combine_gram()
 };
@@ -160,7 +168,7 @@ bool sliced_supported(const cieg_mat* m);
 bool sliced_ready(cieg_ctx* ctx, cieg_mat* m);
 // the mode's choice for width mc (auto: sliced for mc >= kSlicedMinCols)
 bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
-constexpr std::uint32_t kSlicedMinCols = 9;
+constexpr std::uint32_t kSlicedMinCols = 2;  // measured on config 2: sliced 2.5 / 2.85 ms vs DMMA single pass 2.78 / 2.95 ms at m = 4 / 8; m = 1 stays scalar (2.10 vs 2.31 ms)
 // Digitize X and run the sliced kernel: owner rows of Y written, every
 // off-diagonal item's transposed product stored to its partial slot (the
 // caller runs sp_reduce and the non-finite fix-up as for the single pass).

@@ -305,10 +305,12 @@ inline void lu_solve(Index n, const double* lu, const Index* perm, Index m, doub
       for (Index k = 0; k < i; ++k) s -= lu[i + k * n] * tmp[k];
       tmp[i] = s;
     }
-    for (Index i = n - 1; i >= 0; --i) {
-      double s = tmp[i];
-      for (Index k = i + 1; k < n; ++k) s -= lu[i + k * n] * tmp[k];
-      tmp[i] = s / lu[i + i * n];
+    // back substitution column by column from the last (Eigen's column-major
+    // upper-triangular solve): x_k = t_k / u_kk, then t_i -= u_ik x_k for i < k
+    for (Index k = n - 1; k >= 0; --k) {
+      const double xk = tmp[k] / lu[k + k * n];
+      tmp[k] = xk;
+      for (Index i = 0; i < k; ++i) tmp[i] -= lu[i + k * n] * xk;
     }
     for (Index i = 0; i < n; ++i) col[i] = tmp[i];
   }

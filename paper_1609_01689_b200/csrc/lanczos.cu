@@ -179,6 +179,7 @@ class Lanczos {
   Lanczos(cieg_ctx* ctx, const cieg_mat* mat, const cieg_lanczos_options& opt, cieg_report& rep)
       : ctx_(ctx), mat_(mat), opt_(opt), rep_(rep), n_(mat->dim) {}
   ~Lanczos() {
+    clock_discard(ctx_);
     for (double* p : owned_) cudaFree(p);
   }
   void run(const double* v0_host);
@@ -379,6 +380,7 @@ void Lanczos::run(const double* v0_host) {
   CIEG_CUDA(cudaMemcpyAsync(rep_.trial.data(), x, sizeof(double) * rep_.trial.size(), cudaMemcpyDeviceToHost,
                             ctx_->stream));
   CIEG_CUDA(cudaStreamSynchronize(ctx_->stream));
+  clock_flush(ctx_);
   rep_.timing_ms[kTotal] =
       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
 }

@@ -119,17 +119,31 @@ __device__ bool lu_factor(double* A, int n, int ld, int* perm, double mu, const 
   for (int i = tid; i < n; i += blockDim.x) perm[i] = i;
   __syncthreads();
   for (int k = 0; k < n; ++k) {
-    if (tid == 0) {  // first occurrence of the largest |a_ik|, i >= k
+    if (tid < 32) {  // first occurrence of the largest |a_ik|, i >= k (one warp; a NaN never wins, a NaN at k keeps k)
+      const double a0 = fabs(A[k + k * ld]);
       int p = k;
-      double best = fabs(A[k + k * ld]);
-      for (int i = k + 1; i < n; ++i) {
-        const double v = fabs(A[i + k * ld]);
-        if (v > best) {
-          best = v;
-          p = i;
+      if (a0 == a0) {
+        double bv = -1.0;
+        int bi = n;
+        for (int i = k + tid; i < n; i += 32) {
+          const double v = fabs(A[i + k * ld]);
+          if (v > bv) {  // (false for NaN)
+            bv = v;
+            bi = i;
+          }
         }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+          const double ov = __shfl_xor_sync(0xffffffffu, bv, off);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+          if (ov > bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+          }
+        }
+        p = bi;
       }
-      red_i[0] = p;
+      if (tid == 0) red_i[0] = p;
     }
     __syncthreads();
     const int p = red_i[0];
@@ -198,22 +212,40 @@ __global__ void __launch_bounds__(kLuThreads) lu_direct_kernel(const __grid_cons
     }
     return;
   }
-  const int c0 = p.col_start[s], c1 = p.col_start[s + 1];
-  for (int ci = c0 + static_cast<int>(threadIdx.x); ci < c1; ci += blockDim.x) {
-    const int j = p.cols[ci];
-    double* t = tmp_dyn + static_cast<std::size_t>(ci - c0) * kMaxDirect;
-    for (int i = 0; i < n; ++i) t[i] = p.r[static_cast<std::size_t>(r0 + perm[i]) * p.k + j];
-    for (int i = 0; i < n; ++i) {
-      double acc = t[i];
-      for (int kk = 0; kk < i; ++kk) acc = DSUB(acc, DMUL(A[i + kk * ld], t[kk]));
-      t[i] = acc;
+  // Triangular solves for this shift's columns, every (row, column) on its
+  // own thread and one barrier per step: the forward sweep column by column
+  // (each t_i sees its updates in increasing k, as the row-oriented sweep),
+  // the back substitution column by column from the last (dense_small.hpp).
+  const int c0 = p.col_start[s], cnt = p.col_start[s + 1] - c0;
+  double* t = tmp_dyn;                                                // [cnt][kMaxDirect]
+  double* xs = tmp_dyn + static_cast<std::size_t>(cnt) * kMaxDirect;  // solutions
+  const int tot = cnt * n;
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int ci = e / n, i = e - ci * n;
+    t[ci * kMaxDirect + i] = p.r[static_cast<std::size_t>(r0 + perm[i]) * p.k + p.cols[c0 + ci]];
+  }
+  __syncthreads();
+  for (int kk = 0; kk + 1 < n; ++kk) {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int ci = e / n, i = e - ci * n;
+      if (i > kk) t[ci * kMaxDirect + i] = DSUB(t[ci * kMaxDirect + i], DMUL(A[i + kk * ld], t[ci * kMaxDirect + kk]));
     }
-    for (int i = n - 1; i >= 0; --i) {
-      double acc = t[i];
-      for (int kk = i + 1; kk < n; ++kk) acc = DSUB(acc, DMUL(A[i + kk * ld], t[kk]));
-      t[i] = DDIV(acc, A[i + i * ld]);
+    __syncthreads();
+  }
+  for (int kk = n - 1; kk >= 0; --kk) {
+    for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+      const int ci = e / n, i = e - ci * n;
+      const double xk = DDIV(t[ci * kMaxDirect + kk], A[kk + kk * ld]);
+      if (i < kk)
+        t[ci * kMaxDirect + i] = DSUB(t[ci * kMaxDirect + i], DMUL(A[i + kk * ld], xk));
+      else if (i == kk)
+        xs[ci * kMaxDirect + kk] = xk;
     }
-    for (int i = 0; i < n; ++i) p.w[static_cast<std::size_t>(r0 + i) * p.k + j] = t[i];
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < tot; e += blockDim.x) {
+    const int ci = e / n, i = e - ci * n;
+    p.w[static_cast<std::size_t>(r0 + i) * p.k + p.cols[c0 + ci]] = xs[ci * kMaxDirect + i];
   }
 }
 
@@ -276,10 +308,10 @@ __device__ void tiny_lu_solve(double* hm, int m, double* rhs) {
     for (int kk = 0; kk < i; ++kk) s = DSUB(s, DMUL(hm[i + kk * m], t[kk]));
     t[i] = s;
   }
-  for (int i = m - 1; i >= 0; --i) {
-    double s = t[i];
-    for (int kk = i + 1; kk < m; ++kk) s = DSUB(s, DMUL(hm[i + kk * m], t[kk]));
-    t[i] = DDIV(s, hm[i + i * m]);
+  for (int kk = m - 1; kk >= 0; --kk) {  // column-oriented back substitution (dense_small.hpp order)
+    const double xk = DDIV(t[kk], hm[kk + kk * m]);
+    t[kk] = xk;
+    for (int i = 0; i < kk; ++i) t[i] = DSUB(t[i], DMUL(hm[i + kk * m], xk));
   }
   for (int i = 0; i < m; ++i) rhs[i] = t[i];
 }
@@ -671,7 +703,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
 }  // namespace
 
 int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::uint32_t k,
-                  const ShiftPlan& plan, const cieg_precond_config& cfg, double* w) {
+                  const ShiftPlan& plan, const cieg_precond_config& cfg, double* w, int* singular_accum) {
   const std::size_t bytes = static_cast<std::size_t>(prec->dim) * k * sizeof(double);
   if (w != r && bytes) CIEG_CUDA(cudaMemcpyAsync(w, r, bytes, cudaMemcpyDeviceToDevice, ctx->stream));
   std::vector<int> engaged;
@@ -681,22 +713,30 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
   if (engaged.size() > static_cast<std::size_t>(kMaxCols)) fail(CIEG_ERR_CONFIG, "preconditioner: more than 64 columns");
   if (cfg.inner_iters < 1) fail(CIEG_ERR_CONFIG, "fom_solve: iters must be >= 1");
 
-  std::vector<std::uint32_t> small, large;
-  for (std::uint32_t g = 0; g < prec->ngroups; ++g) {
-    const std::uint32_t sz = prec->bounds_host[g + 1] - prec->bounds_host[g];
-    if (sz == 0) continue;
-    (static_cast<int>(sz) <= cfg.small_block_cutoff ? small : large).push_back(g);
+  if (prec->lists_cutoff != cfg.small_block_cutoff) {
+    prec->small_host.clear();
+    prec->large_host.clear();
+    for (std::uint32_t g = 0; g < prec->ngroups; ++g) {
+      const std::uint32_t sz = prec->bounds_host[g + 1] - prec->bounds_host[g];
+      if (sz == 0) continue;
+      (static_cast<int>(sz) <= cfg.small_block_cutoff ? prec->small_host : prec->large_host).push_back(g);
+    }
+    std::vector<std::uint32_t> all(prec->small_host);
+    all.insert(all.end(), prec->large_host.begin(), prec->large_host.end());
+    all.resize(all.size() + 2, 0u);  // + the int counter slot (kept 8-byte aligned)
+    if (all.size() & 1) all.push_back(0u);
+    cudaFree(prec->lists);
+    prec->lists = nullptr;
+    CIEG_CUDA(cudaMalloc(&prec->lists, sizeof(std::uint32_t) * all.size()));
+    CIEG_CUDA(cudaMemcpy(prec->lists, all.data(), sizeof(std::uint32_t) * all.size(), cudaMemcpyHostToDevice));
+    prec->lists_cutoff = cfg.small_block_cutoff;
   }
-  std::uint32_t* dgroups = static_cast<std::uint32_t*>(
-      ctx->scratch_red.get(sizeof(std::uint32_t) * (small.size() + large.size() + 64) + 256));
-  int* dcount = reinterpret_cast<int*>(dgroups + small.size() + large.size() + 32);
-  CIEG_CUDA(cudaMemsetAsync(dcount, 0, sizeof(int), ctx->stream));
-  if (!small.empty())
-    CIEG_CUDA(cudaMemcpyAsync(dgroups, small.data(), sizeof(std::uint32_t) * small.size(),
-                              cudaMemcpyHostToDevice, ctx->stream));
-  if (!large.empty())
-    CIEG_CUDA(cudaMemcpyAsync(dgroups + small.size(), large.data(), sizeof(std::uint32_t) * large.size(),
-                              cudaMemcpyHostToDevice, ctx->stream));
+  const std::vector<std::uint32_t>& small = prec->small_host;
+  const std::vector<std::uint32_t>& large = prec->large_host;
+  std::uint32_t* dgroups = prec->lists;
+  int* dcount = singular_accum ? singular_accum
+                               : reinterpret_cast<int*>(dgroups + ((small.size() + large.size() + 1) & ~std::size_t{1}));
+  if (!singular_accum) CIEG_CUDA(cudaMemsetAsync(dcount, 0, sizeof(int), ctx->stream));
 
   if (!small.empty()) {
     if (cfg.small_block_cutoff > kMaxDirect && prec->max_group > static_cast<std::uint32_t>(kMaxDirect))
@@ -723,7 +763,7 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
     lp.col_start[s] = o;
     int maxcols = 0;
     for (int t = 0; t < lp.nshift; ++t) maxcols = std::max(maxcols, lp.col_start[t + 1] - lp.col_start[t]);
-    const std::size_t smem = sizeof(double) * static_cast<std::size_t>(maxcols) * kMaxDirect;
+    const std::size_t smem = 2 * sizeof(double) * static_cast<std::size_t>(maxcols) * kMaxDirect;
     dim3 grid(static_cast<unsigned>(small.size()), static_cast<unsigned>(lp.nshift));
     auto lu = prec->blocks32 ? lu_direct_kernel<true> : lu_direct_kernel<false>;
     CIEG_CUDA(cudaFuncSetAttribute(lu, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -778,6 +818,7 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
     CIEG_CUDA(cudaGetLastError());
     ++ctx->launches;
   }
+  if (singular_accum) return 0;
   int* pin = static_cast<int*>(ctx->pinned_small.get(sizeof(double) * 48 * 48));
   CIEG_CUDA(cudaMemcpyAsync(pin, dcount, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   CIEG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -17,6 +17,11 @@ struct cieg_prec {
   double* blocks = nullptr;                   // device, column-major per group (fp64) ...
   float* blocks32 = nullptr;                  // ... or fp32 (blocks of an fp32 H; exact)
   std::uint32_t max_group = 0;
+  // group lists by size class for one small-block cutoff, kept on the device
+  // (the partition is fixed per preconditioner and cutoff)
+  mutable int lists_cutoff = -1;
+  mutable std::vector<std::uint32_t> small_host, large_host;
+  mutable std::uint32_t* lists = nullptr;  // small groups then large groups, + an int counter slot
   ~cieg_prec();
 };
 
@@ -33,8 +38,11 @@ ShiftPlan choose_shifts(const std::vector<double>& theta, const std::vector<doub
                         int iteration, double tol, const cieg_precond_config& cfg);
 
 // W = apply_preconditioner(tiles, R, plan) on device (R, W row-major n x k,
-// contiguous). Returns the number of singular-shift pass-throughs.
+// contiguous). Returns the number of singular-shift pass-throughs, reported on
+// stderr like the reference -- unless singular_accum (a device counter) is
+// given: then the count is added there with no host synchronisation (the
+// caller reports it) and 0 is returned.
 int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::uint32_t k,
-                  const ShiftPlan& plan, const cieg_precond_config& cfg, double* w);
+                  const ShiftPlan& plan, const cieg_precond_config& cfg, double* w, int* singular_accum = nullptr);
 
 }  // namespace cieg

@@ -13,4 +13,5 @@ for r in range(5):
     rep = ci.lobpcg_solve(h, x0, opt)
     ms = (time.perf_counter() - t0) * 1e3
     parts = sum(v for k, v in rep.timing_ms.items() if k != "total")
-    print(f"run {r}: wall {ms:.1f} ms  total {rep.timing_ms['total']:.1f}  phases {parts:.1f}  iters {rep.iterations}")
+    print(f"run {r}: wall {ms:.1f} ms  total {rep.timing_ms['total']:.1f}  phases {parts:.1f}  iters {rep.iterations}  "
+          + " ".join(f"{k} {v:.1f}" for k, v in rep.timing_ms.items() if k != "total"))
