@@ -571,7 +571,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
     for (int a = 0; a < 4; ++a)
 #pragma unroll
       for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-    // A fragments (raw storage type) are prefetched one 16-wide k chunk
+    // A fragments (raw storage type) are prefetched three 16-wide k chunks
     // ahead and widened at use, so global latency overlaps the DMMAs
     using Raw = typename std::conditional<F32, float, double>::type;
     const Raw* blk_raw = F32 ? reinterpret_cast<const Raw*>(blk.f) : reinterpret_cast<const Raw*>(blk.d);
@@ -605,12 +605,20 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
           for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], av, bf[u][b]);
         }
     };
+    // four 16-wide k chunks in flight (loads three chunks ahead of the DMMAs)
+    Raw a2[4][4], a3[4][4];
     load_a(0, a0);
-    for (int k0 = 0; k0 < NP; k0 += 32) {
-      load_a(k0 + 16, a1);
+    load_a(16, a1);
+    load_a(32, a2);
+    for (int k0 = 0; k0 < NP; k0 += 64) {
+      load_a(k0 + 48, a3);
       mma_chunk(k0, a0);
-      load_a(k0 + 32, a0);
+      load_a(k0 + 64, a0);
       mma_chunk(k0 + 16, a1);
+      load_a(k0 + 80, a1);
+      mma_chunk(k0 + 32, a2);
+      load_a(k0 + 96, a2);
+      mma_chunk(k0 + 48, a3);
     }
     // w = z - mu v_m
 #pragma unroll
