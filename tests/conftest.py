@@ -102,6 +102,7 @@ def single_pass_shards(h, world, m, x):
         assert phi == sm.row_lo and plo <= phi
         y = torch.empty((sm.local_rows, m), dtype=torch.float64, device="cuda")
         yh = torch.full((max(phi - plo, 1), m), float("nan"), dtype=torch.float64, device="cuda")
+        torch.cuda.synchronize()  # the fill runs on torch's stream, the library on its own
         ci._check(_lib.load().cieg_spmm_partial(dev.handle, sm.handle, C.c_void_p(xs.data_ptr()),
                                                 C.c_void_p(y.data_ptr()), m, C.c_void_p(yh.data_ptr())))
         dev.synchronize()

@@ -20,3 +20,5 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:spmm_sliced -s 1 -c 1 -o $O/${TAG}_sliced_full \
   python tools/diag/sliced_prof.py 16 sliced > $O/${TAG}_sliced_full.log 2>&1; echo ncu2 rc=$?
 timeout 600 python tools/diag/sliced_trace.py > $O/${TAG}_sliced_trace.txt 2>&1; echo trace rc=$?
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:fom_fast -s 2 -c 1 -o $O/${TAG}_fom_full \
+  python tools/prof_cfg4_iter.py 8 > $O/${TAG}_fom_full.log 2>&1; echo ncu3 rc=$?
