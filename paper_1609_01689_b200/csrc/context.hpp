@@ -169,12 +169,11 @@ bool sliced_ready(cieg_ctx* ctx, cieg_mat* m);
 // the mode's choice for width mc (auto: sliced for mc >= kSlicedMinCols)
 bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
 constexpr std::uint32_t kSlicedMinCols = 2;  // measured on config 2: sliced 2.5 / 2.85 ms vs DMMA single pass 2.78 / 2.95 ms at m = 4 / 8; m = 1 stays scalar (2.10 vs 2.31 ms)
-// Digitize X and run the sliced kernel: owner rows of Y written, every
-// off-diagonal item's transposed product stored to its partial slot (the
-// caller runs sp_reduce and the non-finite fix-up as for the single pass).
+// Digitize X and run the sliced kernel: every row of Y written (row parts and
+// transposed parts accumulated in exact fixed point, then converted); the
+// caller runs the tiny-entry and non-finite fix-ups.
 void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
-                        std::uint32_t ldy, std::uint32_t mc, double* partial, unsigned* nonfinite,
-                        unsigned launch_id);
+                        std::uint32_t ldy, std::uint32_t mc, unsigned* nonfinite, unsigned launch_id);
 void destroy_sliced(cieg_mat* m);
 // the K1 mode launch_spmm runs for width mc (CIEG_SPMM_OWNER / SINGLE_PASS / SLICED)
 int spmm_effective_mode(cieg_ctx* ctx, cieg_mat* m, std::uint32_t mc);

@@ -910,24 +910,6 @@ __global__ void sp_reduce_kernel(const double* partial, const std::uint32_t* col
   }
 }
 
-// The same for the sliced K1's column-major slots (slot k, column c: rows at
-// partial + (k * mcols + c) * td): one fixed order per block column.
-__global__ void sp_reduce_cm_kernel(const double* partial, const std::uint32_t* col_off, const std::uint32_t* col_items,
-                                    const std::uint32_t* panel_start, double* y, std::uint32_t ldy, std::uint32_t mcols,
-                                    std::uint32_t td) {
-  const std::uint32_t Q = blockIdx.x;
-  const std::uint32_t k0 = col_off[Q], k1 = col_off[Q + 1];
-  if (k0 == k1) return;
-  const std::uint32_t q0 = panel_start[Q], rows = panel_start[Q + 1] - q0;
-  for (std::uint32_t e = threadIdx.x; e < td * mcols; e += blockDim.x) {
-    const std::uint32_t c = e / td, r = e - c * td;
-    if (r >= rows) continue;
-    double sum = 0.0;
-    for (std::uint32_t k = k0; k < k1; ++k) sum += partial[(static_cast<std::size_t>(col_items[k]) * mcols + c) * td + r];
-    y[static_cast<std::size_t>(q0 + r) * ldy + c] += sum;
-  }
-}
-
 template <typename V, int TD, int NT, bool SP, int SCM = 0>
 void launch_variant(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args) {
   using S = Shape<V, TD, NT>;
@@ -1020,7 +1002,7 @@ bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc) {
   const int mode = effective_mode(ctx);
   if (mode == CIEG_SPMM_SLICED) return true;
   if (mode != CIEG_SPMM_AUTO) return false;
-  return mc >= kSlicedMinCols && single_pass_fits(ctx, m, mc);
+  return mc >= kSlicedMinCols;
 }
 
 
@@ -1066,7 +1048,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                   ++ctx->spmm_launch_id,
                   nullptr};
     const bool sliced = !shard && sliced_rule(ctx, m, mc) && sliced_ready(ctx, const_cast<cieg_mat*>(m));
-    const bool sp = sliced || (shard ? shard_sp : single_pass_default(ctx, m, mc));
+    const bool sp = !sliced && (shard ? shard_sp : single_pass_default(ctx, m, mc));
     if (sp) {
       args.sched_off = m->sp_sched_off;
       args.sched = reinterpret_cast<const uint4*>(m->sp_sched);
@@ -1074,8 +1056,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
           ctx->scratch_partial.get(sizeof(double) * std::max<std::size_t>(1, std::size_t(m->sp_items) * m->tile_edge * mc)));
     }
     if (sliced) {
-      launch_spmm_sliced(ctx, const_cast<cieg_mat*>(m), x + c0, ldx, y + c0, ldy, mc, args.partial, args.nonfinite,
-                         args.launch_id);
+      launch_spmm_sliced(ctx, const_cast<cieg_mat*>(m), x + c0, ldx, y + c0, ldy, mc, args.nonfinite, args.launch_id);
     } else if (m->precision == 0) {
       if (m->tile_edge == 64)
         dispatch_nt<float, 64>(ctx, m, args, mc, sp);
@@ -1084,12 +1065,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
     } else {  // fp64 values: 64-row tiles (a 128-row fp64 tile pair exceeds shared memory)
       dispatch_nt<double, 64>(ctx, m, args, mc, sp);
     }
-    if (sliced) {
-      sp_reduce_cm_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
-                                                               m->panel_start, y + c0, ldy, mc, m->tile_edge);
-      CIEG_CUDA(cudaGetLastError());
-      ++ctx->launches;
-    } else if (sp) {
+    if (sp) {
       sp_reduce_kernel<<<m->npanels, 256, 0, ctx->stream>>>(args.partial, m->sp_col_off, m->sp_col_items,
                                                             m->panel_start, y + c0, ldy, mc, m->tile_edge, m->row_lo,
                                                             shard_sp && yhalo ? yhalo + c0 : nullptr, ldh, m->sp_partial_lo);

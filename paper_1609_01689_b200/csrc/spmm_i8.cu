@@ -103,6 +103,17 @@ struct SlicedPlan {
   std::uint32_t ntiny_rows = 0;
   std::uint32_t *tiny_rows = nullptr, *tiny_off = nullptr, *tiny_in = nullptr;
   double* tiny_val = nullptr;
+  // Fixed-point accumulation of every contribution to a panel's rows (the
+  // row part and the transposed parts), int64, exact and order-independent:
+  // yint[Q][column][row] in units of 2^(escale[Q][column] - 62). The scales
+  // are bounds on |Y| per (panel, column), set every call from the X digit
+  // exponents of the panel's neighbours (scales_kernel).
+  long long* yint = nullptr;
+  int* escale = nullptr;
+  std::uint32_t* nb_off = nullptr;  // per panel: neighbours (P | 1 << 31 for a transposed contributor)
+  std::uint32_t* nb = nullptr;
+  int* erq = nullptr;  // per panel: max row scale e_r of its rows
+  int* edq = nullptr;  // per panel: max exponent of its stored diagonal
   std::uint64_t nrec = 0;
   std::uint32_t ctas = 0;
   bool usable = true;  // every stored value finite and the planes fit (else the DMMA kernels run)
@@ -119,6 +130,12 @@ struct SlicedPlan {
     cudaFree(tiny_off);
     cudaFree(tiny_in);
     cudaFree(tiny_val);
+    cudaFree(yint);
+    cudaFree(escale);
+    cudaFree(nb_off);
+    cudaFree(nb);
+    cudaFree(erq);
+    cudaFree(edq);
   }
 };
 
@@ -416,6 +433,63 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
   }
 }
 
+// Per (panel, column) bound exponents of Y: |y| < 2^escale. Every
+// contribution to a row of Q is below 2^(e + 7) -- a row part of tile (Q, P):
+// e = max e_r (rows of Q) + ex_P (|h| < 2^e_r, |x_P| < 2^ex_P, 128 terms);
+// a transposed part of tile (P, Q): e = ex'_P (|x_P 2^e_r| < 2^ex'_P); the
+// diagonal term d_r x_r below 2^(max exponent of d in Q + ex_Q) -- and there
+// are cnt of them, so escale = max + ceil(log2(cnt + 1)) + 1 bounds their sum.
+__global__ void scales_kernel(const std::uint32_t* nb_off, const std::uint32_t* nb, const int* erq, const int* edq,
+                              const std::uint8_t* xd, const std::uint8_t* xt, int* escale) {
+  const std::uint32_t Q = blockIdx.x;
+  const int j = threadIdx.x;
+  if (j >= 16) return;
+  auto xe = [&](const std::uint8_t* slabs, std::uint32_t P) {
+    return reinterpret_cast<const int*>(slabs + static_cast<std::size_t>(P) * kSlabBytes + kSlab)[j];
+  };
+  int e = INT_MIN / 4;
+  std::uint32_t cnt = 1;
+  for (std::uint32_t t = nb_off[Q]; t < nb_off[Q + 1]; ++t, ++cnt) {
+    const std::uint32_t v = nb[t], P = v & 0x7fffffffu;
+    e = max(e, (v >> 31) ? xe(xt, P) + 7 : erq[Q] + xe(xd, P) + 7);
+  }
+  e = max(e, edq[Q] + xe(xd, Q));
+  if (e < -1000) e = 0;  // no contribution at all (Y rows of Q are zero)
+  escale[Q * 16 + j] = e + (32 - __clz(cnt + 1)) + 1;
+}
+
+// Y = yint 2^(escale - 62) (one rounding, deterministic) for the columns of
+// this call; yint is zeroed for the next call.
+__global__ void __launch_bounds__(256) yint_to_y_kernel(long long* yint, const int* escale,
+                                                       const std::uint32_t* panel_start, double* y, std::uint32_t ldy,
+                                                       std::uint32_t mc, std::uint32_t row_base) {
+  __shared__ double t[16][kTD + 1];  // [column][row], transposed through shared memory
+  __shared__ double sc[16];
+  const std::uint32_t Q = blockIdx.x;
+  const std::uint32_t q0 = panel_start[Q], rows = panel_start[Q + 1] - q0;
+  long long* yi = yint + static_cast<std::size_t>(Q) * kTD * 16;
+  const int tid = threadIdx.x;
+  if (tid < 16) sc[tid] = pow2(escale[Q * 16 + tid] - 62);
+  long long v[kTD * 16 / 256];
+#pragma unroll
+  for (int u = 0; u < kTD * 16 / 256; ++u) v[u] = __ldcg(yi + tid + 256 * u);  // yint is [column][row]: coalesced
+#pragma unroll
+  for (int u = 0; u < kTD * 16 / 256; ++u) __stcg(yi + tid + 256 * u, 0ll);   // cleared for the next call
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kTD * 16 / 256; ++u) {
+    const int e = tid + 256 * u, c = e / kTD, r = e - c * kTD;
+    t[c][r] = __ll2double_rn(v[u]) * sc[c];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < kTD * 16 / 256; ++u) {  // Y rows: coalesced writes
+    const int e = tid + 256 * u, r = e >> 4, c = e & 15;
+    if (r < static_cast<int>(rows) && c < static_cast<int>(mc))
+      y[static_cast<std::size_t>(q0 + r - row_base) * ldy + c] = t[c][r];
+  }
+}
+
 struct SlicedArgs {
   const OzItem* items;
   const std::uint32_t* cta_off;
@@ -425,11 +499,11 @@ struct SlicedArgs {
   const int* rowexp;
   const float* diag;
   const double* x;  // the call's X (the diagonal term d_r x_r)
-  double* y;
-  double* partial;
-  std::uint32_t ldx, ldy, mc, row_base;
+  long long* yint;     // fixed-point Y, [panel][column][row], units 2^(escale - 62)
+  const int* escale;   // [panel][column]
+  std::uint32_t ldx, mc;
   long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
-  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no partial stores, 2 planes of item 0 only
+  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no transposed reduction, 2 planes of item 0 only
 };
 
 // (slabs hold the digits only -- every operand starts on a 1024-byte
@@ -438,12 +512,13 @@ struct SlicedArgs {
 struct Smem {
   std::uint8_t planes[2][kPlanes];
   std::uint8_t xd[2][kSlab];
-  std::uint8_t xt[2][kSlab];
+  std::uint8_t xt[kSlab];  // the owner panel's slab (one buffer: the row MMAs of an owner's first item cover its load)
+  long long stage[kTD * 16];  // one transposed contribution in fixed point, [column][row], for the bulk reduction
   // the slabs' column exponents, staged with them (4 deep: an epilogue reads
   // an item's exponents before it releases the item's accumulator stage)
   int xd_exp[4][16];
   int xt_exp[4][16];
-  std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2];
+  std::uint64_t full_a[2], empty_a[2], full_t, empty_t, acc_full[2], acc_empty[2];
   std::uint32_t tmem;
 };
 
@@ -479,6 +554,22 @@ __device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8]) 
   }
 }
 
+// ---- fixed-point accumulation into yint
+// one transposed contribution (the 16 KB stage) added to yint by the TMA
+// engine (integer adds in L2: exact, order-independent)
+__device__ __forceinline__ void bulk_reduce_add(long long* dst, const long long* src, std::uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
+               "r"(umma::smem_u32(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// named barrier of the eight transposed-epilogue warps
+__device__ __forceinline__ void tbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// v 2^e rounded to the nearest integer (|result| < 2^62 by the scale bounds)
+__device__ __forceinline__ long long fixp(double v, int e) { return __double2ll_rn(v * pow2(e)); }
+
 #define TRACE(item, slot, cond)                                                                      \
   do {                                                                                               \
     if (a.trace && blockIdx.x == 0 && (cond) && (item) - i_beg < 256)                                \
@@ -501,11 +592,12 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     for (int b = 0; b < 2; ++b) {
       umma::mbar_init(&S.full_a[b], 1);
       umma::mbar_init(&S.empty_a[b], 1);
-      umma::mbar_init(&S.full_t[b], 1);
-      umma::mbar_init(&S.empty_t[b], 1);
+
       umma::mbar_init(&S.acc_full[b], 1);
       umma::mbar_init(&S.acc_empty[b], kEpiWarps);
     }
+    umma::mbar_init(&S.full_t, 1);
+    umma::mbar_init(&S.empty_t, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) umma::tmem_alloc<512>(&S.tmem);
@@ -534,20 +626,14 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     // warp-uniform (base descriptor + constant offsets, in uniform
     // registers), one elected lane executes each tcgen05.mma.
     std::uint32_t k = 0, owners = 0;
-    int o = 0;
     const std::uint64_t a_k0 = umma::sdesc(umma::smem_u32(S.planes[0]), 128, 1024);   // A K-major (H X)
     const std::uint64_t a_mn0 = umma::sdesc(umma::smem_u32(S.planes[0]), 1024, 128);  // A MN-major (H^T X)
     const std::uint64_t b_d0 = umma::sdesc(umma::smem_u32(S.xd[0]), 128, 1024);
-    const std::uint64_t b_t0 = umma::sdesc(umma::smem_u32(S.xt[0]), 128, 1024);
+    const std::uint64_t bt = umma::sdesc(umma::smem_u32(S.xt), 128, 1024);
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
       const OzItem it = a.items[i];
       const int b = k & 1;
       TRACE(i, 0, lane == 0);
-      if ((it.flags >> 8) & 1u) {
-        o = owners & 1;
-        umma::mbar_wait(&S.full_t[o], (owners >> 1) & 1u);
-        ++owners;
-      }
       umma::mbar_wait(&S.full_a[b], (k >> 1) & 1u);
       TRACE(i, 1, lane == 0);
       umma::mbar_wait(&S.acc_empty[b], ((k >> 1) & 1u) ^ 1u);
@@ -558,24 +644,35 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       // descriptor start-address field: (byte offset) >> 4, no carry out of 14 bits
       const std::uint64_t ab = static_cast<std::uint64_t>(b * (kPlanes >> 4));
       const std::uint64_t bd = b_d0 + static_cast<std::uint64_t>(b * (kSlab >> 4));
-      const std::uint64_t bt = b_t0 + static_cast<std::uint64_t>(o * (kSlab >> 4));
+      // row part first: at an owner's first item it covers the owner slab's load
 #pragma unroll 1
       for (int s = 0; s < kAS; ++s) {
         const int n = 16 * min(kXD, kDiag - s);  // digits t with s + t < kDiag
         const std::uint32_t id_row = umma::idesc_i8(1, 1, 0, 0, 128, n);  // balanced digits: all signed
-        const std::uint32_t id_tr = umma::idesc_i8(1, 1, 1, 0, 128, n);
 #pragma unroll
-        for (int ks = 0; ks < kTD / 32; ++ks) {
+        for (int ks = 0; ks < kTD / 32; ++ks)
           umma::mma_i8_warp(d_row + 16 * s, a_k0 + ab + ((s * kPlane + 256 * ks) >> 4), bd + ((256 * ks) >> 4), id_row,
                             (s | ks) != 0);
-          if (trans)
+      }
+      if ((it.flags >> 8) & 1u) {
+        umma::mbar_wait(&S.full_t, owners & 1u);
+        ++owners;
+        umma::fence_after();
+      }
+      if (trans) {
+#pragma unroll 1
+        for (int s = 0; s < kAS; ++s) {
+          const int n = 16 * min(kXD, kDiag - s);
+          const std::uint32_t id_tr = umma::idesc_i8(1, 1, 1, 0, 128, n);
+#pragma unroll
+          for (int ks = 0; ks < kTD / 32; ++ks)
             umma::mma_i8_warp(d_tr + 16 * s, a_mn0 + ab + ((s * kPlane + 4096 * ks) >> 4), bt + ((256 * ks) >> 4),
                               id_tr, (s | ks) != 0);
         }
       }
       umma::commit_warp(&S.empty_a[b]);
       umma::commit_warp(&S.acc_full[b]);
-      if ((it.flags >> 9) & 1u) umma::commit_warp(&S.empty_t[o]);
+      if ((it.flags >> 9) & 1u) umma::commit_warp(&S.empty_t);
       TRACE(i, 3, lane == 0);
     }
   } else if (warp == 1) {
@@ -591,13 +688,12 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         const OzItem it = a.items[i];
         const int b = k & 1;
         TRACE(i, 8, true);
-        if ((it.flags >> 8) & 1u) {
-          const int o = owners & 1;
-          umma::mbar_wait(&S.empty_t[o], ((owners >> 1) & 1u) ^ 1u);
-          umma::mbar_arrive_tx(&S.full_t[o], kSlab + 64);
+        if ((it.flags >> 8) & 1u) {  // (the previous owner's MMAs read the slab until empty_t)
+          umma::mbar_wait(&S.empty_t, (owners & 1u) ^ 1u);
+          umma::mbar_arrive_tx(&S.full_t, kSlab + 64);
           const std::uint8_t* src = a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes;
-          umma::bulk_g2s(S.xt[o], src, kSlab, &S.full_t[o]);
-          umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t[o]);
+          umma::bulk_g2s(S.xt, src, kSlab, &S.full_t);
+          umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t);
           ++owners;
         }
         umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
@@ -618,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     // (TMEM lanes = tile rows; 8 of the 16 columns per warp)
     const int r = 32 * eq + lane, j0 = 8 * half;
     double yacc[8];
-    int er = 0;
+    int er = 0, osc[8];
     std::uint32_t k = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
       const OzItem it = a.items[i];
@@ -626,7 +722,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       const int prow = static_cast<int>(it.flags >> 16);
       if ((it.flags >> 8) & 1u) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) yacc[j] = 0.0;
+        for (int j = 0; j < 8; ++j) {
+          yacc[j] = 0.0;
+          osc[j] = __ldg(a.escale + it.owner * 16 + j0 + j);
+        }
         er = r < prow ? a.rowexp[it.r0 + r] : 0;
       }
       TRACE(i, 9, lane == 0 && warp == 4);
@@ -657,23 +756,31 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
           yacc[j] = fma(dr, isfinite(xv) ? xv : 0.0, yacc[j]);
         }
       }
-      if (((it.flags >> 9) & 1u) && r < prow) {
-        double* yr = a.y + static_cast<std::size_t>(it.r0 + r - a.row_base) * a.ldy + j0;
+      if (((it.flags >> 9) & 1u) && r < prow) {  // the owner's row part, in fixed point, added to yint
+        unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
+                                 static_cast<std::size_t>(it.owner) * kTD * 16 + static_cast<std::size_t>(j0) * kTD + r;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          if (j0 + j < static_cast<int>(a.mc)) yr[j] = yacc[j];
+          atomicAdd(yr + j * kTD, static_cast<unsigned long long>(fixp(yacc[j], 62 - osc[j])));
       }
     }
   } else {
     // ------------------------------------------ transposed-part epilogue
-    // (TMEM lanes = tile columns): the item's partial slot, 8 columns per warp
-    const int c = 32 * eq + lane, j0 = 8 * half;
+    // (TMEM lanes = tile columns; 8 of the 16 columns per warp): the item's
+    // contribution to its partner panel, in fixed point, staged in shared
+    // memory by the eight warps and added to yint by one bulk reduction.
+    const int c = 32 * eq + lane, j0 = 8 * half, gt = tid - 320;
     std::uint32_t k = 0, owners = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
       const OzItem it = a.items[i];
       const int b = k & 1;
       const bool trans = (it.flags & 0xffu) == 0u;
       if ((it.flags >> 8) & 1u) ++owners;
+      int psc[8];
+      if (trans) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) psc[j] = __ldg(a.escale + it.partner * 16 + j0 + j);
+      }
       umma::mbar_wait(&S.acc_full[b], (k >> 1) & 1u);
       TRACE(i, 14, lane == 0 && warp == 12);
       umma::fence_after();
@@ -690,15 +797,18 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       __syncwarp();
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
       TRACE(i, 15, lane == 0 && warp == 12);
-      if (trans && c < static_cast<int>(it.orow) && !(a.ablate & 1)) {
-        // the slot is column-major (128 rows per column): one warp store =
-        // 32 consecutive rows of one column, 256 contiguous bytes
-        double* out = a.partial + static_cast<std::size_t>(it.slot) * kTD * a.mc + c;
+      if (!trans || (a.ablate & 1)) continue;
+      if (gt == 0) bulk_wait_read();  // the previous contribution has left the stage
+      tbar();
+      const bool in = c < static_cast<int>(it.orow);
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (j0 + j < static_cast<int>(a.mc)) out[static_cast<std::size_t>(j0 + j) * kTD] = v[j] * pow2(ex[j] - 36);
-      }
+      for (int j = 0; j < 8; ++j)
+        S.stage[(j0 + j) * kTD + c] = in ? fixp(v[j], ex[j] - 36 + 62 - psc[j]) : 0ll;
+      umma::fence_async_smem();
+      tbar();
+      if (gt == 0) bulk_reduce_add(a.yint + static_cast<std::size_t>(it.partner) * kTD * 16, S.stage, kTD * 16 * 8);
     }
+    if (gt == 0) bulk_wait_all();
   }
   umma::fence_before();
   __syncthreads();
@@ -812,6 +922,8 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
     std::vector<int> eh(rows);
     CIEG_CUDA(cudaMemcpy(eh.data(), pl->rowexp, sizeof(int) * rows, cudaMemcpyDeviceToHost));
+    std::vector<char> e_valid(rows);
+    for (std::uint32_t r = 0; r < rows; ++r) e_valid[r] = eh[r] > 0;
     for (int& e : eh) e = e > 0 ? e - 2048 : 0;
     CIEG_CUDA(cudaMemcpy(pl->rowexp, eh.data(), sizeof(int) * rows, cudaMemcpyHostToDevice));
     unsigned bad_h = 0;
@@ -882,6 +994,40 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     }
     cudaFree(pl->rec);
     pl->rec = nullptr;
+    if (pl->usable) {
+      // neighbour lists and per-panel row / diagonal exponents (host)
+      const std::uint32_t np = m->npanels;
+      std::vector<std::vector<std::uint32_t>> nbs(np);
+      for (const OzItem& it : items) {
+        const std::uint32_t kind = it.flags & 0xffu;
+        if (kind == 0u) {
+          nbs[it.owner].push_back(it.partner);
+          nbs[it.partner].push_back(it.owner | 0x80000000u);
+        } else if (kind == 2u) {
+          nbs[it.owner].push_back(it.owner);
+        }
+      }
+      std::vector<std::uint32_t> off(np + 1, 0), flat;
+      for (std::uint32_t q = 0; q < np; ++q) {
+        flat.insert(flat.end(), nbs[q].begin(), nbs[q].end());
+        off[q + 1] = static_cast<std::uint32_t>(flat.size());
+      }
+      std::vector<float> dh(rows);
+      CIEG_CUDA(cudaMemcpy(dh.data(), pl->diag, sizeof(float) * rows, cudaMemcpyDeviceToHost));
+      std::vector<int> erq(np, INT_MIN / 4), edq(np, INT_MIN / 4);
+      for (std::uint32_t q = 0; q < np; ++q)
+        for (std::uint32_t r = ps[q]; r < ps[q + 1]; ++r) {
+          if (e_valid[r]) erq[q] = std::max(erq[q], eh[r]);
+          if (dh[r] != 0.0f) edq[q] = std::max(edq[q], std::ilogb(dh[r]) + 1);
+        }
+      pl->nb_off = upload(off);
+      pl->nb = upload(flat);
+      pl->erq = upload(erq);
+      pl->edq = upload(edq);
+      CIEG_CUDA(cudaMalloc(&pl->escale, sizeof(int) * np * 16));
+      CIEG_CUDA(cudaMalloc(&pl->yint, sizeof(long long) * np * kTD * 16));
+      CIEG_CUDA(cudaMemset(pl->yint, 0, sizeof(long long) * np * kTD * 16));
+    }
   } catch (...) {
     delete pl;
     throw;
@@ -936,7 +1082,7 @@ void destroy_sliced(cieg_mat* m) {
 }
 
 void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32_t ldx, double* y, std::uint32_t ldy,
-                        std::uint32_t mc, double* partial, unsigned* nonfinite, unsigned launch_id) {
+                        std::uint32_t mc, unsigned* nonfinite, unsigned launch_id) {
   if (!sliced_ready(ctx, m))
     fail(CIEG_ERR_CONFIG, "sliced SpMM needs an unsharded fp32 matrix with 128-row panels and finite values");
   if (mc == 0 || mc > 16) fail(CIEG_ERR_ARGUMENT, "sliced SpMM: 1..16 columns per launch");
@@ -944,14 +1090,16 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
   digitize_kernel<<<m->npanels, 128, 0, ctx->stream>>>(x, ldx, mc, m->panel_start, pl->rowexp, pl->xd, pl->xt,
                                                        nonfinite, launch_id);
   CIEG_CUDA(cudaGetLastError());
+  scales_kernel<<<m->npanels, 32, 0, ctx->stream>>>(pl->nb_off, pl->nb, pl->erq, pl->edq, pl->xd, pl->xt, pl->escale);
+  CIEG_CUDA(cudaGetLastError());
   static const char* trace_path = std::getenv("CIEG_SLICED_TRACE");
   long long* trace = nullptr;
   if (trace_path) {
     CIEG_CUDA(cudaMalloc(&trace, sizeof(long long) * 256 * 16));
     CIEG_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 256 * 16, ctx->stream));
   }
-  SlicedArgs args{pl->items, pl->cta_off, pl->dense, pl->xd, pl->xt, pl->rowexp, pl->diag, x, y, partial,
-                  ldx,       ldy,         mc,        m->row_lo, trace, 0};
+  SlicedArgs args{pl->items, pl->cta_off, pl->dense, pl->xd, pl->xt, pl->rowexp, pl->diag, x,
+                  pl->yint,  pl->escale,  ldx,       mc,     trace,  0};
   static const int ablate = [] {
     const char* e = std::getenv("CIEG_SLICED_ABLATE");
     return e ? std::atoi(e) : 0;
@@ -972,7 +1120,9 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
       std::fclose(f);
     }
   }
-  ctx->launches += 2;
+  yint_to_y_kernel<<<m->npanels, 256, 0, ctx->stream>>>(pl->yint, pl->escale, m->panel_start, y, ldy, mc, m->row_lo);
+  CIEG_CUDA(cudaGetLastError());
+  ctx->launches += 4;
 }
 
 }  // namespace cieg
