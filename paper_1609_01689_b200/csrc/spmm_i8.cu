@@ -436,9 +436,10 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
 // Per (panel, column) bound exponents of Y: |y| < 2^escale. Every
 // contribution to a row of Q is below 2^(e + 7) -- a row part of tile (Q, P):
 // e = max e_r (rows of Q) + ex_P (|h| < 2^e_r, |x_P| < 2^ex_P, 128 terms);
-// a transposed part of tile (P, Q): e = ex'_P (|x_P 2^e_r| < 2^ex'_P); the
-// diagonal term d_r x_r below 2^(max exponent of d in Q + ex_Q) -- and there
-// are cnt of them, so escale = max + ceil(log2(cnt + 1)) + 1 bounds their sum.
+// a transposed part of tile (P, Q): e = ex'_P (|x_P 2^e_r| < 2^ex'_P) -- and
+// there are cnt of them, so escale = max + ceil(log2(cnt + 1)) + 1 bounds
+// their sum. (The diagonal d_r x_r is not in yint: yint_to_y_kernel adds it
+// in fp64, so a row's own diagonal never sets its panel's scale.)
 __global__ void scales_kernel(const std::uint32_t* nb_off, const std::uint32_t* nb, const int* erq, const int* edq,
                               const std::uint8_t* xd, const std::uint8_t* xt, int* escale) {
   const std::uint32_t Q = blockIdx.x;
@@ -453,15 +454,16 @@ __global__ void scales_kernel(const std::uint32_t* nb_off, const std::uint32_t* 
     const std::uint32_t v = nb[t], P = v & 0x7fffffffu;
     e = max(e, (v >> 31) ? xe(xt, P) + 7 : erq[Q] + xe(xd, P) + 7);
   }
-  e = max(e, edq[Q] + xe(xd, Q));
-  if (e < -1000) e = 0;  // no contribution at all (Y rows of Q are zero)
+  (void)edq;               // (the diagonal term is added in fp64 after the conversion)
+  if (e < -1000) e = 0;  // no contribution at all
   escale[Q * 16 + j] = e + (32 - __clz(cnt + 1)) + 1;
 }
 
-// Y = yint 2^(escale - 62) (one rounding, deterministic) for the columns of
-// this call; yint is zeroed for the next call.
+// Y = yint 2^(escale - 62) (one rounding, deterministic) + D X for the
+// columns of this call; yint is zeroed for the next call.
 __global__ void __launch_bounds__(256) yint_to_y_kernel(long long* yint, const int* escale,
-                                                       const std::uint32_t* panel_start, double* y, std::uint32_t ldy,
+                                                       const std::uint32_t* panel_start, const float* diag,
+                                                       const double* x, std::uint32_t ldx, double* y, std::uint32_t ldy,
                                                        std::uint32_t mc, std::uint32_t row_base) {
   __shared__ double t[16][kTD + 1];  // [column][row], transposed through shared memory
   __shared__ double sc[16];
@@ -485,8 +487,12 @@ __global__ void __launch_bounds__(256) yint_to_y_kernel(long long* yint, const i
 #pragma unroll
   for (int u = 0; u < kTD * 16 / 256; ++u) {  // Y rows: coalesced writes
     const int e = tid + 256 * u, r = e >> 4, c = e & 15;
-    if (r < static_cast<int>(rows) && c < static_cast<int>(mc))
-      y[static_cast<std::size_t>(q0 + r - row_base) * ldy + c] = t[c][r];
+    if (r < static_cast<int>(rows) && c < static_cast<int>(mc)) {
+      // + d_r x_r in fp64 (Inf/NaN x: the caller's fix-up adds it)
+      const double xv = x[static_cast<std::size_t>(q0 + r) * ldx + c];
+      y[static_cast<std::size_t>(q0 + r - row_base) * ldy + c] =
+          fma(static_cast<double>(diag[q0 + r]), isfinite(xv) ? xv : 0.0, t[c][r]);
+    }
   }
 }
 
@@ -747,15 +753,6 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
 #pragma unroll
       for (int j = 0; j < 8; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 36), yacc[j]);
       TRACE(i, 10, lane == 0 && warp == 4);
-      if ((it.flags & 0xffu) == 2u && r < prow) {  // d_r x_r in fp64 (Inf/NaN x: the caller's fix-up adds it)
-        const double dr = static_cast<double>(a.diag[it.r0 + r]);
-        const double* xr = a.x + static_cast<std::size_t>(it.r0 + r) * a.ldx + j0;
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const double xv = j0 + j < static_cast<int>(a.mc) ? xr[j] : 0.0;
-          yacc[j] = fma(dr, isfinite(xv) ? xv : 0.0, yacc[j]);
-        }
-      }
       if (((it.flags >> 9) & 1u) && r < prow) {  // the owner's row part, in fixed point, added to yint
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
                                  static_cast<std::size_t>(it.owner) * kTD * 16 + static_cast<std::size_t>(j0) * kTD + r;
@@ -1120,7 +1117,8 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
       std::fclose(f);
     }
   }
-  yint_to_y_kernel<<<m->npanels, 256, 0, ctx->stream>>>(pl->yint, pl->escale, m->panel_start, y, ldy, mc, m->row_lo);
+  yint_to_y_kernel<<<m->npanels, 256, 0, ctx->stream>>>(pl->yint, pl->escale, m->panel_start, pl->diag, x, ldx, y,
+                                                        ldy, mc, m->row_lo);
   CIEG_CUDA(cudaGetLastError());
   ctx->launches += 4;
 }
