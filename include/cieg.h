@@ -86,7 +86,7 @@ int cieg_ctx_set_exact_order(cieg_ctx* ctx, int exact);
  * H and X split into exact 8-bit integer slices (Ozaki scheme), int32
  * accumulators in TMEM, recombined in fp64 -- fp32 H with 128-row panels on
  * unsharded matrices; agrees with the fp64 modes to rounding (~1e-16), not
- * bit for bit. AUTO picks it for widths >= 2 where supported. */
+ * bit for bit. AUTO picks it for widths >= 9 where supported. */
 enum { CIEG_SPMM_AUTO = 0, CIEG_SPMM_OWNER = 1, CIEG_SPMM_SINGLE_PASS = 2, CIEG_SPMM_SLICED = 3 };
 int cieg_ctx_set_spmm_mode(cieg_ctx* ctx, int mode);
 /* The K1 kernel the current mode runs for a 16-column chunk of width m on

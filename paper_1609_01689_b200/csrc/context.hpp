@@ -168,7 +168,7 @@ bool sliced_supported(const cieg_mat* m);
 bool sliced_ready(cieg_ctx* ctx, cieg_mat* m);
 // the mode's choice for width mc (auto: sliced for mc >= kSlicedMinCols)
 bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
-constexpr std::uint32_t kSlicedMinCols = 2;  // measured on config 2: sliced 2.5 / 2.85 ms vs DMMA single pass 2.78 / 2.95 ms at m = 4 / 8; m = 1 stays scalar (2.10 vs 2.31 ms)
+constexpr std::uint32_t kSlicedMinCols = 9;  // config 2 (fixed-point sliced K1): 2.78 / 2.94 ms at m = 4 / 8, the DMMA single pass 2.78 / 2.95 ms -- a tie; m = 16: 2.82 vs 4.92 ms
 // Digitize X and run the sliced kernel: every row of Y written (row parts and
 // transposed parts accumulated in exact fixed point, then converted); the
 // caller runs the tiny-entry and non-finite fix-ups.

@@ -251,6 +251,9 @@ __global__ void __launch_bounds__(kLuThreads) lu_direct_kernel(const __grid_cons
 
 // ------------------------------------------------------------------ FOM
 constexpr int kFomThreads = 256;
+// fom_fast_kernel: 16 warps (each two 8-row m-tiles of the block product);
+// its reductions keep the 16 row lanes of the first 256 threads
+constexpr int kFomFastThreads = 512, kFomWarps = kFomFastThreads / 32, kFomMT = 256 / (8 * kFomWarps);
 constexpr int kFomMaxSteps = 3;
 
 struct FomParams {
@@ -495,8 +498,9 @@ __global__ void __launch_bounds__(kFomThreads) fom_kernel(const __grid_constant_
 constexpr int kFastSC = 20;  // smem row stride of basis / w (doubles), 4 mod 16
 
 __device__ __forceinline__ double fom_col_reduce(double part, double* red, int c_of_t, int rsub, int cc) {
-  // part: this thread's partial for column c_of_t (t & 15), row lane rsub (t >> 4)
-  red[rsub * 16 + c_of_t] = part;
+  // part: this thread's partial for column c_of_t (t & 15), row lane rsub (t >> 4);
+  // threads beyond the first 256 (16 row lanes) only join the barriers
+  if (threadIdx.x < 256) red[rsub * 16 + c_of_t] = part;
   __syncthreads();
   double s = 0.0;
   if (threadIdx.x < 16) {
@@ -511,7 +515,7 @@ __device__ __forceinline__ double fom_col_reduce(double part, double* red, int c
 }
 
 template <bool F32>
-__global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_constant__ FomParams p) {
+__global__ void __launch_bounds__(kFomFastThreads) fom_fast_kernel(const __grid_constant__ FomParams p) {
   extern __shared__ double sm[];
   const std::uint32_t grp = p.groups[blockIdx.x];
   const std::uint32_t r0 = p.bounds[grp];
@@ -541,7 +545,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
 
   // beta_j = ||rhs_j||; basis_0 = rhs / beta (rows >= n zero)
   double part = 0.0;
-  for (int i = trow; i < n; i += 16) {
+  for (int i = trow; i < n && tid < 256; i += 16) {
     const double v = tcol ? p.r[static_cast<std::size_t>(r0 + i) * p.k + jcol] : 0.0;
     part = fma(v, v, part);
   }
@@ -566,30 +570,30 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
   const int mtiles = NP / 8;
   for (int m = 0; m < mmax; ++m) {
     // z = block * v_m on the tensor pipe; warp w owns m-tiles w, w+8, w+16, w+24
-    double acc[4][2][2];
+    double acc[kFomMT][2][2];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < kFomMT; ++a)
 #pragma unroll
       for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     // A fragments (raw storage type) are prefetched three 16-wide k chunks
     // ahead and widened at use, so global latency overlaps the DMMAs
     using Raw = typename std::conditional<F32, float, double>::type;
     const Raw* blk_raw = F32 ? reinterpret_cast<const Raw*>(blk.f) : reinterpret_cast<const Raw*>(blk.d);
-    Raw a0[4][4], a1[4][4];
-    auto load_a = [&](int k0, Raw (&dst)[4][4]) {
+    Raw a0[4][kFomMT], a1[4][kFomMT];
+    auto load_a = [&](int k0, Raw (&dst)[4][kFomMT]) {
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int kk = k0 + 4 * u + q;
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const int mt = warp + 8 * a;
+        for (int a = 0; a < kFomMT; ++a) {
+          const int mt = warp + kFomWarps * a;
           const int i = 8 * mt + g;
           dst[u][a] = (k0 < NP && mt < mtiles && i < n && kk < n) ? __ldg(blk_raw + i + static_cast<std::size_t>(kk) * n)
                                                                   : Raw(0);
         }
       }
     };
-    auto mma_chunk = [&](int k0, const Raw (&src)[4][4]) {
+    auto mma_chunk = [&](int k0, const Raw (&src)[4][kFomMT]) {
       if (k0 >= NP) return;
       double bf[4][2];
 #pragma unroll
@@ -599,14 +603,14 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
 #pragma unroll
       for (int u = 0; u < 4; ++u)
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
+        for (int a = 0; a < kFomMT; ++a) {
           const double av = static_cast<double>(src[u][a]);
 #pragma unroll
           for (int b = 0; b < 2; ++b) dmma_8x8x4(acc[a][b][0], acc[a][b][1], av, bf[u][b]);
         }
     };
     // four 16-wide k chunks in flight (loads three chunks ahead of the DMMAs)
-    Raw a2[4][4], a3[4][4];
+    Raw a2[4][kFomMT], a3[4][kFomMT];
     load_a(0, a0);
     load_a(16, a1);
     load_a(32, a2);
@@ -622,8 +626,8 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
     }
     // w = z - mu v_m
 #pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      const int mt = warp + 8 * a;
+    for (int a = 0; a < kFomMT; ++a) {
+      const int mt = warp + kFomWarps * a;
       if (mt >= mtiles) continue;
       const int i = 8 * mt + g;
 #pragma unroll
@@ -638,14 +642,14 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
     __syncthreads();
     // scale = max(beta, ||w||)
     part = 0.0;
-    for (int i = trow; i < n; i += 16) part = fma(W(i, tc), W(i, tc), part);
+    for (int i = trow; i < n && tid < 256; i += 16) part = fma(W(i, tc), W(i, tc), part);
     const double wn = sqrt(fom_col_reduce(part, red, tc, trow, cc));
     if (tid < 16) scal[tid] = beta[tid] > wn ? beta[tid] : wn;
     // two-pass modified Gram-Schmidt
     for (int pass = 0; pass < 2; ++pass) {
       for (int ib = 0; ib <= m; ++ib) {
         part = 0.0;
-        for (int i = trow; i < n; i += 16) part = fma(B(ib, i, tc), W(i, tc), part);
+        for (int i = trow; i < n && tid < 256; i += 16) part = fma(B(ib, i, tc), W(i, tc), part);
         const double hv = fom_col_reduce(part, red, tc, trow, cc);
         if (tid < 16 && active[tid]) {
           double& hh = hess[tid * 16 + ib + m * 4];
@@ -661,7 +665,7 @@ __global__ void __launch_bounds__(kFomThreads) fom_fast_kernel(const __grid_cons
       }
     }
     part = 0.0;
-    for (int i = trow; i < n; i += 16) part = fma(W(i, tc), W(i, tc), part);
+    for (int i = trow; i < n && tid < 256; i += 16) part = fma(W(i, tc), W(i, tc), part);
     const double nrm = sqrt(fom_col_reduce(part, red, tc, trow, cc));
     if (tid < 16 && active[tid]) {
       steps[tid] = m + 1;
@@ -807,7 +811,7 @@ int precond_apply(cieg_ctx* ctx, const cieg_prec* prec, const double* r, std::ui
       auto fom = prec->blocks32 ? fom_fast_kernel<true> : fom_fast_kernel<false>;
       CIEG_CUDA(cudaFuncSetAttribute(fom, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       dim3 grid(static_cast<unsigned>(large.size()), static_cast<unsigned>((fp.ncols + chunk - 1) / chunk));
-      fom<<<grid, kFomThreads, smem, ctx->stream>>>(fp);
+      fom<<<grid, kFomFastThreads, smem, ctx->stream>>>(fp);
     } else {
       // reference-order path: chunk so that shared memory stays below ~200 KB
       int chunk = 16;
