@@ -144,3 +144,67 @@ def test_dropin_cache_follows_content_not_address(ref_lib):
         rr = ref_lib.lobpcg_solve(rm, x0, 3, 1e-8, 500, ref_lib.RefTileDiagonal(rm, h.groups))
         assert iters.value == rr.iterations
         np.testing.assert_allclose(eig, rr.eigenvalues, rtol=1e-10)
+
+
+CLI_GPU = os.path.join(ROOT, "integration", "_build", "ci_eigen_gpu")
+CLI_REF = os.path.join(ROOT, "integration", "_build", "ci_eigen_ref")
+
+
+def _cli(exe, *args):
+    import subprocess
+
+    p = subprocess.run([exe, *args], capture_output=True, text=True, timeout=600)
+    return p.returncode, p.stdout
+
+
+def _solve_summary(out):
+    lines = out.splitlines()
+    it = next(l for l in lines if l.startswith("solver "))
+    ev = [float(l.split()[-1]) for l in lines if l.startswith("eigenvalue ")]
+    ctr = next(l for l in lines if l.startswith("spmm_calls "))
+    return it, ev, ctr
+
+
+@pytest.mark.parametrize("args", [
+    ["--nucleus", "4He", "--nmax", "4", "--k", "4", "--precond", "tile", "--tol", "1e-8", "--storage", "double"],
+    ["--nucleus", "4He", "--nmax", "4", "--k", "4", "--tol", "1e-8", "--storage", "single"],
+    ["--nucleus", "4He", "--nmax", "4", "--k", "3", "--solver", "lanczos", "--tol", "1e-8", "--storage", "double"],
+    ["--nucleus", "4He", "--nmax", "4", "--k", "2", "--guess", "multilevel", "--levels", "2", "--precond", "tile",
+     "--tol", "1e-8", "--storage", "double"],
+])
+def test_reference_cli_on_the_gpu(tmp_path, args):
+    """The reference's own CLI (proj/tools/ci_eigen.cpp, unmodified; CLI11 API
+    shim) linked against the drop-in: `solve` prints the same iteration
+    count, operation counters and eigenvalues as the same CLI linked against
+    the eleven reference TUs; --history writes the same CSV rows."""
+    if not (os.path.exists(CLI_GPU) and os.path.exists(CLI_REF)):
+        pytest.skip("integration/_build not built (needs the reference sources at build time)")
+    hg, hr = str(tmp_path / "g.csv"), str(tmp_path / "r.csv")
+    rg, og = _cli(CLI_GPU, "solve", *args, "--history", hg)
+    rr, orf = _cli(CLI_REF, "solve", *args, "--history", hr)
+    assert rg == rr, (og, orf)
+    itg, evg, cg = _solve_summary(og)
+    itr, evr, cr = _solve_summary(orf)
+    assert itg == itr and cg == cr, (og, orf)
+    np.testing.assert_allclose(evg, evr, rtol=1e-10, atol=1e-11)
+    lg = open(hg).read().splitlines()
+    lr = open(hr).read().splitlines()
+    assert len(lg) == len(lr) and lg[0] == lr[0]
+
+
+def test_reference_cli_assemble_and_compare(tmp_path):
+    """`assemble` (host code in both builds) writes byte-identical CSB1;
+    `compare` runs the four preconditioner / guess solves per seed on the GPU
+    with the reference's iteration counts."""
+    if not (os.path.exists(CLI_GPU) and os.path.exists(CLI_REF)):
+        pytest.skip("integration/_build not built (needs the reference sources at build time)")
+    a = ["--nucleus", "4He", "--nmax", "4", "--storage", "double"]
+    pg, pr = str(tmp_path / "g.csb"), str(tmp_path / "r.csb")
+    assert _cli(CLI_GPU, "assemble", *a, "--out", pg)[0] == 0
+    assert _cli(CLI_REF, "assemble", *a, "--out", pr)[0] == 0
+    assert open(pg, "rb").read() == open(pr, "rb").read()
+    c = ["--nucleus", "4He", "--nmax", "4", "--k", "2", "--tol", "1e-8", "--seeds", "1,2"]
+    rg, og = _cli(CLI_GPU, "compare", *c)
+    rr, orf = _cli(CLI_REF, "compare", *c)
+    assert rg == rr == 0
+    assert og == orf, (og, orf)
