@@ -105,7 +105,7 @@ struct SlicedPlan {
   double* tiny_val = nullptr;
   // Fixed-point accumulation of every contribution to a panel's rows (the
   // row part and the transposed parts), int64, exact and order-independent:
-  // yint[Q][column][row] in units of 2^(escale[Q][column] - 62). The scales
+  // yint[Q][row quarter][column][32 rows] in units of 2^(escale[Q][column] - 62). The scales
   // are bounds on |Y| per (panel, column), set every call from the X digit
   // exponents of the panel's neighbours (scales_kernel).
   long long* yint = nullptr;
@@ -474,13 +474,13 @@ __global__ void __launch_bounds__(256) yint_to_y_kernel(long long* yint, const i
   if (tid < 16) sc[tid] = pow2(escale[Q * 16 + tid] - 62);
   long long v[kTD * 16 / 256];
 #pragma unroll
-  for (int u = 0; u < kTD * 16 / 256; ++u) v[u] = __ldcg(yi + tid + 256 * u);  // yint is [column][row]: coalesced
+  for (int u = 0; u < kTD * 16 / 256; ++u) v[u] = __ldcg(yi + tid + 256 * u);  // coalesced
 #pragma unroll
   for (int u = 0; u < kTD * 16 / 256; ++u) __stcg(yi + tid + 256 * u, 0ll);   // cleared for the next call
   __syncthreads();
 #pragma unroll
-  for (int u = 0; u < kTD * 16 / 256; ++u) {
-    const int e = tid + 256 * u, c = e / kTD, r = e - c * kTD;
+  for (int u = 0; u < kTD * 16 / 256; ++u) {  // yint is [row quarter][column][32 rows]
+    const int e = tid + 256 * u, c = (e >> 5) & 15, r = ((e >> 9) << 5) | (e & 31);
     t[c][r] = __ll2double_rn(v[u]) * sc[c];
   }
   __syncthreads();
@@ -505,7 +505,7 @@ struct SlicedArgs {
   const int* rowexp;
   const float* diag;
   const double* x;  // the call's X (the diagonal term d_r x_r)
-  long long* yint;     // fixed-point Y, [panel][column][row], units 2^(escale - 62)
+  long long* yint;     // fixed-point Y, [panel][row quarter][column][32 rows], units 2^(escale - 62)
   const int* escale;   // [panel][column]
   std::uint32_t ldx, mc;
   long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
@@ -519,7 +519,6 @@ struct Smem {
   std::uint8_t planes[2][kPlanes];
   std::uint8_t xd[2][kSlab];
   std::uint8_t xt[kSlab];  // the owner panel's slab (one buffer: the row MMAs of an owner's first item cover its load)
-  long long stage[kTD * 16];  // one transposed contribution in fixed point, [column][row], for the bulk reduction
   // the slabs' column exponents, staged with them (4 deep: an epilogue reads
   // an item's exponents before it releases the item's accumulator stage)
   int xd_exp[4][16];
@@ -560,19 +559,8 @@ __device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8]) 
   }
 }
 
-// ---- fixed-point accumulation into yint
-// one transposed contribution (the 16 KB stage) added to yint by the TMA
-// engine (integer adds in L2: exact, order-independent)
-__device__ __forceinline__ void bulk_reduce_add(long long* dst, const long long* src, std::uint32_t bytes) {
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(dst),
-               "r"(umma::smem_u32(src)), "r"(bytes)
-               : "memory");
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-}
-__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-// named barrier of the eight transposed-epilogue warps
-__device__ __forceinline__ void tbar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+// ---- fixed-point accumulation into yint: 64-bit integer adds in L2
+// (red.global.add.u64 -- exact, so the result does not depend on their order)
 // v 2^e rounded to the nearest integer (|result| < 2^62 by the scale bounds)
 __device__ __forceinline__ long long fixp(double v, int e) { return __double2ll_rn(v * pow2(e)); }
 
@@ -690,6 +678,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     if (lane == 0) {
       std::uint32_t k = 0, owners = 0;
       const std::uint64_t stream = umma::createpolicy_evict_first();
+      // the X digit slabs are re-read by every item of the sector band: keep them
+      const std::uint64_t keep = umma::createpolicy_evict_last();
       for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
         const OzItem it = a.items[i];
         const int b = k & 1;
@@ -698,7 +688,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
           umma::mbar_wait(&S.empty_t, (owners & 1u) ^ 1u);
           umma::mbar_arrive_tx(&S.full_t, kSlab + 64);
           const std::uint8_t* src = a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes;
-          umma::bulk_g2s(S.xt, src, kSlab, &S.full_t);
+          umma::bulk_g2s_hint(S.xt, src, kSlab, &S.full_t, keep);
           umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t);
           ++owners;
         }
@@ -706,7 +696,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         TRACE(i, 4, true);
         umma::mbar_arrive_tx(&S.full_a[b], kSlab + 64 + kPlanes);
         const std::uint8_t* xsrc = a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes;
-        umma::bulk_g2s(S.xd[b], xsrc, kSlab, &S.full_a[b]);
+        umma::bulk_g2s_hint(S.xd[b], xsrc, kSlab, &S.full_a[b], keep);
         umma::bulk_g2s(S.xd_exp[k & 3], xsrc + kSlab, 64, &S.full_a[b]);
         const std::uint8_t* src = a.dense + static_cast<std::size_t>((a.ablate & 2) ? 0 : i) * kPlanes;
 #pragma unroll 1
@@ -755,10 +745,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       TRACE(i, 10, lane == 0 && warp == 4);
       if (((it.flags >> 9) & 1u) && r < prow) {  // the owner's row part, in fixed point, added to yint
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
-                                 static_cast<std::size_t>(it.owner) * kTD * 16 + static_cast<std::size_t>(j0) * kTD + r;
+                                 static_cast<std::size_t>(it.owner) * kTD * 16 + eq * 512 + j0 * 32 + lane;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          atomicAdd(yr + j * kTD, static_cast<unsigned long long>(fixp(yacc[j], 62 - osc[j])));
+          atomicAdd(yr + j * 32, static_cast<unsigned long long>(fixp(yacc[j], 62 - osc[j])));
       }
     }
   } else {
@@ -795,17 +785,15 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
       TRACE(i, 15, lane == 0 && warp == 12);
       if (!trans || (a.ablate & 1)) continue;
-      if (gt == 0) bulk_wait_read();  // the previous contribution has left the stage
-      tbar();
-      const bool in = c < static_cast<int>(it.orow);
+      if (c < static_cast<int>(it.orow)) {  // the contribution to the partner's rows, in fixed point
+        unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
+                                 static_cast<std::size_t>(it.partner) * kTD * 16 + eq * 512 + j0 * 32 + lane;
 #pragma unroll
-      for (int j = 0; j < 8; ++j)
-        S.stage[(j0 + j) * kTD + c] = in ? fixp(v[j], ex[j] - 36 + 62 - psc[j]) : 0ll;
-      umma::fence_async_smem();
-      tbar();
-      if (gt == 0) bulk_reduce_add(a.yint + static_cast<std::size_t>(it.partner) * kTD * 16, S.stage, kTD * 16 * 8);
+        for (int j = 0; j < 8; ++j)
+          atomicAdd(yr + j * 32, static_cast<unsigned long long>(fixp(v[j], ex[j] - 36 + 62 - psc[j])));
+      }
     }
-    if (gt == 0) bulk_wait_all();
+
   }
   umma::fence_before();
   __syncthreads();
