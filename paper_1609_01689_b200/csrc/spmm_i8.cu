@@ -518,12 +518,12 @@ struct SlicedArgs {
 struct Smem {
   std::uint8_t planes[2][kPlanes];
   std::uint8_t xd[2][kSlab];
-  std::uint8_t xt[kSlab];  // the owner panel's slab (one buffer: the row MMAs of an owner's first item cover its load)
+  std::uint8_t xt[2][kSlab];  // the owner panels' slabs (the next owner's is loaded while the current one's items run)
   // the slabs' column exponents, staged with them (4 deep: an epilogue reads
   // an item's exponents before it releases the item's accumulator stage)
   int xd_exp[4][16];
   int xt_exp[4][16];
-  std::uint64_t full_a[2], empty_a[2], full_t, empty_t, acc_full[2], acc_empty[2];
+  std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2];
   std::uint32_t tmem;
 };
 
@@ -590,8 +590,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       umma::mbar_init(&S.acc_full[b], 1);
       umma::mbar_init(&S.acc_empty[b], kEpiWarps);
     }
-    umma::mbar_init(&S.full_t, 1);
-    umma::mbar_init(&S.empty_t, 1);
+    for (int b = 0; b < 2; ++b) {
+      umma::mbar_init(&S.full_t[b], 1);
+      umma::mbar_init(&S.empty_t[b], 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) umma::tmem_alloc<512>(&S.tmem);
@@ -623,7 +625,8 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     const std::uint64_t a_k0 = umma::sdesc(umma::smem_u32(S.planes[0]), 128, 1024);   // A K-major (H X)
     const std::uint64_t a_mn0 = umma::sdesc(umma::smem_u32(S.planes[0]), 1024, 128);  // A MN-major (H^T X)
     const std::uint64_t b_d0 = umma::sdesc(umma::smem_u32(S.xd[0]), 128, 1024);
-    const std::uint64_t bt = umma::sdesc(umma::smem_u32(S.xt), 128, 1024);
+    const std::uint64_t b_t0 = umma::sdesc(umma::smem_u32(S.xt[0]), 128, 1024);
+    int o = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
       const OzItem it = a.items[i];
       const int b = k & 1;
@@ -649,10 +652,12 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
                             (s | ks) != 0);
       }
       if ((it.flags >> 8) & 1u) {
-        umma::mbar_wait(&S.full_t, owners & 1u);
+        o = owners & 1;
+        umma::mbar_wait(&S.full_t[o], (owners >> 1) & 1u);
         ++owners;
         umma::fence_after();
       }
+      const std::uint64_t bt = b_t0 + static_cast<std::uint64_t>(o * (kSlab >> 4));
       if (trans) {
 #pragma unroll 1
         for (int s = 0; s < kAS; ++s) {
@@ -666,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       }
       umma::commit_warp(&S.empty_a[b]);
       umma::commit_warp(&S.acc_full[b]);
-      if ((it.flags >> 9) & 1u) umma::commit_warp(&S.empty_t);
+      if ((it.flags >> 9) & 1u) umma::commit_warp(&S.empty_t[o]);
       TRACE(i, 3, lane == 0);
     }
   } else if (warp == 1) {
@@ -684,12 +689,13 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         const OzItem it = a.items[i];
         const int b = k & 1;
         TRACE(i, 8, true);
-        if ((it.flags >> 8) & 1u) {  // (the previous owner's MMAs read the slab until empty_t)
-          umma::mbar_wait(&S.empty_t, (owners & 1u) ^ 1u);
-          umma::mbar_arrive_tx(&S.full_t, kSlab + 64);
+        if ((it.flags >> 8) & 1u) {  // (the owner before last read this buffer until empty_t)
+          const int o = owners & 1;
+          umma::mbar_wait(&S.empty_t[o], ((owners >> 1) & 1u) ^ 1u);
+          umma::mbar_arrive_tx(&S.full_t[o], kSlab + 64);
           const std::uint8_t* src = a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes;
-          umma::bulk_g2s_hint(S.xt, src, kSlab, &S.full_t, keep);
-          umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t);
+          umma::bulk_g2s_hint(S.xt[o], src, kSlab, &S.full_t[o], keep);
+          umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t[o]);
           ++owners;
         }
         umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
