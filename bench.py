@@ -858,10 +858,11 @@ def ours(args):
         gb = lambda t: round(nbytes / (t * 1e-3) / 1e9, 3)
         e2e = {"value": gb(ms_e2e), "unit": "GB/s", "h2d_bytes_per_step": n * m * 8, "d2h_bytes_per_step": n * m * 8,
                "ms_per_step": round(ms_e2e, 4), "wall_ms_per_step": round(wall_e2e, 4), "steps": ke,
-               "call": "cieg_spmm_host per step on pageable host X/U (ci::spmm's call in the drop-in; chunked "
-                       "pinned staging ring inside the library)",
+               "call": "cieg_spmm_host per step on pageable host X/U (ci::spmm's call in the drop-in; inside the "
+                       "library the upload, the sliced kernels and the download are pipelined over row chunks "
+                       "through pinned staging rings)",
                "pinned": {"value": gb(ms_single), "ms_per_step": round(ms_single, 4),
-                          "call": "cieg_spmm_host per step, pinned host X/U"},
+                          "call": "cieg_spmm_host per step, pinned host X/U (the same chunk pipeline, no staging copies)"},
                "pinned_batch": {"value": gb(ms_batch), "ms_per_step": round(ms_batch, 4),
                                 "call": "cieg_spmm_host_batch (pinned; copies of neighbouring steps overlap K1)"}}
     else:

@@ -4,6 +4,9 @@
 
 #include <algorithm>
 #include <cstring>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 #include <memory>
 #include <string>
 
@@ -148,6 +151,10 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   for (auto& b : ctx->solver_pool) b.release();
   ctx->pinned_small.release();
   ctx->pinned_stage.release();
+  ctx->pinned_stage_down.release();
+  for (auto& e : ctx->pipe_ev) cudaEventDestroy(e);
+  if (ctx->pipe_up) cudaStreamDestroy(ctx->pipe_up);
+  if (ctx->pipe_down) cudaStreamDestroy(ctx->pipe_down);
   cieg::destroy_nccl(ctx);
   for (auto& e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
@@ -480,12 +487,48 @@ bool host_pinned(const void* p) {
 
 // Host copy of one staging chunk, split over the OpenMP threads.
 void par_copy(void* dst, const void* src, std::size_t bytes) {
-  constexpr std::size_t kPiece = 1u << 20;
+  constexpr std::size_t kPiece = 256u << 10;  // (an 8 MB staging chunk keeps every thread busy)
   const std::int64_t pieces = static_cast<std::int64_t>((bytes + kPiece - 1) / kPiece);
 #pragma omp parallel for schedule(static) if (pieces > 1)
   for (std::int64_t i = 0; i < pieces; ++i) {
     const std::size_t o = static_cast<std::size_t>(i) * kPiece;
     std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kPiece, bytes - o));
+  }
+}
+
+// The same with non-temporal stores: the copy out of the pinned ring into the
+// caller's U (hundreds of MB, not read again soon) skips the read-for-ownership
+// of the destination lines and leaves the cache to the staging rings.
+void stream_piece(char* dst, const char* src, std::size_t bytes) {
+#if defined(__SSE2__)
+  const std::size_t head = std::min(bytes, (16 - (reinterpret_cast<std::uintptr_t>(dst) & 15)) & 15);
+  std::memcpy(dst, src, head);
+  dst += head, src += head, bytes -= head;
+  const std::size_t body = bytes & ~static_cast<std::size_t>(63);
+  for (std::size_t o = 0; o < body; o += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + o));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + o + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + o + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + o + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + o), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + o + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + o + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + o + 48), d);
+  }
+  _mm_sfence();
+  std::memcpy(dst + body, src + body, bytes - body);
+#else
+  std::memcpy(dst, src, bytes);
+#endif
+}
+
+void par_copy_stream(void* dst, const void* src, std::size_t bytes) {
+  constexpr std::size_t kPiece = 256u << 10;
+  const std::int64_t pieces = static_cast<std::int64_t>((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) if (pieces > 1)
+  for (std::int64_t i = 0; i < pieces; ++i) {
+    const std::size_t o = static_cast<std::size_t>(i) * kPiece;
+    stream_piece(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, std::min(kPiece, bytes - o));
   }
 }
 
@@ -531,7 +574,7 @@ void download_staged(cieg_ctx* ctx, void* dst, const void* src, std::size_t byte
     const int slot = static_cast<int>(c % kStageSlots);
     const std::size_t off = c * kStageChunk, len = std::min(kStageChunk, bytes - off);
     CIEG_CUDA(cudaEventSynchronize(ctx->stage_ev[slot]));
-    par_copy(static_cast<char*>(dst) + off, ring + slot * kStageChunk, len);
+    par_copy_stream(static_cast<char*>(dst) + off, ring + slot * kStageChunk, len);
     if (c + kStageSlots < chunks) issue(c + kStageSlots);
   }
 }
@@ -550,14 +593,19 @@ int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, dou
     const std::size_t ybytes = static_cast<std::size_t>(mat->row_hi - mat->row_lo) * m * sizeof(double);
     if (xbytes == 0) return;
     if (!x_host || !y_host) cieg::fail(CIEG_ERR_ARGUMENT, "cieg_spmm_host: null vector");
+    CIEG_CUDA(cudaSetDevice(ctx->device));
+    const bool x_pinned = host_pinned(x_host), y_pinned = host_pinned(y_host);
+    // the sliced kernel: upload, kernels and download pipelined over row chunks
+    if (m <= 16 && cieg::sliced_spmm_host(ctx, const_cast<cieg_mat*>(mat), x_host, y_host, m, x_pinned, y_pinned, par_copy, par_copy_stream))
+      return;
     double* dx = static_cast<double*>(ctx->scratch_x.get(xbytes));
     double* dy = static_cast<double*>(ctx->scratch_y.get(ybytes));
-    if (host_pinned(x_host))
+    if (x_pinned)
       CIEG_CUDA(cudaMemcpyAsync(dx, x_host, xbytes, cudaMemcpyHostToDevice, ctx->stream));
     else
       upload_staged(ctx, dx, x_host, xbytes);
     cieg::launch_spmm(ctx, mat, dx, m, dy, m, m);
-    if (host_pinned(y_host))
+    if (y_pinned)
       CIEG_CUDA(cudaMemcpyAsync(y_host, dy, ybytes, cudaMemcpyDeviceToHost, ctx->stream));
     else
       download_staged(ctx, y_host, dy, ybytes);

@@ -80,6 +80,10 @@ struct cieg_ctx {
   cieg::PinnedBuf pinned_small;
   cieg::PinnedBuf pinned_stage;         // pageable host X/U: chunked staging ring (capi.cu)
   cudaEvent_t stage_ev[4] = {};
+  // the chunk-pipelined host SpMM (spmm_i8.cu sliced_spmm_host): copy streams, the download ring, an event pool
+  cudaStream_t pipe_up = nullptr, pipe_down = nullptr;
+  cieg::PinnedBuf pinned_stage_down;
+  std::vector<cudaEvent_t> pipe_ev;
   // phase timers (report.hpp Clock): event pairs read at the end of a solve,
   // so timing a phase does not synchronise the host with the device
   struct ClockRec {
@@ -168,13 +172,24 @@ bool sliced_supported(const cieg_mat* m);
 bool sliced_ready(cieg_ctx* ctx, cieg_mat* m);
 // the mode's choice for width mc (auto: sliced for mc >= kSlicedMinCols)
 bool sliced_rule(const cieg_ctx* ctx, const cieg_mat* m, std::uint32_t mc);
-constexpr std::uint32_t kSlicedMinCols = 9;  // config 2 (fixed-point sliced K1): 2.78 / 2.94 ms at m = 4 / 8, the DMMA single pass 2.78 / 2.95 ms -- a tie; m = 16: 2.82 vs 4.92 ms
+constexpr std::uint32_t kSlicedMinCols = 2;  // config 2, sliced vs the DMMA / scalar single pass: m = 1 2.37 vs 2.10 ms; m = 4 2.41 vs 2.79; m = 8 2.43 vs 2.95; m = 16 2.59 vs 4.95
 // Digitize X and run the sliced kernel: every row of Y written (row parts and
 // transposed parts accumulated in exact fixed point, then converted); the
 // caller runs the tiny-entry and non-finite fix-ups.
 void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
                         std::uint32_t ldy, std::uint32_t mc, unsigned* nonfinite, unsigned launch_id);
 void destroy_sliced(cieg_mat* m);
+// ci::spmm's host call on the sliced kernel, pipelined over row chunks (upload,
+// kernels and download overlap); false when the sliced kernel does not apply
+// (the caller then runs upload -> launch_spmm -> download). `copy` / `copy_out` =
+// the caller's threaded host copies into / out of the pinned rings (pageable buffers).
+bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* y_host, std::uint32_t mc,
+                      bool x_pinned, bool y_pinned, void (*copy)(void*, const void*, std::size_t),
+                      void (*copy_out)(void*, const void*, std::size_t));
+// K1's non-finite-input flag and the fix-up of the launch tagged launch_id
+unsigned* nonfinite_flag(cieg_ctx* ctx);
+void launch_nonfinite_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
+                          std::uint32_t ldy, std::uint32_t mc, unsigned launch_id);
 // the K1 mode launch_spmm runs for width mc (CIEG_SPMM_OWNER / SINGLE_PASS / SLICED)
 int spmm_effective_mode(cieg_ctx* ctx, cieg_mat* m, std::uint32_t mc);
 // NCCL data plane (nccl_plane.cu)

@@ -1015,6 +1015,55 @@ unsigned* nonfinite_flag(cieg_ctx* ctx) {
   return f;
 }
 
+namespace {
+// the Inf/NaN fix-up of the K1 launch described by args (exits at once when
+// that launch's flag is clear; forced on a single-pass shard)
+void launch_nonfinite_fix_args(cieg_ctx* ctx, const cieg_mat* m, const SpmmArgs& args, bool force) {
+  // owned panels of this (shard) matrix
+  const auto& ps = m->panel_start_host;
+  const std::uint32_t p_lo = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_lo) - ps.begin());
+  const std::uint32_t p_hi = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_hi) - ps.begin());
+  const int prec = m->precision;
+  if (prec == 0)
+    nonfinite_fix_kernel<float><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
+                                                                        m->halo_lo, m->halo_hi, force ? 1 : 0);
+  else
+    nonfinite_fix_kernel<double><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
+                                                                         m->halo_lo, m->halo_hi, force ? 1 : 0);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+SpmmArgs make_args(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y, std::uint32_t ldy,
+                   std::uint32_t mc, unsigned launch_id) {
+  return SpmmArgs{m->panel_start,
+                  m->work_off,
+                  m->work_tile,
+                  m->work_other,
+                  m->work_kind,
+                  m->sched_off,
+                  reinterpret_cast<const uint4*>(m->sched),
+                  m->tile_off,
+                  m->idx,
+                  m->val,
+                  x,
+                  y,
+                  ldx,
+                  ldy,
+                  mc,
+                  m->npanels,
+                  m->row_lo,
+                  nonfinite_flag(ctx),
+                  launch_id,
+                  nullptr};
+}
+}  // namespace
+
+void launch_nonfinite_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
+                          std::uint32_t ldy, std::uint32_t mc, unsigned launch_id) {
+  launch_nonfinite_fix_args(ctx, m, make_args(ctx, m, x, ldx, y, ldy, mc, launch_id), false);
+}
+
 void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,
                  std::uint32_t ldy, std::uint32_t mcols, double* yhalo, std::uint32_t ldh, bool shard_single_pass) {
   if (mcols == 0 || m->dim == 0) return;
@@ -1027,26 +1076,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
                                 ctx->stream));
   for (std::uint32_t c0 = 0; c0 < mcols; c0 += 16) {
     const std::uint32_t mc = std::min<std::uint32_t>(16, mcols - c0);
-    SpmmArgs args{m->panel_start,
-                  m->work_off,
-                  m->work_tile,
-                  m->work_other,
-                  m->work_kind,
-                  m->sched_off,
-                  reinterpret_cast<const uint4*>(m->sched),
-                  m->tile_off,
-                  m->idx,
-                  m->val,
-                  x + c0,
-                  y + c0,
-                  ldx,
-                  ldy,
-                  mc,
-                  m->npanels,
-                  m->row_lo,
-                  nonfinite_flag(ctx),
-                  ++ctx->spmm_launch_id,
-                  nullptr};
+    SpmmArgs args = make_args(ctx, m, x + c0, ldx, y + c0, ldy, mc, ++ctx->spmm_launch_id);
     const bool sliced = !shard && sliced_rule(ctx, m, mc) && sliced_ready(ctx, const_cast<cieg_mat*>(m));
     const bool sp = !sliced && (shard ? shard_sp : single_pass_default(ctx, m, mc));
     if (sp) {
@@ -1073,19 +1103,7 @@ void launch_spmm(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_
       ++ctx->launches;
     }
     if (sliced) launch_sliced_tiny_fix(ctx, m, x + c0, ldx, y + c0, ldy, mc);
-    // owned panels of this (shard) matrix
-    const auto& ps = m->panel_start_host;
-    const std::uint32_t p_lo = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_lo) - ps.begin());
-    const std::uint32_t p_hi = static_cast<std::uint32_t>(std::lower_bound(ps.begin(), ps.end(), m->row_hi) - ps.begin());
-    const int prec = m->precision;
-    if (prec == 0)
-      nonfinite_fix_kernel<float><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
-                                                                          m->halo_lo, m->halo_hi, shard_sp ? 1 : 0);
-    else
-      nonfinite_fix_kernel<double><<<ctx->sm_count, 256, 0, ctx->stream>>>(args, m->tile_edge, prec, p_lo, p_hi,
-                                                                           m->halo_lo, m->halo_hi, shard_sp ? 1 : 0);
-    CIEG_CUDA(cudaGetLastError());
-    ++ctx->launches;
+    launch_nonfinite_fix_args(ctx, m, args, shard_sp);
   }
 }
 

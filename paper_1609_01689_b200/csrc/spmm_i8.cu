@@ -15,10 +15,13 @@
 //     five balanced signed 8-bit digits.
 //     The diagonal is not sliced (its d_r x_r is added in fp64), so e_r is
 //     the off-diagonal scale of the row.
-//     Built once per matrix on the device (records_kernel): one 8-byte record
-//     per stored entry = its position in the 128 x 128 core-matrix tile layout
-//     (umma.cuh) + the five slice bytes -- the same 8 bytes per entry as the
-//     fp32 value + packed index of the DMMA stream.
+//     Built once per matrix on the device: records_kernel writes one 8-byte
+//     record per stored entry (its position in the 128 x 128 core-matrix tile
+//     layout of umma.cuh + the five slice bytes), dense_kernel scatters them
+//     into every item's five dense slice planes (5 x 16 KB, zeros included)
+//     and the records are dropped. Entries too small for their row's slices
+//     go to an fp64 list (tiny_fix_kernel), so every stored value enters
+//     exactly.
 //   * X: per 128-row panel and column, x = x_int * 2^(ex - 54), |x_int| <= 2^54,
 //     as seven balanced signed 8-bit digits (digitize_kernel, every call). For
 //     the transposed product the row scale 2^e_r is folded into X first, so
@@ -27,36 +30,48 @@
 //     A_s X_t: one MMA per H slice s computes all its diagonals at once (B =
 //     digits 0 .. min(6, 7-s), D columns from 16 s), diagonals d <= 7 are kept
 //     (the dropped terms are below 2^-58 of max|a| max|x| per product), each
-//     D_d is an exact int32 over the 128-long tile dot product, and the
-//     epilogue recombines sum_d D_d 2^(-8 d) in fp64 and scales by
-//     2^(e_r + ex - 12).
+//     D_d is an exact int32 over the 128-long tile dot product; the epilogue
+//     recombines the diagonals exactly in int64 (two groups of four, joined
+//     in fp64 with one rounding).
+//   * Y: every contribution to a panel's rows -- the owner's row part (kept in
+//     fp64 registers over the owner's items) and the transposed parts of the
+//     tiles below it -- is converted to fixed point (int64, units of
+//     2^(escale - 62), escale a bound on |Y| per (panel, column) set every
+//     call by scales_kernel from the neighbours' X exponents) and added to
+//     yint with 64-bit integer reds: exact, so the sum does not depend on the
+//     order of the additions -- deterministic without slots, tickets or a
+//     second reduction pass. yint_to_y_kernel converts (one rounding), adds the
+//     diagonal term d_r x_r in fp64 and clears yint for the next call.
 // The result agrees with the fp64 reference to rounding (tests compare at
 // 1e-13 relative), but its rounding is not the DMMA kernels': this mode is
 // selected per width (cieg_ctx_set_spmm_mode, CIEG_SPMM_SLICED).
 //
-// Schedule: the single-pass item list (tiling.cpp): one item per stored tile
-// of its row panel, items of an owner panel consecutive. The row part
-// accumulates in fp64 registers of the owner's epilogue warps and is written
-// once; the transposed part goes to the item's partial slot, added to its
-// block column by sp_reduce_kernel in a fixed order (spmm.cu) -- no atomics,
-// deterministic. Diagonal tiles are stored mirrored (both triangles) and use
-// the row part only.
+// Schedule: the single-pass item list (tiling.cpp), one item per stored tile
+// of its row panel, items of an owner panel consecutive; owner panels dealt
+// to the CTAs in ascending order (least-loaded CTA first), so the grid sweeps
+// the matrix front to back. Diagonal tiles are stored mirrored (both
+// triangles) and use the row part only.
 //
-// CTA (one per SM, 512 threads):
+// CTA (one per SM, 18 warps):
 //   warp 0      TMEM allocation; one lane issues the MMAs (40 per tile)
-//   warps 1-7   producers: zero a slice buffer, scatter the item's records
-//               (5 byte stores each, bank-ordered at build), bulk-copy the X
-//               digit slabs (cp.async.bulk, mbarrier complete_tx)
-//   warps 8-11  row epilogue (TMEM lanes = tile rows): recombine, accumulate
-//   warps 12-15 transposed epilogue (TMEM lanes = tile columns): partials
-// Two slice buffers, two owner slabs, two TMEM accumulator stages, all handed
+//   warp 1      one lane issues the bulk copies (cp.async.bulk, mbarrier
+//               complete_tx): the item's planes (evict-first), the partner's
+//               and the owner's X digit slabs (evict-last), their exponents
+//   warps 2-17  epilogue, four per TMEM lane quarter: row part columns 0-7 /
+//               8-15, transposed part columns 0-7 / 8-15
+// Two plane buffers, two owner slabs, two TMEM accumulator stages, all handed
 // over with mbarriers (tcgen05.commit for the MMA side).
+//
+// The host call (sliced_spmm_host, ci::spmm's path in the drop-in) runs the
+// same kernels over chunks of owner panels, pipelined with the upload of X
+// and the download of U (see there).
 #include <algorithm>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <vector>
 
 #include "context.hpp"
@@ -77,6 +92,13 @@ constexpr int kSlab = kNB * kTD;           // 14336: X digits of one panel
 constexpr int kSlabBytes = kSlab + 64;     // + 16 int32 exponents
 constexpr int kStageCols = 2 * kND;        // TMEM columns per accumulator stage (row + transposed)
 constexpr std::uint16_t kNoEntry = 0xffff;
+// Sparse lowest slice: digit 4 (weight 2^0) is non-zero only for entries below
+// 2^-7 of their row scale -- ~2 % of the generator's entries -- so its plane is
+// kept as a per-item list (position | digit << 16, at most kL4Cap entries) and
+// scattered into a zero plane in shared memory by the copy warp instead of
+// being streamed dense (64.5 KB per item instead of 80 KB). A matrix with a
+// fuller lowest slice keeps the five dense planes.
+constexpr int kL4Cap = 512;
 
 struct OzItem {
   std::uint64_t rec0;   // first record
@@ -94,7 +116,9 @@ struct SlicedPlan {
   OzItem* items = nullptr;
   std::uint32_t* cta_off = nullptr;
   uint2* rec = nullptr;
-  std::uint8_t* dense = nullptr;  // dense mode: every item's five slice planes (kPlanes bytes), TMA-loaded
+  std::uint8_t* dense = nullptr;  // every item's dense slice planes (five, or four with the sparse lowest slice), TMA-loaded
+  std::uint32_t* list4 = nullptr;  // sparse lowest slice: kL4Cap entries per item (OzItem.pad = the item's count)
+  bool sparse4 = false;
   int* rowexp = nullptr;
   float* diag = nullptr;  // stored diagonal of H (applied in fp64, not sliced)
   std::uint8_t* xd = nullptr;                 // per-call digit slabs, npanels * kSlabBytes
@@ -116,12 +140,25 @@ struct SlicedPlan {
   int* edq = nullptr;  // per panel: max exponent of its stored diagonal
   std::uint64_t nrec = 0;
   std::uint32_t ctas = 0;
+  // host copies for the chunked host call (sliced_spmm_host): the items'
+  // owner panels in schedule order, the CTA ranges, the tiny rows, and per
+  // panel the prefix maximum of its highest neighbour panel (a panel's
+  // scales need the digits of all its neighbours; its rows are final once
+  // every owner up to that neighbour has run)
+  std::vector<std::uint32_t> item_owner_host, cta_off_host, tiny_rows_host, nb_prefix_max;
+  struct Chunks {
+    std::vector<std::uint32_t> panel;  // chunk c = owner panels [panel[c], panel[c + 1])
+    std::uint32_t* cta_lim = nullptr;  // device [(chunks + 1) * ctas]: CTA b runs items [c * ctas + b], [(c + 1) * ctas + b])
+  };
+  std::vector<Chunks> chunkings;
   bool usable = true;  // every stored value finite and the planes fit (else the DMMA kernels run)
   ~SlicedPlan() {
+    for (auto& c : chunkings) cudaFree(c.cta_lim);
     cudaFree(items);
     cudaFree(cta_off);
     cudaFree(rec);
     cudaFree(dense);
+    cudaFree(list4);
     cudaFree(rowexp);
     cudaFree(diag);
     cudaFree(xd);
@@ -293,12 +330,12 @@ __global__ void records_kernel(const OzItem* items, const std::uint32_t* sp_sche
 // Dense mode: every item's records scattered once into its five slice planes
 // in HBM (kPlanes bytes per item, zeros included), so the SpMM streams them
 // with bulk copies instead of scattering records every call.
-__global__ void dense_kernel(const OzItem* items, const uint2* rec, std::uint8_t* dense) {
+__global__ void dense_kernel(const OzItem* items, const uint2* rec, std::uint8_t* dense, int nplanes) {
   const std::uint32_t i = blockIdx.x;
   const OzItem it = items[i];
-  std::uint8_t* d = dense + static_cast<std::size_t>(i) * kPlanes;
+  std::uint8_t* d = dense + static_cast<std::size_t>(i) * nplanes * kPlane;
   uint4* d4 = reinterpret_cast<uint4*>(d);
-  for (int u = threadIdx.x; u < kPlanes / 16; u += blockDim.x) d4[u] = make_uint4(0, 0, 0, 0);
+  for (int u = threadIdx.x; u < nplanes * kPlane / 16; u += blockDim.x) d4[u] = make_uint4(0, 0, 0, 0);
   __syncthreads();
   for (std::uint32_t k = threadIdx.x; k < it.nrec; k += blockDim.x) {
     const uint2 r = rec[it.rec0 + k];
@@ -308,7 +345,31 @@ __global__ void dense_kernel(const OzItem* items, const uint2* rec, std::uint8_t
     d[pos + kPlane] = static_cast<std::uint8_t>(r.x >> 24);
     d[pos + 2 * kPlane] = static_cast<std::uint8_t>(r.y);
     d[pos + 3 * kPlane] = static_cast<std::uint8_t>(r.y >> 8);
-    d[pos + 4 * kPlane] = static_cast<std::uint8_t>(r.y >> 16);
+    if (nplanes == kAS) d[pos + 4 * kPlane] = static_cast<std::uint8_t>(r.y >> 16);
+  }
+}
+
+// The lowest slice of every item as a list (position | digit << 16; the order
+// within an item does not matter: positions are distinct). The item's count
+// goes to its descriptor; *over is set when an item exceeds kL4Cap.
+__global__ void list4_kernel(OzItem* items, const uint2* rec, std::uint32_t* list4, unsigned* over) {
+  __shared__ unsigned cnt;
+  const std::uint32_t i = blockIdx.x;
+  const OzItem it = items[i];
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  std::uint32_t* l = list4 + static_cast<std::size_t>(i) * kL4Cap;
+  for (std::uint32_t k = threadIdx.x; k < it.nrec; k += blockDim.x) {
+    const uint2 r = rec[it.rec0 + k];
+    const std::uint32_t pos = r.x & 0xffffu, d4 = (r.y >> 16) & 0xffu;
+    if (pos >= static_cast<std::uint32_t>(kPlane) || d4 == 0) continue;
+    const unsigned t = atomicAdd(&cnt, 1u);
+    if (t < static_cast<unsigned>(kL4Cap)) l[t] = pos | (d4 << 16);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    items[i].pad = min(cnt, static_cast<unsigned>(kL4Cap));
+    if (cnt > static_cast<unsigned>(kL4Cap)) *over = 1u;
   }
 }
 
@@ -347,11 +408,11 @@ __device__ __forceinline__ int exp_mq(long long m, int q) {
 __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uint32_t ldx, std::uint32_t mc,
                                                        const std::uint32_t* panel_start, const int* rowexp,
                                                        std::uint8_t* xd, std::uint8_t* xt, unsigned* nonfinite,
-                                                       unsigned launch_id) {
+                                                       unsigned launch_id, std::uint32_t p_base) {
   __shared__ __align__(16) std::uint8_t sd[2][kSlab];
   __shared__ int wmax[2][8][16];
   __shared__ int cmax[2][16];
-  const std::uint32_t P = blockIdx.x, p0 = panel_start[P], rows = panel_start[P + 1] - p0;
+  const std::uint32_t P = blockIdx.x + p_base, p0 = panel_start[P], rows = panel_start[P + 1] - p0;
   const int tid = threadIdx.x, j = tid & 15, g = tid >> 4;
   long long mv[16];
   int qv[16], er[16];
@@ -441,8 +502,8 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
 // their sum. (The diagonal d_r x_r is not in yint: yint_to_y_kernel adds it
 // in fp64, so a row's own diagonal never sets its panel's scale.)
 __global__ void scales_kernel(const std::uint32_t* nb_off, const std::uint32_t* nb, const int* erq, const int* edq,
-                              const std::uint8_t* xd, const std::uint8_t* xt, int* escale) {
-  const std::uint32_t Q = blockIdx.x;
+                              const std::uint8_t* xd, const std::uint8_t* xt, int* escale, std::uint32_t q_base) {
+  const std::uint32_t Q = blockIdx.x + q_base;
   const int j = threadIdx.x;
   if (j >= 16) return;
   auto xe = [&](const std::uint8_t* slabs, std::uint32_t P) {
@@ -464,10 +525,10 @@ __global__ void scales_kernel(const std::uint32_t* nb_off, const std::uint32_t* 
 __global__ void __launch_bounds__(256) yint_to_y_kernel(long long* yint, const int* escale,
                                                        const std::uint32_t* panel_start, const float* diag,
                                                        const double* x, std::uint32_t ldx, double* y, std::uint32_t ldy,
-                                                       std::uint32_t mc, std::uint32_t row_base) {
+                                                       std::uint32_t mc, std::uint32_t row_base, std::uint32_t q_base) {
   __shared__ double t[16][kTD + 1];  // [column][row], transposed through shared memory
   __shared__ double sc[16];
-  const std::uint32_t Q = blockIdx.x;
+  const std::uint32_t Q = blockIdx.x + q_base;
   const std::uint32_t q0 = panel_start[Q], rows = panel_start[Q + 1] - q0;
   long long* yi = yint + static_cast<std::size_t>(Q) * kTD * 16;
   const int tid = threadIdx.x;
@@ -498,8 +559,10 @@ __global__ void __launch_bounds__(256) yint_to_y_kernel(long long* yint, const i
 
 struct SlicedArgs {
   const OzItem* items;
-  const std::uint32_t* cta_off;
-  const std::uint8_t* dense;  // every item's five slice planes (kPlanes bytes)
+  const std::uint32_t* cta_beg;  // per CTA: its items [cta_beg[b], cta_end[b]) of this launch
+  const std::uint32_t* cta_end;
+  const std::uint8_t* dense;  // every item's dense slice planes (five, or four + list4)
+  const std::uint32_t* list4;
   const std::uint8_t* xd;
   const std::uint8_t* xt;
   const int* rowexp;
@@ -523,7 +586,9 @@ struct Smem {
   // an item's exponents before it releases the item's accumulator stage)
   int xd_exp[4][16];
   int xt_exp[4][16];
+  std::uint32_t list4[4][kL4Cap];  // sparse lowest slice: the lists of four consecutive items (bulk-copy targets, 16-byte aligned)
   std::uint64_t full_a[2], empty_a[2], full_t[2], empty_t[2], acc_full[2], acc_empty[2];
+  std::uint64_t full_l[4];
   std::uint32_t tmem;
 };
 
@@ -536,7 +601,8 @@ __device__ __forceinline__ double l2d(long long v) {
 // (8 columns of this warp's 32 lanes): the diagonals are combined exactly in
 // int64 in two groups of four (|D_d| < 2^24, so each group is below 2^49) and
 // the two groups are joined in fp64 with a single rounding.
-__device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8]) {
+template <typename Release>
+__device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8], Release release) {
   static_assert(kDiag == 8, "two groups of four diagonals");
   std::int32_t d0[8], d1[8], d2[8], d3[8];
   long long hi[8];
@@ -547,6 +613,7 @@ __device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8]) 
     umma::ld8(taddr + 16 * (4 * g + 2), d2);
     umma::ld8(taddr + 16 * (4 * g + 3), d3);
     umma::ld_wait();
+    if (g == 1) release();  // every diagonal is in registers: the accumulator stage goes back before the arithmetic
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const long long w = static_cast<long long>(d3[j]) + (static_cast<long long>(d2[j]) << 8) +
@@ -577,14 +644,15 @@ constexpr int kWarps = 18;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kEpiWarps = 16;
 
+template <bool S4>
 __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedArgs a) {
   extern __shared__ __align__(1024) std::uint8_t smem_raw[];
   Smem& S = *reinterpret_cast<Smem*>(smem_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const std::uint32_t i_beg = a.cta_off[blockIdx.x], i_end = a.cta_off[blockIdx.x + 1];
+  const std::uint32_t i_beg = a.cta_beg[blockIdx.x], i_end = a.cta_end[blockIdx.x];
   if (tid == 0) {
     for (int b = 0; b < 2; ++b) {
-      umma::mbar_init(&S.full_a[b], 1);
+      umma::mbar_init(&S.full_a[b], S4 ? 2 : 1);  // the copies' expect_tx arrival (+ the scattered lowest slice)
       umma::mbar_init(&S.empty_a[b], 1);
 
       umma::mbar_init(&S.acc_full[b], 1);
@@ -594,7 +662,15 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       umma::mbar_init(&S.full_t[b], 1);
       umma::mbar_init(&S.empty_t[b], 1);
     }
+    for (int b = 0; b < 4; ++b) umma::mbar_init(&S.full_l[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (S4) {  // the lowest-slice planes start as zeros (each item's entries are scattered in and wiped again)
+    for (int b = 0; b < 2; ++b) {
+      uint4* z = reinterpret_cast<uint4*>(S.planes[b] + (kAS - 1) * kPlane);
+      for (int u = tid; u < kPlane / 16; u += kThreads) z[u] = make_uint4(0, 0, 0, 0);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 0) umma::tmem_alloc<512>(&S.tmem);
   umma::fence_before();
@@ -680,36 +756,74 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     // evict-first, so the X digit slabs of the sector band stay in L2) and
     // the partner's X digit slab into a free buffer; the owner's slab when a
     // new owner panel starts.
-    if (lane == 0) {
-      std::uint32_t k = 0, owners = 0;
-      const std::uint64_t stream = umma::createpolicy_evict_first();
-      // the X digit slabs are re-read by every item of the sector band: keep them
-      const std::uint64_t keep = umma::createpolicy_evict_last();
-      for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
-        const OzItem it = a.items[i];
-        const int b = k & 1;
-        TRACE(i, 8, true);
-        if ((it.flags >> 8) & 1u) {  // (the owner before last read this buffer until empty_t)
-          const int o = owners & 1;
-          umma::mbar_wait(&S.empty_t[o], ((owners >> 1) & 1u) ^ 1u);
-          umma::mbar_arrive_tx(&S.full_t[o], kSlab + 64);
-          const std::uint8_t* src = a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes;
-          umma::bulk_g2s_hint(S.xt[o], src, kSlab, &S.full_t[o], keep);
-          umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t[o]);
-          ++owners;
-        }
-        umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
-        TRACE(i, 4, true);
-        umma::mbar_arrive_tx(&S.full_a[b], kSlab + 64 + kPlanes);
+    std::uint32_t k = 0, owners = 0;
+    const std::uint64_t stream = umma::createpolicy_evict_first();
+    // the X digit slabs are re-read by every item of the sector band: keep them
+    const std::uint64_t keep = umma::createpolicy_evict_last();
+    constexpr int kDense = S4 ? kAS - 1 : kAS;  // planes streamed dense
+    // sparse lowest slice: item k's list sits in ring slot k & 3 (requested one
+    // item ahead); n4 of items k, k - 1, k - 2
+    std::uint32_t n4 = 0, n4_p1 = 0, n4_p2 = 0;
+    auto list_bytes = [](std::uint32_t n) { return std::max<std::uint32_t>(16u, (4u * n + 15u) & ~15u); };
+    auto request_list = [&](std::uint32_t i, std::uint32_t kk, std::uint32_t n) {
+      umma::mbar_arrive_tx(&S.full_l[kk & 3], list_bytes(n));
+      umma::bulk_g2s(S.list4[kk & 3], a.list4 + static_cast<std::size_t>((a.ablate & 2) ? 0 : i) * kL4Cap,
+                     list_bytes(n), &S.full_l[kk & 3]);
+    };
+    if (S4 && i_beg < i_end) {
+      n4 = a.items[i_beg].pad;
+      if (lane == 0) request_list(i_beg, 0, n4);
+    }
+    for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
+      const OzItem it = a.items[i];
+      const int b = k & 1;
+      TRACE(i, 8, lane == 0);
+      if (((it.flags >> 8) & 1u) && lane == 0) {  // (the owner before last read this buffer until empty_t)
+        const int o = owners & 1;
+        umma::mbar_wait(&S.empty_t[o], ((owners >> 1) & 1u) ^ 1u);
+        umma::mbar_arrive_tx(&S.full_t[o], kSlab + 64);
+        const std::uint8_t* src = a.xt + static_cast<std::size_t>(it.owner) * kSlabBytes;
+        umma::bulk_g2s_hint(S.xt[o], src, kSlab, &S.full_t[o], keep);
+        umma::bulk_g2s(S.xt_exp[owners & 3], src + kSlab, 64, &S.full_t[o]);
+      }
+      if ((it.flags >> 8) & 1u) ++owners;
+      if (S4 || lane == 0) umma::mbar_wait(&S.empty_a[b], ((k >> 1) & 1u) ^ 1u);
+      TRACE(i, 4, lane == 0);
+      if (lane == 0) {
+        umma::mbar_arrive_tx(&S.full_a[b], kSlab + 64 + kDense * kPlane);
         const std::uint8_t* xsrc = a.xd + static_cast<std::size_t>(it.partner) * kSlabBytes;
         umma::bulk_g2s_hint(S.xd[b], xsrc, kSlab, &S.full_a[b], keep);
         umma::bulk_g2s(S.xd_exp[k & 3], xsrc + kSlab, 64, &S.full_a[b]);
-        const std::uint8_t* src = a.dense + static_cast<std::size_t>((a.ablate & 2) ? 0 : i) * kPlanes;
+        const std::uint8_t* src = a.dense + static_cast<std::size_t>((a.ablate & 2) ? 0 : i) * (kDense * kPlane);
 #pragma unroll 1
-        for (int s = 0; s < kAS; ++s)
+        for (int s = 0; s < kDense; ++s)
           umma::bulk_g2s_hint(S.planes[b] + s * kPlane, src + s * kPlane, kPlane, &S.full_a[b], stream);
-        TRACE(i, 7, true);
       }
+      if (S4) {
+        std::uint8_t* p4 = S.planes[b] + (kAS - 1) * kPlane;
+        // wipe the entries of the item that used this buffer last (k - 2)
+        if (k >= 2)
+          for (std::uint32_t e = lane; e < n4_p2; e += 32) p4[S.list4[(k - 2) & 3][e] & 0xffffu] = 0;
+        __syncwarp();
+        // request the next item's list (its ring slot held item k - 3's, wiped one item ago)
+        std::uint32_t n4_next = 0;
+        if (i + 1 < i_end) {
+          n4_next = a.items[i + 1].pad;
+          if (lane == 0) request_list(i + 1, k + 1, n4_next);
+        }
+        umma::mbar_wait(&S.full_l[k & 3], (k >> 2) & 1u);
+        for (std::uint32_t e = lane; e < n4; e += 32) {
+          const std::uint32_t v = S.list4[k & 3][e];
+          p4[v & 0xffffu] = static_cast<std::uint8_t>(v >> 16);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic stores -> the tensor core's reads
+        __syncwarp();
+        if (lane == 0) umma::mbar_arrive(&S.full_a[b]);
+        n4_p2 = n4_p1;
+        n4_p1 = n4;
+        n4 = n4_next;
+      }
+      TRACE(i, 7, lane == 0);
     }
   } else if (orient == 0) {
     // ------------------------------------------------- row-part epilogue
@@ -738,13 +852,14 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
 #pragma unroll
       for (int j = 0; j < 8; ++j) ex[j] = S.xd_exp[k & 3][j0 + j];
       double v[8];
-      recombine8(tbase + ecol + b * kStageCols, v);
-      umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
-      umma::st_wait();
-      TRACE(i, 12, lane == 0 && warp == 4);
-      umma::fence_before();
-      __syncwarp();
-      if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
+      recombine8(tbase + ecol + b * kStageCols, v, [&] {
+        umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
+        umma::st_wait();
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
+        TRACE(i, 12, lane == 0 && warp == 4);
+      });
       TRACE(i, 13, lane == 0 && warp == 4);
 #pragma unroll
       for (int j = 0; j < 8; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 36), yacc[j]);
@@ -781,15 +896,21 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
 #pragma unroll
       for (int j = 0; j < 8; ++j) ex[j] = S.xt_exp[(owners - 1) & 3][j0 + j];
       double v[8];
+      auto release = [&] {
+        umma::fence_before();
+        __syncwarp();
+        if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
+        TRACE(i, 15, lane == 0 && warp == 12);
+      };
       if (trans) {
-        recombine8(tbase + ecol + b * kStageCols, v);
-        umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
-        umma::st_wait();
+        recombine8(tbase + ecol + b * kStageCols, v, [&] {
+          umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
+          umma::st_wait();
+          release();
+        });
+      } else {
+        release();
       }
-      umma::fence_before();
-      __syncwarp();
-      if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
-      TRACE(i, 15, lane == 0 && warp == 12);
       if (!trans || (a.ablate & 1)) continue;
       if (c < static_cast<int>(it.orow)) {  // the contribution to the partner's rows, in fixed point
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
@@ -897,6 +1018,9 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     pl->items = upload(items);
     pl->ctas = ctas;
     pl->cta_off = upload(cta_off);
+    pl->cta_off_host = cta_off;
+    pl->item_owner_host.resize(nitems);
+    for (std::uint32_t i = 0; i < nitems; ++i) pl->item_owner_host[i] = items[i].owner;
     CIEG_CUDA(cudaMalloc(&pl->rec, sizeof(uint2) * std::max<std::uint64_t>(1, total)));
     const std::uint32_t rows = ps.back() + kTD;
     CIEG_CUDA(cudaMalloc(&pl->rowexp, sizeof(int) * rows));
@@ -953,6 +1077,7 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
       off.push_back(nt);
       pl->ntiny_rows = static_cast<std::uint32_t>(rows.size());
       pl->tiny_rows = upload(rows);
+      pl->tiny_rows_host = rows;
       pl->tiny_off = upload(off);
       pl->tiny_in = upload(in);
       pl->tiny_val = upload(v);
@@ -966,15 +1091,41 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
     cudaFree(tpj);
     CIEG_CUDA(cudaMalloc(&pl->xd, static_cast<std::size_t>(m->npanels) * kSlabBytes));
     CIEG_CUDA(cudaMalloc(&pl->xt, static_cast<std::size_t>(m->npanels) * kSlabBytes));
-    // The slice planes of every item (kPlanes bytes each, 10 bytes per stored
-    // entry at the generator's 40 % tile density) when they fit in three
-    // quarters of the free memory; the records are dropped once scattered.
-    // Otherwise the matrix keeps the fp64 DMMA kernels.
-    const std::size_t dense_bytes = static_cast<std::size_t>(nitems) * kPlanes;
+    // The lowest slice as per-item lists when every item's fits (else five
+    // dense planes; CIEG_SLICED_DENSE5=1 forces that).
     std::size_t free_b = 0, total_b = 0;
+    static const bool dense5 = [] {
+      const char* e = std::getenv("CIEG_SLICED_DENSE5");
+      return e && std::atoi(e) != 0;
+    }();
+    if (nitems && pl->usable && !dense5 &&
+        cudaMalloc(&pl->list4, sizeof(std::uint32_t) * kL4Cap * static_cast<std::size_t>(nitems)) == cudaSuccess) {
+      unsigned* over = upload(std::vector<unsigned>{0u});
+      list4_kernel<<<nitems, 256, 0, ctx->stream>>>(pl->items, pl->rec, pl->list4, over);
+      CIEG_CUDA(cudaGetLastError());
+      unsigned over_h = 0;
+      CIEG_CUDA(cudaMemcpyAsync(&over_h, over, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+      CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+      cudaFree(over);
+      ++ctx->launches;
+      pl->sparse4 = over_h == 0;
+      if (!pl->sparse4) {
+        cudaFree(pl->list4);
+        pl->list4 = nullptr;
+      }
+    } else {
+      cudaGetLastError();
+      pl->list4 = nullptr;
+    }
+    // The dense slice planes of every item (16 KB each: 10 bytes per stored
+    // entry with four planes at the generator's 40 % tile density) when they
+    // fit in three quarters of the free memory; the records are dropped once
+    // scattered. Otherwise the matrix keeps the fp64 DMMA kernels.
+    const int nplanes = pl->sparse4 ? kAS - 1 : kAS;
+    const std::size_t dense_bytes = static_cast<std::size_t>(nitems) * nplanes * kPlane;
     if (nitems && pl->usable && cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && dense_bytes <= free_b / 4 * 3 &&
         cudaMalloc(&pl->dense, dense_bytes) == cudaSuccess) {
-      dense_kernel<<<nitems, 256, 0, ctx->stream>>>(pl->items, pl->rec, pl->dense);
+      dense_kernel<<<nitems, 256, 0, ctx->stream>>>(pl->items, pl->rec, pl->dense, nplanes);
       CIEG_CUDA(cudaGetLastError());
       CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
       ++ctx->launches;
@@ -999,9 +1150,13 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
         }
       }
       std::vector<std::uint32_t> off(np + 1, 0), flat;
+      pl->nb_prefix_max.assign(np, 0);
       for (std::uint32_t q = 0; q < np; ++q) {
         flat.insert(flat.end(), nbs[q].begin(), nbs[q].end());
         off[q + 1] = static_cast<std::uint32_t>(flat.size());
+        std::uint32_t hi = q;
+        for (std::uint32_t v : nbs[q]) hi = std::max(hi, v & 0x7fffffffu);
+        pl->nb_prefix_max[q] = q ? std::max(hi, pl->nb_prefix_max[q - 1]) : hi;
       }
       std::vector<float> dh(rows);
       CIEG_CUDA(cudaMemcpy(dh.data(), pl->diag, sizeof(float) * rows, cudaMemcpyDeviceToHost));
@@ -1029,11 +1184,12 @@ SlicedPlan* build_plan(cieg_ctx* ctx, cieg_mat* m) {
 // y[out] += sum h x[in] over the tiny entries of each output row (fixed
 // order; non-finite x are left to the caller's non-finite fix-up).
 __global__ void tiny_fix_kernel(const std::uint32_t* rows, const std::uint32_t* off, const std::uint32_t* in,
-                                const double* val, std::uint32_t nrows, const double* x, std::uint32_t ldx, double* y,
-                                std::uint32_t ldy, std::uint32_t mc, std::uint32_t row_base) {
+                                const double* val, std::uint32_t t_lo, std::uint32_t t_hi, const double* x,
+                                std::uint32_t ldx, double* y, std::uint32_t ldy, std::uint32_t mc,
+                                std::uint32_t row_base) {
   const std::uint32_t e = blockIdx.x * blockDim.x + threadIdx.x;
-  const std::uint32_t t = e >> 4, j = e & 15u;
-  if (t >= nrows || j >= mc) return;
+  const std::uint32_t t = t_lo + (e >> 4), j = e & 15u;
+  if (t >= t_hi || j >= mc) return;
   double s = 0.0;
   for (std::uint32_t k = off[t]; k < off[t + 1]; ++k) {
     const double xv = x[static_cast<std::size_t>(in[k]) * ldx + j];
@@ -1050,7 +1206,7 @@ void launch_sliced_tiny_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, s
   if (!pl || pl->ntiny_rows == 0) return;
   const std::uint32_t threads = pl->ntiny_rows * 16;
   tiny_fix_kernel<<<(threads + 255) / 256, 256, 0, ctx->stream>>>(pl->tiny_rows, pl->tiny_off, pl->tiny_in,
-                                                                  pl->tiny_val, pl->ntiny_rows, x, ldx, y, ldy, mc,
+                                                                  pl->tiny_val, 0, pl->ntiny_rows, x, ldx, y, ldy, mc,
                                                                   m->row_lo);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
@@ -1072,25 +1228,30 @@ void destroy_sliced(cieg_mat* m) {
   m->sliced = nullptr;
 }
 
-void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32_t ldx, double* y, std::uint32_t ldy,
-                        std::uint32_t mc, unsigned* nonfinite, unsigned launch_id) {
-  if (!sliced_ready(ctx, m))
-    fail(CIEG_ERR_CONFIG, "sliced SpMM needs an unsharded fp32 matrix with 128-row panels and finite values");
-  if (mc == 0 || mc > 16) fail(CIEG_ERR_ARGUMENT, "sliced SpMM: 1..16 columns per launch");
-  SlicedPlan* pl = m->sliced;
-  digitize_kernel<<<m->npanels, 128, 0, ctx->stream>>>(x, ldx, mc, m->panel_start, pl->rowexp, pl->xd, pl->xt,
-                                                       nonfinite, launch_id);
+namespace {
+
+void launch_digitize(cieg_ctx* ctx, const cieg_mat* m, SlicedPlan* pl, const double* x, std::uint32_t ldx,
+                     std::uint32_t mc, unsigned* nonfinite, unsigned launch_id, std::uint32_t p_lo, std::uint32_t p_hi) {
+  if (p_hi <= p_lo) return;
+  digitize_kernel<<<p_hi - p_lo, 128, 0, ctx->stream>>>(x, ldx, mc, m->panel_start, pl->rowexp, pl->xd, pl->xt,
+                                                        nonfinite, launch_id, p_lo);
   CIEG_CUDA(cudaGetLastError());
-  scales_kernel<<<m->npanels, 32, 0, ctx->stream>>>(pl->nb_off, pl->nb, pl->erq, pl->edq, pl->xd, pl->xt, pl->escale);
+  ++ctx->launches;
+}
+
+void launch_scales(cieg_ctx* ctx, SlicedPlan* pl, std::uint32_t q_lo, std::uint32_t q_hi) {
+  if (q_hi <= q_lo) return;
+  scales_kernel<<<q_hi - q_lo, 32, 0, ctx->stream>>>(pl->nb_off, pl->nb, pl->erq, pl->edq, pl->xd, pl->xt, pl->escale,
+                                                     q_lo);
   CIEG_CUDA(cudaGetLastError());
-  static const char* trace_path = std::getenv("CIEG_SLICED_TRACE");
-  long long* trace = nullptr;
-  if (trace_path) {
-    CIEG_CUDA(cudaMalloc(&trace, sizeof(long long) * 256 * 16));
-    CIEG_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 256 * 16, ctx->stream));
-  }
-  SlicedArgs args{pl->items, pl->cta_off, pl->dense, pl->xd, pl->xt, pl->rowexp, pl->diag, x,
-                  pl->yint,  pl->escale,  ldx,       mc,     trace,  0};
+  ++ctx->launches;
+}
+
+// the main kernel over the items [beg[b], end[b]) of every CTA b
+void launch_main(cieg_ctx* ctx, SlicedPlan* pl, const double* x, std::uint32_t ldx, std::uint32_t mc,
+                 const std::uint32_t* beg, const std::uint32_t* end, long long* trace) {
+  SlicedArgs args{pl->items, beg, end, pl->dense, pl->list4, pl->xd, pl->xt, pl->rowexp, pl->diag, x,
+                  pl->yint,  pl->escale, ldx, mc, trace, 0};
   static const int ablate = [] {
     const char* e = std::getenv("CIEG_SLICED_ABLATE");
     return e ? std::atoi(e) : 0;
@@ -1098,9 +1259,92 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
   args.ablate = ablate;
   constexpr std::size_t smem = sizeof(Smem) + 1024;
   static_assert(smem <= 227 * 1024, "shared memory budget");
-  CIEG_CUDA(cudaFuncSetAttribute(spmm_sliced_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  spmm_sliced_kernel<<<pl->ctas, kThreads, smem, ctx->stream>>>(args);
+  static const bool attr_set = [] {
+    CIEG_CUDA(cudaFuncSetAttribute(spmm_sliced_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    CIEG_CUDA(cudaFuncSetAttribute(spmm_sliced_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(smem)));
+    return true;
+  }();
+  (void)attr_set;
+  if (pl->sparse4)
+    spmm_sliced_kernel<true><<<pl->ctas, kThreads, smem, ctx->stream>>>(args);
+  else
+    spmm_sliced_kernel<false><<<pl->ctas, kThreads, smem, ctx->stream>>>(args);
   CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+void launch_convert(cieg_ctx* ctx, const cieg_mat* m, SlicedPlan* pl, const double* x, std::uint32_t ldx, double* y,
+                    std::uint32_t ldy, std::uint32_t mc, std::uint32_t q_lo, std::uint32_t q_hi) {
+  if (q_hi <= q_lo) return;
+  yint_to_y_kernel<<<q_hi - q_lo, 256, 0, ctx->stream>>>(pl->yint, pl->escale, m->panel_start, pl->diag, x, ldx, y,
+                                                         ldy, mc, m->row_lo, q_lo);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+// the tiny-entry terms of the output rows [r_lo, r_hi)
+void launch_tiny_rows(cieg_ctx* ctx, const cieg_mat* m, const SlicedPlan* pl, const double* x, std::uint32_t ldx,
+                      double* y, std::uint32_t ldy, std::uint32_t mc, std::uint32_t r_lo, std::uint32_t r_hi) {
+  const auto& tr = pl->tiny_rows_host;
+  const std::uint32_t t_lo = static_cast<std::uint32_t>(std::lower_bound(tr.begin(), tr.end(), r_lo) - tr.begin());
+  const std::uint32_t t_hi = static_cast<std::uint32_t>(std::lower_bound(tr.begin(), tr.end(), r_hi) - tr.begin());
+  if (t_hi <= t_lo) return;
+  const std::uint32_t threads = (t_hi - t_lo) * 16;
+  tiny_fix_kernel<<<(threads + 255) / 256, 256, 0, ctx->stream>>>(pl->tiny_rows, pl->tiny_off, pl->tiny_in,
+                                                                  pl->tiny_val, t_lo, t_hi, x, ldx, y, ldy, mc,
+                                                                  m->row_lo);
+  CIEG_CUDA(cudaGetLastError());
+  ++ctx->launches;
+}
+
+// Owner panels cut into `want` chunks of about equal rows; per chunk and CTA
+// the item range (a CTA's items ascend by owner panel). Cached per chunk count.
+const SlicedPlan::Chunks& chunking(const cieg_mat* m, SlicedPlan* pl, std::uint32_t want) {
+  const auto& ps = m->panel_start_host;
+  const std::uint32_t np = m->npanels;
+  want = std::max<std::uint32_t>(1, std::min(want, np));
+  for (const auto& c : pl->chunkings)
+    if (c.panel.size() == want + 1) return c;
+  SlicedPlan::Chunks ch;
+  ch.panel.assign(want + 1, np);
+  ch.panel[0] = 0;
+  for (std::uint32_t c = 1; c < want; ++c) {
+    const std::uint32_t row = static_cast<std::uint32_t>(static_cast<std::uint64_t>(m->dim) * c / want);
+    ch.panel[c] = std::max(ch.panel[c - 1], panel_of(ps, row));
+  }
+  const std::uint32_t ctas = pl->ctas;
+  std::vector<std::uint32_t> lim(static_cast<std::size_t>(want + 1) * ctas);
+  for (std::uint32_t b = 0; b < ctas; ++b) {
+    const auto first = pl->item_owner_host.begin() + pl->cta_off_host[b];
+    const auto last = pl->item_owner_host.begin() + pl->cta_off_host[b + 1];
+    for (std::uint32_t c = 0; c <= want; ++c)
+      lim[static_cast<std::size_t>(c) * ctas + b] =
+          static_cast<std::uint32_t>(std::lower_bound(first, last, ch.panel[c]) - pl->item_owner_host.begin());
+  }
+  ch.cta_lim = upload(lim);
+  pl->chunkings.push_back(std::move(ch));
+  return pl->chunkings.back();
+}
+
+}  // namespace
+
+void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32_t ldx, double* y, std::uint32_t ldy,
+                        std::uint32_t mc, unsigned* nonfinite, unsigned launch_id) {
+  if (!sliced_ready(ctx, m))
+    fail(CIEG_ERR_CONFIG, "sliced SpMM needs an unsharded fp32 matrix with 128-row panels and finite values");
+  if (mc == 0 || mc > 16) fail(CIEG_ERR_ARGUMENT, "sliced SpMM: 1..16 columns per launch");
+  SlicedPlan* pl = m->sliced;
+  launch_digitize(ctx, m, pl, x, ldx, mc, nonfinite, launch_id, 0, m->npanels);
+  launch_scales(ctx, pl, 0, m->npanels);
+  static const char* trace_path = std::getenv("CIEG_SLICED_TRACE");
+  long long* trace = nullptr;
+  if (trace_path) {
+    CIEG_CUDA(cudaMalloc(&trace, sizeof(long long) * 256 * 16));
+    CIEG_CUDA(cudaMemsetAsync(trace, 0, sizeof(long long) * 256 * 16, ctx->stream));
+  }
+  launch_main(ctx, pl, x, ldx, mc, pl->cta_off, pl->cta_off + 1, trace);
   if (trace) {  // debug: dump CTA 0's timeline
     std::vector<long long> h(256 * 16);
     CIEG_CUDA(cudaMemcpyAsync(h.data(), trace, sizeof(long long) * h.size(), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1111,10 +1355,185 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
       std::fclose(f);
     }
   }
-  yint_to_y_kernel<<<m->npanels, 256, 0, ctx->stream>>>(pl->yint, pl->escale, m->panel_start, pl->diag, x, ldx, y,
-                                                        ldy, mc, m->row_lo);
-  CIEG_CUDA(cudaGetLastError());
-  ctx->launches += 4;
+  launch_convert(ctx, m, pl, x, ldx, y, ldy, mc, 0, m->npanels);
+}
+
+// ---- ci::spmm's host call on the sliced kernel, pipelined over row chunks.
+//
+// The stored triangle couples an owner panel P only to partner panels Q <= P,
+// and the schedule sweeps the owner panels front to back. So the call is cut
+// into chunks of owner panels: while chunk c's rows of X are on the wire
+// (upload stream), the digits of the chunks before it are formed, every panel
+// whose neighbours are all digitized gets its fixed-point scales, every chunk
+// whose panels all have scales runs the main kernel, every panel whose
+// contributing owners have all run is converted to fp64 and its rows of U go
+// home on the download stream. Upload, kernels and download overlap; the
+// fixed-point accumulation does not depend on the order of the additions, so
+// the result is bitwise that of the one-launch call. For the block-banded
+// sector matrices a panel's neighbours lie within +-2 sectors, so U trails X
+// by about that band; for a matrix without such structure the pipeline
+// degenerates to upload, compute, download.
+//
+// Pageable host buffers (the std::vector inside ci::BlockVectors) stream
+// through pinned rings in both directions; `copy` / `copy_out` are the caller's
+// threaded host copies into / out of the rings.
+bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* y_host, std::uint32_t mc,
+                      bool x_pinned, bool y_pinned, void (*copy)(void*, const void*, std::size_t),
+                      void (*copy_out)(void*, const void*, std::size_t)) {
+  const bool shard = m->row_lo != 0 || m->row_hi != m->dim;
+  if (shard || mc == 0 || mc > 16 || !sliced_rule(ctx, m, mc) || !sliced_ready(ctx, m)) return false;
+  static const bool off = [] {
+    const char* e = std::getenv("CIEG_HOST_PIPELINE");
+    return e && std::atoi(e) == 0;
+  }();
+  if (off) return false;
+  SlicedPlan* pl = m->sliced;
+  const auto& ps = m->panel_start_host;
+  const std::uint32_t np = m->npanels, n = m->dim;
+  const std::size_t row_bytes = sizeof(double) * mc;
+  constexpr std::size_t kChunkBytes = 8u << 20;  // ring slot size = upload chunk bound
+  const std::size_t xbytes = static_cast<std::size_t>(n) * row_bytes;
+  // about 16 MB of X per chunk, at most 32 chunks (measured on config 2: 16 chunks 7.9 ms, 32 8.0 ms, 48 8.3 ms
+  // on pinned buffers; CIEG_HOST_CHUNKS overrides)
+  std::uint32_t want = static_cast<std::uint32_t>(std::min<std::size_t>(32, (xbytes + kChunkBytes) / (2 * kChunkBytes)));
+  if (const char* e = std::getenv("CIEG_HOST_CHUNKS")) want = static_cast<std::uint32_t>(std::max(1, std::atoi(e)));
+  const auto& ch = chunking(m, pl, want);
+  const std::uint32_t nch = static_cast<std::uint32_t>(ch.panel.size() - 1);
+  double* dx = static_cast<double*>(ctx->scratch_x.get(xbytes));
+  double* dy = static_cast<double*>(ctx->scratch_y.get(xbytes));
+  if (!ctx->pipe_up) CIEG_CUDA(cudaStreamCreateWithFlags(&ctx->pipe_up, cudaStreamNonBlocking));
+  if (!ctx->pipe_down) CIEG_CUDA(cudaStreamCreateWithFlags(&ctx->pipe_down, cudaStreamNonBlocking));
+  std::size_t ev_next = 0;
+  auto event = [&]() {
+    if (ev_next == ctx->pipe_ev.size()) {
+      cudaEvent_t e = nullptr;
+      CIEG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ctx->pipe_ev.push_back(e);
+    }
+    return ctx->pipe_ev[ev_next++];
+  };
+  constexpr int kUpSlots = 3, kDownSlots = 4;
+  char* up_ring = x_pinned ? nullptr : static_cast<char*>(ctx->pinned_stage.get(kUpSlots * kChunkBytes));
+  char* down_ring = y_pinned ? nullptr : static_cast<char*>(ctx->pinned_stage_down.get(kDownSlots * kChunkBytes));
+  unsigned* flag = nonfinite_flag(ctx);
+  const unsigned launch_id = ++ctx->spmm_launch_id;
+
+  // nothing may touch dx / dy before the work already queued on the context stream
+  cudaEvent_t e0 = event();
+  CIEG_CUDA(cudaEventRecord(e0, ctx->stream));
+  CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_up, e0, 0));
+  CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_down, e0, 0));
+
+  struct Pending {
+    cudaEvent_t ev;
+    const char* src;
+    char* dst;
+    std::size_t len;
+  };
+  std::deque<Pending> pending;  // downloads in ring slots awaiting their host copy
+  std::size_t down_count = 0;
+  auto retire = [&](bool block) {
+    while (!pending.empty()) {
+      if (block) {
+        CIEG_CUDA(cudaEventSynchronize(pending.front().ev));
+      } else {
+        const cudaError_t q = cudaEventQuery(pending.front().ev);
+        if (q == cudaErrorNotReady) return;
+        CIEG_CUDA(q);
+      }
+      copy_out(pending.front().dst, pending.front().src, pending.front().len);
+      pending.pop_front();
+      if (block) return;
+    }
+  };
+  // rows [r_lo, r_hi) of U, ready on the context stream -> host
+  auto download = [&](std::uint32_t r_lo, std::uint32_t r_hi) {
+    if (r_hi <= r_lo) return;
+    cudaEvent_t ready = event();
+    CIEG_CUDA(cudaEventRecord(ready, ctx->stream));
+    CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_down, ready, 0));
+    const std::size_t b0 = r_lo * row_bytes, b1 = r_hi * row_bytes;
+    if (y_pinned) {
+      CIEG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(y_host) + b0, reinterpret_cast<const char*>(dy) + b0, b1 - b0,
+                                cudaMemcpyDeviceToHost, ctx->pipe_down));
+      return;
+    }
+    for (std::size_t o = b0; o < b1; o += kChunkBytes) {
+      const std::size_t len = std::min(kChunkBytes, b1 - o);
+      while (pending.size() >= static_cast<std::size_t>(kDownSlots)) retire(true);
+      char* slot = down_ring + (down_count++ % kDownSlots) * kChunkBytes;
+      CIEG_CUDA(cudaMemcpyAsync(slot, reinterpret_cast<const char*>(dy) + o, len, cudaMemcpyDeviceToHost, ctx->pipe_down));
+      cudaEvent_t done = event();
+      CIEG_CUDA(cudaEventRecord(done, ctx->pipe_down));
+      pending.push_back(Pending{done, slot, reinterpret_cast<char*>(y_host) + o, len});
+    }
+  };
+
+  const auto& pm = pl->nb_prefix_max;
+  auto below = [&](std::uint32_t lim) {  // panels whose neighbours all lie below lim
+    return lim >= np ? np : static_cast<std::uint32_t>(std::lower_bound(pm.begin(), pm.end(), lim) - pm.begin());
+  };
+  std::uint32_t scaled = 0, next_chunk = 0, computed = 0, converted = 0;
+  std::vector<cudaEvent_t> up_done(kUpSlots, nullptr);
+  std::size_t up_count = 0;
+  for (std::uint32_t c = 0; c < nch; ++c) {
+    const std::uint32_t p_lo = ch.panel[c], p_hi = ch.panel[c + 1];
+    if (p_hi <= p_lo) continue;
+    const std::size_t b0 = ps[p_lo] * row_bytes, b1 = (p_hi == np ? n : ps[p_hi]) * row_bytes;
+    if (x_pinned) {
+      CIEG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dx) + b0, reinterpret_cast<const char*>(x_host) + b0, b1 - b0,
+                                cudaMemcpyHostToDevice, ctx->pipe_up));
+    } else {
+      for (std::size_t o = b0; o < b1; o += kChunkBytes) {
+        const std::size_t len = std::min(kChunkBytes, b1 - o);
+        const int s = static_cast<int>(up_count++ % kUpSlots);
+        if (up_done[s]) CIEG_CUDA(cudaEventSynchronize(up_done[s]));
+        copy(up_ring + s * kChunkBytes, reinterpret_cast<const char*>(x_host) + o, len);
+        CIEG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dx) + o, up_ring + s * kChunkBytes, len,
+                                  cudaMemcpyHostToDevice, ctx->pipe_up));
+        up_done[s] = event();
+        CIEG_CUDA(cudaEventRecord(up_done[s], ctx->pipe_up));
+        retire(false);
+      }
+    }
+    cudaEvent_t uploaded = event();
+    CIEG_CUDA(cudaEventRecord(uploaded, ctx->pipe_up));
+    CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, uploaded, 0));
+    launch_digitize(ctx, m, pl, dx, mc, mc, flag, launch_id, p_lo, p_hi);
+    const std::uint32_t s_hi = below(p_hi);
+    launch_scales(ctx, pl, scaled, s_hi);
+    scaled = std::max(scaled, s_hi);
+    while (next_chunk < nch && ch.panel[next_chunk + 1] <= scaled) {
+      if (ch.panel[next_chunk + 1] > ch.panel[next_chunk])
+        launch_main(ctx, pl, dx, mc, mc, ch.cta_lim + static_cast<std::size_t>(next_chunk) * pl->ctas,
+                    ch.cta_lim + static_cast<std::size_t>(next_chunk + 1) * pl->ctas, nullptr);
+      computed = ch.panel[++next_chunk];
+    }
+    const std::uint32_t y_hi = below(computed);
+    if (y_hi > converted) {
+      const std::uint32_t r_lo = ps[converted], r_hi = y_hi == np ? n : ps[y_hi];
+      launch_convert(ctx, m, pl, dx, mc, dy, mc, mc, converted, y_hi);
+      launch_tiny_rows(ctx, m, pl, dx, mc, dy, mc, mc, r_lo, r_hi);
+      download(r_lo, r_hi);
+      converted = y_hi;
+    }
+    retire(false);
+  }
+  if (converted != np || next_chunk != nch) fail(CIEG_ERR_CUDA, "sliced host pipeline: incomplete schedule");
+  // Inf/NaN in X (staged as zeros): the rare path -- the exact stored-entry
+  // terms are added on the device and U is downloaded again, whole
+  unsigned* flag_host = static_cast<unsigned*>(ctx->pinned_small.get(256));
+  CIEG_CUDA(cudaMemcpyAsync(flag_host, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
+  while (!pending.empty()) retire(true);
+  CIEG_CUDA(cudaStreamSynchronize(ctx->pipe_down));
+  CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (*flag_host == launch_id) {
+    launch_nonfinite_fix(ctx, m, dx, mc, dy, mc, mc, launch_id);
+    download(0, n);
+    while (!pending.empty()) retire(true);
+    CIEG_CUDA(cudaStreamSynchronize(ctx->pipe_down));
+  }
+  return true;
 }
 
 }  // namespace cieg

@@ -172,3 +172,74 @@ def test_sliced_lobpcg_matches_reference(sliced, ref_lib):
     assert [rep.counters.spmm_calls, rep.counters.spmv_equivalents, rep.counters.precond_applications,
             rep.counters.orthogonalizations] == rr.counters.tolist()
     np.testing.assert_allclose(rep.eigenvalues, rr.eigenvalues, rtol=1e-9)
+
+
+# ---- the chunk-pipelined host call (cieg_spmm_host on the sliced kernel)
+
+def _device_spmm(dm, x):
+    """One-launch sliced SpMM on device-resident X (cieg_spmm)."""
+    import torch
+
+    xd = torch.from_numpy(x).cuda()
+    yd = torch.empty_like(xd)
+    torch.cuda.synchronize()
+    dm.spmm_ptr(xd.data_ptr(), yd.data_ptr(), x.shape[1])
+    dm.device.synchronize()
+    return yd.cpu().numpy()
+
+
+@pytest.mark.parametrize("chunks", [1, 2, 5, 12, 40])
+@pytest.mark.parametrize("m", [1, 7, 16])
+def test_host_pipeline_bitwise(sliced, ref_lib, monkeypatch, chunks, m):
+    """Upload, kernels and download pipelined over row chunks: bitwise the
+    one-launch result at every chunk count (the fixed-point accumulation does
+    not depend on the order of the additions), pageable and pinned buffers."""
+    import torch
+
+    h = gen_from((40000, 10, 256, 0.02, 0.4, 21, 0, 2000))
+    dm = ci.device_matrix(h)
+    x = ci.random_block(h.dim, m, 300 + m)
+    y_one = _device_spmm(dm, x)
+    assert rel_cols(y_one, ref_lib.RefMatrix(h).spmm(x, serial=True)) < TOL
+    monkeypatch.setenv("CIEG_HOST_CHUNKS", str(chunks))
+    assert np.array_equal(dm.spmm_host(x), y_one)
+    xp = torch.from_numpy(x).pin_memory()
+    yp = torch.empty_like(xp).pin_memory()
+    ci._check(ci._lib.load().cieg_spmm_host(dm.device.handle, dm.handle, ci._ptr(xp.numpy()), ci._ptr(yp.numpy()), m))
+    assert np.array_equal(yp.numpy(), y_one)
+
+
+def test_host_pipeline_nonfinite_and_tiny(sliced, ref_lib, monkeypatch):
+    """Inf/NaN rows of X (fixed up after the pipeline, U downloaded again) and
+    the tiny-entry terms added per converted row range."""
+    h = gen_from((40000, 10, 256, 0.02, 0.4, 22, 0, 2000))
+    vals = h.values.copy()
+    vals[::1000] *= 2.0 ** -30  # entries too small for their row's slices: the fp64 tiny list
+    h2 = _with_values(h, vals)
+    dm = ci.DeviceMatrix(h2)
+    x = ci.random_block(h.dim, 16, 17)
+    monkeypatch.setenv("CIEG_HOST_CHUNKS", "9")
+    y = dm.spmm_host(x)
+    y_ref = ref_lib.RefMatrix(h2).spmm(x, serial=True)
+    assert rel_cols(y, y_ref) < TOL
+    assert np.array_equal(y, _device_spmm(dm, x))
+    x[123, 3] = np.inf
+    x[30000, 0] = np.nan
+    y = dm.spmm_host(x)
+    y_ref = ref_lib.RefMatrix(h2).spmm(x, serial=True)
+    assert np.array_equal(np.isnan(y), np.isnan(y_ref)) and np.array_equal(np.isinf(y), np.isinf(y_ref))
+    fin = np.isfinite(y_ref)
+    assert np.abs(y[fin] - y_ref[fin]).max() <= TOL * np.abs(y_ref[fin]).max()
+
+
+def test_host_pipeline_unbanded(sliced, ref_lib, monkeypatch):
+    """A matrix whose last panel couples to the first (two sectors, band
+    covering both): no panel is final before the last owner ran; the pipeline
+    degenerates to upload, compute, download."""
+    h = gen_from((6000, 2, 128, 0.1, 0.5, 4, 0, 2000))
+    dm = ci.device_matrix(h)
+    x = ci.random_block(h.dim, 16, 5)
+    monkeypatch.setenv("CIEG_HOST_CHUNKS", "6")
+    y = dm.spmm_host(x)
+    assert np.array_equal(y, _device_spmm(dm, x))
+    assert rel_cols(y, ref_lib.RefMatrix(h).spmm(x, serial=True)) < TOL
