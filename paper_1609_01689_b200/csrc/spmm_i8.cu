@@ -572,7 +572,8 @@ struct SlicedArgs {
   const int* escale;   // [panel][column]
   std::uint32_t ldx, mc;
   long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
-  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no transposed reduction, 2 planes of item 0 only
+  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no transposed reduction, 2 planes of item 0 only,
+                     // 4 no TMEM reads in the epilogue, 8 no transposed MMAs
 };
 
 // (slabs hold the digits only -- every operand starts on a 1024-byte
@@ -592,28 +593,30 @@ struct Smem {
   std::uint32_t tmem;
 };
 
-// exact int64 -> double for |v| < 2^51 (the 2^52 + 2^51 bias; no conversion unit)
-__device__ __forceinline__ double l2d(long long v) {
-  return __longlong_as_double(v + 0x4338000000000000ll) - 6755399441055744.0;
-}
-
 // sum_d D_d 2^(24 - 8 d) over the kDiag diagonal blocks at TMEM address taddr
 // (8 columns of this warp's 32 lanes): the diagonals are combined exactly in
 // int64 in two groups of four (|D_d| < 2^24, so each group is below 2^49) and
 // the two groups are joined in fp64 with a single rounding.
+// sum_d D_d 2^(24 - 8 d) over the kDiag diagonal blocks at TMEM address taddr
+// (8 columns of this warp's 32 lanes), exactly, as hi 2^32 + lo: the diagonals
+// are combined in int64 in two groups of four (|D_d| < 2^24, so each group is
+// below 2^49). `release` runs once every diagonal is in registers (the
+// accumulator stage goes back before the arithmetic).
 template <typename Release>
-__device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8], Release release) {
+__device__ __forceinline__ void recombine8(std::uint32_t taddr, long long (&hi)[8], long long (&lo)[8],
+                                           Release release, bool skip_loads = false) {
   static_assert(kDiag == 8, "two groups of four diagonals");
-  std::int32_t d0[8], d1[8], d2[8], d3[8];
-  long long hi[8];
+  std::int32_t d0[8] = {}, d1[8] = {}, d2[8] = {}, d3[8] = {};
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
-    umma::ld8(taddr + 16 * (4 * g), d0);
-    umma::ld8(taddr + 16 * (4 * g + 1), d1);
-    umma::ld8(taddr + 16 * (4 * g + 2), d2);
-    umma::ld8(taddr + 16 * (4 * g + 3), d3);
-    umma::ld_wait();
-    if (g == 1) release();  // every diagonal is in registers: the accumulator stage goes back before the arithmetic
+    if (!skip_loads) {  // (timing-only ablation: no TMEM reads)
+      umma::ld8(taddr + 16 * (4 * g), d0);
+      umma::ld8(taddr + 16 * (4 * g + 1), d1);
+      umma::ld8(taddr + 16 * (4 * g + 2), d2);
+      umma::ld8(taddr + 16 * (4 * g + 3), d3);
+      umma::ld_wait();
+    }
+    if (g == 1) release();
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const long long w = static_cast<long long>(d3[j]) + (static_cast<long long>(d2[j]) << 8) +
@@ -621,15 +624,24 @@ __device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8], 
       if (g == 0)
         hi[j] = w;
       else
-        v[j] = fma(l2d(w), 0x1p-32, l2d(hi[j]));
+        lo[j] = w;
     }
   }
 }
 
+// round((hi 2^32 + lo) 2^-r) to the nearest integer (halves up), |hi 2^32 + lo|
+// < 2^82: the contribution in units of the panel's fixed-point scale. Integer
+// arithmetic only (the FP64 pipe stays out of the epilogue); r >= 14 by the
+// scale bounds whenever the value is non-zero, and a shift beyond the value's
+// bits gives 0.
+__device__ __forceinline__ long long shift_round(long long hi, long long lo, int r) {
+  r = max(1, min(r, 126));
+  const __int128 w = (static_cast<__int128>(hi) << 32) + static_cast<__int128>(lo) + (static_cast<__int128>(1) << (r - 1));
+  return static_cast<long long>(w >> r);
+}
+
 // ---- fixed-point accumulation into yint: 64-bit integer adds in L2
 // (red.global.add.u64 -- exact, so the result does not depend on their order)
-// v 2^e rounded to the nearest integer (|result| < 2^62 by the scale bounds)
-__device__ __forceinline__ long long fixp(double v, int e) { return __double2ll_rn(v * pow2(e)); }
 
 #define TRACE(item, slot, cond)                                                                      \
   do {                                                                                               \
@@ -734,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         umma::fence_after();
       }
       const std::uint64_t bt = b_t0 + static_cast<std::uint64_t>(o * (kSlab >> 4));
-      if (trans) {
+      if (trans && !(a.ablate & 8)) {
 #pragma unroll 1
         for (int s = 0; s < kAS; ++s) {
           const int n = 16 * min(kXD, kDiag - s);
@@ -829,7 +841,10 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     // ------------------------------------------------- row-part epilogue
     // (TMEM lanes = tile rows; 8 of the 16 columns per warp)
     const int r = 32 * eq + lane, j0 = 8 * half;
-    double yacc[8];
+    // the owner's rows in fixed point (units 2^(escale - 62) of the owner
+    // panel): every item's contribution is rounded to that unit and the exact
+    // int64 sum is added to yint once per owner
+    long long yacc[8];
     int er = 0, osc[8];
     std::uint32_t k = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
@@ -839,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       if ((it.flags >> 8) & 1u) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          yacc[j] = 0.0;
+          yacc[j] = 0;
           osc[j] = __ldg(a.escale + it.owner * 16 + j0 + j);
         }
         er = r < prow ? a.rowexp[it.r0 + r] : 0;
@@ -851,25 +866,25 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       int ex[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) ex[j] = S.xd_exp[k & 3][j0 + j];
-      double v[8];
-      recombine8(tbase + ecol + b * kStageCols, v, [&] {
+      long long hi[8], lo[8];
+      recombine8(tbase + ecol + b * kStageCols, hi, lo, [&] {
         umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
         umma::st_wait();
         umma::fence_before();
         __syncwarp();
         if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
         TRACE(i, 12, lane == 0 && warp == 4);
-      });
+      }, (a.ablate & 4) != 0);
       TRACE(i, 13, lane == 0 && warp == 4);
+      // v 2^(e_r + ex - 36) in units of 2^(osc - 62), v = hi + lo 2^-32
 #pragma unroll
-      for (int j = 0; j < 8; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 36), yacc[j]);
+      for (int j = 0; j < 8; ++j) yacc[j] += shift_round(hi[j], lo[j], osc[j] + 6 - er - ex[j]);
       TRACE(i, 10, lane == 0 && warp == 4);
-      if (((it.flags >> 9) & 1u) && r < prow) {  // the owner's row part, in fixed point, added to yint
+      if (((it.flags >> 9) & 1u) && r < prow) {
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
                                  static_cast<std::size_t>(it.owner) * kTD * 16 + eq * 512 + j0 * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          atomicAdd(yr + j * 32, static_cast<unsigned long long>(fixp(yacc[j], 62 - osc[j])));
+        for (int j = 0; j < 8; ++j) atomicAdd(yr + j * 32, static_cast<unsigned long long>(yacc[j]));
       }
     }
   } else {
@@ -895,7 +910,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       int ex[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) ex[j] = S.xt_exp[(owners - 1) & 3][j0 + j];
-      double v[8];
+      long long hi[8], lo[8];
       auto release = [&] {
         umma::fence_before();
         __syncwarp();
@@ -903,21 +918,21 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         TRACE(i, 15, lane == 0 && warp == 12);
       };
       if (trans) {
-        recombine8(tbase + ecol + b * kStageCols, v, [&] {
+        recombine8(tbase + ecol + b * kStageCols, hi, lo, [&] {
           umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
           umma::st_wait();
           release();
-        });
+        }, (a.ablate & 4) != 0);
       } else {
         release();
       }
       if (!trans || (a.ablate & 1)) continue;
-      if (c < static_cast<int>(it.orow)) {  // the contribution to the partner's rows, in fixed point
+      if (c < static_cast<int>(it.orow)) {  // the contribution to the partner's rows, in its fixed-point units
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
                                  static_cast<std::size_t>(it.partner) * kTD * 16 + eq * 512 + j0 * 32 + lane;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          atomicAdd(yr + j * 32, static_cast<unsigned long long>(fixp(v[j], ex[j] - 36 + 62 - psc[j])));
+          atomicAdd(yr + j * 32, static_cast<unsigned long long>(shift_round(hi[j], lo[j], psc[j] + 6 - ex[j])));
       }
     }
 
