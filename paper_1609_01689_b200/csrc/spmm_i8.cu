@@ -401,11 +401,11 @@ __device__ __forceinline__ int exp_mq(long long m, int q) {
 // X digits of one panel: B-operand slabs for the row part (x) and the
 // transposed part (x 2^e_r), seven balanced digits per value, plus the
 // per-column exponents, in integer arithmetic on the bit patterns. Thread
-// (column j, row group g) handles rows 4 (g + 8 u) .. +3, u = 0..3, so each
+// (column j, row group g) handles rows 4 (g + 16 u) .. +3, u = 0..1, so each
 // digit of four consecutive rows is one 32-bit shared store. Non-finite
 // values are staged as 0 (flag set; the caller's fix-up adds their exact
 // terms).
-__global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uint32_t ldx, std::uint32_t mc,
+__global__ void __launch_bounds__(256, 4) digitize_kernel(const double* x, std::uint32_t ldx, std::uint32_t mc,
                                                        const std::uint32_t* panel_start, const int* rowexp,
                                                        std::uint8_t* xd, std::uint8_t* xt, unsigned* nonfinite,
                                                        unsigned launch_id, std::uint32_t p_base) {
@@ -414,15 +414,15 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
   __shared__ int cmax[2][16];
   const std::uint32_t P = blockIdx.x + p_base, p0 = panel_start[P], rows = panel_start[P + 1] - p0;
   const int tid = threadIdx.x, j = tid & 15, g = tid >> 4;
-  long long mv[16];
-  int qv[16], er[16];
+  long long mv[8];
+  int qv[8], er[8];
   int E = INT_MIN / 4, Ep = INT_MIN / 4;
   bool bad = false;
 #pragma unroll
-  for (int u = 0; u < 4; ++u)
+  for (int u = 0; u < 2; ++u)
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
-      const int r = 4 * (g + 8 * u) + v, e = 4 * u + v;
+      const int r = 4 * (g + 16 * u) + v, e = 4 * u + v;
       const bool in = r < static_cast<int>(rows);
       double xv = (in && j < static_cast<int>(mc)) ? x[static_cast<std::size_t>(p0 + r) * ldx + j] : 0.0;
       er[e] = in ? rowexp[p0 + r] : 0;
@@ -447,7 +447,9 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
   __syncthreads();
   if (tid < 32) {
     const int k = tid >> 4, jj = tid & 15;
-    const int m = max(max(wmax[k][0][jj], wmax[k][1][jj]), max(wmax[k][2][jj], wmax[k][3][jj]));
+    int m = wmax[k][0][jj];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = max(m, wmax[k][w][jj]);
     cmax[k][jj] = m < INT_MIN / 8 ? 0 : m;  // all-zero column: exponent 0, digits 0
   }
   __syncthreads();
@@ -460,7 +462,7 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
   for (int k = 0; k < 2; ++k) {
     const int cm = cmax[k][j];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 2; ++u) {
       std::uint32_t lo[4], hi[4];
 #pragma unroll
       for (int v = 0; v < 4; ++v) {
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
         const std::uint32_t* src = t < 4 ? lo : hi;
         const std::uint32_t sel = static_cast<std::uint32_t>(t & 3) | (static_cast<std::uint32_t>(4 + (t & 3)) << 4);
         const std::uint32_t p01 = __byte_perm(src[0], src[1], sel), p23 = __byte_perm(src[2], src[3], sel);
-        *reinterpret_cast<std::uint32_t*>(&sd[k][off_b(16 * (kXD - 1 - t) + j, 4 * (g + 8 * u))]) =
+        *reinterpret_cast<std::uint32_t*>(&sd[k][off_b(16 * (kXD - 1 - t) + j, 4 * (g + 16 * u))]) =
             __byte_perm(p01, p23, 0x5410);
       }
     }
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(128) digitize_kernel(const double* x, std::uin
   const uint4* s1 = reinterpret_cast<const uint4*>(sd[1]);
   uint4* g0 = reinterpret_cast<uint4*>(xd + static_cast<std::size_t>(P) * kSlabBytes);
   uint4* g1 = reinterpret_cast<uint4*>(xt + static_cast<std::size_t>(P) * kSlabBytes);
-  for (int e = tid; e < kSlab / 16; e += 128) {
+  for (int e = tid; e < kSlab / 16; e += 256) {
     g0[e] = s0[e];
     g1[e] = s1[e];
   }
@@ -572,8 +574,7 @@ struct SlicedArgs {
   const int* escale;   // [panel][column]
   std::uint32_t ldx, mc;
   long long* trace;  // debug timeline (CIEG_SLICED_TRACE): CTA 0, 16 clock64 slots per item
-  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no transposed reduction, 2 planes of item 0 only,
-                     // 4 no TMEM reads in the epilogue, 8 no transposed MMAs
+  int ablate;        // timing-only (CIEG_SLICED_ABLATE, results invalid): 1 no transposed reduction, 2 planes of item 0 only
 };
 
 // (slabs hold the digits only -- every operand starts on a 1024-byte
@@ -593,30 +594,28 @@ struct Smem {
   std::uint32_t tmem;
 };
 
+// exact int64 -> double for |v| < 2^51 (the 2^52 + 2^51 bias; no conversion unit)
+__device__ __forceinline__ double l2d(long long v) {
+  return __longlong_as_double(v + 0x4338000000000000ll) - 6755399441055744.0;
+}
+
 // sum_d D_d 2^(24 - 8 d) over the kDiag diagonal blocks at TMEM address taddr
 // (8 columns of this warp's 32 lanes): the diagonals are combined exactly in
 // int64 in two groups of four (|D_d| < 2^24, so each group is below 2^49) and
 // the two groups are joined in fp64 with a single rounding.
-// sum_d D_d 2^(24 - 8 d) over the kDiag diagonal blocks at TMEM address taddr
-// (8 columns of this warp's 32 lanes), exactly, as hi 2^32 + lo: the diagonals
-// are combined in int64 in two groups of four (|D_d| < 2^24, so each group is
-// below 2^49). `release` runs once every diagonal is in registers (the
-// accumulator stage goes back before the arithmetic).
 template <typename Release>
-__device__ __forceinline__ void recombine8(std::uint32_t taddr, long long (&hi)[8], long long (&lo)[8],
-                                           Release release, bool skip_loads = false) {
+__device__ __forceinline__ void recombine8(std::uint32_t taddr, double (&v)[8], Release release) {
   static_assert(kDiag == 8, "two groups of four diagonals");
-  std::int32_t d0[8] = {}, d1[8] = {}, d2[8] = {}, d3[8] = {};
+  std::int32_t d0[8], d1[8], d2[8], d3[8];
+  long long hi[8];
 #pragma unroll
   for (int g = 0; g < 2; ++g) {
-    if (!skip_loads) {  // (timing-only ablation: no TMEM reads)
-      umma::ld8(taddr + 16 * (4 * g), d0);
-      umma::ld8(taddr + 16 * (4 * g + 1), d1);
-      umma::ld8(taddr + 16 * (4 * g + 2), d2);
-      umma::ld8(taddr + 16 * (4 * g + 3), d3);
-      umma::ld_wait();
-    }
-    if (g == 1) release();
+    umma::ld8(taddr + 16 * (4 * g), d0);
+    umma::ld8(taddr + 16 * (4 * g + 1), d1);
+    umma::ld8(taddr + 16 * (4 * g + 2), d2);
+    umma::ld8(taddr + 16 * (4 * g + 3), d3);
+    umma::ld_wait();
+    if (g == 1) release();  // every diagonal is in registers: the accumulator stage goes back before the arithmetic
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const long long w = static_cast<long long>(d3[j]) + (static_cast<long long>(d2[j]) << 8) +
@@ -624,24 +623,15 @@ __device__ __forceinline__ void recombine8(std::uint32_t taddr, long long (&hi)[
       if (g == 0)
         hi[j] = w;
       else
-        lo[j] = w;
+        v[j] = fma(l2d(w), 0x1p-32, l2d(hi[j]));
     }
   }
 }
 
-// round((hi 2^32 + lo) 2^-r) to the nearest integer (halves up), |hi 2^32 + lo|
-// < 2^82: the contribution in units of the panel's fixed-point scale. Integer
-// arithmetic only (the FP64 pipe stays out of the epilogue); r >= 14 by the
-// scale bounds whenever the value is non-zero, and a shift beyond the value's
-// bits gives 0.
-__device__ __forceinline__ long long shift_round(long long hi, long long lo, int r) {
-  r = max(1, min(r, 126));
-  const __int128 w = (static_cast<__int128>(hi) << 32) + static_cast<__int128>(lo) + (static_cast<__int128>(1) << (r - 1));
-  return static_cast<long long>(w >> r);
-}
-
 // ---- fixed-point accumulation into yint: 64-bit integer adds in L2
 // (red.global.add.u64 -- exact, so the result does not depend on their order)
+// v 2^e rounded to the nearest integer (|result| < 2^62 by the scale bounds)
+__device__ __forceinline__ long long fixp(double v, int e) { return __double2ll_rn(v * pow2(e)); }
 
 #define TRACE(item, slot, cond)                                                                      \
   do {                                                                                               \
@@ -746,7 +736,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         umma::fence_after();
       }
       const std::uint64_t bt = b_t0 + static_cast<std::uint64_t>(o * (kSlab >> 4));
-      if (trans && !(a.ablate & 8)) {
+      if (trans) {
 #pragma unroll 1
         for (int s = 0; s < kAS; ++s) {
           const int n = 16 * min(kXD, kDiag - s);
@@ -841,10 +831,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
     // ------------------------------------------------- row-part epilogue
     // (TMEM lanes = tile rows; 8 of the 16 columns per warp)
     const int r = 32 * eq + lane, j0 = 8 * half;
-    // the owner's rows in fixed point (units 2^(escale - 62) of the owner
-    // panel): every item's contribution is rounded to that unit and the exact
-    // int64 sum is added to yint once per owner
-    long long yacc[8];
+    double yacc[8];
     int er = 0, osc[8];
     std::uint32_t k = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
@@ -854,7 +841,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       if ((it.flags >> 8) & 1u) {
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          yacc[j] = 0;
+          yacc[j] = 0.0;
           osc[j] = __ldg(a.escale + it.owner * 16 + j0 + j);
         }
         er = r < prow ? a.rowexp[it.r0 + r] : 0;
@@ -866,25 +853,25 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       int ex[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) ex[j] = S.xd_exp[k & 3][j0 + j];
-      long long hi[8], lo[8];
-      recombine8(tbase + ecol + b * kStageCols, hi, lo, [&] {
+      double v[8];
+      recombine8(tbase + ecol + b * kStageCols, v, [&] {
         umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
         umma::st_wait();
         umma::fence_before();
         __syncwarp();
         if (lane == 0) umma::mbar_arrive(&S.acc_empty[b]);
         TRACE(i, 12, lane == 0 && warp == 4);
-      }, (a.ablate & 4) != 0);
+      });
       TRACE(i, 13, lane == 0 && warp == 4);
-      // v 2^(e_r + ex - 36) in units of 2^(osc - 62), v = hi + lo 2^-32
 #pragma unroll
-      for (int j = 0; j < 8; ++j) yacc[j] += shift_round(hi[j], lo[j], osc[j] + 6 - er - ex[j]);
+      for (int j = 0; j < 8; ++j) yacc[j] = fma(v[j], pow2(er + ex[j] - 36), yacc[j]);
       TRACE(i, 10, lane == 0 && warp == 4);
-      if (((it.flags >> 9) & 1u) && r < prow) {
+      if (((it.flags >> 9) & 1u) && r < prow) {  // the owner's row part, in fixed point, added to yint
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
                                  static_cast<std::size_t>(it.owner) * kTD * 16 + eq * 512 + j0 * 32 + lane;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) atomicAdd(yr + j * 32, static_cast<unsigned long long>(yacc[j]));
+        for (int j = 0; j < 8; ++j)
+          atomicAdd(yr + j * 32, static_cast<unsigned long long>(fixp(yacc[j], 62 - osc[j])));
       }
     }
   } else {
@@ -910,7 +897,7 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       int ex[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) ex[j] = S.xt_exp[(owners - 1) & 3][j0 + j];
-      long long hi[8], lo[8];
+      double v[8];
       auto release = [&] {
         umma::fence_before();
         __syncwarp();
@@ -918,21 +905,21 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         TRACE(i, 15, lane == 0 && warp == 12);
       };
       if (trans) {
-        recombine8(tbase + ecol + b * kStageCols, hi, lo, [&] {
+        recombine8(tbase + ecol + b * kStageCols, v, [&] {
           umma::st8_zero(tbase + ecol + b * kStageCols + 16 * (kDiag - 1));
           umma::st_wait();
           release();
-        }, (a.ablate & 4) != 0);
+        });
       } else {
         release();
       }
       if (!trans || (a.ablate & 1)) continue;
-      if (c < static_cast<int>(it.orow)) {  // the contribution to the partner's rows, in its fixed-point units
+      if (c < static_cast<int>(it.orow)) {  // the contribution to the partner's rows, in fixed point
         unsigned long long* yr = reinterpret_cast<unsigned long long*>(a.yint) +
                                  static_cast<std::size_t>(it.partner) * kTD * 16 + eq * 512 + j0 * 32 + lane;
 #pragma unroll
         for (int j = 0; j < 8; ++j)
-          atomicAdd(yr + j * 32, static_cast<unsigned long long>(shift_round(hi[j], lo[j], psc[j] + 6 - ex[j])));
+          atomicAdd(yr + j * 32, static_cast<unsigned long long>(fixp(v[j], ex[j] - 36 + 62 - psc[j])));
       }
     }
 
@@ -1248,7 +1235,7 @@ namespace {
 void launch_digitize(cieg_ctx* ctx, const cieg_mat* m, SlicedPlan* pl, const double* x, std::uint32_t ldx,
                      std::uint32_t mc, unsigned* nonfinite, unsigned launch_id, std::uint32_t p_lo, std::uint32_t p_hi) {
   if (p_hi <= p_lo) return;
-  digitize_kernel<<<p_hi - p_lo, 128, 0, ctx->stream>>>(x, ldx, mc, m->panel_start, pl->rowexp, pl->xd, pl->xt,
+  digitize_kernel<<<p_hi - p_lo, 256, 0, ctx->stream>>>(x, ldx, mc, m->panel_start, pl->rowexp, pl->xd, pl->xt,
                                                         nonfinite, launch_id, p_lo);
   CIEG_CUDA(cudaGetLastError());
   ++ctx->launches;
