@@ -141,8 +141,12 @@ int cieg_matrix_info(const cieg_mat* mat, uint32_t* dim, uint64_t* nnz, uint32_t
  * (leading dimension m). Deterministic: every output row is reduced by one
  * owner in a fixed order (bitwise identical run to run). */
 int cieg_spmm(cieg_ctx* ctx, const cieg_mat* mat, const double* x_dev, double* y_dev, uint32_t m);
-/* Same with host buffers: H2D of X, SpMM, D2H of U on the context stream,
- * synchronous on return. This is the call a ci::spmm drop-in makes. */
+/* Same with host buffers (pageable or pinned), synchronous on return. This is
+ * the call a ci::spmm drop-in makes. Where the sliced kernel applies (an
+ * unsharded fp32 H, m <= 16) the upload of X, the kernels and the download of
+ * U are pipelined over chunks of row panels on the context's copy streams,
+ * with results bitwise those of cieg_spmm; otherwise H2D, SpMM, D2H on the
+ * context stream. */
 int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, double* y_host,
                    uint32_t m);
 /* `count` independent products U_i = H X_i through host buffers (pinned for
