@@ -7,7 +7,12 @@
 #if defined(__SSE2__)
 #include <emmintrin.h>
 #endif
+#include <condition_variable>
+#include <deque>
 #include <memory>
+#include <mutex>
+#include <thread>
+#include <omp.h>
 #include <string>
 
 #include "context.hpp"
@@ -155,6 +160,7 @@ int cieg_ctx_destroy(cieg_ctx* ctx) {
   for (auto& e : ctx->pipe_ev) cudaEventDestroy(e);
   if (ctx->pipe_up) cudaStreamDestroy(ctx->pipe_up);
   if (ctx->pipe_down) cudaStreamDestroy(ctx->pipe_down);
+  cieg::destroy_copier(ctx);
   cieg::destroy_nccl(ctx);
   for (auto& e : ctx->stage_ev)
     if (e) cudaEventDestroy(e);
@@ -581,6 +587,137 @@ void download_staged(cieg_ctx* ctx, void* dst, const void* src, std::size_t byte
 
 }  // namespace
 
+}  // extern "C"
+
+namespace cieg {
+
+// ---- pageable host buffers of the pipelined host SpMM (context.hpp)
+namespace {
+void copy_pieces(void* dst, const void* src, std::size_t bytes, int threads, bool stream) {
+  constexpr std::size_t kPiece = 256u << 10;
+  const std::int64_t pieces = static_cast<std::int64_t>((bytes + kPiece - 1) / kPiece);
+#pragma omp parallel for schedule(static) num_threads(threads) if (pieces > 1)
+  for (std::int64_t i = 0; i < pieces; ++i) {
+    const std::size_t o = static_cast<std::size_t>(i) * kPiece, len = std::min(kPiece, bytes - o);
+    if (stream)
+      stream_piece(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, len);
+    else
+      std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o, len);
+  }
+}
+}  // namespace
+
+struct HostCopier {
+  struct Job {
+    cudaEvent_t ev;
+    char* dst;
+    const char* src;
+    std::size_t len;
+  };
+  std::thread th;
+  std::mutex mu;
+  std::condition_variable cv_job, cv_done;
+  std::deque<Job> q;
+  std::size_t submitted = 0, retired = 0;
+  bool stop = false;
+  std::string error;
+  int device = 0, threads = 1;
+  void run() {
+    cudaSetDevice(device);
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> lk(mu);
+        cv_job.wait(lk, [&] { return stop || !q.empty(); });
+        if (q.empty()) return;
+        j = q.front();
+        q.pop_front();
+      }
+      const cudaError_t e = cudaEventSynchronize(j.ev);
+      if (e == cudaSuccess) copy_pieces(j.dst, j.src, j.len, threads, true);
+      {
+        std::lock_guard<std::mutex> lk(mu);
+        if (e != cudaSuccess && error.empty()) error = cudaGetErrorString(e);
+        ++retired;
+      }
+      cv_done.notify_all();
+    }
+  }
+};
+
+namespace {
+HostCopier* copier(cieg_ctx* ctx) {
+  if (!ctx->copier) {
+    auto* c = new HostCopier;
+    c->device = ctx->device;
+    c->threads = std::max(1, omp_get_max_threads() / 2);
+    c->th = std::thread([c] { c->run(); });
+    ctx->copier = c;
+  }
+  return ctx->copier;
+}
+}  // namespace
+
+void host_copy_in(void* dst, const void* src, std::size_t bytes, bool shared) {
+  const int all = std::max(1, omp_get_max_threads());
+  copy_pieces(dst, src, bytes, shared ? std::max(1, all - all / 2) : all, false);
+}
+
+std::size_t copier_submit(cieg_ctx* ctx, cudaEvent_t ev, void* dst, const void* src, std::size_t bytes) {
+  HostCopier* c = copier(ctx);
+  std::size_t n;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->q.push_back(HostCopier::Job{ev, static_cast<char*>(dst), static_cast<const char*>(src), bytes});
+    n = ++c->submitted;
+  }
+  c->cv_job.notify_one();
+  return n;
+}
+
+std::size_t copier_submitted(cieg_ctx* ctx) {
+  HostCopier* c = copier(ctx);
+  std::lock_guard<std::mutex> lk(c->mu);
+  return c->submitted;
+}
+
+void copier_wait(cieg_ctx* ctx, std::size_t jobs) {
+  HostCopier* c = copier(ctx);
+  std::unique_lock<std::mutex> lk(c->mu);
+  c->cv_done.wait(lk, [&] { return c->retired >= jobs; });
+  if (!c->error.empty()) {
+    const std::string msg = "download copy: " + c->error;
+    c->error.clear();
+    lk.unlock();
+    fail(CIEG_ERR_CUDA, msg);
+  }
+}
+
+void copier_drain(cieg_ctx* ctx) noexcept {
+  if (!ctx->copier) return;
+  HostCopier* c = ctx->copier;
+  std::unique_lock<std::mutex> lk(c->mu);
+  c->cv_done.wait(lk, [&] { return c->retired >= c->submitted; });
+  c->error.clear();
+}
+
+void destroy_copier(cieg_ctx* ctx) {
+  if (!ctx->copier) return;
+  HostCopier* c = ctx->copier;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->stop = true;
+  }
+  c->cv_job.notify_all();
+  if (c->th.joinable()) c->th.join();
+  delete c;
+  ctx->copier = nullptr;
+}
+
+}  // namespace cieg
+
+extern "C" {
+
 // ci::spmm's host call (the drop-in binds it, integration/ci_gpu_dropin.cpp):
 // pinned host buffers go straight to the copy engines; pageable ones (the
 // std::vector inside ci::BlockVectors) stream through a pinned chunk ring
@@ -596,7 +733,7 @@ int cieg_spmm_host(cieg_ctx* ctx, const cieg_mat* mat, const double* x_host, dou
     CIEG_CUDA(cudaSetDevice(ctx->device));
     const bool x_pinned = host_pinned(x_host), y_pinned = host_pinned(y_host);
     // the sliced kernel: upload, kernels and download pipelined over row chunks
-    if (m <= 16 && cieg::sliced_spmm_host(ctx, const_cast<cieg_mat*>(mat), x_host, y_host, m, x_pinned, y_pinned, par_copy, par_copy_stream))
+    if (m <= 16 && cieg::sliced_spmm_host(ctx, const_cast<cieg_mat*>(mat), x_host, y_host, m, x_pinned, y_pinned))
       return;
     double* dx = static_cast<double*>(ctx->scratch_x.get(xbytes));
     double* dy = static_cast<double*>(ctx->scratch_y.get(ybytes));

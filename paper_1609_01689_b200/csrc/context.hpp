@@ -59,6 +59,7 @@ struct PinnedBuf {
 };
 
 struct SlicedPlan;  // spmm_i8.cu
+struct HostCopier;  // capi.cu: the helper thread that copies finished downloads out of the pinned ring
 struct NcclPlane;   // nccl_plane.cu
 
 }  // namespace cieg
@@ -84,6 +85,7 @@ struct cieg_ctx {
   cudaStream_t pipe_up = nullptr, pipe_down = nullptr;
   cieg::PinnedBuf pinned_stage_down;
   std::vector<cudaEvent_t> pipe_ev;
+  cieg::HostCopier* copier = nullptr;
   // phase timers (report.hpp Clock): event pairs read at the end of a solve,
   // so timing a phase does not synchronise the host with the device
   struct ClockRec {
@@ -181,11 +183,22 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
 void destroy_sliced(cieg_mat* m);
 // ci::spmm's host call on the sliced kernel, pipelined over row chunks (upload,
 // kernels and download overlap); false when the sliced kernel does not apply
-// (the caller then runs upload -> launch_spmm -> download). `copy` / `copy_out` =
-// the caller's threaded host copies into / out of the pinned rings (pageable buffers).
+// (the caller then runs upload -> launch_spmm -> download).
 bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* y_host, std::uint32_t mc,
-                      bool x_pinned, bool y_pinned, void (*copy)(void*, const void*, std::size_t),
-                      void (*copy_out)(void*, const void*, std::size_t));
+                      bool x_pinned, bool y_pinned);
+// Host side of pageable buffers (capi.cu). host_copy_in: threaded copy into a
+// pinned upload slot on the calling thread (`shared`: the helper thread is
+// copying too -- half the threads each). copier_submit: once `ev` completes,
+// the helper thread copies a finished download out of its ring slot
+// (non-temporal stores); returns the number of jobs submitted so far.
+// copier_wait blocks until that many jobs are done (throws on a failed one);
+// copier_drain waits for all of them and never throws.
+void host_copy_in(void* dst, const void* src, std::size_t bytes, bool shared);
+std::size_t copier_submit(cieg_ctx* ctx, cudaEvent_t ev, void* dst, const void* src, std::size_t bytes);
+std::size_t copier_submitted(cieg_ctx* ctx);
+void copier_wait(cieg_ctx* ctx, std::size_t jobs);
+void copier_drain(cieg_ctx* ctx) noexcept;
+void destroy_copier(cieg_ctx* ctx);
 // K1's non-finite-input flag and the fix-up of the launch tagged launch_id
 unsigned* nonfinite_flag(cieg_ctx* ctx);
 void launch_nonfinite_fix(cieg_ctx* ctx, const cieg_mat* m, const double* x, std::uint32_t ldx, double* y,

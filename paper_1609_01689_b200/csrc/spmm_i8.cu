@@ -1377,11 +1377,11 @@ void launch_spmm_sliced(cieg_ctx* ctx, cieg_mat* m, const double* x, std::uint32
 // degenerates to upload, compute, download.
 //
 // Pageable host buffers (the std::vector inside ci::BlockVectors) stream
-// through pinned rings in both directions; `copy` / `copy_out` are the caller's
-// threaded host copies into / out of the rings.
+// through pinned rings in both directions: the calling thread copies X into
+// the upload ring, a helper thread (capi.cu) copies finished pieces of U out of
+// the download ring, half the OpenMP threads each.
 bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* y_host, std::uint32_t mc,
-                      bool x_pinned, bool y_pinned, void (*copy)(void*, const void*, std::size_t),
-                      void (*copy_out)(void*, const void*, std::size_t)) {
+                      bool x_pinned, bool y_pinned) {
   const bool shard = m->row_lo != 0 || m->row_hi != m->dim;
   if (shard || mc == 0 || mc > 16 || !sliced_rule(ctx, m, mc) || !sliced_ready(ctx, m)) return false;
   static const bool off = [] {
@@ -1426,28 +1426,10 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
   CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_up, e0, 0));
   CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_down, e0, 0));
 
-  struct Pending {
-    cudaEvent_t ev;
-    const char* src;
-    char* dst;
-    std::size_t len;
-  };
-  std::deque<Pending> pending;  // downloads in ring slots awaiting their host copy
-  std::size_t down_count = 0;
-  auto retire = [&](bool block) {
-    while (!pending.empty()) {
-      if (block) {
-        CIEG_CUDA(cudaEventSynchronize(pending.front().ev));
-      } else {
-        const cudaError_t q = cudaEventQuery(pending.front().ev);
-        if (q == cudaErrorNotReady) return;
-        CIEG_CUDA(q);
-      }
-      copy_out(pending.front().dst, pending.front().src, pending.front().len);
-      pending.pop_front();
-      if (block) return;
-    }
-  };
+  // downloads in ring slots are copied out by the helper thread, in order
+  const std::size_t jobs0 = y_pinned ? 0 : copier_submitted(ctx);
+  std::size_t issued = 0;
+  try {
   // rows [r_lo, r_hi) of U, ready on the context stream -> host
   auto download = [&](std::uint32_t r_lo, std::uint32_t r_hi) {
     if (r_hi <= r_lo) return;
@@ -1462,12 +1444,13 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
     }
     for (std::size_t o = b0; o < b1; o += kChunkBytes) {
       const std::size_t len = std::min(kChunkBytes, b1 - o);
-      while (pending.size() >= static_cast<std::size_t>(kDownSlots)) retire(true);
-      char* slot = down_ring + (down_count++ % kDownSlots) * kChunkBytes;
+      if (issued >= static_cast<std::size_t>(kDownSlots)) copier_wait(ctx, jobs0 + issued - kDownSlots + 1);  // the slot's last piece is home
+      char* slot = down_ring + (issued % kDownSlots) * kChunkBytes;
       CIEG_CUDA(cudaMemcpyAsync(slot, reinterpret_cast<const char*>(dy) + o, len, cudaMemcpyDeviceToHost, ctx->pipe_down));
       cudaEvent_t done = event();
       CIEG_CUDA(cudaEventRecord(done, ctx->pipe_down));
-      pending.push_back(Pending{done, slot, reinterpret_cast<char*>(y_host) + o, len});
+      copier_submit(ctx, done, reinterpret_cast<char*>(y_host) + o, slot, len);
+      ++issued;
     }
   };
 
@@ -1490,12 +1473,11 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
         const std::size_t len = std::min(kChunkBytes, b1 - o);
         const int s = static_cast<int>(up_count++ % kUpSlots);
         if (up_done[s]) CIEG_CUDA(cudaEventSynchronize(up_done[s]));
-        copy(up_ring + s * kChunkBytes, reinterpret_cast<const char*>(x_host) + o, len);
+        host_copy_in(up_ring + s * kChunkBytes, reinterpret_cast<const char*>(x_host) + o, len, !y_pinned);
         CIEG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dx) + o, up_ring + s * kChunkBytes, len,
                                   cudaMemcpyHostToDevice, ctx->pipe_up));
         up_done[s] = event();
         CIEG_CUDA(cudaEventRecord(up_done[s], ctx->pipe_up));
-        retire(false);
       }
     }
     cudaEvent_t uploaded = event();
@@ -1519,21 +1501,24 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
       download(r_lo, r_hi);
       converted = y_hi;
     }
-    retire(false);
   }
   if (converted != np || next_chunk != nch) fail(CIEG_ERR_CUDA, "sliced host pipeline: incomplete schedule");
   // Inf/NaN in X (staged as zeros): the rare path -- the exact stored-entry
   // terms are added on the device and U is downloaded again, whole
   unsigned* flag_host = static_cast<unsigned*>(ctx->pinned_small.get(256));
   CIEG_CUDA(cudaMemcpyAsync(flag_host, flag, sizeof(unsigned), cudaMemcpyDeviceToHost, ctx->stream));
-  while (!pending.empty()) retire(true);
+  if (!y_pinned) copier_wait(ctx, jobs0 + issued);
   CIEG_CUDA(cudaStreamSynchronize(ctx->pipe_down));
   CIEG_CUDA(cudaStreamSynchronize(ctx->stream));
   if (*flag_host == launch_id) {
     launch_nonfinite_fix(ctx, m, dx, mc, dy, mc, mc, launch_id);
     download(0, n);
-    while (!pending.empty()) retire(true);
+    if (!y_pinned) copier_wait(ctx, jobs0 + issued);
     CIEG_CUDA(cudaStreamSynchronize(ctx->pipe_down));
+  }
+  } catch (...) {
+    if (!y_pinned) copier_drain(ctx);  // no copy into the caller's U after the call has failed
+    throw;
   }
   return true;
 }
