@@ -720,8 +720,13 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
       const std::uint64_t ab = static_cast<std::uint64_t>(b * (kPlanes >> 4));
       const std::uint64_t bd = b_d0 + static_cast<std::uint64_t>(b * (kSlab >> 4));
       // row part first: at an owner's first item it covers the owner slab's load
+      // (CIEG_ABLATE_ROW_MMA / CIEG_ABLATE_TRANS_MMA: timing-only builds without one orientation's MMAs)
 #pragma unroll 1
+#ifdef CIEG_ABLATE_ROW_MMA
+      for (int s = 0; s < 0; ++s) {
+#else
       for (int s = 0; s < kAS; ++s) {
+#endif
         const int n = 16 * min(kXD, kDiag - s);  // digits t with s + t < kDiag
         const std::uint32_t id_row = umma::idesc_i8(1, 1, 0, 0, 128, n);  // balanced digits: all signed
 #pragma unroll
@@ -736,7 +741,11 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
         umma::fence_after();
       }
       const std::uint64_t bt = b_t0 + static_cast<std::uint64_t>(o * (kSlab >> 4));
+#ifdef CIEG_ABLATE_TRANS_MMA
+      if (false) {
+#else
       if (trans) {
+#endif
 #pragma unroll 1
         for (int s = 0; s < kAS; ++s) {
           const int n = 16 * min(kXD, kDiag - s);
