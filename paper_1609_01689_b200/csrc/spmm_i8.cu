@@ -66,6 +66,7 @@
 // same kernels over chunks of owner panels, pipelined with the upload of X
 // and the download of U (see there).
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdint>
 #include <cstdio>
@@ -1423,7 +1424,7 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
     }
     return ctx->pipe_ev[ev_next++];
   };
-  constexpr int kUpSlots = 3, kDownSlots = 4;
+  constexpr int kUpSlots = 4, kDownSlots = 8;
   char* up_ring = x_pinned ? nullptr : static_cast<char*>(ctx->pinned_stage.get(kUpSlots * kChunkBytes));
   char* down_ring = y_pinned ? nullptr : static_cast<char*>(ctx->pinned_stage_down.get(kDownSlots * kChunkBytes));
   unsigned* flag = nonfinite_flag(ctx);
@@ -1435,6 +1436,12 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
   CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_up, e0, 0));
   CIEG_CUDA(cudaStreamWaitEvent(ctx->pipe_down, e0, 0));
 
+  // host-side time split of the call (CIEG_HOST_TRACE=1: printed to stderr)
+  static const bool host_trace = std::getenv("CIEG_HOST_TRACE") != nullptr;
+  using clk = std::chrono::steady_clock;
+  double t_copy = 0, t_upwait = 0, t_downwait = 0, t_enqueue = 0;
+  const auto t_begin = clk::now();
+  auto since = [](clk::time_point t0) { return std::chrono::duration<double, std::milli>(clk::now() - t0).count(); };
   // downloads in ring slots are copied out by the helper thread, in order
   const std::size_t jobs0 = y_pinned ? 0 : copier_submitted(ctx);
   std::size_t issued = 0;
@@ -1453,7 +1460,11 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
     }
     for (std::size_t o = b0; o < b1; o += kChunkBytes) {
       const std::size_t len = std::min(kChunkBytes, b1 - o);
-      if (issued >= static_cast<std::size_t>(kDownSlots)) copier_wait(ctx, jobs0 + issued - kDownSlots + 1);  // the slot's last piece is home
+      if (issued >= static_cast<std::size_t>(kDownSlots)) {  // the slot's last piece is home
+        const auto t0 = clk::now();
+        copier_wait(ctx, jobs0 + issued - kDownSlots + 1);
+        t_downwait += since(t0);
+      }
       char* slot = down_ring + (issued % kDownSlots) * kChunkBytes;
       CIEG_CUDA(cudaMemcpyAsync(slot, reinterpret_cast<const char*>(dy) + o, len, cudaMemcpyDeviceToHost, ctx->pipe_down));
       cudaEvent_t done = event();
@@ -1481,14 +1492,19 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
       for (std::size_t o = b0; o < b1; o += kChunkBytes) {
         const std::size_t len = std::min(kChunkBytes, b1 - o);
         const int s = static_cast<int>(up_count++ % kUpSlots);
+        auto t0 = clk::now();
         if (up_done[s]) CIEG_CUDA(cudaEventSynchronize(up_done[s]));
+        t_upwait += since(t0);
+        t0 = clk::now();
         host_copy_in(up_ring + s * kChunkBytes, reinterpret_cast<const char*>(x_host) + o, len, !y_pinned);
+        t_copy += since(t0);
         CIEG_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(dx) + o, up_ring + s * kChunkBytes, len,
                                   cudaMemcpyHostToDevice, ctx->pipe_up));
         up_done[s] = event();
         CIEG_CUDA(cudaEventRecord(up_done[s], ctx->pipe_up));
       }
     }
+    const auto t_enq = clk::now();
     cudaEvent_t uploaded = event();
     CIEG_CUDA(cudaEventRecord(uploaded, ctx->pipe_up));
     CIEG_CUDA(cudaStreamWaitEvent(ctx->stream, uploaded, 0));
@@ -1510,7 +1526,9 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
       download(r_lo, r_hi);
       converted = y_hi;
     }
+    t_enqueue += since(t_enq);
   }
+  const double t_loop = since(t_begin);
   if (converted != np || next_chunk != nch) fail(CIEG_ERR_CUDA, "sliced host pipeline: incomplete schedule");
   // Inf/NaN in X (staged as zeros): the rare path -- the exact stored-entry
   // terms are added on the device and U is downloaded again, whole
@@ -1525,6 +1543,10 @@ bool sliced_spmm_host(cieg_ctx* ctx, cieg_mat* m, const double* x_host, double* 
     if (!y_pinned) copier_wait(ctx, jobs0 + issued);
     CIEG_CUDA(cudaStreamSynchronize(ctx->pipe_down));
   }
+  if (host_trace)
+    std::fprintf(stderr, "sliced_spmm_host: %u chunks, loop %.3f ms (copy-in %.3f, upload-slot waits %.3f, enqueue incl. "
+                 "download-slot waits %.3f / %.3f), total %.3f ms\n", nch, t_loop, t_copy, t_upwait, t_enqueue, t_downwait,
+                 since(t_begin));
   } catch (...) {
     if (!y_pinned) copier_drain(ctx);  // no copy into the caller's U after the call has failed
     throw;

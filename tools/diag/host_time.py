@@ -19,7 +19,8 @@ yp = torch.empty_like(xp).pin_memory()
 lib = ci._lib.load()
 nbytes = configs.spmm_bytes(dm.nnz, dm.dim, m, 0)
 ref = None
-for name, xa, ya in (("pageable", x, y), ("pinned", xp.numpy(), yp.numpy())):
+for name, xa, ya in (("pageable", x, y), ("pinned", xp.numpy(), yp.numpy()), ("pageable X / pinned U", x, yp.numpy()),
+                     ("pinned X / pageable U", xp.numpy(), y)):
     for _ in range(3):
         ci._check(lib.cieg_spmm_host(dev.handle, dm.handle, ci._ptr(xa), ci._ptr(ya), m))
     t0 = time.perf_counter()
