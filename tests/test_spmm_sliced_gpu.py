@@ -243,3 +243,44 @@ def test_host_pipeline_unbanded(sliced, ref_lib, monkeypatch):
     y = dm.spmm_host(x)
     assert np.array_equal(y, _device_spmm(dm, x))
     assert rel_cols(y, ref_lib.RefMatrix(h).spmm(x, serial=True)) < TOL
+
+
+def test_sliced_full_lowest_slice(sliced, ref_lib):
+    """The lowest H slice is streamed as a per-item sparse list (at most 512
+    entries per tile). Values spread over 14 binades within every row fill
+    that slice for about half the entries -- far more than the list holds --
+    so this matrix keeps five dense planes; same result either way."""
+    h = gen_from((12000, 4, 200, 0.08, 0.4, 5, 0, 2000))
+    rng = np.random.default_rng(11)
+    mag = np.exp2(-rng.integers(0, 15, h.values.size)).astype(np.float32)
+    vals = (np.sign(h.values) * mag * np.float32(0.01)).astype(np.float32)
+    vals[h.values == 0] = 0
+    h2 = _with_values(h, vals)
+    x = ci.random_block(h.dim, 16, 23)
+    y = ci.spmm(h2, x)
+    y_ref = ref_lib.RefMatrix(h2).spmm(x, serial=True)
+    assert rel_cols(y, y_ref) < TOL
+    assert np.array_equal(ci.spmm(h2, x), y)
+
+
+def test_sliced_sparse_and_dense_lowest_slice_agree(tmp_path):
+    """CIEG_SLICED_DENSE5=1 (five dense planes) and the default (sparse lowest
+    slice) run the same arithmetic: bitwise equal results."""
+    import subprocess, sys, os
+
+    script = tmp_path / "run.py"
+    script.write_text(
+        "import sys, numpy as np\n"
+        "sys.path.insert(0, %r)\n"
+        "from paper_1609_01689_b200 import ci\n"
+        "h = ci.generate_sector_matrix(20000, 5, 256, 0.03, 0.4, 31, 0, 2000)\n"
+        "ci.Device.default().set_spmm_mode('sliced')\n"
+        "x = ci.random_block(h.dim, 16, 3)\n"
+        "np.save(sys.argv[1], ci.spmm(h, x))\n" % os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    outs = []
+    for dense5 in ("0", "1"):
+        out = tmp_path / f"y{dense5}.npy"
+        env = dict(os.environ, CIEG_SLICED_DENSE5=dense5)
+        subprocess.run([sys.executable, str(script), str(out)], check=True, env=env, timeout=300)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0], outs[1])
