@@ -186,9 +186,6 @@ __host__ __device__ __forceinline__ std::uint32_t off_b(std::uint32_t n, std::ui
   return (n >> 3) * 1024u + (k >> 4) * 128u + (n & 7u) * 16u + (k & 15u);
 }
 
-// exponent E with |v| < 2^E (frexp), for finite nonzero v
-__device__ __forceinline__ int exp_of(double v) { return ilogb(v) + 1; }
-
 // 2^e as a double, exact and branchless for |e| <= 2044 (a product of two
 // normal powers of two; subnormal results are exact too)
 __device__ __forceinline__ double pow2(int e) {
@@ -196,12 +193,6 @@ __device__ __forceinline__ double pow2(int e) {
   const int h = e >> 1;
   return __longlong_as_double(static_cast<long long>(h + 1023) << 52) *
          __longlong_as_double(static_cast<long long>(e - h + 1023) << 52);
-}
-
-// exact int32 -> double without the conversion unit: 2^52 + 2^31 + v
-__device__ __forceinline__ double i2d(std::int32_t v) {
-  return __hiloint2double(0x43300000, static_cast<int>(static_cast<unsigned>(v) ^ 0x80000000u)) -
-         4503601774854144.0;
 }
 
 // ---------------------------------------------------------------- build time
@@ -887,9 +878,9 @@ __global__ void __launch_bounds__(kThreads, 1) spmm_sliced_kernel(const SlicedAr
   } else {
     // ------------------------------------------ transposed-part epilogue
     // (TMEM lanes = tile columns; 8 of the 16 columns per warp): the item's
-    // contribution to its partner panel, in fixed point, staged in shared
-    // memory by the eight warps and added to yint by one bulk reduction.
-    const int c = 32 * eq + lane, j0 = 8 * half, gt = tid - 320;
+    // contribution to its partner panel, in fixed point, added to yint with
+    // coalesced 64-bit integer reds from the registers.
+    const int c = 32 * eq + lane, j0 = 8 * half;
     std::uint32_t k = 0, owners = 0;
     for (std::uint32_t i = i_beg; i < i_end; ++i, ++k) {
       const OzItem it = a.items[i];
