@@ -148,6 +148,7 @@ struct SlicedPlan {
   // every owner up to that neighbour has run)
   std::vector<std::uint32_t> item_owner_host, cta_off_host, tiny_rows_host, nb_prefix_max;
   struct Chunks {
+    std::uint32_t want = 0;            // the chunk count asked for (cache key)
     std::vector<std::uint32_t> panel;  // chunk c = owner panels [panel[c], panel[c + 1])
     std::uint32_t* cta_lim = nullptr;  // device [(chunks + 1) * ctas]: CTA b runs items [c * ctas + b], [(c + 1) * ctas + b])
   };
@@ -1302,27 +1303,37 @@ void launch_tiny_rows(cieg_ctx* ctx, const cieg_mat* m, const SlicedPlan* pl, co
   ++ctx->launches;
 }
 
-// Owner panels cut into `want` chunks of about equal rows; per chunk and CTA
-// the item range (a CTA's items ascend by owner panel). Cached per chunk count.
+// Owner panels cut into chunks of about equal rows -- `want` of them over the
+// matrix, the last quarter of the rows in half-size chunks (what is still to
+// do once the last rows of X have arrived -- the band's kernels and the
+// download of the rows that were waiting for them -- shrinks with the chunk
+// size there); per chunk and CTA the item range (a CTA's items ascend by owner
+// panel). Cached per `want`.
 const SlicedPlan::Chunks& chunking(const cieg_mat* m, SlicedPlan* pl, std::uint32_t want) {
   const auto& ps = m->panel_start_host;
   const std::uint32_t np = m->npanels;
   want = std::max<std::uint32_t>(1, std::min(want, np));
   for (const auto& c : pl->chunkings)
-    if (c.panel.size() == want + 1) return c;
+    if (c.want == want) return c;
   SlicedPlan::Chunks ch;
-  ch.panel.assign(want + 1, np);
-  ch.panel[0] = 0;
-  for (std::uint32_t c = 1; c < want; ++c) {
-    const std::uint32_t row = static_cast<std::uint32_t>(static_cast<std::uint64_t>(m->dim) * c / want);
-    ch.panel[c] = std::max(ch.panel[c - 1], panel_of(ps, row));
+  ch.want = want;
+  ch.panel.push_back(0);
+  // cuts in units of 1 / (2 want) of the rows: pairs of units up to 3/4, single units after
+  for (std::uint32_t u = 1; u < 2 * want; ++u) {
+    const bool tail = 4ull * u > 6ull * want;  // u / (2 want) > 3/4
+    if (!tail && (u & 1u)) continue;
+    const std::uint32_t row = static_cast<std::uint32_t>(static_cast<std::uint64_t>(m->dim) * u / (2ull * want));
+    const std::uint32_t p = std::max(ch.panel.back(), panel_of(ps, row));
+    if (p > ch.panel.back() && p < np) ch.panel.push_back(p);
   }
+  ch.panel.push_back(np);
+  const std::uint32_t nchunks = static_cast<std::uint32_t>(ch.panel.size() - 1);
   const std::uint32_t ctas = pl->ctas;
-  std::vector<std::uint32_t> lim(static_cast<std::size_t>(want + 1) * ctas);
+  std::vector<std::uint32_t> lim(static_cast<std::size_t>(nchunks + 1) * ctas);
   for (std::uint32_t b = 0; b < ctas; ++b) {
     const auto first = pl->item_owner_host.begin() + pl->cta_off_host[b];
     const auto last = pl->item_owner_host.begin() + pl->cta_off_host[b + 1];
-    for (std::uint32_t c = 0; c <= want; ++c)
+    for (std::uint32_t c = 0; c <= nchunks; ++c)
       lim[static_cast<std::size_t>(c) * ctas + b] =
           static_cast<std::uint32_t>(std::lower_bound(first, last, ch.panel[c]) - pl->item_owner_host.begin());
   }
